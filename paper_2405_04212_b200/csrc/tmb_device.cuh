@@ -1,0 +1,71 @@
+// tmb_device.cuh -- per-literal-position Type I / Type II automaton updates
+// shared by the plugin feedback kernel and the fused trainer.
+#pragma once
+
+#include "tmb_common.cuh"
+
+namespace tmb {
+
+struct FbParams {
+    uint64_t t_inc;   // ceil(((s-1)/s) * 2^53): increment iff draw53 < t_inc
+    uint64_t t_dec;   // ceil((1/s) * 2^53)
+    double p_inc;     // (s-1)/s  (explicit-draws hook compares doubles)
+    double p_dec;     // 1/s
+    int boost;
+    int smin;
+    int smax;
+};
+
+inline FbParams make_fb_params(double s, int boost, int smin, int smax) {
+    FbParams f;
+    f.p_inc = (s - 1.0) / s;  // kernels/_numba.py:73-74
+    f.p_dec = 1.0 / s;
+    f.t_inc = prob_threshold(f.p_inc);
+    f.t_dec = prob_threshold(f.p_dec);
+    f.boost = boost;
+    f.smin = smin;
+    f.smax = smax;
+    return f;
+}
+
+// Type I at one position (kernels/_numba.py:71-90).  `sk` = seed + G*(base+1)
+// so the draw for position p is mix64(sk + G*p).  Draws whose outcome cannot
+// change the state (clamped automaton, boosted increment) are skipped: the
+// stream is random-access, so skipping is bit-exact (core.py:7-10).
+__device__ __forceinline__ int type_i_stream(int st, int lit, int out, const FbParams &fp,
+                                             uint64_t sk, uint32_t p, uint64_t &ndraws) {
+    if (out && lit) {
+        if (st < fp.smax) {
+            if (fp.boost) return st + 1;
+            ++ndraws;
+            if ((mix64(sk + kGolden * (uint64_t)p) >> 11) < fp.t_inc) return st + 1;
+        }
+    } else if (st > fp.smin) {
+        ++ndraws;
+        if ((mix64(sk + kGolden * (uint64_t)p) >> 11) < fp.t_dec) return st - 1;
+    }
+    return st;
+}
+
+// Same with an explicit uniform draw u (test hook).
+__device__ __forceinline__ int type_i_explicit(int st, int lit, int out, const FbParams &fp,
+                                               double u) {
+    if (out && lit) {
+        if ((fp.boost || u < fp.p_inc) && st < fp.smax) return st + 1;
+    } else if (u < fp.p_dec && st > fp.smin) {
+        return st - 1;
+    }
+    return st;
+}
+
+// Type II at one position (kernels/_numba.py:93-98): output 1 only.
+__device__ __forceinline__ int type_ii(int st, int lit, int out) {
+    return (out && !lit && st < 0) ? st + 1 : st;
+}
+
+int dev_pack_literals(const uint8_t *x, int64_t N, int64_t cols, int negations, int64_t P,
+                      uint32_t *out, cudaStream_t st);
+int dev_build_masks(const int8_t *states, int64_t C, int64_t P, uint32_t *masks,
+                    int32_t *counts, cudaStream_t st);
+
+}  // namespace tmb

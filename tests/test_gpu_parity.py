@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI) against reference-generated
+golden fixtures and the CPU oracle.  Bit-exact for everything (integer /
+byte / index work; the float64 decision math is IEEE-identical)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_rng_matches_reference(gpu):
+    import torch
+    g = golden("rng")
+    from paper_2405_04212_b200 import _lib
+    from paper_2405_04212_b200.runtime import ptr, stream_ptr
+    for r, st in enumerate(g["starts"]):
+        out = torch.empty(64, dtype=torch.int64, device="cuda")
+        _lib.call("tmb_stream_u64_block", int(g["block_seed"]), int(st), 64, ptr(out),
+                  stream_ptr())
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), g["blocks"][r])
+
+
+def test_plugin_outputs_and_feedback_golden(gpu):
+    k = gpu.kernels
+    g = golden("kernels")
+    for t in range(int(g["n_cases"])):
+        p = lambda n: g[f"c{t}_{n}"]  # noqa: E731
+        label, negative, boost, smin, smax, budget = (int(v) for v in p("scalars"))
+        states = p("states")
+        assert np.array_equal(k.clause_outputs(states, p("lits"), True, budget), p("o_tr"))
+        assert np.array_equal(k.clause_outputs(states, p("lits"), False, budget), p("o_inf"))
+        assert np.array_equal(k.clause_outputs_batch(states, p("x_lit"), True, budget), p("b_tr"))
+        assert np.array_equal(k.clause_outputs_batch(states, p("x_lit"), False, budget),
+                              p("b_inf"))
+        st, w = states.copy(), p("weights").copy()
+        c = k.bank_feedback(st, w, p("lits"), p("outputs"), label, negative, p("ut"), p("un"),
+                            float(p("s")), boost, smin, smax, p("seed"), p("counter"))
+        assert int(c) == int(p("new_counter")), t
+        assert np.array_equal(st, p("st_after")), t
+        assert np.array_equal(w, p("w_after")), t
+
+
+def test_explicit_draws_hook(gpu, oracle):
+    """One step's state delta is bit-exact when GPU and oracle consume the
+    same explicit uniform draws -- both reference-stream draws (checked
+    against the reference's own result) and arbitrary draws."""
+    k = gpu.kernels
+    g = golden("kernels")
+    rs = np.random.default_rng(8)
+    for t in range(int(g["n_cases"])):
+        p = lambda n: g[f"c{t}_{n}"]  # noqa: E731
+        label, negative, boost, smin, smax, _ = (int(v) for v in p("scalars"))
+        n_ev = int(p("ut").sum() + p("un").sum())
+        P = p("states").shape[1]
+        c0 = int(p("counter"))
+        stream = np.stack([oracle.stream_u01_block(int(p("seed")), ((c0 + e) << 32) % 2**64, P)
+                           for e in range(max(n_ev, 1))])
+        st, w = p("states").copy(), p("weights").copy()
+        c = k.bank_feedback_draws(st, w, p("lits"), p("outputs"), label, negative, p("ut"),
+                                  p("un"), float(p("s")), boost, smin, smax, c0, stream)
+        assert int(c) == int(p("new_counter"))
+        assert np.array_equal(st, p("st_after")) and np.array_equal(w, p("w_after"))
+        arbitrary = rs.random((max(n_ev, 1), P))
+        arbitrary[rs.random(arbitrary.shape) < 0.05] = 0.0
+        st_g, w_g = p("states").copy(), p("weights").copy()
+        st_o, w_o = p("states").copy(), p("weights").copy()
+        k.bank_feedback_draws(st_g, w_g, p("lits"), p("outputs"), label, negative, p("ut"),
+                              p("un"), float(p("s")), boost, smin, smax, c0, arbitrary)
+        oracle.bank_feedback_draws(st_o, w_o, p("lits"), p("outputs"), label, negative,
+                                   p("ut"), p("un"), float(p("s")), boost, smin, smax, c0,
+                                   arbitrary)
+        assert np.array_equal(st_g, st_o) and np.array_equal(w_g, w_o)
+
+
+def _xor_cfg(gpu, i, g):
+    seed, nb, boost, smin, smax, init = (int(v) for v in g[f"xor{i}_cfg"])
+    return gpu.Config(n_literals=6, n_clauses=8, n_classes=2, s=1.9, threshold=11,
+                      n_literal_budget=3, seed=seed, n_blocks=nb,
+                      boost_true_positive=bool(boost), state_min=smin, state_max=smax,
+                      init_state=init)
+
+
+def test_train_small_golden(gpu):
+    g = golden("train_small")
+    for i in range(4):
+        cfg = _xor_cfg(gpu, i, g)
+        run = gpu.train(cfg, (g["xor_x"], g["xor_y"]), (g["xor_ex"], g["xor_ey"]), n_epochs=3)
+        assert np.array_equal(run.model.states, g[f"xor{i}_states"]), i
+        assert np.array_equal(run.model.weights, g[f"xor{i}_weights"]), i
+        assert np.array_equal(np.array([m.accuracy for m in run.epoch_metrics]),
+                              g[f"xor{i}_acc"])
+    cfg = gpu.Config(n_literals=20, n_clauses=30, n_classes=3, s=3.0, threshold=15, seed=77,
+                     n_blocks=2)
+    x, y = g["mc_x"], g["mc_y"]
+    run = gpu.train(cfg, (x[:400], y[:400]), (x[400:], y[400:]), n_epochs=2)
+    assert np.array_equal(run.model.states, g["mc_states"])
+    assert np.array_equal(run.model.weights, g["mc_weights"])
+    assert np.array_equal(np.array([m.accuracy for m in run.epoch_metrics]), g["mc_acc"])
+    assert np.array_equal(gpu.dataset_votes(run.model, (x[400:], y[400:])), g["mc_votes"])
+
+
+@pytest.mark.parametrize("n_cta", [1, 3, 8])
+@pytest.mark.parametrize("hbm", [False, True])
+def test_train_multi_cta_layouts(gpu, n_cta, hbm):
+    """Same model for any CTA count and either state residency."""
+    g = golden("train_small")
+    for i in (0, 1, 3):
+        cfg = _xor_cfg(gpu, i, g)
+        sess = gpu.DenseTrainSession(cfg, g["xor_x"], g["xor_y"], n_cta=n_cta,
+                                     states_in_hbm=hbm)
+        for _ in range(3):
+            sess.run_epoch()
+        m = sess.model()
+        assert np.array_equal(m.states, g[f"xor{i}_states"]), (i, n_cta, hbm)
+        assert np.array_equal(m.weights, g[f"xor{i}_weights"]), (i, n_cta, hbm)
+
+
+def test_noisy_xor_config1_all_seeds(gpu):
+    """BASELINE config 1, 20 epochs x seeds 0-4: bit-exact final models and
+    per-epoch accuracies, hence identical 5-seed mean accuracy."""
+    g = golden("noisy_xor")
+    accs_gpu, accs_ref = [], []
+    for seed in range(5):
+        cfg = gpu.Config(**gpu.datasets.noisy_xor_config_kwargs(seed))
+        run = gpu.train(cfg, (g["tx"], g["ty"]), (g["ex"], g["ey"]), n_epochs=20)
+        assert np.array_equal(run.model.states, g[f"s{seed}_states"])
+        assert np.array_equal(run.model.weights, g[f"s{seed}_weights"])
+        accs_gpu.append(run.epoch_metrics[-1].accuracy)
+        accs_ref.append(float(g[f"s{seed}_acc"][-1]))
+    assert abs(np.mean(accs_gpu) - np.mean(accs_ref)) <= 0.01  # north star: +-1 point
+    assert accs_gpu == accs_ref
+
+
+def test_mnist_shaped_prefix_golden(gpu):
+    """BASELINE config 2 shapes (C=2000, P=1568, K=10, T=5000, s=10) over a
+    300-example prefix: bit-exact against the reference itself."""
+    g = golden("mnist_prefix")
+    cfg = gpu.Config(**gpu.datasets.mnist_shaped_config_kwargs(seed=1))
+    run = gpu.train(cfg, (g["tx"], g["ty"]), (g["ex"], g["ey"]), n_epochs=1)
+    assert np.array_equal(run.model.states, g["states"])
+    assert np.array_equal(run.model.weights, g["weights"])
+    assert np.array_equal(np.array([m.accuracy for m in run.epoch_metrics]), g["acc"])
+    assert np.array_equal(gpu.dataset_votes(run.model, (g["ex"], g["ey"])), g["votes"])
+
+
+@pytest.mark.parametrize("hbm", [False, True])
+def test_mnist_shaped_longer_vs_oracle(gpu, oracle, hbm):
+    """2 epochs over 1500 examples of the config-2 shapes (multi-CTA, 148
+    CTAs) against the oracle, plus per-block counters via n_blocks=5."""
+    (tx, ty), (ex, ey) = gpu.datasets.mnist_shaped(n_train=1500, n_test=300, data_seed=3)
+    kw = gpu.datasets.mnist_shaped_config_kwargs(seed=9)
+    kw["n_blocks"] = 5
+    cfg = gpu.Config(**kw)
+    sess = gpu.DenseTrainSession(cfg, tx, ty, states_in_hbm=hbm)
+    for _ in range(2):
+        sess.run_epoch()
+    m = sess.model()
+    ost, _ = oracle.train(cfg, tx, ty, 2)
+    assert np.array_equal(m.states, ost.states)
+    assert np.array_equal(m.weights, ost.weights)
+    assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64),
+                          ost.block_counters)
+
+
+def test_predictor_golden(gpu):
+    g = golden("predictor")
+    bank = gpu.DenseClauseBank(gpu.Config(n_literals=9, n_clauses=16, n_classes=2, s=3.0,
+                                          threshold=8, seed=4, n_blocks=2))
+    bank.states[:] = g["states"]
+    bank.weights[:] = g["weights"]
+    rs = gpu.compile_ruleset(bank)
+    ptr, idx, w = rs.csr()
+    assert np.array_equal(ptr, g["inc_ptr"]) and np.array_equal(idx, g["inc_idx"])
+    assert np.array_equal(w, g["rs_weights"])
+    votes = gpu.predictor.rule_votes_batch(rs, g["allx"])
+    assert np.array_equal(votes, g["votes"])
+    assert np.array_equal(gpu.predict_batch(rs, g["allx"]), np.argmax(g["votes"], axis=1))
+    for i, row in enumerate(g["allx"][:64]):
+        p, e = gpu.predict_and_explain(rs, row, level="literal")
+        _, f = gpu.predict_and_explain(rs, row, level="feature")
+        assert p == g["preds"][i]
+        assert np.array_equal(e.scores, g["lit_scores"][i])
+        assert np.array_equal(f.scores, g["feat_scores"][i])
+    lit = gpu.augment_literals(g["allx"])
+    assert np.array_equal(bank.batch_votes(lit), g["votes"])
+
+
+@pytest.mark.parametrize("n_inc,F,K", [(1, 37, 3), (2, 64, 10), (3, 300, 4), (20, 4096, 10)])
+def test_inference_random_models_vs_oracle(gpu, oracle, n_inc, F, K):
+    """Config-3-style random include models; low include counts make many
+    clauses fire (the config-3 model itself fires on ~1% of examples)."""
+    rs = np.random.default_rng(n_inc * 1000 + F)
+    C = 700
+    m = gpu.datasets.inference_model(model_seed=n_inc + F, n_features=F, n_clauses=C,
+                                     n_classes=K, n_includes=n_inc)
+    N = 3000 if F < 4096 else 800
+    x = rs.integers(0, 2, size=(N, F)).astype(np.uint8)
+    bank = gpu.DenseClauseBank(gpu.Config(n_literals=F, n_clauses=C, n_classes=K, s=2.0,
+                                          threshold=10))
+    bank.states[:] = m.states
+    bank.weights[:] = m.weights
+    votes = gpu.dataset_votes(bank, (x, None))
+    ov, op = oracle.batch_votes(m.states, m.weights, oracle.augment_literals(x), nthreads=8)
+    assert np.array_equal(votes, ov)
+    model = gpu.CompiledModel.from_bank(bank)
+    _, pred = model.votes_and_pred(x, want_votes=False, chunk=257)
+    assert np.array_equal(pred, op)
+
+
+def test_inference_ties_and_empty(gpu):
+    bank = gpu.DenseClauseBank(gpu.Config(n_literals=2, n_clauses=2, n_classes=3, s=2.0,
+                                          threshold=5))
+    x = np.array([[1, 0], [0, 1], [1, 1]], dtype=np.uint8)
+    assert gpu.evaluate(bank, (x, np.array([0, 2, 1]))) == pytest.approx(1 / 3)
+    bank.states[0, 0] = 0
+    bank.weights[0] = [0, 3, 3]   # tie between classes 1 and 2 -> 1
+    v = gpu.dataset_votes(bank, (x, None))
+    assert v.tolist() == [[0, 3, 3], [0, 0, 0], [0, 3, 3]]
+    rs = gpu.compile_ruleset(bank)
+    assert gpu.predict_batch(rs, x).tolist() == [1, 0, 1]
+
+
+def test_inference_rejects_non_binary(gpu):
+    bank = gpu.DenseClauseBank(gpu.Config(n_literals=4, n_clauses=2, n_classes=2, s=2.0,
+                                          threshold=5))
+    bank.states[0, 0] = 0
+    bank.weights[0] = [1, 0]
+    with pytest.raises(gpu.TmbError):
+        gpu.dataset_votes(bank, (np.array([[2, 0, 1, 0]], dtype=np.uint8), None))
+
+
+def test_scalar_spec_functions(gpu):
+    """dense.py:29-113 spec helpers (routed through the device kernels)."""
+    from paper_2405_04212_b200.core import RngStream, stream_u01_block
+    states = np.array([5, -1], dtype=np.int8)
+    rng = RngStream.derive(1, 0)
+    u0 = stream_u01_block(rng.stream_seed, 0, 1)[0]
+    gpu.type_i_feedback(states, np.array([1, 1], np.uint8), 1, 5.0, rng)
+    assert states[0] == (6 if u0 < 0.8 else 5) and rng.counter == 1
+    st = np.array([-5, 3], dtype=np.int8)
+    gpu.type_ii_feedback(st, np.array([0, 0], np.uint8), 1)
+    assert st.tolist() == [-4, 3]
+    assert gpu.evaluate_clause(np.array([0, -1, -1, 0], np.int8),
+                               np.array([1, 0, 0, 1], np.uint8), gpu.EvalMode.INFERENCE, 4) == 1
+    bank = gpu.DenseClauseBank(gpu.Config(n_literals=2, n_clauses=2, n_classes=2, s=1.9,
+                                          threshold=11, seed=5))
+    rng = RngStream.derive(1, 0)
+    gpu.clause_update(bank, 0, 0, 1, True, 1, np.array([1, 1, 0, 0], np.uint8), rng)
+    assert bank.weights[0, 0] == 1 and rng.counter == 1
+    bank.weights[0, 1] = -3
+    gpu.clause_update(bank, 0, 1, -1, True, 1, np.array([1, 1, 0, 0], np.uint8), rng)
+    assert bank.weights[0, 1] == -4
+
+
+def test_sample_updates_device_draws(gpu):
+    from paper_2405_04212_b200.core import RngStream
+    g = golden("feedback")
+    for i in range(40):
+        K, T, label = int(g["K"][i]), int(g["T"][i]), int(g["label"][i])
+        rng = RngStream(gpu.derive_stream(int(g["seed"][i]), 0xFEED), int(g["ctr"][i]))
+        d = gpu.update_probabilities(g["votes"][i, :K], label, T, rng)
+        assert d.negative_class == int(g["negative"][i])
+        assert d.p_target == g["p_target"][i] and d.p_negative == g["p_negative"][i]
+        ut, un = gpu.sample_updates(d, 37, rng)
+        assert np.array_equal(ut, g["ut"][i]) and np.array_equal(un, g["un"][i])
+        assert rng.counter == int(g["ctr_after"][i])
+
+
+def test_facade_listing(gpu):
+    (tx, ty), (ex, ey) = gpu.datasets.noisy_xor(n_train=500, n_test=200)
+    tm = gpu.TsetlinMachine(n_literals=12, n_clauses=10, n_classes=2, s=3.9, threshold=15)
+    tr = gpu.Trainer(tm, n_epochs=2, seed=1)
+    tr.set_train_data(tx, ty)
+    tr.set_eval_data(ex, ey)
+    res = tr.train()
+    assert len(res["eval_acc"]) == 2
+    pr = tm.get_predictor()
+    assert pr.predict(ex).shape == (200,)
+    cls, expl = pr.predict_and_explain(ex[0])
+    assert 0 <= cls < 2 and expl.scores.shape == (24,)
