@@ -1,0 +1,575 @@
+"""Benchmark: BASELINE.json metric "train examples/sec; inference examples/sec
+at 1/2/4/8 B200 vs roofline".
+
+Default workload (the ONE JSON line's headline): configs[1], MNIST-shaped
+Coalesced-TM training (784 features / 1568 literals, 2000 clauses, 10
+classes, T=5000, s=10, 60000 examples).  A step is one training epoch over
+the 60000 examples (one launch of the fused persistent kernel).  The line
+also carries a "secondary" object for configs[2] (batched inference over
+2^22 examples, 10000 clauses x 20 includes, 4096 features).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--workload c2-train|c3-infer|c1-train]
+
+N > 1 (torchrun, NCCL): training is sequential per example, so
+each rank trains an independent replica (different model seed) -- "replicas
+only", weak scaling; inference shards examples across ranks.  Times are CUDA
+events on the launching stream, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PEAKS = {}
+try:
+    with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+        PEAKS = json.load(fh)
+except OSError:
+    pass
+HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
+HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
+
+
+# ---------------------------------------------------------------- infra --
+
+def dist_init():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        time.sleep(0.15)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = max(mx, float(parts[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            os.unlink(self.path)
+        except OSError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def host_desc():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+# --------------------------------------------------------- c2 training --
+
+def c2_data(rank: int):
+    from paper_2405_04212_b200 import datasets
+    return datasets.mnist_shaped(data_seed=7)
+
+
+def oracle_train_rate(cfg, states, weights, counters, fb_counter, x_lit, labels, order,
+                      budget_s: float):
+    """Time the CPU oracle (C restatement of the reference train loop) from a
+    given model state on a prefix of `order`; returns (ex/s, examples)."""
+    from oracle import oracle
+    st = oracle.OracleTrainState(states.copy(), weights.copy(), counters.copy().view(np.uint64),
+                                 fb_counter, 0)
+    done, t0 = 0, time.perf_counter()
+    chunk = 100
+    while time.perf_counter() - t0 < budget_s and done < len(order):
+        oracle.train_steps(cfg, st, x_lit, labels, order[done:done + chunk])
+        done += min(chunk, len(order) - done)
+    dt = time.perf_counter() - t0
+    return done / dt, done, dt
+
+
+def bench_c2_train(args, rank, world, local):
+    import torch
+
+    import paper_2405_04212_b200 as tmb
+    from paper_2405_04212_b200 import _lib, datasets
+    (tx, ty), (ex, ey) = c2_data(rank)
+    cfg = tmb.Config(**datasets.mnist_shaped_config_kwargs(seed=rank))
+    sess = tmb.DenseTrainSession(cfg, tx, ty)
+    N = len(ty)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        sess.run_epoch()
+    torch.cuda.synchronize()
+    # model state at the start of the timed region (for the CPU baseline)
+    st0 = sess.states.cpu().numpy().copy()
+    w0 = sess.weights.cpu().numpy().copy()
+    c0 = sess.block_counters.cpu().numpy().copy()
+    fb0 = sess.fb_counter
+    stats0 = sess.stats_dict()
+    launches0 = _lib.launch_count()
+    orders = [sess.next_order().astype(np.int32) for _ in range(args.steps)]
+    orders_dev = [torch.from_numpy(o).cuda() for o in orders]
+    k_ms = []
+    barrier(world)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            flush_l2(flush)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sess.run_steps(orders_dev[i])
+            b.record(stream)
+            k_ms.append((a, b))
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    elapsed_ms = t_start.elapsed_time(t_end)
+    launches = _lib.launch_count() - launches0
+    kern_ms = [a.elapsed_time(b) for a, b in k_ms]
+    stats1 = sess.stats_dict()
+    dstats = {k: stats1[k] - stats0[k] for k in stats1}
+    elapsed_ms = max_over_ranks(elapsed_ms, world)
+    total_examples = args.steps * N * world
+    value = total_examples / (elapsed_ms / 1e3)
+
+    # ---- end to end through the public API with host buffers (per step:
+    # H2D of the epoch's features+labels from pinned memory, device packing,
+    # host shuffle, the fused kernel, D2H of the trained model)
+    xp = torch.from_numpy(np.ascontiguousarray(tx)).pin_memory()
+    yp = torch.from_numpy(np.ascontiguousarray(ty.astype(np.int32))).pin_memory()
+    st_host = torch.empty(sess.states.shape, dtype=torch.int8).pin_memory()
+    w_host = torch.empty(sess.weights.shape, dtype=torch.int32).pin_memory()
+    barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        xd = xp.to("cuda", non_blocking=True)
+        sess.labels = yp.to("cuda", non_blocking=True)
+        from paper_2405_04212_b200.runtime import ptr, stream_ptr
+        _lib.call("tmb_pack_literals", ptr(xd), N, cfg.n_literals, 1, ptr(sess.lit_words),
+                  stream_ptr())
+        order = sess.next_order().astype(np.int32)
+        od = torch.from_numpy(order).pin_memory().to("cuda", non_blocking=True)
+        sess.run_steps(od)
+        st_host.copy_(sess.states, non_blocking=True)
+        w_host.copy_(sess.weights, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_value = total_examples / (e2e_ms / 1e3)
+    h2d = tx.nbytes + N * 4 + N * 4
+    d2h = sess.states.numel() + 4 * sess.weights.numel()
+
+    # ---- roofline of the dominant kernel (k_train)
+    per_launch_ms = float(np.mean(kern_ms))
+    ex_per_launch = N
+    P, C, W = cfg.n_literal_positions, cfg.n_clauses, (cfg.n_literal_positions + 31) // 32
+    # algorithmic HBM bytes per example: literal row (W words) + label +
+    # order entry; the model is on-chip for the whole launch.
+    hbm_bytes_ex = 4 * W + 4 + 4
+    achieved_gbs = hbm_bytes_ex * ex_per_launch / (per_launch_ms / 1e3) / 1e9
+    ev_per_ex = dstats["events"] / max(dstats["examples"], 1)
+    draws_per_ex = dstats["draws"] / max(dstats["examples"], 1)
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    clocks = clk.summary()
+    f_sm = (clocks["sm_mhz"] or 1965.0) * 1e6
+    # integer-pipe roofline: SplitMix64 draw = ~30 SASS integer ops
+    # (see DESIGN.md); eval = C*W LOP3 (+popc) per example.
+    int_ops_ex = draws_per_ex * 30 + C * W * 3
+    int_peak = sm_count * 128 * f_sm  # ALU + FMA pipes, 64 lanes/clk each
+    int_achieved = int_ops_ex * ex_per_launch / (per_launch_ms / 1e3)
+
+    line = {
+        "metric": "train examples/sec (configs[1] MNIST-shaped CoTM training)",
+        "value": value, "unit": "examples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int8 TA states / int32 weights / u64 SplitMix64",
+        "data": "synthetic (seeded MNIST-shaped generator, datasets.mnist_shaped)",
+        "config": {"workload": "configs[1]: MNIST-shaped CoTM training, step = 1 epoch",
+                   "n_features": 784, "n_literals": P, "n_clauses": C, "n_classes": 10,
+                   "threshold": cfg.threshold, "s": cfg.s, "examples_per_epoch": N,
+                   "epochs_timed": f"{args.warmup + 1}..{args.warmup + args.steps}",
+                   "parallelism": f"replicas x{world} (online training is sequential)",
+                   "l2": "256 MiB buffer written before every timed epoch",
+                   "launch": sess.launch},
+        "gpu_launches": int(launches),
+        "work": {"events_per_example": ev_per_ex, "draws_per_example": draws_per_ex,
+                 "type_i_per_example": dstats["type_i"] / max(dstats["examples"], 1),
+                 "state_updates_per_example": dstats["state_updates"] / max(dstats["examples"], 1)},
+        "roofline": {"kernel": "k_train<true> (fused persistent trainer)", "bound": "hbm",
+                     "achieved": achieved_gbs, "peak": HBM_PEAK, "unit": "GB/s",
+                     "frac": achieved_gbs / HBM_PEAK, "traffic": None,
+                     "peak_source": HBM_PEAK_SRC,
+                     "algorithmic_bytes_per_example": hbm_bytes_ex,
+                     "avg_launch_ms": per_launch_ms,
+                     "note": "model is SMEM-resident for the whole launch; HBM carries only "
+                             "the packed literal rows, so this kernel is latency / "
+                             "integer-pipe bound -- see roofline_int"},
+        "roofline_int": {"bound": "int (ALU+FMA issue)", "achieved": int_achieved / 1e12,
+                         "peak": int_peak / 1e12, "unit": "Tops/s",
+                         "frac": int_achieved / int_peak,
+                         "ops_per_example": int_ops_ex,
+                         "us_per_example": per_launch_ms * 1e3 / ex_per_launch},
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": "examples/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "path": "pinned host features/labels -> H2D -> tmb_pack_literals -> host "
+                        "Fisher-Yates -> tmb_trainer_run -> D2H model"},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle
+        x_lit = oracle.augment_literals(tx)
+        rate, n_done, dt = oracle_train_rate(cfg, st0, w0, c0, fb0, x_lit, ty,
+                                             orders[0].astype(np.int64), args.cpu_seconds)
+        model_name, ncpu = host_desc()
+        line["cpu_baseline"] = {"value": rate, "unit": "examples/s", "cores": 1, "kind": "port",
+                                "sample": f"oracle C port of executor.train, {n_done} examples "
+                                          f"of timed epoch {args.warmup + 1} from the same "
+                                          f"model state ({dt:.1f}s, 1 thread; training is "
+                                          f"sequential with n_blocks=1)",
+                                "host": model_name, "host_cores": ncpu}
+    if not args.no_secondary:
+        line["secondary"] = bench_c3_infer(args, rank, world, local, embedded=True)
+    return line
+
+
+# -------------------------------------------------------- c3 inference --
+
+def c3_inputs_device(n: int, start: int, data_seed: int = 3, F: int = 4096):
+    """Device-side synthesis of the counter-based C3 inputs (same bits as
+    datasets.inference_examples)."""
+    import torch
+
+    from paper_2405_04212_b200 import _lib, datasets
+    from paper_2405_04212_b200.runtime import ptr, stream_ptr
+    W = (F + 63) // 64
+    x = torch.empty((n, F), dtype=torch.uint8, device="cuda")
+    seed = datasets.inference_stream_seed(data_seed)
+    chunk = 1 << 18
+    shifts = torch.arange(8, device="cuda", dtype=torch.uint8)
+    for lo in range(0, n, chunk):
+        m = min(chunk, n - lo)
+        words = torch.empty(m * W, dtype=torch.int64, device="cuda")
+        _lib.call("tmb_stream_u64_block", seed, (start + lo) * W, m * W, ptr(words), stream_ptr())
+        b = words.view(torch.uint8).view(m, W * 8)
+        bits = (b.unsqueeze(-1) >> shifts) & 1
+        x[lo:lo + m] = bits.view(m, W * 64)[:, :F]
+        del words, b, bits
+    return x
+
+
+def bench_c3_infer(args, rank, world, local, embedded=False):
+    import torch
+
+    import paper_2405_04212_b200 as tmb
+    from paper_2405_04212_b200 import _lib, datasets
+    F, C, K = 4096, 10000, 10
+    N_total = args.c3_examples
+    per = N_total // world
+    start = rank * per
+    n = per if rank < world - 1 else N_total - start
+    m = datasets.inference_model(model_seed=11, n_features=F, n_clauses=C, n_classes=K)
+    bank = tmb.DenseClauseBank(tmb.Config(n_literals=F, n_clauses=C, n_classes=K, s=2.0,
+                                          threshold=100))
+    bank.states[:] = m.states
+    bank.weights[:] = m.weights
+    model = tmb.CompiledModel.from_bank(bank)
+    x = c3_inputs_device(n, start)
+    pred = torch.empty(n, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        model.infer_device(x, pred_dev=pred)
+    _lib.call("tmb_infer_status", None)
+    launches0 = _lib.launch_count()
+    evs = []
+    barrier(world)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            model.infer_device(x, pred_dev=pred)
+            b.record(stream)
+            evs.append((a, b))
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = _lib.launch_count() - launches0
+    ms = max_over_ranks(t0.elapsed_time(t1), world)
+    value = N_total * args.steps / (ms / 1e3)
+    per_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    bytes_ex = F + 8  # uint8 features in, int64 prediction out
+    achieved = bytes_ex * n / (per_launch_ms / 1e3) / 1e9
+    # parity sample against the CPU oracle
+    parity = None
+    if rank == 0:
+        from oracle import oracle
+        xs = x[:1024].cpu().numpy()
+        _, op = oracle.batch_votes(m.states, m.weights, oracle.augment_literals(xs), nthreads=8)
+        parity = bool(np.array_equal(pred[:1024].cpu().numpy(), op))
+    # e2e: host (pinned) uint8 features -> tmbh_infer (chunked H2D overlapped
+    # with the kernel) -> host predictions
+    n_e2e = min(n, args.c3_e2e_examples)
+    xh = torch.empty((n_e2e, F), dtype=torch.uint8).pin_memory()
+    xh.copy_(x[:n_e2e])
+    ph = np.empty(n_e2e, dtype=np.int64)
+    from paper_2405_04212_b200.runtime import np_ptr
+    _lib.call("tmbh_infer", model._h, ct_ptr(xh), n_e2e, None, np_ptr(ph), 1 << 18)
+    barrier(world)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        _lib.call("tmbh_infer", model._h, ct_ptr(xh), n_e2e, None, np_ptr(ph), 1 << 18)
+    e2e_s = max_over_ranks(time.perf_counter() - t, world)
+    e2e_value = n_e2e * world * args.steps / e2e_s
+    out = {
+        "metric": "inference examples/sec (configs[2] batched CoTM inference)",
+        "value": value, "unit": "examples/s", "n_gpus": world, "steps": args.steps,
+        "ms_per_step": ms / args.steps,
+        "config": {"workload": "configs[2]: 2^22 examples x 4096 features, 10000 clauses x 20 "
+                               "includes, 10 classes; step = one pass over all examples",
+                   "examples": N_total, "sharding": f"contiguous example ranges over {world}",
+                   "rules": model.n_rules, "l2": "inputs (17 GB) far larger than L2"},
+        "gpu_launches": int(launches),
+        "parity_sample_1024": parity,
+        "roofline": {"kernel": "k_infer (bit-sliced rule evaluation)", "bound": "hbm",
+                     "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
+                     "frac": achieved / HBM_PEAK, "traffic": None, "peak_source": HBM_PEAK_SRC,
+                     "algorithmic_bytes_per_example": bytes_ex, "avg_launch_ms": per_launch_ms},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": "examples/s", "h2d_bytes_per_step": n_e2e * F,
+                "d2h_bytes_per_step": n_e2e * 8,
+                "path": f"pinned host uint8 [{n_e2e}, 4096] -> tmbh_infer (2-deep chunked "
+                        "H2D/compute overlap) -> host int64 predictions"},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle
+        _, ncpu = host_desc()
+        xs = x[:args.c3_cpu_examples].cpu().numpy()
+        t = time.perf_counter()
+        oracle.batch_votes(m.states, m.weights, oracle.augment_literals(xs), nthreads=ncpu,
+                           want_votes=False)
+        dt = time.perf_counter() - t
+        out["cpu_baseline"] = {"value": len(xs) / dt, "unit": "examples/s", "cores": ncpu,
+                               "kind": "port",
+                               "sample": f"oracle C port of batch_votes, {len(xs)}-example "
+                                         f"prefix, {ncpu} threads ({dt:.1f}s)"}
+    del x
+    torch.cuda.empty_cache()
+    return out
+
+
+def ct_ptr(t):
+    import ctypes as ct
+    return ct.c_void_p(t.data_ptr())
+
+
+# -------------------------------------------------------- reference arm --
+
+def bench_reference(args, rank, world):
+    """The reference's own CPU algorithm on the host cores: the oracle port
+    (a C restatement of tsetlinkit's numba loops; the Python reference does
+    not exist on the GPU box).  Rank 0 only."""
+    if rank != 0:
+        return None
+    from oracle import oracle
+
+    from paper_2405_04212_b200 import datasets
+    model_name, ncpu = host_desc()
+    if args.workload == "c3-infer":
+        m = datasets.inference_model(model_seed=11)
+        xs = datasets.inference_examples(3, 0, args.c3_cpu_examples)
+        x_lit = oracle.augment_literals(xs)
+        rates = []
+        for i in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            oracle.batch_votes(m.states, m.weights, x_lit, nthreads=ncpu, want_votes=False)
+            if i >= args.warmup:
+                rates.append(len(xs) / (time.perf_counter() - t))
+        value = float(np.mean(rates))
+        metric = "inference examples/sec (configs[2] batched CoTM inference)"
+        sample = f"{len(xs)}-example prefix per step, {ncpu} threads"
+        cores = ncpu
+    else:
+        (tx, ty), _ = c2_data(0)
+        cfg = oracle.OracleCfg(**datasets.mnist_shaped_config_kwargs(seed=0))
+        st = oracle.new_train_state(cfg)
+        x_lit = oracle.augment_literals(tx)
+        order, _ = oracle.shuffle_permutation(len(ty), oracle.derive_stream(0, 0xD157), 0)
+        rates, pos = [], 0
+        per_step = args.ref_examples
+        for i in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            oracle.train_steps(cfg, st, x_lit, ty, order[pos:pos + per_step])
+            pos += per_step
+            if i >= args.warmup:
+                rates.append(per_step / (time.perf_counter() - t))
+        value = float(np.mean(rates))
+        metric = "train examples/sec (configs[1] MNIST-shaped CoTM training)"
+        sample = (f"{per_step} consecutive examples of epoch 1 per step (warm-up steps "
+                  f"advance the model), 1 thread: training is sequential (n_blocks=1)")
+        cores = 1
+    return {"metric": metric, "value": value, "unit": "examples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 / u64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.workload},
+            "cpu_baseline": {"value": value, "unit": "examples/s", "cores": cores,
+                             "kind": "port", "sample": sample, "host": model_name},
+            "e2e": {"value": value, "unit": "examples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+# ------------------------------------------------------------------ main --
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2-train", choices=["c2-train", "c3-infer"])
+    ap.add_argument("--c3-examples", type=int, default=1 << 22)
+    ap.add_argument("--c3-e2e-examples", type=int, default=1 << 20)
+    ap.add_argument("--c3-cpu-examples", type=int, default=1 << 13)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-examples", type=int, default=1500)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        line = bench_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    rank, world, local = dist_init()
+    import paper_2405_04212_b200 as tmb
+    tmb.runtime.require_device()
+    if args.workload == "c3-infer":
+        line = bench_c3_infer(args, rank, world, local)
+        line.update({"higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                     "warmup": args.warmup, "dtype": "u8 features / int32 votes",
+                     "data": "synthetic (counter-based Bernoulli(0.5) generator)"})
+        line["scaling"] = "strong"
+    else:
+        line = bench_c2_train(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -212,14 +212,136 @@ typedef struct {
 
 /* kernels/_numba.py:71-90.  u01 draw for position k is supplied either by
  * the stream (draws == NULL: stream_u01(seed, base + k)) or by an explicit
- * row (draws != NULL: draws[k]) -- the explicit-draws test hook. */
+ * row (draws != NULL: draws[k]) -- the explicit-draws test hook.  The stream
+ * loop is written branch-free so the compiler vectorises the 64-bit
+ * SplitMix64 arithmetic the way numba/LLVM does for the reference (AVX-512DQ
+ * vpmullq); target_clones keeps the .so portable across host CPUs. */
+/* Draw phase of Type I for positions [k0, k0+n): bit i of inc_bits / dec_bits
+ * = (u_{k0+i} < p_inc) / (u_{k0+i} < p_dec), computed as the exact integer
+ * compare (z >> 11) < ceil(p * 2^53) (u = (z >> 11) * 2^-53 is a multiple of
+ * 2^-53, tests/test_oracle_golden.py::test_integer_threshold_identity).  An
+ * AVX-512DQ path (8 SplitMix64 lanes per vpmullq) is chosen at run time when
+ * the host supports it -- the reference's numba kernels are likewise compiled
+ * for the host CPU. */
+#include <immintrin.h>
+#define OR_CHUNK 512
+
+static uint64_t or_threshold(double p) {
+    double x = p * 9007199254740992.0;
+    if (x <= 0.0) return 0;
+    if (x >= 9007199254740992.0) return 1ULL << 53;
+    return (uint64_t)ceil(x);
+}
+
+__attribute__((target("avx512f,avx512dq")))
+static void or_draw_bits_avx512(uint64_t zb, int64_t k0, int64_t n, uint64_t t_inc,
+                                uint64_t t_dec, uint8_t *inc_bits, uint8_t *dec_bits) {
+    const __m512i G = _mm512_set1_epi64((long long)OR_GOLDEN);
+    const __m512i C1 = _mm512_set1_epi64((long long)OR_C1);
+    const __m512i C2 = _mm512_set1_epi64((long long)OR_C2);
+    const __m512i TI = _mm512_set1_epi64((long long)t_inc);
+    const __m512i TD = _mm512_set1_epi64((long long)t_dec);
+    const __m512i lane = _mm512_set_epi64(7, 6, 5, 4, 3, 2, 1, 0);
+    const __m512i ZB = _mm512_set1_epi64((long long)zb);
+    for (int64_t i = 0; i < n; i += 8) {
+        __m512i k = _mm512_add_epi64(_mm512_set1_epi64(k0 + i), lane);
+        __m512i z = _mm512_add_epi64(ZB, _mm512_mullo_epi64(G, k));
+        z = _mm512_mullo_epi64(_mm512_xor_si512(z, _mm512_srli_epi64(z, 30)), C1);
+        z = _mm512_mullo_epi64(_mm512_xor_si512(z, _mm512_srli_epi64(z, 27)), C2);
+        z = _mm512_xor_si512(z, _mm512_srli_epi64(z, 31));
+        __m512i m = _mm512_srli_epi64(z, 11);
+        inc_bits[i >> 3] = (uint8_t)_mm512_cmplt_epu64_mask(m, TI);
+        dec_bits[i >> 3] = (uint8_t)_mm512_cmplt_epu64_mask(m, TD);
+    }
+}
+
+static void or_draw_bits_scalar(uint64_t zb, int64_t k0, int64_t n, uint64_t t_inc,
+                                uint64_t t_dec, uint8_t *inc_bits, uint8_t *dec_bits) {
+    for (int64_t i = 0; i < n; i += 8) {
+        uint8_t a = 0, b = 0;
+        for (int q = 0; q < 8; ++q) {
+            uint64_t m = or_mix64(zb + OR_GOLDEN * (uint64_t)(k0 + i + q)) >> 11;
+            a |= (uint8_t)((m < t_inc) << q);
+            b |= (uint8_t)((m < t_dec) << q);
+        }
+        inc_bits[i >> 3] = a;
+        dec_bits[i >> 3] = b;
+    }
+}
+
+static int or_have_avx512 = -1;
+
+/* Byte phase, 64 positions per step (AVX-512BW masked adds). */
+__attribute__((target("avx512f,avx512bw")))
+static void or_apply_avx512(int8_t *row, const uint8_t *lits, int64_t n, int output, int boost,
+                            int smin, int smax, const uint8_t *ib, const uint8_t *db) {
+    const __m512i one = _mm512_set1_epi8(1);
+    const __m512i vmax = _mm512_set1_epi8((char)smax), vmin = _mm512_set1_epi8((char)smin);
+    int64_t i = 0;
+    for (; i + 64 <= n; i += 64) {
+        __m512i st = _mm512_loadu_si512((const void *)(row + i));
+        __m512i li = _mm512_loadu_si512((const void *)(lits + i));
+        __mmask64 on = output ? _mm512_cmpeq_epi8_mask(li, one) : 0;
+        uint64_t ibits, dbits;
+        memcpy(&ibits, ib + (i >> 3), 8);
+        memcpy(&dbits, db + (i >> 3), 8);
+        __mmask64 inc = on & (boost ? ~0ULL : ibits) & _mm512_cmplt_epi8_mask(st, vmax);
+        __mmask64 dec = ~on & dbits & _mm512_cmpgt_epi8_mask(st, vmin);
+        st = _mm512_mask_add_epi8(st, inc, st, one);
+        st = _mm512_mask_sub_epi8(st, dec, st, one);
+        _mm512_storeu_si512((void *)(row + i), st);
+    }
+    for (; i < n; ++i) {
+        int st = row[i];
+        int on = output & (lits[i] == 1);
+        int inc = on & (boost | ((ib[i >> 3] >> (i & 7)) & 1)) & (st < smax);
+        int dec = (!on) & ((db[i >> 3] >> (i & 7)) & 1) & (st > smin);
+        row[i] = (int8_t)(st + inc - dec);
+    }
+}
+
+static void type_i_stream_row(int8_t *row, int64_t P, const uint8_t *lits, int output,
+                              double p_inc, double p_dec, int boost, int smin, int smax,
+                              uint64_t seed, uint64_t base) {
+    if (or_have_avx512 < 0) {
+        __builtin_cpu_init();
+        or_have_avx512 = __builtin_cpu_supports("avx512f") &&
+                         __builtin_cpu_supports("avx512dq") && __builtin_cpu_supports("avx512bw");
+    }
+    const uint64_t zb = seed + OR_GOLDEN * (base + 1);
+    const uint64_t t_inc = or_threshold(p_inc), t_dec = or_threshold(p_dec);
+    uint8_t ib[OR_CHUNK / 8 + 8], db[OR_CHUNK / 8 + 8];
+    for (int64_t k0 = 0; k0 < P; k0 += OR_CHUNK) {
+        int64_t n = P - k0 < OR_CHUNK ? P - k0 : OR_CHUNK;
+        int64_t n8 = (n + 7) & ~7LL;
+        if (or_have_avx512) {
+            or_draw_bits_avx512(zb, k0, n8, t_inc, t_dec, ib, db);
+            or_apply_avx512(row + k0, lits + k0, n, output, boost, smin, smax, ib, db);
+            continue;
+        }
+        or_draw_bits_scalar(zb, k0, n8, t_inc, t_dec, ib, db);
+        for (int64_t i = 0; i < n; ++i) {
+            int st = row[k0 + i];
+            int on = output & (lits[k0 + i] == 1);
+            int inc = on & (boost | ((ib[i >> 3] >> (i & 7)) & 1)) & (st < smax);
+            int dec = (!on) & ((db[i >> 3] >> (i & 7)) & 1) & (st > smin);
+            row[k0 + i] = (int8_t)(st + inc - dec);
+        }
+    }
+}
+
 static void type_i(int8_t *row, int64_t P, const uint8_t *lits, int output,
                    const or_fb_params *fp, uint64_t seed, uint64_t base,
                    const double *draws) {
     double p_inc = (fp->s - 1.0) / fp->s;
     double p_dec = 1.0 / fp->s;
+    if (!draws) {
+        type_i_stream_row(row, P, lits, output == 1, p_inc, p_dec, fp->boost != 0,
+                          fp->state_min, fp->state_max, seed, base);
+        return;
+    }
     for (int64_t k = 0; k < P; ++k) {
-        double u = draws ? draws[k] : or_stream_u01(seed, base + (uint64_t)k);
+        double u = draws[k];
         int st = row[k];
         if (output == 1 && lits[k] == 1) {
             if ((fp->boost || u < p_inc) && st < fp->state_max) row[k] = (int8_t)(st + 1);
