@@ -117,6 +117,29 @@ def test_train_multi_cta_layouts(gpu, n_cta, hbm):
         assert np.array_equal(m.weights, g[f"xor{i}_weights"]), (i, n_cta, hbm)
 
 
+@pytest.mark.parametrize("n_cta", [1, 7, 16, 20, 37])
+@pytest.mark.parametrize("n_blocks", [1, 3, 11])
+def test_train_block_layouts_vs_oracle(gpu, oracle, n_cta, n_blocks):
+    """Clause blocks that straddle CTA boundaries in both sync domains
+    (cluster mode up to 16 CTAs, grid mode above), odd P (not a multiple of
+    4: scalar state path), HBM-resident states."""
+    rs = np.random.default_rng(n_cta * 100 + n_blocks)
+    x = rs.integers(0, 2, size=(250, 27)).astype(np.uint8)
+    y = ((x[:, 0] + x[:, 3] * 2 + x[:, 9]) % 4).astype(np.int64)
+    cfg = gpu.Config(n_literals=27, n_clauses=45, n_classes=4, s=2.5, threshold=9, seed=n_cta,
+                     n_blocks=n_blocks, n_literal_budget=6)
+    for hbm in (False, True):
+        sess = gpu.DenseTrainSession(cfg, x, y, n_cta=n_cta, states_in_hbm=hbm)
+        sess.run_epoch()
+        sess.run_epoch()
+        m = sess.model()
+        ost, _ = oracle.train(cfg, x, y, 2)
+        assert np.array_equal(m.states, ost.states), (n_cta, n_blocks, hbm)
+        assert np.array_equal(m.weights, ost.weights), (n_cta, n_blocks, hbm)
+        assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64),
+                              ost.block_counters)
+
+
 def test_noisy_xor_config1_all_seeds(gpu):
     """BASELINE config 1, 20 epochs x seeds 0-4: bit-exact final models and
     per-epoch accuracies, hence identical 5-seed mean accuracy."""
@@ -145,15 +168,17 @@ def test_mnist_shaped_prefix_golden(gpu):
     assert np.array_equal(gpu.dataset_votes(run.model, (g["ex"], g["ey"])), g["votes"])
 
 
-@pytest.mark.parametrize("hbm", [False, True])
-def test_mnist_shaped_longer_vs_oracle(gpu, oracle, hbm):
-    """2 epochs over 1500 examples of the config-2 shapes (multi-CTA, 148
-    CTAs) against the oracle, plus per-block counters via n_blocks=5."""
+@pytest.mark.parametrize("n_cta,hbm", [(0, False), (0, True), (148, False), (148, True),
+                                       (5, False), (64, True)])
+def test_mnist_shaped_longer_vs_oracle(gpu, oracle, n_cta, hbm):
+    """2 epochs over 1500 examples of the config-2 shapes against the oracle,
+    in cluster mode (<= 16 CTAs, DSMEM exchange) and grid mode (cooperative
+    grid, global barrier), with per-block counters via n_blocks=5."""
     (tx, ty), (ex, ey) = gpu.datasets.mnist_shaped(n_train=1500, n_test=300, data_seed=3)
     kw = gpu.datasets.mnist_shaped_config_kwargs(seed=9)
     kw["n_blocks"] = 5
     cfg = gpu.Config(**kw)
-    sess = gpu.DenseTrainSession(cfg, tx, ty, states_in_hbm=hbm)
+    sess = gpu.DenseTrainSession(cfg, tx, ty, n_cta=n_cta, states_in_hbm=hbm)
     for _ in range(2):
         sess.run_epoch()
     m = sess.model()
