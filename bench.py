@@ -190,7 +190,7 @@ def bench_c2_train(args, rank, world, local):
     from paper_2405_04212_b200 import _lib, datasets
     (tx, ty), (ex, ey) = c2_data(rank)
     cfg = tmb.Config(**datasets.mnist_shaped_config_kwargs(seed=rank))
-    sess = tmb.DenseTrainSession(cfg, tx, ty)
+    sess = tmb.DenseTrainSession(cfg, tx, ty, n_cta=args.train_cta, threads=args.train_threads)
     N = len(ty)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -541,6 +541,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-examples", type=int, default=1500)
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--train-cta", type=int, default=0, help="0 = auto")
+    ap.add_argument("--train-threads", type=int, default=0, help="0 = auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

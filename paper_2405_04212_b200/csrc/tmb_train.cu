@@ -83,22 +83,27 @@ __device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+
 enum : int { I_TEV = 1, I_NEV = 2, I_T1 = 4, I_N1 = 8, I_OUT = 16 };
+enum : int { MODE_CLUSTER = 0, MODE_GRID = 1 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Flag-draw precompute capacity (entries per stream) in shared memory.
+constexpr int kMaxPrecompute = 4096;
+
 struct Smem {
     uint32_t *lit0, *lit1, *masks, *ut_bits, *un_bits;
-    int32_t *word_cum, *weights, *work, *info, *lpref, *cta_pfx, *blk_lo, *blk_hi, *wsum;
-    uint64_t *sk_t, *sk_n, *blk_ctr, *draw_t, *draw_n;
+    int32_t *word_cum, *weights, *work, *info, *cnt;
+    uint64_t *sk_t, *sk_n, *blk_ctr, *blk_seed, *draw_t, *draw_n;
     int8_t *states;
-    long long *votes;  // [K] partial (cluster) / total (single)
-    int *misc;         // [0]=n_work [1]=negative [2]=label [3..5]=example ring
-    uint64_t *thr;     // [0]=t_t [1]=t_n
+    long long *vin;    // cluster: [2][16][K] vote inbox (pushed by every CTA)
+    int *misc;         // [0]=n_work [3..5]=example ring
+    uint64_t *thr;     // grid: [0]=t_t [1]=t_n [2]=negative
 };
 
 // Shared-memory carve-up; identical on host (size) and device (pointers).
-__host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states, bool cluster,
+__host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states, int mode,
                                               char *base, Smem *s) {
     size_t off = 0;
     auto take = [&](size_t bytes) -> char * {
@@ -111,33 +116,23 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.sk_t = (uint64_t *)take(8 * k.cmax);
     t.sk_n = (uint64_t *)take(8 * k.cmax);
     t.blk_ctr = (uint64_t *)take(8 * (k.bmax + 1));
-    t.thr = (uint64_t *)take(8 * 2);
-    t.votes = (long long *)take(8 * k.K);
+    t.blk_seed = (uint64_t *)take(8 * (k.bmax + 1));
+    t.thr = (uint64_t *)take(8 * 4);
+    t.vin = mode == MODE_CLUSTER ? (long long *)take(8 * 2 * 16 * k.K) : nullptr;
     t.lit0 = (uint32_t *)take(4 * k.W);
     t.lit1 = (uint32_t *)take(4 * k.W);
     t.masks = (uint32_t *)take(4 * (size_t)k.cmax * k.W);
     t.weights = (int32_t *)take(4 * (size_t)k.cmax * k.K);
     t.work = (int32_t *)take(4 * k.cmax);
     t.info = (int32_t *)take(4 * k.cmax);
+    t.cnt = (int32_t *)take(4 * k.cmax);
     t.misc = (int *)take(4 * 8);
-    t.wsum = (int32_t *)take(4 * 32);
-    if (cluster) {
-        t.draw_t = (uint64_t *)take(8 * k.cmax);
-        t.draw_n = (uint64_t *)take(8 * k.cmax);
-        t.lpref = (int32_t *)take(4 * (k.cmax + 1));
-        t.cta_pfx = (int32_t *)take(4 * 32);
-        t.blk_lo = (int32_t *)take(4 * (k.bmax + 1));
-        t.blk_hi = (int32_t *)take(4 * (k.bmax + 1));
-        t.ut_bits = t.un_bits = nullptr;
-        t.word_cum = nullptr;
-    } else {
-        t.ut_bits = (uint32_t *)take(4 * k.fmax_words);
-        t.un_bits = (uint32_t *)take(4 * k.fmax_words);
-        t.word_cum = (int32_t *)take(4 * (k.fmax_words + 1));
-        t.draw_t = (uint64_t *)take(8 * 32 * k.fmax_words);
-        t.draw_n = (uint64_t *)take(8 * 32 * k.fmax_words);
-        t.lpref = t.cta_pfx = t.blk_lo = t.blk_hi = nullptr;
-    }
+    t.ut_bits = (uint32_t *)take(4 * k.fmax_words);
+    t.un_bits = (uint32_t *)take(4 * k.fmax_words);
+    t.word_cum = (int32_t *)take(4 * (k.fmax_words + 1));
+    const bool pre = 32 * k.fmax_words <= kMaxPrecompute;
+    t.draw_t = pre ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
+    t.draw_n = pre ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
     if (s) *s = t;
     return align_up(off, 16);
@@ -148,98 +143,125 @@ struct Counters {
 };
 
 // Per-position feedback over the CTA's work list, four positions per thread
-// (one 32-bit state word), include masks rebuilt from the new states.
-// kernels/_numba.py:71-98 semantics per position, target event then negative
-// event.
+// (one 32-bit state word), include masks + include counts rebuilt from the
+// new states.  kernels/_numba.py:71-98 per position, target event then
+// negative event.  Up to four state words per thread are loaded
+// before any is processed so the L2 round trips of HBM-resident states
+// overlap.
 template <bool SMEM_STATES>
 __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, int c0,
                                                const uint32_t *lit, int n_work, Counters &cn) {
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int QP = k.Ppad >> 2;  // quads per (padded) row; multiple of 32
     const int total = n_work * QP;
-    int wc = tid / QP, q = tid - (tid / QP) * QP;
-    for (int it = tid; it < total; it += nthr) {
-        const int j = s.work[wc];
-        const int info = s.info[j];
-        const int out = (info & I_OUT) ? 1 : 0;
-        const int p0 = q << 2;
-        uint32_t word;
-        int8_t *grow = k.states + (int64_t)(c0 + j) * k.P;
-        if (SMEM_STATES) {
-            word = *reinterpret_cast<const uint32_t *>(s.states + (size_t)j * k.Ppad + p0);
-        } else if (k.vec4 && p0 + 4 <= k.P) {
-            word = *reinterpret_cast<const uint32_t *>(grow + p0);
-        } else {
-            word = 0xFFFFFFFFu;
-            for (int b = 0; b < 4; ++b)
-                if (p0 + b < k.P) word = (word & ~(0xFFu << (8 * b))) | ((uint32_t)(uint8_t)grow[p0 + b] << (8 * b));
-        }
-        const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
-        uint32_t nw = word, nib = 0;
+    constexpr int B = 4;
+    for (int it0 = tid; it0 < total; it0 += B * nthr) {
+        uint32_t word[B];
+        int jj[B], pp[B];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int p = p0 + b;
-            int st = (int)(int8_t)(word >> (8 * b));
-            if (p < k.P) {
-                const int l = (litn >> b) & 1;
-                int st0 = st;
-                uint64_t nd = 0;
-                if (info & I_TEV) {
-                    if (info & I_T1) st = type_i_stream(st, l, out, k.fp, s.sk_t[j], (uint32_t)p, nd);
-                    else st = type_ii(st, l, out);
+        for (int u = 0; u < B; ++u) {
+            const int it = it0 + u * nthr;
+            jj[u] = -1;
+            word[u] = 0xFFFFFFFFu;
+            if (it < total) {
+                const int wc = it / QP;
+                const int p0 = (it - wc * QP) << 2;
+                const int j = s.work[wc];
+                jj[u] = j;
+                pp[u] = p0;
+                if (SMEM_STATES) {
+                    word[u] = *reinterpret_cast<const uint32_t *>(s.states + (size_t)j * k.Ppad + p0);
+                } else {
+                    const int8_t *grow = k.states + (int64_t)(c0 + j) * k.P;
+                    if (k.vec4 && p0 + 4 <= k.P) {
+                        word[u] = __ldcg(reinterpret_cast<const unsigned int *>(grow + p0));
+                    } else {
+                        for (int b = 0; b < 4; ++b)
+                            if (p0 + b < k.P)
+                                word[u] = (word[u] & ~(0xFFu << (8 * b))) |
+                                          ((uint32_t)(uint8_t)grow[p0 + b] << (8 * b));
+                    }
                 }
-                if (info & I_NEV) {
-                    if (info & I_N1) st = type_i_stream(st, l, out, k.fp, s.sk_n[j], (uint32_t)p, nd);
-                    else st = type_ii(st, l, out);
-                }
-                cn.draws += nd;
-                if (st != st0) {
-                    ++cn.upd;
-                    nw = (nw & ~(0xFFu << (8 * b))) | ((uint32_t)(uint8_t)st << (8 * b));
-                }
-                nib |= (uint32_t)(st >= 0) << b;
             }
         }
-        if (nw != word) {
-            if (SMEM_STATES) {
-                *reinterpret_cast<uint32_t *>(s.states + (size_t)j * k.Ppad + p0) = nw;
-            } else if (k.vec4 && p0 + 4 <= k.P) {
-                *reinterpret_cast<uint32_t *>(grow + p0) = nw;
-            } else {
-                for (int b = 0; b < 4; ++b)
-                    if (p0 + b < k.P) grow[p0 + b] = (int8_t)(nw >> (8 * b));
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (it0 + u * nthr >= total) break;  // warp-uniform (total % 32 == 0)
+            const int j = jj[u], p0 = pp[u];
+            const int info = s.info[j];
+            const int out = (info & I_OUT) ? 1 : 0;
+            const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
+            uint32_t nw = word[u], nib = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int p = p0 + b;
+                int st = (int)(int8_t)(word[u] >> (8 * b));
+                if (p < k.P) {
+                    const int l = (litn >> b) & 1;
+                    const int st0 = st;
+                    uint64_t nd = 0;
+                    if (info & I_TEV) {
+                        if (info & I_T1) st = type_i_stream(st, l, out, k.fp, s.sk_t[j], (uint32_t)p, nd);
+                        else st = type_ii(st, l, out);
+                    }
+                    if (info & I_NEV) {
+                        if (info & I_N1) st = type_i_stream(st, l, out, k.fp, s.sk_n[j], (uint32_t)p, nd);
+                        else st = type_ii(st, l, out);
+                    }
+                    cn.draws += nd;
+                    if (st != st0) {
+                        ++cn.upd;
+                        nw = (nw & ~(0xFFu << (8 * b))) | ((uint32_t)(uint8_t)st << (8 * b));
+                    }
+                    nib |= (uint32_t)(st >= 0) << b;
+                }
             }
-        }
-        // mask word for positions 32*w .. : lanes 8g..8g+7 hold its 8 nibbles
-        uint32_t m = nib << ((lane & 7) * 4);
-        m |= __shfl_xor_sync(0xffffffffu, m, 1);
-        m |= __shfl_xor_sync(0xffffffffu, m, 2);
-        m |= __shfl_xor_sync(0xffffffffu, m, 4);
-        if ((lane & 7) == 0) {
-            const int w = p0 >> 5;
-            if (w < k.W) s.masks[j * k.W + w] = m;
-        }
-        q += nthr;
-        while (q >= QP) {
-            q -= QP;
-            ++wc;
+            if (nw != word[u]) {
+                if (SMEM_STATES) {
+                    *reinterpret_cast<uint32_t *>(s.states + (size_t)j * k.Ppad + p0) = nw;
+                } else {
+                    int8_t *grow = k.states + (int64_t)(c0 + j) * k.P;
+                    if (k.vec4 && p0 + 4 <= k.P) {
+                        __stcg(reinterpret_cast<unsigned int *>(grow + p0), nw);
+                    } else {
+                        for (int b = 0; b < 4; ++b)
+                            if (p0 + b < k.P) grow[p0 + b] = (int8_t)(nw >> (8 * b));
+                    }
+                }
+            }
+            // mask word for positions 32w..32w+31: lanes 8g..8g+7 hold its nibbles
+            uint32_t m = nib << ((lane & 7) * 4);
+            m |= __shfl_xor_sync(0xffffffffu, m, 1);
+            m |= __shfl_xor_sync(0xffffffffu, m, 2);
+            m |= __shfl_xor_sync(0xffffffffu, m, 4);
+            if ((lane & 7) == 0) {
+                const int w = p0 >> 5;
+                if (w < k.W) {
+                    const uint32_t old = s.masks[j * k.W + w];
+                    if (old != m) {
+                        s.masks[j * k.W + w] = m;
+                        atomicAdd(&s.cnt[j], __popc(m) - __popc(old));
+                    }
+                }
+            }
         }
     }
 }
 
-// Load the model slice into shared memory and build the include masks.
+// Load the model slice into shared memory, build include masks and counts.
 template <bool SMEM_STATES>
 __device__ __forceinline__ void load_slice(const TrainK &k, const Smem &s, int c0, int cown) {
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int warp = tid >> 5, nwarps = nthr >> 5;
     for (int i = tid; i < cown * k.K; i += nthr) s.weights[i] = k.weights[(int64_t)c0 * k.K + i];
+    for (int i = tid; i < cown; i += nthr) s.cnt[i] = 0;
     if (SMEM_STATES) {
         for (int i = tid; i < cown * k.Ppad; i += nthr) {
             int j = i / k.Ppad, p = i - j * k.Ppad;
             s.states[i] = p < k.P ? k.states[(int64_t)(c0 + j) * k.P + p] : (int8_t)-1;
         }
-        __syncthreads();
     }
+    __syncthreads();
     for (int it = warp; it < cown * k.W; it += nwarps) {
         int j = it / k.W, w = it - j * k.W;
         int p = w * 32 + lane;
@@ -247,7 +269,10 @@ __device__ __forceinline__ void load_slice(const TrainK &k, const Smem &s, int c
         if (SMEM_STATES) st = s.states[j * k.Ppad + p];
         else st = p < k.P ? k.states[(int64_t)(c0 + j) * k.P + p] : -1;
         unsigned m = __ballot_sync(0xffffffffu, st >= 0);
-        if (lane == 0) s.masks[j * k.W + w] = m;
+        if (lane == 0) {
+            s.masks[j * k.W + w] = m;
+            if (m) atomicAdd(&s.cnt[j], __popc(m));
+        }
     }
 }
 
@@ -284,13 +309,11 @@ __device__ __forceinline__ void flush_stats(const TrainK &k, Counters &cn, bool 
         atomicAdd((unsigned long long *)&k.stats->examples, (unsigned long long)k.n_steps);
 }
 
-// Example ring in shared memory: misc[3 + (i % 3)] = order[i]; rows of
-// example i live in lit[i & 1].  Issued one/two examples ahead so the
-// dependent global loads overlap the current example.
+// Example ring in shared memory: misc[3 + (i % 3)] = order[i]; the literal
+// row of example i lives in lit{i&1}.  Issued one / two examples ahead so
+// the dependent global loads overlap the current example.
 __device__ __forceinline__ void prefetch(const TrainK &k, const Smem &s, int64_t i) {
-    // order index two ahead
     if (threadIdx.x == 0 && i + 2 < k.n_steps) s.misc[3 + (int)((i + 2) % 3)] = __ldg(&k.order[i + 2]);
-    // literal row one ahead (its index arrived one iteration ago)
     if (i + 1 < k.n_steps) {
         const int ex = s.misc[3 + (int)((i + 1) % 3)];
         uint32_t *dst = ((i + 1) & 1) ? s.lit1 : s.lit0;
@@ -310,265 +333,58 @@ __device__ __forceinline__ void prologue_ring(const TrainK &k, const Smem &s) {
         s.lit0[w] = __ldg(&k.lit_words[(int64_t)ex * k.W + w]);
 }
 
-// training-mode clause outputs (kernels/_numba.py:36-50) -> info[j] = I_OUT|0
-__device__ __forceinline__ void eval_own(const TrainK &k, const Smem &s, const uint32_t *lit,
-                                         int cown) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (int j = warp; j < cown; j += nwarps) {
-        uint32_t viol = 0;
-        int cnt = 0;
-        for (int w = lane; w < k.W; w += 32) {
-            uint32_t m = s.masks[j * k.W + w];
-            viol |= m & ~lit[w];
-            cnt += __popc(m);
-        }
-        viol = __reduce_or_sync(0xffffffffu, viol);
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) s.info[j] = (viol == 0 && cnt <= k.budget) ? I_OUT : 0;
-    }
-}
-
-// partial class sums of own clauses (dense.py:153): warp per class
-__device__ __forceinline__ void partial_votes(const TrainK &k, const Smem &s, int cown) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (int kk = warp; kk < k.K; kk += nwarps) {
-        long long v = 0;
-        for (int j = lane; j < cown; j += 32)
-            if (s.info[j] & I_OUT) v += s.weights[j * k.K + kk];
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) s.votes[kk] = v;
-    }
-}
-
-// feedback.py:33-44 given the summed votes of the label / negative classes.
-__device__ __forceinline__ void decide(const TrainK &k, long long vl, long long vn, uint64_t *thr) {
+// feedback.py:33-44: clipped update probabilities -> integer thresholds.
+__device__ __forceinline__ void decide(const TrainK &k, long long vl, long long vn,
+                                       uint64_t &t_t, uint64_t &t_n) {
     const long long T = k.T;
-    long long cl = vl < -T ? -T : (vl > T ? T : vl);
-    long long cn = vn < -T ? -T : (vn > T ? T : vn);
-    double pt = (double)(T - cl) / (2.0 * (double)T);
-    double pn = (double)(T + cn) / (2.0 * (double)T);
-    thr[0] = prob_threshold(pt);
-    thr[1] = prob_threshold(pn);
+    const long long cl = vl < -T ? -T : (vl > T ? T : vl);
+    const long long cn = vn < -T ? -T : (vn > T ? T : vn);
+    const double pt = (double)(T - cl) / (2.0 * (double)T);
+    const double pn = (double)(T + cn) / (2.0 * (double)T);
+    t_t = prob_threshold(pt);
+    t_n = prob_threshold(pn);
 }
 
 __device__ __forceinline__ int negative_class(const TrainK &k, int label, uint64_t fbc) {
-    double u = u01_from53(draw53(k.fb_seed, fbc));
+    const double u = u01_from53(draw53(k.fb_seed, fbc));
     return (int)((label + 1 + (int64_t)(u * (double)(k.K - 1))) % k.K);
 }
 
-// Event bookkeeping for own clause j given its window ordinal (events of its
-// block before it, plus the block counter).  Updates weights (feedback first,
-// then weight) and appends to the work list.
-__device__ __forceinline__ void clause_events(const TrainK &k, const Smem &s, int j, int c,
-                                              bool t_ev, bool n_ev, uint64_t ord, int label,
-                                              int neg, Counters &cn) {
-    int info = s.info[j] & I_OUT;
-    if (t_ev || n_ev) {
-        const uint64_t bseed = k.block_seeds[block_of(c, k.C, k.n_blocks)];
-        const bool out = info & I_OUT;
-        int32_t *w = s.weights + j * k.K;
-        const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
-        if (t_ev) {
-            info |= I_TEV | (t1 ? I_T1 : 0);
-            s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
-            ++cn.events;
-            if (t1) ++cn.t1; else if (out) ++cn.t2;
-        }
-        if (n_ev) {
-            const uint64_t o2 = ord + (t_ev ? 1 : 0);
-            info |= I_NEV | (n1 ? I_N1 : 0);
-            s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
-            ++cn.events;
-            if (n1) ++cn.t1; else if (out) ++cn.t2;
-        }
-        if (out) {
-            if (t_ev) w[label] += 1;
-            if (n_ev) w[neg] -= 1;
-        }
-        const bool work = (t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out));
-        if (work) s.work[atomicAdd(&s.misc[0], 1)] = j;
-    }
-    s.info[j] = info;
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// ============================================================ CLUSTER mode
-template <bool SMEM_STATES>
-__global__ void __launch_bounds__(512, 1) k_train_cluster(TrainK k) {
+// One fused kernel, two synchronisation domains (see the header comment).
+template <int MODE, bool SMEM_STATES>
+__global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
     extern __shared__ __align__(16) char smem_raw[];
-    cg::cluster_group cluster = cg::this_cluster();
     Smem s;
-    smem_layout(k, SMEM_STATES, true, smem_raw, &s);
+    smem_layout(k, SMEM_STATES, MODE, smem_raw, &s);
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int rank = (int)cluster.block_rank();
-    const int n_cta = k.n_cta, C = k.C, K = k.K;
+    const int nwarps = nthr >> 5;
+    int rank;
+    if (MODE == MODE_CLUSTER) rank = (int)cg::this_cluster().block_rank();
+    else rank = blockIdx.x;
+    const int C = k.C, K = k.K, n_cta = k.n_cta;
     const int c0 = cta_begin(rank, C, n_cta), c1 = cta_begin(rank + 1, C, n_cta);
-    const int cown = c1 - c0;
-    const int b0 = block_of(c0, C, k.n_blocks), b1 = block_of(c1 - 1, C, k.n_blocks);
-
-    load_slice<SMEM_STATES>(k, s, c0, cown);
-    for (int i = tid; i <= b1 - b0; i += nthr) s.blk_ctr[i] = k.block_counters[b0 + i];
-    prologue_ring(k, s);
-    __syncthreads();
-    cluster.sync();  // every CTA of the cluster is resident before DSMEM use
-
-    Counters cn;
-    const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
-    for (int64_t i = 0; i < k.n_steps; ++i) {
-        const uint32_t *lit = (i & 1) ? s.lit1 : s.lit0;
-        const int ex = s.misc[3 + (int)(i % 3)];
-        const int label = __ldg(&k.labels[ex]);
-        const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
-        // 1. outputs of own clauses; update-flag draws of own clauses (they do
-        //    not depend on the votes); prefetch the next example
-        eval_own(k, s, lit, cown);
-        for (int j = tid; j < cown; j += nthr) {
-            s.draw_t[j] = draw53(k.fb_seed, fbc + 1 + (uint64_t)(c0 + j));
-            s.draw_n[j] = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)(c0 + j));
-        }
-        if (tid == 0) s.misc[0] = 0;
-        prefetch(k, s, i);
-        const int neg = negative_class(k, label, fbc);
-        __syncthreads();
-        // 2. partial class sums
-        partial_votes(k, s, cown);
-        cluster.sync();  // #1: partial votes visible cluster-wide
-        // 3. decision from the cluster's summed votes
-        if (warp == 0) {
-            long long v = 0;
-            if (lane < n_cta) {
-                const long long *rv = cluster.map_shared_rank(s.votes, lane);
-                v = rv[label];
-            } else if (lane >= 16 && lane - 16 < n_cta) {
-                const long long *rv = cluster.map_shared_rank(s.votes, lane - 16);
-                v = rv[neg];
-            }
-            long long vl = v, vn = v;
-            if (lane >= 16) vl = 0; else vn = 0;
-            for (int o = 16; o; o >>= 1) {
-                vl += __shfl_xor_sync(0xffffffffu, vl, o);
-                vn += __shfl_xor_sync(0xffffffffu, vn, o);
-            }
-            if (lane == 0) decide(k, vl, vn, s.thr);
-        }
-        __syncthreads();
-        // 4. own update flags and their exclusive prefix (block-wide scan)
-        {
-            const uint64_t t_t = s.thr[0], t_n = s.thr[1];
-            int carry = 0;
-            for (int base = 0; base < cown; base += nthr) {
-                const int j = base + tid;
-                int f = 0;
-                if (j < cown) {
-                    const bool te = s.draw_t[j] < t_t, ne = s.draw_n[j] < t_n;
-                    f = (int)te + (int)ne;
-                    s.info[j] |= (te ? I_TEV : 0) | (ne ? I_NEV : 0);
-                }
-                int x = f;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                int *wsum = s.wsum;
-                if (lane == 31) wsum[warp] = x;
-                __syncthreads();
-                if (warp == 0) {
-                    int v = lane < (nthr >> 5) ? wsum[lane] : 0;
-                    for (int o = 1; o < 32; o <<= 1) {
-                        int y = __shfl_up_sync(0xffffffffu, v, o);
-                        if (lane >= o) v += y;
-                    }
-                    wsum[lane] = v;
-                }
-                __syncthreads();
-                const int excl = carry + (warp ? wsum[warp - 1] : 0) + x - f;
-                if (j < cown) s.lpref[j] = excl;
-                carry += wsum[(nthr >> 5) - 1];
-                __syncthreads();
-            }
-            if (tid == 0) s.lpref[cown] = carry;
-        }
-        cluster.sync();  // #2: event prefixes visible cluster-wide
-        // 5. CTA prefixes (events over clauses [0, cta_begin(r)))
-        if (warp == 0) {
-            int v = 0;
-            if (lane < n_cta) {
-                const int r_own = cta_begin(lane + 1, C, n_cta) - cta_begin(lane, C, n_cta);
-                const int *rp = cluster.map_shared_rank(s.lpref, lane);
-                v = rp[r_own];
-            }
-            int x = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            s.cta_pfx[lane] = x - v;  // exclusive
-        }
-        __syncthreads();
-        // Pfx(x): events over clauses [0, x) (x may belong to another CTA)
-        auto pfx = [&](int x) -> int {
-            if (x >= C) return s.cta_pfx[n_cta];  // total events of the cluster
-            if (x >= c0 && x < c1) return s.cta_pfx[rank] + s.lpref[x - c0];
-            const int r = cta_of(x, C, n_cta);
-            const int *rp = cluster.map_shared_rank(s.lpref, r);
-            return s.cta_pfx[r] + rp[x - cta_begin(r, C, n_cta)];
-        };
-        for (int bi = tid; bi <= b1 - b0; bi += nthr) {
-            s.blk_lo[bi] = pfx(block_begin(b0 + bi, C, k.n_blocks));
-            s.blk_hi[bi] = pfx(block_begin(b0 + bi + 1, C, k.n_blocks));
-        }
-        __syncthreads();
-        // 6. window ordinals, event types, weights, work list
-        for (int j = tid; j < cown; j += nthr) {
-            const int c = c0 + j;
-            const int inf = s.info[j];
-            const bool t_ev = inf & I_TEV, n_ev = inf & I_NEV;
-            uint64_t ord = 0;
-            if (t_ev || n_ev) {
-                const int bi = block_of(c, C, k.n_blocks) - b0;
-                ord = s.blk_ctr[bi] + (uint64_t)(s.cta_pfx[rank] + s.lpref[j] - s.blk_lo[bi]);
-            }
-            s.info[j] = inf & I_OUT;
-            clause_events(k, s, j, c, t_ev, n_ev, ord, label, neg, cn);
-        }
-        __syncthreads();
-        for (int bi = tid; bi <= b1 - b0; bi += nthr)
-            s.blk_ctr[bi] += (uint64_t)(s.blk_hi[bi] - s.blk_lo[bi]);
-        // 7. per-position Type I / II on the work list
-        feedback_quads<SMEM_STATES>(k, s, c0, lit, s.misc[0], cn);
-        __syncthreads();
-    }
-    cluster.sync();  // no CTA leaves while others may still read its DSMEM
-    store_slice<SMEM_STATES>(k, s, c0, cown);
-    for (int bi = tid; bi <= b1 - b0; bi += nthr) {
-        const int b = b0 + bi;
-        const int last = block_begin(b + 1, C, k.n_blocks) - 1;
-        if (last >= c0 && last < c1) k.block_counters[b] = s.blk_ctr[bi];
-    }
-    flush_stats(k, cn, rank == 0);
-    (void)K;
-}
-
-// =============================================================== GRID mode
-template <bool SMEM_STATES>
-__global__ void __launch_bounds__(512, 1) k_train_grid(TrainK k) {
-    extern __shared__ __align__(16) char smem_raw[];
-    Smem s;
-    smem_layout(k, SMEM_STATES, false, smem_raw, &s);
-    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int cta = blockIdx.x;
-    const int C = k.C, K = k.K;
-    const int c0 = cta_begin(cta, C, k.n_cta), c1 = cta_begin(cta + 1, C, k.n_cta);
     const int cown = c1 - c0;
     const int b0 = block_of(c0, C, k.n_blocks), b1 = block_of(c1 - 1, C, k.n_blocks);
     const int fs = block_begin(b0, C, k.n_blocks), fe = block_begin(b1 + 1, C, k.n_blocks);
     const int fsa = fs & ~31;
     const int nfw = (fe - fsa + 31) >> 5;
+    const bool pre = s.draw_t != nullptr;
 
     load_slice<SMEM_STATES>(k, s, c0, cown);
-    for (int i = tid; i <= b1 - b0; i += nthr) s.blk_ctr[i] = k.block_counters[b0 + i];
+    for (int i = tid; i <= b1 - b0; i += nthr) {
+        s.blk_ctr[i] = k.block_counters[b0 + i];
+        s.blk_seed[i] = k.block_seeds[b0 + i];
+    }
     prologue_ring(k, s);
     __syncthreads();
+    if (MODE == MODE_CLUSTER) cg::this_cluster().sync();  // DSMEM peers resident
 
     Counters cn;
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
@@ -576,51 +392,101 @@ __global__ void __launch_bounds__(512, 1) k_train_grid(TrainK k) {
         const uint32_t *lit = (i & 1) ? s.lit1 : s.lit0;
         const int ex = s.misc[3 + (int)(i % 3)];
         const int label = __ldg(&k.labels[ex]);
-        const int slot = (int)(i % 3);
         const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
-        eval_own(k, s, lit, cown);
-        if (tid == 0) s.misc[0] = 0;
         const int neg = negative_class(k, label, fbc);
-        __syncthreads();
-        partial_votes(k, s, cown);
-        __syncthreads();
-        // arrive: K relaxed atomics then a release increment (one thread)
-        if (tid == 0) {
-            for (int kk = 0; kk < K; ++kk)
-                if (s.votes[kk]) atomicAdd(&k.ring[slot * K + kk], (unsigned long long)s.votes[kk]);
-            red_release_add(k.bar, 1u);
+        // 1. training-mode outputs of own clauses (kernels/_numba.py:36-50)
+        for (int j = warp; j < cown; j += nwarps) {
+            uint32_t viol = 0;
+            for (int w = lane; w < k.W; w += 32) viol |= s.masks[j * k.W + w] & ~lit[w];
+            viol = __reduce_or_sync(0xffffffffu, viol);
+            if (lane == 0) s.info[j] = (viol == 0 && s.cnt[j] <= k.budget) ? I_OUT : 0;
         }
-        // while the barrier is pending: update-flag draws for [fs, fe)
-        for (int idx = tid; idx < nfw * 32; idx += nthr) {
-            const int j = fsa + idx;
-            s.draw_t[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
-            s.draw_n[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
+        if (tid == 0) s.misc[0] = 0;
+        __syncthreads();
+        // 2. partial class sums (dense.py:153), warp per class, then all-reduce
+        const int buf = (int)(i & 1);
+        for (int kk = warp; kk < K; kk += nwarps) {
+            long long v = 0;
+            for (int j = lane; j < cown; j += 32)
+                if (s.info[j] & I_OUT) v += s.weights[j * K + kk];
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (MODE == MODE_CLUSTER) {
+                // push into every CTA's inbox (DSMEM stores, no round trip)
+                if (lane < n_cta) {
+                    long long *dst = cg::this_cluster().map_shared_rank(s.vin, lane);
+                    dst[(buf * 16 + rank) * K + kk] = v;
+                }
+            } else if (lane == 0 && v) {
+                atomicAdd(&k.ring[(int)(i % 3) * K + kk], (unsigned long long)v);
+            }
+        }
+        if (MODE == MODE_CLUSTER) {
+            cluster_arrive();
+        } else {
+            __syncthreads();
+            if (tid == 0) red_release_add(k.bar, 1u);
+        }
+        // while the all-reduce is pending: update-flag draws for [fs, fe)
+        // (feedback.py:47-53; independent of the votes) and the next example
+        if (pre) {
+            for (int idx = tid; idx < nfw * 32; idx += nthr) {
+                const int j = fsa + idx;
+                s.draw_t[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
+                s.draw_n[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
+            }
         }
         prefetch(k, s, i);
-        if (tid == 0) {
-            const unsigned target = (unsigned)((i + 1) * k.n_cta);
-            while ((int)(ld_acquire_u32(k.bar) - target) < 0) {
+        uint64_t t_t, t_n;
+        if (MODE == MODE_CLUSTER) {
+            cluster_wait();
+            // every warp sums the inbox itself: no CTA-wide broadcast needed
+            long long v = 0;
+            if (lane < n_cta) v = s.vin[(buf * 16 + lane) * K + label];
+            else if (lane >= 16 && lane - 16 < n_cta) v = s.vin[(buf * 16 + lane - 16) * K + neg];
+            long long vl = lane < 16 ? v : 0, vn = lane < 16 ? 0 : v;
+            for (int o = 16; o; o >>= 1) {
+                vl += __shfl_xor_sync(0xffffffffu, vl, o);
+                vn += __shfl_xor_sync(0xffffffffu, vn, o);
             }
-            const long long vl = (long long)__ldcg(&k.ring[slot * K + label]);
-            const long long vn = (long long)__ldcg(&k.ring[slot * K + neg]);
-            decide(k, vl, vn, s.thr);
-            // slot (i+2)%3 == (i-1)%3: every CTA read it before arriving here
-            if (cta == 0)
-                for (int kk = 0; kk < K; ++kk) k.ring[((i + 2) % 3) * K + kk] = 0ull;
+            decide(k, vl, vn, t_t, t_n);
+        } else {
+            if (tid == 0) {
+                const unsigned target = (unsigned)((i + 1) * n_cta);
+                while ((int)(ld_acquire_u32(k.bar) - target) < 0) {
+                }
+                const int slot = (int)(i % 3);
+                const long long vl = (long long)__ldcg(&k.ring[slot * K + label]);
+                const long long vn = (long long)__ldcg(&k.ring[slot * K + neg]);
+                decide(k, vl, vn, s.thr[0], s.thr[1]);
+                // slot (i+2)%3 == (i-1)%3: every CTA read it before arriving
+                if (rank == 0)
+                    for (int kk = 0; kk < K; ++kk) k.ring[((i + 2) % 3) * K + kk] = 0ull;
+            }
+            __syncthreads();
+            t_t = s.thr[0];
+            t_n = s.thr[1];
         }
-        __syncthreads();
-        const uint64_t t_t = s.thr[0], t_n = s.thr[1];
+        // 3. update flags over [fs, fe) as bitmaps
         for (int idx = tid; idx < nfw * 32; idx += nthr) {
             const int j = fsa + idx;
             const bool valid = j >= fs && j < fe;
-            const unsigned wt = __ballot_sync(0xffffffffu, valid && s.draw_t[idx] < t_t);
-            const unsigned wn = __ballot_sync(0xffffffffu, valid && s.draw_n[idx] < t_n);
+            uint64_t mt, mn;
+            if (pre) {
+                mt = s.draw_t[idx];
+                mn = s.draw_n[idx];
+            } else {
+                mt = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
+                mn = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
+            }
+            const unsigned wt = __ballot_sync(0xffffffffu, valid && mt < t_t);
+            const unsigned wn = __ballot_sync(0xffffffffu, valid && mn < t_n);
             if (lane == 0) {
                 s.ut_bits[idx >> 5] = wt;
                 s.un_bits[idx >> 5] = wn;
             }
         }
         __syncthreads();
+        // 4. exclusive prefix of events per flag word
         if (warp == 0) {
             int carry = 0;
             for (int base = 0; base < nfw; base += 32) {
@@ -629,7 +495,7 @@ __global__ void __launch_bounds__(512, 1) k_train_grid(TrainK k) {
                 int x = v;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(0xffffffffu, x, o);
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
                     if (lane >= o) x += y;
                 }
                 if (w < nfw) s.word_cum[w] = carry + x - v;
@@ -647,18 +513,46 @@ __global__ void __launch_bounds__(512, 1) k_train_grid(TrainK k) {
             }
             return v;
         };
+        // 5. window ordinals, event types, weights (feedback then weight,
+        //    SPEC.md:171), work list
         for (int j = tid; j < cown; j += nthr) {
             const int c = c0 + j;
             const int q = (c - fsa) >> 5, r = (c - fsa) & 31;
             const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
-            uint64_t ord = 0;
+            int info = s.info[j] & I_OUT;
             if (t_ev || n_ev) {
-                const int b = block_of(c, C, k.n_blocks);
-                ord = s.blk_ctr[b - b0] + (uint64_t)(cum(c) - cum(block_begin(b, C, k.n_blocks)));
+                const int bi = block_of(c, C, k.n_blocks) - b0;
+                const uint64_t ord =
+                    s.blk_ctr[bi] + (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
+                const uint64_t bseed = s.blk_seed[bi];
+                const bool out = info & I_OUT;
+                int32_t *w = s.weights + j * K;
+                const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
+                if (t_ev) {
+                    info |= I_TEV | (t1 ? I_T1 : 0);
+                    s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
+                    ++cn.events;
+                    if (t1) ++cn.t1; else if (out) ++cn.t2;
+                }
+                if (n_ev) {
+                    const uint64_t o2 = ord + (t_ev ? 1 : 0);
+                    info |= I_NEV | (n1 ? I_N1 : 0);
+                    s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
+                    ++cn.events;
+                    if (n1) ++cn.t1; else if (out) ++cn.t2;
+                }
+                if (out) {
+                    if (t_ev) w[label] += 1;
+                    if (n_ev) w[neg] -= 1;
+                }
+                if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
+                    s.work[atomicAdd(&s.misc[0], 1)] = j;
             }
-            clause_events(k, s, j, c, t_ev, n_ev, ord, label, neg, cn);
+            s.info[j] = info;
         }
         __syncthreads();
+        // 6. block counters (one window per applied event) and the per-position
+        //    Type I / II updates
         for (int bi = tid; bi <= b1 - b0; bi += nthr) {
             const int bs = block_begin(b0 + bi, C, k.n_blocks);
             const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
@@ -667,13 +561,14 @@ __global__ void __launch_bounds__(512, 1) k_train_grid(TrainK k) {
         feedback_quads<SMEM_STATES>(k, s, c0, lit, s.misc[0], cn);
         __syncthreads();
     }
+    if (MODE == MODE_CLUSTER) cg::this_cluster().sync();  // peers done with our inbox
     store_slice<SMEM_STATES>(k, s, c0, cown);
     for (int bi = tid; bi <= b1 - b0; bi += nthr) {
         const int b = b0 + bi;
         const int last = block_begin(b + 1, C, k.n_blocks) - 1;
         if (last >= c0 && last < c1) k.block_counters[b] = s.blk_ctr[bi];
     }
-    flush_stats(k, cn, cta == 0);
+    flush_stats(k, cn, rank == 0);
 }
 
 }  // namespace tmb
@@ -709,8 +604,10 @@ void per_cta_maxima(TrainK &k) {
 }
 
 const void *kernel_for(bool cluster, bool smem_states) {
-    if (cluster) return smem_states ? (const void *)k_train_cluster<true> : (const void *)k_train_cluster<false>;
-    return smem_states ? (const void *)k_train_grid<true> : (const void *)k_train_grid<false>;
+    if (cluster)
+        return smem_states ? (const void *)k_train<MODE_CLUSTER, true>
+                           : (const void *)k_train<MODE_CLUSTER, false>;
+    return smem_states ? (const void *)k_train<MODE_GRID, true> : (const void *)k_train<MODE_GRID, false>;
 }
 
 }  // namespace
@@ -756,8 +653,8 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     cudaGetDevice(&dev);
     int max_smem = 0;
     TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    const size_t need_on = smem_layout(k, true, cluster, nullptr, nullptr);
-    const size_t need_off = smem_layout(k, false, cluster, nullptr, nullptr);
+    const size_t need_on = smem_layout(k, true, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
+    const size_t need_off = smem_layout(k, false, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
     // flags bit 0 forces HBM-resident states (tests the streaming path)
     const int smem_states = (need_on <= (size_t)max_smem && !(c.flags & 1)) ? 1 : 0;
     const size_t need = smem_states ? need_on : need_off;
