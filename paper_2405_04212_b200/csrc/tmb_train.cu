@@ -48,8 +48,7 @@ struct TrainK {
     int32_t *weights;
     uint64_t *block_counters;
     const uint64_t *block_seeds;
-    unsigned long long *ring;  // [3][K] (grid mode)
-    unsigned int *bar;
+    unsigned long long *rec;   // grid mode: [2][n_cta][2] self-tagged vote records
     tmb_train_stats *stats;
 };
 
@@ -97,8 +96,9 @@ struct Smem {
     int32_t *word_cum, *weights, *work, *info, *cnt;
     uint64_t *sk_t, *sk_n, *blk_ctr, *blk_seed, *draw_t, *draw_n;
     int8_t *states;
-    long long *vin;    // cluster: [2][16][K] vote inbox (pushed by every CTA)
-    int *misc;         // [0]=n_work [3..5]=example ring
+    long long *vin;    // cluster: [2][16][2] (label, negative) vote inbox
+    long long *vsum;   // grid: [2] summed votes
+    int *misc;         // [0]=n_work [3..5]=example ring [8..10]=label ring
     uint64_t *thr;     // grid: [0]=t_t [1]=t_n [2]=negative
 };
 
@@ -118,7 +118,8 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.blk_ctr = (uint64_t *)take(8 * (k.bmax + 1));
     t.blk_seed = (uint64_t *)take(8 * (k.bmax + 1));
     t.thr = (uint64_t *)take(8 * 4);
-    t.vin = mode == MODE_CLUSTER ? (long long *)take(8 * 2 * 16 * k.K) : nullptr;
+    t.vin = mode == MODE_CLUSTER ? (long long *)take(8 * 2 * 16 * 2) : nullptr;
+    t.vsum = (long long *)take(8 * 2);
     t.lit0 = (uint32_t *)take(4 * k.W);
     t.lit1 = (uint32_t *)take(4 * k.W);
     t.masks = (uint32_t *)take(4 * (size_t)k.cmax * k.W);
@@ -126,7 +127,7 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.work = (int32_t *)take(4 * k.cmax);
     t.info = (int32_t *)take(4 * k.cmax);
     t.cnt = (int32_t *)take(4 * k.cmax);
-    t.misc = (int *)take(4 * 8);
+    t.misc = (int *)take(4 * 16);
     t.ut_bits = (uint32_t *)take(4 * k.fmax_words);
     t.un_bits = (uint32_t *)take(4 * k.fmax_words);
     t.word_cum = (int32_t *)take(4 * (k.fmax_words + 1));
@@ -313,9 +314,12 @@ __device__ __forceinline__ void flush_stats(const TrainK &k, Counters &cn, bool 
 // row of example i lives in lit{i&1}.  Issued one / two examples ahead so
 // the dependent global loads overlap the current example.
 __device__ __forceinline__ void prefetch(const TrainK &k, const Smem &s, int64_t i) {
-    if (threadIdx.x == 0 && i + 2 < k.n_steps) s.misc[3 + (int)((i + 2) % 3)] = __ldg(&k.order[i + 2]);
     if (i + 1 < k.n_steps) {
         const int ex = s.misc[3 + (int)((i + 1) % 3)];
+        if (threadIdx.x == blockDim.x - 1) {  // not warp 0: it polls the votes
+            s.misc[8 + (int)((i + 1) % 3)] = __ldg(&k.labels[ex]);
+            if (i + 2 < k.n_steps) s.misc[3 + (int)((i + 2) % 3)] = __ldg(&k.order[i + 2]);
+        }
         uint32_t *dst = ((i + 1) & 1) ? s.lit1 : s.lit0;
         for (int w = threadIdx.x; w < k.W; w += blockDim.x)
             dst[w] = __ldg(&k.lit_words[(int64_t)ex * k.W + w]);
@@ -325,6 +329,7 @@ __device__ __forceinline__ void prefetch(const TrainK &k, const Smem &s, int64_t
 __device__ __forceinline__ void prologue_ring(const TrainK &k, const Smem &s) {
     if (threadIdx.x == 0) {
         s.misc[3] = __ldg(&k.order[0]);
+        s.misc[8] = __ldg(&k.labels[s.misc[3]]);
         if (k.n_steps > 1) s.misc[4] = __ldg(&k.order[1]);
     }
     __syncthreads();
@@ -390,8 +395,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
     for (int64_t i = 0; i < k.n_steps; ++i) {
         const uint32_t *lit = (i & 1) ? s.lit1 : s.lit0;
-        const int ex = s.misc[3 + (int)(i % 3)];
-        const int label = __ldg(&k.labels[ex]);
+        const int label = s.misc[8 + (int)(i % 3)];
         const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
         const int neg = negative_class(k, label, fbc);
         // 1. training-mode outputs of own clauses (kernels/_numba.py:36-50)
@@ -403,9 +407,12 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         }
         if (tid == 0) s.misc[0] = 0;
         __syncthreads();
-        // 2. partial class sums (dense.py:153), warp per class, then all-reduce
+        // 2. partial class sums of the two classes the decision reads
+        //    (dense.py:153 restricted to label / negative), then all-reduce
         const int buf = (int)(i & 1);
-        for (int kk = warp; kk < K; kk += nwarps) {
+        const unsigned tag = (unsigned)(i % 65535) + 1u;
+        if (warp < 2) {
+            const int kk = warp == 0 ? label : neg;
             long long v = 0;
             for (int j = lane; j < cown; j += 32)
                 if (s.info[j] & I_OUT) v += s.weights[j * K + kk];
@@ -414,18 +421,16 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 // push into every CTA's inbox (DSMEM stores, no round trip)
                 if (lane < n_cta) {
                     long long *dst = cg::this_cluster().map_shared_rank(s.vin, lane);
-                    dst[(buf * 16 + rank) * K + kk] = v;
+                    dst[(buf * 16 + rank) * 2 + warp] = v;
                 }
-            } else if (lane == 0 && v) {
-                atomicAdd(&k.ring[(int)(i % 3) * K + kk], (unsigned long long)v);
+            } else if (lane == 0) {
+                // self-tagged record: 16-bit example tag | 48-bit signed partial
+                const unsigned long long r =
+                    ((unsigned long long)tag << 48) | ((unsigned long long)v & 0xFFFFFFFFFFFFull);
+                __stcg(&k.rec[((size_t)buf * n_cta + rank) * 2 + warp], r);
             }
         }
-        if (MODE == MODE_CLUSTER) {
-            cluster_arrive();
-        } else {
-            __syncthreads();
-            if (tid == 0) red_release_add(k.bar, 1u);
-        }
+        if (MODE == MODE_CLUSTER) cluster_arrive();
         // while the all-reduce is pending: update-flag draws for [fs, fe)
         // (feedback.py:47-53; independent of the votes) and the next example
         if (pre) {
@@ -441,8 +446,8 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             cluster_wait();
             // every warp sums the inbox itself: no CTA-wide broadcast needed
             long long v = 0;
-            if (lane < n_cta) v = s.vin[(buf * 16 + lane) * K + label];
-            else if (lane >= 16 && lane - 16 < n_cta) v = s.vin[(buf * 16 + lane - 16) * K + neg];
+            if (lane < n_cta) v = s.vin[(buf * 16 + lane) * 2 + 0];
+            else if (lane >= 16 && lane - 16 < n_cta) v = s.vin[(buf * 16 + lane - 16) * 2 + 1];
             long long vl = lane < 16 ? v : 0, vn = lane < 16 ? 0 : v;
             for (int o = 16; o; o >>= 1) {
                 vl += __shfl_xor_sync(0xffffffffu, vl, o);
@@ -450,21 +455,31 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
             decide(k, vl, vn, t_t, t_n);
         } else {
-            if (tid == 0) {
-                const unsigned target = (unsigned)((i + 1) * n_cta);
-                while ((int)(ld_acquire_u32(k.bar) - target) < 0) {
+            // the records are the barrier: warp 0 polls every CTA's pair until
+            // all carry this example's tag (no counter, no second round trip)
+            if (warp == 0) {
+                long long vl = 0, vn = 0;
+                for (int r = lane; r < n_cta; r += 32) {
+                    const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(
+                        k.rec + ((size_t)buf * n_cta + r) * 2);
+                    ulonglong2 p;
+                    do {
+                        p = __ldcg(src);
+                    } while ((unsigned)(p.x >> 48) != tag || (unsigned)(p.y >> 48) != tag);
+                    vl += (long long)(p.x << 16) >> 16;
+                    vn += (long long)(p.y << 16) >> 16;
                 }
-                const int slot = (int)(i % 3);
-                const long long vl = (long long)__ldcg(&k.ring[slot * K + label]);
-                const long long vn = (long long)__ldcg(&k.ring[slot * K + neg]);
-                decide(k, vl, vn, s.thr[0], s.thr[1]);
-                // slot (i+2)%3 == (i-1)%3: every CTA read it before arriving
-                if (rank == 0)
-                    for (int kk = 0; kk < K; ++kk) k.ring[((i + 2) % 3) * K + kk] = 0ull;
+                for (int o = 16; o; o >>= 1) {
+                    vl += __shfl_xor_sync(0xffffffffu, vl, o);
+                    vn += __shfl_xor_sync(0xffffffffu, vn, o);
+                }
+                if (lane == 0) {
+                    s.vsum[0] = vl;
+                    s.vsum[1] = vn;
+                }
             }
             __syncthreads();
-            t_t = s.thr[0];
-            t_n = s.thr[1];
+            decide(k, s.vsum[0], s.vsum[1], t_t, t_n);
         }
         // 3. update flags over [fs, fe) as bitmaps
         for (int idx = tid; idx < nfw * 32; idx += nthr) {
@@ -486,7 +501,9 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
         }
         __syncthreads();
-        // 4. exclusive prefix of events per flag word
+        // 4-5. warp 0: exclusive prefix of events per flag word, then window
+        //      ordinals, event types, weights (feedback then weight,
+        //      SPEC.md:171) and the work list of the own clauses
         if (warp == 0) {
             int carry = 0;
             for (int base = 0; base < nfw; base += 32) {
@@ -502,62 +519,61 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
             if (lane == 0) s.word_cum[nfw] = carry;
+            __syncwarp();
+            auto cum = [&](int x) -> int {  // events over clauses [fsa, x)
+                const int q = (x - fsa) >> 5, r = (x - fsa) & 31;
+                int v = s.word_cum[q];
+                if (r) {
+                    const unsigned lo = (1u << r) - 1u;
+                    v += __popc(s.ut_bits[q] & lo) + __popc(s.un_bits[q] & lo);
+                }
+                return v;
+            };
+            for (int j = lane; j < cown; j += 32) {
+                const int c = c0 + j;
+                const int q = (c - fsa) >> 5, r = (c - fsa) & 31;
+                const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
+                int info = s.info[j] & I_OUT;
+                if (t_ev || n_ev) {
+                    const int bi = block_of(c, C, k.n_blocks) - b0;
+                    const uint64_t ord = s.blk_ctr[bi] +
+                        (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
+                    const uint64_t bseed = s.blk_seed[bi];
+                    const bool out = info & I_OUT;
+                    int32_t *w = s.weights + j * K;
+                    const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
+                    if (t_ev) {
+                        info |= I_TEV | (t1 ? I_T1 : 0);
+                        s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
+                        ++cn.events;
+                        if (t1) ++cn.t1; else if (out) ++cn.t2;
+                    }
+                    if (n_ev) {
+                        const uint64_t o2 = ord + (t_ev ? 1 : 0);
+                        info |= I_NEV | (n1 ? I_N1 : 0);
+                        s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
+                        ++cn.events;
+                        if (n1) ++cn.t1; else if (out) ++cn.t2;
+                    }
+                    if (out) {
+                        if (t_ev) w[label] += 1;
+                        if (n_ev) w[neg] -= 1;
+                    }
+                    if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
+                        s.work[atomicAdd(&s.misc[0], 1)] = j;
+                }
+                s.info[j] = info;
+            }
+            __syncwarp();
+            // one window per applied event (block counters)
+            for (int bi = lane; bi <= b1 - b0; bi += 32) {
+                const int bs = block_begin(b0 + bi, C, k.n_blocks);
+                const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
+                s.blk_ctr[bi] += (uint64_t)(cum(be) - cum(bs));
+            }
         }
         __syncthreads();
-        auto cum = [&](int x) -> int {  // events over clauses [fsa, x)
-            const int q = (x - fsa) >> 5, r = (x - fsa) & 31;
-            int v = s.word_cum[q];
-            if (r) {
-                const unsigned lo = (1u << r) - 1u;
-                v += __popc(s.ut_bits[q] & lo) + __popc(s.un_bits[q] & lo);
-            }
-            return v;
-        };
-        // 5. window ordinals, event types, weights (feedback then weight,
-        //    SPEC.md:171), work list
-        for (int j = tid; j < cown; j += nthr) {
-            const int c = c0 + j;
-            const int q = (c - fsa) >> 5, r = (c - fsa) & 31;
-            const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
-            int info = s.info[j] & I_OUT;
-            if (t_ev || n_ev) {
-                const int bi = block_of(c, C, k.n_blocks) - b0;
-                const uint64_t ord =
-                    s.blk_ctr[bi] + (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
-                const uint64_t bseed = s.blk_seed[bi];
-                const bool out = info & I_OUT;
-                int32_t *w = s.weights + j * K;
-                const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
-                if (t_ev) {
-                    info |= I_TEV | (t1 ? I_T1 : 0);
-                    s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
-                    ++cn.events;
-                    if (t1) ++cn.t1; else if (out) ++cn.t2;
-                }
-                if (n_ev) {
-                    const uint64_t o2 = ord + (t_ev ? 1 : 0);
-                    info |= I_NEV | (n1 ? I_N1 : 0);
-                    s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
-                    ++cn.events;
-                    if (n1) ++cn.t1; else if (out) ++cn.t2;
-                }
-                if (out) {
-                    if (t_ev) w[label] += 1;
-                    if (n_ev) w[neg] -= 1;
-                }
-                if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
-                    s.work[atomicAdd(&s.misc[0], 1)] = j;
-            }
-            s.info[j] = info;
-        }
-        __syncthreads();
-        // 6. block counters (one window per applied event) and the per-position
-        //    Type I / II updates
-        for (int bi = tid; bi <= b1 - b0; bi += nthr) {
-            const int bs = block_begin(b0 + bi, C, k.n_blocks);
-            const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
-            s.blk_ctr[bi] += (uint64_t)(cum(be) - cum(bs));
-        }
+        // 6. per-position Type I / II updates of the work list
         feedback_quads<SMEM_STATES>(k, s, c0, lit, s.misc[0], cn);
         __syncthreads();
     }
@@ -583,7 +599,7 @@ struct tmb_trainer {
     int n_cta, threads, smem, smem_states, cluster;
     TrainK k;
     uint64_t *block_seeds_d = nullptr;
-    unsigned long long *ring_d = nullptr;  // ring [3K] + barrier word
+    unsigned long long *ring_d = nullptr;  // grid-mode vote records [2][n_cta][2]
 };
 
 namespace {
@@ -698,15 +714,14 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     std::vector<uint64_t> seeds(c.n_blocks);
     for (int64_t b = 0; b < c.n_blocks; ++b) seeds[b] = derive_stream(c.seed, (uint64_t)b);
     if ((rc = check_cuda(cudaMalloc(&t->block_seeds_d, 8 * c.n_blocks), "cudaMalloc")) ||
-        (rc = check_cuda(cudaMalloc(&t->ring_d, 8 * (3 * K + 2)), "cudaMalloc")) ||
+        (rc = check_cuda(cudaMalloc(&t->ring_d, 8 * (size_t)(2 * 2 * n_cta)), "cudaMalloc")) ||
         (rc = check_cuda(cudaMemcpy(t->block_seeds_d, seeds.data(), 8 * c.n_blocks,
                                     cudaMemcpyHostToDevice), "cudaMemcpy"))) {
         tmb_trainer_destroy(t);
         return rc;
     }
     k.block_seeds = t->block_seeds_d;
-    k.ring = t->ring_d;
-    k.bar = reinterpret_cast<unsigned *>(t->ring_d + 3 * K);
+    k.rec = t->ring_d;
     k.states = states; k.weights = weights; k.block_counters = block_counters;
     t->k = k;
     *out = t;
@@ -760,7 +775,7 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         lc.numAttrs = 1;
         TMB_CUDA(cudaLaunchKernelExC(&lc, fn, args));
     } else {
-        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 8 * (3 * k.K + 2), st));
+        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 8 * (size_t)(2 * 2 * t->n_cta), st));
         TMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(t->n_cta), dim3(t->threads), args,
                                              (size_t)t->smem, st));
     }
