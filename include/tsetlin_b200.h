@@ -158,6 +158,12 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
                        uint64_t *block_counters, int n_cta, int threads,
                        tmb_trainer **out);
 int tmb_trainer_destroy(tmb_trainer *t);
+/* Per-example trace for tests / debugging (the device analogue of the
+ * reference's observer hook, executor.py:276): when non-NULL, every
+ * tmb_trainer_run writes trace[i*4 + {0,1,2,3}] = negative class, summed
+ * votes of the label, of the negative class, and applied events (the last
+ * only when n_blocks == 1) for its example i.  Device int64 [n_steps*4]. */
+int tmb_trainer_set_trace(tmb_trainer *t, int64_t *trace);
 /* Launch configuration actually used (for reporting). */
 int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_bytes,
                      int *states_in_smem);

@@ -50,6 +50,7 @@ struct TrainK {
     const uint64_t *block_seeds;
     unsigned long long *rec;   // grid mode: [2][n_cta][2] self-tagged vote records
     tmb_train_stats *stats;
+    long long *trace;  // optional [n_steps][4]: negative, votes[label], votes[neg], events
 };
 
 // executor.py:36-47 partition: block of clause c and block start.
@@ -454,6 +455,11 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 vn += __shfl_xor_sync(0xffffffffu, vn, o);
             }
             decide(k, vl, vn, t_t, t_n);
+            if (k.trace && rank == 0 && tid == 0) {
+                k.trace[i * 4 + 0] = neg;
+                k.trace[i * 4 + 1] = vl;
+                k.trace[i * 4 + 2] = vn;
+            }
         } else {
             // the records are the barrier: warp 0 polls every CTA's pair until
             // all carry this example's tag (no counter, no second round trip)
@@ -480,6 +486,11 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
             __syncthreads();
             decide(k, s.vsum[0], s.vsum[1], t_t, t_n);
+            if (k.trace && rank == 0 && tid == 0) {
+                k.trace[i * 4 + 0] = neg;
+                k.trace[i * 4 + 1] = s.vsum[0];
+                k.trace[i * 4 + 2] = s.vsum[1];
+            }
         }
         // 3. update flags over [fs, fe) as bitmaps
         for (int idx = tid; idx < nfw * 32; idx += nthr) {
@@ -518,7 +529,10 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 if (w < nfw) s.word_cum[w] = carry + x - v;
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
-            if (lane == 0) s.word_cum[nfw] = carry;
+            if (lane == 0) {
+                s.word_cum[nfw] = carry;
+                if (k.trace && rank == 0 && fs == 0 && fe == C) k.trace[i * 4 + 3] = carry;
+            }
             __syncwarp();
             auto cum = [&](int x) -> int {  // events over clauses [fsa, x)
                 const int q = (x - fsa) >> 5, r = (x - fsa) & 31;
@@ -725,6 +739,12 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     k.states = states; k.weights = weights; k.block_counters = block_counters;
     t->k = k;
     *out = t;
+    return TMB_OK;
+}
+
+int tmb_trainer_set_trace(tmb_trainer *t, int64_t *trace) {
+    if (!t) return fail(TMB_E_INVALID, "trainer_set_trace: NULL trainer");
+    t->k.trace = reinterpret_cast<long long *>(trace);
     return TMB_OK;
 }
 
