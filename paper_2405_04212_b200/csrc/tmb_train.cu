@@ -42,6 +42,7 @@ struct TrainK {
     FbParams fp;
     uint64_t fb_seed, fb_counter0;
     int64_t n_steps;
+    uint64_t tag_base;  // launch-unique offset of the vote-record tags
     const uint32_t *lit_words;
     const int32_t *labels, *order;
     int8_t *states;
@@ -81,6 +82,18 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
 }
 __device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Strong (morally strong, gpu scope) accesses for the vote records.  Weak
+// loads (ld.global.cg) may be served from the other L2 partition's stale
+// copy of the line and never observe the update.
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_relaxed_v2u64(const unsigned long long *p) {
+    ulonglong2 r;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
+    return r;
 }
 
 
@@ -411,7 +424,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         // 2. partial class sums of the two classes the decision reads
         //    (dense.py:153 restricted to label / negative), then all-reduce
         const int buf = (int)(i & 1);
-        const unsigned tag = (unsigned)(i % 65535) + 1u;
+        const unsigned tag = (unsigned)((k.tag_base + (uint64_t)i) % 65535u) + 1u;
         if (warp < 2) {
             const int kk = warp == 0 ? label : neg;
             long long v = 0;
@@ -428,7 +441,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 // self-tagged record: 16-bit example tag | 48-bit signed partial
                 const unsigned long long r =
                     ((unsigned long long)tag << 48) | ((unsigned long long)v & 0xFFFFFFFFFFFFull);
-                __stcg(&k.rec[((size_t)buf * n_cta + rank) * 2 + warp], r);
+                st_relaxed_u64(&k.rec[((size_t)buf * n_cta + rank) * 2 + warp], r);
             }
         }
         if (MODE == MODE_CLUSTER) cluster_arrive();
@@ -466,11 +479,10 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             if (warp == 0) {
                 long long vl = 0, vn = 0;
                 for (int r = lane; r < n_cta; r += 32) {
-                    const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(
-                        k.rec + ((size_t)buf * n_cta + r) * 2);
+                    const unsigned long long *src = k.rec + ((size_t)buf * n_cta + r) * 2;
                     ulonglong2 p;
                     do {
-                        p = __ldcg(src);
+                        p = ld_relaxed_v2u64(src);
                     } while ((unsigned)(p.x >> 48) != tag || (unsigned)(p.y >> 48) != tag);
                     vl += (long long)(p.x << 16) >> 16;
                     vn += (long long)(p.y << 16) >> 16;
@@ -486,6 +498,10 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
             __syncthreads();
             decide(k, s.vsum[0], s.vsum[1], t_t, t_n);
+            if (k.trace && tid == 0 && k.n_steps == 1) {
+                k.trace[4 + rank * 2 + 0] = s.vsum[0];
+                k.trace[4 + rank * 2 + 1] = s.vsum[1];
+            }
             if (k.trace && rank == 0 && tid == 0) {
                 k.trace[i * 4 + 0] = neg;
                 k.trace[i * 4 + 1] = s.vsum[0];
@@ -611,6 +627,7 @@ struct tmb_trainer {
     int32_t *weights;
     uint64_t *block_counters;
     int n_cta, threads, smem, smem_states, cluster;
+    uint64_t launches = 0;
     TrainK k;
     uint64_t *block_seeds_d = nullptr;
     unsigned long long *ring_d = nullptr;  // grid-mode vote records [2][n_cta][2]
@@ -778,6 +795,8 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     TrainK k = t->k;
     k.lit_words = lit_words; k.labels = labels; k.order = order;
     k.n_steps = n_steps; k.fb_counter0 = fb_counter; k.stats = stats;
+    k.tag_base = t->launches;
+    t->launches += (uint64_t)n_steps + 7;
     void *args[] = {&k};
     const void *fn = kernel_for(t->cluster, t->smem_states);
     if (t->cluster) {
