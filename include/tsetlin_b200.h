@@ -164,6 +164,12 @@ int tmb_trainer_destroy(tmb_trainer *t);
  * votes of the label, of the negative class, and applied events (the last
  * only when n_blocks == 1) for its example i.  Device int64 [n_steps*4]. */
 int tmb_trainer_set_trace(tmb_trainer *t, int64_t *trace);
+/* Phase profiling: when non-NULL, every launch writes, per CTA, the clock64
+ * cycles thread 0 spent in each of 8 kernel phases (device uint64
+ * [n_cta * 8]): eval, partial votes + arrive, flag-draw precompute +
+ * prefetch, all-reduce wait + decision, flag bitmaps, scan + events,
+ * per-position feedback. */
+int tmb_trainer_set_profile(tmb_trainer *t, uint64_t *phase);
 /* Launch configuration actually used (for reporting). */
 int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_bytes,
                      int *states_in_smem);

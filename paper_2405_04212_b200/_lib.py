@@ -74,6 +74,7 @@ SIGNATURES = {
     "tmb_trainer_create": (i32, [vp, vp, vp, vp, i32, i32, vp]),
     "tmb_trainer_destroy": (i32, [vp]),
     "tmb_trainer_set_trace": (i32, [vp, vp]),
+    "tmb_trainer_set_profile": (i32, [vp, vp]),
     "tmb_trainer_info": (i32, [vp, vp, vp, vp, vp]),
     "tmb_trainer_run": (i32, [vp, vp, vp, vp, i64, u64, vp, vp]),
     "tmb_rules_from_bank": (i32, [vp, vp, i64, i64, i64, i64, i32, vp, vp]),

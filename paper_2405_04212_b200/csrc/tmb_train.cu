@@ -49,7 +49,9 @@ struct TrainK {
     int32_t *weights;
     uint64_t *block_counters;
     const uint64_t *block_seeds;
-    unsigned long long *rec;   // grid mode: [2][n_cta][2] self-tagged vote records
+    unsigned long long *rec;   // grid mode: [3][2] summed (label, negative) votes
+    unsigned int *bar;         // grid mode: arrival counter
+    unsigned long long *phase;  // optional [n_cta][8] clock64 per phase (profiling)
     tmb_train_stats *stats;
     long long *trace;  // optional [n_steps][4]: negative, votes[label], votes[neg], events
 };
@@ -88,6 +90,19 @@ __device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
 // copy of the line and never observe the update.
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acquire() {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ ulonglong2 ld_relaxed_v2u64(const unsigned long long *p) {
     ulonglong2 r;
@@ -376,6 +391,17 @@ __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Phase profiling (k.phase != nullptr): thread 0 of every CTA accumulates
+// clock64 deltas between consecutive PHASE marks.
+#define PHASE(n)                                                          \
+    do {                                                                  \
+        if (prof && tid == 0) {                                           \
+            const long long now = clock64();                              \
+            ph[n] += (unsigned long long)(now - t_mark);                  \
+            t_mark = now;                                                 \
+        }                                                                 \
+    } while (0)
+
 // One fused kernel, two synchronisation domains (see the header comment).
 template <int MODE, bool SMEM_STATES>
 __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
@@ -406,6 +432,9 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
     if (MODE == MODE_CLUSTER) cg::this_cluster().sync();  // DSMEM peers resident
 
     Counters cn;
+    const bool prof = k.phase != nullptr;
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long t_mark = clock64();
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
     for (int64_t i = 0; i < k.n_steps; ++i) {
         const uint32_t *lit = (i & 1) ? s.lit1 : s.lit0;
@@ -421,10 +450,10 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         }
         if (tid == 0) s.misc[0] = 0;
         __syncthreads();
+        PHASE(0);
         // 2. partial class sums of the two classes the decision reads
         //    (dense.py:153 restricted to label / negative), then all-reduce
         const int buf = (int)(i & 1);
-        const unsigned tag = (unsigned)((k.tag_base + (uint64_t)i) % 65535u) + 1u;
         if (warp < 2) {
             const int kk = warp == 0 ? label : neg;
             long long v = 0;
@@ -437,14 +466,17 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                     long long *dst = cg::this_cluster().map_shared_rank(s.vin, lane);
                     dst[(buf * 16 + rank) * 2 + warp] = v;
                 }
-            } else if (lane == 0) {
-                // self-tagged record: 16-bit example tag | 48-bit signed partial
-                const unsigned long long r =
-                    ((unsigned long long)tag << 48) | ((unsigned long long)v & 0xFFFFFFFFFFFFull);
-                st_relaxed_u64(&k.rec[((size_t)buf * n_cta + rank) * 2 + warp], r);
+            } else if (lane == 0 && v) {
+                atomicAdd(&k.rec[(int)(i % 3) * 2 + warp], (unsigned long long)v);
             }
         }
-        if (MODE == MODE_CLUSTER) cluster_arrive();
+        if (MODE == MODE_CLUSTER) {
+            cluster_arrive();
+        } else {
+            __syncthreads();  // both partial sums issued before the arrival
+            if (tid == 0) red_release_add(k.bar, 1u);
+        }
+        PHASE(1);
         // while the all-reduce is pending: update-flag draws for [fs, fe)
         // (feedback.py:47-53; independent of the votes) and the next example
         if (pre) {
@@ -455,6 +487,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
         }
         prefetch(k, s, i);
+        PHASE(2);
         uint64_t t_t, t_n;
         if (MODE == MODE_CLUSTER) {
             cluster_wait();
@@ -474,26 +507,20 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 k.trace[i * 4 + 2] = vn;
             }
         } else {
-            // the records are the barrier: warp 0 polls every CTA's pair until
-            // all carry this example's tag (no counter, no second round trip)
-            if (warp == 0) {
-                long long vl = 0, vn = 0;
-                for (int r = lane; r < n_cta; r += 32) {
-                    const unsigned long long *src = k.rec + ((size_t)buf * n_cta + r) * 2;
-                    ulonglong2 p;
-                    do {
-                        p = ld_relaxed_v2u64(src);
-                    } while ((unsigned)(p.x >> 48) != tag || (unsigned)(p.y >> 48) != tag);
-                    vl += (long long)(p.x << 16) >> 16;
-                    vn += (long long)(p.y << 16) >> 16;
+            // counter barrier: release arrivals, relaxed spin + acquire, then
+            // strong reads of the two summed votes
+            if (tid == 0) {
+                const unsigned target = (unsigned)((i + 1) * n_cta);
+                while ((int)(ld_relaxed_u32(k.bar) - target) < 0) {
                 }
-                for (int o = 16; o; o >>= 1) {
-                    vl += __shfl_xor_sync(0xffffffffu, vl, o);
-                    vn += __shfl_xor_sync(0xffffffffu, vn, o);
-                }
-                if (lane == 0) {
-                    s.vsum[0] = vl;
-                    s.vsum[1] = vn;
+                fence_acquire();
+                const int slot = (int)(i % 3);
+                s.vsum[0] = (long long)ld_relaxed_u64(&k.rec[slot * 2 + 0]);
+                s.vsum[1] = (long long)ld_relaxed_u64(&k.rec[slot * 2 + 1]);
+                // slot (i+2)%3 == (i-1)%3: every CTA read it before arriving here
+                if (rank == 0) {
+                    st_relaxed_u64(&k.rec[((i + 2) % 3) * 2 + 0], 0ull);
+                    st_relaxed_u64(&k.rec[((i + 2) % 3) * 2 + 1], 0ull);
                 }
             }
             __syncthreads();
@@ -508,6 +535,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 k.trace[i * 4 + 2] = s.vsum[1];
             }
         }
+        PHASE(3);
         // 3. update flags over [fs, fe) as bitmaps
         for (int idx = tid; idx < nfw * 32; idx += nthr) {
             const int j = fsa + idx;
@@ -528,6 +556,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
         }
         __syncthreads();
+        PHASE(4);
         // 4-5. warp 0: exclusive prefix of events per flag word, then window
         //      ordinals, event types, weights (feedback then weight,
         //      SPEC.md:171) and the work list of the own clauses
@@ -603,10 +632,14 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
         }
         __syncthreads();
+        PHASE(5);
         // 6. per-position Type I / II updates of the work list
         feedback_quads<SMEM_STATES>(k, s, c0, lit, s.misc[0], cn);
         __syncthreads();
+        PHASE(6);
     }
+    if (prof && tid == 0)
+        for (int q = 0; q < 8; ++q) k.phase[rank * 8 + q] = ph[q];
     if (MODE == MODE_CLUSTER) cg::this_cluster().sync();  // peers done with our inbox
     store_slice<SMEM_STATES>(k, s, c0, cown);
     for (int bi = tid; bi <= b1 - b0; bi += nthr) {
@@ -630,7 +663,7 @@ struct tmb_trainer {
     uint64_t launches = 0;
     TrainK k;
     uint64_t *block_seeds_d = nullptr;
-    unsigned long long *ring_d = nullptr;  // grid-mode vote records [2][n_cta][2]
+    unsigned long long *ring_d = nullptr;  // grid mode: vote ring [3][2] + counter
 };
 
 namespace {
@@ -745,7 +778,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     std::vector<uint64_t> seeds(c.n_blocks);
     for (int64_t b = 0; b < c.n_blocks; ++b) seeds[b] = derive_stream(c.seed, (uint64_t)b);
     if ((rc = check_cuda(cudaMalloc(&t->block_seeds_d, 8 * c.n_blocks), "cudaMalloc")) ||
-        (rc = check_cuda(cudaMalloc(&t->ring_d, 8 * (size_t)(2 * 2 * n_cta)), "cudaMalloc")) ||
+        (rc = check_cuda(cudaMalloc(&t->ring_d, 8 * 8), "cudaMalloc")) ||
         (rc = check_cuda(cudaMemcpy(t->block_seeds_d, seeds.data(), 8 * c.n_blocks,
                                     cudaMemcpyHostToDevice), "cudaMemcpy"))) {
         tmb_trainer_destroy(t);
@@ -753,9 +786,16 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     }
     k.block_seeds = t->block_seeds_d;
     k.rec = t->ring_d;
+    k.bar = reinterpret_cast<unsigned *>(t->ring_d + 6);
     k.states = states; k.weights = weights; k.block_counters = block_counters;
     t->k = k;
     *out = t;
+    return TMB_OK;
+}
+
+int tmb_trainer_set_profile(tmb_trainer *t, uint64_t *phase) {
+    if (!t) return fail(TMB_E_INVALID, "trainer_set_profile: NULL trainer");
+    t->k.phase = reinterpret_cast<unsigned long long *>(phase);
     return TMB_OK;
 }
 
@@ -814,7 +854,7 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         lc.numAttrs = 1;
         TMB_CUDA(cudaLaunchKernelExC(&lc, fn, args));
     } else {
-        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 8 * (size_t)(2 * 2 * t->n_cta), st));
+        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 8 * 8, st));
         TMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(t->n_cta), dim3(t->threads), args,
                                              (size_t)t->smem, st));
     }
