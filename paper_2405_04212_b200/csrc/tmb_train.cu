@@ -49,8 +49,7 @@ struct TrainK {
     int32_t *weights;
     uint64_t *block_counters;
     const uint64_t *block_seeds;
-    unsigned long long *rec;   // grid mode: [3][2] summed (label, negative) votes
-    unsigned int *bar;         // grid mode: arrival counter
+    unsigned long long *rec;   // grid mode: [n_steps][2] {arrivals:24 | biased vote sum:40}
     unsigned long long *phase;  // optional [n_cta][8] clock64 per phase (profiling)
     tmb_train_stats *stats;
     long long *trace;  // optional [n_steps][4]: negative, votes[label], votes[neg], events
@@ -90,6 +89,10 @@ __device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
 // copy of the line and never observe the update.
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+constexpr long long kVoteBias = 1LL << 31;  // |partial votes of one CTA| < 2^31
+__device__ __forceinline__ void red_relaxed_add_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
     unsigned long long v;
@@ -381,7 +384,8 @@ __device__ __forceinline__ void decide(const TrainK &k, long long vl, long long 
 
 __device__ __forceinline__ int negative_class(const TrainK &k, int label, uint64_t fbc) {
     const double u = u01_from53(draw53(k.fb_seed, fbc));
-    return (int)((label + 1 + (int64_t)(u * (double)(k.K - 1))) % k.K);
+    int neg = label + 1 + (int)(u * (double)(k.K - 1));  // < 2K
+    return neg >= k.K ? neg - k.K : neg;
 }
 
 __device__ __forceinline__ void cluster_arrive() {
@@ -466,16 +470,14 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                     long long *dst = cg::this_cluster().map_shared_rank(s.vin, lane);
                     dst[(buf * 16 + rank) * 2 + warp] = v;
                 }
-            } else if (lane == 0 && v) {
-                atomicAdd(&k.rec[(int)(i % 3) * 2 + warp], (unsigned long long)v);
+            } else if (lane == 0) {
+                // fence-free arrival: one relaxed atomic carries the arrival
+                // count (bits 40..63) and the biased partial (bits 0..39)
+                red_relaxed_add_u64(&k.rec[i * 2 + warp],
+                                    (1ull << 40) + (unsigned long long)(v + kVoteBias));
             }
         }
-        if (MODE == MODE_CLUSTER) {
-            cluster_arrive();
-        } else {
-            __syncthreads();  // both partial sums issued before the arrival
-            if (tid == 0) red_release_add(k.bar, 1u);
-        }
+        if (MODE == MODE_CLUSTER) cluster_arrive();
         PHASE(1);
         // while the all-reduce is pending: update-flag draws for [fs, fe)
         // (feedback.py:47-53; independent of the votes) and the next example
@@ -507,21 +509,16 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 k.trace[i * 4 + 2] = vn;
             }
         } else {
-            // counter barrier: release arrivals, relaxed spin + acquire, then
-            // strong reads of the two summed votes
+            // all-reduce complete when both words count n_cta arrivals
             if (tid == 0) {
-                const unsigned target = (unsigned)((i + 1) * n_cta);
-                while ((int)(ld_relaxed_u32(k.bar) - target) < 0) {
-                }
-                fence_acquire();
-                const int slot = (int)(i % 3);
-                s.vsum[0] = (long long)ld_relaxed_u64(&k.rec[slot * 2 + 0]);
-                s.vsum[1] = (long long)ld_relaxed_u64(&k.rec[slot * 2 + 1]);
-                // slot (i+2)%3 == (i-1)%3: every CTA read it before arriving here
-                if (rank == 0) {
-                    st_relaxed_u64(&k.rec[((i + 2) % 3) * 2 + 0], 0ull);
-                    st_relaxed_u64(&k.rec[((i + 2) % 3) * 2 + 1], 0ull);
-                }
+                const unsigned long long want = (unsigned long long)n_cta;
+                ulonglong2 p;
+                do {
+                    p = ld_relaxed_v2u64(&k.rec[i * 2]);
+                } while ((p.x >> 40) != want || (p.y >> 40) != want);
+                const long long bias = (long long)n_cta * kVoteBias;
+                s.vsum[0] = (long long)(p.x & ((1ull << 40) - 1)) - bias;
+                s.vsum[1] = (long long)(p.y & ((1ull << 40) - 1)) - bias;
             }
             __syncthreads();
             decide(k, s.vsum[0], s.vsum[1], t_t, t_n);
@@ -594,9 +591,15 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
                 int info = s.info[j] & I_OUT;
                 if (t_ev || n_ev) {
-                    const int bi = block_of(c, C, k.n_blocks) - b0;
-                    const uint64_t ord = s.blk_ctr[bi] +
-                        (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
+                    int bi = 0;
+                    uint64_t ord;
+                    if (k.n_blocks == 1) {  // fs == 0: events before c in the block
+                        ord = s.blk_ctr[0] + (uint64_t)cum(c);
+                    } else {
+                        bi = block_of(c, C, k.n_blocks) - b0;
+                        ord = s.blk_ctr[bi] +
+                              (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
+                    }
                     const uint64_t bseed = s.blk_seed[bi];
                     const bool out = info & I_OUT;
                     int32_t *w = s.weights + j * K;
@@ -625,7 +628,9 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
             __syncwarp();
             // one window per applied event (block counters)
-            for (int bi = lane; bi <= b1 - b0; bi += 32) {
+            if (k.n_blocks == 1) {
+                if (lane == 0) s.blk_ctr[0] += (uint64_t)s.word_cum[nfw];
+            } else for (int bi = lane; bi <= b1 - b0; bi += 32) {
                 const int bs = block_begin(b0 + bi, C, k.n_blocks);
                 const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
                 s.blk_ctr[bi] += (uint64_t)(cum(be) - cum(bs));
@@ -663,7 +668,8 @@ struct tmb_trainer {
     uint64_t launches = 0;
     TrainK k;
     uint64_t *block_seeds_d = nullptr;
-    unsigned long long *ring_d = nullptr;  // grid mode: vote ring [3][2] + counter
+    unsigned long long *ring_d = nullptr;  // grid mode: per-example vote slots [cap][2]
+    int64_t ring_cap = 0;
 };
 
 namespace {
@@ -715,6 +721,8 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     n_cta = std::max(1, std::min(n_cta, C));
     if (n_cta > 16 && n_cta > sms) n_cta = sms;
     const bool cluster = n_cta <= 16;
+    if (!cluster && n_cta >= 256)
+        return fail(TMB_E_UNSUPPORTED, "trainer_create: grid mode supports < 256 CTAs");
     if (threads <= 0) threads = (n_cta == 1 && work <= 16384) ? 256 : 512;
     threads = std::max(64, std::min(512, threads / 32 * 32));
 
@@ -778,15 +786,14 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     std::vector<uint64_t> seeds(c.n_blocks);
     for (int64_t b = 0; b < c.n_blocks; ++b) seeds[b] = derive_stream(c.seed, (uint64_t)b);
     if ((rc = check_cuda(cudaMalloc(&t->block_seeds_d, 8 * c.n_blocks), "cudaMalloc")) ||
-        (rc = check_cuda(cudaMalloc(&t->ring_d, 8 * 8), "cudaMalloc")) ||
+
         (rc = check_cuda(cudaMemcpy(t->block_seeds_d, seeds.data(), 8 * c.n_blocks,
                                     cudaMemcpyHostToDevice), "cudaMemcpy"))) {
         tmb_trainer_destroy(t);
         return rc;
     }
     k.block_seeds = t->block_seeds_d;
-    k.rec = t->ring_d;
-    k.bar = reinterpret_cast<unsigned *>(t->ring_d + 6);
+
     k.states = states; k.weights = weights; k.block_counters = block_counters;
     t->k = k;
     *out = t;
@@ -829,8 +836,7 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     if (!t) return fail(TMB_E_INVALID, "trainer_run: NULL trainer");
     if (n_steps <= 0) return TMB_OK;
     if (!lit_words || !labels || !order) return fail(TMB_E_INVALID, "trainer_run: NULL data");
-    if (n_steps > (int64_t)(0xFFFFFFFFu / (unsigned)t->n_cta) - 1)
-        return fail(TMB_E_UNSUPPORTED, "trainer_run: split runs longer than 2^32/n_cta steps");
+
     cudaStream_t st = as_stream(stream);
     TrainK k = t->k;
     k.lit_words = lit_words; k.labels = labels; k.order = order;
@@ -854,7 +860,18 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         lc.numAttrs = 1;
         TMB_CUDA(cudaLaunchKernelExC(&lc, fn, args));
     } else {
-        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 8 * 8, st));
+        if (t->ring_cap < n_steps) {
+            if (t->ring_d) {
+                cudaStreamSynchronize(st);
+                cudaFree(t->ring_d);
+            }
+            t->ring_d = nullptr;
+            t->ring_cap = 0;
+            TMB_CUDA(cudaMalloc(&t->ring_d, 16 * (size_t)n_steps));
+            t->ring_cap = n_steps;
+        }
+        k.rec = t->ring_d;
+        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 16 * (size_t)n_steps, st));
         TMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(t->n_cta), dim3(t->threads), args,
                                              (size_t)t->smem, st));
     }
