@@ -345,16 +345,42 @@ __device__ __forceinline__ void flush_stats(const TrainK &k, Counters &cn, bool 
 // Example ring in shared memory: misc[3 + (i % 3)] = order[i]; the literal
 // row of example i lives in lit{i&1}.  Issued one / two examples ahead so
 // the dependent global loads overlap the current example.
-__device__ __forceinline__ void prefetch(const TrainK &k, const Smem &s, int64_t i) {
-    if (i + 1 < k.n_steps) {
-        const int ex = s.misc[3 + (int)((i + 1) % 3)];
-        if (threadIdx.x == blockDim.x - 1) {  // not warp 0: it polls the votes
-            s.misc[8 + (int)((i + 1) % 3)] = __ldg(&k.labels[ex]);
-            if (i + 2 < k.n_steps) s.misc[3 + (int)((i + 2) % 3)] = __ldg(&k.order[i + 2]);
-        }
-        uint32_t *dst = ((i + 1) & 1) ? s.lit1 : s.lit0;
-        for (int w = threadIdx.x; w < k.W; w += blockDim.x)
-            dst[w] = __ldg(&k.lit_words[(int64_t)ex * k.W + w]);
+// Next-example prefetch, split so the global loads are issued at the top of
+// example i (into registers) and committed to shared memory at its end --
+// their latency hides behind the whole example instead of stalling it.
+constexpr int kRowRegs = 4;  // literal words per thread (W <= 4 * blockDim)
+struct Prefetch {
+    uint32_t row[kRowRegs];
+    int label, ex2;
+};
+
+__device__ __forceinline__ void prefetch_issue(const TrainK &k, const Smem &s, int64_t i,
+                                               Prefetch &pf) {
+    if (i + 1 >= k.n_steps) return;
+    const int ex = s.misc[3 + (int)((i + 1) % 3)];
+#pragma unroll
+    for (int q = 0; q < kRowRegs; ++q) {
+        const int w = threadIdx.x + q * blockDim.x;
+        if (w < k.W) pf.row[q] = __ldg(&k.lit_words[(int64_t)ex * k.W + w]);
+    }
+    if (threadIdx.x == blockDim.x - 1) {
+        pf.label = __ldg(&k.labels[ex]);
+        if (i + 2 < k.n_steps) pf.ex2 = __ldg(&k.order[i + 2]);
+    }
+}
+
+__device__ __forceinline__ void prefetch_commit(const TrainK &k, const Smem &s, int64_t i,
+                                                const Prefetch &pf) {
+    if (i + 1 >= k.n_steps) return;
+    uint32_t *dst = ((i + 1) & 1) ? s.lit1 : s.lit0;
+#pragma unroll
+    for (int q = 0; q < kRowRegs; ++q) {
+        const int w = threadIdx.x + q * blockDim.x;
+        if (w < k.W) dst[w] = pf.row[q];
+    }
+    if (threadIdx.x == blockDim.x - 1) {
+        s.misc[8 + (int)((i + 1) % 3)] = pf.label;
+        if (i + 2 < k.n_steps) s.misc[3 + (int)((i + 2) % 3)] = pf.ex2;
     }
 }
 
@@ -445,6 +471,8 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         const int label = s.misc[8 + (int)(i % 3)];
         const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
         const int neg = negative_class(k, label, fbc);
+        Prefetch pf;
+        prefetch_issue(k, s, i, pf);
         // 1. training-mode outputs of own clauses (kernels/_numba.py:36-50)
         for (int j = warp; j < cown; j += nwarps) {
             uint32_t viol = 0;
@@ -488,7 +516,6 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 s.draw_n[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
             }
         }
-        prefetch(k, s, i);
         PHASE(2);
         uint64_t t_t, t_n;
         if (MODE == MODE_CLUSTER) {
@@ -640,6 +667,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         PHASE(5);
         // 6. per-position Type I / II updates of the work list
         feedback_quads<SMEM_STATES>(k, s, c0, lit, s.misc[0], cn);
+        prefetch_commit(k, s, i, pf);
         __syncthreads();
         PHASE(6);
     }
@@ -726,6 +754,8 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     if (threads <= 0) threads = (n_cta == 1 && work <= 16384) ? 256 : 512;
     threads = std::max(64, std::min(512, threads / 32 * 32));
 
+    if (W > kRowRegs * threads)
+        return fail(TMB_E_UNSUPPORTED, "trainer_create: literal rows wider than 4*threads words");
     TrainK k{};
     k.C = C; k.P = P; k.K = K; k.W = W; k.Ppad = Ppad;
     k.n_blocks = (int)c.n_blocks; k.n_cta = n_cta;
