@@ -1,0 +1,93 @@
+// tmb_microbench.cu -- latency microbenchmarks of the per-example all-reduce
+// candidates used by the fused trainer (design evidence, not product code).
+#include <cooperative_groups.h>
+
+#include "tmb_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tmb {
+
+__device__ __forceinline__ void mb_red(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long mb_ld(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// mode 0: one relaxed red per CTA into a fresh per-iteration word, thread 0
+//         polls until the count reaches n_cta, __syncthreads.
+// mode 1: same with __nanosleep(64) backoff between polls.
+// mode 2: every CTA's red goes to one of 8 words 256 B apart; warp 0 polls
+//         all 8 in parallel.
+// mode 3: cooperative_groups grid.sync().
+__global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
+                               unsigned long long *cycles) {
+    const int n = gridDim.x;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        if (mode == 3) {
+            cg::this_grid().sync();
+            continue;
+        }
+        if (mode == 2) {
+            unsigned long long *base = slots + (size_t)i * 8 * 32;
+            if (threadIdx.x == 0) mb_red(base + (blockIdx.x & 7) * 32, 1ull);
+            if (threadIdx.x < 32) {
+                const int g = threadIdx.x;
+                const unsigned long long want = (g < 8) ? (unsigned long long)((n - g + 7) / 8) : 0;
+                bool done;
+                do {
+                    const unsigned long long v = g < 8 ? mb_ld(base + g * 32) : 0;
+                    done = __all_sync(0xffffffffu, v >= want);
+                } while (!done);
+            }
+            __syncthreads();
+            continue;
+        }
+        unsigned long long *w = slots + (size_t)i * 32;
+        if (threadIdx.x == 0) {
+            mb_red(w, 1ull);
+            while (mb_ld(w) < (unsigned long long)n) {
+                if (mode == 1) __nanosleep(64);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = (unsigned long long)(clock64() - t0);
+}
+
+}  // namespace tmb
+
+using namespace tmb;
+
+extern "C" int tmb_microbench_allreduce(int n_cta, int threads, int iters, int mode,
+                                        double *us_per_iter) {
+    int rc = require_device();
+    if (rc) return rc;
+    unsigned long long *slots = nullptr, *cyc = nullptr;
+    size_t words = (size_t)iters * (mode == 2 ? 8 * 32 : 32);
+    TMB_CUDA(cudaMalloc(&slots, 8 * words));
+    TMB_CUDA(cudaMalloc(&cyc, 8));
+    TMB_CUDA(cudaMemset(slots, 0, 8 * words));
+    void *args[] = {&slots, &iters, &mode, &cyc};
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    rc = check_cuda(cudaLaunchCooperativeKernel((const void *)k_mb_allreduce, dim3(n_cta),
+                                                dim3(threads), args, 0, 0),
+                    "microbench launch");
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    if (!rc) *us_per_iter = (double)ms * 1e3 / iters;
+    cudaFree(slots);
+    cudaFree(cyc);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return rc;
+}
