@@ -57,6 +57,12 @@ int tmb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
 /* Number of this library's kernel launches since load (for gpu_launches). */
 uint64_t tmb_launch_count(void);
 
+/* All-reduce latency microbenchmark (design evidence for the trainer's
+ * per-example synchronisation).  mode 0: relaxed red + poll;
+ * 1: same with backoff; 2: 8 sub-counters; 3: cooperative grid.sync(). */
+int tmb_microbench_allreduce(int n_cta, int threads, int iters, int mode,
+                             double *us_per_iter);
+
 /* ----------------------------------------------------- RNG (core.py) -- */
 /* core.py:66-95 on the host; used by the host driver and tests. */
 uint64_t tmb_derive_stream(uint64_t seed, uint64_t index);
