@@ -42,7 +42,6 @@ struct TrainK {
     FbParams fp;
     uint64_t fb_seed, fb_counter0;
     int64_t n_steps;
-    uint64_t tag_base;  // launch-unique offset of the vote-record tags
     const uint32_t *lit_words;
     const int32_t *labels, *order;
     int8_t *states;
@@ -549,10 +548,6 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             }
             __syncthreads();
             decide(k, s.vsum[0], s.vsum[1], t_t, t_n);
-            if (k.trace && tid == 0 && k.n_steps == 1) {
-                k.trace[4 + rank * 2 + 0] = s.vsum[0];
-                k.trace[4 + rank * 2 + 1] = s.vsum[1];
-            }
             if (k.trace && rank == 0 && tid == 0) {
                 k.trace[i * 4 + 0] = neg;
                 k.trace[i * 4 + 1] = s.vsum[0];
@@ -871,8 +866,6 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     TrainK k = t->k;
     k.lit_words = lit_words; k.labels = labels; k.order = order;
     k.n_steps = n_steps; k.fb_counter0 = fb_counter; k.stats = stats;
-    k.tag_base = t->launches;
-    t->launches += (uint64_t)n_steps + 7;
     void *args[] = {&k};
     const void *fn = kernel_for(t->cluster, t->smem_states);
     if (t->cluster) {
