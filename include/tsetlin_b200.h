@@ -218,6 +218,10 @@ int tmb_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes,
  * the last check saw a feature byte other than 0 / 1 (the device path
  * requires binary inputs); clears the flag. */
 int tmb_infer_status(void *stream);
+/* Library options (tests / tuning): "infer.force_generic" = 1 routes
+ * tmb_infer to the generic one-CTA-per-tile kernel instead of the 4-CTA
+ * cluster kernel. */
+int tmb_set_option(const char *name, int64_t value);
 /* End-to-end variant with HOST buffers: streams x (host, ideally pinned)
  * through the device in chunks with copy/compute overlap and returns host
  * votes / pred (either may be NULL).  Synchronous. */

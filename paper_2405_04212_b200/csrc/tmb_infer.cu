@@ -13,10 +13,14 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "tmb_common.cuh"
 #include "tmb_device.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 struct tmb_rules {
     int64_t R = 0, K = 0, F = 0, n_inc = 0;
@@ -24,7 +28,13 @@ struct tmb_rules {
     uint32_t *inc = nullptr;     // device [n_inc]: (feature << 1) | negated
     int64_t *ptr = nullptr;      // device [R+1]
     int32_t *weights = nullptr;  // device [R, K]
-    int vote_bits = 32;
+    // head/tail form for the cluster kernel (uint16 codes; F + 1 < 32768):
+    // the first 16 include codes of every rule, padded with the always-true
+    // code (F << 1) that addresses an all-ones X^T row; the rest in a CSR tail
+    uint16_t *heads = nullptr;   // device [R, 16]
+    int32_t *tail_ptr = nullptr; // device [R+1]
+    uint16_t *tails = nullptr;   // device [n_tail]
+    int heads_ok = 0;
 };
 
 namespace tmb {
@@ -147,6 +157,219 @@ __global__ void __launch_bounds__(512) k_infer(InferK k) {
     if (bad) atomicOr(k.bad_input, 1u);
 }
 
+// ---------------------------------------------------------------------------
+// Cluster kernel: CS = 4 CTAs per cluster split the rule set (each keeps the
+// 16-code heads of its quarter resident in shared memory) and share one
+// bit-transposed tile of TG*32 examples: CTA r transposes feature chunks
+// [r*nch/4, (r+1)*nch/4) of the raw bytes and stores the X^T words into all
+// four CTAs' shared memory (DSMEM).  Tiles are double-buffered so the next
+// tile's HBM reads overlap the current tile's rule evaluation; partial class
+// sums are pushed to the CTA that owns each 32-example block, which sums the
+// four partials and writes votes / predictions.  One cluster barrier per tile.
+constexpr int kCS = 4;   // CTAs per cluster
+constexpr int kTG = 4;   // 32-example groups per tile
+constexpr int kHead = 16;
+
+struct InferCK {
+    const uint8_t *x;
+    int64_t N, F;
+    const uint16_t *heads;
+    const int32_t *tail_ptr;
+    const uint16_t *tails;
+    const int32_t *w;
+    int R, K;
+    int64_t *votes, *pred;
+    const int64_t *labels;
+    unsigned long long *correct;
+    unsigned int *bad_input;
+    int vec_ok;
+    int rloc_max;
+};
+
+__device__ __forceinline__ uint32_t pack8(unsigned long long q) {
+    return (uint32_t)(((q & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56);
+}
+
+// up to 8 feature bytes starting at column f (bounds-checked against F)
+__device__ __forceinline__ unsigned long long load8_tail(const uint8_t *src, int64_t f, int64_t F) {
+    unsigned long long v = 0;
+    for (int bb = 0; bb < 8; ++bb)
+        if (f + bb < F) v |= (unsigned long long)src[bb] << (8 * bb);
+    return v;
+}
+
+// 32x32 bit transpose across the warp: lane i holds row i (bit j = A[i][j]);
+// afterwards lane j holds column j (bit i = A[i][j]).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) {
+        const uint32_t m0 = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                          : j == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~m0) | ((y >> j) & m0)) : ((x & m0) | ((y << j) & ~m0));
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int K = k.K;
+    const int64_t F = k.F;
+    const int xrows = (int)F + 1;  // + all-ones row for padding codes
+    // shared layout: heads | xt[2] | part | inbox[2][kCS][32][K]
+    uint4 *heads = reinterpret_cast<uint4 *>(smem_raw);                       // [rloc][2]
+    uint32_t *xt0 = reinterpret_cast<uint32_t *>(heads + 2 * (size_t)k.rloc_max);
+    uint32_t *xt1 = xt0 + (size_t)xrows * kTG;
+    int32_t *part = reinterpret_cast<int32_t *>(xt1 + (size_t)xrows * kTG);   // [32*kTG][K]
+    int32_t *inbox = part + 32 * kTG * K;                                     // [2][kCS][32][K]
+
+    const int r0 = (int)((int64_t)rank * k.R / kCS), r1 = (int)((int64_t)(rank + 1) * k.R / kCS);
+    const int rloc = r1 - r0;
+    for (int i = tid; i < rloc * 2; i += blockDim.x)
+        heads[i] = reinterpret_cast<const uint4 *>(k.heads)[(size_t)r0 * 2 + i];
+    // all-ones padding row in both buffers
+    if (tid < kTG) {
+        xt0[(size_t)F * kTG + tid] = 0xFFFFFFFFu;
+        xt1[(size_t)F * kTG + tid] = 0xFFFFFFFFu;
+    }
+
+    const int64_t tile_n = 32 * kTG;
+    const int64_t n_tiles = (k.N + tile_n - 1) / tile_n;
+    const int n_clusters = gridDim.x / kCS;
+    const int cid = blockIdx.x / kCS;
+    const int nch = (int)((F + 31) / 32);
+    const int ch0 = (int)((int64_t)rank * nch / kCS), ch1 = (int)((int64_t)(rank + 1) * nch / kCS);
+    uint32_t bad = 0;
+    unsigned long long hits = 0;
+
+    // transpose this CTA's feature quarter of tile `t` into buffer `buf` of
+    // every CTA in the cluster
+    auto transpose = [&](int64_t t, int buf) {
+        const int64_t e0 = t * tile_n;
+        uint32_t *mine = buf ? xt1 : xt0;
+        const int units = (ch1 - ch0) * kTG;
+        for (int u = warp; u < units; u += nwarps) {
+            const int g = u % kTG;
+            const int c = ch0 + u / kTG;
+            const int64_t e = e0 + 32 * g + lane;
+            const int64_t f0 = (int64_t)c * 32;
+            unsigned long long q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+            if (e < k.N) {
+                const uint8_t *src = k.x + e * F + f0;
+                if (k.vec_ok && f0 + 32 <= F) {
+                    const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(src));
+                    const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(src) + 1);
+                    q0 = ((unsigned long long)a.y << 32) | a.x;
+                    q1 = ((unsigned long long)a.w << 32) | a.z;
+                    q2 = ((unsigned long long)b.y << 32) | b.x;
+                    q3 = ((unsigned long long)b.w << 32) | b.z;
+                } else {
+                    q0 = load8_tail(src, f0, F);
+                    q1 = load8_tail(src + 8, f0 + 8, F);
+                    q2 = load8_tail(src + 16, f0 + 16, F);
+                    q3 = load8_tail(src + 24, f0 + 24, F);
+                }
+            }
+            bad |= (uint32_t)(((q0 | q1 | q2 | q3) & 0xFEFEFEFEFEFEFEFEull) != 0);
+            const uint32_t row = pack8(q0) | (pack8(q1) << 8) | (pack8(q2) << 16) |
+                                 (pack8(q3) << 24);
+            const uint32_t col = warp_transpose32(row, lane);  // feature f0+lane, 32 examples
+            if (f0 + lane < F) {
+                const size_t idx = (size_t)(f0 + lane) * kTG + g;
+#pragma unroll
+                for (int p = 0; p < kCS; ++p) cluster.map_shared_rank(mine, p)[idx] = col;
+            }
+        }
+    };
+
+    int64_t it = 0;
+    int64_t t = cid;
+    if (t < n_tiles) transpose(t, 0);
+    cluster.sync();
+    for (; t < n_tiles; t += n_clusters, ++it) {
+        const int buf = (int)(it & 1);
+        const uint32_t *xt = buf ? xt1 : xt0;
+        for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
+        const int64_t tn = t + n_clusters;
+        if (tn < n_tiles) transpose(tn, buf ^ 1);
+        __syncthreads();
+        // ---- evaluate the local rules: lane = (rule slot, group)
+        constexpr int S = 32 / kTG;
+        const int slot = lane / kTG, g = lane % kTG;
+        for (int rc = warp; rc * S < rloc; rc += nwarps) {
+            const int r = rc * S + slot;
+            const int rr = r < rloc ? r : 0;  // idle lanes still join the votes
+            uint32_t acc = r < rloc ? 0xFFFFFFFFu : 0u;
+            {
+                const uint4 h0 = heads[rr * 2], h1 = heads[rr * 2 + 1];
+                const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t c0 = hw[q] & 0xFFFFu, c1 = hw[q] >> 16;
+                    const uint32_t x0 = xt[(c0 >> 1) * kTG + g] ^ (0u - (c0 & 1u));
+                    const uint32_t x1 = xt[(c1 >> 1) * kTG + g] ^ (0u - (c1 & 1u));
+                    acc &= x0 & x1;
+                    if ((q & 1) && !__any_sync(0xffffffffu, acc)) break;
+                }
+            }
+            if (acc && r < rloc) {
+                const int rg = r0 + r;
+                for (int q = __ldg(&k.tail_ptr[rg]), qe = __ldg(&k.tail_ptr[rg + 1]); q < qe && acc; ++q) {
+                    const uint32_t c = __ldg(&k.tails[q]);
+                    acc &= xt[(c >> 1) * kTG + g] ^ (0u - (c & 1u));
+                }
+                if (acc) {
+                    const int32_t *wr = k.w + (size_t)rg * K;
+                    while (acc) {
+                        const int b = __ffs(acc) - 1;
+                        acc &= acc - 1;
+                        int32_t *dst = part + (g * 32 + b) * K;
+                        for (int kk = 0; kk < K; ++kk) {
+                            const int32_t wv = __ldg(&wr[kk]);
+                            if (wv) atomicAdd(&dst[kk], wv);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- push partial sums of example block b to CTA b's inbox
+        for (int i = tid; i < 32 * kTG * K; i += blockDim.x) {
+            const int b = i / (32 * K);  // example block == owning CTA
+            const int rem = i - b * 32 * K;
+            int32_t *dst = cluster.map_shared_rank(inbox, b);
+            dst[((buf * kCS + rank) * 32) * K + rem] = part[i];
+        }
+        cluster.sync();
+        // ---- finalize the 32 examples of block `rank`
+        if (warp == 0) {
+            const int64_t e = t * tile_n + 32 * rank + lane;
+            if (e < k.N) {
+                int best = 0;
+                int32_t bv = 0;
+                for (int kk = 0; kk < K; ++kk) {
+                    int32_t sum = 0;
+#pragma unroll
+                    for (int p = 0; p < kCS; ++p) sum += inbox[((buf * kCS + p) * 32 + lane) * K + kk];
+                    if (kk == 0 || sum > bv) { bv = sum; best = kk; }
+                    if (k.votes) k.votes[e * K + kk] = (int64_t)sum;
+                }
+                if (k.pred) k.pred[e] = best;
+                if (k.labels) hits += (k.labels[e] == best);
+            }
+        }
+    }
+    cluster.sync();  // peers may still write into our buffers until here
+    if (k.correct) {
+        for (int o = 16; o; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+        if (lane == 0 && hits) atomicAdd(k.correct, hits);
+    }
+    if (bad) atomicOr(k.bad_input, 1u);
+}
+
 static unsigned int *g_bad_flag = nullptr;
 
 static int pick_g(int64_t F, int64_t K, int max_smem, int *G_out, size_t *smem_out) {
@@ -161,17 +384,28 @@ static int pick_g(int64_t F, int64_t K, int max_smem, int *G_out, size_t *smem_o
     return fail(TMB_E_UNSUPPORTED, "infer: feature width too large for one tile in shared memory");
 }
 
+static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes,
+                                int64_t *pred, const int64_t *labels,
+                                unsigned long long *correct, cudaStream_t st, bool *launched);
+
+int g_force_generic_infer = 0;
+
 int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, int64_t *pred,
                  const int64_t *labels, unsigned long long *correct, cudaStream_t st) {
     if (N == 0) return TMB_OK;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int max_smem = 0;
-    TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     if (!g_bad_flag) {
         TMB_CUDA(cudaMalloc(&g_bad_flag, sizeof(unsigned)));
         TMB_CUDA(cudaMemset(g_bad_flag, 0, sizeof(unsigned)));
     }
+    if (!g_force_generic_infer && r->heads_ok) {
+        bool launched = false;
+        int rc = launch_infer_cluster(r, x, N, votes, pred, labels, correct, st, &launched);
+        if (rc || launched) return rc;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int max_smem = 0;
+    TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     int G;
     size_t smem;
     int rc = pick_g(r->F, r->K, std::min(max_smem, 200 * 1024), &G, &smem);
@@ -192,6 +426,55 @@ int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes
     void *args[] = {&k};
     TMB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(threads), args, smem, st));
     TMB_LAUNCHED();
+    return TMB_OK;
+}
+
+static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes,
+                                int64_t *pred, const int64_t *labels,
+                                unsigned long long *correct, cudaStream_t st, bool *launched) {
+    *launched = false;
+    if (r->K > 32 || r->R < 1) return TMB_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int max_smem = 0;
+    TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const int64_t rloc_max = (r->R + kCS - 1) / kCS;
+    const size_t smem = 32 * (size_t)rloc_max + 2 * 4 * (size_t)(r->F + 1) * kTG +
+                        4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K;
+    if (smem > (size_t)max_smem) return TMB_OK;  // generic kernel instead
+    InferCK k;
+    k.x = x; k.N = N; k.F = r->F; k.heads = r->heads; k.tail_ptr = r->tail_ptr; k.tails = r->tails;
+    k.w = r->weights; k.R = (int)r->R; k.K = (int)r->K; k.votes = votes; k.pred = pred;
+    k.labels = labels; k.correct = correct; k.bad_input = g_bad_flag;
+    k.vec_ok = (r->F % 16 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+    k.rloc_max = (int)rloc_max;
+    const void *fn = (const void *)k_infer_cluster;
+    TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int threads = 512;
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.blockDim = dim3(threads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    lc.gridDim = dim3(kCS);
+    int max_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, fn, &lc) != cudaSuccess || max_clusters < 1) {
+        cudaGetLastError();
+        return TMB_OK;
+    }
+    const int64_t tiles = (N + 32 * kTG - 1) / (32 * kTG);
+    const int64_t n_clusters = std::min<int64_t>(tiles, max_clusters);
+    lc.gridDim = dim3((unsigned)(n_clusters * kCS));
+    void *args[] = {&k};
+    TMB_CUDA(cudaLaunchKernelExC(&lc, fn, args));
+    TMB_LAUNCHED();
+    *launched = true;
     return TMB_OK;
 }
 
@@ -237,6 +520,30 @@ static int upload_rules(const std::vector<int64_t> &ptr, const std::vector<uint3
         (rc = check_cuda(cudaMalloc(&r->weights, 4 * std::max<size_t>(w.size(), 1)), "cudaMalloc"))) {
         tmb_rules_destroy(r);
         return rc;
+    }
+    // head / tail form (uint16 codes) for the cluster kernel
+    if (F + 1 < 32768 && r->R > 0) {
+        std::vector<uint16_t> heads((size_t)r->R * 16, (uint16_t)(F << 1));
+        std::vector<int32_t> tptr((size_t)r->R + 1, 0);
+        std::vector<uint16_t> tails;
+        for (int64_t i = 0; i < r->R; ++i) {
+            const int64_t a = ptr[i], b = ptr[i + 1];
+            for (int64_t q = a; q < b; ++q) {
+                if (q - a < 16) heads[(size_t)i * 16 + (q - a)] = (uint16_t)inc[q];
+                else tails.push_back((uint16_t)inc[q]);
+            }
+            tptr[i + 1] = (int32_t)tails.size();
+        }
+        if ((rc = check_cuda(cudaMalloc(&r->heads, 2 * heads.size()), "cudaMalloc")) ||
+            (rc = check_cuda(cudaMalloc(&r->tail_ptr, 4 * tptr.size()), "cudaMalloc")) ||
+            (rc = check_cuda(cudaMalloc(&r->tails, 2 * std::max<size_t>(tails.size(), 1)), "cudaMalloc"))) {
+            tmb_rules_destroy(r);
+            return rc;
+        }
+        cudaMemcpy(r->heads, heads.data(), 2 * heads.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(r->tail_ptr, tptr.data(), 4 * tptr.size(), cudaMemcpyHostToDevice);
+        if (!tails.empty()) cudaMemcpy(r->tails, tails.data(), 2 * tails.size(), cudaMemcpyHostToDevice);
+        r->heads_ok = 1;
     }
     cudaMemcpy(r->ptr, ptr.data(), 8 * ptr.size(), cudaMemcpyHostToDevice);
     if (!inc.empty()) cudaMemcpy(r->inc, inc.data(), 4 * inc.size(), cudaMemcpyHostToDevice);
@@ -318,6 +625,9 @@ int tmb_rules_destroy(tmb_rules *r) {
     if (r->ptr) cudaFree(r->ptr);
     if (r->inc) cudaFree(r->inc);
     if (r->weights) cudaFree(r->weights);
+    if (r->heads) cudaFree(r->heads);
+    if (r->tail_ptr) cudaFree(r->tail_ptr);
+    if (r->tails) cudaFree(r->tails);
     delete r;
     return TMB_OK;
 }
@@ -337,6 +647,15 @@ int tmb_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, i
         return fail(TMB_E_INVALID, "infer: bad arguments");
     cudaStream_t st = as_stream(stream);
     return launch_infer(r, x, N, votes, pred, labels, (unsigned long long *)correct, st);
+}
+
+int tmb_set_option(const char *name, int64_t value) {
+    if (!name) return fail(TMB_E_INVALID, "set_option: NULL name");
+    if (std::string(name) == "infer.force_generic") {
+        g_force_generic_infer = (int)value;
+        return TMB_OK;
+    }
+    return fail(TMB_E_INVALID, std::string("set_option: unknown option ") + name);
 }
 
 int tmb_infer_status(void *stream) {

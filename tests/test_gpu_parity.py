@@ -234,6 +234,39 @@ def test_inference_random_models_vs_oracle(gpu, oracle, n_inc, F, K):
     assert np.array_equal(pred, op)
 
 
+@pytest.mark.parametrize("kernel", ["cluster", "generic"])
+@pytest.mark.parametrize("n_inc,F,K,C,N", [(40, 64, 3, 300, 1000), (17, 784, 10, 2001, 700),
+                                           (1, 32, 32, 33, 129), (5, 1000, 2, 5000, 300)])
+def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C, N):
+    """Both inference kernels: rules longer than the 16-code heads (tails),
+    feature widths that are not multiples of 32, K up to 32, ragged tiles."""
+    from paper_2405_04212_b200 import _lib
+    _lib.call("tmb_set_option", b"infer.force_generic", int(kernel == "generic"))
+    try:
+        rs = np.random.default_rng(n_inc + F + K)
+        m = gpu.datasets.inference_model(model_seed=C, n_features=F, n_clauses=C, n_classes=K,
+                                         n_includes=n_inc, weight_range=7)
+        # plant firing: make some examples satisfy some clauses
+        x = rs.integers(0, 2, size=(N, F)).astype(np.uint8)
+        for e in range(0, N, 3):
+            j = int(rs.integers(0, C))
+            inc = np.flatnonzero(m.states[j] >= 0)
+            x[e, inc[inc < F]] = 1
+            x[e, inc[inc >= F] - F] = 0
+        bank = gpu.DenseClauseBank(gpu.Config(n_literals=F, n_clauses=C, n_classes=K, s=2.0,
+                                              threshold=10))
+        bank.states[:] = m.states
+        bank.weights[:] = m.weights
+        model = gpu.CompiledModel.from_bank(bank)
+        votes, pred = model.votes_and_pred(x, chunk=200)
+        ov, op = oracle.batch_votes(m.states, m.weights, oracle.augment_literals(x), nthreads=8)
+        assert np.array_equal(votes, ov)
+        assert np.array_equal(pred, op)
+        assert (ov != 0).any()
+    finally:
+        _lib.call("tmb_set_option", b"infer.force_generic", 0)
+
+
 def test_inference_ties_and_empty(gpu):
     bank = gpu.DenseClauseBank(gpu.Config(n_literals=2, n_clauses=2, n_classes=3, s=2.0,
                                           threshold=5))
