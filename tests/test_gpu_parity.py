@@ -244,8 +244,18 @@ def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C,
     _lib.call("tmb_set_option", b"infer.force_generic", int(kernel == "generic"))
     try:
         rs = np.random.default_rng(n_inc + F + K)
-        m = gpu.datasets.inference_model(model_seed=C, n_features=F, n_clauses=C, n_classes=K,
-                                         n_includes=n_inc, weight_range=7)
+        # satisfiable clauses: n_inc distinct features, random polarity
+        states = np.full((C, 2 * F), -1, dtype=np.int8)
+        for j in range(C):
+            feats = rs.choice(F, size=n_inc, replace=False)
+            pol = rs.integers(0, 2, size=n_inc)
+            states[j, feats + F * pol] = 0
+        weights = rs.integers(-7, 8, size=(C, K)).astype(np.int32)
+
+        class _M:
+            pass
+        m = _M()
+        m.states, m.weights = states, weights
         # plant firing: make some examples satisfy some clauses
         x = rs.integers(0, 2, size=(N, F)).astype(np.uint8)
         for e in range(0, N, 3):
