@@ -285,20 +285,38 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         }
     };
 
+    // bulk L2 prefetch of this CTA's feature quarter of tile `t` (one TMA
+    // bulk-prefetch per example row; no registers, no shared memory)
+    auto prefetch_l2 = [&](int64_t t) {
+        if (t >= n_tiles || !k.vec_ok) return;
+        const int64_t e0 = t * tile_n;
+        const int64_t off = (int64_t)ch0 * 32;
+        const int64_t len = std::min<int64_t>((int64_t)(ch1 - ch0) * 32, F - off);
+        if (len <= 0) return;
+        const unsigned bytes = (unsigned)(len & ~15LL);
+        for (int i = tid; i < tile_n; i += blockDim.x) {
+            const int64_t e = e0 + i;
+            if (e < k.N && bytes)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(k.x + e * F + off),
+                             "r"(bytes) : "memory");
+        }
+    };
+
     int64_t it = 0;
     int64_t t = cid;
+    prefetch_l2(t);
+    prefetch_l2(t + n_clusters);
     if (t < n_tiles) transpose(t, 0);
     cluster.sync();
+    constexpr int S = 32 / kTG;
+    const int slot = lane / kTG, g = lane % kTG;
     for (; t < n_tiles; t += n_clusters, ++it) {
         const int buf = (int)(it & 1);
         const uint32_t *xt = buf ? xt1 : xt0;
+        prefetch_l2(t + 2 * (int64_t)n_clusters);
         for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
-        const int64_t tn = t + n_clusters;
-        if (tn < n_tiles) transpose(tn, buf ^ 1);
         __syncthreads();
         // ---- evaluate the local rules: lane = (rule slot, group)
-        constexpr int S = 32 / kTG;
-        const int slot = lane / kTG, g = lane % kTG;
         for (int rc = warp; rc * S < rloc; rc += nwarps) {
             const int r = rc * S + slot;
             const int rr = r < rloc ? r : 0;  // idle lanes still join the votes
@@ -343,6 +361,9 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
             int32_t *dst = cluster.map_shared_rank(inbox, b);
             dst[((buf * kCS + rank) * 32) * K + rem] = part[i];
         }
+        // ---- next tile's X^T (its raw rows were prefetched into L2)
+        const int64_t tn = t + n_clusters;
+        if (tn < n_tiles) transpose(tn, buf ^ 1);
         cluster.sync();
         // ---- finalize the 32 examples of block `rank`
         if (warp == 0) {
