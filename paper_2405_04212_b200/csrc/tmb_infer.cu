@@ -184,6 +184,7 @@ struct InferCK {
     unsigned int *bad_input;
     int vec_ok;
     int rloc_max;
+    int dbg;  // bit0: skip eval, bit1: skip transpose (timing experiments only)
 };
 
 __device__ __forceinline__ uint32_t pack8(unsigned long long q) {
@@ -308,43 +309,56 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     prefetch_l2(t + n_clusters);
     if (t < n_tiles) transpose(t, 0);
     cluster.sync();
-    constexpr int S = 32 / kTG;
-    const int slot = lane / kTG, g = lane % kTG;
     for (; t < n_tiles; t += n_clusters, ++it) {
         const int buf = (int)(it & 1);
         const uint32_t *xt = buf ? xt1 : xt0;
         prefetch_l2(t + 2 * (int64_t)n_clusters);
         for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
         __syncthreads();
-        // ---- evaluate the local rules: lane = (rule slot, group)
-        for (int rc = warp; rc * S < rloc; rc += nwarps) {
-            const int r = rc * S + slot;
+        // ---- evaluate the local rules: one lane per rule; an include code
+        //      reads the 16-byte X^T row of its feature = 128 examples
+        const uint4 *xrow = reinterpret_cast<const uint4 *>(xt);
+        for (int rc = warp; rc * 32 < rloc && !(k.dbg & 1); rc += nwarps) {
+            const int r = rc * 32 + lane;
             const int rr = r < rloc ? r : 0;  // idle lanes still join the votes
-            uint32_t acc = r < rloc ? 0xFFFFFFFFu : 0u;
-            {
-                const uint4 h0 = heads[rr * 2], h1 = heads[rr * 2 + 1];
-                const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+            const uint32_t live = r < rloc ? 0xFFFFFFFFu : 0u;
+            uint32_t a0 = live, a1 = live, a2 = live, a3 = live;
+            const uint4 h0 = heads[rr * 2], h1 = heads[rr * 2 + 1];
+            const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const uint32_t c0 = hw[q] & 0xFFFFu, c1 = hw[q] >> 16;
-                    const uint32_t x0 = xt[(c0 >> 1) * kTG + g] ^ (0u - (c0 & 1u));
-                    const uint32_t x1 = xt[(c1 >> 1) * kTG + g] ^ (0u - (c1 & 1u));
-                    acc &= x0 & x1;
-                    if ((q & 1) && !__any_sync(0xffffffffu, acc)) break;
+            for (int q = 0; q < 8; ++q) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint32_t c = hh ? (hw[q] >> 16) : (hw[q] & 0xFFFFu);
+                    const uint4 x = xrow[c >> 1];
+                    const uint32_t m = 0u - (c & 1u);
+                    a0 &= x.x ^ m;
+                    a1 &= x.y ^ m;
+                    a2 &= x.z ^ m;
+                    a3 &= x.w ^ m;
                 }
+                if ((q & 1) && !__any_sync(0xffffffffu, a0 | a1 | a2 | a3)) break;
             }
-            if (acc && r < rloc) {
+            if ((a0 | a1 | a2 | a3) && r < rloc) {
                 const int rg = r0 + r;
-                for (int q = __ldg(&k.tail_ptr[rg]), qe = __ldg(&k.tail_ptr[rg + 1]); q < qe && acc; ++q) {
+                for (int q = __ldg(&k.tail_ptr[rg]), qe = __ldg(&k.tail_ptr[rg + 1]);
+                     q < qe && (a0 | a1 | a2 | a3); ++q) {
                     const uint32_t c = __ldg(&k.tails[q]);
-                    acc &= xt[(c >> 1) * kTG + g] ^ (0u - (c & 1u));
+                    const uint4 x = xrow[c >> 1];
+                    const uint32_t m = 0u - (c & 1u);
+                    a0 &= x.x ^ m;
+                    a1 &= x.y ^ m;
+                    a2 &= x.z ^ m;
+                    a3 &= x.w ^ m;
                 }
-                if (acc) {
-                    const int32_t *wr = k.w + (size_t)rg * K;
+                const int32_t *wr = k.w + (size_t)rg * K;
+#pragma unroll
+                for (int gq = 0; gq < kTG; ++gq) {
+                    uint32_t acc = gq == 0 ? a0 : gq == 1 ? a1 : gq == 2 ? a2 : a3;
                     while (acc) {
                         const int b = __ffs(acc) - 1;
                         acc &= acc - 1;
-                        int32_t *dst = part + (g * 32 + b) * K;
+                        int32_t *dst = part + (gq * 32 + b) * K;
                         for (int kk = 0; kk < K; ++kk) {
                             const int32_t wv = __ldg(&wr[kk]);
                             if (wv) atomicAdd(&dst[kk], wv);
@@ -363,7 +377,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         }
         // ---- next tile's X^T (its raw rows were prefetched into L2)
         const int64_t tn = t + n_clusters;
-        if (tn < n_tiles) transpose(tn, buf ^ 1);
+        if (tn < n_tiles && !(k.dbg & 2)) transpose(tn, buf ^ 1);
         cluster.sync();
         // ---- finalize the 32 examples of block `rank`
         if (warp == 0) {
@@ -410,6 +424,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
                                 unsigned long long *correct, cudaStream_t st, bool *launched);
 
 int g_force_generic_infer = 0;
+int g_infer_dbg = 0;
 
 int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, int64_t *pred,
                  const int64_t *labels, unsigned long long *correct, cudaStream_t st) {
@@ -469,6 +484,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     k.labels = labels; k.correct = correct; k.bad_input = g_bad_flag;
     k.vec_ok = (r->F % 16 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
     k.rloc_max = (int)rloc_max;
+    k.dbg = g_infer_dbg;
     const void *fn = (const void *)k_infer_cluster;
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int threads = 512;
@@ -674,6 +690,10 @@ int tmb_set_option(const char *name, int64_t value) {
     if (!name) return fail(TMB_E_INVALID, "set_option: NULL name");
     if (std::string(name) == "infer.force_generic") {
         g_force_generic_infer = (int)value;
+        return TMB_OK;
+    }
+    if (std::string(name) == "infer.debug_skip") {  // timing experiments only
+        g_infer_dbg = (int)value;
         return TMB_OK;
     }
     return fail(TMB_E_INVALID, std::string("set_option: unknown option ") + name);

@@ -1,0 +1,31 @@
+"""Time the C3 inference kernel with eval / transpose phases disabled (timing
+experiment: which phase bounds the kernel)."""
+import sys
+import torch
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+import paper_2405_04212_b200 as tmb  # noqa: E402
+from paper_2405_04212_b200 import _lib, datasets  # noqa: E402
+
+tmb.runtime.require_device()
+N = 1 << 22
+m = datasets.inference_model(model_seed=11)
+bank = tmb.DenseClauseBank(tmb.Config(n_literals=4096, n_clauses=10000, n_classes=10, s=2.0,
+                                      threshold=100))
+bank.states[:] = m.states
+bank.weights[:] = m.weights
+model = tmb.CompiledModel.from_bank(bank)
+x = bench.c3_inputs_device(N, 0)
+pred = torch.empty(N, dtype=torch.int64, device="cuda")
+for mode, name in ((0, "full"), (1, "skip eval"), (2, "skip transpose"), (3, "skip both")):
+    _lib.call("tmb_set_option", b"infer.debug_skip", mode)
+    for _ in range(2):
+        model.infer_device(x, pred_dev=pred)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(3):
+        model.infer_device(x, pred_dev=pred)
+    b.record()
+    torch.cuda.synchronize()
+    print(f"{name:15s} {a.elapsed_time(b) / 3:8.2f} ms")
+_lib.call("tmb_set_option", b"infer.debug_skip", 0)
