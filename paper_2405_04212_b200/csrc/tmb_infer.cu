@@ -531,6 +531,57 @@ int check_bad_input(cudaStream_t st) {
 
 using namespace tmb;
 
+
+// Build the 16-code heads (and CSR tails) of every rule.  A conjunction is
+// order-independent, so within every 32-rule chunk that one warp of the
+// cluster kernel evaluates together (chunks restart at each CTA's rule-slice
+// boundary), the includes placed at head position q are chosen greedily so
+// the 32 X^T rows read at that step spread over the 8 shared-memory bank
+// quads (row f occupies quad f mod 8): fewer bank conflicts, same result.
+static void balance_heads(const std::vector<int64_t> &ptr, const std::vector<uint32_t> &inc,
+                          int64_t R, int64_t F, std::vector<uint16_t> &heads,
+                          std::vector<int32_t> &tptr, std::vector<uint16_t> &tails) {
+    std::vector<std::vector<uint32_t>> left((size_t)R);
+    for (int64_t i = 0; i < R; ++i) left[i].assign(inc.begin() + ptr[i], inc.begin() + ptr[i + 1]);
+    for (int rank = 0; rank < kCS; ++rank) {
+        const int64_t s0 = rank * R / kCS, s1 = (rank + 1) * R / kCS;
+        for (int64_t c0 = s0; c0 < s1; c0 += 32) {
+            const int64_t c1 = std::min<int64_t>(c0 + 32, s1);
+            for (int q = 0; q < 16; ++q) {
+                int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                // rules with fewer remaining choices pick first
+                std::vector<int64_t> order;
+                for (int64_t i = c0; i < c1; ++i) order.push_back(i);
+                std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+                    return left[a].size() < left[b].size();
+                });
+                for (int64_t i : order) {
+                    auto &L = left[i];
+                    if (L.empty()) {  // padding code reads the all-ones row F
+                        cnt[(F) & 7]++;
+                        continue;
+                    }
+                    size_t best = 0;
+                    int bc = 1 << 30;
+                    for (size_t j = 0; j < L.size(); ++j) {
+                        const int qd = (int)((L[j] >> 1) & 7);
+                        if (cnt[qd] < bc) { bc = cnt[qd]; best = j; }
+                    }
+                    heads[(size_t)i * 16 + q] = (uint16_t)L[best];
+                    cnt[(L[best] >> 1) & 7]++;
+                    L[best] = L.back();
+                    L.pop_back();
+                }
+            }
+        }
+    }
+    for (int64_t i = 0; i < R; ++i) {
+        std::sort(left[i].begin(), left[i].end());
+        for (uint32_t c : left[i]) tails.push_back((uint16_t)c);
+        tptr[i + 1] = (int32_t)tails.size();
+    }
+}
+
 static int upload_rules(const std::vector<int64_t> &ptr, const std::vector<uint32_t> &inc,
                         const std::vector<int32_t> &w, int64_t K, int64_t F, int negations,
                         tmb_rules **out) {
@@ -563,14 +614,7 @@ static int upload_rules(const std::vector<int64_t> &ptr, const std::vector<uint3
         std::vector<uint16_t> heads((size_t)r->R * 16, (uint16_t)(F << 1));
         std::vector<int32_t> tptr((size_t)r->R + 1, 0);
         std::vector<uint16_t> tails;
-        for (int64_t i = 0; i < r->R; ++i) {
-            const int64_t a = ptr[i], b = ptr[i + 1];
-            for (int64_t q = a; q < b; ++q) {
-                if (q - a < 16) heads[(size_t)i * 16 + (q - a)] = (uint16_t)inc[q];
-                else tails.push_back((uint16_t)inc[q]);
-            }
-            tptr[i + 1] = (int32_t)tails.size();
-        }
+        balance_heads(ptr, inc, r->R, F, heads, tptr, tails);
         if ((rc = check_cuda(cudaMalloc(&r->heads, 2 * heads.size()), "cudaMalloc")) ||
             (rc = check_cuda(cudaMalloc(&r->tail_ptr, 4 * tptr.size()), "cudaMalloc")) ||
             (rc = check_cuda(cudaMalloc(&r->tails, 2 * std::max<size_t>(tails.size(), 1)), "cudaMalloc"))) {
