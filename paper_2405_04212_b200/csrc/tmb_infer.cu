@@ -191,6 +191,24 @@ __device__ __forceinline__ uint32_t pack8(unsigned long long q) {
     return (uint32_t)(((q & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56);
 }
 
+// 4 bytes of 0/1 -> 4 bits (bit t = byte t)
+__device__ __forceinline__ uint32_t pack4(uint32_t w) {
+    return ((w & 0x01010101u) * 0x01020408u) >> 24;
+}
+
+// 8x8 bit-matrix transpose: byte i = row i (bit t = column t) -> byte t =
+// column t (bit i = row i)
+__device__ __forceinline__ unsigned long long transpose8x8(unsigned long long x) {
+    unsigned long long t;
+    t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+    x = x ^ t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+    x = x ^ t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+    x = x ^ t ^ (t << 28);
+    return x;
+}
+
 // up to 8 feature bytes starting at column f (bounds-checked against F)
 __device__ __forceinline__ unsigned long long load8_tail(const uint8_t *src, int64_t f, int64_t F) {
     unsigned long long v = 0;
@@ -247,41 +265,69 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     unsigned long long hits = 0;
 
     // transpose this CTA's feature quarter of tile `t` into buffer `buf` of
-    // every CTA in the cluster
+    // every CTA in the cluster.  Unit = 32 examples (one group) x 128
+    // features: 8 coalesced 16-byte loads per lane (4 rows x 128 B per
+    // instruction), byte->bit packing, two in-register 8x8 bit transposes and
+    // a 4-lane byte exchange leave each lane with 4 finished X^T words.
+    const int64_t qf0 = (int64_t)ch0 * 32;
+    const int64_t qf1 = std::min<int64_t>((int64_t)ch1 * 32, F);
+    const int nblk = (int)((qf1 - qf0 + 127) / 128);
     auto transpose = [&](int64_t t, int buf) {
         const int64_t e0 = t * tile_n;
         uint32_t *mine = buf ? xt1 : xt0;
-        const int units = (ch1 - ch0) * kTG;
+        const int j = lane >> 3, c16 = lane & 7;
+        const int units = nblk * kTG;
         for (int u = warp; u < units; u += nwarps) {
             const int g = u % kTG;
-            const int c = ch0 + u / kTG;
-            const int64_t e = e0 + 32 * g + lane;
-            const int64_t f0 = (int64_t)c * 32;
-            unsigned long long q0 = 0, q1 = 0, q2 = 0, q3 = 0;
-            if (e < k.N) {
-                const uint8_t *src = k.x + e * F + f0;
-                if (k.vec_ok && f0 + 32 <= F) {
-                    const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(src));
-                    const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(src) + 1);
-                    q0 = ((unsigned long long)a.y << 32) | a.x;
-                    q1 = ((unsigned long long)a.w << 32) | a.z;
-                    q2 = ((unsigned long long)b.y << 32) | b.x;
-                    q3 = ((unsigned long long)b.w << 32) | b.z;
-                } else {
-                    q0 = load8_tail(src, f0, F);
-                    q1 = load8_tail(src + 8, f0 + 8, F);
-                    q2 = load8_tail(src + 16, f0 + 16, F);
-                    q3 = load8_tail(src + 24, f0 + 24, F);
-                }
-            }
-            bad |= (uint32_t)(((q0 | q1 | q2 | q3) & 0xFEFEFEFEFEFEFEFEull) != 0);
-            const uint32_t row = pack8(q0) | (pack8(q1) << 8) | (pack8(q2) << 16) |
-                                 (pack8(q3) << 24);
-            const uint32_t col = warp_transpose32(row, lane);  // feature f0+lane, 32 examples
-            if (f0 + lane < F) {
-                const size_t idx = (size_t)(f0 + lane) * kTG + g;
+            const int64_t fb = qf0 + (int64_t)(u / kTG) * 128 + 16 * c16;  // my 16 features
+            uint32_t v[8];
 #pragma unroll
-                for (int p = 0; p < kCS; ++p) cluster.map_shared_rank(mine, p)[idx] = col;
+            for (int i = 0; i < 8; ++i) {
+                const int64_t e = e0 + 32 * g + 8 * j + i;
+                uint4 w = make_uint4(0, 0, 0, 0);
+                if (e < k.N && fb < qf1) {
+                    const uint8_t *src = k.x + e * F + fb;
+                    if (k.vec_ok && fb + 16 <= F) {
+                        w = __ldcs(reinterpret_cast<const uint4 *>(src));
+                    } else {
+                        uint32_t b4[4] = {0, 0, 0, 0};
+                        for (int bb = 0; bb < 16; ++bb)
+                            if (fb + bb < F) b4[bb >> 2] |= (uint32_t)src[bb] << (8 * (bb & 3));
+                        w = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+                    }
+                }
+                bad |= (w.x | w.y | w.z | w.w) & 0xFEFEFEFEu;
+                v[i] = pack4(w.x) | (pack4(w.y) << 4) | (pack4(w.z) << 8) | (pack4(w.w) << 12);
+            }
+            unsigned long long lo = 0, hi = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                lo |= (unsigned long long)(v[i] & 0xFFu) << (8 * i);
+                hi |= (unsigned long long)(v[i] >> 8) << (8 * i);
+            }
+            lo = transpose8x8(lo);
+            hi = transpose8x8(hi);
+            const uint32_t R0 = (uint32_t)lo, R1 = (uint32_t)(lo >> 32);
+            const uint32_t R2 = (uint32_t)hi, R3 = (uint32_t)(hi >> 32);
+            uint32_t recv[4];
+#pragma unroll
+            for (int sft = 0; sft < 4; ++sft) {
+                const int d = j ^ sft;
+                const uint32_t send = d == 0 ? R0 : d == 1 ? R1 : d == 2 ? R2 : R3;
+                recv[sft] = sft ? __shfl_xor_sync(0xffffffffu, send, 8 * sft) : send;
+            }
+#pragma unroll
+            for (int kq = 0; kq < 4; ++kq) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int sft = 0; sft < 4; ++sft)
+                    word |= ((recv[sft] >> (8 * kq)) & 0xFFu) << (8 * (j ^ sft));
+                const int64_t f = fb - 16 * c16 + 16 * c16 + 4 * j + kq;
+                if (f < qf1) {
+                    const size_t idx = (size_t)f * kTG + g;
+#pragma unroll
+                    for (int p = 0; p < kCS; ++p) cluster.map_shared_rank(mine, p)[idx] = word;
+                }
             }
         }
     };
