@@ -191,6 +191,38 @@ __device__ __forceinline__ uint32_t pack8(unsigned long long q) {
     return (uint32_t)(((q & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56);
 }
 
+// ---- mbarrier / bulk-copy helpers (shared::cta / shared::cluster, sm_90+)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *mb, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t *mb, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *mb, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done) : "r"(smem_u32(mb)), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, uint32_t src_cta,
+                                                  uint32_t bytes, uint32_t mbar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst_cluster), "r"(src_cta), "r"(bytes), "r"(mbar_cluster) : "memory");
+}
+
 // 4 bytes of 0/1 -> 4 bits (bit t = byte t)
 __device__ __forceinline__ uint32_t pack4(uint32_t w) {
     return ((w & 0x01010101u) * 0x01020408u) >> 24;
@@ -244,6 +276,8 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     uint32_t *xt1 = xt0 + (size_t)xrows * kTG;
     int32_t *part = reinterpret_cast<int32_t *>(xt1 + (size_t)xrows * kTG);   // [32*kTG][K]
     int32_t *inbox = part + 32 * kTG * K;                                     // [2][kCS][32][K]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(
+        reinterpret_cast<uintptr_t>(inbox + 2 * kCS * 32 * K + 3) & ~(uintptr_t)7);  // [2]
 
     const int r0 = (int)((int64_t)rank * k.R / kCS), r1 = (int)((int64_t)(rank + 1) * k.R / kCS);
     const int rloc = r1 - r0;
@@ -323,11 +357,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
                 for (int sft = 0; sft < 4; ++sft)
                     word |= ((recv[sft] >> (8 * kq)) & 0xFFu) << (8 * (j ^ sft));
                 const int64_t f = fb - 16 * c16 + 16 * c16 + 4 * j + kq;
-                if (f < qf1) {
-                    const size_t idx = (size_t)f * kTG + g;
-#pragma unroll
-                    for (int p = 0; p < kCS; ++p) cluster.map_shared_rank(mine, p)[idx] = word;
-                }
+                if (f < qf1) mine[(size_t)f * kTG + g] = word;
             }
         }
     };
@@ -349,12 +379,51 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         }
     };
 
+    // rows [0, F) of every tile come from the four quarters; my peers send
+    // (F - my quarter) rows x 16 B into each of my buffers per use
+    const uint32_t my_bytes = (uint32_t)((qf1 > qf0 ? qf1 - qf0 : 0) * 16);
+    const uint32_t expect_bytes = (uint32_t)(F * 16) - my_bytes;
+    uint32_t parity[2] = {0, 0};
+    // share this CTA's freshly transposed quarter of buffer `buf` with peers
+    auto publish = [&](int buf) {
+        __syncthreads();
+        if (tid == 0 && my_bytes) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t src = smem_u32((buf ? xt1 : xt0) + (size_t)qf0 * kTG);
+            for (int p = 0; p < kCS; ++p) {
+                if (p == rank) continue;
+                bulk_copy_to_peer(mapa_u32(src, p), src, my_bytes, mapa_u32(smem_u32(&mbar[buf]), p));
+            }
+        }
+    };
+    auto await_tile = [&](int buf) {
+        if (expect_bytes) mbar_wait(&mbar[buf], parity[buf]);
+        parity[buf] ^= 1u;
+        __syncthreads();
+        // re-arm for this buffer's next use (before the cluster barrier that
+        // lets peers write into it again)
+        if (tid == 0 && expect_bytes) mbar_arm(&mbar[buf], expect_bytes);
+    };
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (expect_bytes) {
+            mbar_arm(&mbar[0], expect_bytes);
+            mbar_arm(&mbar[1], expect_bytes);
+        }
+    }
+    cluster.sync();
+
     int64_t it = 0;
     int64_t t = cid;
     prefetch_l2(t);
     prefetch_l2(t + n_clusters);
-    if (t < n_tiles) transpose(t, 0);
-    cluster.sync();
+    if (t < n_tiles) {
+        transpose(t, 0);
+        publish(0);
+        await_tile(0);
+    }
     for (; t < n_tiles; t += n_clusters, ++it) {
         const int buf = (int)(it & 1);
         const uint32_t *xt = buf ? xt1 : xt0;
@@ -423,8 +492,12 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         }
         // ---- next tile's X^T (its raw rows were prefetched into L2)
         const int64_t tn = t + n_clusters;
-        if (tn < n_tiles && !(k.dbg & 2)) transpose(tn, buf ^ 1);
+        if (tn < n_tiles && !(k.dbg & 2)) {
+            transpose(tn, buf ^ 1);
+            publish(buf ^ 1);
+        }
         cluster.sync();
+        if (tn < n_tiles && !(k.dbg & 2)) await_tile(buf ^ 1);
         // ---- finalize the 32 examples of block `rank`
         if (warp == 0) {
             const int64_t e = t * tile_n + 32 * rank + lane;
@@ -522,7 +595,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const int64_t rloc_max = (r->R + kCS - 1) / kCS;
     const size_t smem = 32 * (size_t)rloc_max + 2 * 4 * (size_t)(r->F + 1) * kTG +
-                        4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K;
+                        4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K + 32;
     if (smem > (size_t)max_smem) return TMB_OK;  // generic kernel instead
     InferCK k;
     k.x = x; k.N = N; k.F = r->F; k.heads = r->heads; k.tail_ptr = r->tail_ptr; k.tails = r->tails;
