@@ -276,8 +276,10 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     uint32_t *xt1 = xt0 + (size_t)xrows * kTG;
     int32_t *part = reinterpret_cast<int32_t *>(xt1 + (size_t)xrows * kTG);   // [32*kTG][K]
     int32_t *inbox = part + 32 * kTG * K;                                     // [2][kCS][32][K]
+    int32_t *iflag = inbox + 2 * kCS * 32 * K;                                // [2][kCS]
+    int32_t *dirty = iflag + 2 * kCS;                                         // [kTG]
     uint64_t *mbar = reinterpret_cast<uint64_t *>(
-        reinterpret_cast<uintptr_t>(inbox + 2 * kCS * 32 * K + 3) & ~(uintptr_t)7);  // [2]
+        reinterpret_cast<uintptr_t>(dirty + kTG + 3) & ~(uintptr_t)7);       // [2]
 
     const int r0 = (int)((int64_t)rank * k.R / kCS), r1 = (int)((int64_t)(rank + 1) * k.R / kCS);
     const int rloc = r1 - r0;
@@ -314,24 +316,35 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         for (int u = warp; u < units; u += nwarps) {
             const int g = u % kTG;
             const int64_t fb = qf0 + (int64_t)(u / kTG) * 128 + 16 * c16;  // my 16 features
-            uint32_t v[8];
+            uint4 w[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 8; ++i) {  // all eight loads in flight first
                 const int64_t e = e0 + 32 * g + 8 * j + i;
-                uint4 w = make_uint4(0, 0, 0, 0);
+                w[i] = make_uint4(0, 0, 0, 0);
                 if (e < k.N && fb < qf1) {
                     const uint8_t *src = k.x + e * F + fb;
                     if (k.vec_ok && fb + 16 <= F) {
-                        w = __ldcs(reinterpret_cast<const uint4 *>(src));
+                        w[i] = *reinterpret_cast<const uint4 *>(src);
                     } else {
-                        uint32_t b4[4] = {0, 0, 0, 0};
-                        for (int bb = 0; bb < 16; ++bb)
-                            if (fb + bb < F) b4[bb >> 2] |= (uint32_t)src[bb] << (8 * (bb & 3));
-                        w = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+                        uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+                        for (int bb = 0; bb < 16; ++bb) {
+                            if (fb + bb >= F) break;
+                            const uint32_t byte = (uint32_t)src[bb] << (8 * (bb & 3));
+                            if (bb < 4) b0 |= byte;
+                            else if (bb < 8) b1 |= byte;
+                            else if (bb < 12) b2 |= byte;
+                            else b3 |= byte;
+                        }
+                        w[i] = make_uint4(b0, b1, b2, b3);
                     }
                 }
-                bad |= (w.x | w.y | w.z | w.w) & 0xFEFEFEFEu;
-                v[i] = pack4(w.x) | (pack4(w.y) << 4) | (pack4(w.z) << 8) | (pack4(w.w) << 12);
+            }
+            uint32_t v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                bad |= (w[i].x | w[i].y | w[i].z | w[i].w) & 0xFEFEFEFEu;
+                v[i] = pack4(w[i].x) | (pack4(w[i].y) << 4) | (pack4(w[i].z) << 8) |
+                       (pack4(w[i].w) << 12);
             }
             unsigned long long lo = 0, hi = 0;
 #pragma unroll
@@ -429,6 +442,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         const uint32_t *xt = buf ? xt1 : xt0;
         prefetch_l2(t + 2 * (int64_t)n_clusters);
         for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
+        if (tid < kTG) dirty[tid] = 0;
         __syncthreads();
         // ---- evaluate the local rules: one lane per rule; an include code
         //      reads the 16-byte X^T row of its feature = 128 examples
@@ -470,6 +484,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
 #pragma unroll
                 for (int gq = 0; gq < kTG; ++gq) {
                     uint32_t acc = gq == 0 ? a0 : gq == 1 ? a1 : gq == 2 ? a2 : a3;
+                    if (acc) dirty[gq] = 1;
                     while (acc) {
                         const int b = __ffs(acc) - 1;
                         acc &= acc - 1;
@@ -483,13 +498,16 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
             }
         }
         __syncthreads();
-        // ---- push partial sums of example block b to CTA b's inbox
+        // ---- push partial sums of example block b to CTA b's inbox; blocks
+        //      where no local rule fired only send their (zero) flag
         for (int i = tid; i < 32 * kTG * K; i += blockDim.x) {
             const int b = i / (32 * K);  // example block == owning CTA
+            if (!dirty[b]) continue;
             const int rem = i - b * 32 * K;
             int32_t *dst = cluster.map_shared_rank(inbox, b);
             dst[((buf * kCS + rank) * 32) * K + rem] = part[i];
         }
+        if (tid < kCS) cluster.map_shared_rank(iflag, tid)[buf * kCS + rank] = dirty[tid];
         // ---- next tile's X^T (its raw rows were prefetched into L2)
         const int64_t tn = t + n_clusters;
         if (tn < n_tiles && !(k.dbg & 2)) {
@@ -507,7 +525,8 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
                 for (int kk = 0; kk < K; ++kk) {
                     int32_t sum = 0;
 #pragma unroll
-                    for (int p = 0; p < kCS; ++p) sum += inbox[((buf * kCS + p) * 32 + lane) * K + kk];
+                    for (int p = 0; p < kCS; ++p)
+                        if (iflag[buf * kCS + p]) sum += inbox[((buf * kCS + p) * 32 + lane) * K + kk];
                     if (kk == 0 || sum > bv) { bv = sum; best = kk; }
                     if (k.votes) k.votes[e * K + kk] = (int64_t)sum;
                 }
@@ -595,7 +614,8 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const int64_t rloc_max = (r->R + kCS - 1) / kCS;
     const size_t smem = 32 * (size_t)rloc_max + 2 * 4 * (size_t)(r->F + 1) * kTG +
-                        4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K + 32;
+                        4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K +
+                        4 * (2 * kCS + kTG) + 32;
     if (smem > (size_t)max_smem) return TMB_OK;  // generic kernel instead
     InferCK k;
     k.x = x; k.N = N; k.F = r->F; k.heads = r->heads; k.tail_ptr = r->tail_ptr; k.tails = r->tails;
