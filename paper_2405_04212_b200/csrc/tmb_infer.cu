@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     // bulk L2 prefetch of this CTA's feature quarter of tile `t` (one TMA
     // bulk-prefetch per example row; no registers, no shared memory)
     auto prefetch_l2 = [&](int64_t t) {
-        if (t >= n_tiles || !k.vec_ok) return;
+        if (t >= n_tiles || !k.vec_ok || (k.dbg & 4)) return;
         const int64_t e0 = t * tile_n;
         const int64_t off = (int64_t)ch0 * 32;
         const int64_t len = std::min<int64_t>((int64_t)(ch1 - ch0) * 32, F - off);

@@ -17,7 +17,7 @@ bank.weights[:] = m.weights
 model = tmb.CompiledModel.from_bank(bank)
 x = bench.c3_inputs_device(N, 0)
 pred = torch.empty(N, dtype=torch.int64, device="cuda")
-for mode, name in ((0, "full"), (1, "skip eval"), (2, "skip transpose"), (3, "skip both")):
+for mode, name in ((0, "full"), (1, "skip eval"), (2, "skip transpose"), (3, "skip both"), (4, "no prefetch"), (7, "skip all")):
     _lib.call("tmb_set_option", b"infer.debug_skip", mode)
     for _ in range(2):
         model.infer_device(x, pred_dev=pred)
