@@ -223,6 +223,13 @@ __device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, uint32_t
         ::"r"(dst_cluster), "r"(src_cta), "r"(bytes), "r"(mbar_cluster) : "memory");
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
 // 4 bytes of 0/1 -> 4 bits (bit t = byte t)
 __device__ __forceinline__ uint32_t pack4(uint32_t w) {
     return ((w & 0x01010101u) * 0x01020408u) >> 24;
@@ -446,20 +453,21 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         __syncthreads();
         // ---- evaluate the local rules: one lane per rule; an include code
         //      reads the 16-byte X^T row of its feature = 128 examples
-        const uint4 *xrow = reinterpret_cast<const uint4 *>(xt);
+        const uint32_t xaddr = smem_u32(xt);  // explicit shared-window loads
+        const uint32_t haddr = smem_u32(heads);
         for (int rc = warp; rc * 32 < rloc && !(k.dbg & 1); rc += nwarps) {
             const int r = rc * 32 + lane;
             const int rr = r < rloc ? r : 0;  // idle lanes still join the votes
             const uint32_t live = r < rloc ? 0xFFFFFFFFu : 0u;
             uint32_t a0 = live, a1 = live, a2 = live, a3 = live;
-            const uint4 h0 = heads[rr * 2], h1 = heads[rr * 2 + 1];
+            const uint4 h0 = lds128(haddr + rr * 32), h1 = lds128(haddr + rr * 32 + 16);
             const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     const uint32_t c = hh ? (hw[q] >> 16) : (hw[q] & 0xFFFFu);
-                    const uint4 x = xrow[c >> 1];
+                    const uint4 x = lds128(xaddr + (c >> 1) * 16);
                     const uint32_t m = 0u - (c & 1u);
                     a0 &= x.x ^ m;
                     a1 &= x.y ^ m;
@@ -473,7 +481,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
                 for (int q = __ldg(&k.tail_ptr[rg]), qe = __ldg(&k.tail_ptr[rg + 1]);
                      q < qe && (a0 | a1 | a2 | a3); ++q) {
                     const uint32_t c = __ldg(&k.tails[q]);
-                    const uint4 x = xrow[c >> 1];
+                    const uint4 x = lds128(xaddr + (c >> 1) * 16);
                     const uint32_t m = 0u - (c & 1u);
                     a0 &= x.x ^ m;
                     a1 &= x.y ^ m;
