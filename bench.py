@@ -203,6 +203,7 @@ def bench_c2_train(args, rank, world, local):
     c0 = sess.block_counters.cpu().numpy().copy()
     fb0 = sess.fb_counter
     stats0 = sess.stats_dict()
+    snap = sess.snapshot()  # e2e replays the same epochs from this state
     launches0 = _lib.launch_count()
     orders = [sess.next_order().astype(np.int32) for _ in range(args.steps)]
     orders_dev = [torch.from_numpy(o).cuda() for o in orders]
@@ -235,7 +236,9 @@ def bench_c2_train(args, rank, world, local):
 
     # ---- end to end through the public API with host buffers (per step:
     # H2D of the epoch's features+labels from pinned memory, device packing,
-    # host shuffle, the fused kernel, D2H of the trained model)
+    # host shuffle, the fused kernel, D2H of the trained model).  Replays the
+    # timed epochs from the same model state, so the work is identical.
+    sess.restore(snap)
     xp = torch.from_numpy(np.ascontiguousarray(tx)).pin_memory()
     yp = torch.from_numpy(np.ascontiguousarray(ty.astype(np.int32))).pin_memory()
     st_host = torch.empty(sess.states.shape, dtype=torch.int8).pin_memory()

@@ -740,7 +740,9 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     const int Ppad = ((P + 127) / 128) * 128;
     const int sms = sm_count();
     const int64_t work = (int64_t)C * Ppad;
-    if (n_cta <= 0) n_cta = work <= 65536 ? 1 : (work <= (64LL << 20) ? 16 : sms);
+    // auto: one CTA for tiny banks, else one CTA per SM (grid mode measured
+    // faster than the 16-CTA cluster mode on the configs[1] shapes)
+    if (n_cta <= 0) n_cta = work <= 65536 ? 1 : sms;
     n_cta = std::max(1, std::min(n_cta, C));
     if (n_cta > 16 && n_cta > sms) n_cta = sms;
     const bool cluster = n_cta <= 16;

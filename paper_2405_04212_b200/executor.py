@@ -157,6 +157,19 @@ class DenseTrainSession:
         self.N = int(x.shape[0])
         del xd
 
+    def snapshot(self):
+        """Device copy of the full training state (model + RNG counters)."""
+        return (self.states.clone(), self.weights.clone(), self.block_counters.clone(),
+                self.fb_counter, self.shuffle_rng.counter)
+
+    def restore(self, snap):
+        st, w, bc, fb, sh = snap
+        self.states.copy_(st)
+        self.weights.copy_(w)
+        self.block_counters.copy_(bc)
+        self.fb_counter = fb
+        self.shuffle_rng.counter = sh
+
     def next_order(self) -> np.ndarray:
         return shuffle_permutation(self.N, self.shuffle_rng)
 
