@@ -259,6 +259,14 @@ int tmb_sparse_destroy(tmb_sparse *sp);
 int tmb_sparse_train(tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
                      const int32_t *labels, const int32_t *order, int64_t n_steps,
                      uint64_t fb_counter, tmb_train_stats *stats, void *stream);
+/* SparseClauseBank.apply_feedback (sparse.py:241-249) for a single-block
+ * bank with explicit outputs / update flags (device uint8 [C]) and the
+ * block's event counter; active: device int32 [n_active] sorted literals.
+ * The advanced counter is returned in *counter_out (host; synchronises). */
+int tmb_sparse_feedback(tmb_sparse *sp, const int32_t *active, int64_t n_active,
+                        const uint8_t *outputs, int64_t label, int64_t negative,
+                        const uint8_t *ut, const uint8_t *un, uint64_t stream_seed,
+                        uint64_t counter, uint64_t *counter_out, void *stream);
 /* Copy the model out: lens int32 [C], lits int32 [C*slab], states int8
  * [C*slab], weights int32 [C,K], block counters uint64 [n_blocks] (device
  * pointers).  Returns TMB_E_UNSUPPORTED if a slab overflowed. */
@@ -270,6 +278,10 @@ int tmb_sparse_set(tmb_sparse *sp, const int32_t *lens, const int32_t *lits,
 /* Inference-mode votes / predictions for CSR documents (device). */
 int tmb_sparse_infer(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
                      int64_t N, int64_t *votes, int64_t *pred, void *stream);
+/* Inference-mode clause outputs (sparse.py:123-138 with EvalMode.INFERENCE)
+ * for CSR documents: device uint8 [N, C]. */
+int tmb_sparse_outputs(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
+                       int64_t N, uint8_t *outputs, void *stream);
 
 #ifdef __cplusplus
 }

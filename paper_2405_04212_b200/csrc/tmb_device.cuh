@@ -63,6 +63,47 @@ __device__ __forceinline__ int type_ii(int st, int lit, int out) {
     return (out && !lit && st < 0) ? st + 1 : st;
 }
 
+// ---- partitions (executor.py:36-47): block of clause c, block start, CTA ranges
+__host__ __device__ __forceinline__ int block_of(int c, int C, int nb) {
+    int base = C / nb, extra = C % nb;
+    int big = extra * (base + 1);
+    return c < big ? c / (base + 1) : extra + (c - big) / base;
+}
+__host__ __device__ __forceinline__ int block_begin(int b, int C, int nb) {
+    int base = C / nb, extra = C % nb;
+    return b * base + (b < extra ? b : extra);
+}
+__host__ __device__ __forceinline__ int cta_begin(int r, int C, int n_cta) {
+    return (int)((int64_t)r * C / n_cta);
+}
+
+// ---- fence-free cross-CTA vote all-reduce (see tmb_train.cu)
+constexpr long long kVoteBias = 1LL << 31;  // |partial votes of one CTA| < 2^31
+__device__ __forceinline__ void red_relaxed_add_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acquire() {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_relaxed_v2u64(const unsigned long long *p) {
+    ulonglong2 r;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
+    return r;
+}
+
+
+
 int dev_pack_literals(const uint8_t *x, int64_t N, int64_t cols, int negations, int64_t P,
                       uint32_t *out, cudaStream_t st);
 int dev_build_masks(const int8_t *states, int64_t C, int64_t P, uint32_t *masks,

@@ -1,32 +1,965 @@
-// tmb_sparse.cu -- SparseTM (sparse.py:78-256) on the device.  Placeholder
-// until the sparse kernels land: every entry point reports TMB_E_UNSUPPORTED.
+// tmb_sparse.cu -- SparseTM (sparse.py:78-256) on the device.
+//
+// Model: per clause a sorted list of (literal int32, state int8) pairs in a
+// fixed-capacity slab (double-buffered: an event writes the other buffer),
+// weights int32 [C, K], per-block event counters.  Documents are CSR
+// (indptr int64 [N+1], indices int32 sorted per row).
+//
+// Training (executor.py:275-340 with the sparse banks): one cooperative grid
+// launch per run of examples with the dense trainer's fence-free vote
+// exchange and flag scan (tmb_train.cu), and per event a warp-parallel merge:
+//   Type I  over stored U active     (sparse.py:162-190), draw per literal INDEX
+//   Type II over stored U candidates (sparse.py:192-210), output 1 only
+//   keep rule (sparse.py:212-220): drop st <= floor; an insertion (literal not
+//   stored) is dropped iff >= capacity pairs were emitted before it.  Every
+//   condition-true element before position i is emitted unless it is a
+//   dropped insertion, and insertions are only dropped once that count has
+//   reached the capacity, so the sequential rule equals the parallel prefix
+//   rule  keep_i = cond_i && (stored_i || #cond_true_before_i < capacity).
+// Inference: inverted index literal -> clauses, one warp per document.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
 #include "tmb_common.cuh"
+#include "tmb_device.cuh"
+
+namespace tmb {
+
+constexpr int kMaxActive = 4096;  // active literals of one document held in smem
+constexpr int kMaxIns = 512;      // Type II insertions per event (per-warp smem)
+
+struct SparseK {
+    int C, K, n_blocks, n_cta, cmax, fmax_words, bmax, slab;
+    int64_t budget, T;
+    int floor_, smax, capacity;  // capacity < 0: None
+    FbParams fp;
+    uint64_t fb_seed, fb_counter0;
+    int64_t n_steps;
+    const int64_t *indptr;
+    const int32_t *indices;
+    const int32_t *labels, *order;
+    const int32_t *cands;
+    int64_t n_cand;
+    int32_t *lits0, *lits1;  // [C][slab]
+    int8_t *sts0, *sts1;
+    int32_t *len;
+    uint8_t *cur;
+    int32_t *weights;
+    uint64_t *block_counters;
+    const uint64_t *block_seeds;
+    unsigned long long *rec;  // [n_steps][2]
+    unsigned int *overflow;
+    tmb_train_stats *stats;
+    // explicit-flag single-example mode (SparseClauseBank.apply_feedback)
+    const uint8_t *x_ut, *x_un, *x_out;
+    int x_label, x_neg;
+    uint64_t x_counter, x_seed;
+};
+
+__device__ __forceinline__ int32_t *lits_of(const SparseK &k, int c, int which) {
+    return (which ? k.lits1 : k.lits0) + (size_t)c * k.slab;
+}
+__device__ __forceinline__ int8_t *sts_of(const SparseK &k, int c, int which) {
+    return (which ? k.sts1 : k.sts0) + (size_t)c * k.slab;
+}
+
+// number of elements < v in sorted a[0..n)
+__device__ __forceinline__ int count_below(const int32_t *a, int n, int32_t v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ bool contains(const int32_t *a, int n, int32_t v) {
+    const int p = count_below(a, n, v);
+    return p < n && a[p] == v;
+}
+
+// warp-wide exclusive scan of a 0/1 flag; *tot = warp total
+__device__ __forceinline__ int warp_excl(int f, int lane, int *tot) {
+    int x = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    *tot = __shfl_sync(0xffffffffu, x, 31);
+    return x - f;
+}
+
+// Type I on clause c (one warp): domain = stored U active, merged by a merge
+// path (stored first on ties; the active duplicate of a stored literal is
+// skipped).  Returns the new length in the other buffer, -1 on slab overflow.
+__device__ int event_type_i(const SparseK &k, int c, int src, const int32_t *act, int n_act,
+                            int out, uint64_t sk, int lane, uint64_t &ndraws) {
+    const int32_t *L = lits_of(k, c, src);
+    const int8_t *S = sts_of(k, c, src);
+    int32_t *DL = lits_of(k, c, src ^ 1);
+    int8_t *DS = sts_of(k, c, src ^ 1);
+    const int n = k.len[c];
+    const int total = n + n_act;
+    int emitted = 0, cond_before = 0;
+    for (int base = 0; base < total; base += 32) {
+        const int d = base + lane;  // merged position
+        bool valid = d < total;
+        int32_t lit = 0;
+        int st = k.floor_;
+        bool stored = false, active = false;
+        if (valid) {
+            // i = number of stored elements among the first d merged ones
+            int lo = max(0, d - n_act), hi = min(d, n);
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (L[mid] <= act[d - 1 - mid]) lo = mid + 1;
+                else hi = mid;
+            }
+            const int i = lo, a = d - lo;
+            if (i < n && (a >= n_act || L[i] <= act[a])) {
+                lit = L[i];
+                st = S[i];
+                stored = true;
+                active = a < n_act && act[a] == lit;
+            } else {
+                lit = act[a];
+                active = true;
+                if (i > 0 && L[i - 1] == lit) valid = false;  // duplicate
+            }
+        }
+        bool cond = false;
+        if (valid) {
+            const uint64_t m = mix64(sk + kGolden * (uint64_t)(uint32_t)lit) >> 11;
+            ++ndraws;
+            if (out == 1 && active) {
+                if ((k.fp.boost || m < k.fp.t_inc) && st < k.smax) st += 1;
+            } else if (m < k.fp.t_dec && st > k.floor_) {
+                st -= 1;
+            }
+            cond = st > k.floor_;
+        }
+        int ctot, ktot;
+        const int cpre = warp_excl(cond ? 1 : 0, lane, &ctot) + cond_before;
+        const bool keep = cond && (stored || k.capacity < 0 || cpre < k.capacity);
+        const int kpre = warp_excl(keep ? 1 : 0, lane, &ktot) + emitted;
+        if (keep && kpre < k.slab) {
+            DL[kpre] = lit;
+            DS[kpre] = (int8_t)st;
+        }
+        emitted += ktot;
+        cond_before += ctot;
+    }
+    return emitted <= k.slab ? emitted : -1;
+}
+
+// Type II, output 1 (one warp): every stored pair survives (states only move
+// up from above the floor); inserted = the first non-stored, non-active
+// candidates x with #stored(<x) + #inserted(<x) < capacity, at floor + 1.
+__device__ int event_type_ii(const SparseK &k, int c, int src, const int32_t *act, int n_act,
+                             int32_t *ins_buf, int lane) {
+    const int32_t *L = lits_of(k, c, src);
+    const int8_t *S = sts_of(k, c, src);
+    int32_t *DL = lits_of(k, c, src ^ 1);
+    int8_t *DS = sts_of(k, c, src ^ 1);
+    const int n = k.len[c];
+    const int cap = k.capacity;
+    int ins = 0;
+    bool overflow = false;
+    for (int64_t cb = 0; cb < k.n_cand; cb += 32) {
+        const int64_t ci = cb + lane;
+        int32_t x = 0;
+        bool cand = false;
+        int below = 0;
+        if (ci < k.n_cand) {
+            x = __ldg(&k.cands[ci]);
+            below = count_below(L, n, x);
+            cand = !(below < n && L[below] == x) && !contains(act, n_act, x);
+        }
+        int ctot, ktot;
+        const int cpre = warp_excl(cand ? 1 : 0, lane, &ctot) + ins;
+        const bool keep = cand && (cap < 0 || below + cpre < cap);
+        const unsigned fail = __ballot_sync(0xffffffffu, cand && !keep);
+        const int kpre = warp_excl(keep ? 1 : 0, lane, &ktot) + ins;
+        if (keep) {
+            if (kpre < kMaxIns) ins_buf[kpre] = x;
+            else overflow = true;
+        }
+        ins += ktot;
+        if (fail) break;  // monotone: every later candidate fails as well
+    }
+    __syncwarp();
+    if (__any_sync(0xffffffffu, overflow) || n + ins > k.slab) return -1;
+    // stored pairs: shifted by the insertions below them
+    for (int i = lane; i < n; i += 32) {
+        const int32_t lit = L[i];
+        int st = S[i];
+        if (st < 0 && !contains(act, n_act, lit)) st += 1;
+        const int pos = i + count_below(ins_buf, ins, lit);
+        DL[pos] = lit;
+        DS[pos] = (int8_t)st;
+    }
+    // insertions: shifted by the stored pairs below them
+    for (int m = lane; m < ins; m += 32) {
+        const int32_t x = ins_buf[m];
+        const int pos = m + count_below(L, n, x);
+        DL[pos] = x;
+        DS[pos] = (int8_t)(k.floor_ + 1);
+    }
+    __syncwarp();
+    return n + ins;
+}
+
+struct SSmem {
+    int32_t *act;       // [kMaxActive] current document
+    int32_t *ins;       // [nwarps][kMaxIns]
+    uint32_t *ut_bits, *un_bits;
+    int32_t *word_cum, *info, *work, *misc;
+    uint64_t *sk_t, *sk_n, *blk_ctr, *blk_seed, *draw_t, *draw_n;
+    long long *vsum;
+};
+
+__host__ __device__ inline size_t salign(size_t x) { return (x + 15) / 16 * 16; }
+
+__host__ __device__ inline size_t sparse_smem(const SparseK &k, int nwarps, char *base, SSmem *s) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char * {
+        off = salign(off);
+        char *p = base ? base + off : nullptr;
+        off += bytes;
+        return p;
+    };
+    SSmem t;
+    t.act = (int32_t *)take(4 * kMaxActive);
+    t.ins = (int32_t *)take(4 * (size_t)kMaxIns * nwarps);
+    t.ut_bits = (uint32_t *)take(4 * k.fmax_words);
+    t.un_bits = (uint32_t *)take(4 * k.fmax_words);
+    t.word_cum = (int32_t *)take(4 * (k.fmax_words + 1));
+    t.info = (int32_t *)take(4 * k.cmax);
+    t.work = (int32_t *)take(4 * k.cmax);
+    t.misc = (int32_t *)take(4 * 8);
+    t.sk_t = (uint64_t *)take(8 * k.cmax);
+    t.sk_n = (uint64_t *)take(8 * k.cmax);
+    t.blk_ctr = (uint64_t *)take(8 * (k.bmax + 1));
+    t.blk_seed = (uint64_t *)take(8 * (k.bmax + 1));
+    t.draw_t = (uint64_t *)take(8 * 32 * (size_t)k.fmax_words);
+    t.draw_n = (uint64_t *)take(8 * 32 * (size_t)k.fmax_words);
+    t.vsum = (long long *)take(8 * 2);
+    if (s) *s = t;
+    return salign(off);
+}
+
+enum : int { SI_TEV = 1, SI_NEV = 2, SI_T1 = 4, SI_N1 = 8, SI_OUT = 16 };
+
+// One cooperative grid; CTA b owns clauses [c0, c1).  k.x_ut != nullptr runs
+// a single example with explicit outputs / flags / counter (bank-level API).
+__global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    SSmem s;
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = nthr >> 5;
+    sparse_smem(k, nwarps, smem_raw, &s);
+    const int rank = blockIdx.x, n_cta = k.n_cta, C = k.C, K = k.K;
+    const int c0 = cta_begin(rank, C, n_cta), c1 = cta_begin(rank + 1, C, n_cta);
+    const int cown = c1 - c0;
+    const int b0 = block_of(c0, C, k.n_blocks), b1 = block_of(c1 - 1, C, k.n_blocks);
+    const int fs = block_begin(b0, C, k.n_blocks), fe = block_begin(b1 + 1, C, k.n_blocks);
+    const int fsa = fs & ~31;
+    const int nfw = (fe - fsa + 31) >> 5;
+    const bool explicit_flags = k.x_ut != nullptr;
+    for (int i = tid; i <= b1 - b0; i += nthr) {
+        s.blk_ctr[i] = explicit_flags ? k.x_counter : k.block_counters[b0 + i];
+        s.blk_seed[i] = explicit_flags ? k.x_seed : k.block_seeds[b0 + i];
+    }
+    __syncthreads();
+    uint64_t n_draws = 0, n_events = 0, n_t1 = 0, n_t2 = 0;
+    const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
+    for (int64_t it = 0; it < k.n_steps; ++it) {
+        const int ex = explicit_flags ? 0 : __ldg(&k.order[it]);
+        const int64_t a0 = __ldg(&k.indptr[ex]), a1 = __ldg(&k.indptr[ex + 1]);
+        const int n_act = (int)(a1 - a0 < kMaxActive ? a1 - a0 : kMaxActive);
+        if (a1 - a0 > kMaxActive && tid == 0) atomicOr(k.overflow, 2u);
+        for (int q = tid; q < n_act; q += nthr) s.act[q] = __ldg(&k.indices[a0 + q]);
+        const uint64_t fbc = k.fb_counter0 + (uint64_t)it * step_draws;
+        int label, neg;
+        if (explicit_flags) {
+            label = k.x_label;
+            neg = k.x_neg;
+        } else {
+            label = __ldg(&k.labels[ex]);
+            const double u = u01_from53(draw53(k.fb_seed, fbc));
+            neg = label + 1 + (int)(u * (double)(K - 1));
+            if (neg >= K) neg -= K;
+        }
+        if (tid == 0) s.misc[0] = 0;
+        __syncthreads();
+        // 1. training-mode outputs of own clauses (sparse.py:123-138), warp
+        //    per clause: included = stored with state >= 0, all must be active
+        for (int j = warp; j < cown; j += nwarps) {
+            const int c = c0 + j;
+            int outv;
+            if (explicit_flags) {
+                outv = k.x_out[c];
+            } else {
+                const int src = k.cur[c];
+                const int32_t *L = lits_of(k, c, src);
+                const int8_t *S = sts_of(k, c, src);
+                const int n = k.len[c];
+                int n_inc = 0;
+                bool viol = false;
+                for (int q = lane; q < n; q += 32) {
+                    if (S[q] >= 0) {
+                        ++n_inc;
+                        if (!contains(s.act, n_act, L[q])) viol = true;
+                    }
+                }
+                n_inc = __reduce_add_sync(0xffffffffu, n_inc);
+                viol = __any_sync(0xffffffffu, viol);
+                outv = n_inc == 0 ? 1 : ((n_inc > k.budget || viol) ? 0 : 1);
+            }
+            if (lane == 0) s.info[j] = outv ? SI_OUT : 0;
+        }
+        __syncthreads();
+        uint64_t t_t = 0, t_n = 0;
+        if (!explicit_flags) {
+            // 2. partial sums of the label / negative class, fence-free exchange
+            if (warp < 2) {
+                const int kk = warp == 0 ? label : neg;
+                long long v = 0;
+                for (int j = lane; j < cown; j += 32)
+                    if (s.info[j] & SI_OUT) v += k.weights[(size_t)(c0 + j) * K + kk];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0)
+                    red_relaxed_add_u64(&k.rec[it * 2 + warp],
+                                        (1ull << 40) + (unsigned long long)(v + kVoteBias));
+            }
+            for (int idx = tid; idx < nfw * 32; idx += nthr) {
+                const int j = fsa + idx;
+                s.draw_t[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
+                s.draw_n[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
+            }
+            if (tid == 0) {
+                const unsigned long long want = (unsigned long long)n_cta;
+                ulonglong2 p;
+                do {
+                    p = ld_relaxed_v2u64(&k.rec[it * 2]);
+                } while ((p.x >> 40) != want || (p.y >> 40) != want);
+                const long long bias = (long long)n_cta * kVoteBias;
+                s.vsum[0] = (long long)(p.x & ((1ull << 40) - 1)) - bias;
+                s.vsum[1] = (long long)(p.y & ((1ull << 40) - 1)) - bias;
+            }
+            __syncthreads();
+            const long long T = k.T, vl = s.vsum[0], vn = s.vsum[1];
+            const long long cl = vl < -T ? -T : (vl > T ? T : vl);
+            const long long cn2 = vn < -T ? -T : (vn > T ? T : vn);
+            t_t = prob_threshold((double)(T - cl) / (2.0 * (double)T));
+            t_n = prob_threshold((double)(T + cn2) / (2.0 * (double)T));
+        }
+        // 3. update-flag bitmaps over [fs, fe)
+        for (int idx = tid; idx < nfw * 32; idx += nthr) {
+            const int j = fsa + idx;
+            const bool valid = j >= fs && j < fe;
+            bool bt, bn;
+            if (explicit_flags) {
+                bt = valid && k.x_ut[j];
+                bn = valid && k.x_un[j];
+            } else {
+                bt = valid && s.draw_t[idx] < t_t;
+                bn = valid && s.draw_n[idx] < t_n;
+            }
+            const unsigned wt = __ballot_sync(0xffffffffu, bt);
+            const unsigned wn = __ballot_sync(0xffffffffu, bn);
+            if (lane == 0) {
+                s.ut_bits[idx >> 5] = wt;
+                s.un_bits[idx >> 5] = wn;
+            }
+        }
+        __syncthreads();
+        // 4. warp 0: event prefix, ordinals, types, weights, work list
+        if (warp == 0) {
+            int carry = 0;
+            for (int base = 0; base < nfw; base += 32) {
+                const int w = base + lane;
+                const int v = w < nfw ? __popc(s.ut_bits[w]) + __popc(s.un_bits[w]) : 0;
+                int x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (w < nfw) s.word_cum[w] = carry + x - v;
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) s.word_cum[nfw] = carry;
+            __syncwarp();
+            auto cum = [&](int x) -> int {
+                const int q = (x - fsa) >> 5, r = (x - fsa) & 31;
+                int v = s.word_cum[q];
+                if (r) {
+                    const unsigned lo = (1u << r) - 1u;
+                    v += __popc(s.ut_bits[q] & lo) + __popc(s.un_bits[q] & lo);
+                }
+                return v;
+            };
+            for (int j = lane; j < cown; j += 32) {
+                const int c = c0 + j;
+                const int q = (c - fsa) >> 5, r = (c - fsa) & 31;
+                const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
+                int info = s.info[j] & SI_OUT;
+                if (t_ev || n_ev) {
+                    const int bi = block_of(c, C, k.n_blocks) - b0;
+                    const uint64_t ord =
+                        s.blk_ctr[bi] + (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
+                    const uint64_t bseed = s.blk_seed[bi];
+                    const bool out = info & SI_OUT;
+                    int32_t *w = k.weights + (size_t)c * K;
+                    const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
+                    if (t_ev) {
+                        info |= SI_TEV | (t1 ? SI_T1 : 0);
+                        s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
+                        ++n_events;
+                        if (t1) ++n_t1; else if (out) ++n_t2;
+                    }
+                    if (n_ev) {
+                        const uint64_t o2 = ord + (t_ev ? 1 : 0);
+                        info |= SI_NEV | (n1 ? SI_N1 : 0);
+                        s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
+                        ++n_events;
+                        if (n1) ++n_t1; else if (out) ++n_t2;
+                    }
+                    if (out) {
+                        if (t_ev) w[label] += 1;
+                        if (n_ev) w[neg] -= 1;
+                    }
+                    if ((t_ev && ((info & SI_T1) || out)) || (n_ev && ((info & SI_N1) || out)))
+                        s.work[atomicAdd(&s.misc[0], 1)] = j;
+                }
+                s.info[j] = info;
+            }
+            __syncwarp();
+            for (int bi = lane; bi <= b1 - b0; bi += 32) {
+                const int bs = block_begin(b0 + bi, C, k.n_blocks);
+                const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
+                s.blk_ctr[bi] += (uint64_t)(cum(be) - cum(bs));
+            }
+        }
+        __syncthreads();
+        // 5. events: warp per clause of the work list, target then negative
+        const int n_work = s.misc[0];
+        for (int wi = warp; wi < n_work; wi += nwarps) {
+            const int j = s.work[wi];
+            const int c = c0 + j;
+            const int info = s.info[j];
+            const int out = (info & SI_OUT) ? 1 : 0;
+            int src = k.cur[c];
+            for (int ev = 0; ev < 2; ++ev) {
+                const bool has = ev == 0 ? (info & SI_TEV) : (info & SI_NEV);
+                if (!has) continue;
+                const bool t1 = ev == 0 ? (info & SI_T1) : (info & SI_N1);
+                int nl;
+                if (t1) {
+                    nl = event_type_i(k, c, src, s.act, n_act, out, ev == 0 ? s.sk_t[j] : s.sk_n[j],
+                                      lane, n_draws);
+                } else if (out) {
+                    nl = event_type_ii(k, c, src, s.act, n_act, s.ins + (size_t)warp * kMaxIns, lane);
+                } else {
+                    continue;  // Type II on output 0: no-op (window still consumed)
+                }
+                if (nl < 0) {
+                    if (lane == 0) atomicOr(k.overflow, 1u);
+                    nl = 0;
+                }
+                __syncwarp();
+                src ^= 1;
+                if (lane == 0) {
+                    k.len[c] = nl;
+                    k.cur[c] = (uint8_t)src;
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    }
+    for (int bi = tid; bi <= b1 - b0; bi += nthr) {
+        const int b = b0 + bi;
+        const int last = block_begin(b + 1, C, k.n_blocks) - 1;
+        if (last >= c0 && last < c1) k.block_counters[b] = s.blk_ctr[bi];
+    }
+    if (k.stats) {
+        for (int o = 16; o; o >>= 1) {
+            n_draws += __shfl_xor_sync(0xffffffffu, n_draws, o);
+            n_events += __shfl_xor_sync(0xffffffffu, n_events, o);
+            n_t1 += __shfl_xor_sync(0xffffffffu, n_t1, o);
+            n_t2 += __shfl_xor_sync(0xffffffffu, n_t2, o);
+        }
+        if (lane == 0) {
+            atomicAdd((unsigned long long *)&k.stats->draws, (unsigned long long)n_draws);
+            atomicAdd((unsigned long long *)&k.stats->events, (unsigned long long)n_events);
+            atomicAdd((unsigned long long *)&k.stats->type_i, (unsigned long long)n_t1);
+            atomicAdd((unsigned long long *)&k.stats->type_ii, (unsigned long long)n_t2);
+        }
+        if (rank == 0 && tid == 0)
+            atomicAdd((unsigned long long *)&k.stats->examples, (unsigned long long)k.n_steps);
+    }
+}
+
+// ---------------------------------------------------------- inference --
+// Inverted index: post_ptr [n_literals + 1] (int32) -> post_clause [n_post];
+// n_inc[c] = included literals of clause c (0: never fires in inference).
+struct SparseInferK {
+    const int64_t *indptr;
+    const int32_t *indices;
+    int64_t N;
+    const int32_t *post_ptr, *post_clause, *n_inc;
+    int64_t n_literals;
+    const int32_t *weights;
+    int C, K;
+    int64_t *votes, *pred;
+    const int32_t *outputs_mode;  // unused
+    uint8_t *outputs;             // optional [N, C] inference-mode outputs
+    unsigned int *overflow;
+};
+
+constexpr int kMaxHits = 1024;  // clause hits of one document (per-warp smem)
+
+__global__ void __launch_bounds__(256) k_sparse_infer(SparseInferK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    int32_t *hits = reinterpret_cast<int32_t *>(smem_raw) + (size_t)warp * kMaxHits;
+    long long *vacc = reinterpret_cast<long long *>(
+        reinterpret_cast<int32_t *>(smem_raw) + (size_t)nwarps * kMaxHits) + (size_t)warp * 32;
+    for (int64_t d = (int64_t)blockIdx.x * nwarps + warp; d < k.N; d += (int64_t)gridDim.x * nwarps) {
+        const int64_t a0 = k.indptr[d], a1 = k.indptr[d + 1];
+        // gather clause hits of the document's active literals
+        int nh = 0;
+        bool ovf = false;
+        for (int64_t base = a0; base < a1; base += 32) {
+            const int64_t q = base + lane;
+            int p0 = 0, p1 = 0;
+            if (q < a1) {
+                const int32_t lit = k.indices[q];
+                if (lit >= 0 && lit < k.n_literals) {
+                    p0 = k.post_ptr[lit];
+                    p1 = k.post_ptr[lit + 1];
+                }
+            }
+            int tot;
+            int x = p1 - p0;
+            int incl = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            tot = __shfl_sync(0xffffffffu, incl, 31);
+            const int off = nh + incl - x;
+            for (int m = 0; m < x; ++m) {
+                if (off + m < kMaxHits) hits[off + m] = k.post_clause[p0 + m];
+                else ovf = true;
+            }
+            nh += tot;
+        }
+        __syncwarp();
+        if (__any_sync(0xffffffffu, ovf)) {
+            if (lane == 0) atomicOr(k.overflow, 4u);
+            nh = kMaxHits;
+        }
+        // clause c fires iff it was hit n_inc[c] times (distinct includes);
+        // count with the first occurrence of every clause
+        for (int kk = lane; kk < 32; kk += 32) vacc[kk] = 0;
+        __syncwarp();
+        for (int m = lane; m < nh; m += 32) {
+            const int32_t c = hits[m];
+            int cnt = 0;
+            bool first = true;
+            for (int q = 0; q < nh; ++q) {
+                const int32_t o = hits[q];
+                if (o == c) {
+                    ++cnt;
+                    if (q < m) first = false;
+                }
+            }
+            if (first && cnt == k.n_inc[c]) {
+                for (int kk = 0; kk < k.K; ++kk) {
+                    const int32_t wv = k.weights[(size_t)c * k.K + kk];
+                    if (wv) atomicAdd((unsigned long long *)&vacc[kk], (unsigned long long)(long long)wv);
+                }
+                if (k.outputs) k.outputs[d * k.C + c] = 1;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            int best = 0;
+            for (int kk = 0; kk < k.K; ++kk) {
+                if (k.votes) k.votes[d * k.K + kk] = vacc[kk];
+                if (vacc[kk] > vacc[best]) best = kk;
+            }
+            if (k.pred) k.pred[d] = best;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace tmb
 
 using namespace tmb;
 
 struct tmb_sparse {
-    int unused;
+    tmb_sparse_cfg cfg;
+    int n_cta = 0, threads = 512;
+    size_t smem = 0;
+    int32_t *lits[2] = {nullptr, nullptr};
+    int8_t *sts[2] = {nullptr, nullptr};
+    int32_t *len = nullptr;
+    uint8_t *cur = nullptr;
+    int32_t *weights = nullptr;
+    uint64_t *block_counters = nullptr, *block_seeds = nullptr;
+    int32_t *cands = nullptr;
+    int64_t n_cand = 0;
+    unsigned long long *rec = nullptr;
+    int64_t rec_cap = 0;
+    unsigned int *overflow = nullptr;
+    SparseK k{};
 };
 
+namespace {
+
+int sparse_fill_k(tmb_sparse *sp) {
+    const tmb_sparse_cfg &c = sp->cfg;
+    SparseK &k = sp->k;
+    k.C = (int)c.n_clauses;
+    k.K = (int)c.n_classes;
+    k.n_blocks = (int)c.n_blocks;
+    k.n_cta = sp->n_cta;
+    k.slab = (int)c.slab;
+    k.budget = c.budget;
+    k.T = c.threshold;
+    k.floor_ = c.floor_;
+    k.smax = c.state_max;
+    k.capacity = c.capacity;
+    k.fp = make_fb_params(c.s, c.boost, c.floor_, c.state_max);
+    k.fb_seed = derive_stream(c.seed, 0xFEED);
+    int cmax = 0, fmax = 0, bmax = 0;
+    for (int b = 0; b < k.n_cta; ++b) {
+        const int c0 = cta_begin(b, k.C, k.n_cta), c1 = cta_begin(b + 1, k.C, k.n_cta);
+        cmax = std::max(cmax, c1 - c0);
+        const int b0 = block_of(c0, k.C, k.n_blocks), b1 = block_of(c1 - 1, k.C, k.n_blocks);
+        const int fs = block_begin(b0, k.C, k.n_blocks), fe = block_begin(b1 + 1, k.C, k.n_blocks);
+        fmax = std::max(fmax, (fe - (fs & ~31) + 31) / 32);
+        bmax = std::max(bmax, b1 - b0 + 1);
+    }
+    k.cmax = cmax;
+    k.fmax_words = fmax;
+    k.bmax = bmax;
+    k.lits0 = sp->lits[0];
+    k.lits1 = sp->lits[1];
+    k.sts0 = sp->sts[0];
+    k.sts1 = sp->sts[1];
+    k.len = sp->len;
+    k.cur = sp->cur;
+    k.weights = sp->weights;
+    k.block_counters = sp->block_counters;
+    k.block_seeds = sp->block_seeds;
+    k.cands = sp->cands;
+    k.n_cand = sp->n_cand;
+    k.overflow = sp->overflow;
+    return TMB_OK;
+}
+
+int sparse_launch(tmb_sparse *sp, SparseK &k, cudaStream_t st) {
+    void *args[] = {&k};
+    TMB_CUDA(cudaLaunchCooperativeKernel((const void *)k_sparse_train, dim3(sp->n_cta),
+                                         dim3(sp->threads), args, sp->smem, st));
+    TMB_LAUNCHED();
+    return TMB_OK;
+}
+
+int sparse_check_overflow(tmb_sparse *sp, cudaStream_t st) {
+    unsigned v = 0;
+    TMB_CUDA(cudaMemcpyAsync(&v, sp->overflow, 4, cudaMemcpyDeviceToHost, st));
+    TMB_CUDA(cudaStreamSynchronize(st));
+    if (v) {
+        cudaMemsetAsync(sp->overflow, 0, 4, st);
+        return fail(TMB_E_UNSUPPORTED,
+                    std::string("sparse: ") +
+                        ((v & 1) ? "a clause list exceeded the device slab; raise cfg.slab" :
+                         (v & 2) ? "a document has more than 4096 active literals" :
+                                   "a document hit more than 1024 clause postings"));
+    }
+    return TMB_OK;
+}
+
+}  // namespace
+
 extern "C" {
-int tmb_sparse_create(const tmb_sparse_cfg *, const int32_t *, int64_t, tmb_sparse **) {
-    return fail(TMB_E_UNSUPPORTED, "sparse: not built yet");
+
+int tmb_sparse_create(const tmb_sparse_cfg *cfg, const int32_t *candidates, int64_t n_candidates,
+                      tmb_sparse **out) {
+    int rc = require_device();
+    if (rc) return rc;
+    if (!cfg || !out || cfg->n_clauses < 1 || cfg->n_classes < 2 || cfg->n_blocks < 1 ||
+        cfg->n_blocks > cfg->n_clauses || !(cfg->s > 1.0) || cfg->slab < 8 ||
+        cfg->slab > (1 << 20) || cfg->floor_ >= 0 || n_candidates < 0 ||
+        (n_candidates > 0 && !candidates) || cfg->n_literals >= (1LL << 31))
+        return fail(TMB_E_INVALID, "sparse_create: bad arguments");
+    tmb_sparse *sp = new tmb_sparse();
+    sp->cfg = *cfg;
+    sp->cfg.slab = (cfg->slab + 15) / 16 * 16;
+    const int64_t C = cfg->n_clauses, K = cfg->n_classes, slab = sp->cfg.slab;
+    const int sms = sm_count();
+    sp->n_cta = (int)std::min<int64_t>(C, sms);
+    sp->threads = 512;
+    auto cleanup = [&](int code) {
+        tmb_sparse_destroy(sp);
+        return code;
+    };
+    for (int b = 0; b < 2; ++b) {
+        if ((rc = check_cuda(cudaMalloc(&sp->lits[b], 4 * C * slab), "cudaMalloc")) ||
+            (rc = check_cuda(cudaMalloc(&sp->sts[b], C * slab), "cudaMalloc")))
+            return cleanup(rc);
+    }
+    if ((rc = check_cuda(cudaMalloc(&sp->len, 4 * C), "cudaMalloc")) ||
+        (rc = check_cuda(cudaMalloc(&sp->cur, C), "cudaMalloc")) ||
+        (rc = check_cuda(cudaMalloc(&sp->weights, 4 * C * K), "cudaMalloc")) ||
+        (rc = check_cuda(cudaMalloc(&sp->block_counters, 8 * cfg->n_blocks), "cudaMalloc")) ||
+        (rc = check_cuda(cudaMalloc(&sp->block_seeds, 8 * cfg->n_blocks), "cudaMalloc")) ||
+        (rc = check_cuda(cudaMalloc(&sp->cands, 4 * std::max<int64_t>(n_candidates, 1)), "cudaMalloc")) ||
+        (rc = check_cuda(cudaMalloc(&sp->overflow, 4), "cudaMalloc")))
+        return cleanup(rc);
+    cudaMemset(sp->len, 0, 4 * C);
+    cudaMemset(sp->cur, 0, C);
+    cudaMemset(sp->weights, 0, 4 * C * K);
+    cudaMemset(sp->block_counters, 0, 8 * cfg->n_blocks);
+    cudaMemset(sp->overflow, 0, 4);
+    std::vector<uint64_t> seeds(cfg->n_blocks);
+    for (int64_t b = 0; b < cfg->n_blocks; ++b) seeds[b] = derive_stream(cfg->seed, (uint64_t)b);
+    cudaMemcpy(sp->block_seeds, seeds.data(), 8 * cfg->n_blocks, cudaMemcpyHostToDevice);
+    if (n_candidates)
+        cudaMemcpy(sp->cands, candidates, 4 * n_candidates, cudaMemcpyHostToDevice);
+    sp->n_cand = n_candidates;
+    if ((rc = check_cuda(cudaGetLastError(), "sparse_create"))) return cleanup(rc);
+    sparse_fill_k(sp);
+    sp->smem = sparse_smem(sp->k, sp->threads / 32, nullptr, nullptr);
+    int max_smem = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (sp->smem > (size_t)max_smem) return cleanup(fail(TMB_E_UNSUPPORTED, "sparse: smem"));
+    if ((rc = check_cuda(cudaFuncSetAttribute((const void *)k_sparse_train,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sp->smem), "cudaFuncSetAttribute")))
+        return cleanup(rc);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k_sparse_train,
+                                                  sp->threads, sp->smem);
+    if (per_sm * sms < sp->n_cta) return cleanup(fail(TMB_E_UNSUPPORTED, "sparse: co-residency"));
+    *out = sp;
+    return TMB_OK;
 }
-int tmb_sparse_destroy(tmb_sparse *) { return TMB_OK; }
-int tmb_sparse_train(tmb_sparse *, const int64_t *, const int32_t *, const int32_t *,
-                     const int32_t *, int64_t, uint64_t, tmb_train_stats *, void *) {
-    return fail(TMB_E_UNSUPPORTED, "sparse: not built yet");
+
+int tmb_sparse_destroy(tmb_sparse *sp) {
+    if (!sp) return TMB_OK;
+    for (int b = 0; b < 2; ++b) {
+        if (sp->lits[b]) cudaFree(sp->lits[b]);
+        if (sp->sts[b]) cudaFree(sp->sts[b]);
+    }
+    for (void *p : {(void *)sp->len, (void *)sp->cur, (void *)sp->weights,
+                    (void *)sp->block_counters, (void *)sp->block_seeds, (void *)sp->cands,
+                    (void *)sp->rec, (void *)sp->overflow})
+        if (p) cudaFree(p);
+    delete sp;
+    return TMB_OK;
 }
-int tmb_sparse_get(const tmb_sparse *, int32_t *, int32_t *, int8_t *, int32_t *, uint64_t *,
-                   void *) {
-    return fail(TMB_E_UNSUPPORTED, "sparse: not built yet");
+
+int tmb_sparse_train(tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
+                     const int32_t *labels, const int32_t *order, int64_t n_steps,
+                     uint64_t fb_counter, tmb_train_stats *stats, void *stream) {
+    if (!sp) return fail(TMB_E_INVALID, "sparse_train: NULL");
+    if (n_steps <= 0) return TMB_OK;
+    if (!indptr || !indices || !labels || !order) return fail(TMB_E_INVALID, "sparse_train: NULL data");
+    cudaStream_t st = as_stream(stream);
+    if (sp->rec_cap < n_steps) {
+        if (sp->rec) {
+            cudaStreamSynchronize(st);
+            cudaFree(sp->rec);
+        }
+        sp->rec = nullptr;
+        sp->rec_cap = 0;
+        TMB_CUDA(cudaMalloc(&sp->rec, 16 * (size_t)n_steps));
+        sp->rec_cap = n_steps;
+    }
+    TMB_CUDA(cudaMemsetAsync(sp->rec, 0, 16 * (size_t)n_steps, st));
+    SparseK k = sp->k;
+    k.indptr = indptr; k.indices = indices; k.labels = labels; k.order = order;
+    k.n_steps = n_steps; k.fb_counter0 = fb_counter; k.stats = stats; k.rec = sp->rec;
+    k.x_ut = k.x_un = k.x_out = nullptr;
+    int rc = sparse_launch(sp, k, st);
+    if (rc) return rc;
+    return sparse_check_overflow(sp, st);
 }
-int tmb_sparse_set(tmb_sparse *, const int32_t *, const int32_t *, const int8_t *,
-                   const int32_t *, const uint64_t *, void *) {
-    return fail(TMB_E_UNSUPPORTED, "sparse: not built yet");
+
+int tmb_sparse_feedback(tmb_sparse *sp, const int32_t *active, int64_t n_active,
+                        const uint8_t *outputs, int64_t label, int64_t negative,
+                        const uint8_t *ut, const uint8_t *un, uint64_t stream_seed,
+                        uint64_t counter, uint64_t *counter_out, void *stream) {
+    if (!sp) return fail(TMB_E_INVALID, "sparse_feedback: NULL");
+    if (sp->cfg.n_blocks != 1) return fail(TMB_E_UNSUPPORTED, "sparse_feedback: one block only");
+    if (!outputs || !ut || !un || (n_active > 0 && !active) || label < 0 ||
+        label >= sp->cfg.n_classes || negative < 0 || negative >= sp->cfg.n_classes)
+        return fail(TMB_E_INVALID, "sparse_feedback: bad arguments");
+    cudaStream_t st = as_stream(stream);
+    int64_t *dptr = nullptr;
+    TMB_CUDA(cudaMallocAsync(&dptr, 16, st));
+    int64_t hptr[2] = {0, n_active};
+    TMB_CUDA(cudaMemcpyAsync(dptr, hptr, 16, cudaMemcpyHostToDevice, st));
+    SparseK k = sp->k;
+    k.indptr = dptr;
+    k.indices = active ? active : sp->cands;
+    k.n_steps = 1;
+    k.x_ut = ut; k.x_un = un; k.x_out = outputs;
+    k.x_label = (int)label; k.x_neg = (int)negative; k.x_counter = counter;
+    k.x_seed = stream_seed;
+    k.stats = nullptr;
+    uint64_t *bc = nullptr;
+    TMB_CUDA(cudaMallocAsync(&bc, 8, st));
+    k.block_counters = bc;  // the counter comes from x_counter, result lands here
+    int rc = sparse_launch(sp, k, st);
+    uint64_t res = 0;
+    if (!rc) rc = check_cuda(cudaMemcpyAsync(&res, bc, 8, cudaMemcpyDeviceToHost, st), "copy");
+    if (!rc) rc = sparse_check_overflow(sp, st);
+    cudaFreeAsync(dptr, st);
+    cudaFreeAsync(bc, st);
+    cudaStreamSynchronize(st);
+    if (!rc && counter_out) *counter_out = res;
+    return rc;
 }
-int tmb_sparse_infer(const tmb_sparse *, const int64_t *, const int32_t *, int64_t, int64_t *,
-                     int64_t *, void *) {
-    return fail(TMB_E_UNSUPPORTED, "sparse: not built yet");
+
+int tmb_sparse_get(const tmb_sparse *sp, int32_t *lens, int32_t *lits, int8_t *states,
+                   int32_t *weights, uint64_t *block_counters, void *stream) {
+    if (!sp) return fail(TMB_E_INVALID, "sparse_get: NULL");
+    cudaStream_t st = as_stream(stream);
+    const int64_t C = sp->cfg.n_clauses, slab = sp->cfg.slab, K = sp->cfg.n_classes;
+    std::vector<uint8_t> cur(C);
+    std::vector<int32_t> len(C);
+    TMB_CUDA(cudaMemcpyAsync(cur.data(), sp->cur, C, cudaMemcpyDeviceToHost, st));
+    TMB_CUDA(cudaMemcpyAsync(len.data(), sp->len, 4 * C, cudaMemcpyDeviceToHost, st));
+    TMB_CUDA(cudaStreamSynchronize(st));
+    if (lens) TMB_CUDA(cudaMemcpyAsync(lens, sp->len, 4 * C, cudaMemcpyDeviceToDevice, st));
+    for (int64_t c = 0; c < C; ++c) {
+        const int b = cur[c];
+        if (lits && len[c])
+            TMB_CUDA(cudaMemcpyAsync(lits + c * slab, sp->lits[b] + c * slab, 4 * len[c],
+                                     cudaMemcpyDeviceToDevice, st));
+        if (states && len[c])
+            TMB_CUDA(cudaMemcpyAsync(states + c * slab, sp->sts[b] + c * slab, len[c],
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+    if (weights) TMB_CUDA(cudaMemcpyAsync(weights, sp->weights, 4 * C * K, cudaMemcpyDeviceToDevice, st));
+    if (block_counters)
+        TMB_CUDA(cudaMemcpyAsync(block_counters, sp->block_counters, 8 * sp->cfg.n_blocks,
+                                 cudaMemcpyDeviceToDevice, st));
+    return TMB_OK;
 }
+
+int tmb_sparse_set(tmb_sparse *sp, const int32_t *lens, const int32_t *lits, const int8_t *states,
+                   const int32_t *weights, const uint64_t *block_counters, void *stream) {
+    if (!sp) return fail(TMB_E_INVALID, "sparse_set: NULL");
+    cudaStream_t st = as_stream(stream);
+    const int64_t C = sp->cfg.n_clauses, slab = sp->cfg.slab, K = sp->cfg.n_classes;
+    if (lens) {
+        TMB_CUDA(cudaMemcpyAsync(sp->len, lens, 4 * C, cudaMemcpyDeviceToDevice, st));
+        TMB_CUDA(cudaMemsetAsync(sp->cur, 0, C, st));
+    }
+    if (lits) TMB_CUDA(cudaMemcpyAsync(sp->lits[0], lits, 4 * C * slab, cudaMemcpyDeviceToDevice, st));
+    if (states) TMB_CUDA(cudaMemcpyAsync(sp->sts[0], states, C * slab, cudaMemcpyDeviceToDevice, st));
+    if (weights) TMB_CUDA(cudaMemcpyAsync(sp->weights, weights, 4 * C * K, cudaMemcpyDeviceToDevice, st));
+    if (block_counters)
+        TMB_CUDA(cudaMemcpyAsync(sp->block_counters, block_counters, 8 * sp->cfg.n_blocks,
+                                 cudaMemcpyDeviceToDevice, st));
+    return TMB_OK;
 }
+
+static int sparse_infer_impl(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
+                             int64_t N, int64_t *votes, int64_t *pred, uint8_t *outputs,
+                             void *stream) {
+    if (!sp) return fail(TMB_E_INVALID, "sparse_infer: NULL");
+    if (N < 0 || (N > 0 && (!indptr || !indices))) return fail(TMB_E_INVALID, "sparse_infer: bad args");
+    if (N == 0) return TMB_OK;
+    cudaStream_t st = as_stream(stream);
+    const int64_t C = sp->cfg.n_clauses, slab = sp->cfg.slab, K = sp->cfg.n_classes;
+    const int64_t L = sp->cfg.n_literals;
+    // build the inverted index on the host from the device lists (model
+    // compile step, once per call: a few MB)
+    std::vector<uint8_t> cur(C);
+    std::vector<int32_t> len(C);
+    TMB_CUDA(cudaMemcpyAsync(cur.data(), sp->cur, C, cudaMemcpyDeviceToHost, st));
+    TMB_CUDA(cudaMemcpyAsync(len.data(), sp->len, 4 * C, cudaMemcpyDeviceToHost, st));
+    TMB_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> hl(C * slab);
+    std::vector<int8_t> hs(C * slab);
+    for (int b = 0; b < 2; ++b) {
+        std::vector<int32_t> tl(C * slab);
+        std::vector<int8_t> ts(C * slab);
+        TMB_CUDA(cudaMemcpyAsync(tl.data(), sp->lits[b], 4 * C * slab, cudaMemcpyDeviceToHost, st));
+        TMB_CUDA(cudaMemcpyAsync(ts.data(), sp->sts[b], C * slab, cudaMemcpyDeviceToHost, st));
+        TMB_CUDA(cudaStreamSynchronize(st));
+        for (int64_t c = 0; c < C; ++c)
+            if (cur[c] == b)
+                for (int q = 0; q < len[c]; ++q) {
+                    hl[c * slab + q] = tl[c * slab + q];
+                    hs[c * slab + q] = ts[c * slab + q];
+                }
+    }
+    std::vector<int32_t> n_inc(C, 0), cnt(L + 1, 0);
+    for (int64_t c = 0; c < C; ++c)
+        for (int q = 0; q < len[c]; ++q)
+            if (hs[c * slab + q] >= 0) {
+                ++n_inc[c];
+                ++cnt[hl[c * slab + q] + 1];
+            }
+    for (int64_t l = 0; l < L; ++l) cnt[l + 1] += cnt[l];
+    std::vector<int32_t> post(cnt[L]);
+    std::vector<int32_t> fillp(cnt.begin(), cnt.end() - 1);
+    for (int64_t c = 0; c < C; ++c)
+        for (int q = 0; q < len[c]; ++q)
+            if (hs[c * slab + q] >= 0) post[fillp[hl[c * slab + q]]++] = (int32_t)c;
+    int32_t *d_ptr = nullptr, *d_post = nullptr, *d_ninc = nullptr;
+    TMB_CUDA(cudaMallocAsync(&d_ptr, 4 * (L + 1), st));
+    TMB_CUDA(cudaMallocAsync(&d_post, 4 * std::max<size_t>(post.size(), 1), st));
+    TMB_CUDA(cudaMallocAsync(&d_ninc, 4 * C, st));
+    TMB_CUDA(cudaMemcpyAsync(d_ptr, cnt.data(), 4 * (L + 1), cudaMemcpyHostToDevice, st));
+    if (!post.empty())
+        TMB_CUDA(cudaMemcpyAsync(d_post, post.data(), 4 * post.size(), cudaMemcpyHostToDevice, st));
+    TMB_CUDA(cudaMemcpyAsync(d_ninc, n_inc.data(), 4 * C, cudaMemcpyHostToDevice, st));
+    SparseInferK k{};
+    k.indptr = indptr; k.indices = indices; k.N = N;
+    k.post_ptr = d_ptr; k.post_clause = d_post; k.n_inc = d_ninc; k.n_literals = L;
+    k.weights = sp->weights; k.C = (int)C; k.K = (int)K; k.votes = votes; k.pred = pred;
+    k.outputs = outputs; k.overflow = sp->overflow;
+    if (outputs) TMB_CUDA(cudaMemsetAsync(outputs, 0, (size_t)N * C, st));
+    if (K > 32) return fail(TMB_E_UNSUPPORTED, "sparse_infer: K > 32");
+    const int threads = 256;
+    const size_t smem = 4 * (size_t)kMaxHits * (threads / 32) + 8 * 32 * (threads / 32);
+    TMB_CUDA(cudaFuncSetAttribute((const void *)k_sparse_infer,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t grid = std::min<int64_t>((N + 7) / 8, (int64_t)sm_count() * 8);
+    k_sparse_infer<<<(unsigned)grid, threads, smem, st>>>(k);
+    TMB_LAUNCHED();
+    cudaFreeAsync(d_ptr, st);
+    cudaFreeAsync(d_post, st);
+    cudaFreeAsync(d_ninc, st);
+    return sparse_check_overflow(const_cast<tmb_sparse *>(sp), st);
+}
+
+int tmb_sparse_infer(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
+                     int64_t N, int64_t *votes, int64_t *pred, void *stream) {
+    return sparse_infer_impl(sp, indptr, indices, N, votes, pred, nullptr, stream);
+}
+
+int tmb_sparse_outputs(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
+                       int64_t N, uint8_t *outputs, void *stream) {
+    if (!outputs) return fail(TMB_E_INVALID, "sparse_outputs: NULL outputs");
+    return sparse_infer_impl(sp, indptr, indices, N, nullptr, nullptr, outputs, stream);
+}
+
+}  // extern "C"

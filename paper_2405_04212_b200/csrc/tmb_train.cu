@@ -54,19 +54,6 @@ struct TrainK {
     long long *trace;  // optional [n_steps][4]: negative, votes[label], votes[neg], events
 };
 
-// executor.py:36-47 partition: block of clause c and block start.
-__host__ __device__ __forceinline__ int block_of(int c, int C, int nb) {
-    int base = C / nb, extra = C % nb;
-    int big = extra * (base + 1);
-    return c < big ? c / (base + 1) : extra + (c - big) / base;
-}
-__host__ __device__ __forceinline__ int block_begin(int b, int C, int nb) {
-    int base = C / nb, extra = C % nb;
-    return b * base + (b < extra ? b : extra);
-}
-__host__ __device__ __forceinline__ int cta_begin(int r, int C, int n_cta) {
-    return (int)((int64_t)r * C / n_cta);
-}
 // CTA owning clause c (inverse of cta_begin).
 __device__ __forceinline__ int cta_of(int c, int C, int n_cta) {
     int r = (int)(((int64_t)c * n_cta + n_cta - 1) / C);
@@ -89,31 +76,6 @@ __device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-constexpr long long kVoteBias = 1LL << 31;  // |partial votes of one CTA| < 2^31
-__device__ __forceinline__ void red_relaxed_add_u64(unsigned long long *p, unsigned long long v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void fence_acquire() {
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
-__device__ __forceinline__ ulonglong2 ld_relaxed_v2u64(const unsigned long long *p) {
-    ulonglong2 r;
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
-                 : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
-    return r;
-}
-
-
 enum : int { I_TEV = 1, I_NEV = 2, I_T1 = 4, I_N1 = 8, I_OUT = 16 };
 enum : int { MODE_CLUSTER = 0, MODE_GRID = 1 };
 

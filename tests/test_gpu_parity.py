@@ -348,3 +348,123 @@ def test_facade_listing(gpu):
     assert pr.predict(ex).shape == (200,)
     cls, expl = pr.predict_and_explain(ex[0])
     assert 0 <= cls < 2 and expl.scores.shape == (24,)
+
+
+# ------------------------------------------------------------------ SparseTM
+
+def _sparse_golden_data(gpu):
+    g = golden("sparse")
+    ptr, ind = g["indptr"], g["indices"]
+    ex = [gpu.SparseExample(ind[ptr[i]:ptr[i + 1]], int(g["labels"][i]))
+          for i in range(ptr.shape[0] - 1)]
+    return g, gpu.SparseDataset(60, ex)
+
+
+def test_sparse_train_golden(gpu):
+    """SparseClauseBank training incl. capacity rule, floor/evict, candidate
+    domain and 3 clause blocks: bit-exact lists, states, weights, votes."""
+    g, ds = _sparse_golden_data(gpu)
+    for i in range(3):
+        seed, cap, floor, nb = (int(v) for v in g[f"r{i}_cfg"])
+        cfg = gpu.Config(n_literals=60, n_clauses=10, n_classes=2, s=float(g[f"r{i}_s"]),
+                         threshold=6, negated_literals_enabled=False, seed=seed,
+                         sparse_capacity=None if cap < 0 else cap, sparse_floor=floor,
+                         n_blocks=nb)
+        m = gpu.train(cfg, ds, n_epochs=2).model
+        lens = np.array([a.size for a in m.clause_literals])
+        assert np.array_equal(lens, g[f"r{i}_lens"]), i
+        if lens.sum():
+            assert np.array_equal(np.concatenate(m.clause_literals), g[f"r{i}_lits"])
+            assert np.array_equal(np.concatenate(m.clause_states), g[f"r{i}_sts"])
+        assert np.array_equal(m.weights, g[f"r{i}_weights"])
+        assert np.array_equal(m.batch_votes(ds.examples), g[f"r{i}_votes"])
+
+
+def test_sparse_dense_equivalence(gpu):
+    """test_acceptance.py:66-96 oracle: with the floor at the dense clamp and
+    no capacity, the sparse engine replays the dense engine exactly."""
+    rs = np.random.default_rng(11)
+    ex = []
+    for _ in range(100):
+        k = int(rs.integers(3, 12))
+        ex.append(gpu.SparseExample(np.sort(rs.choice(50, size=k, replace=False)),
+                                    int(rs.integers(0, 2))))
+    data = gpu.SparseDataset(50, ex)
+    floor = -15
+    cfg = gpu.Config(n_literals=50, n_clauses=16, n_classes=2, s=2.5, threshold=10, seed=99,
+                     n_blocks=4, negated_literals_enabled=False, init_state=floor,
+                     state_min=floor, sparse_floor=floor)
+    for epochs in (1, 3):
+        dense = gpu.train(cfg, data.densify(), n_epochs=epochs).model
+        sparse = gpu.train(cfg, data, n_epochs=epochs).model
+        assert np.array_equal(dense.weights, sparse.weights)
+        for j in range(cfg.n_clauses):
+            lits = sparse.clause_literals[j]
+            assert np.array_equal(dense.states[j, lits], sparse.clause_states[j])
+            assert np.all(dense.states[j, np.setdiff1d(np.arange(50), lits)] == floor)
+        xs, _ = data.densify()
+        assert np.array_equal(gpu.dataset_votes(dense, (xs, None)), sparse.batch_votes(ex))
+
+
+def test_sparse_bank_feedback_rules(gpu):
+    """test_sparse.py:107-163 semantics through the bank-level device API."""
+    from paper_2405_04212_b200.core import RngStream
+
+    def bank(cands=None, **kw):
+        p = dict(n_literals=12, n_clauses=2, n_classes=2, s=2.0, threshold=5, seed=1,
+                 negated_literals_enabled=False, sparse_floor=-4)
+        p.update(kw)
+        cfg = gpu.Config(**p)
+        return gpu.SparseClauseBank(cfg, candidate_literals=np.arange(12) if cands is None
+                                    else cands)
+
+    ex = lambda a: gpu.SparseExample(np.array(a, dtype=np.int64), 0)  # noqa: E731
+    b = bank()
+    b.weights[0, 1] = 1
+    gpu.sparse.sparse_feedback(b, 0, 1, -1, True, 1, ex([0]), RngStream.derive(1, 0))
+    assert b.lookup(0, 3) == -3 and b.lookup(0, 0) == -4
+    b = bank(cands=np.array([0, 1]))
+    b.weights[0, 1] = 1
+    gpu.sparse.sparse_feedback(b, 0, 1, -1, True, 1, ex([0]), RngStream.derive(1, 0))
+    assert b.clause_literals[0].tolist() == [1]
+    b = bank(s=1.0001)
+    b.clause_literals[0] = np.array([4], dtype=np.int64)
+    b.clause_states[0] = np.array([-3], dtype=np.int8)
+    gpu.sparse.sparse_feedback(b, 0, 0, 1, True, 0, ex([]), RngStream.derive(1, 0))
+    assert b.clause_literals[0].size == 0
+    b = bank(sparse_capacity=2)
+    b.weights[0, 1] = 1
+    rng = RngStream.derive(1, 0)
+    gpu.sparse.sparse_feedback(b, 0, 1, -1, True, 1, ex([11]), rng)
+    assert b.clause_literals[0].tolist() == [0, 1] and b.clause_states[0].tolist() == [-3, -3]
+    assert rng.counter == 1
+    # capacity is not a hard cap: stored pairs always survive (SURVEY 0.8)
+    b = bank(sparse_capacity=2)
+    b.clause_literals[0] = np.array([5, 6], dtype=np.int64)
+    b.clause_states[0] = np.array([-2, -3], dtype=np.int8)
+    b.weights[0, 1] = 1
+    gpu.sparse.sparse_feedback(b, 0, 1, -1, True, 1, ex([]), RngStream.derive(1, 0))
+    assert b.clause_literals[0].tolist() == [0, 1, 5, 6]
+
+
+def test_sparse_large_vocab_prefix_vs_oracle(gpu, oracle):
+    """configs[4] shapes on a small slice: 10^6-literal universe, Zipf(1.05)
+    documents of 100 tokens, 2000 clauses, capacity 64, floor -15, T=2000,
+    s=5 -- 3 training documents against the oracle (its Type II walks all
+    ~10^5 candidates), then inference parity on 200 documents."""
+    d = gpu.datasets.sparse_zipf(n_docs=2000)
+    kw = gpu.datasets.sparse_config_kwargs(seed=3)
+    cfg = gpu.Config(**kw)
+    acts = [d.row(i) for i in range(len(d))]
+    from paper_2405_04212_b200.sparse_train import SparseTrainSession
+    sess = SparseTrainSession(cfg, d.indptr, d.indices, d.labels)
+    sess.run_epoch(max_steps=3)
+    m = sess.model()
+    banks, bctr, _ = oracle.sparse_train(cfg, acts, d.labels, n_epochs=1, max_steps=3)
+    ob = banks[0]
+    assert np.array_equal(m.weights, ob.weights)
+    for j in range(cfg.n_clauses):
+        assert np.array_equal(m.clause_literals[j], ob.lits[j]), j
+        assert np.array_equal(m.clause_states[j], ob.sts[j]), j
+    ex = [gpu.SparseExample(a, 0) for a in acts[:200]]
+    assert np.array_equal(m.batch_votes(ex), oracle.sparse_batch_votes(banks, acts[:200]))
