@@ -285,12 +285,36 @@ def sparse_fixture():
     save("sparse", **out)
 
 
+def tuning_fixture():
+    """tuning.stratified_kfold assignments and a cross_validate report."""
+    from tsetlinkit.tuning import cross_validate, stratified_kfold
+    rs = np.random.default_rng(17)
+    out = {}
+    for t in range(12):
+        k = int(rs.integers(2, 6))
+        labels = rs.integers(0, 3, size=int(rs.integers(3 * k + 3, 90)))
+        while np.bincount(labels, minlength=3).min() < k:
+            labels = rs.integers(0, 3, size=labels.size)
+        out[f"t{t}_labels"] = labels
+        out[f"t{t}_k"] = np.int64(k)
+        out[f"t{t}_folds"] = stratified_kfold(labels, k, seed=t)
+    x = rs.integers(0, 2, size=(240, 6)).astype(np.uint8)
+    y = (x[:, 0] ^ x[:, 1]).astype(np.int64)
+    cfg = tk.Config(n_literals=6, n_clauses=8, n_classes=2, s=1.9, threshold=11,
+                    n_literal_budget=3, seed=0)
+    rep = cross_validate(cfg, (x, y), 4, 2, seed=9)
+    out["cv_x"], out["cv_y"] = x, y
+    out["cv_acc"] = np.array(rep.fold_accuracies)
+    out["cv_folds"] = rep.fold_assignments
+    save("tuning", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "kernels", "feedback", "train", "noisy_xor", "mnist",
-                             "predictor", "sparse"]
+                             "predictor", "sparse", "tuning"]
     table = {"rng": rng_fixture, "kernels": kernel_fixture, "feedback": feedback_fixture,
              "train": train_fixture, "noisy_xor": noisy_xor_fixture,
              "mnist": mnist_prefix_fixture, "predictor": predictor_fixture,
-             "sparse": sparse_fixture}
+             "sparse": sparse_fixture, "tuning": tuning_fixture}
     for name in which:
         table[name]()

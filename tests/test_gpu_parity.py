@@ -468,3 +468,14 @@ def test_sparse_large_vocab_prefix_vs_oracle(gpu, oracle):
         assert np.array_equal(m.clause_states[j], ob.sts[j]), j
     ex = [gpu.SparseExample(a, 0) for a in acts[:200]]
     assert np.array_equal(m.batch_votes(ex), oracle.sparse_batch_votes(banks, acts[:200]))
+
+
+def test_cross_validate_golden(gpu):
+    """tuning.cross_validate on the GPU trainer == the reference's report."""
+    g = golden("tuning")
+    cfg = gpu.Config(n_literals=6, n_clauses=8, n_classes=2, s=1.9, threshold=11,
+                     n_literal_budget=3, seed=0)
+    from paper_2405_04212_b200 import tuning
+    rep = tuning.cross_validate(cfg, (g["cv_x"], g["cv_y"]), 4, 2, seed=9)
+    assert np.array_equal(rep.fold_assignments, g["cv_folds"])
+    assert np.array_equal(np.array(rep.fold_accuracies), g["cv_acc"])
