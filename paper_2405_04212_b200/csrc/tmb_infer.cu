@@ -185,6 +185,7 @@ struct InferCK {
     int vec_ok;
     int rloc_max;
     int dbg;  // bit0: skip eval, bit1: skip transpose (timing experiments only)
+    unsigned long long *phase;  // optional [grid][8] clock64 per phase (thread 0)
 };
 
 __device__ __forceinline__ uint32_t pack8(unsigned long long q) {
@@ -435,6 +436,16 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     }
     cluster.sync();
 
+    unsigned long long iph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long imark = clock64();
+#define IPH(n)                                                            \
+    do {                                                                  \
+        if (k.phase && tid == 0) {                                        \
+            const long long now = clock64();                              \
+            iph[n] += (unsigned long long)(now - imark);                  \
+            imark = now;                                                  \
+        }                                                                 \
+    } while (0)
     int64_t it = 0;
     int64_t t = cid;
     prefetch_l2(t);
@@ -447,7 +458,9 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     for (; t < n_tiles; t += n_clusters, ++it) {
         const int buf = (int)(it & 1);
         const uint32_t *xt = buf ? xt1 : xt0;
+        IPH(7);
         prefetch_l2(t + 2 * (int64_t)n_clusters);
+        IPH(0);
         for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
         if (tid < kTG) dirty[tid] = 0;
         __syncthreads();
@@ -506,6 +519,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
             }
         }
         __syncthreads();
+        IPH(1);
         // ---- push partial sums of example block b to CTA b's inbox; blocks
         //      where no local rule fired only send their (zero) flag
         for (int i = tid; i < 32 * kTG * K; i += blockDim.x) {
@@ -516,14 +530,19 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
             dst[((buf * kCS + rank) * 32) * K + rem] = part[i];
         }
         if (tid < kCS) cluster.map_shared_rank(iflag, tid)[buf * kCS + rank] = dirty[tid];
+        IPH(2);
         // ---- next tile's X^T (its raw rows were prefetched into L2)
         const int64_t tn = t + n_clusters;
         if (tn < n_tiles && !(k.dbg & 2)) {
             transpose(tn, buf ^ 1);
+            IPH(3);
             publish(buf ^ 1);
         }
+        IPH(4);
         cluster.sync();
+        IPH(5);
         if (tn < n_tiles && !(k.dbg & 2)) await_tile(buf ^ 1);
+        IPH(6);
         // ---- finalize the 32 examples of block `rank`
         if (warp == 0) {
             const int64_t e = t * tile_n + 32 * rank + lane;
@@ -543,6 +562,8 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
             }
         }
     }
+    if (k.phase && tid == 0)
+        for (int q = 0; q < 8; ++q) k.phase[blockIdx.x * 8 + q] = iph[q];
     cluster.sync();  // peers may still write into our buffers until here
     if (k.correct) {
         for (int o = 16; o; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
@@ -571,6 +592,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
 
 int g_force_generic_infer = 0;
 int g_infer_dbg = 0;
+unsigned long long *g_infer_phase = nullptr;
 
 int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, int64_t *pred,
                  const int64_t *labels, unsigned long long *correct, cudaStream_t st) {
@@ -632,6 +654,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     k.vec_ok = (r->F % 16 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
     k.rloc_max = (int)rloc_max;
     k.dbg = g_infer_dbg;
+    k.phase = g_infer_phase;
     const void *fn = (const void *)k_infer_cluster;
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int threads = 512;
@@ -885,6 +908,10 @@ int tmb_set_option(const char *name, int64_t value) {
     }
     if (std::string(name) == "infer.debug_skip") {  // timing experiments only
         g_infer_dbg = (int)value;
+        return TMB_OK;
+    }
+    if (std::string(name) == "infer.phase_buffer") {  // device uint64 [grid*8] or 0
+        g_infer_phase = reinterpret_cast<unsigned long long *>(value);
         return TMB_OK;
     }
     return fail(TMB_E_INVALID, std::string("set_option: unknown option ") + name);

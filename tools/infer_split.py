@@ -29,3 +29,17 @@ for mode, name in ((0, "full"), (1, "skip eval"), (2, "skip transpose"), (3, "sk
     torch.cuda.synchronize()
     print(f"{name:15s} {a.elapsed_time(b) / 3:8.2f} ms")
 _lib.call("tmb_set_option", b"infer.debug_skip", 0)
+
+# per-phase clock64 profile of thread 0 of every CTA (us per tile)
+ph = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+_lib.call("tmb_set_option", b"infer.phase_buffer", ph.data_ptr())
+model.infer_device(x, pred_dev=pred)
+torch.cuda.synchronize()
+_lib.call("tmb_set_option", b"infer.phase_buffer", 0)
+clk = torch.cuda.get_device_properties(0).clock_rate * 1e3
+p = ph.cpu().numpy().reshape(148, 8).astype(float) / clk * 1e6
+tiles = (N // 128) / (148 // 4)
+names = ["prefetch", "zero+sync+eval", "sync", "transpose", "publish", "cluster.sync",
+         "await", "finalize+loop"]
+for q in range(8):
+    print(f"  {names[q]:16s} {p[:, q].mean() / tiles:7.3f} us/tile (max CTA {p[:, q].max() / tiles:7.3f})")
