@@ -321,15 +321,15 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         uint32_t *mine = buf ? xt1 : xt0;
         const int j = lane >> 3, c16 = lane & 7;
         const int units = nblk * kTG;
-        for (int u = warp; u < units; u += nwarps) {
+        auto load_unit = [&](int u, uint4 (&w)[8], int64_t &fb_out) {
             const int g = u % kTG;
             const int64_t fb = qf0 + (int64_t)(u / kTG) * 128 + 16 * c16;  // my 16 features
-            uint4 w[8];
+            fb_out = fb;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {  // all eight loads in flight first
+            for (int i = 0; i < 8; ++i) {
                 const int64_t e = e0 + 32 * g + 8 * j + i;
                 w[i] = make_uint4(0, 0, 0, 0);
-                if (e < k.N && fb < qf1) {
+                if (u < units && e < k.N && fb < qf1) {
                     const uint8_t *src = k.x + e * F + fb;
                     if (k.vec_ok && fb + 16 <= F) {
                         w[i] = *reinterpret_cast<const uint4 *>(src);
@@ -347,6 +347,9 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
                     }
                 }
             }
+        };
+        auto finish_unit = [&](int u, const uint4 (&w)[8], int64_t fb) {
+            const int g = u % kTG;
             uint32_t v[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -377,16 +380,25 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
 #pragma unroll
                 for (int sft = 0; sft < 4; ++sft)
                     word |= ((recv[sft] >> (8 * kq)) & 0xFFu) << (8 * (j ^ sft));
-                const int64_t f = fb - 16 * c16 + 16 * c16 + 4 * j + kq;
+                const int64_t f = fb + 4 * j + kq;
                 if (f < qf1) mine[(size_t)f * kTG + g] = word;
             }
+        };
+        for (int u = warp; u < units; u += 2 * nwarps) {
+            uint4 wa[8], wb[8];
+            int64_t fa, fbb;
+            const int u2 = u + nwarps;
+            load_unit(u, wa, fa);
+            load_unit(u2, wb, fbb);  // both units' 16 loads in flight together
+            finish_unit(u, wa, fa);
+            if (u2 < units) finish_unit(u2, wb, fbb);
         }
     };
 
     // bulk L2 prefetch of this CTA's feature quarter of tile `t` (one TMA
     // bulk-prefetch per example row; no registers, no shared memory)
     auto prefetch_l2 = [&](int64_t t) {
-        if (t >= n_tiles || !k.vec_ok || (k.dbg & 4)) return;
+        if (t >= n_tiles || !k.vec_ok || !(k.dbg & 8)) return;  // opt-in (measured no gain)
         const int64_t e0 = t * tile_n;
         const int64_t off = (int64_t)ch0 * 32;
         const int64_t len = std::min<int64_t>((int64_t)(ch1 - ch0) * 32, F - off);
@@ -487,7 +499,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
                     a2 &= x.z ^ m;
                     a3 &= x.w ^ m;
                 }
-                if ((q & 1) && !__any_sync(0xffffffffu, a0 | a1 | a2 | a3)) break;
+                if (!__any_sync(0xffffffffu, a0 | a1 | a2 | a3)) break;
             }
             if ((a0 | a1 | a2 | a3) && r < rloc) {
                 const int rg = r0 + r;
