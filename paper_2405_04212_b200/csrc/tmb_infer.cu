@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     int32_t *iflag = inbox + 2 * kCS * 32 * K;                                // [2][kCS]
     int32_t *dirty = iflag + 2 * kCS;                                         // [kTG]
     uint64_t *mbar = reinterpret_cast<uint64_t *>(
-        reinterpret_cast<uintptr_t>(dirty + kTG + 1 + 3) & ~(uintptr_t)7);   // [2]
+        reinterpret_cast<uintptr_t>(dirty + kTG + 3) & ~(uintptr_t)7);       // [2]
 
     const int r0 = (int)((int64_t)rank * k.R / kCS), r1 = (int)((int64_t)(rank + 1) * k.R / kCS);
     const int rloc = r1 - r0;
@@ -316,11 +316,12 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     const int64_t qf0 = (int64_t)ch0 * 32;
     const int64_t qf1 = std::min<int64_t>((int64_t)ch1 * 32, F);
     const int nblk = (int)((qf1 - qf0 + 127) / 128);
-    const int tj = lane >> 3, c16 = lane & 7;
-    const int units = nblk * kTG;
-    auto load_unit = [&](int64_t t, int u, uint4 (&w)[8], int64_t &fb_out) {
-            const int64_t e0 = t * tile_n;
-            const int j = tj;
+    auto transpose = [&](int64_t t, int buf) {
+        const int64_t e0 = t * tile_n;
+        uint32_t *mine = buf ? xt1 : xt0;
+        const int j = lane >> 3, c16 = lane & 7;
+        const int units = nblk * kTG;
+        auto load_unit = [&](int u, uint4 (&w)[8], int64_t &fb_out) {
             const int g = u % kTG;
             const int64_t fb = qf0 + (int64_t)(u / kTG) * 128 + 16 * c16;  // my 16 features
             fb_out = fb;
@@ -347,9 +348,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
                 }
             }
         };
-    auto finish_unit = [&](int buf, int u, const uint4 (&w)[8], int64_t fb) {
-            uint32_t *mine = buf ? xt1 : xt0;
-            const int j = tj;
+        auto finish_unit = [&](int u, const uint4 (&w)[8], int64_t fb) {
             const int g = u % kTG;
             uint32_t v[8];
 #pragma unroll
@@ -385,19 +384,16 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
                 if (f < qf1) mine[(size_t)f * kTG + g] = word;
             }
         };
-    // units [u_first, units) of this warp, two at a time (16 loads in flight)
-    auto transpose_from = [&](int64_t t, int buf, int u_first) {
-        for (int u = u_first; u < units; u += 2 * nwarps) {
+        for (int u = warp; u < units; u += 2 * nwarps) {
             uint4 wa[8], wb[8];
             int64_t fa, fbb;
             const int u2 = u + nwarps;
-            load_unit(t, u, wa, fa);
-            load_unit(t, u2, wb, fbb);
-            finish_unit(buf, u, wa, fa);
-            if (u2 < units) finish_unit(buf, u2, wb, fbb);
+            load_unit(u, wa, fa);
+            load_unit(u2, wb, fbb);  // both units' 16 loads in flight together
+            finish_unit(u, wa, fa);
+            if (u2 < units) finish_unit(u2, wb, fbb);
         }
     };
-    auto transpose = [&](int64_t t, int buf) { transpose_from(t, buf, warp); };
 
     // bulk L2 prefetch of this CTA's feature quarter of tile `t` (one TMA
     // bulk-prefetch per example row; no registers, no shared memory)
@@ -476,23 +472,15 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         const uint32_t *xt = buf ? xt1 : xt0;
         IPH(7);
         prefetch_l2(t + 2 * (int64_t)n_clusters);
-        // software pipelining: this warp's first unit of the next tile is in
-        // flight (registers) for the whole evaluation of this tile
-        const int64_t tn = t + n_clusters;
-        const bool has_next = tn < n_tiles && !(k.dbg & 2);
-        uint4 pre[8];
-        int64_t pre_fb = 0;
-        if (has_next) load_unit(tn, warp, pre, pre_fb);
         IPH(0);
         for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
         if (tid < kTG) dirty[tid] = 0;
-        if (tid == 0) dirty[kTG] = nwarps;  // next free eval chunk
         __syncthreads();
         // ---- evaluate the local rules: one lane per rule; an include code
         //      reads the 16-byte X^T row of its feature = 128 examples
         const uint32_t xaddr = smem_u32(xt);  // explicit shared-window loads
         const uint32_t haddr = smem_u32(heads);
-        for (int rc = warp; rc * 32 < rloc && !(k.dbg & 1);) {
+        for (int rc = warp; rc * 32 < rloc && !(k.dbg & 1); rc += nwarps) {
             const int r = rc * 32 + lane;
             const int rr = r < rloc ? r : 0;  // idle lanes still join the votes
             const uint32_t live = r < rloc ? 0xFFFFFFFFu : 0u;
@@ -541,9 +529,6 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
                     }
                 }
             }
-            int nxt = 0;
-            if (lane == 0) nxt = atomicAdd(&dirty[kTG], 1);
-            rc = __shfl_sync(0xffffffffu, nxt, 0);
         }
         __syncthreads();
         IPH(1);
@@ -558,17 +543,17 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
         }
         if (tid < kCS) cluster.map_shared_rank(iflag, tid)[buf * kCS + rank] = dirty[tid];
         IPH(2);
-        // ---- next tile's X^T: finish the pre-loaded unit, then the rest
-        if (has_next) {
-            if (warp < units) finish_unit(buf ^ 1, warp, pre, pre_fb);
-            transpose_from(tn, buf ^ 1, warp + nwarps);
+        // ---- next tile's X^T (its raw rows were prefetched into L2)
+        const int64_t tn = t + n_clusters;
+        if (tn < n_tiles && !(k.dbg & 2)) {
+            transpose(tn, buf ^ 1);
             IPH(3);
             publish(buf ^ 1);
         }
         IPH(4);
         cluster.sync();
         IPH(5);
-        if (has_next) await_tile(buf ^ 1);
+        if (tn < n_tiles && !(k.dbg & 2)) await_tile(buf ^ 1);
         IPH(6);
         // ---- finalize the 32 examples of block `rank`
         if (warp == 0) {
@@ -672,7 +657,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     const int64_t rloc_max = (r->R + kCS - 1) / kCS;
     const size_t smem = 32 * (size_t)rloc_max + 2 * 4 * (size_t)(r->F + 1) * kTG +
                         4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K +
-                        4 * (2 * kCS + kTG + 1) + 32;
+                        4 * (2 * kCS + kTG) + 32;
     if (smem > (size_t)max_smem) return TMB_OK;  // generic kernel instead
     InferCK k;
     k.x = x; k.N = N; k.F = r->F; k.heads = r->heads; k.tail_ptr = r->tail_ptr; k.tails = r->tails;
