@@ -72,5 +72,6 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int sm_count();
+extern int64_t g_train_key_chunk;  // keyed trainer: steps per launch override (tmb_train.cu)
 
 }  // namespace tmb

@@ -918,6 +918,10 @@ int tmb_set_option(const char *name, int64_t value) {
         g_force_generic_infer = (int)value;
         return TMB_OK;
     }
+    if (std::string(name) == "train.key_chunk") {  // keyed trainer: steps per launch (0 = auto)
+        g_train_key_chunk = value;
+        return TMB_OK;
+    }
     if (std::string(name) == "infer.debug_skip") {  // timing experiments only
         g_infer_dbg = (int)value;
         return TMB_OK;

@@ -20,9 +20,14 @@
 //     per-CTA event prefixes are exchanged through distributed shared memory
 //     and two hardware cluster barriers per example -- no global memory
 //     round trips on the critical path.
-//   GRID mode (n_cta > 16, cooperative launch, up to one CTA per SM): K int64
-//     atomics + one global barrier per example; update-flag draws for the
-//     CTA's block range are precomputed while the barrier is pending.
+//   GRID mode (n_cta > 16, cooperative launch, up to one CTA per SM): two
+//     relaxed 64-bit atomics per CTA + a spin per example.  With one block
+//     (the common case) the update-flag draws of a whole run are generated up
+//     front by k_flag_keys as 16-bit keys (the top bits of each 53-bit draw,
+//     exact compare only on a key tie), streamed one example ahead into
+//     shared memory with cp.async, and counted with SIMD byte-pair compares;
+//     otherwise the CTA's block range of draws is computed while the spin is
+//     pending.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -38,12 +43,15 @@ namespace tmb {
 struct TrainK {
     int C, P, K, W, Ppad, n_blocks, n_cta, cmax, fmax_words, bmax;
     int vec4;  // states rows 4-byte addressable in global memory
+    int keyed, Cw;  // keyed flag path; u32 words (2 keys) per stream, % 4 == 0
     int64_t budget, T;
     FbParams fp;
     uint64_t fb_seed, fb_counter0;
     int64_t n_steps;
     const uint32_t *lit_words;
     const int32_t *labels, *order;
+    const uint32_t *keys;  // keyed: [n_steps][2][Cw] packed 16-bit flag keys
+    const int32_t *nrand;  // keyed: [n_steps] int(u * (K - 1)) of the negative draw
     int8_t *states;
     int32_t *weights;
     uint64_t *block_counters;
@@ -93,6 +101,9 @@ struct Smem {
     long long *vsum;   // grid: [2] summed votes
     int *misc;         // [0]=n_work [3..5]=example ring [8..10]=label ring
     uint64_t *thr;     // grid: [0]=t_t [1]=t_n [2]=negative
+    uint32_t *keys;    // keyed: [2 buffers][2 streams][Cw]
+    unsigned *wcnt;    // keyed: [16] per-warp prefix events, [16] per-warp totals
+    unsigned long long *vacc;  // grid: [2] CTA partial votes (label, negative)
 };
 
 // Shared-memory carve-up; identical on host (size) and device (pointers).
@@ -125,8 +136,11 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.un_bits = (uint32_t *)take(4 * k.fmax_words);
     t.word_cum = (int32_t *)take(4 * (k.fmax_words + 1));
     const bool pre = 32 * k.fmax_words <= kMaxPrecompute;
-    t.draw_t = pre ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
-    t.draw_n = pre ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
+    t.draw_t = pre && !k.keyed ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
+    t.draw_n = pre && !k.keyed ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
+    t.keys = k.keyed ? (uint32_t *)take(4 * 4 * (size_t)k.Cw) : nullptr;
+    t.wcnt = (unsigned *)take(4 * 32);
+    t.vacc = (unsigned long long *)take(8 * 2);
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
     if (s) *s = t;
     return align_up(off, 16);
@@ -312,12 +326,29 @@ __device__ __forceinline__ void flush_stats(const TrainK &k, Counters &cn, bool 
 constexpr int kRowRegs = 4;  // literal words per thread (W <= 4 * blockDim)
 struct Prefetch {
     uint32_t row[kRowRegs];
-    int label, ex2;
+    int label, ex2, nr;
 };
 
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Keyed path: step i's flag keys (both streams) into key buffer i & 1.
+__device__ __forceinline__ void keys_issue(const TrainK &k, const Smem &s, int64_t i) {
+    const uint32_t *src = k.keys + i * 2 * (int64_t)k.Cw;
+    uint32_t *dst = s.keys + (i & 1) * 2 * k.Cw;
+    for (int q = threadIdx.x; q < k.Cw / 2; q += blockDim.x) cp_async16(dst + 4 * q, src + 4 * q);
+    cp_async_commit();
+}
+
+template <bool KEYS>
 __device__ __forceinline__ void prefetch_issue(const TrainK &k, const Smem &s, int64_t i,
                                                Prefetch &pf) {
     if (i + 1 >= k.n_steps) return;
+    if (KEYS) keys_issue(k, s, i + 1);
     const int ex = s.misc[3 + (int)((i + 1) % 3)];
 #pragma unroll
     for (int q = 0; q < kRowRegs; ++q) {
@@ -326,13 +357,16 @@ __device__ __forceinline__ void prefetch_issue(const TrainK &k, const Smem &s, i
     }
     if (threadIdx.x == blockDim.x - 1) {
         pf.label = __ldg(&k.labels[ex]);
+        if (KEYS) pf.nr = __ldg(&k.nrand[i + 1]);
         if (i + 2 < k.n_steps) pf.ex2 = __ldg(&k.order[i + 2]);
     }
 }
 
+template <bool KEYS>
 __device__ __forceinline__ void prefetch_commit(const TrainK &k, const Smem &s, int64_t i,
                                                 const Prefetch &pf) {
     if (i + 1 >= k.n_steps) return;
+    if (KEYS) cp_async_wait_all();
     uint32_t *dst = ((i + 1) & 1) ? s.lit1 : s.lit0;
 #pragma unroll
     for (int q = 0; q < kRowRegs; ++q) {
@@ -341,20 +375,27 @@ __device__ __forceinline__ void prefetch_commit(const TrainK &k, const Smem &s, 
     }
     if (threadIdx.x == blockDim.x - 1) {
         s.misc[8 + (int)((i + 1) % 3)] = pf.label;
+        if (KEYS) s.misc[12 + (int)((i + 1) % 3)] = pf.nr;
         if (i + 2 < k.n_steps) s.misc[3 + (int)((i + 2) % 3)] = pf.ex2;
     }
 }
 
+template <bool KEYS>
 __device__ __forceinline__ void prologue_ring(const TrainK &k, const Smem &s) {
+    if (KEYS) keys_issue(k, s, 0);
     if (threadIdx.x == 0) {
         s.misc[3] = __ldg(&k.order[0]);
         s.misc[8] = __ldg(&k.labels[s.misc[3]]);
+        if (KEYS) s.misc[12] = __ldg(&k.nrand[0]);
         if (k.n_steps > 1) s.misc[4] = __ldg(&k.order[1]);
+        s.vacc[0] = 0;
+        s.vacc[1] = 0;
     }
     __syncthreads();
     const int ex = s.misc[3];
     for (int w = threadIdx.x; w < k.W; w += blockDim.x)
         s.lit0[w] = __ldg(&k.lit_words[(int64_t)ex * k.W + w]);
+    if (KEYS) cp_async_wait_all();
 }
 
 // feedback.py:33-44: clipped update probabilities -> integer thresholds.
@@ -373,6 +414,45 @@ __device__ __forceinline__ int negative_class(const TrainK &k, int label, uint64
     const double u = u01_from53(draw53(k.fb_seed, fbc));
     int neg = label + 1 + (int)(u * (double)(k.K - 1));  // < 2K
     return neg >= k.K ? neg - k.K : neg;
+}
+
+// Update flags of clauses j0, j0 + 1 of one stream from their packed 16-bit
+// keys (key = draw53 >> 37): bit 0 / bit 16.  A key equal to the threshold's
+// top bits is resolved with the exact draw (probability 2^-16 per flag).
+__device__ __forceinline__ uint32_t flag_pair(uint32_t v, uint64_t t, uint64_t seed,
+                                              uint64_t ctr_j0) {
+    const uint32_t tb = (uint32_t)(t >> 37);
+    if (tb >= 65536u) return 0x00010001u;  // p == 1
+    const uint32_t tb2 = tb | (tb << 16);
+    uint32_t lt = __vcmpltu2(v, tb2) & 0x00010001u;
+    const uint32_t eq = __vcmpeq2(v, tb2) & 0x00010001u;
+    if (eq) {
+        if ((eq & 1u) && draw53(seed, ctr_j0) < t) lt |= 1u;
+        if ((eq >> 16) && draw53(seed, ctr_j0 + 1) < t) lt |= 0x10000u;
+    }
+    return lt;
+}
+
+// k_flag_keys: the update-flag draws of steps [0, n_steps) as packed 16-bit
+// keys, plus the negative-class draw (feedback.py:47-53, same counters as
+// the per-CTA path).  Padding keys are 0xFFFF and masked by the counter.
+__global__ void k_flag_keys(uint64_t seed, uint64_t fbc0, int C, int Cw, int K, int64_t n_steps,
+                            uint32_t *keys, int32_t *nrand) {
+    const int64_t per = 2LL * Cw, total = n_steps * per;
+    const uint64_t step_draws = 1ull + 2ull * (uint64_t)C;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / per;
+        const int r = (int)(e - i * per);
+        const int str = r >= Cw ? 1 : 0;
+        const int j0 = 2 * (r - str * Cw);
+        const uint64_t fbc = fbc0 + (uint64_t)i * step_draws;
+        const uint64_t base = fbc + 1 + (str ? (uint64_t)C : 0);
+        const uint32_t lo = j0 < C ? (uint32_t)(draw53(seed, base + j0) >> 37) : 0xFFFFu;
+        const uint32_t hi = j0 + 1 < C ? (uint32_t)(draw53(seed, base + j0 + 1) >> 37) : 0xFFFFu;
+        keys[e] = lo | (hi << 16);
+        if (r == 0) nrand[i] = (int)(u01_from53(draw53(seed, fbc)) * (double)(K - 1));
+    }
 }
 
 __device__ __forceinline__ void cluster_arrive() {
@@ -394,7 +474,7 @@ __device__ __forceinline__ void cluster_wait() {
     } while (0)
 
 // One fused kernel, two synchronisation domains (see the header comment).
-template <int MODE, bool SMEM_STATES>
+template <int MODE, bool SMEM_STATES, bool KEYS>
 __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
     extern __shared__ __align__(16) char smem_raw[];
     Smem s;
@@ -418,7 +498,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         s.blk_ctr[i] = k.block_counters[b0 + i];
         s.blk_seed[i] = k.block_seeds[b0 + i];
     }
-    prologue_ring(k, s);
+    prologue_ring<KEYS>(k, s);
     __syncthreads();
     if (MODE == MODE_CLUSTER) cg::this_cluster().sync();  // DSMEM peers resident
 
@@ -427,50 +507,101 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long t_mark = clock64();
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
+
+    // Event bookkeeping of own clause j (kernels/_numba.py:101-125): window
+    // ordinal `ord` of its first event, event types, feedback-then-weight
+    // and the work list.
+    auto apply_events = [&](int j, bool t_ev, bool n_ev, uint64_t ord, uint64_t bseed,
+                            int label, int neg) {
+        int info = s.info[j] & I_OUT;
+        if (t_ev || n_ev) {
+            const bool out = info & I_OUT;
+            int32_t *w = s.weights + j * K;
+            const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
+            if (t_ev) {
+                info |= I_TEV | (t1 ? I_T1 : 0);
+                s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
+                ++cn.events;
+                if (t1) ++cn.t1; else if (out) ++cn.t2;
+            }
+            if (n_ev) {
+                const uint64_t o2 = ord + (t_ev ? 1 : 0);
+                info |= I_NEV | (n1 ? I_N1 : 0);
+                s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
+                ++cn.events;
+                if (n1) ++cn.t1; else if (out) ++cn.t2;
+            }
+            if (out) {
+                if (t_ev) w[label] += 1;
+                if (n_ev) w[neg] -= 1;
+            }
+            if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
+                s.work[atomicAdd(&s.misc[0], 1)] = j;
+        }
+        s.info[j] = info;
+    };
+
     for (int64_t i = 0; i < k.n_steps; ++i) {
         const uint32_t *lit = (i & 1) ? s.lit1 : s.lit0;
         const int label = s.misc[8 + (int)(i % 3)];
         const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
-        const int neg = negative_class(k, label, fbc);
+        int neg;
+        if (KEYS) {
+            neg = label + 1 + s.misc[12 + (int)(i % 3)];
+            if (neg >= K) neg -= K;
+        } else {
+            neg = negative_class(k, label, fbc);
+        }
         Prefetch pf;
-        prefetch_issue(k, s, i, pf);
-        // 1. training-mode outputs of own clauses (kernels/_numba.py:36-50)
+        prefetch_issue<KEYS>(k, s, i, pf);
+        // 1. training-mode outputs of own clauses (kernels/_numba.py:36-50);
+        //    grid mode folds the two class sums the decision reads
+        //    (dense.py:153 restricted to label / negative) into the same pass
         for (int j = warp; j < cown; j += nwarps) {
             uint32_t viol = 0;
             for (int w = lane; w < k.W; w += 32) viol |= s.masks[j * k.W + w] & ~lit[w];
             viol = __reduce_or_sync(0xffffffffu, viol);
-            if (lane == 0) s.info[j] = (viol == 0 && s.cnt[j] <= k.budget) ? I_OUT : 0;
+            if (lane == 0) {
+                const bool out = viol == 0 && s.cnt[j] <= k.budget;
+                s.info[j] = out ? I_OUT : 0;
+                if (MODE == MODE_GRID && out) {
+                    atomicAdd(&s.vacc[0], (unsigned long long)(long long)s.weights[j * K + label]);
+                    atomicAdd(&s.vacc[1], (unsigned long long)(long long)s.weights[j * K + neg]);
+                }
+            }
         }
         if (tid == 0) s.misc[0] = 0;
         __syncthreads();
         PHASE(0);
-        // 2. partial class sums of the two classes the decision reads
-        //    (dense.py:153 restricted to label / negative), then all-reduce
+        // 2. all-reduce of the partial class sums
         const int buf = (int)(i & 1);
-        if (warp < 2) {
-            const int kk = warp == 0 ? label : neg;
-            long long v = 0;
-            for (int j = lane; j < cown; j += 32)
-                if (s.info[j] & I_OUT) v += s.weights[j * K + kk];
-            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (MODE == MODE_CLUSTER) {
+        if (MODE == MODE_CLUSTER) {
+            if (warp < 2) {
+                const int kk = warp == 0 ? label : neg;
+                long long v = 0;
+                for (int j = lane; j < cown; j += 32)
+                    if (s.info[j] & I_OUT) v += s.weights[j * K + kk];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 // push into every CTA's inbox (DSMEM stores, no round trip)
                 if (lane < n_cta) {
                     long long *dst = cg::this_cluster().map_shared_rank(s.vin, lane);
                     dst[(buf * 16 + rank) * 2 + warp] = v;
                 }
-            } else if (lane == 0) {
-                // fence-free arrival: one relaxed atomic carries the arrival
-                // count (bits 40..63) and the biased partial (bits 0..39)
-                red_relaxed_add_u64(&k.rec[i * 2 + warp],
-                                    (1ull << 40) + (unsigned long long)(v + kVoteBias));
             }
+            cluster_arrive();
+        } else if (tid == 0) {
+            // fence-free arrival: one relaxed atomic per word carries the
+            // arrival count (bits 40..63) and the biased partial (bits 0..39)
+            const long long vl = (long long)s.vacc[0], vn = (long long)s.vacc[1];
+            s.vacc[0] = 0;
+            s.vacc[1] = 0;
+            red_relaxed_add_u64(&k.rec[i * 2 + 0], (1ull << 40) + (unsigned long long)(vl + kVoteBias));
+            red_relaxed_add_u64(&k.rec[i * 2 + 1], (1ull << 40) + (unsigned long long)(vn + kVoteBias));
         }
-        if (MODE == MODE_CLUSTER) cluster_arrive();
         PHASE(1);
         // while the all-reduce is pending: update-flag draws for [fs, fe)
-        // (feedback.py:47-53; independent of the votes) and the next example
-        if (pre) {
+        // (feedback.py:47-53; independent of the votes)
+        if (!KEYS && pre) {
             for (int idx = tid; idx < nfw * 32; idx += nthr) {
                 const int j = fsa + idx;
                 s.draw_t[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
@@ -497,7 +628,8 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 k.trace[i * 4 + 2] = vn;
             }
         } else {
-            // all-reduce complete when both words count n_cta arrivals
+            // all-reduce complete when both words count n_cta arrivals;
+            // thread 0 decides and broadcasts the two thresholds
             if (tid == 0) {
                 const unsigned long long want = (unsigned long long)n_cta;
                 ulonglong2 p;
@@ -505,126 +637,165 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                     p = ld_relaxed_v2u64(&k.rec[i * 2]);
                 } while ((p.x >> 40) != want || (p.y >> 40) != want);
                 const long long bias = (long long)n_cta * kVoteBias;
-                s.vsum[0] = (long long)(p.x & ((1ull << 40) - 1)) - bias;
-                s.vsum[1] = (long long)(p.y & ((1ull << 40) - 1)) - bias;
+                const long long vl = (long long)(p.x & ((1ull << 40) - 1)) - bias;
+                const long long vn = (long long)(p.y & ((1ull << 40) - 1)) - bias;
+                decide(k, vl, vn, t_t, t_n);
+                s.thr[0] = t_t;
+                s.thr[1] = t_n;
+                if (k.trace && rank == 0) {
+                    k.trace[i * 4 + 0] = neg;
+                    k.trace[i * 4 + 1] = vl;
+                    k.trace[i * 4 + 2] = vn;
+                }
             }
             __syncthreads();
-            decide(k, s.vsum[0], s.vsum[1], t_t, t_n);
-            if (k.trace && rank == 0 && tid == 0) {
-                k.trace[i * 4 + 0] = neg;
-                k.trace[i * 4 + 1] = s.vsum[0];
-                k.trace[i * 4 + 2] = s.vsum[1];
-            }
+            t_t = s.thr[0];
+            t_n = s.thr[1];
         }
         PHASE(3);
-        // 3. update flags over [fs, fe) as bitmaps
-        for (int idx = tid; idx < nfw * 32; idx += nthr) {
-            const int j = fsa + idx;
-            const bool valid = j >= fs && j < fe;
-            uint64_t mt, mn;
-            if (pre) {
-                mt = s.draw_t[idx];
-                mn = s.draw_n[idx];
-            } else {
-                mt = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
-                mn = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
+        if (KEYS) {
+            // 3. events over [0, c0) and [0, C) from the step's keys
+            const uint32_t *kt = s.keys + (i & 1) * 2 * k.Cw, *kn = kt + k.Cw;
+            const uint64_t ct = fbc + 1, cnn = fbc + 1 + (uint64_t)C;
+            unsigned pre_ev = 0, tot_ev = 0;
+            for (int w = tid; 2 * w < C; w += nthr) {
+                const int j0 = 2 * w;
+                const uint32_t f = flag_pair(kt[w], t_t, k.fb_seed, ct + j0) +
+                                   flag_pair(kn[w], t_n, k.fb_seed, cnn + j0);
+                const uint32_t valid = j0 + 1 < C ? 0xFFFFFFFFu : 0xFFFFu;
+                const uint32_t prem = j0 + 1 < c0 ? 0xFFFFFFFFu : (j0 < c0 ? 0xFFFFu : 0u);
+                const uint32_t fv = f & valid;  // two 16-bit counts, each <= 2
+                tot_ev += (fv & 0xFFFFu) + (fv >> 16);
+                pre_ev += (fv & prem & 0xFFFFu) + ((fv & prem) >> 16);
             }
-            const unsigned wt = __ballot_sync(0xffffffffu, valid && mt < t_t);
-            const unsigned wn = __ballot_sync(0xffffffffu, valid && mn < t_n);
+            pre_ev = __reduce_add_sync(0xffffffffu, pre_ev);
+            tot_ev = __reduce_add_sync(0xffffffffu, tot_ev);
             if (lane == 0) {
-                s.ut_bits[idx >> 5] = wt;
-                s.un_bits[idx >> 5] = wn;
+                s.wcnt[warp] = pre_ev;
+                s.wcnt[16 + warp] = tot_ev;
             }
-        }
-        __syncthreads();
-        PHASE(4);
-        // 4-5. warp 0: exclusive prefix of events per flag word, then window
-        //      ordinals, event types, weights (feedback then weight,
-        //      SPEC.md:171) and the work list of the own clauses
-        if (warp == 0) {
-            int carry = 0;
-            for (int base = 0; base < nfw; base += 32) {
-                const int w = base + lane;
-                const int v = w < nfw ? __popc(s.ut_bits[w]) + __popc(s.un_bits[w]) : 0;
-                int x = v;
+            __syncthreads();
+            PHASE(4);
+            // 4-5. warp 0: ordinals of the own clauses' events
+            if (warp == 0) {
+                unsigned pv = lane < nwarps ? s.wcnt[lane] : 0u;
+                unsigned tv = lane < nwarps ? s.wcnt[16 + lane] : 0u;
+                pv = __reduce_add_sync(0xffffffffu, pv);
+                tv = __reduce_add_sync(0xffffffffu, tv);
+                const uint64_t base = s.blk_ctr[0] + pv;
+                unsigned carry = 0;
+                for (int jb = 0; jb < cown; jb += 32) {
+                    const int j = jb + lane;
+                    bool t_ev = false, n_ev = false;
+                    if (j < cown) {
+                        const int c = c0 + j, sh = 16 * (c & 1);
+                        const uint32_t ft = flag_pair(kt[c >> 1], t_t, k.fb_seed, ct + (c & ~1));
+                        const uint32_t fn = flag_pair(kn[c >> 1], t_n, k.fb_seed, cnn + (c & ~1));
+                        t_ev = (ft >> sh) & 1u;
+                        n_ev = (fn >> sh) & 1u;
+                    }
+                    const unsigned v = (unsigned)t_ev + (unsigned)n_ev;
+                    unsigned x = v;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (j < cown)
+                        apply_events(j, t_ev, n_ev, base + carry + (x - v), s.blk_seed[0], label, neg);
+                    carry += __shfl_sync(0xffffffffu, x, 31);
                 }
-                if (w < nfw) s.word_cum[w] = carry + x - v;
-                carry += __shfl_sync(0xffffffffu, x, 31);
-            }
-            if (lane == 0) {
-                s.word_cum[nfw] = carry;
-                if (k.trace && rank == 0 && fs == 0 && fe == C) k.trace[i * 4 + 3] = carry;
-            }
-            __syncwarp();
-            auto cum = [&](int x) -> int {  // events over clauses [fsa, x)
-                const int q = (x - fsa) >> 5, r = (x - fsa) & 31;
-                int v = s.word_cum[q];
-                if (r) {
-                    const unsigned lo = (1u << r) - 1u;
-                    v += __popc(s.ut_bits[q] & lo) + __popc(s.un_bits[q] & lo);
+                __syncwarp();
+                if (lane == 0) {
+                    s.blk_ctr[0] += (uint64_t)tv;
+                    if (k.trace && rank == 0) k.trace[i * 4 + 3] = tv;
                 }
-                return v;
-            };
-            for (int j = lane; j < cown; j += 32) {
-                const int c = c0 + j;
-                const int q = (c - fsa) >> 5, r = (c - fsa) & 31;
-                const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
-                int info = s.info[j] & I_OUT;
-                if (t_ev || n_ev) {
+            }
+        } else {
+            // 3. update flags over [fs, fe) as bitmaps
+            for (int idx = tid; idx < nfw * 32; idx += nthr) {
+                const int j = fsa + idx;
+                const bool valid = j >= fs && j < fe;
+                uint64_t mt, mn;
+                if (pre) {
+                    mt = s.draw_t[idx];
+                    mn = s.draw_n[idx];
+                } else {
+                    mt = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
+                    mn = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
+                }
+                const unsigned wt = __ballot_sync(0xffffffffu, valid && mt < t_t);
+                const unsigned wn = __ballot_sync(0xffffffffu, valid && mn < t_n);
+                if (lane == 0) {
+                    s.ut_bits[idx >> 5] = wt;
+                    s.un_bits[idx >> 5] = wn;
+                }
+            }
+            __syncthreads();
+            PHASE(4);
+            // 4-5. warp 0: exclusive prefix of events per flag word, then
+            //      window ordinals and the work list of the own clauses
+            if (warp == 0) {
+                int carry = 0;
+                for (int base = 0; base < nfw; base += 32) {
+                    const int w = base + lane;
+                    const int v = w < nfw ? __popc(s.ut_bits[w]) + __popc(s.un_bits[w]) : 0;
+                    int x = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (w < nfw) s.word_cum[w] = carry + x - v;
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (lane == 0) {
+                    s.word_cum[nfw] = carry;
+                    if (k.trace && rank == 0 && fs == 0 && fe == C) k.trace[i * 4 + 3] = carry;
+                }
+                __syncwarp();
+                auto cum = [&](int x) -> int {  // events over clauses [fsa, x)
+                    const int q = (x - fsa) >> 5, r = (x - fsa) & 31;
+                    int v = s.word_cum[q];
+                    if (r) {
+                        const unsigned lo = (1u << r) - 1u;
+                        v += __popc(s.ut_bits[q] & lo) + __popc(s.un_bits[q] & lo);
+                    }
+                    return v;
+                };
+                for (int j = lane; j < cown; j += 32) {
+                    const int c = c0 + j;
+                    const int q = (c - fsa) >> 5, r = (c - fsa) & 31;
+                    const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
                     int bi = 0;
-                    uint64_t ord;
-                    if (k.n_blocks == 1) {  // fs == 0: events before c in the block
-                        ord = s.blk_ctr[0] + (uint64_t)cum(c);
-                    } else {
-                        bi = block_of(c, C, k.n_blocks) - b0;
-                        ord = s.blk_ctr[bi] +
-                              (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
+                    uint64_t ord = 0;
+                    if (t_ev || n_ev) {
+                        if (k.n_blocks == 1) {  // fs == 0: events before c in the block
+                            ord = s.blk_ctr[0] + (uint64_t)cum(c);
+                        } else {
+                            bi = block_of(c, C, k.n_blocks) - b0;
+                            ord = s.blk_ctr[bi] +
+                                  (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
+                        }
                     }
-                    const uint64_t bseed = s.blk_seed[bi];
-                    const bool out = info & I_OUT;
-                    int32_t *w = s.weights + j * K;
-                    const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
-                    if (t_ev) {
-                        info |= I_TEV | (t1 ? I_T1 : 0);
-                        s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
-                        ++cn.events;
-                        if (t1) ++cn.t1; else if (out) ++cn.t2;
-                    }
-                    if (n_ev) {
-                        const uint64_t o2 = ord + (t_ev ? 1 : 0);
-                        info |= I_NEV | (n1 ? I_N1 : 0);
-                        s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
-                        ++cn.events;
-                        if (n1) ++cn.t1; else if (out) ++cn.t2;
-                    }
-                    if (out) {
-                        if (t_ev) w[label] += 1;
-                        if (n_ev) w[neg] -= 1;
-                    }
-                    if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
-                        s.work[atomicAdd(&s.misc[0], 1)] = j;
+                    apply_events(j, t_ev, n_ev, ord, s.blk_seed[bi], label, neg);
                 }
-                s.info[j] = info;
-            }
-            __syncwarp();
-            // one window per applied event (block counters)
-            if (k.n_blocks == 1) {
-                if (lane == 0) s.blk_ctr[0] += (uint64_t)s.word_cum[nfw];
-            } else for (int bi = lane; bi <= b1 - b0; bi += 32) {
-                const int bs = block_begin(b0 + bi, C, k.n_blocks);
-                const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
-                s.blk_ctr[bi] += (uint64_t)(cum(be) - cum(bs));
+                __syncwarp();
+                // one window per applied event (block counters)
+                if (k.n_blocks == 1) {
+                    if (lane == 0) s.blk_ctr[0] += (uint64_t)s.word_cum[nfw];
+                } else for (int bi = lane; bi <= b1 - b0; bi += 32) {
+                    const int bs = block_begin(b0 + bi, C, k.n_blocks);
+                    const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
+                    s.blk_ctr[bi] += (uint64_t)(cum(be) - cum(bs));
+                }
             }
         }
         __syncthreads();
         PHASE(5);
         // 6. per-position Type I / II updates of the work list
         feedback_quads<SMEM_STATES>(k, s, c0, lit, s.misc[0], cn);
-        prefetch_commit(k, s, i, pf);
+        prefetch_commit<KEYS>(k, s, i, pf);
         __syncthreads();
         PHASE(6);
     }
@@ -655,6 +826,9 @@ struct tmb_trainer {
     uint64_t *block_seeds_d = nullptr;
     unsigned long long *ring_d = nullptr;  // grid mode: per-example vote slots [cap][2]
     int64_t ring_cap = 0;
+    uint32_t *keys_d = nullptr;  // keyed: [key_cap][2][Cw]
+    int32_t *nrand_d = nullptr;  // keyed: [key_cap]
+    int64_t key_cap = 0;
 };
 
 namespace {
@@ -674,12 +848,27 @@ void per_cta_maxima(TrainK &k) {
     k.bmax = bmax;
 }
 
-const void *kernel_for(bool cluster, bool smem_states) {
+const void *kernel_for(bool cluster, bool smem_states, bool keyed) {
     if (cluster)
-        return smem_states ? (const void *)k_train<MODE_CLUSTER, true>
-                           : (const void *)k_train<MODE_CLUSTER, false>;
-    return smem_states ? (const void *)k_train<MODE_GRID, true> : (const void *)k_train<MODE_GRID, false>;
+        return smem_states ? (const void *)k_train<MODE_CLUSTER, true, false>
+                           : (const void *)k_train<MODE_CLUSTER, false, false>;
+    if (keyed)
+        return smem_states ? (const void *)k_train<MODE_GRID, true, true>
+                           : (const void *)k_train<MODE_GRID, false, true>;
+    return smem_states ? (const void *)k_train<MODE_GRID, true, false>
+                       : (const void *)k_train<MODE_GRID, false, false>;
 }
+
+// Keyed-path key buffer budget: runs longer than this are launched in chunks.
+constexpr size_t kKeyBufferBytes = size_t(1) << 30;
+
+}  // namespace
+
+namespace tmb {
+int64_t g_train_key_chunk = 0;  // tmb_set_option("train.key_chunk"): test override
+}
+
+namespace {
 
 }  // namespace
 
@@ -723,6 +912,10 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     k.fp = make_fb_params(c.s, c.boost, c.state_min, c.state_max);
     k.fb_seed = derive_stream(c.seed, 0xFEED);
     per_cta_maxima(k);
+    // keyed flag path: grid mode, one block, keys of one step <= 32 KB
+    // (flags bit 1 forces the per-CTA draw path)
+    k.Cw = (int)(((C + 1) / 2 + 3) / 4 * 4);
+    k.keyed = (!cluster && c.n_blocks == 1 && !(c.flags & 2) && 8LL * k.Cw <= 32768) ? 1 : 0;
     if (cluster && k.cmax > 32 * 1024)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: too many clauses per CTA");
 
@@ -739,7 +932,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
         return fail(TMB_E_UNSUPPORTED,
                     "trainer_create: per-CTA include masks exceed shared memory (" +
                         std::to_string(need) + " B); use more CTAs");
-    const void *fn = kernel_for(cluster, smem_states);
+    const void *fn = kernel_for(cluster, smem_states, k.keyed);
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
     if (cluster) {
         if (n_cta > 8)
@@ -805,6 +998,8 @@ int tmb_trainer_destroy(tmb_trainer *t) {
     if (!t) return TMB_OK;
     if (t->block_seeds_d) cudaFree(t->block_seeds_d);
     if (t->ring_d) cudaFree(t->ring_d);
+    if (t->keys_d) cudaFree(t->keys_d);
+    if (t->nrand_d) cudaFree(t->nrand_d);
     delete t;
     return TMB_OK;
 }
@@ -831,7 +1026,7 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     k.lit_words = lit_words; k.labels = labels; k.order = order;
     k.n_steps = n_steps; k.fb_counter0 = fb_counter; k.stats = stats;
     void *args[] = {&k};
-    const void *fn = kernel_for(t->cluster, t->smem_states);
+    const void *fn = kernel_for(t->cluster, t->smem_states, k.keyed);
     if (t->cluster) {
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute at[1];
@@ -846,23 +1041,52 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         lc.attrs = at;
         lc.numAttrs = 1;
         TMB_CUDA(cudaLaunchKernelExC(&lc, fn, args));
-    } else {
-        if (t->ring_cap < n_steps) {
-            if (t->ring_d) {
-                cudaStreamSynchronize(st);
-                cudaFree(t->ring_d);
-            }
-            t->ring_d = nullptr;
-            t->ring_cap = 0;
-            TMB_CUDA(cudaMalloc(&t->ring_d, 16 * (size_t)n_steps));
-            t->ring_cap = n_steps;
+        TMB_LAUNCHED();
+        return TMB_OK;
+    }
+    // grid mode; keyed runs are split into chunks whose keys fit the buffer
+    int64_t chunk = n_steps;
+    if (k.keyed) {
+        chunk = std::max<int64_t>(1, (int64_t)(kKeyBufferBytes / (8 * (size_t)k.Cw)));
+        if (g_train_key_chunk > 0) chunk = std::min(chunk, g_train_key_chunk);
+    }
+    const int64_t slots = std::min(n_steps, chunk);
+    if (t->ring_cap < slots || (k.keyed && t->key_cap < slots)) {
+        cudaStreamSynchronize(st);
+        if (t->ring_d) cudaFree(t->ring_d);
+        if (t->keys_d) cudaFree(t->keys_d);
+        if (t->nrand_d) cudaFree(t->nrand_d);
+        t->ring_d = nullptr; t->keys_d = nullptr; t->nrand_d = nullptr;
+        t->ring_cap = 0; t->key_cap = 0;
+        TMB_CUDA(cudaMalloc(&t->ring_d, 16 * (size_t)slots));
+        t->ring_cap = slots;
+        if (k.keyed) {
+            TMB_CUDA(cudaMalloc(&t->keys_d, 8 * (size_t)k.Cw * (size_t)slots));
+            TMB_CUDA(cudaMalloc(&t->nrand_d, 4 * (size_t)slots));
+            t->key_cap = slots;
         }
+    }
+    const uint64_t step_draws = 1ull + 2ull * (uint64_t)k.C;
+    for (int64_t off = 0; off < n_steps; off += chunk) {
+        const int64_t n = std::min(chunk, n_steps - off);
+        k.order = order + off;
+        k.n_steps = n;
+        k.fb_counter0 = fb_counter + (uint64_t)off * step_draws;
         k.rec = t->ring_d;
-        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 16 * (size_t)n_steps, st));
+        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 16 * (size_t)n, st));
+        if (k.keyed) {
+            k.keys = t->keys_d;
+            k.nrand = t->nrand_d;
+            const int64_t elems = n * 2 * (int64_t)k.Cw;
+            const int blocks = (int)std::min<int64_t>((elems + 255) / 256, (int64_t)sm_count() * 16);
+            k_flag_keys<<<blocks, 256, 0, st>>>(k.fb_seed, k.fb_counter0, k.C, k.Cw, k.K, n,
+                                                 t->keys_d, t->nrand_d);
+            TMB_LAUNCHED();
+        }
         TMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(t->n_cta), dim3(t->threads), args,
                                              (size_t)t->smem, st));
+        TMB_LAUNCHED();
     }
-    TMB_LAUNCHED();
     return TMB_OK;
 }
 

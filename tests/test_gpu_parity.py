@@ -168,17 +168,21 @@ def test_mnist_shaped_prefix_golden(gpu):
     assert np.array_equal(gpu.dataset_votes(run.model, (g["ex"], g["ey"])), g["votes"])
 
 
-@pytest.mark.parametrize("n_cta,hbm", [(0, False), (0, True), (148, False), (148, True),
-                                       (5, False), (64, True)])
-def test_mnist_shaped_longer_vs_oracle(gpu, oracle, n_cta, hbm):
+@pytest.mark.parametrize("n_cta,hbm,n_blocks,keys", [
+    (0, False, 5, True), (0, True, 5, True), (148, False, 5, True), (148, True, 5, True),
+    (5, False, 5, True), (64, True, 5, True),
+    (148, False, 1, True), (148, True, 1, True), (148, False, 1, False), (37, False, 1, True)])
+def test_mnist_shaped_longer_vs_oracle(gpu, oracle, n_cta, hbm, n_blocks, keys):
     """2 epochs over 1500 examples of the config-2 shapes against the oracle,
     in cluster mode (<= 16 CTAs, DSMEM exchange) and grid mode (cooperative
-    grid, global barrier), with per-block counters via n_blocks=5."""
+    grid, global barrier), with per-block counters via n_blocks=5, and with
+    one block through both flag paths (precomputed 16-bit keys: ~180 key
+    ties resolved exactly over the run; per-CTA draws)."""
     (tx, ty), (ex, ey) = gpu.datasets.mnist_shaped(n_train=1500, n_test=300, data_seed=3)
     kw = gpu.datasets.mnist_shaped_config_kwargs(seed=9)
-    kw["n_blocks"] = 5
+    kw["n_blocks"] = n_blocks
     cfg = gpu.Config(**kw)
-    sess = gpu.DenseTrainSession(cfg, tx, ty, n_cta=n_cta, states_in_hbm=hbm)
+    sess = gpu.DenseTrainSession(cfg, tx, ty, n_cta=n_cta, states_in_hbm=hbm, flag_keys=keys)
     for _ in range(2):
         sess.run_epoch()
     m = sess.model()
@@ -187,6 +191,25 @@ def test_mnist_shaped_longer_vs_oracle(gpu, oracle, n_cta, hbm):
     assert np.array_equal(m.weights, ost.weights)
     assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64),
                           ost.block_counters)
+
+
+def test_keyed_trainer_chunked_launches(gpu, oracle):
+    """The keyed trainer splits long runs into launches whose keys fit its
+    buffer; a tiny forced chunk (and one not dividing the epoch) must give
+    the same model."""
+    (tx, ty), _ = gpu.datasets.mnist_shaped(n_train=700, n_test=10, data_seed=4)
+    cfg = gpu.Config(**gpu.datasets.mnist_shaped_config_kwargs(seed=2))
+    ost, _ = oracle.train(cfg, tx, ty, 1)
+    try:
+        for chunk in (1, 97):
+            gpu._lib.call("tmb_set_option", b"train.key_chunk", chunk)
+            sess = gpu.DenseTrainSession(cfg, tx, ty, n_cta=148)
+            sess.run_epoch()
+            m = sess.model()
+            assert np.array_equal(m.states, ost.states), chunk
+            assert np.array_equal(m.weights, ost.weights), chunk
+    finally:
+        gpu._lib.call("tmb_set_option", b"train.key_chunk", 0)
 
 
 def test_predictor_golden(gpu):

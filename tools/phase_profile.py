@@ -16,7 +16,7 @@ import paper_2405_04212_b200 as tmb  # noqa: E402
 from paper_2405_04212_b200 import _lib, datasets  # noqa: E402
 from paper_2405_04212_b200.runtime import ptr  # noqa: E402
 
-NAMES = ["eval", "votes+arrive", "precompute+prefetch", "wait+decide", "flag bitmaps",
+NAMES = ["eval(+votes)", "arrive", "precompute", "wait+decide", "flag count/bitmaps",
          "scan+events", "feedback", "-"]
 
 ap = argparse.ArgumentParser()
@@ -24,13 +24,15 @@ ap.add_argument("--cta", type=int, nargs="*", default=[16, 148])
 ap.add_argument("--threads", type=int, default=0)
 ap.add_argument("--epochs", type=int, default=4)
 ap.add_argument("--n-train", type=int, default=60000)
+ap.add_argument("--no-keys", action="store_true", help="per-CTA flag draws instead of keys")
 args = ap.parse_args()
 
 (tx, ty), _ = datasets.mnist_shaped(n_train=args.n_train, n_test=10)
 clk_hz = torch.cuda.get_device_properties(0).clock_rate * 1e3
 for n_cta in args.cta:
     cfg = tmb.Config(**datasets.mnist_shaped_config_kwargs(seed=0))
-    sess = tmb.DenseTrainSession(cfg, tx, ty, n_cta=n_cta, threads=args.threads)
+    sess = tmb.DenseTrainSession(cfg, tx, ty, n_cta=n_cta, threads=args.threads,
+                                 flag_keys=not args.no_keys)
     for _ in range(args.epochs - 1):
         sess.run_epoch()
     ph = torch.zeros(sess.launch["n_cta"] * 8, dtype=torch.int64, device="cuda")
