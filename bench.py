@@ -283,6 +283,12 @@ def bench_c2_train(args, rank, world, local):
     int_ops_ex = draws_per_ex * 30 + C * W * 3
     int_peak = sm_count * 128 * f_sm  # ALU + FMA pipes, 64 lanes/clk each
     int_achieved = int_ops_ex * ex_per_launch / (per_launch_ms / 1e3)
+    # latency floor of sequential online training: one grid-wide all-reduce
+    # per example, measured live by the same relaxed-atomic scheme in isolation
+    import ctypes as ct
+    floor = ct.c_double()
+    _lib.call("tmb_microbench_allreduce", sess.launch["n_cta"], 512, 20000, 0, ct.byref(floor))
+    us_ex = per_launch_ms * 1e3 / ex_per_launch
 
     line = {
         "metric": "train examples/sec (configs[1] MNIST-shaped CoTM training)",
@@ -302,7 +308,8 @@ def bench_c2_train(args, rank, world, local):
         "work": {"events_per_example": ev_per_ex, "draws_per_example": draws_per_ex,
                  "type_i_per_example": dstats["type_i"] / max(dstats["examples"], 1),
                  "state_updates_per_example": dstats["state_updates"] / max(dstats["examples"], 1)},
-        "roofline": {"kernel": "k_train<true> (fused persistent trainer)", "bound": "hbm",
+        "roofline": {"kernel": "k_step_records + k_train_fast (fused persistent trainer)",
+                     "bound": "hbm",
                      "achieved": achieved_gbs, "peak": HBM_PEAK, "unit": "GB/s",
                      "frac": achieved_gbs / HBM_PEAK, "traffic": None,
                      "peak_source": HBM_PEAK_SRC,
@@ -315,7 +322,11 @@ def bench_c2_train(args, rank, world, local):
                          "peak": int_peak / 1e12, "unit": "Tops/s",
                          "frac": int_achieved / int_peak,
                          "ops_per_example": int_ops_ex,
-                         "us_per_example": per_launch_ms * 1e3 / ex_per_launch},
+                         "us_per_example": us_ex},
+        "roofline_latency": {"bound": "one grid all-reduce per example (sequential training)",
+                             "floor_us_per_example": floor.value, "achieved_us_per_example": us_ex,
+                             "frac": floor.value / us_ex,
+                             "floor_source": "tmb_microbench_allreduce mode 0, same CTA count"},
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "examples/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),

@@ -72,6 +72,8 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int sm_count();
-extern int64_t g_train_key_chunk;  // keyed trainer: steps per launch override (tmb_train.cu)
+extern int64_t g_train_key_chunk;
+extern int g_train_dbg;  // trainer timing ablations (tmb_train.cu)
+//  // keyed trainer: steps per launch override (tmb_train.cu)
 
 }  // namespace tmb

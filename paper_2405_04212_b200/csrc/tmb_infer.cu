@@ -922,6 +922,10 @@ int tmb_set_option(const char *name, int64_t value) {
         g_train_key_chunk = value;
         return TMB_OK;
     }
+    if (std::string(name) == "train.debug_skip") {  // timing ablations only (not bit-exact)
+        g_train_dbg = (int)value;
+        return TMB_OK;
+    }
     if (std::string(name) == "infer.debug_skip") {  // timing experiments only
         g_infer_dbg = (int)value;
         return TMB_OK;

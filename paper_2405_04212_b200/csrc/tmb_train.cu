@@ -21,13 +21,17 @@
 //     and two hardware cluster barriers per example -- no global memory
 //     round trips on the critical path.
 //   GRID mode (n_cta > 16, cooperative launch, up to one CTA per SM): two
-//     relaxed 64-bit atomics per CTA + a spin per example.  With one block
-//     (the common case) the update-flag draws of a whole run are generated up
-//     front by k_flag_keys as 16-bit keys (the top bits of each 53-bit draw,
-//     exact compare only on a key tie), streamed one example ahead into
-//     shared memory with cp.async, and counted with SIMD byte-pair compares;
-//     otherwise the CTA's block range of draws is computed while the spin is
-//     pending.
+//     relaxed 64-bit atomics per CTA + a spin per example; the CTA's block
+//     range of update-flag draws is computed while the spin is pending.
+//
+//   FAST grid mode (k_train_fast: one block, C <= 65536, the common case):
+//     a pre-pass (k_step_records) builds one record per step -- example,
+//     label, negative class, literal row and the step's update-flag draws as
+//     16-bit keys bucketed by their top byte -- which the trainer streams two
+//     steps ahead into shared memory with cp.async.  Next-example clause
+//     outputs are computed while the all-reduce is pending (only clauses the
+//     feedback changed are re-evaluated afterwards), and the events of a step
+//     are read straight off the key buckets below the decision thresholds.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -43,15 +47,15 @@ namespace tmb {
 struct TrainK {
     int C, P, K, W, Ppad, n_blocks, n_cta, cmax, fmax_words, bmax;
     int vec4;  // states rows 4-byte addressable in global memory
-    int keyed, Cw;  // keyed flag path; u32 words (2 keys) per stream, % 4 == 0
+    int fast, Wp, Cp, R;  // fast path: padded literal words / clauses, record words
+    int dbg;        // timing ablations only (tmb_set_option "train.debug_skip")
     int64_t budget, T;
     FbParams fp;
     uint64_t fb_seed, fb_counter0;
     int64_t n_steps;
     const uint32_t *lit_words;
     const int32_t *labels, *order;
-    const uint32_t *keys;  // keyed: [n_steps][2][Cw] packed 16-bit flag keys
-    const int32_t *nrand;  // keyed: [n_steps] int(u * (K - 1)) of the negative draw
+    const uint32_t *recs;  // fast: [n_steps][R] step records (k_step_records)
     int8_t *states;
     int32_t *weights;
     uint64_t *block_counters;
@@ -101,8 +105,9 @@ struct Smem {
     long long *vsum;   // grid: [2] summed votes
     int *misc;         // [0]=n_work [3..5]=example ring [8..10]=label ring
     uint64_t *thr;     // grid: [0]=t_t [1]=t_n [2]=negative
-    uint32_t *keys;    // keyed: [2 buffers][2 streams][Cw]
-    unsigned *wcnt;    // keyed: [16] per-warp prefix events, [16] per-warp totals
+    uint32_t *rec3;    // fast: [3][R] step records in flight
+    int *nout, *oflag; // fast: [2][cmax] next-example outputs; [cmax] own event flags
+    unsigned *wcnt;    // per-warp event counts [32]
     unsigned long long *vacc;  // grid: [2] CTA partial votes (label, negative)
 };
 
@@ -136,9 +141,11 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.un_bits = (uint32_t *)take(4 * k.fmax_words);
     t.word_cum = (int32_t *)take(4 * (k.fmax_words + 1));
     const bool pre = 32 * k.fmax_words <= kMaxPrecompute;
-    t.draw_t = pre && !k.keyed ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
-    t.draw_n = pre && !k.keyed ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
-    t.keys = k.keyed ? (uint32_t *)take(4 * 4 * (size_t)k.Cw) : nullptr;
+    t.draw_t = pre && !k.fast ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
+    t.draw_n = pre && !k.fast ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
+    t.rec3 = k.fast ? (uint32_t *)take(4 * 3 * (size_t)k.R) : nullptr;
+    t.nout = k.fast ? (int *)take(4 * 2 * (size_t)k.cmax) : nullptr;
+    t.oflag = k.fast ? (int *)take(4 * (size_t)k.cmax) : nullptr;
     t.wcnt = (unsigned *)take(4 * 32);
     t.vacc = (unsigned long long *)take(8 * 2);
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
@@ -326,7 +333,7 @@ __device__ __forceinline__ void flush_stats(const TrainK &k, Counters &cn, bool 
 constexpr int kRowRegs = 4;  // literal words per thread (W <= 4 * blockDim)
 struct Prefetch {
     uint32_t row[kRowRegs];
-    int label, ex2, nr;
+    int label, ex2;
 };
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
@@ -336,19 +343,9 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Keyed path: step i's flag keys (both streams) into key buffer i & 1.
-__device__ __forceinline__ void keys_issue(const TrainK &k, const Smem &s, int64_t i) {
-    const uint32_t *src = k.keys + i * 2 * (int64_t)k.Cw;
-    uint32_t *dst = s.keys + (i & 1) * 2 * k.Cw;
-    for (int q = threadIdx.x; q < k.Cw / 2; q += blockDim.x) cp_async16(dst + 4 * q, src + 4 * q);
-    cp_async_commit();
-}
-
-template <bool KEYS>
 __device__ __forceinline__ void prefetch_issue(const TrainK &k, const Smem &s, int64_t i,
                                                Prefetch &pf) {
     if (i + 1 >= k.n_steps) return;
-    if (KEYS) keys_issue(k, s, i + 1);
     const int ex = s.misc[3 + (int)((i + 1) % 3)];
 #pragma unroll
     for (int q = 0; q < kRowRegs; ++q) {
@@ -357,16 +354,13 @@ __device__ __forceinline__ void prefetch_issue(const TrainK &k, const Smem &s, i
     }
     if (threadIdx.x == blockDim.x - 1) {
         pf.label = __ldg(&k.labels[ex]);
-        if (KEYS) pf.nr = __ldg(&k.nrand[i + 1]);
         if (i + 2 < k.n_steps) pf.ex2 = __ldg(&k.order[i + 2]);
     }
 }
 
-template <bool KEYS>
 __device__ __forceinline__ void prefetch_commit(const TrainK &k, const Smem &s, int64_t i,
                                                 const Prefetch &pf) {
     if (i + 1 >= k.n_steps) return;
-    if (KEYS) cp_async_wait_all();
     uint32_t *dst = ((i + 1) & 1) ? s.lit1 : s.lit0;
 #pragma unroll
     for (int q = 0; q < kRowRegs; ++q) {
@@ -375,18 +369,14 @@ __device__ __forceinline__ void prefetch_commit(const TrainK &k, const Smem &s, 
     }
     if (threadIdx.x == blockDim.x - 1) {
         s.misc[8 + (int)((i + 1) % 3)] = pf.label;
-        if (KEYS) s.misc[12 + (int)((i + 1) % 3)] = pf.nr;
         if (i + 2 < k.n_steps) s.misc[3 + (int)((i + 2) % 3)] = pf.ex2;
     }
 }
 
-template <bool KEYS>
 __device__ __forceinline__ void prologue_ring(const TrainK &k, const Smem &s) {
-    if (KEYS) keys_issue(k, s, 0);
     if (threadIdx.x == 0) {
         s.misc[3] = __ldg(&k.order[0]);
         s.misc[8] = __ldg(&k.labels[s.misc[3]]);
-        if (KEYS) s.misc[12] = __ldg(&k.nrand[0]);
         if (k.n_steps > 1) s.misc[4] = __ldg(&k.order[1]);
         s.vacc[0] = 0;
         s.vacc[1] = 0;
@@ -395,19 +385,25 @@ __device__ __forceinline__ void prologue_ring(const TrainK &k, const Smem &s) {
     const int ex = s.misc[3];
     for (int w = threadIdx.x; w < k.W; w += blockDim.x)
         s.lit0[w] = __ldg(&k.lit_words[(int64_t)ex * k.W + w]);
-    if (KEYS) cp_async_wait_all();
 }
 
-// feedback.py:33-44: clipped update probabilities -> integer thresholds.
+// feedback.py:33-44: update probability (a / 2T, a in [0, 2T]) -> integer
+// threshold.  The saturated ends are common once the class sums reach T and
+// would take the division's slow path (zero numerator), so they are exact
+// constants here.
+__device__ __forceinline__ uint64_t threshold_of(long long a, long long T) {
+    if (a <= 0) return 0;
+    if (a >= 2 * T) return 1ull << 53;
+    return prob_threshold((double)a / (2.0 * (double)T));
+}
+
 __device__ __forceinline__ void decide(const TrainK &k, long long vl, long long vn,
                                        uint64_t &t_t, uint64_t &t_n) {
     const long long T = k.T;
     const long long cl = vl < -T ? -T : (vl > T ? T : vl);
     const long long cn = vn < -T ? -T : (vn > T ? T : vn);
-    const double pt = (double)(T - cl) / (2.0 * (double)T);
-    const double pn = (double)(T + cn) / (2.0 * (double)T);
-    t_t = prob_threshold(pt);
-    t_n = prob_threshold(pn);
+    t_t = threshold_of(T - cl, T);
+    t_n = threshold_of(T + cn, T);
 }
 
 __device__ __forceinline__ int negative_class(const TrainK &k, int label, uint64_t fbc) {
@@ -416,43 +412,49 @@ __device__ __forceinline__ int negative_class(const TrainK &k, int label, uint64
     return neg >= k.K ? neg - k.K : neg;
 }
 
-// Update flags of clauses j0, j0 + 1 of one stream from their packed 16-bit
-// keys (key = draw53 >> 37): bit 0 / bit 16.  A key equal to the threshold's
-// top bits is resolved with the exact draw (probability 2^-16 per flag).
-__device__ __forceinline__ uint32_t flag_pair(uint32_t v, uint64_t t, uint64_t seed,
-                                              uint64_t ctr_j0) {
-    const uint32_t tb = (uint32_t)(t >> 37);
-    if (tb >= 65536u) return 0x00010001u;  // p == 1
-    const uint32_t tb2 = tb | (tb << 16);
-    uint32_t lt = __vcmpltu2(v, tb2) & 0x00010001u;
-    const uint32_t eq = __vcmpeq2(v, tb2) & 0x00010001u;
-    if (eq) {
-        if ((eq & 1u) && draw53(seed, ctr_j0) < t) lt |= 1u;
-        if ((eq >> 16) && draw53(seed, ctr_j0 + 1) < t) lt |= 0x10000u;
+// Event bookkeeping of own clause j (kernels/_numba.py:101-125): window
+// ordinal `ord` of its first event, event types, feedback-then-weight
+// and the work list.  s.info[j] & I_OUT holds its output.
+__device__ __forceinline__ void apply_events(const TrainK &k, const Smem &s, Counters &cn, int j,
+                                             bool t_ev, bool n_ev, uint64_t ord, uint64_t bseed,
+                                             int label, int neg) {
+    int info = s.info[j] & I_OUT;
+    if (t_ev || n_ev) {
+        const bool out = info & I_OUT;
+        int32_t *w = s.weights + j * k.K;
+        const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
+        if (t_ev) {
+            info |= I_TEV | (t1 ? I_T1 : 0);
+            s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
+            ++cn.events;
+            if (t1) ++cn.t1; else if (out) ++cn.t2;
+        }
+        if (n_ev) {
+            const uint64_t o2 = ord + (t_ev ? 1 : 0);
+            info |= I_NEV | (n1 ? I_N1 : 0);
+            s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
+            ++cn.events;
+            if (n1) ++cn.t1; else if (out) ++cn.t2;
+        }
+        if (out) {
+            if (t_ev) w[label] += 1;
+            if (n_ev) w[neg] -= 1;
+        }
+        if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
+            s.work[atomicAdd(&s.misc[0], 1)] = j;
     }
-    return lt;
+    s.info[j] = info;
 }
 
-// k_flag_keys: the update-flag draws of steps [0, n_steps) as packed 16-bit
-// keys, plus the negative-class draw (feedback.py:47-53, same counters as
-// the per-CTA path).  Padding keys are 0xFFFF and masked by the counter.
-__global__ void k_flag_keys(uint64_t seed, uint64_t fbc0, int C, int Cw, int K, int64_t n_steps,
-                            uint32_t *keys, int32_t *nrand) {
-    const int64_t per = 2LL * Cw, total = n_steps * per;
-    const uint64_t step_draws = 1ull + 2ull * (uint64_t)C;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / per;
-        const int r = (int)(e - i * per);
-        const int str = r >= Cw ? 1 : 0;
-        const int j0 = 2 * (r - str * Cw);
-        const uint64_t fbc = fbc0 + (uint64_t)i * step_draws;
-        const uint64_t base = fbc + 1 + (str ? (uint64_t)C : 0);
-        const uint32_t lo = j0 < C ? (uint32_t)(draw53(seed, base + j0) >> 37) : 0xFFFFu;
-        const uint32_t hi = j0 + 1 < C ? (uint32_t)(draw53(seed, base + j0 + 1) >> 37) : 0xFFFFu;
-        keys[e] = lo | (hi << 16);
-        if (r == 0) nrand[i] = (int)(u01_from53(draw53(seed, fbc)) * (double)(K - 1));
-    }
+// Training-mode output of own clause j against literal row `lit` (warp-
+// collective; kernels/_numba.py:36-50): no included literal false and the
+// include count within the budget.
+__device__ __forceinline__ bool clause_out(const TrainK &k, const Smem &s, int j,
+                                           const uint32_t *lit) {
+    uint32_t viol = 0;
+    for (int w = (int)(threadIdx.x & 31); w < k.W; w += 32) viol |= s.masks[j * k.W + w] & ~lit[w];
+    viol = __reduce_or_sync(0xffffffffu, viol);
+    return viol == 0 && s.cnt[j] <= k.budget;
 }
 
 __device__ __forceinline__ void cluster_arrive() {
@@ -466,15 +468,31 @@ __device__ __forceinline__ void cluster_wait() {
 // clock64 deltas between consecutive PHASE marks.
 #define PHASE(n)                                                          \
     do {                                                                  \
-        if (prof && tid == 0) {                                           \
+        if (prof && warp == 0) {                                          \
             const long long now = clock64();                              \
             ph[n] += (unsigned long long)(now - t_mark);                  \
             t_mark = now;                                                 \
         }                                                                 \
     } while (0)
 
+// Grid-mode timeline (profiling): %globaltimer of thread 0 at arrival,
+// all-reduce detection and step end for steps [64, 128), stored after the
+// phase array as [64][n_cta][3].
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TIMELINE(i, q)                                                              \
+    do {                                                                            \
+        if (prof && warp == 0 && (i) >= 64 && (i) < 128) {                          \
+            const unsigned long long g_ = gtimer();                                 \
+            if (lane == 0) k.phase[n_cta * 8 + (((i) - 64) * n_cta + rank) * 3 + (q)] = g_; \
+        }                                                                           \
+    } while (0)
+
 // One fused kernel, two synchronisation domains (see the header comment).
-template <int MODE, bool SMEM_STATES, bool KEYS>
+template <int MODE, bool SMEM_STATES>
 __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
     extern __shared__ __align__(16) char smem_raw[];
     Smem s;
@@ -498,7 +516,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         s.blk_ctr[i] = k.block_counters[b0 + i];
         s.blk_seed[i] = k.block_seeds[b0 + i];
     }
-    prologue_ring<KEYS>(k, s);
+    prologue_ring(k, s);
     __syncthreads();
     if (MODE == MODE_CLUSTER) cg::this_cluster().sync();  // DSMEM peers resident
 
@@ -508,56 +526,17 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
     long long t_mark = clock64();
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
 
-    // Event bookkeeping of own clause j (kernels/_numba.py:101-125): window
-    // ordinal `ord` of its first event, event types, feedback-then-weight
-    // and the work list.
-    auto apply_events = [&](int j, bool t_ev, bool n_ev, uint64_t ord, uint64_t bseed,
-                            int label, int neg) {
-        int info = s.info[j] & I_OUT;
-        if (t_ev || n_ev) {
-            const bool out = info & I_OUT;
-            int32_t *w = s.weights + j * K;
-            const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
-            if (t_ev) {
-                info |= I_TEV | (t1 ? I_T1 : 0);
-                s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
-                ++cn.events;
-                if (t1) ++cn.t1; else if (out) ++cn.t2;
-            }
-            if (n_ev) {
-                const uint64_t o2 = ord + (t_ev ? 1 : 0);
-                info |= I_NEV | (n1 ? I_N1 : 0);
-                s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
-                ++cn.events;
-                if (n1) ++cn.t1; else if (out) ++cn.t2;
-            }
-            if (out) {
-                if (t_ev) w[label] += 1;
-                if (n_ev) w[neg] -= 1;
-            }
-            if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
-                s.work[atomicAdd(&s.misc[0], 1)] = j;
-        }
-        s.info[j] = info;
-    };
-
     for (int64_t i = 0; i < k.n_steps; ++i) {
         const uint32_t *lit = (i & 1) ? s.lit1 : s.lit0;
         const int label = s.misc[8 + (int)(i % 3)];
         const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
-        int neg;
-        if (KEYS) {
-            neg = label + 1 + s.misc[12 + (int)(i % 3)];
-            if (neg >= K) neg -= K;
-        } else {
-            neg = negative_class(k, label, fbc);
-        }
+        const int neg = negative_class(k, label, fbc);
         Prefetch pf;
-        prefetch_issue<KEYS>(k, s, i, pf);
+        prefetch_issue(k, s, i, pf);
         // 1. training-mode outputs of own clauses (kernels/_numba.py:36-50);
         //    grid mode folds the two class sums the decision reads
         //    (dense.py:153 restricted to label / negative) into the same pass
-        for (int j = warp; j < cown; j += nwarps) {
+        for (int j = warp; j < ((k.dbg & 2) ? 0 : cown); j += nwarps) {
             uint32_t viol = 0;
             for (int w = lane; w < k.W; w += 32) viol |= s.masks[j * k.W + w] & ~lit[w];
             viol = __reduce_or_sync(0xffffffffu, viol);
@@ -597,11 +576,12 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             s.vacc[1] = 0;
             red_relaxed_add_u64(&k.rec[i * 2 + 0], (1ull << 40) + (unsigned long long)(vl + kVoteBias));
             red_relaxed_add_u64(&k.rec[i * 2 + 1], (1ull << 40) + (unsigned long long)(vn + kVoteBias));
+            TIMELINE(i, 0);
         }
         PHASE(1);
         // while the all-reduce is pending: update-flag draws for [fs, fe)
         // (feedback.py:47-53; independent of the votes)
-        if (!KEYS && pre) {
+        if (pre) {
             for (int idx = tid; idx < nfw * 32; idx += nthr) {
                 const int j = fsa + idx;
                 s.draw_t[idx] = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
@@ -636,10 +616,12 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 do {
                     p = ld_relaxed_v2u64(&k.rec[i * 2]);
                 } while ((p.x >> 40) != want || (p.y >> 40) != want);
+                TIMELINE(i, 1);
                 const long long bias = (long long)n_cta * kVoteBias;
                 const long long vl = (long long)(p.x & ((1ull << 40) - 1)) - bias;
                 const long long vn = (long long)(p.y & ((1ull << 40) - 1)) - bias;
                 decide(k, vl, vn, t_t, t_n);
+                if (k.dbg & 4) t_t = t_n = 0;
                 s.thr[0] = t_t;
                 s.thr[1] = t_n;
                 if (k.trace && rank == 0) {
@@ -653,151 +635,92 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             t_n = s.thr[1];
         }
         PHASE(3);
-        if (KEYS) {
-            // 3. events over [0, c0) and [0, C) from the step's keys
-            const uint32_t *kt = s.keys + (i & 1) * 2 * k.Cw, *kn = kt + k.Cw;
-            const uint64_t ct = fbc + 1, cnn = fbc + 1 + (uint64_t)C;
-            unsigned pre_ev = 0, tot_ev = 0;
-            for (int w = tid; 2 * w < C; w += nthr) {
-                const int j0 = 2 * w;
-                const uint32_t f = flag_pair(kt[w], t_t, k.fb_seed, ct + j0) +
-                                   flag_pair(kn[w], t_n, k.fb_seed, cnn + j0);
-                const uint32_t valid = j0 + 1 < C ? 0xFFFFFFFFu : 0xFFFFu;
-                const uint32_t prem = j0 + 1 < c0 ? 0xFFFFFFFFu : (j0 < c0 ? 0xFFFFu : 0u);
-                const uint32_t fv = f & valid;  // two 16-bit counts, each <= 2
-                tot_ev += (fv & 0xFFFFu) + (fv >> 16);
-                pre_ev += (fv & prem & 0xFFFFu) + ((fv & prem) >> 16);
+        // 3. update flags over [fs, fe) as bitmaps
+        for (int idx = tid; idx < nfw * 32; idx += nthr) {
+            const int j = fsa + idx;
+            const bool valid = j >= fs && j < fe;
+            uint64_t mt, mn;
+            if (pre) {
+                mt = s.draw_t[idx];
+                mn = s.draw_n[idx];
+            } else {
+                mt = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
+                mn = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
             }
-            pre_ev = __reduce_add_sync(0xffffffffu, pre_ev);
-            tot_ev = __reduce_add_sync(0xffffffffu, tot_ev);
+            const unsigned wt = __ballot_sync(0xffffffffu, valid && mt < t_t);
+            const unsigned wn = __ballot_sync(0xffffffffu, valid && mn < t_n);
             if (lane == 0) {
-                s.wcnt[warp] = pre_ev;
-                s.wcnt[16 + warp] = tot_ev;
+                s.ut_bits[idx >> 5] = wt;
+                s.un_bits[idx >> 5] = wn;
             }
-            __syncthreads();
-            PHASE(4);
-            // 4-5. warp 0: ordinals of the own clauses' events
-            if (warp == 0) {
-                unsigned pv = lane < nwarps ? s.wcnt[lane] : 0u;
-                unsigned tv = lane < nwarps ? s.wcnt[16 + lane] : 0u;
-                pv = __reduce_add_sync(0xffffffffu, pv);
-                tv = __reduce_add_sync(0xffffffffu, tv);
-                const uint64_t base = s.blk_ctr[0] + pv;
-                unsigned carry = 0;
-                for (int jb = 0; jb < cown; jb += 32) {
-                    const int j = jb + lane;
-                    bool t_ev = false, n_ev = false;
-                    if (j < cown) {
-                        const int c = c0 + j, sh = 16 * (c & 1);
-                        const uint32_t ft = flag_pair(kt[c >> 1], t_t, k.fb_seed, ct + (c & ~1));
-                        const uint32_t fn = flag_pair(kn[c >> 1], t_n, k.fb_seed, cnn + (c & ~1));
-                        t_ev = (ft >> sh) & 1u;
-                        n_ev = (fn >> sh) & 1u;
-                    }
-                    const unsigned v = (unsigned)t_ev + (unsigned)n_ev;
-                    unsigned x = v;
+        }
+        __syncthreads();
+        PHASE(4);
+        // 4-5. warp 0: exclusive prefix of events per flag word, then
+        //      window ordinals and the work list of the own clauses
+        if (warp == 0) {
+            int carry = 0;
+            for (int base = 0; base < nfw; base += 32) {
+                const int w = base + lane;
+                const int v = w < nfw ? __popc(s.ut_bits[w]) + __popc(s.un_bits[w]) : 0;
+                int x = v;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-                        if (lane >= o) x += y;
-                    }
-                    if (j < cown)
-                        apply_events(j, t_ev, n_ev, base + carry + (x - v), s.blk_seed[0], label, neg);
-                    carry += __shfl_sync(0xffffffffu, x, 31);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
                 }
-                __syncwarp();
-                if (lane == 0) {
-                    s.blk_ctr[0] += (uint64_t)tv;
-                    if (k.trace && rank == 0) k.trace[i * 4 + 3] = tv;
-                }
+                if (w < nfw) s.word_cum[w] = carry + x - v;
+                carry += __shfl_sync(0xffffffffu, x, 31);
             }
-        } else {
-            // 3. update flags over [fs, fe) as bitmaps
-            for (int idx = tid; idx < nfw * 32; idx += nthr) {
-                const int j = fsa + idx;
-                const bool valid = j >= fs && j < fe;
-                uint64_t mt, mn;
-                if (pre) {
-                    mt = s.draw_t[idx];
-                    mn = s.draw_n[idx];
-                } else {
-                    mt = draw53(k.fb_seed, fbc + 1 + (uint64_t)j);
-                    mn = draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)j);
-                }
-                const unsigned wt = __ballot_sync(0xffffffffu, valid && mt < t_t);
-                const unsigned wn = __ballot_sync(0xffffffffu, valid && mn < t_n);
-                if (lane == 0) {
-                    s.ut_bits[idx >> 5] = wt;
-                    s.un_bits[idx >> 5] = wn;
-                }
+            if (lane == 0) {
+                s.word_cum[nfw] = carry;
+                if (k.trace && rank == 0 && fs == 0 && fe == C) k.trace[i * 4 + 3] = carry;
             }
-            __syncthreads();
-            PHASE(4);
-            // 4-5. warp 0: exclusive prefix of events per flag word, then
-            //      window ordinals and the work list of the own clauses
-            if (warp == 0) {
-                int carry = 0;
-                for (int base = 0; base < nfw; base += 32) {
-                    const int w = base + lane;
-                    const int v = w < nfw ? __popc(s.ut_bits[w]) + __popc(s.un_bits[w]) : 0;
-                    int x = v;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, x, o);
-                        if (lane >= o) x += y;
+            __syncwarp();
+            auto cum = [&](int x) -> int {  // events over clauses [fsa, x)
+                const int q = (x - fsa) >> 5, r = (x - fsa) & 31;
+                int v = s.word_cum[q];
+                if (r) {
+                    const unsigned lo = (1u << r) - 1u;
+                    v += __popc(s.ut_bits[q] & lo) + __popc(s.un_bits[q] & lo);
+                }
+                return v;
+            };
+            for (int j = lane; j < cown; j += 32) {
+                const int c = c0 + j;
+                const int q = (c - fsa) >> 5, r = (c - fsa) & 31;
+                const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
+                int bi = 0;
+                uint64_t ord = 0;
+                if (t_ev || n_ev) {
+                    if (k.n_blocks == 1) {  // fs == 0: events before c in the block
+                        ord = s.blk_ctr[0] + (uint64_t)cum(c);
+                    } else {
+                        bi = block_of(c, C, k.n_blocks) - b0;
+                        ord = s.blk_ctr[bi] +
+                              (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
                     }
-                    if (w < nfw) s.word_cum[w] = carry + x - v;
-                    carry += __shfl_sync(0xffffffffu, x, 31);
                 }
-                if (lane == 0) {
-                    s.word_cum[nfw] = carry;
-                    if (k.trace && rank == 0 && fs == 0 && fe == C) k.trace[i * 4 + 3] = carry;
-                }
-                __syncwarp();
-                auto cum = [&](int x) -> int {  // events over clauses [fsa, x)
-                    const int q = (x - fsa) >> 5, r = (x - fsa) & 31;
-                    int v = s.word_cum[q];
-                    if (r) {
-                        const unsigned lo = (1u << r) - 1u;
-                        v += __popc(s.ut_bits[q] & lo) + __popc(s.un_bits[q] & lo);
-                    }
-                    return v;
-                };
-                for (int j = lane; j < cown; j += 32) {
-                    const int c = c0 + j;
-                    const int q = (c - fsa) >> 5, r = (c - fsa) & 31;
-                    const bool t_ev = (s.ut_bits[q] >> r) & 1, n_ev = (s.un_bits[q] >> r) & 1;
-                    int bi = 0;
-                    uint64_t ord = 0;
-                    if (t_ev || n_ev) {
-                        if (k.n_blocks == 1) {  // fs == 0: events before c in the block
-                            ord = s.blk_ctr[0] + (uint64_t)cum(c);
-                        } else {
-                            bi = block_of(c, C, k.n_blocks) - b0;
-                            ord = s.blk_ctr[bi] +
-                                  (uint64_t)(cum(c) - cum(block_begin(b0 + bi, C, k.n_blocks)));
-                        }
-                    }
-                    apply_events(j, t_ev, n_ev, ord, s.blk_seed[bi], label, neg);
-                }
-                __syncwarp();
-                // one window per applied event (block counters)
-                if (k.n_blocks == 1) {
-                    if (lane == 0) s.blk_ctr[0] += (uint64_t)s.word_cum[nfw];
-                } else for (int bi = lane; bi <= b1 - b0; bi += 32) {
-                    const int bs = block_begin(b0 + bi, C, k.n_blocks);
-                    const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
-                    s.blk_ctr[bi] += (uint64_t)(cum(be) - cum(bs));
-                }
+                apply_events(k, s, cn, j, t_ev, n_ev, ord, s.blk_seed[bi], label, neg);
+            }
+            __syncwarp();
+            // one window per applied event (block counters)
+            if (k.n_blocks == 1) {
+                if (lane == 0) s.blk_ctr[0] += (uint64_t)s.word_cum[nfw];
+            } else for (int bi = lane; bi <= b1 - b0; bi += 32) {
+                const int bs = block_begin(b0 + bi, C, k.n_blocks);
+                const int be = block_begin(b0 + bi + 1, C, k.n_blocks);
+                s.blk_ctr[bi] += (uint64_t)(cum(be) - cum(bs));
             }
         }
         __syncthreads();
         PHASE(5);
         // 6. per-position Type I / II updates of the work list
-        feedback_quads<SMEM_STATES>(k, s, c0, lit, s.misc[0], cn);
-        prefetch_commit<KEYS>(k, s, i, pf);
+        feedback_quads<SMEM_STATES>(k, s, c0, lit, (k.dbg & 1) ? 0 : s.misc[0], cn);
+        prefetch_commit(k, s, i, pf);
         __syncthreads();
         PHASE(6);
+        if (MODE == MODE_GRID) TIMELINE(i, 2);
     }
     if (prof && tid == 0)
         for (int q = 0; q < 8; ++q) k.phase[rank * 8 + q] = ph[q];
@@ -808,6 +731,313 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         const int last = block_begin(b + 1, C, k.n_blocks) - 1;
         if (last >= c0 && last < c1) k.block_counters[b] = s.blk_ctr[bi];
     }
+    flush_stats(k, cn, rank == 0);
+}
+
+
+// ------------------------------------------------------------- fast path --
+// Step record (u32 words): [0..3] example, label, negative class, 0;
+// [4, 4 + Wp) literal row; then u16 bucket starts [2][260] (stream 0 =
+// target flags, 1 = negative flags; start[256] = C); then entries u32
+// [2][Cp] = key << 16 | clause grouped by bucket key >> 8, key = draw53 >> 37
+// (order inside a bucket arbitrary).  Flag of clause c in stream s is
+// draw53(fb_seed, fbc + 1 + s*C + c) < t_s  <=>  key < t_s >> 37, or key equal
+// and the exact draw below t_s (feedback.py:47-53).
+__host__ __device__ inline int rec_buckets(const TrainK &k) { return 4 + k.Wp; }
+__host__ __device__ inline int rec_entries(const TrainK &k) { return 4 + k.Wp + 260; }
+
+// One CTA per (step, stream); dynamic shared memory: u16 keys [C].
+__global__ void __launch_bounds__(256) k_step_records(TrainK k, uint32_t *out) {
+    extern __shared__ uint16_t skey[];
+    __shared__ unsigned hist[256], wsum[8];
+    const int64_t i = blockIdx.x;
+    const int str = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C = k.C;
+    uint32_t *r = out + i * (int64_t)k.R;
+    const uint64_t fbc = k.fb_counter0 + (uint64_t)i * (1ull + 2ull * (uint64_t)C);
+    if (str == 0) {
+        const int ex = __ldg(&k.order[i]);
+        if (tid == 0) {
+            const int label = __ldg(&k.labels[ex]);
+            r[0] = (uint32_t)ex;
+            r[1] = (uint32_t)label;
+            r[2] = (uint32_t)negative_class(k, label, fbc);
+            r[3] = 0;
+        }
+        for (int w = tid; w < k.Wp; w += 256)
+            r[4 + w] = w < k.W ? __ldg(&k.lit_words[(int64_t)ex * k.W + w]) : 0u;
+    }
+    hist[tid] = 0;
+    __syncthreads();
+    const uint64_t base = fbc + 1 + (str ? (uint64_t)C : 0);
+    for (int j = tid; j < C; j += 256) {
+        const unsigned key = (unsigned)(draw53(k.fb_seed, base + (uint64_t)j) >> 37);
+        skey[j] = (uint16_t)key;
+        atomicAdd(&hist[key >> 8], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the 256 bucket sizes
+    const unsigned h = hist[tid];
+    unsigned x = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    unsigned wb = 0;
+    for (int q = 0; q < warp; ++q) wb += wsum[q];
+    const unsigned start = wb + x - h;
+    uint16_t *off = reinterpret_cast<uint16_t *>(r + rec_buckets(k)) + str * 260;
+    off[tid] = (uint16_t)start;
+    if (tid == 0) off[256] = (uint16_t)C;
+    __syncthreads();  // everyone read hist[] before it becomes the cursor
+    hist[tid] = start;
+    __syncthreads();
+    uint32_t *ent = r + rec_entries(k) + str * k.Cp;
+    for (int j = tid; j < C; j += 256) {
+        const unsigned key = skey[j];
+        const unsigned pos = atomicAdd(&hist[key >> 8], 1u);
+        ent[pos] = (key << 16) | (unsigned)j;
+    }
+}
+
+// Record of step i into ring slot i % 3 (cp.async, 16 B per copy).
+__device__ __forceinline__ void rec_issue(const TrainK &k, const Smem &s, int64_t i, int t0,
+                                          int nt) {
+    const uint32_t *src = k.recs + i * (int64_t)k.R;
+    uint32_t *dst = s.rec3 + (int)(i % 3) * k.R;
+    for (int q = t0; q < k.R / 4; q += nt) cp_async16(dst + 4 * q, src + 4 * q);
+    cp_async_commit();
+}
+
+// Warp 0: outputs of example e (nout buffer e & 1) into info, and thread 0's
+// partial class sums for its label and negative class (dense.py:153).
+__device__ __forceinline__ void votes_pass(const TrainK &k, const Smem &s, int cown, int64_t e,
+                                           long long &vl, long long &vn) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t *rc = s.rec3 + (int)(e % 3) * k.R;
+    const int label = (int)rc[1], neg = (int)rc[2];
+    const int *no = s.nout + (int)(e & 1) * k.cmax;
+    long long a = 0, b = 0;
+    for (int j = lane; j < cown; j += 32) {
+        const int o = no[j];
+        s.info[j] = o ? I_OUT : 0;
+        if (o) {
+            a += s.weights[j * k.K + label];
+            b += s.weights[j * k.K + neg];
+        }
+    }
+    // 64-bit warp sums from 32-bit reductions: low 24 bits unsigned, the
+    // rest signed (no overflow for fewer than 2^23 clauses per lane)
+    const unsigned al = __reduce_add_sync(0xffffffffu, (unsigned)(a & 0xFFFFFF));
+    const unsigned bl = __reduce_add_sync(0xffffffffu, (unsigned)(b & 0xFFFFFF));
+    const int ah = __reduce_add_sync(0xffffffffu, (int)(a >> 24));
+    const int bh = __reduce_add_sync(0xffffffffu, (int)(b >> 24));
+    vl = (long long)ah * (1LL << 24) + (long long)al;
+    vn = (long long)bh * (1LL << 24) + (long long)bl;
+}
+
+template <bool SMEM_STATES>
+__global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    Smem s;
+    smem_layout(k, SMEM_STATES, MODE_GRID, smem_raw, &s);
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = nthr >> 5;
+    const int rank = blockIdx.x;
+    const int C = k.C, n_cta = k.n_cta;
+    const int c0 = cta_begin(rank, C, n_cta), c1 = cta_begin(rank + 1, C, n_cta);
+    const int cown = c1 - c0;
+    const int64_t n = k.n_steps;
+    const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
+
+    load_slice<SMEM_STATES>(k, s, c0, cown);
+    if (tid == 0) {
+        s.blk_ctr[0] = k.block_counters[0];
+        s.blk_seed[0] = k.block_seeds[0];
+        s.misc[0] = 0;
+    }
+    for (int j = tid; j < cown; j += nthr) s.oflag[j] = 0;
+    rec_issue(k, s, 0, tid, nthr);
+    if (n > 1) rec_issue(k, s, 1, tid, nthr);
+    cp_async_wait_all();
+    __syncthreads();
+    for (int j = warp; j < cown; j += nwarps) {
+        const bool o = clause_out(k, s, j, s.rec3 + 4);
+        if (lane == 0) s.nout[j] = o;
+    }
+    __syncthreads();
+    long long vl = 0, vn = 0;  // thread 0: partial sums of the current example
+    if (warp == 0) votes_pass(k, s, cown, 0, vl, vn);
+
+    Counters cn;
+    const bool prof = k.phase != nullptr;
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long t_mark = clock64();
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t *rc = s.rec3 + (int)(i % 3) * k.R;
+        const uint32_t *lit = rc + 4;
+        const int label = (int)rc[1], neg = (int)rc[2];
+        const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
+        // 1. arrival: one relaxed atomic per word carries the arrival count
+        //    (bits 40..63) and the biased partial (bits 0..39)
+        if (tid == 0) {
+            red_relaxed_add_u64(&k.rec[i * 2 + 0], (1ull << 40) + (unsigned long long)(vl + kVoteBias));
+            red_relaxed_add_u64(&k.rec[i * 2 + 1], (1ull << 40) + (unsigned long long)(vn + kVoteBias));
+            TIMELINE(i, 0);
+        }
+        PHASE(0);
+        if (warp == 0) {
+            // 2. all-reduce, then the decision (feedback.py:33-53): lane 0
+            //    the target threshold, lane 1 the negative one
+            //    The whole warp spins on the same 16 B (one request per
+            //    iteration) so it stays converged: a lone spinning lane
+            //    sends the lanes waiting for it down the collective slow path.
+            const unsigned long long want = (unsigned long long)n_cta;
+            ulonglong2 p;
+            do {
+                p = ld_relaxed_v2u64(&k.rec[i * 2]);
+            } while ((p.x >> 40) != want || (p.y >> 40) != want);
+            TIMELINE(i, 1);
+            PHASE(1);
+            const unsigned long long px = p.x, py = p.y;
+            const long long bias = (long long)n_cta * kVoteBias;
+            const long long gl = (long long)(px & ((1ull << 40) - 1)) - bias;
+            const long long gn = (long long)(py & ((1ull << 40) - 1)) - bias;
+            if (lane < 2) {
+                const long long T = k.T;
+                const long long v = lane == 0 ? gl : gn;
+                const long long cv = v < -T ? -T : (v > T ? T : v);
+                s.thr[lane] = (k.dbg & 4) ? 0 : (k.dbg & 8) ? (1ull << 44)
+                                               : threshold_of(lane == 0 ? T - cv : T + cv, T);
+            }
+            if (k.trace && rank == 0 && lane == 0) {
+                k.trace[i * 4 + 0] = neg;
+                k.trace[i * 4 + 1] = gl;
+                k.trace[i * 4 + 2] = gn;
+            }
+            PHASE(2);
+        } else {
+            // shadow of the all-reduce: record i+2 in flight, and the
+            // outputs of example i+1 under the current include masks
+            long long sh0 = 0;
+            if (prof && tid == 32) sh0 = clock64();
+            if (i + 2 < n) rec_issue(k, s, i + 2, tid - 32, nthr - 32);
+            if (i + 1 < n && !(k.dbg & 16)) {
+                const uint32_t *litn = s.rec3 + (int)((i + 1) % 3) * k.R + 4;
+                int *no = s.nout + (int)((i + 1) & 1) * k.cmax;
+                for (int j = warp - 1; j < cown; j += nwarps - 1) {
+                    const bool o = clause_out(k, s, j, litn);
+                    if (lane == 0) no[j] = o;
+                }
+            }
+            (void)sh0;
+        }
+        __syncthreads();
+        PHASE(3);
+        // 3. the step's events: every entry of the buckets up to the
+        //    threshold's bucket whose key is below it (exact draw on a tie);
+        //    count those before c0 (window ordinals) and in total, and flag
+        //    the own clauses'
+        {
+            const uint32_t *ent = rc + rec_entries(k);
+            const uint16_t *off = reinterpret_cast<const uint16_t *>(rc + rec_buckets(k));
+            const uint64_t tt = s.thr[0], tn = s.thr[1];
+            const unsigned tbt = (unsigned)(tt >> 37), tbn = (unsigned)(tn >> 37);
+            const int hi_t = tbt >= 65536u ? C : off[(tbt >> 8) + 1];
+            const int hi_n = tbn >= 65536u ? C : off[260 + (tbn >> 8) + 1];
+            unsigned pre = 0, tot = 0;
+            for (int e = tid; e < hi_t + hi_n; e += nthr) {
+                const int str = e >= hi_t ? 1 : 0;
+                const uint32_t v = ent[str * k.Cp + e - str * hi_t];
+                const unsigned key = v >> 16, c = v & 0xFFFFu;
+                const unsigned tb = str ? tbn : tbt;
+                bool q = key < tb;
+                if (key == tb)
+                    q = draw53(k.fb_seed, fbc + 1 + (str ? (uint64_t)C : 0) + c) < (str ? tn : tt);
+                if (q) {
+                    ++tot;
+                    pre += c < (unsigned)c0 ? 1u : 0u;
+                    if (c >= (unsigned)c0 && c < (unsigned)c1) atomicOr(&s.oflag[c - c0], 1 << str);
+                }
+            }
+            pre = __reduce_add_sync(0xffffffffu, pre);
+            tot = __reduce_add_sync(0xffffffffu, tot);
+            if (lane == 0) {
+                s.wcnt[warp] = pre;
+                s.wcnt[16 + warp] = tot;
+            }
+        }
+        __syncthreads();
+        PHASE(4);
+        // 4-5. warp 0: window ordinals, event types, weights, work list
+        if (warp == 0) {
+            unsigned pv = lane < nwarps ? s.wcnt[lane] : 0u;
+            unsigned tv = lane < nwarps ? s.wcnt[16 + lane] : 0u;
+            pv = __reduce_add_sync(0xffffffffu, pv);
+            tv = __reduce_add_sync(0xffffffffu, tv);
+            if (lane == 0) s.misc[0] = 0;
+            __syncwarp();
+            const uint64_t obase = s.blk_ctr[0] + pv;
+            unsigned carry = 0;
+            for (int jb = 0; jb < cown; jb += 32) {
+                const int j = jb + lane;
+                int f = 0;
+                if (j < cown) {
+                    f = s.oflag[j];
+                    s.oflag[j] = 0;
+                }
+                const unsigned v = (unsigned)(f & 1) + (unsigned)(f >> 1);
+                unsigned x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (j < cown)
+                    apply_events(k, s, cn, j, f & 1, f & 2, obase + carry + (x - v), s.blk_seed[0],
+                                 label, neg);
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                s.blk_ctr[0] += (uint64_t)tv;
+                if (k.trace && rank == 0) k.trace[i * 4 + 3] = tv;
+            }
+        }
+        __syncthreads();
+        PHASE(5);
+        // 6. per-position Type I / II updates of the work list
+        const int n_work = s.misc[0];
+        feedback_quads<SMEM_STATES>(k, s, c0, lit, (k.dbg & 1) ? 0 : n_work, cn);
+        cp_async_wait_all();  // record i+2 landed
+        __syncthreads();
+        PHASE(6);
+        TIMELINE(i, 2);
+        if (i + 1 < n) {
+            // 7. re-evaluate, for example i+1, the clauses the feedback changed
+            if (n_work > 0) {
+                const uint32_t *litn = s.rec3 + (int)((i + 1) % 3) * k.R + 4;
+                int *no = s.nout + (int)((i + 1) & 1) * k.cmax;
+                for (int q = warp; q < n_work; q += nwarps) {
+                    const int j = s.work[q];
+                    const bool o = clause_out(k, s, j, litn);
+                    if (lane == 0) no[j] = o;
+                }
+                __syncthreads();
+            }
+            // 8. warp 0: outputs and partial sums of example i+1
+            if (warp == 0) votes_pass(k, s, cown, i + 1, vl, vn);
+        }
+        PHASE(7);
+    }
+    if (prof && tid == 0)
+        for (int q = 0; q < 8; ++q) k.phase[rank * 8 + q] = ph[q];
+    __syncthreads();
+    store_slice<SMEM_STATES>(k, s, c0, cown);
+    if (tid == 0 && rank == n_cta - 1) k.block_counters[0] = s.blk_ctr[0];
     flush_stats(k, cn, rank == 0);
 }
 
@@ -826,9 +1056,8 @@ struct tmb_trainer {
     uint64_t *block_seeds_d = nullptr;
     unsigned long long *ring_d = nullptr;  // grid mode: per-example vote slots [cap][2]
     int64_t ring_cap = 0;
-    uint32_t *keys_d = nullptr;  // keyed: [key_cap][2][Cw]
-    int32_t *nrand_d = nullptr;  // keyed: [key_cap]
-    int64_t key_cap = 0;
+    uint32_t *recs_d = nullptr;  // fast path: step records [rec_cap][R]
+    int64_t rec_cap = 0;
 };
 
 namespace {
@@ -848,24 +1077,23 @@ void per_cta_maxima(TrainK &k) {
     k.bmax = bmax;
 }
 
-const void *kernel_for(bool cluster, bool smem_states, bool keyed) {
+const void *kernel_for(bool cluster, bool smem_states, bool fast) {
     if (cluster)
-        return smem_states ? (const void *)k_train<MODE_CLUSTER, true, false>
-                           : (const void *)k_train<MODE_CLUSTER, false, false>;
-    if (keyed)
-        return smem_states ? (const void *)k_train<MODE_GRID, true, true>
-                           : (const void *)k_train<MODE_GRID, false, true>;
-    return smem_states ? (const void *)k_train<MODE_GRID, true, false>
-                       : (const void *)k_train<MODE_GRID, false, false>;
+        return smem_states ? (const void *)k_train<MODE_CLUSTER, true>
+                           : (const void *)k_train<MODE_CLUSTER, false>;
+    if (fast)
+        return smem_states ? (const void *)k_train_fast<true> : (const void *)k_train_fast<false>;
+    return smem_states ? (const void *)k_train<MODE_GRID, true> : (const void *)k_train<MODE_GRID, false>;
 }
 
-// Keyed-path key buffer budget: runs longer than this are launched in chunks.
-constexpr size_t kKeyBufferBytes = size_t(1) << 30;
+// Fast-path step-record budget: longer runs are launched in chunks.
+constexpr size_t kRecordBufferBytes = size_t(2) << 30;
 
 }  // namespace
 
 namespace tmb {
 int64_t g_train_key_chunk = 0;  // tmb_set_option("train.key_chunk"): test override
+int g_train_dbg = 0;            // tmb_set_option("train.debug_skip"): timing ablations
 }
 
 namespace {
@@ -912,10 +1140,12 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     k.fp = make_fb_params(c.s, c.boost, c.state_min, c.state_max);
     k.fb_seed = derive_stream(c.seed, 0xFEED);
     per_cta_maxima(k);
-    // keyed flag path: grid mode, one block, keys of one step <= 32 KB
-    // (flags bit 1 forces the per-CTA draw path)
-    k.Cw = (int)(((C + 1) / 2 + 3) / 4 * 4);
-    k.keyed = (!cluster && c.n_blocks == 1 && !(c.flags & 2) && 8LL * k.Cw <= 32768) ? 1 : 0;
+    // fast path: grid mode, one block, 16-bit clause ids (flags bit 1 forces
+    // the generic grid kernel)
+    k.Wp = (W + 3) / 4 * 4;
+    k.Cp = (C + 3) / 4 * 4;
+    k.R = 4 + k.Wp + 260 + 2 * k.Cp;
+    k.fast = (!cluster && c.n_blocks == 1 && !(c.flags & 2) && C <= 65535) ? 1 : 0;
     if (cluster && k.cmax > 32 * 1024)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: too many clauses per CTA");
 
@@ -923,6 +1153,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     cudaGetDevice(&dev);
     int max_smem = 0;
     TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (k.fast && smem_layout(k, false, MODE_GRID, nullptr, nullptr) > (size_t)max_smem) k.fast = 0;
     const size_t need_on = smem_layout(k, true, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
     const size_t need_off = smem_layout(k, false, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
     // flags bit 0 forces HBM-resident states (tests the streaming path)
@@ -932,7 +1163,10 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
         return fail(TMB_E_UNSUPPORTED,
                     "trainer_create: per-CTA include masks exceed shared memory (" +
                         std::to_string(need) + " B); use more CTAs");
-    const void *fn = kernel_for(cluster, smem_states, k.keyed);
+    const void *fn = kernel_for(cluster, smem_states, k.fast);
+    if (k.fast && 2 * C > 48 * 1024)
+        TMB_CUDA(cudaFuncSetAttribute((const void *)k_step_records,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * C));
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
     if (cluster) {
         if (n_cta > 8)
@@ -998,8 +1232,7 @@ int tmb_trainer_destroy(tmb_trainer *t) {
     if (!t) return TMB_OK;
     if (t->block_seeds_d) cudaFree(t->block_seeds_d);
     if (t->ring_d) cudaFree(t->ring_d);
-    if (t->keys_d) cudaFree(t->keys_d);
-    if (t->nrand_d) cudaFree(t->nrand_d);
+    if (t->recs_d) cudaFree(t->recs_d);
     delete t;
     return TMB_OK;
 }
@@ -1025,8 +1258,9 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     TrainK k = t->k;
     k.lit_words = lit_words; k.labels = labels; k.order = order;
     k.n_steps = n_steps; k.fb_counter0 = fb_counter; k.stats = stats;
+    k.dbg = g_train_dbg;
     void *args[] = {&k};
-    const void *fn = kernel_for(t->cluster, t->smem_states, k.keyed);
+    const void *fn = kernel_for(t->cluster, t->smem_states, k.fast);
     if (t->cluster) {
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute at[1];
@@ -1044,26 +1278,24 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         TMB_LAUNCHED();
         return TMB_OK;
     }
-    // grid mode; keyed runs are split into chunks whose keys fit the buffer
+    // grid mode; fast-path runs are split into chunks whose records fit
     int64_t chunk = n_steps;
-    if (k.keyed) {
-        chunk = std::max<int64_t>(1, (int64_t)(kKeyBufferBytes / (8 * (size_t)k.Cw)));
+    if (k.fast) {
+        chunk = std::max<int64_t>(1, (int64_t)(kRecordBufferBytes / (4 * (size_t)k.R)));
         if (g_train_key_chunk > 0) chunk = std::min(chunk, g_train_key_chunk);
     }
     const int64_t slots = std::min(n_steps, chunk);
-    if (t->ring_cap < slots || (k.keyed && t->key_cap < slots)) {
+    if (t->ring_cap < slots || (k.fast && t->rec_cap < slots)) {
         cudaStreamSynchronize(st);
         if (t->ring_d) cudaFree(t->ring_d);
-        if (t->keys_d) cudaFree(t->keys_d);
-        if (t->nrand_d) cudaFree(t->nrand_d);
-        t->ring_d = nullptr; t->keys_d = nullptr; t->nrand_d = nullptr;
-        t->ring_cap = 0; t->key_cap = 0;
+        if (t->recs_d) cudaFree(t->recs_d);
+        t->ring_d = nullptr; t->recs_d = nullptr;
+        t->ring_cap = 0; t->rec_cap = 0;
         TMB_CUDA(cudaMalloc(&t->ring_d, 16 * (size_t)slots));
         t->ring_cap = slots;
-        if (k.keyed) {
-            TMB_CUDA(cudaMalloc(&t->keys_d, 8 * (size_t)k.Cw * (size_t)slots));
-            TMB_CUDA(cudaMalloc(&t->nrand_d, 4 * (size_t)slots));
-            t->key_cap = slots;
+        if (k.fast) {
+            TMB_CUDA(cudaMalloc(&t->recs_d, 4 * (size_t)k.R * (size_t)slots));
+            t->rec_cap = slots;
         }
     }
     const uint64_t step_draws = 1ull + 2ull * (uint64_t)k.C;
@@ -1074,13 +1306,9 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         k.fb_counter0 = fb_counter + (uint64_t)off * step_draws;
         k.rec = t->ring_d;
         TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 16 * (size_t)n, st));
-        if (k.keyed) {
-            k.keys = t->keys_d;
-            k.nrand = t->nrand_d;
-            const int64_t elems = n * 2 * (int64_t)k.Cw;
-            const int blocks = (int)std::min<int64_t>((elems + 255) / 256, (int64_t)sm_count() * 16);
-            k_flag_keys<<<blocks, 256, 0, st>>>(k.fb_seed, k.fb_counter0, k.C, k.Cw, k.K, n,
-                                                 t->keys_d, t->nrand_d);
+        if (k.fast) {
+            k.recs = t->recs_d;
+            k_step_records<<<dim3((unsigned)n, 2), 256, 2 * (size_t)k.C, st>>>(k, t->recs_d);
             TMB_LAUNCHED();
         }
         TMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(t->n_cta), dim3(t->threads), args,

@@ -16,14 +16,17 @@ import paper_2405_04212_b200 as tmb  # noqa: E402
 from paper_2405_04212_b200 import _lib, datasets  # noqa: E402
 from paper_2405_04212_b200.runtime import ptr  # noqa: E402
 
-NAMES = ["eval(+votes)", "arrive", "precompute", "wait+decide", "flag count/bitmaps",
+NAMES = ["eval(+votes)", "arrive", "precompute", "wait+decide", "flag bitmaps",
          "scan+events", "feedback", "-"]
+NAMES_FAST = ["arrive", "all-reduce wait", "decide", "sync (B1)", "event count", "events (warp 0)",
+              "feedback", "re-eval+votes"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cta", type=int, nargs="*", default=[16, 148])
 ap.add_argument("--threads", type=int, default=0)
 ap.add_argument("--epochs", type=int, default=4)
 ap.add_argument("--n-train", type=int, default=60000)
+ap.add_argument("--skip", type=int, default=0, help="train.debug_skip ablation bits")
 ap.add_argument("--no-keys", action="store_true", help="per-CTA flag draws instead of keys")
 args = ap.parse_args()
 
@@ -35,19 +38,53 @@ for n_cta in args.cta:
                                  flag_keys=not args.no_keys)
     for _ in range(args.epochs - 1):
         sess.run_epoch()
-    ph = torch.zeros(sess.launch["n_cta"] * 8, dtype=torch.int64, device="cuda")
+    nc = sess.launch["n_cta"]
+    ph = torch.zeros(nc * (8 + 192), dtype=torch.int64, device="cuda")
     _lib.call("tmb_trainer_set_profile", sess._h, ptr(ph))
+    _lib.call("tmb_set_option", b"train.debug_skip", args.skip)
     st = torch.cuda.Event(enable_timing=True)
     en = torch.cuda.Event(enable_timing=True)
     st.record()
     sess.run_epoch()
     en.record()
     torch.cuda.synchronize()
+    _lib.call("tmb_set_option", b"train.debug_skip", 0)
     ms = st.elapsed_time(en)
-    p = ph.cpu().numpy().reshape(-1, 8).astype(np.float64) / clk_hz * 1e6 / len(ty)
+    tl = ph.cpu().numpy()[nc * 8:].reshape(64, nc, 3).astype(np.float64)
+    p = ph.cpu().numpy()[:nc * 8].reshape(-1, 8).astype(np.float64) / clk_hz * 1e6 / len(ty)
     print(f"n_cta={sess.launch['n_cta']} threads={sess.launch['threads']} "
           f"smem_states={sess.launch['states_in_smem']}: {ms * 1e3 / len(ty):.2f} us/example "
           f"(clock {clk_hz / 1e6:.0f} MHz)")
-    for q in range(7):
-        print(f"   {NAMES[q]:22s} mean {p[:, q].mean():6.3f}  max {p[:, q].max():6.3f}  "
+    for q in range(8):
+        name = (NAMES if args.no_keys else NAMES_FAST)[q]
+        print(f"   {name:22s} mean {p[:, q].mean():6.3f}  max {p[:, q].max():6.3f}  "
               f"cta0 {p[0, q]:6.3f} us/ex")
+    if tl[:, :, 0].min() > 0:
+        last = tl[:, :, 0].max(axis=1, keepdims=True)
+        det = tl[:, :, 1] - last            # detection after the last arrival
+        skew = last - tl[:, :, 0]           # own arrival before the last one
+        step = np.diff(tl[:, :, 2].max(axis=1))
+        who = np.argmax(tl[:, :, 0], axis=1)
+        print(f"   timeline (ns, steps 64..127): step {np.median(step):.0f} median; "
+              f"detect-after-last-arrival mean {det.mean():.0f} min {det.min():.0f} "
+              f"max {det.max():.0f}; arrival skew mean {skew.mean():.0f} "
+              f"max {skew.max():.0f}; last arriver CTAs {np.bincount(who, minlength=nc).argsort()[-5:]}")
+        end_to_arr = tl[1:, :, 0] - tl[:-1, :, 2].max(axis=1, keepdims=True)
+        print(f"   from the previous step's last end to arrival: mean {end_to_arr.mean():.0f} "
+              f"min {end_to_arr.min():.0f} max {end_to_arr.max():.0f}")
+        med = np.median(tl, axis=1, keepdims=True)
+        off = (tl - med).mean(axis=0)  # per CTA mean offset of arrival / detect / end
+        worst = np.argsort(off[:, 0])[-6:]
+        for r in worst:
+            print(f"   cta {r:3d}: arrival {off[r, 0]:7.0f}  detect {off[r, 1]:7.0f}  "
+                  f"end {off[r, 2]:7.0f} ns vs median")
+        print(f"   median CTA spread of detection {np.median(tl[:, :, 1].max(1) - tl[:, :, 1].min(1)):.0f} ns")
+        A = np.median(tl[:, :, 0], axis=1); L = tl[:, :, 0].max(axis=1)
+        D = np.median(tl[:, :, 1], axis=1); E = np.median(tl[:, :, 2], axis=1)
+        EM = tl[:, :, 2].max(axis=1)
+        q = lambda v: f"p50 {np.median(v):6.0f} mean {v.mean():6.0f} p90 {np.percentile(v, 90):6.0f}"
+        print("   per step: last-arrival minus median arrival  ", q(L - A))
+        print("             median detect minus last arrival   ", q(D - L))
+        print("             median end minus median detect     ", q(E - D))
+        print("             max end minus median end           ", q(EM - E))
+        print("             next median arrival minus med. end ", q(A[1:] - E[:-1]))
