@@ -107,6 +107,8 @@ struct Smem {
     uint64_t *thr;     // grid: [0]=t_t [1]=t_n [2]=negative
     uint32_t *rec3;    // fast: [3][R] step records in flight
     int *nout, *oflag; // fast: [2][cmax] next-example outputs; [cmax] own event flags
+    long long *clo;    // fast: [2 parity][2 class][cmax] shadow-time vote contributions
+    unsigned long long *vsh;  // fast: [2 parity][2] shadow-time partial sums
     unsigned *wcnt;    // per-warp event counts [32]
     unsigned long long *vacc;  // grid: [2] CTA partial votes (label, negative)
 };
@@ -148,6 +150,8 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.oflag = k.fast ? (int *)take(4 * (size_t)k.cmax) : nullptr;
     t.wcnt = (unsigned *)take(4 * 32);
     t.vacc = (unsigned long long *)take(8 * 2);
+    t.clo = k.fast ? (long long *)take(8 * 4 * (size_t)k.cmax) : nullptr;
+    t.vsh = k.fast ? (unsigned long long *)take(8 * 4) : nullptr;
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
     if (s) *s = t;
     return align_up(off, 16);
@@ -812,6 +816,17 @@ __device__ __forceinline__ void rec_issue(const TrainK &k, const Smem &s, int64_
     cp_async_commit();
 }
 
+// Two 64-bit warp sums from 32-bit reductions: low 24 bits unsigned, the rest
+// signed (exact while |x| < 2^54 per lane).
+__device__ __forceinline__ void warp_sum2(long long a, long long b, long long &sa, long long &sb) {
+    const unsigned al = __reduce_add_sync(0xffffffffu, (unsigned)(a & 0xFFFFFF));
+    const unsigned bl = __reduce_add_sync(0xffffffffu, (unsigned)(b & 0xFFFFFF));
+    const int ah = __reduce_add_sync(0xffffffffu, (int)(a >> 24));
+    const int bh = __reduce_add_sync(0xffffffffu, (int)(b >> 24));
+    sa = (long long)ah * (1LL << 24) + (long long)al;
+    sb = (long long)bh * (1LL << 24) + (long long)bl;
+}
+
 // Warp 0: outputs of example e (nout buffer e & 1) into info, and thread 0's
 // partial class sums for its label and negative class (dense.py:153).
 __device__ __forceinline__ void votes_pass(const TrainK &k, const Smem &s, int cown, int64_t e,
@@ -829,14 +844,7 @@ __device__ __forceinline__ void votes_pass(const TrainK &k, const Smem &s, int c
             b += s.weights[j * k.K + neg];
         }
     }
-    // 64-bit warp sums from 32-bit reductions: low 24 bits unsigned, the
-    // rest signed (no overflow for fewer than 2^23 clauses per lane)
-    const unsigned al = __reduce_add_sync(0xffffffffu, (unsigned)(a & 0xFFFFFF));
-    const unsigned bl = __reduce_add_sync(0xffffffffu, (unsigned)(b & 0xFFFFFF));
-    const int ah = __reduce_add_sync(0xffffffffu, (int)(a >> 24));
-    const int bh = __reduce_add_sync(0xffffffffu, (int)(b >> 24));
-    vl = (long long)ah * (1LL << 24) + (long long)al;
-    vn = (long long)bh * (1LL << 24) + (long long)bl;
+    warp_sum2(a, b, vl, vn);
 }
 
 template <bool SMEM_STATES>
@@ -860,6 +868,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
         s.misc[0] = 0;
     }
     for (int j = tid; j < cown; j += nthr) s.oflag[j] = 0;
+    if (tid < 4) s.vsh[tid] = 0;
     rec_issue(k, s, 0, tid, nthr);
     if (n > 1) rec_issue(k, s, 1, tid, nthr);
     cp_async_wait_all();
@@ -925,12 +934,31 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
             long long sh0 = 0;
             if (prof && tid == 32) sh0 = clock64();
             if (i + 2 < n) rec_issue(k, s, i + 2, tid - 32, nthr - 32);
-            if (i + 1 < n && !(k.dbg & 16)) {
-                const uint32_t *litn = s.rec3 + (int)((i + 1) % 3) * k.R + 4;
-                int *no = s.nout + (int)((i + 1) & 1) * k.cmax;
-                for (int j = warp - 1; j < cown; j += nwarps - 1) {
-                    const bool o = clause_out(k, s, j, litn);
-                    if (lane == 0) no[j] = o;
+            // outputs of example i into info (read by this step's events);
+            // outputs of example i+1 and their contributions to its two
+            // class sums with the weights as they stand (the end of the step
+            // corrects the clauses this step touches)
+            const int par = (int)((i + 1) & 1);
+            const int *nc = s.nout + (int)(i & 1) * k.cmax;
+            int *no = s.nout + par * k.cmax;
+            long long *cl = s.clo + par * 2 * k.cmax;
+            const bool more = i + 1 < n && !(k.dbg & 16);
+            const uint32_t *rn = s.rec3 + (int)((i + 1) % 3) * k.R;
+            const int label1 = more ? (int)rn[1] : 0, neg1 = more ? (int)rn[2] : 0;
+            for (int j = warp - 1; j < cown; j += nwarps - 1) {
+                bool o = false;
+                if (more) o = clause_out(k, s, j, rn + 4);
+                if (lane == 0) {
+                    s.info[j] = nc[j] ? I_OUT : 0;
+                    if (more) {
+                        no[j] = o;
+                        const long long a = o ? s.weights[j * k.K + label1] : 0;
+                        const long long b = o ? s.weights[j * k.K + neg1] : 0;
+                        cl[j] = a;
+                        cl[k.cmax + j] = b;
+                        if (a) atomicAdd(&s.vsh[par * 2 + 0], (unsigned long long)a);
+                        if (b) atomicAdd(&s.vsh[par * 2 + 1], (unsigned long long)b);
+                    }
                 }
             }
             (void)sh0;
@@ -984,11 +1012,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
             unsigned carry = 0;
             for (int jb = 0; jb < cown; jb += 32) {
                 const int j = jb + lane;
-                int f = 0;
-                if (j < cown) {
-                    f = s.oflag[j];
-                    s.oflag[j] = 0;
-                }
+                const int f = j < cown ? s.oflag[j] : 0;  // cleared at the step's end
                 const unsigned v = (unsigned)(f & 1) + (unsigned)(f >> 1);
                 unsigned x = v;
 #pragma unroll
@@ -1028,8 +1052,40 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                 }
                 __syncthreads();
             }
-            // 8. warp 0: outputs and partial sums of example i+1
-            if (warp == 0) votes_pass(k, s, cown, i + 1, vl, vn);
+            // 8. warp 0: partial sums of example i+1 = the shadow's sums
+            //    corrected for the clauses this step's events touched
+            //    (weights of label / negative, outputs via the re-evaluation)
+            if (warp == 0) {
+                const int par = (int)((i + 1) & 1);
+                const uint32_t *rn = s.rec3 + (int)((i + 1) % 3) * k.R;
+                const int label1 = (int)rn[1], neg1 = (int)rn[2];
+                const int *no = s.nout + par * k.cmax;
+                const long long *cl = s.clo + par * 2 * k.cmax;
+                long long dl = 0, dn = 0;
+                bool any = false;
+                for (int j = lane; j < cown; j += 32) {
+                    if (s.oflag[j]) {
+                        s.oflag[j] = 0;
+                        any = true;
+                        const bool o = no[j] != 0;
+                        dl += (o ? s.weights[j * k.K + label1] : 0) - cl[j];
+                        dn += (o ? s.weights[j * k.K + neg1] : 0) - cl[k.cmax + j];
+                    }
+                }
+                vl = (long long)s.vsh[par * 2 + 0];
+                vn = (long long)s.vsh[par * 2 + 1];
+                if (__any_sync(0xffffffffu, any)) {
+                    long long a, b;
+                    warp_sum2(dl, dn, a, b);
+                    vl += a;
+                    vn += b;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    s.vsh[par * 2 + 0] = 0;
+                    s.vsh[par * 2 + 1] = 0;
+                }
+            }
         }
         PHASE(7);
     }
