@@ -47,6 +47,22 @@ __device__ __forceinline__ int type_i_stream(int st, int lit, int out, const FbP
     return st;
 }
 
+// type_i_stream without data-dependent branches, for warps whose lanes hold
+// different states / literals: the draw mix64(z) (z = sk + G*p) is computed
+// for every position and used only where the reference consumes one, so a
+// warp never runs the mixer twice on diverged paths.  Bit-identical.
+__device__ __forceinline__ int type_i_bf(int st, int lit, int out, const FbParams &fp, uint64_t z,
+                                         uint64_t &ndraws) {
+    const bool inc = out && lit;
+    const bool room = st < fp.smax;
+    const bool need = inc ? (room && !fp.boost) : (st > fp.smin);
+    const bool hit = (mix64(z) >> 11) < (inc ? fp.t_inc : fp.t_dec);
+    ndraws += need ? 1u : 0u;
+    const int up = (inc && room && (fp.boost || hit)) ? 1 : 0;
+    const int down = (!inc && need && hit) ? 1 : 0;
+    return st + up - down;
+}
+
 // Same with an explicit uniform draw u (test hook).
 __device__ __forceinline__ int type_i_explicit(int st, int lit, int out, const FbParams &fp,
                                                double u) {

@@ -105,7 +105,7 @@ struct Smem {
     long long *vsum;   // grid: [2] summed votes
     int *misc;         // [0]=n_work [3..5]=example ring [8..10]=label ring
     uint64_t *thr;     // grid: [0]=t_t [1]=t_n [2]=negative
-    uint32_t *rec3;    // fast: [3][R] step records in flight
+    uint32_t *rec3;    // fast: [4][R] step records in flight (ring i & 3)
     int *nout, *oflag; // fast: [2][cmax] next-example outputs; [cmax] own event flags
     long long *clo;    // fast: [2 parity][2 class][cmax] shadow-time vote contributions
     unsigned long long *vsh;  // fast: [2 parity][2] shadow-time partial sums
@@ -145,7 +145,7 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     const bool pre = 32 * k.fmax_words <= kMaxPrecompute;
     t.draw_t = pre && !k.fast ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
     t.draw_n = pre && !k.fast ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
-    t.rec3 = k.fast ? (uint32_t *)take(4 * 3 * (size_t)k.R) : nullptr;
+    t.rec3 = k.fast ? (uint32_t *)take(4 * 4 * (size_t)k.R) : nullptr;
     t.nout = k.fast ? (int *)take(4 * 2 * (size_t)k.cmax) : nullptr;
     t.oflag = k.fast ? (int *)take(4 * (size_t)k.cmax) : nullptr;
     t.wcnt = (unsigned *)take(4 * 32);
@@ -174,17 +174,25 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
     const int QP = k.Ppad >> 2;  // quads per (padded) row; multiple of 32
     const int total = n_work * QP;
     constexpr int B = 4;
+    // quad index it = (work item wc, quad rem), advanced by nthr per unit
+    // without a division (nthr < 2 * QP is not assumed: a short loop)
+    int wc_next = tid / QP, rem_next = tid - (tid / QP) * QP;
     for (int it0 = tid; it0 < total; it0 += B * nthr) {
         uint32_t word[B];
         int jj[B], pp[B];
 #pragma unroll
         for (int u = 0; u < B; ++u) {
             const int it = it0 + u * nthr;
+            const int wc = wc_next, rem = rem_next;
+            rem_next += nthr;
+            while (rem_next >= QP) {
+                rem_next -= QP;
+                ++wc_next;
+            }
             jj[u] = -1;
             word[u] = 0xFFFFFFFFu;
             if (it < total) {
-                const int wc = it / QP;
-                const int p0 = (it - wc * QP) << 2;
+                const int p0 = rem << 2;
                 const int j = s.work[wc];
                 jj[u] = j;
                 pp[u] = p0;
@@ -211,6 +219,9 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
             const int out = (info & I_OUT) ? 1 : 0;
             const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
             uint32_t nw = word[u], nib = 0;
+            // draw counters of position p0 in both streams; p0 + b adds b*G
+            const uint64_t zt = s.sk_t[j] + kGolden * (uint64_t)p0;
+            const uint64_t zn = s.sk_n[j] + kGolden * (uint64_t)p0;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
                 const int p = p0 + b;
@@ -220,11 +231,11 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
                     const int st0 = st;
                     uint64_t nd = 0;
                     if (info & I_TEV) {
-                        if (info & I_T1) st = type_i_stream(st, l, out, k.fp, s.sk_t[j], (uint32_t)p, nd);
+                        if (info & I_T1) st = type_i_bf(st, l, out, k.fp, zt + kGolden * (uint64_t)b, nd);
                         else st = type_ii(st, l, out);
                     }
                     if (info & I_NEV) {
-                        if (info & I_N1) st = type_i_stream(st, l, out, k.fp, s.sk_n[j], (uint32_t)p, nd);
+                        if (info & I_N1) st = type_i_bf(st, l, out, k.fp, zn + kGolden * (uint64_t)b, nd);
                         else st = type_ii(st, l, out);
                     }
                     cn.draws += nd;
@@ -807,11 +818,11 @@ __global__ void __launch_bounds__(256) k_step_records(TrainK k, uint32_t *out) {
     }
 }
 
-// Record of step i into ring slot i % 3 (cp.async, 16 B per copy).
+// Record of step i into ring slot i & 3 (cp.async, 16 B per copy).
 __device__ __forceinline__ void rec_issue(const TrainK &k, const Smem &s, int64_t i, int t0,
                                           int nt) {
     const uint32_t *src = k.recs + i * (int64_t)k.R;
-    uint32_t *dst = s.rec3 + (int)(i % 3) * k.R;
+    uint32_t *dst = s.rec3 + (int)(i & 3) * k.R;
     for (int q = t0; q < k.R / 4; q += nt) cp_async16(dst + 4 * q, src + 4 * q);
     cp_async_commit();
 }
@@ -832,7 +843,7 @@ __device__ __forceinline__ void warp_sum2(long long a, long long b, long long &s
 __device__ __forceinline__ void votes_pass(const TrainK &k, const Smem &s, int cown, int64_t e,
                                            long long &vl, long long &vn) {
     const int lane = threadIdx.x & 31;
-    const uint32_t *rc = s.rec3 + (int)(e % 3) * k.R;
+    const uint32_t *rc = s.rec3 + (int)(e & 3) * k.R;
     const int label = (int)rc[1], neg = (int)rc[2];
     const int *no = s.nout + (int)(e & 1) * k.cmax;
     long long a = 0, b = 0;
@@ -847,6 +858,53 @@ __device__ __forceinline__ void votes_pass(const TrainK &k, const Smem &s, int c
     warp_sum2(a, b, vl, vn);
 }
 
+// Fast-path event application for own clause j (apply_events plus the class
+// sum correction of example i+1): returns true when j joined the work list
+// (its correction then comes with its re-evaluation).
+__device__ __forceinline__ void fast_events(const TrainK &k, const Smem &s, Counters &cn, int j,
+                                            bool t_ev, bool n_ev, uint64_t ord, int label,
+                                            int neg, bool more, int par, int label1, int neg1) {
+    const int n0 = s.misc[0];
+    (void)n0;
+    int info = s.info[j] & I_OUT;
+    const bool out = info & I_OUT;
+    int32_t *w = s.weights + j * k.K;
+    const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
+    const uint64_t bseed = s.blk_seed[0];
+    if (t_ev) {
+        info |= I_TEV | (t1 ? I_T1 : 0);
+        s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
+        ++cn.events;
+        if (t1) ++cn.t1; else if (out) ++cn.t2;
+    }
+    if (n_ev) {
+        const uint64_t o2 = ord + (t_ev ? 1 : 0);
+        info |= I_NEV | (n1 ? I_N1 : 0);
+        s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
+        ++cn.events;
+        if (n1) ++cn.t1; else if (out) ++cn.t2;
+    }
+    if (out) {
+        if (t_ev) w[label] += 1;
+        if (n_ev) w[neg] -= 1;
+    }
+    s.info[j] = info;
+    if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out))) {
+        s.work[atomicAdd(&s.misc[0], 1)] = j;
+    } else if (more && out) {
+        // weights moved, output unchanged: correct example i+1's sums now
+        const bool o = s.nout[par * k.cmax + j] != 0;
+        const long long *cl = s.clo + par * 2 * k.cmax;
+        const long long dl = (o ? w[label1] : 0) - cl[j], dn = (o ? w[neg1] : 0) - cl[k.cmax + j];
+        if (dl) atomicAdd(&s.vsh[par * 2 + 0], (unsigned long long)dl);
+        if (dn) atomicAdd(&s.vsh[par * 2 + 1], (unsigned long long)dn);
+    }
+}
+
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+constexpr int kRecRing = 4;  // step records in shared memory (i & 3)
+
 template <bool SMEM_STATES>
 __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
     extern __shared__ __align__(16) char smem_raw[];
@@ -860,6 +918,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
     const int cown = c1 - c0;
     const int64_t n = k.n_steps;
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
+    auto REC = [&](int64_t e) { return s.rec3 + (int)(e & (kRecRing - 1)) * k.R; };
 
     load_slice<SMEM_STATES>(k, s, c0, cown);
     if (tid == 0) {
@@ -869,41 +928,46 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
     }
     for (int j = tid; j < cown; j += nthr) s.oflag[j] = 0;
     if (tid < 4) s.vsh[tid] = 0;
-    rec_issue(k, s, 0, tid, nthr);
-    if (n > 1) rec_issue(k, s, 1, tid, nthr);
+    for (int64_t q = 0; q < 3 && q < n; ++q) rec_issue(k, s, q, tid, nthr);
     cp_async_wait_all();
     __syncthreads();
     for (int j = warp; j < cown; j += nwarps) {
-        const bool o = clause_out(k, s, j, s.rec3 + 4);
+        const bool o = clause_out(k, s, j, REC(0) + 4);
         if (lane == 0) s.nout[j] = o;
     }
     __syncthreads();
-    long long vl = 0, vn = 0;  // thread 0: partial sums of the current example
-    if (warp == 0) votes_pass(k, s, cown, 0, vl, vn);
+    // arrival of step 0: one relaxed atomic per word carries the arrival
+    // count (bits 40..63) and the biased partial class sum (bits 0..39)
+    if (warp == 0) {
+        long long vl = 0, vn = 0;
+        votes_pass(k, s, cown, 0, vl, vn);
+        if (lane == 0 && n > 0) {
+            red_relaxed_add_u64(&k.rec[0], (1ull << 40) + (unsigned long long)(vl + kVoteBias));
+            red_relaxed_add_u64(&k.rec[1], (1ull << 40) + (unsigned long long)(vn + kVoteBias));
+        }
+    }
 
     Counters cn;
     const bool prof = k.phase != nullptr;
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long t_mark = clock64();
     for (int64_t i = 0; i < n; ++i) {
-        uint32_t *rc = s.rec3 + (int)(i % 3) * k.R;
+        uint32_t *rc = REC(i);
         const uint32_t *lit = rc + 4;
         const int label = (int)rc[1], neg = (int)rc[2];
         const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
-        // 1. arrival: one relaxed atomic per word carries the arrival count
-        //    (bits 40..63) and the biased partial (bits 0..39)
-        if (tid == 0) {
-            red_relaxed_add_u64(&k.rec[i * 2 + 0], (1ull << 40) + (unsigned long long)(vl + kVoteBias));
-            red_relaxed_add_u64(&k.rec[i * 2 + 1], (1ull << 40) + (unsigned long long)(vn + kVoteBias));
-            TIMELINE(i, 0);
-        }
+        const bool more = i + 1 < n;
+        const int par = (int)((i + 1) & 1);
+        const uint32_t *rn = REC(i + 1);
+        const int label1 = more ? (int)rn[1] : 0, neg1 = more ? (int)rn[2] : 0;
+        // 1. arrival (issued at the end of the previous step, or in the
+        //    prologue for step 0)
         PHASE(0);
         if (warp == 0) {
             // 2. all-reduce, then the decision (feedback.py:33-53): lane 0
-            //    the target threshold, lane 1 the negative one
-            //    The whole warp spins on the same 16 B (one request per
-            //    iteration) so it stays converged: a lone spinning lane
-            //    sends the lanes waiting for it down the collective slow path.
+            //    the target threshold, lane 1 the negative one.  The whole
+            //    warp spins on the same 16 B (one request per iteration) so
+            //    it stays converged.
             const unsigned long long want = (unsigned long long)n_cta;
             ulonglong2 p;
             do {
@@ -911,16 +975,14 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
             } while ((p.x >> 40) != want || (p.y >> 40) != want);
             TIMELINE(i, 1);
             PHASE(1);
-            const unsigned long long px = p.x, py = p.y;
             const long long bias = (long long)n_cta * kVoteBias;
-            const long long gl = (long long)(px & ((1ull << 40) - 1)) - bias;
-            const long long gn = (long long)(py & ((1ull << 40) - 1)) - bias;
+            const long long gl = (long long)(p.x & ((1ull << 40) - 1)) - bias;
+            const long long gn = (long long)(p.y & ((1ull << 40) - 1)) - bias;
             if (lane < 2) {
                 const long long T = k.T;
                 const long long v = lane == 0 ? gl : gn;
                 const long long cv = v < -T ? -T : (v > T ? T : v);
-                s.thr[lane] = (k.dbg & 4) ? 0 : (k.dbg & 8) ? (1ull << 44)
-                                               : threshold_of(lane == 0 ? T - cv : T + cv, T);
+                s.thr[lane] = (k.dbg & 4) ? 0 : threshold_of(lane == 0 ? T - cv : T + cv, T);
             }
             if (k.trace && rank == 0 && lane == 0) {
                 k.trace[i * 4 + 0] = neg;
@@ -929,28 +991,23 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
             }
             PHASE(2);
         } else {
-            // shadow of the all-reduce: record i+2 in flight, and the
-            // outputs of example i+1 under the current include masks
-            long long sh0 = 0;
-            if (prof && tid == 32) sh0 = clock64();
-            if (i + 2 < n) rec_issue(k, s, i + 2, tid - 32, nthr - 32);
-            // outputs of example i into info (read by this step's events);
-            // outputs of example i+1 and their contributions to its two
-            // class sums with the weights as they stand (the end of the step
-            // corrects the clauses this step touches)
-            const int par = (int)((i + 1) & 1);
+            // shadow of the all-reduce: record i+3 in flight; outputs of
+            // example i into info (read by this step's events); outputs of
+            // example i+1 with the current masks and their contributions to
+            // its two class sums with the current weights (the clauses this
+            // step touches are corrected later)
+            if (i + 3 < n) rec_issue(k, s, i + 3, tid - 32, nthr - 32);
+            else cp_async_commit();
             const int *nc = s.nout + (int)(i & 1) * k.cmax;
             int *no = s.nout + par * k.cmax;
             long long *cl = s.clo + par * 2 * k.cmax;
-            const bool more = i + 1 < n && !(k.dbg & 16);
-            const uint32_t *rn = s.rec3 + (int)((i + 1) % 3) * k.R;
-            const int label1 = more ? (int)rn[1] : 0, neg1 = more ? (int)rn[2] : 0;
+            const bool ev1 = more && !(k.dbg & 16);
             for (int j = warp - 1; j < cown; j += nwarps - 1) {
                 bool o = false;
-                if (more) o = clause_out(k, s, j, rn + 4);
+                if (ev1) o = clause_out(k, s, j, rn + 4);
                 if (lane == 0) {
                     s.info[j] = nc[j] ? I_OUT : 0;
-                    if (more) {
+                    if (ev1) {
                         no[j] = o;
                         const long long a = o ? s.weights[j * k.K + label1] : 0;
                         const long long b = o ? s.weights[j * k.K + neg1] : 0;
@@ -961,23 +1018,42 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                     }
                 }
             }
-            (void)sh0;
+            cp_async_wait_1();  // record i+2 landed (this thread's part); B1 publishes it
         }
         __syncthreads();
         PHASE(3);
+        const uint64_t tt = s.thr[0], tn = s.thr[1];
+        if ((tt | tn) == 0) {
+            // both update probabilities are 0 (the example is learned): no
+            // events, nothing changes, the shadow's sums for example i+1 are
+            // final -- arrive for it at once
+            if (warp == 0) {
+                if (lane < 2 && more) {
+                    const long long v = (long long)s.vsh[par * 2 + lane];
+                    s.vsh[par * 2 + lane] = 0;
+                    red_relaxed_add_u64(&k.rec[(i + 1) * 2 + lane],
+                                        (1ull << 40) + (unsigned long long)(v + kVoteBias));
+                }
+                if (k.trace && rank == 0 && lane == 0) k.trace[i * 4 + 3] = 0;
+                if (more) TIMELINE(i + 1, 0);
+            }
+            PHASE(7);
+            continue;
+        }
         // 3. the step's events: every entry of the buckets up to the
-        //    threshold's bucket whose key is below it (exact draw on a tie);
-        //    count those before c0 (window ordinals) and in total, and flag
-        //    the own clauses'
+        //    threshold's bucket whose key is below it (exact draw on a tie).
+        //    Few entries: warp 0 alone, no extra barrier; else all warps.
+        const uint32_t *ent = rc + rec_entries(k);
+        const unsigned tbt = (unsigned)(tt >> 37), tbn = (unsigned)(tn >> 37);
+        int hi_t, hi_n;
         {
-            const uint32_t *ent = rc + rec_entries(k);
             const uint16_t *off = reinterpret_cast<const uint16_t *>(rc + rec_buckets(k));
-            const uint64_t tt = s.thr[0], tn = s.thr[1];
-            const unsigned tbt = (unsigned)(tt >> 37), tbn = (unsigned)(tn >> 37);
-            const int hi_t = tbt >= 65536u ? C : off[(tbt >> 8) + 1];
-            const int hi_n = tbn >= 65536u ? C : off[260 + (tbn >> 8) + 1];
-            unsigned pre = 0, tot = 0;
-            for (int e = tid; e < hi_t + hi_n; e += nthr) {
+            hi_t = tbt >= 65536u ? C : off[(tbt >> 8) + 1];
+            hi_n = tbn >= 65536u ? C : off[260 + (tbn >> 8) + 1];
+        }
+        const int ne = hi_t + hi_n;
+        auto count_entries = [&](int t0, int nt, unsigned &pre, unsigned &tot) {
+            for (int e = t0; e < ne; e += nt) {
                 const int str = e >= hi_t ? 1 : 0;
                 const uint32_t v = ent[str * k.Cp + e - str * hi_t];
                 const unsigned key = v >> 16, c = v & 0xFFFFu;
@@ -991,28 +1067,17 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                     if (c >= (unsigned)c0 && c < (unsigned)c1) atomicOr(&s.oflag[c - c0], 1 << str);
                 }
             }
-            pre = __reduce_add_sync(0xffffffffu, pre);
-            tot = __reduce_add_sync(0xffffffffu, tot);
-            if (lane == 0) {
-                s.wcnt[warp] = pre;
-                s.wcnt[16 + warp] = tot;
-            }
-        }
-        __syncthreads();
-        PHASE(4);
-        // 4-5. warp 0: window ordinals, event types, weights, work list
-        if (warp == 0) {
-            unsigned pv = lane < nwarps ? s.wcnt[lane] : 0u;
-            unsigned tv = lane < nwarps ? s.wcnt[16 + lane] : 0u;
-            pv = __reduce_add_sync(0xffffffffu, pv);
-            tv = __reduce_add_sync(0xffffffffu, tv);
+        };
+        // 4-5. warp 0: window ordinals (events before c0 + own prefix),
+        //      event types, weights, work list
+        auto own_events = [&](unsigned pv, unsigned tv) {
             if (lane == 0) s.misc[0] = 0;
             __syncwarp();
             const uint64_t obase = s.blk_ctr[0] + pv;
             unsigned carry = 0;
             for (int jb = 0; jb < cown; jb += 32) {
                 const int j = jb + lane;
-                const int f = j < cown ? s.oflag[j] : 0;  // cleared at the step's end
+                const int f = j < cown ? s.oflag[j] : 0;
                 const unsigned v = (unsigned)(f & 1) + (unsigned)(f >> 1);
                 unsigned x = v;
 #pragma unroll
@@ -1020,9 +1085,11 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                     const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
                     if (lane >= o) x += y;
                 }
-                if (j < cown)
-                    apply_events(k, s, cn, j, f & 1, f & 2, obase + carry + (x - v), s.blk_seed[0],
-                                 label, neg);
+                if (f) {
+                    s.oflag[j] = 0;
+                    fast_events(k, s, cn, j, f & 1, f & 2, obase + carry + (x - v), label, neg,
+                                more, par, label1, neg1);
+                }
                 carry += __shfl_sync(0xffffffffu, x, 31);
             }
             __syncwarp();
@@ -1030,67 +1097,76 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                 s.blk_ctr[0] += (uint64_t)tv;
                 if (k.trace && rank == 0) k.trace[i * 4 + 3] = tv;
             }
+        };
+        if (ne <= 64) {
+            if (warp == 0) {
+                unsigned pre = 0, tot = 0;
+                count_entries(lane, 32, pre, tot);
+                pre = __reduce_add_sync(0xffffffffu, pre);
+                tot = __reduce_add_sync(0xffffffffu, tot);
+                __syncwarp();
+                own_events(pre, tot);
+            }
+        } else {
+            unsigned pre = 0, tot = 0;
+            count_entries(tid, nthr, pre, tot);
+            pre = __reduce_add_sync(0xffffffffu, pre);
+            tot = __reduce_add_sync(0xffffffffu, tot);
+            if (lane == 0) {
+                s.wcnt[warp] = pre;
+                s.wcnt[16 + warp] = tot;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                unsigned pv = lane < nwarps ? s.wcnt[lane] : 0u;
+                unsigned tv = lane < nwarps ? s.wcnt[16 + lane] : 0u;
+                pv = __reduce_add_sync(0xffffffffu, pv);
+                tv = __reduce_add_sync(0xffffffffu, tv);
+                own_events(pv, tv);
+            }
         }
         __syncthreads();
-        PHASE(5);
-        // 6. per-position Type I / II updates of the work list
-        const int n_work = s.misc[0];
-        feedback_quads<SMEM_STATES>(k, s, c0, lit, (k.dbg & 1) ? 0 : n_work, cn);
-        cp_async_wait_all();  // record i+2 landed
-        __syncthreads();
-        PHASE(6);
-        TIMELINE(i, 2);
-        if (i + 1 < n) {
-            // 7. re-evaluate, for example i+1, the clauses the feedback changed
-            if (n_work > 0) {
-                const uint32_t *litn = s.rec3 + (int)((i + 1) % 3) * k.R + 4;
-                int *no = s.nout + (int)((i + 1) & 1) * k.cmax;
+        PHASE(4);
+        // 6. per-position Type I / II updates of the work list, then the
+        //    re-evaluation for example i+1 of the clauses they changed (with
+        //    the correction of its class sums)
+        const int n_work = (k.dbg & 1) ? 0 : s.misc[0];
+        if (n_work > 0) {
+            feedback_quads<SMEM_STATES>(k, s, c0, lit, n_work, cn);
+            __syncthreads();
+            PHASE(5);
+            if (more) {
+                int *no = s.nout + par * k.cmax;
+                const long long *cl = s.clo + par * 2 * k.cmax;
                 for (int q = warp; q < n_work; q += nwarps) {
                     const int j = s.work[q];
-                    const bool o = clause_out(k, s, j, litn);
-                    if (lane == 0) no[j] = o;
+                    const bool o = clause_out(k, s, j, rn + 4);
+                    if (lane == 0) {
+                        no[j] = o;
+                        const long long dl = (o ? s.weights[j * k.K + label1] : 0) - cl[j];
+                        const long long dn = (o ? s.weights[j * k.K + neg1] : 0) - cl[k.cmax + j];
+                        if (dl) atomicAdd(&s.vsh[par * 2 + 0], (unsigned long long)dl);
+                        if (dn) atomicAdd(&s.vsh[par * 2 + 1], (unsigned long long)dn);
+                    }
                 }
                 __syncthreads();
             }
-            // 8. warp 0: partial sums of example i+1 = the shadow's sums
-            //    corrected for the clauses this step's events touched
-            //    (weights of label / negative, outputs via the re-evaluation)
-            if (warp == 0) {
-                const int par = (int)((i + 1) & 1);
-                const uint32_t *rn = s.rec3 + (int)((i + 1) % 3) * k.R;
-                const int label1 = (int)rn[1], neg1 = (int)rn[2];
-                const int *no = s.nout + par * k.cmax;
-                const long long *cl = s.clo + par * 2 * k.cmax;
-                long long dl = 0, dn = 0;
-                bool any = false;
-                for (int j = lane; j < cown; j += 32) {
-                    if (s.oflag[j]) {
-                        s.oflag[j] = 0;
-                        any = true;
-                        const bool o = no[j] != 0;
-                        dl += (o ? s.weights[j * k.K + label1] : 0) - cl[j];
-                        dn += (o ? s.weights[j * k.K + neg1] : 0) - cl[k.cmax + j];
-                    }
-                }
-                vl = (long long)s.vsh[par * 2 + 0];
-                vn = (long long)s.vsh[par * 2 + 1];
-                if (__any_sync(0xffffffffu, any)) {
-                    long long a, b;
-                    warp_sum2(dl, dn, a, b);
-                    vl += a;
-                    vn += b;
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    s.vsh[par * 2 + 0] = 0;
-                    s.vsh[par * 2 + 1] = 0;
-                }
-            }
+            PHASE(6);
         }
+        TIMELINE(i, 2);
+        // 7. thread 0: class sums of example i+1 -> its arrival
+        //    (lane 0: label word, lane 1: negative word, one instruction)
+        if (warp == 0 && lane < 2 && more) {
+            const long long v = (long long)s.vsh[par * 2 + lane];
+            s.vsh[par * 2 + lane] = 0;
+            red_relaxed_add_u64(&k.rec[(i + 1) * 2 + lane], (1ull << 40) + (unsigned long long)(v + kVoteBias));
+        }
+        if (more) TIMELINE(i + 1, 0);
         PHASE(7);
     }
     if (prof && tid == 0)
         for (int q = 0; q < 8; ++q) k.phase[rank * 8 + q] = ph[q];
+    cp_async_wait_all();
     __syncthreads();
     store_slice<SMEM_STATES>(k, s, c0, cown);
     if (tid == 0 && rank == n_cta - 1) k.block_counters[0] = s.blk_ctr[0];

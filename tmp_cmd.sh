@@ -1,1 +1,2 @@
-python tools/phase_profile.py --cta 148 --epochs 1 --n-train 6000 > /dev/null 2>&1 && ncu --set full --import-source on --clock-control none -k regex:k_train_fast -c 1 -o gpurun_out/prof_fast2 python tools/phase_profile.py --cta 148 --epochs 1 --n-train 6000 > gpurun_out/ncu_fast.log 2>&1; tail -1 gpurun_out/ncu_fast.log
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+python tools/phase_profile.py --cta 148 --epochs 4 > gpurun_out/pp.txt 2>&1

@@ -18,8 +18,8 @@ from paper_2405_04212_b200.runtime import ptr  # noqa: E402
 
 NAMES = ["eval(+votes)", "arrive", "precompute", "wait+decide", "flag bitmaps",
          "scan+events", "feedback", "-"]
-NAMES_FAST = ["arrive", "all-reduce wait", "decide", "sync (B1)", "event count", "events (warp 0)",
-              "feedback", "re-eval+votes"]
+NAMES_FAST = ["arrive", "all-reduce wait", "decide", "sync (B1)", "events (count+apply)",
+              "feedback", "re-eval", "sums"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cta", type=int, nargs="*", default=[16, 148])
