@@ -177,6 +177,9 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
     // quad index it = (work item wc, quad rem), advanced by nthr per unit
     // without a division (nthr < 2 * QP is not assumed: a short loop)
     int wc_next = tid / QP, rem_next = tid - (tid / QP) * QP;
+    const uint64_t t_inc = k.fp.t_inc, t_dec = k.fp.t_dec;
+    const int smin = k.fp.smin, smax = k.fp.smax, boost = k.fp.boost ? 1 : 0;
+    unsigned nd = 0, nupd = 0;  // draws consumed / states changed (statistics)
     for (int it0 = tid; it0 < total; it0 += B * nthr) {
         uint32_t word[B];
         int jj[B], pp[B];
@@ -218,34 +221,50 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
             const int info = s.info[j];
             const int out = (info & I_OUT) ? 1 : 0;
             const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
-            uint32_t nw = word[u], nib = 0;
-            // draw counters of position p0 in both streams; p0 + b adds b*G
-            const uint64_t zt = s.sk_t[j] + kGolden * (uint64_t)p0;
-            const uint64_t zn = s.sk_n[j] + kGolden * (uint64_t)p0;
+            const int lim = k.P - p0;  // positions b < lim are real (the rest is row padding)
+            int st[4], s0[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) s0[b] = st[b] = (int)(int8_t)(word[u] >> (8 * b));
+            // Type I (kernels/_numba.py:71-90) on the quad with draw
+            // mix64(z0 + b*G) for position p0 + b, branch-free: the draw is
+            // computed for every position and counted / used only where the
+            // reference consumes it.  Type II (:93-98) likewise.
+            auto type_i = [&](uint64_t z0) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int vb = b < lim ? 1 : 0;
+                    const int inc = out & (int)((litn >> b) & 1u);
+                    const uint64_t thr = inc ? t_inc : t_dec;
+                    const int hit = (mix64(z0 + kGolden * (uint64_t)b) >> 11) < thr ? 1 : 0;
+                    const int room = st[b] < smax ? 1 : 0;
+                    const int above = st[b] > smin ? 1 : 0;
+                    nd += vb & (inc ? (room & (boost ^ 1)) : above);
+                    const int delta = (inc & room & (boost | hit)) - ((inc ^ 1) & above & hit);
+                    st[b] += vb ? delta : 0;
+                }
+            };
+            auto type_ii = [&]() {
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    st[b] += (b < lim ? 1 : 0) & out & (int)(((litn >> b) & 1u) ^ 1u) & (st[b] < 0 ? 1 : 0);
+            };
+            if (info & I_TEV) {
+                if (info & I_T1) type_i(s.sk_t[j] + kGolden * (uint64_t)p0);
+                else type_ii();
+            }
+            if (info & I_NEV) {
+                if (info & I_N1) type_i(s.sk_n[j] + kGolden * (uint64_t)p0);
+                else type_ii();
+            }
+            uint32_t nib = 0;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                const int p = p0 + b;
-                int st = (int)(int8_t)(word[u] >> (8 * b));
-                if (p < k.P) {
-                    const int l = (litn >> b) & 1;
-                    const int st0 = st;
-                    uint64_t nd = 0;
-                    if (info & I_TEV) {
-                        if (info & I_T1) st = type_i_bf(st, l, out, k.fp, zt + kGolden * (uint64_t)b, nd);
-                        else st = type_ii(st, l, out);
-                    }
-                    if (info & I_NEV) {
-                        if (info & I_N1) st = type_i_bf(st, l, out, k.fp, zn + kGolden * (uint64_t)b, nd);
-                        else st = type_ii(st, l, out);
-                    }
-                    cn.draws += nd;
-                    if (st != st0) {
-                        ++cn.upd;
-                        nw = (nw & ~(0xFFu << (8 * b))) | ((uint32_t)(uint8_t)st << (8 * b));
-                    }
-                    nib |= (uint32_t)(st >= 0) << b;
-                }
+                nupd += st[b] != s0[b] ? 1 : 0;
+                nib |= (uint32_t)(b < lim && st[b] >= 0) << b;
             }
+            const uint32_t nw = __byte_perm(__byte_perm((uint32_t)st[0], (uint32_t)st[1], 0x0040),
+                                            __byte_perm((uint32_t)st[2], (uint32_t)st[3], 0x0040),
+                                            0x5410);
             if (nw != word[u]) {
                 if (SMEM_STATES) {
                     *reinterpret_cast<uint32_t *>(s.states + (size_t)j * k.Ppad + p0) = nw;
@@ -276,6 +295,8 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
             }
         }
     }
+    cn.draws += nd;
+    cn.upd += nupd;
 }
 
 // Load the model slice into shared memory, build include masks and counts.
@@ -982,7 +1003,8 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                 const long long T = k.T;
                 const long long v = lane == 0 ? gl : gn;
                 const long long cv = v < -T ? -T : (v > T ? T : v);
-                s.thr[lane] = (k.dbg & 4) ? 0 : threshold_of(lane == 0 ? T - cv : T + cv, T);
+                s.thr[lane] = (k.dbg & 4) ? 0 : (k.dbg & 32) ? (1ull << 50)
+                                               : threshold_of(lane == 0 ? T - cv : T + cv, T);
             }
             if (k.trace && rank == 0 && lane == 0) {
                 k.trace[i * 4 + 0] = neg;
@@ -1035,6 +1057,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                                         (1ull << 40) + (unsigned long long)(v + kVoteBias));
                 }
                 if (k.trace && rank == 0 && lane == 0) k.trace[i * 4 + 3] = 0;
+                TIMELINE(i, 2);
                 if (more) TIMELINE(i + 1, 0);
             }
             PHASE(7);

@@ -42,6 +42,8 @@ for n_cta in args.cta:
     ph = torch.zeros(nc * (8 + 192), dtype=torch.int64, device="cuda")
     _lib.call("tmb_trainer_set_profile", sess._h, ptr(ph))
     _lib.call("tmb_set_option", b"train.debug_skip", args.skip)
+    trace = torch.zeros(len(ty) * 4, dtype=torch.int64, device="cuda")
+    _lib.call("tmb_trainer_set_trace", sess._h, ptr(trace))
     st = torch.cuda.Event(enable_timing=True)
     en = torch.cuda.Event(enable_timing=True)
     st.record()
@@ -88,3 +90,11 @@ for n_cta in args.cta:
         print("             median end minus median detect     ", q(E - D))
         print("             max end minus median end           ", q(EM - E))
         print("             next median arrival minus med. end ", q(A[1:] - E[:-1]))
+        evs = trace.cpu().numpy().reshape(-1, 4)[64:128, 3]
+        dur = np.diff(np.median(tl[:, :, 1], axis=1))  # detect-to-detect per step
+        ev_next = evs[:-1]
+        for name, m in (("empty", ev_next == 0), ("1-100 events", (ev_next > 0) & (ev_next <= 100)),
+                        (">100 events", ev_next > 100)):
+            if m.any():
+                print(f"   steps with {name:13s}: n={m.sum():3d} median detect-to-detect "
+                      f"{np.median(dur[m]):6.0f} ns mean {dur[m].mean():6.0f}")
