@@ -59,7 +59,9 @@ uint64_t tmb_launch_count(void);
 
 /* All-reduce latency microbenchmark (design evidence for the trainer's
  * per-example synchronisation).  mode 0: relaxed red + poll;
- * 1: same with backoff; 2: 8 sub-counters; 3: cooperative grid.sync(). */
+ * 1: same with backoff; 2: 8 sub-counters; 3: cooperative grid.sync();
+ * 4: the trainer's protocol (two words in one 16 B slot, warp-wide spin);
+ * 5: the two words in different 128 B lines. */
 int tmb_microbench_allreduce(int n_cta, int threads, int iters, int mode,
                              double *us_per_iter);
 

@@ -23,6 +23,9 @@ __device__ __forceinline__ unsigned long long mb_ld(const unsigned long long *p)
 // mode 2: every CTA's red goes to one of 8 words 256 B apart; warp 0 polls
 //         all 8 in parallel.
 // mode 3: cooperative_groups grid.sync().
+// mode 4: the trainer's protocol -- two words in one 16 B slot, both red by
+//         thread 0, warp 0 spins on a 16 B load.
+// mode 5: the two words in different 128 B lines (two loads per spin).
 __global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
                                unsigned long long *cycles) {
     const int n = gridDim.x;
@@ -30,6 +33,25 @@ __global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
     for (int i = 0; i < iters; ++i) {
         if (mode == 3) {
             cg::this_grid().sync();
+            continue;
+        }
+        if (mode == 4 || mode == 5) {
+            unsigned long long *w0 = slots + (size_t)i * 32;
+            unsigned long long *w1 = w0 + (mode == 4 ? 1 : 16);
+            if (threadIdx.x < 2) mb_red(threadIdx.x == 0 ? w0 : w1, 1ull);
+            if (threadIdx.x < 32) {
+                unsigned long long a, b;
+                do {
+                    if (mode == 4) {
+                        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                                     : "=l"(a), "=l"(b) : "l"(w0) : "memory");
+                    } else {
+                        a = mb_ld(w0);
+                        b = mb_ld(w1);
+                    }
+                } while (a < (unsigned long long)n || b < (unsigned long long)n);
+            }
+            __syncthreads();
             continue;
         }
         if (mode == 2) {
