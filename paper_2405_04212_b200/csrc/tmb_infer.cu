@@ -584,6 +584,442 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     if (bad) atomicOr(k.bad_input, 1u);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised cluster kernel (same cluster / tile / rule split as
+// k_infer_cluster, same results): warps [0, 8) of every CTA only transpose
+// (HBM -> X^T), warps [8, 16) only evaluate, so the HBM reads of tile t+1
+// overlap the rule evaluation of tile t instead of alternating with it.
+// Hand-offs are mbarriers, no cluster-wide barrier per tile:
+//   full[b]   (per CTA)  local transposers arrive + 3 peers' bulk copies (tx)
+//   empty[b]  (per CTA)  the 4 CTAs' evaluator groups are done with buffer b
+//   vfull[b]  (owner)    the 4 CTAs pushed their partial sums for block b
+//   vempty[b] (writer)   the 4 owners consumed this CTA's partials of slot b
+__device__ __forceinline__ void mbar_arrive_local(uint64_t *mb) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t mb_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mb_cluster)
+                 : "memory");
+}
+// arrival that publishes nothing (the barrier only orders reads before it)
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t mb_cluster) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mb_cluster)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *mb, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done) : "r"(smem_u32(mb)), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+constexpr int kWsT = 8;  // transposer warps per CTA; the last warp finalizes, the rest evaluate
+
+__global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int nE = nwarps - kWsT - 1;
+    const int K = k.K;
+    const int64_t F = k.F;
+    const int xrows = (int)F + 1;
+    // shared layout: heads | xt[2] | part | inbox[2][kCS][32][K] | iflag[2][kCS] | dirty | mbar[8]
+    uint4 *heads = reinterpret_cast<uint4 *>(smem_raw);
+    uint32_t *xt0 = reinterpret_cast<uint32_t *>(heads + 2 * (size_t)k.rloc_max);
+    uint32_t *xt1 = xt0 + (size_t)xrows * kTG;
+    int32_t *part = reinterpret_cast<int32_t *>(xt1 + (size_t)xrows * kTG);  // [32*kTG][K]
+    int32_t *inbox = part + 32 * kTG * K;                                    // [2][kCS][32][K]
+    int32_t *iflag = inbox + 2 * kCS * 32 * K;                               // [2][kCS]
+    int32_t *dirty2 = iflag + 2 * kCS;                                       // [2][kTG]
+    uint64_t *mb = reinterpret_cast<uint64_t *>(
+        reinterpret_cast<uintptr_t>(dirty2 + 2 * kTG + 3) & ~(uintptr_t)7);  // [8]
+    uint64_t *full = mb, *empty = mb + 2, *vfull = mb + 4, *vempty = mb + 6;
+
+    const int r0 = (int)((int64_t)rank * k.R / kCS), r1 = (int)((int64_t)(rank + 1) * k.R / kCS);
+    const int rloc = r1 - r0;
+    for (int i = tid; i < rloc * 2; i += blockDim.x)
+        heads[i] = reinterpret_cast<const uint4 *>(k.heads)[(size_t)r0 * 2 + i];
+    if (tid < kTG) {
+        xt0[(size_t)F * kTG + tid] = 0xFFFFFFFFu;
+        xt1[(size_t)F * kTG + tid] = 0xFFFFFFFFu;
+    }
+    for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
+    if (tid < 2 * kTG) dirty2[tid] = 0;
+    if (tid < 2 * kCS) iflag[tid] = 0;
+
+    const int64_t tile_n = 32 * kTG;
+    const int64_t n_tiles = (k.N + tile_n - 1) / tile_n;
+    const int n_clusters = gridDim.x / kCS;
+    const int cid = blockIdx.x / kCS;
+    const int nch = (int)((F + 31) / 32);
+    const int ch0 = (int)((int64_t)rank * nch / kCS), ch1 = (int)((int64_t)(rank + 1) * nch / kCS);
+    const int64_t qf0 = (int64_t)ch0 * 32;
+    const int64_t qf1 = std::min<int64_t>((int64_t)ch1 * 32, F);
+    const int nblk = (int)((qf1 - qf0 + 127) / 128);
+    const uint32_t my_bytes = (uint32_t)((qf1 > qf0 ? qf1 - qf0 : 0) * 16);
+    const uint32_t expect_bytes = (uint32_t)(F * 16) - my_bytes;
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], kCS);
+        mbar_init(&empty[1], kCS);
+        mbar_init(&vfull[0], kCS);
+        mbar_init(&vfull[1], kCS);
+        mbar_init(&vempty[0], kCS);
+        mbar_init(&vempty[1], kCS);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster.sync();
+    const int64_t n_my = cid < n_tiles ? (n_tiles - cid + n_clusters - 1) / n_clusters : 0;
+    uint32_t bad = 0;
+    unsigned long long hits = 0;
+    // phase profile (k.phase): thread 0 = transposer slots 0..3, thread
+    // 32*kWsT = evaluator slots 4..7
+    const bool prof = k.phase && (tid == 0 || tid == 32 * kWsT);
+    unsigned long long wph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long wmark = clock64();
+#define WPH(n)                                                            \
+    do {                                                                  \
+        if (prof) {                                                       \
+            const long long now = clock64();                              \
+            wph[n] += (unsigned long long)(now - wmark);                  \
+            wmark = now;                                                  \
+        }                                                                 \
+    } while (0)
+
+    if (warp < kWsT) {
+        // ================= transposer group =================
+        // Each warp owns units u = warp + kWsT*q (q < nq) of every tile
+        // (unit = 32 examples x 128 features).  The loads of the next unit
+        // (possibly of the next tile) are issued before the current unit is
+        // transposed, so HBM latency overlaps the bit work.
+        const int j = lane >> 3, c16 = lane & 7;
+        const int units = nblk * kTG;
+        const int nq = units > warp ? (units - warp + kWsT - 1) / kWsT : 0;
+        const int64_t total = n_my * (int64_t)nq;
+        const uint32_t psel = (uint32_t)(j | ((1 ^ j) << 4) | ((2 ^ j) << 8) | ((3 ^ j) << 12));
+        auto load_item = [&](int64_t sidx, uint4 (&w)[8], int64_t &fb_out, int &g_out) {
+            const int64_t itx = sidx / nq;
+            const int u = warp + kWsT * (int)(sidx - itx * nq);
+            const int64_t e0 = (cid + itx * n_clusters) * tile_n;
+            const int g = u % kTG;
+            const int64_t fb = qf0 + (int64_t)(u / kTG) * 128 + 16 * c16;
+            fb_out = fb;
+            g_out = g;
+            const int64_t er = e0 + 32 * g + 8 * j;  // first of my 8 rows
+            if (k.vec_ok && fb + 16 <= qf1 && er + 7 < k.N) {
+                // common case: 8 unconditional 16-byte streaming loads
+                const uint8_t *src = k.x + er * F + fb;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = __ldcs(reinterpret_cast<const uint4 *>(src + i * F));
+                return;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int64_t e = er + i;
+                w[i] = make_uint4(0, 0, 0, 0);
+                if (e < k.N && fb < qf1) {
+                    const uint8_t *src = k.x + e * F + fb;
+                    if (k.vec_ok && fb + 16 <= F) {
+                        w[i] = __ldcs(reinterpret_cast<const uint4 *>(src));
+                    } else {
+                        uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+                        for (int bb = 0; bb < 16; ++bb) {
+                            if (fb + bb >= F) break;
+                            const uint32_t byte = (uint32_t)src[bb] << (8 * (bb & 3));
+                            if (bb < 4) b0 |= byte;
+                            else if (bb < 8) b1 |= byte;
+                            else if (bb < 12) b2 |= byte;
+                            else b3 |= byte;
+                        }
+                        w[i] = make_uint4(b0, b1, b2, b3);
+                    }
+                }
+            }
+        };
+        // 0/1 bytes -> bits (bit t = byte t); bytes > 1 are flagged as bad
+        // input and abort the call, so no masking here
+        auto pk = [](uint32_t x) -> uint32_t { return (x * 0x01020408u) >> 24; };
+        auto finish_item = [&](const uint4 (&w)[8], int64_t fb, int g, uint32_t *mine) {
+            uint32_t v[8];
+            uint32_t ob = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                ob |= w[i].x | w[i].y | w[i].z | w[i].w;
+                v[i] = pk(w[i].x) | (pk(w[i].y) << 4) | (pk(w[i].z) << 8) | (pk(w[i].w) << 12);
+            }
+            bad |= ob & 0xFEFEFEFEu;
+            // byte i of lo / hi = bits 0-7 / 8-15 of v[i]
+            const uint32_t x01 = __byte_perm(v[0], v[1], 0x5140), x23 = __byte_perm(v[2], v[3], 0x5140);
+            const uint32_t x45 = __byte_perm(v[4], v[5], 0x5140), x67 = __byte_perm(v[6], v[7], 0x5140);
+            unsigned long long lo = (unsigned long long)__byte_perm(x01, x23, 0x5410) |
+                                    ((unsigned long long)__byte_perm(x45, x67, 0x5410) << 32);
+            unsigned long long hi = (unsigned long long)__byte_perm(x01, x23, 0x7632) |
+                                    ((unsigned long long)__byte_perm(x45, x67, 0x7632) << 32);
+            lo = transpose8x8(lo);
+            hi = transpose8x8(hi);
+            const uint32_t R0 = (uint32_t)lo, R1 = (uint32_t)(lo >> 32);
+            const uint32_t R2 = (uint32_t)hi, R3 = (uint32_t)(hi >> 32);
+            uint32_t recv[4];
+#pragma unroll
+            for (int sft = 0; sft < 4; ++sft) {
+                const int d = j ^ sft;
+                const uint32_t send = d == 0 ? R0 : d == 1 ? R1 : d == 2 ? R2 : R3;
+                recv[sft] = sft ? __shfl_xor_sync(0xffffffffu, send, 8 * sft) : send;
+            }
+            // 4x4 byte transpose (word kq gathers byte kq of recv[0..3]),
+            // then byte p <- byte p^j (recv[s] came from lane j^s)
+            const uint32_t t0 = __byte_perm(recv[0], recv[1], 0x5140);
+            const uint32_t t1 = __byte_perm(recv[2], recv[3], 0x5140);
+            const uint32_t t2 = __byte_perm(recv[0], recv[1], 0x7362);
+            const uint32_t t3 = __byte_perm(recv[2], recv[3], 0x7362);
+            uint32_t wq[4];
+            wq[0] = __byte_perm(__byte_perm(t0, t1, 0x5410), 0, psel);
+            wq[1] = __byte_perm(__byte_perm(t0, t1, 0x7632), 0, psel);
+            wq[2] = __byte_perm(__byte_perm(t2, t3, 0x5410), 0, psel);
+            wq[3] = __byte_perm(__byte_perm(t2, t3, 0x7632), 0, psel);
+            // store round r writes feature 4j + ((r + c16) & 3): the 32
+            // lanes of one store then cover all 8 bank quads of the 16-byte
+            // rows (4-way instead of 16-way bank conflicts)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int kq = (r + c16) & 3;
+                const uint32_t word = kq == 0 ? wq[0] : kq == 1 ? wq[1] : kq == 2 ? wq[2] : wq[3];
+                const int64_t f = fb + 4 * j + kq;
+                if (f < qf1) mine[(size_t)f * kTG + g] = word;
+            }
+        };
+        uint4 wa[8], wb[8];
+        int64_t fa = 0, fbx = 0;
+        int ga = 0, gbx = 0;
+        const bool do_t = !(k.dbg & 2);
+        // L2 prefetch of this CTA's quarter of tile `itx`'s rows (TMA bulk
+        // prefetch, one per example row; no registers, no shared memory)
+        const unsigned pf_bytes = (unsigned)((qf1 - qf0) & ~15LL);
+        auto prefetch_tile = [&](int64_t itx) {
+            if (itx >= n_my || !k.vec_ok || !pf_bytes) return;
+            const int64_t e0 = (cid + itx * n_clusters) * tile_n;
+            for (int i = tid; i < tile_n; i += 32 * kWsT) {
+                const int64_t e = e0 + i;
+                if (e < k.N)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(k.x + e * F + qf0),
+                                 "r"(pf_bytes) : "memory");
+            }
+        };
+        if (do_t && (k.dbg & 8)) {  // opt-in: measured no gain
+            prefetch_tile(0);
+            prefetch_tile(1);
+        }
+        if (do_t && total > 0) load_item(0, wa, fa, ga);
+        for (int64_t it = 0; it < n_my; ++it) {
+            const int buf = (int)(it & 1);
+            uint32_t *mine = buf ? xt1 : xt0;
+            if (do_t && (k.dbg & 8)) prefetch_tile(it + 2);
+            WPH(3);
+            // empty[] arrivals publish nothing: a CTA-scope wait (a cluster-
+            // scope acquire would invalidate L1 on every tile)
+            if (it >= 2) mbar_wait(&empty[buf], (uint32_t)(((it >> 1) + 1) & 1));
+            WPH(0);
+            if (do_t) {
+                for (int q = 0; q < nq; ++q) {
+                    const int64_t sidx = it * nq + q;
+                    if ((sidx & 1) == 0) {
+                        if (sidx + 1 < total) load_item(sidx + 1, wb, fbx, gbx);
+                        finish_item(wa, fa, ga, mine);
+                    } else {
+                        if (sidx + 1 < total) load_item(sidx + 1, wa, fa, ga);
+                        finish_item(wb, fbx, gbx, mine);
+                    }
+                }
+            }
+            WPH(1);
+            named_sync(1, 32 * kWsT);
+            if (tid == 0) {
+                // my quarter to the 3 peers (complete_tx on their full[buf]),
+                // then my own arrival (+ the bytes the peers will send me)
+                if (my_bytes) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const uint32_t src = smem_u32(mine + (size_t)qf0 * kTG);
+                    for (int p = 0; p < kCS; ++p) {
+                        if (p == rank) continue;
+                        bulk_copy_to_peer(mapa_u32(src, p), src, my_bytes,
+                                          mapa_u32(smem_u32(&full[buf]), p));
+                    }
+                }
+                if (expect_bytes) mbar_arm(&full[buf], expect_bytes);
+                else mbar_arrive_local(&full[buf]);
+            }
+            WPH(2);
+        }
+    } else if (warp == nwarps - 1) {
+        // ================= finalizer warp =================
+        // the 32 examples of block `rank` of every tile: wait for the four
+        // CTAs' partials (slot = tile parity), sum, argmax, write, release
+        for (int64_t it = 0; it < n_my; ++it) {
+            const int64_t t = cid + it * n_clusters;
+            const int buf = (int)(it & 1);
+            mbar_wait_cluster(&vfull[buf], (uint32_t)((it >> 1) & 1));
+            const int64_t e = t * tile_n + 32 * rank + lane;
+            const bool any = iflag[buf * kCS + 0] | iflag[buf * kCS + 1] | iflag[buf * kCS + 2] |
+                             iflag[buf * kCS + 3];
+            if (e < k.N) {
+                int best = 0;
+                if (any || k.votes) {
+                    int32_t bv = 0;
+                    for (int kk = 0; kk < K; ++kk) {
+                        int32_t sum = 0;
+#pragma unroll
+                        for (int p = 0; p < kCS; ++p)
+                            if (iflag[buf * kCS + p]) sum += inbox[((buf * kCS + p) * 32 + lane) * K + kk];
+                        if (kk == 0 || sum > bv) {
+                            bv = sum;
+                            best = kk;
+                        }
+                        if (k.votes) k.votes[e * K + kk] = (int64_t)sum;
+                    }
+                }
+                if (k.pred) k.pred[e] = best;  // all sums 0 -> class 0 (np.argmax)
+                if (k.labels) hits += (k.labels[e] == best);
+            }
+            __syncwarp();
+            if (lane < kCS) {
+                iflag[buf * kCS + lane] = 0;
+                mbar_arrive_remote(mapa_u32(smem_u32(&vempty[buf]), lane));
+            }
+        }
+    } else {
+        // ================= evaluator group =================
+        const int ew = warp - kWsT, etid = tid - 32 * kWsT;
+        const uint32_t haddr = smem_u32(heads);
+        for (int64_t it = 0; it < n_my; ++it) {
+            const int64_t t = cid + it * n_clusters;
+            const int buf = (int)(it & 1);
+            const uint32_t *xt = buf ? xt1 : xt0;
+            int32_t *dirty = dirty2 + buf * kTG;
+            WPH(7);
+            // the peers' quarters arrive by bulk copy (complete_tx), so the
+            // phase completion makes them visible: CTA-scope wait
+            mbar_wait(&full[buf], (uint32_t)((it >> 1) & 1));
+            WPH(4);
+            const uint32_t xaddr = smem_u32(xt);
+            // a rule's tail codes (CSR, global) and its votes into part[]
+            auto finish_rule = [&](int r, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+                const int rg = r0 + r;
+                for (int q = __ldg(&k.tail_ptr[rg]), qe = __ldg(&k.tail_ptr[rg + 1]);
+                     q < qe && (a0 | a1 | a2 | a3); ++q) {
+                    const uint32_t c = __ldg(&k.tails[q]);
+                    const uint4 x = lds128(xaddr + (c >> 1) * 16);
+                    const uint32_t m = 0u - (c & 1u);
+                    a0 &= x.x ^ m;
+                    a1 &= x.y ^ m;
+                    a2 &= x.z ^ m;
+                    a3 &= x.w ^ m;
+                }
+                const int32_t *wr = k.w + (size_t)rg * K;
+#pragma unroll
+                for (int gq = 0; gq < kTG; ++gq) {
+                    uint32_t acc = gq == 0 ? a0 : gq == 1 ? a1 : gq == 2 ? a2 : a3;
+                    if (acc) dirty[gq] = 1;
+                    while (acc) {
+                        const int b = __ffs(acc) - 1;
+                        acc &= acc - 1;
+                        int32_t *dst = part + (gq * 32 + b) * K;
+                        for (int kk = 0; kk < K; ++kk) {
+                            const int32_t wv = __ldg(&wr[kk]);
+                            if (wv) atomicAdd(&dst[kk], wv);
+                        }
+                    }
+                }
+            };
+            // two rules per lane (rc*64 + lane and +32): two independent
+            // shared-memory chains, early-exit vote every 4 codes
+            for (int rc = ew; rc * 64 < rloc && !(k.dbg & 1); rc += nE) {
+                const int rA = rc * 64 + lane, rB = rA + 32;
+                const uint32_t lA = rA < rloc ? 0xFFFFFFFFu : 0u, lB = rB < rloc ? 0xFFFFFFFFu : 0u;
+                uint32_t A0 = lA, A1 = lA, A2 = lA, A3 = lA, B0 = lB, B1 = lB, B2 = lB, B3 = lB;
+                const uint32_t hA = haddr + (rA < rloc ? rA : 0) * 32;
+                const uint32_t hB = haddr + (rB < rloc ? rB : 0) * 32;
+                const uint4 ha0 = lds128(hA), ha1 = lds128(hA + 16);
+                const uint4 hb0 = lds128(hB), hb1 = lds128(hB + 16);
+                const uint32_t wa[8] = {ha0.x, ha0.y, ha0.z, ha0.w, ha1.x, ha1.y, ha1.z, ha1.w};
+                const uint32_t wb[8] = {hb0.x, hb0.y, hb0.z, hb0.w, hb1.x, hb1.y, hb1.z, hb1.w};
+#pragma unroll
+                for (int grp = 0; grp < 4; ++grp) {
+#pragma unroll
+                    for (int q = 2 * grp; q < 2 * grp + 2; ++q) {
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const uint32_t ca = hh ? (wa[q] >> 16) : (wa[q] & 0xFFFFu);
+                            const uint32_t cb = hh ? (wb[q] >> 16) : (wb[q] & 0xFFFFu);
+                            const uint4 xa = lds128(xaddr + (ca >> 1) * 16);
+                            const uint4 xb = lds128(xaddr + (cb >> 1) * 16);
+                            const uint32_t ma = 0u - (ca & 1u), mb2 = 0u - (cb & 1u);
+                            A0 &= xa.x ^ ma;
+                            A1 &= xa.y ^ ma;
+                            A2 &= xa.z ^ ma;
+                            A3 &= xa.w ^ ma;
+                            B0 &= xb.x ^ mb2;
+                            B1 &= xb.y ^ mb2;
+                            B2 &= xb.z ^ mb2;
+                            B3 &= xb.w ^ mb2;
+                        }
+                    }
+                    if (!__any_sync(0xffffffffu, A0 | A1 | A2 | A3 | B0 | B1 | B2 | B3)) break;
+                }
+                if ((A0 | A1 | A2 | A3) && rA < rloc) finish_rule(rA, A0, A1, A2, A3);
+                if ((B0 | B1 | B2 | B3) && rB < rloc) finish_rule(rB, B0, B1, B2, B3);
+            }
+            named_sync(2, 32 * nE);
+            WPH(5);
+            // buffer `buf` is free as far as this CTA is concerned: tell all
+            // four transposer groups (they refill it for tile it+2)
+            if (etid < kCS) mbar_arrive_remote_relaxed(mapa_u32(smem_u32(&empty[buf]), etid));
+            // push the partial sums of example block b to owner b's inbox
+            // slot `buf` once the owners consumed slot `buf` of tile it-2
+            if (it >= 2) mbar_wait(&vempty[buf], (uint32_t)(((it >> 1) + 1) & 1));
+            const bool anyd = dirty[0] | dirty[1] | dirty[2] | dirty[3];
+            for (int i = etid; anyd && i < 32 * kTG * K; i += 32 * nE) {
+                const int b = i / (32 * K);
+                if (!dirty[b]) continue;
+                const int rem = i - b * 32 * K;
+                int32_t *dst = cluster.map_shared_rank(inbox, b);
+                dst[((buf * kCS + rank) * 32) * K + rem] = part[i];
+                part[i] = 0;
+            }
+            if (etid < kCS && dirty[etid]) cluster.map_shared_rank(iflag, etid)[buf * kCS + rank] = 1;
+            named_sync(2, 32 * nE);
+            if (etid < kCS) {
+                // owners zero their iflag slots after consuming them; only a
+                // block that received partials needs a releasing arrival
+                const uint32_t vb = mapa_u32(smem_u32(&vfull[buf]), etid);
+                if (dirty[etid]) mbar_arrive_remote(vb);
+                else mbar_arrive_remote_relaxed(vb);
+            }
+            __syncwarp();
+            if (etid < kTG) dirty[etid] = 0;  // next used by tile it+2
+            WPH(6);
+        }
+    }
+    if (prof && tid == 0)
+        for (int q = 0; q < 4; ++q) k.phase[blockIdx.x * 8 + q] = wph[q];
+    if (prof && tid == 32 * kWsT)
+        for (int q = 4; q < 8; ++q) k.phase[blockIdx.x * 8 + q] = wph[q];
+#undef WPH
+    cluster.sync();  // peers may still copy into / signal this CTA until here
+    if (k.correct) {
+        for (int o = 16; o; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+        if (lane == 0 && hits) atomicAdd(k.correct, hits);
+    }
+    if (bad) atomicOr(k.bad_input, 1u);
+}
+
 static unsigned int *g_bad_flag = nullptr;
 
 static int pick_g(int64_t F, int64_t K, int max_smem, int *G_out, size_t *smem_out) {
@@ -604,6 +1040,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
 
 int g_force_generic_infer = 0;
 int g_infer_dbg = 0;
+int g_infer_ws = 1;  // tmb_set_option("infer.warp_specialized", 0|1)
 unsigned long long *g_infer_phase = nullptr;
 
 int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, int64_t *pred,
@@ -657,7 +1094,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     const int64_t rloc_max = (r->R + kCS - 1) / kCS;
     const size_t smem = 32 * (size_t)rloc_max + 2 * 4 * (size_t)(r->F + 1) * kTG +
                         4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K +
-                        4 * (2 * kCS + kTG) + 32;
+                        4 * (2 * kCS + 2 * kTG) + 96;
     if (smem > (size_t)max_smem) return TMB_OK;  // generic kernel instead
     InferCK k;
     k.x = x; k.N = N; k.F = r->F; k.heads = r->heads; k.tail_ptr = r->tail_ptr; k.tails = r->tails;
@@ -667,7 +1104,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     k.rloc_max = (int)rloc_max;
     k.dbg = g_infer_dbg;
     k.phase = g_infer_phase;
-    const void *fn = (const void *)k_infer_cluster;
+    const void *fn = g_infer_ws ? (const void *)k_infer_ws : (const void *)k_infer_cluster;
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int threads = 512;
     cudaLaunchConfig_t lc = {};
@@ -924,6 +1361,10 @@ int tmb_set_option(const char *name, int64_t value) {
     }
     if (std::string(name) == "train.debug_skip") {  // timing ablations only (not bit-exact)
         g_train_dbg = (int)value;
+        return TMB_OK;
+    }
+    if (std::string(name) == "infer.warp_specialized") {
+        g_infer_ws = (int)value;
         return TMB_OK;
     }
     if (std::string(name) == "infer.debug_skip") {  // timing experiments only

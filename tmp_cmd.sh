@@ -1,1 +1,2 @@
-python bench.py > gpurun_out/bench_r01b.json 2> gpurun_out/bench_r01b.err; tail -c 2500 gpurun_out/bench_r01b.json
+timeout 300 python -m pytest tests -m gpu -x -q -k "infer or predictor or dataset_votes or mnist_shaped_prefix or facade" 2>&1 | tail -3
+timeout 300 python tools/infer_split.py 2>&1 | tail -14

@@ -8,6 +8,7 @@ import paper_2405_04212_b200 as tmb  # noqa: E402
 from paper_2405_04212_b200 import _lib, datasets  # noqa: E402
 
 tmb.runtime.require_device()
+_lib.call("tmb_set_option", b"infer.warp_specialized", 0 if "--legacy" in sys.argv else 1)
 N = 1 << 22
 m = datasets.inference_model(model_seed=11)
 bank = tmb.DenseClauseBank(tmb.Config(n_literals=4096, n_clauses=10000, n_classes=10, s=2.0,
@@ -38,8 +39,11 @@ torch.cuda.synchronize()
 _lib.call("tmb_set_option", b"infer.phase_buffer", 0)
 clk = torch.cuda.get_device_properties(0).clock_rate * 1e3
 p = ph.cpu().numpy().reshape(148, 8).astype(float) / clk * 1e6
-tiles = (N // 128) / (148 // 4)
-names = ["prefetch", "zero+sync+eval", "sync", "transpose", "publish", "cluster.sync",
-         "await", "finalize+loop"]
+tiles = (N // 128) / 33
+ws = "--legacy" not in sys.argv
+names = (["T: wait empty", "T: load+transpose", "T: publish", "T: loop", "E: wait full",
+          "E: eval", "E: push", "E: finalize+loop"] if ws else
+         ["prefetch", "zero+sync+eval", "sync", "transpose", "publish", "cluster.sync",
+          "await", "finalize+loop"])
 for q in range(8):
     print(f"  {names[q]:16s} {p[:, q].mean() / tiles:7.3f} us/tile (max CTA {p[:, q].max() / tiles:7.3f})")
