@@ -697,25 +697,22 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
     if (warp < kWsT) {
         // ================= transposer group =================
         // Each warp owns units u = warp + kWsT*q (q < nq) of every tile
-        // (unit = 32 examples x 128 features).  The loads of the next unit
-        // (possibly of the next tile) are issued before the current unit is
-        // transposed, so HBM latency overlaps the bit work.
+        // (unit = 32 examples x 128 features; lane (j, c16) loads 16 feature
+        // bytes of 8 example rows).  The loads of the next unit (possibly of
+        // the next tile) are issued before the current unit is transposed,
+        // so HBM latency overlaps the bit work.
         const int j = lane >> 3, c16 = lane & 7;
         const int units = nblk * kTG;
         const int nq = units > warp ? (units - warp + kWsT - 1) / kWsT : 0;
-        const int64_t total = n_my * (int64_t)nq;
+        const int g = warp % kTG;  // every unit of this warp has group warp % 4
+        const int64_t fb0 = qf0 + (int64_t)(warp / kTG) * 128 + 16 * c16;
         const uint32_t psel = (uint32_t)(j | ((1 ^ j) << 4) | ((2 ^ j) << 8) | ((3 ^ j) << 12));
-        auto load_item = [&](int64_t sidx, uint4 (&w)[8], int64_t &fb_out, int &g_out) {
-            const int64_t itx = sidx / nq;
-            const int u = warp + kWsT * (int)(sidx - itx * nq);
-            const int64_t e0 = (cid + itx * n_clusters) * tile_n;
-            const int g = u % kTG;
-            const int64_t fb = qf0 + (int64_t)(u / kTG) * 128 + 16 * c16;
-            fb_out = fb;
-            g_out = g;
-            const int64_t er = e0 + 32 * g + 8 * j;  // first of my 8 rows
+        const bool do_t = !(k.dbg & 2);
+        // item (tile itx, unit q): my 8 rows x 16 bytes
+        auto load_item = [&](int64_t itx, int q, uint4 (&w)[8]) {
+            const int64_t er = (cid + itx * n_clusters) * tile_n + 32 * g + 8 * j;
+            const int64_t fb = fb0 + (int64_t)q * (kWsT / kTG) * 128;
             if (k.vec_ok && fb + 16 <= qf1 && er + 7 < k.N) {
-                // common case: 8 unconditional 16-byte streaming loads
                 const uint8_t *src = k.x + er * F + fb;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) w[i] = __ldcs(reinterpret_cast<const uint4 *>(src + i * F));
@@ -727,51 +724,37 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 w[i] = make_uint4(0, 0, 0, 0);
                 if (e < k.N && fb < qf1) {
                     const uint8_t *src = k.x + e * F + fb;
-                    if (k.vec_ok && fb + 16 <= F) {
-                        w[i] = __ldcs(reinterpret_cast<const uint4 *>(src));
-                    } else {
-                        uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
-                        for (int bb = 0; bb < 16; ++bb) {
-                            if (fb + bb >= F) break;
-                            const uint32_t byte = (uint32_t)src[bb] << (8 * (bb & 3));
-                            if (bb < 4) b0 |= byte;
-                            else if (bb < 8) b1 |= byte;
-                            else if (bb < 12) b2 |= byte;
-                            else b3 |= byte;
-                        }
-                        w[i] = make_uint4(b0, b1, b2, b3);
-                    }
+                    uint32_t bw[4] = {0, 0, 0, 0};
+                    for (int bb = 0; bb < 16 && fb + bb < F; ++bb)
+                        bw[bb >> 2] |= (uint32_t)src[bb] << (8 * (bb & 3));
+                    w[i] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
                 }
             }
         };
-        // 0/1 bytes -> bits (bit t = byte t); bytes > 1 are flagged as bad
-        // input and abort the call, so no masking here
-        auto pk = [](uint32_t x) -> uint32_t { return (x * 0x01020408u) >> 24; };
-        auto finish_item = [&](const uint4 (&w)[8], int64_t fb, int g, uint32_t *mine) {
-            uint32_t v[8];
-            uint32_t ob = 0;
+        auto finish_item = [&](const uint4 (&w)[8], int q, uint32_t *mine) {
+            const int64_t fb = fb0 + (int64_t)q * (kWsT / kTG) * 128;
+            // bytes are 0/1 (anything else is flagged and aborts the call),
+            // so OR-ing row i shifted by i builds, in byte b of R_d, the 8
+            // row bits of feature 4d + b: the byte -> bit transpose is 7
+            // shift-adds per word
+            uint32_t R[4], ob = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                ob |= w[i].x | w[i].y | w[i].z | w[i].w;
-                v[i] = pk(w[i].x) | (pk(w[i].y) << 4) | (pk(w[i].z) << 8) | (pk(w[i].w) << 12);
+            for (int d = 0; d < 4; ++d) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t x = d == 0 ? w[i].x : d == 1 ? w[i].y : d == 2 ? w[i].z : w[i].w;
+                    ob |= x;
+                    acc |= x << i;
+                }
+                R[d] = acc;
             }
             bad |= ob & 0xFEFEFEFEu;
-            // byte i of lo / hi = bits 0-7 / 8-15 of v[i]
-            const uint32_t x01 = __byte_perm(v[0], v[1], 0x5140), x23 = __byte_perm(v[2], v[3], 0x5140);
-            const uint32_t x45 = __byte_perm(v[4], v[5], 0x5140), x67 = __byte_perm(v[6], v[7], 0x5140);
-            unsigned long long lo = (unsigned long long)__byte_perm(x01, x23, 0x5410) |
-                                    ((unsigned long long)__byte_perm(x45, x67, 0x5410) << 32);
-            unsigned long long hi = (unsigned long long)__byte_perm(x01, x23, 0x7632) |
-                                    ((unsigned long long)__byte_perm(x45, x67, 0x7632) << 32);
-            lo = transpose8x8(lo);
-            hi = transpose8x8(hi);
-            const uint32_t R0 = (uint32_t)lo, R1 = (uint32_t)(lo >> 32);
-            const uint32_t R2 = (uint32_t)hi, R3 = (uint32_t)(hi >> 32);
             uint32_t recv[4];
 #pragma unroll
             for (int sft = 0; sft < 4; ++sft) {
-                const int d = j ^ sft;
-                const uint32_t send = d == 0 ? R0 : d == 1 ? R1 : d == 2 ? R2 : R3;
+                const int dd = j ^ sft;
+                const uint32_t send = dd == 0 ? R[0] : dd == 1 ? R[1] : dd == 2 ? R[2] : R[3];
                 recv[sft] = sft ? __shfl_xor_sync(0xffffffffu, send, 8 * sft) : send;
             }
             // 4x4 byte transpose (word kq gathers byte kq of recv[0..3]),
@@ -796,49 +779,16 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 if (f < qf1) mine[(size_t)f * kTG + g] = word;
             }
         };
-        uint4 wa[8], wb[8];
-        int64_t fa = 0, fbx = 0;
-        int ga = 0, gbx = 0;
-        const bool do_t = !(k.dbg & 2);
-        // L2 prefetch of this CTA's quarter of tile `itx`'s rows (TMA bulk
-        // prefetch, one per example row; no registers, no shared memory)
-        const unsigned pf_bytes = (unsigned)((qf1 - qf0) & ~15LL);
-        auto prefetch_tile = [&](int64_t itx) {
-            if (itx >= n_my || !k.vec_ok || !pf_bytes) return;
-            const int64_t e0 = (cid + itx * n_clusters) * tile_n;
-            for (int i = tid; i < tile_n; i += 32 * kWsT) {
-                const int64_t e = e0 + i;
-                if (e < k.N)
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(k.x + e * F + qf0),
-                                 "r"(pf_bytes) : "memory");
-            }
-        };
-        if (do_t && (k.dbg & 8)) {  // opt-in: measured no gain
-            prefetch_tile(0);
-            prefetch_tile(1);
-        }
-        if (do_t && total > 0) load_item(0, wa, fa, ga);
-        for (int64_t it = 0; it < n_my; ++it) {
-            const int buf = (int)(it & 1);
-            uint32_t *mine = buf ? xt1 : xt0;
-            if (do_t && (k.dbg & 8)) prefetch_tile(it + 2);
+        auto tile_begin = [&](int64_t it) {
             WPH(3);
             // empty[] arrivals publish nothing: a CTA-scope wait (a cluster-
             // scope acquire would invalidate L1 on every tile)
-            if (it >= 2) mbar_wait(&empty[buf], (uint32_t)(((it >> 1) + 1) & 1));
+            if (it >= 2) mbar_wait(&empty[it & 1], (uint32_t)(((it >> 1) + 1) & 1));
             WPH(0);
-            if (do_t) {
-                for (int q = 0; q < nq; ++q) {
-                    const int64_t sidx = it * nq + q;
-                    if ((sidx & 1) == 0) {
-                        if (sidx + 1 < total) load_item(sidx + 1, wb, fbx, gbx);
-                        finish_item(wa, fa, ga, mine);
-                    } else {
-                        if (sidx + 1 < total) load_item(sidx + 1, wa, fa, ga);
-                        finish_item(wb, fbx, gbx, mine);
-                    }
-                }
-            }
+        };
+        auto tile_end = [&](int64_t it) {
+            const int buf = (int)(it & 1);
+            uint32_t *mine = buf ? xt1 : xt0;
             WPH(1);
             named_sync(1, 32 * kWsT);
             if (tid == 0) {
@@ -857,6 +807,40 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 else mbar_arrive_local(&full[buf]);
             }
             WPH(2);
+        };
+        if (!do_t || nq == 0) {
+            for (int64_t it = 0; it < n_my; ++it) {
+                tile_begin(it);
+                tile_end(it);
+            }
+        } else {
+            // items in order (it, q); A / B alternate, the next item's loads
+            // go out before the current item is transposed
+            uint4 wa[8], wb[8];
+            int64_t ia = 0, ib = 0;
+            int qa = 0, qb = 0;
+            auto next_of = [&](int64_t itx, int q, int64_t &itn, int &qn) {
+                qn = q + 1;
+                itn = itx;
+                if (qn == nq) {
+                    qn = 0;
+                    ++itn;
+                }
+            };
+            if (n_my > 0) load_item(0, 0, wa);
+            while (ia < n_my) {
+                next_of(ia, qa, ib, qb);
+                if (ib < n_my) load_item(ib, qb, wb);
+                if (qa == 0) tile_begin(ia);
+                finish_item(wa, qa, (ia & 1) ? xt1 : xt0);
+                if (qa == nq - 1) tile_end(ia);
+                if (ib >= n_my) break;
+                next_of(ib, qb, ia, qa);
+                if (ia < n_my) load_item(ia, qa, wa);
+                if (qb == 0) tile_begin(ib);
+                finish_item(wb, qb, (ib & 1) ? xt1 : xt0);
+                if (qb == nq - 1) tile_end(ib);
+            }
         }
     } else if (warp == nwarps - 1) {
         // ================= finalizer warp =================
