@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
             const int buf = (int)(it & 1);
             const uint32_t *xt = buf ? xt1 : xt0;
             int32_t *dirty = dirty2 + buf * kTG;
-            WPH(7);
+            WPH(6);
             // the peers' quarters arrive by bulk copy (complete_tx), so the
             // phase completion makes them visible: CTA-scope wait
             mbar_wait(&full[buf], (uint32_t)((it >> 1) & 1));
@@ -967,7 +967,9 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
             if (etid < kCS) mbar_arrive_remote_relaxed(mapa_u32(smem_u32(&empty[buf]), etid));
             // push the partial sums of example block b to owner b's inbox
             // slot `buf` once the owners consumed slot `buf` of tile it-2
+            WPH(6);
             if (it >= 2) mbar_wait(&vempty[buf], (uint32_t)(((it >> 1) + 1) & 1));
+            WPH(7);
             const bool anyd = dirty[0] | dirty[1] | dirty[2] | dirty[3];
             for (int i = etid; anyd && i < 32 * kTG * K; i += 32 * nE) {
                 const int b = i / (32 * K);
