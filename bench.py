@@ -43,6 +43,29 @@ HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
 HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the newest
+    committed `ncu --set full` summary under profiles/ (captured on the same
+    workload by tools/profile_round.sh), with its source; (None, None) if
+    absent."""
+    import glob
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    for f in sorted(glob.glob(os.path.join(REPO, "profiles", "*_ncu_full_summary.json")),
+                    reverse=True):
+        try:
+            data = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        for rec in data.values():
+            if kernel in rec.get("Kernel Name", ""):
+                tot = 0.0
+                for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    val, unit = rec[key].split()
+                    tot += float(val) * units[unit]
+                return tot, os.path.basename(f)
+    return None, None
+
+
 # ---------------------------------------------------------------- infra --
 
 def dist_init():
@@ -283,6 +306,7 @@ def bench_c2_train(args, rank, world, local):
     int_ops_ex = draws_per_ex * 30 + C * W * 3
     int_peak = sm_count * 128 * f_sm  # ALU + FMA pipes, 64 lanes/clk each
     int_achieved = int_ops_ex * ex_per_launch / (per_launch_ms / 1e3)
+    tr_train, tr_train_src = ncu_traffic("k_train_fast")
     # latency floor of sequential online training: one grid-wide all-reduce
     # per example, measured live by the same relaxed-atomic scheme in isolation
     import ctypes as ct
@@ -308,10 +332,15 @@ def bench_c2_train(args, rank, world, local):
         "work": {"events_per_example": ev_per_ex, "draws_per_example": draws_per_ex,
                  "type_i_per_example": dstats["type_i"] / max(dstats["examples"], 1),
                  "state_updates_per_example": dstats["state_updates"] / max(dstats["examples"], 1)},
-        "roofline": {"kernel": "k_step_records + k_train_fast (fused persistent trainer)",
+        "roofline": {"kernel": "k_train_fast (fused persistent trainer)",
                      "bound": "hbm",
                      "achieved": achieved_gbs, "peak": HBM_PEAK, "unit": "GB/s",
-                     "frac": achieved_gbs / HBM_PEAK, "traffic": None,
+                     "frac": achieved_gbs / HBM_PEAK, "traffic": tr_train,
+                     "traffic_source": tr_train_src,
+                     "traffic_note": "ncu DRAM bytes of one k_train_fast launch (one epoch): "
+                                     "the per-step records (literal row + bucketed 16-bit "
+                                     "flag keys, ~17 KB/step) read once from HBM, then "
+                                     "L2 hits for the other 147 CTAs",
                      "peak_source": HBM_PEAK_SRC,
                      "algorithmic_bytes_per_example": hbm_bytes_ex,
                      "avg_launch_ms": per_launch_ms,
@@ -443,6 +472,9 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
         _lib.call("tmbh_infer", model._h, ct_ptr(xh), n_e2e, None, np_ptr(ph), 1 << 18)
     e2e_s = max_over_ranks(time.perf_counter() - t, world)
     e2e_value = n_e2e * world * args.steps / e2e_s
+    tr_inf, tr_inf_src = ncu_traffic("k_infer_ws")
+    if tr_inf is not None:
+        tr_inf *= (N_total / world) / (1 << 22)  # captured on the 2^22-example launch
     out = {
         "metric": "inference examples/sec (configs[2] batched CoTM inference)",
         "value": value, "unit": "examples/s", "n_gpus": world, "steps": args.steps,
@@ -453,9 +485,11 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
                    "rules": model.n_rules, "l2": "inputs (17 GB) far larger than L2"},
         "gpu_launches": int(launches),
         "parity_sample_1024": parity,
-        "roofline": {"kernel": "k_infer (bit-sliced rule evaluation)", "bound": "hbm",
+        "roofline": {"kernel": "k_infer_ws (warp-specialised bit-sliced rule evaluation)",
+                     "bound": "hbm",
                      "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
-                     "frac": achieved / HBM_PEAK, "traffic": None, "peak_source": HBM_PEAK_SRC,
+                     "frac": achieved / HBM_PEAK, "traffic": tr_inf, "traffic_source": tr_inf_src,
+                     "peak_source": HBM_PEAK_SRC,
                      "algorithmic_bytes_per_example": bytes_ex, "avg_launch_ms": per_launch_ms},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "examples/s", "h2d_bytes_per_step": n_e2e * F,

@@ -1,2 +1,2 @@
-timeout 300 python -m pytest tests -m gpu -x -q -k "infer or predictor or dataset_votes or mnist_shaped_prefix or facade" 2>&1 | tail -3
-timeout 300 python tools/infer_split.py 2>&1 | tail -14
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 600 python bench.py > gpurun_out/bench_r01c.json 2> gpurun_out/bench_r01c.err; echo rc=$?
