@@ -9,7 +9,7 @@ also carries a "secondary" object for configs[2] (batched inference over
 2^22 examples, 10000 clauses x 20 includes, 4096 features).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--workload c2-train|c3-infer|c1-train]
+                  [--workload c2-train|c3-infer|c4-train|c5-sparse]
 
 N > 1 (torchrun, NCCL): training is sequential per example, so
 each rank trains an independent replica (different model seed) -- "replicas
@@ -519,6 +519,269 @@ def ct_ptr(t):
     return ct.c_void_p(t.data_ptr())
 
 
+
+# ------------------------------------------------------- c4 / c5 rows --
+
+def bench_c4_train(args, rank, world, local):
+    """configs[3]: bag-of-words CoTM training, 10^4 clauses x 2*10^4 literal
+    positions (states HBM-resident, 200 MB).  Step = 5000 consecutive
+    examples of the running epoch (a fifth of the 25000-example epoch)."""
+    import ctypes as ct
+
+    import torch
+
+    import paper_2405_04212_b200 as tmb
+    from paper_2405_04212_b200 import _lib, datasets
+    (tx, ty), _ = datasets.bag_of_words(data_seed=4 + rank)
+    cfg = tmb.Config(**datasets.bag_of_words_config_kwargs(seed=rank))
+    sess = tmb.DenseTrainSession(cfg, tx, ty)
+    step_n = 5000
+    order = torch.from_numpy(sess.next_order().astype(np.int32)).cuda()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    pos = 0
+    for _ in range(args.warmup):
+        sess.run_steps(order[pos:pos + step_n])
+        pos += step_n
+    torch.cuda.synchronize()
+    st0 = sess.states.cpu().numpy().copy()
+    w0 = sess.weights.cpu().numpy().copy()
+    c0 = sess.block_counters.cpu().numpy().copy()
+    fb0 = sess.fb_counter
+    stats0 = sess.stats_dict()
+    snap = sess.snapshot()
+    pos0 = pos
+    launches0 = _lib.launch_count()
+    barrier(world)
+    k_ms = []
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            flush_l2(flush)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sess.run_steps(order[pos:pos + step_n])
+            b.record(stream)
+            k_ms.append((a, b))
+            pos += step_n
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end), world)
+    launches = _lib.launch_count() - launches0
+    per_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in k_ms]))
+    st1 = sess.stats_dict()
+    d = {k: st1[k] - stats0[k] for k in st1}
+    n_ex = args.steps * step_n
+    value = n_ex * world / (elapsed_ms / 1e3)
+    P = cfg.n_literal_positions
+    # algorithmic HBM bytes: every Type I / II event reads and writes its
+    # clause's P int8 states (HBM-resident); plus the literal row
+    ev_ex = d["events"] / max(d["examples"], 1)
+    bytes_ex = ev_ex * 2 * P + 4 * ((P + 31) // 32) + 8
+    achieved = bytes_ex * step_n / (per_launch_ms / 1e3) / 1e9
+    draws_ex = d["draws"] / max(d["examples"], 1)
+    clocks = clk.summary()
+    f_sm = (clocks["sm_mhz"] or 1965.0) * 1e6
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    int_ops_ex = draws_ex * 22
+    int_peak = sm_count * 128 * f_sm
+    # e2e: the same slices from the same state through host buffers
+    sess.restore(snap)
+    from paper_2405_04212_b200.runtime import ptr, stream_ptr
+    xp = torch.from_numpy(np.ascontiguousarray(tx)).pin_memory()
+    st_host = torch.empty(sess.states.shape, dtype=torch.int8).pin_memory()
+    w_host = torch.empty(sess.weights.shape, dtype=torch.int32).pin_memory()
+    ordh = order.cpu().pin_memory()
+    barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    pos = pos0
+    for i in range(args.steps):
+        xd = xp.to("cuda", non_blocking=True)
+        _lib.call("tmb_pack_literals", ptr(xd), xp.shape[0], cfg.n_literals, 1,
+                  ptr(sess.lit_words), stream_ptr())
+        od = ordh[pos:pos + step_n].to("cuda", non_blocking=True)
+        sess.run_steps(od)
+        st_host.copy_(sess.states, non_blocking=True)
+        w_host.copy_(sess.weights, non_blocking=True)
+        pos += step_n
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    line = {
+        "metric": "train examples/sec (configs[3] bag-of-words CoTM training)",
+        "value": value, "unit": "examples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int8 TA states (HBM) / int32 weights / u64 SplitMix64",
+        "data": "synthetic (datasets.bag_of_words: Zipf(1.1) documents, planted sets)",
+        "config": {"workload": "configs[3]: bag-of-words training, 10000 clauses x 20000 literal "
+                               "positions, step = 5000 consecutive examples of the epoch",
+                   "launch": sess.launch, "parallelism": f"replicas x{world}",
+                   "l2": "256 MiB buffer written before every timed step"},
+        "gpu_launches": int(launches),
+        "work": {"events_per_example": ev_ex, "draws_per_example": draws_ex},
+        "roofline": {"kernel": "k_train<1, false> (grid mode, HBM-resident states)",
+                     "bound": "hbm", "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
+                     "frac": achieved / HBM_PEAK, "traffic": None, "peak_source": HBM_PEAK_SRC,
+                     "algorithmic_bytes_per_example": bytes_ex,
+                     "avg_launch_ms": per_launch_ms},
+        "roofline_int": {"bound": "int (ALU+FMA issue)",
+                         "achieved": int_ops_ex * step_n / (per_launch_ms / 1e3) / 1e12,
+                         "peak": int_peak / 1e12, "unit": "Tops/s",
+                         "frac": int_ops_ex * step_n / (per_launch_ms / 1e3) / int_peak,
+                         "ops_per_example": int_ops_ex},
+        "clocks": clocks,
+        "e2e": {"value": n_ex * world / (e2e_ms / 1e3), "unit": "examples/s",
+                "h2d_bytes_per_step": int(tx.nbytes + 4 * step_n),
+                "d2h_bytes_per_step": int(sess.states.numel() + 4 * sess.weights.numel()),
+                "path": "pinned host features -> H2D -> tmb_pack_literals -> tmb_trainer_run "
+                        "-> D2H model"},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle
+        x_lit = oracle.augment_literals(tx)
+        rate, n_done, dt = oracle_train_rate(cfg, st0, w0, c0, fb0, x_lit, ty,
+                                             order[pos0:pos0 + step_n].cpu().numpy().astype(np.int64),
+                                             args.cpu_seconds)
+        model_name, ncpu = host_desc()
+        line["cpu_baseline"] = {"value": rate, "unit": "examples/s", "cores": 1, "kind": "port",
+                                "sample": f"oracle C port of executor.train, {n_done} examples of "
+                                          f"the first timed step from the same model state "
+                                          f"({dt:.1f}s, 1 thread)",
+                                "host": model_name, "host_cores": ncpu}
+    return line
+
+
+def bench_c5_sparse(args, rank, world, local):
+    """configs[4]: SparseTM on 10^6 Zipf documents (10^6-literal vocabulary,
+    2000 clauses, capacity 64).  Headline = training documents/s, step =
+    100000 consecutive documents of the epoch; secondary = inverted-index
+    inference over all 10^6 documents per step."""
+    import torch
+
+    import paper_2405_04212_b200 as tmb
+    from paper_2405_04212_b200 import _lib, datasets, sparse_train
+    d = datasets.sparse_zipf(data_seed=5 + rank)
+    cfg = tmb.Config(**datasets.sparse_config_kwargs(seed=rank))
+    sess = sparse_train.SparseTrainSession(cfg, d.indptr, d.indices, d.labels)
+    step_n = 100_000
+    from paper_2405_04212_b200.executor import shuffle_permutation
+    order = torch.from_numpy(shuffle_permutation(sess.N, sess.shuffle_rng).astype(np.int32)).cuda()
+    stream = torch.cuda.current_stream()
+    pos = 0
+    for _ in range(args.warmup):
+        sess.run_steps(order[pos:pos + step_n])
+        pos += step_n
+    torch.cuda.synchronize()
+    stats0 = sess.stats_dict()
+    launches0 = _lib.launch_count()
+    barrier(world)
+    with ClockSampler(local) as clk:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(args.steps):
+            sess.run_steps(order[pos:pos + step_n])
+            pos += step_n
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    t_ms = max_over_ranks(a.elapsed_time(b), world)
+    st1 = sess.stats_dict()
+    dd = {k: st1[k] - stats0[k] for k in st1}
+    n_docs = args.steps * step_n
+    value = n_docs * world / (t_ms / 1e3)
+    nnz = 100
+    csr_bytes = 4 * nnz + 8
+    ev_doc = dd["events"] / max(dd["examples"], 1)
+    # inference over all documents (the trained model)
+    eng = sess.engine
+    for _ in range(2):
+        eng.votes_and_pred(sess.indptr, sess.indices, sess.N)
+    torch.cuda.synchronize()
+    ia = torch.cuda.Event(enable_timing=True)
+    ib = torch.cuda.Event(enable_timing=True)
+    ia.record(stream)
+    for _ in range(args.steps):
+        votes, pred = eng.votes_and_pred(sess.indptr, sess.indices, sess.N)
+    ib.record(stream)
+    torch.cuda.synchronize()
+    inf_ms = ia.elapsed_time(ib)
+    inf_value = sess.N * args.steps / (inf_ms / 1e3)
+    acc = float((pred.cpu().numpy() == d.labels).mean())
+    # e2e inference: host CSR -> device -> infer -> host predictions
+    ip_h = torch.from_numpy(d.indptr).pin_memory()
+    ix_h = torch.from_numpy(d.indices).pin_memory()
+    pr_h = torch.empty(sess.N, dtype=torch.int64).pin_memory()
+    ea = torch.cuda.Event(enable_timing=True)
+    eb = torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    for _ in range(args.steps):
+        ipd = ip_h.to("cuda", non_blocking=True)
+        ixd = ix_h.to("cuda", non_blocking=True)
+        _, pd = eng.votes_and_pred(ipd, ixd, sess.N)
+        pr_h.copy_(pd, non_blocking=True)
+    eb.record(stream)
+    torch.cuda.synchronize()
+    e2e_inf = sess.N * args.steps / (ea.elapsed_time(eb) / 1e3)
+    launches = _lib.launch_count() - launches0
+    line = {
+        "metric": "SparseTM train documents/sec (configs[4])",
+        "value": value, "unit": "documents/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int32 literal ids / int8 states / u64 SplitMix64",
+        "data": "synthetic (datasets.sparse_zipf: 10^6 Zipf(1.05) documents x 100 ids)",
+        "config": {"workload": "configs[4]: SparseTM, 10^6-literal vocabulary, 2000 clauses, "
+                               "capacity 64; step = 100000 consecutive training documents",
+                   "parallelism": f"replicas x{world} (online training is sequential)"},
+        "gpu_launches": int(launches),
+        "work": {"events_per_document": ev_doc,
+                 "draws_per_document": dd["draws"] / max(dd["examples"], 1)},
+        "roofline": {"kernel": "k_sparse_train", "bound": "hbm",
+                     "achieved": csr_bytes * value / world / 1e9, "peak": HBM_PEAK,
+                     "unit": "GB/s", "frac": csr_bytes * value / world / 1e9 / HBM_PEAK,
+                     "traffic": None, "peak_source": HBM_PEAK_SRC,
+                     "algorithmic_bytes_per_example": csr_bytes,
+                     "note": "latency-bound sequential training (one all-reduce per document); "
+                             "clause lists are on chip, HBM carries the document's CSR row"},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_inf, "unit": "documents/s (inference)",
+                "h2d_bytes_per_step": int(d.indptr.nbytes + d.indices.nbytes),
+                "d2h_bytes_per_step": int(8 * sess.N),
+                "path": "pinned host CSR -> H2D -> tmb_sparse_infer -> host predictions"},
+        "secondary": {"metric": "SparseTM inference documents/sec (configs[4])",
+                      "value": inf_value, "unit": "documents/s",
+                      "ms_per_step": inf_ms / args.steps, "accuracy_after_train": acc,
+                      "roofline": {"kernel": "k_sparse_infer (inverted index)", "bound": "hbm",
+                                   "achieved": inf_value * (csr_bytes + 8) / 1e9,
+                                   "peak": HBM_PEAK, "unit": "GB/s",
+                                   "frac": inf_value * (csr_bytes + 8) / 1e9 / HBM_PEAK,
+                                   "traffic": None,
+                                   "algorithmic_bytes_per_example": csr_bytes + 8}},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle
+        model_name, ncpu = host_desc()
+        acts = [d.indices[d.indptr[i]:d.indptr[i + 1]].astype(np.int64) for i in range(200)]
+        t0 = time.perf_counter()
+        n_tr = 40
+        oracle.sparse_train(cfg, acts[:n_tr], d.labels[:n_tr], n_epochs=1)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": n_tr / dt, "unit": "documents/s", "cores": 1,
+                                "kind": "port",
+                                "sample": f"oracle C port of executor.train (sparse), the first "
+                                          f"{n_tr} documents of a 40-document dataset from the "
+                                          f"initial model ({dt:.1f}s, 1 thread)",
+                                "host": model_name, "host_cores": ncpu}
+    return line
+
 # -------------------------------------------------------- reference arm --
 
 def bench_reference(args, rank, world):
@@ -531,6 +794,7 @@ def bench_reference(args, rank, world):
 
     from paper_2405_04212_b200 import datasets
     model_name, ncpu = host_desc()
+    unit = "examples/s"
     if args.workload == "c3-infer":
         m = datasets.inference_model(model_seed=11)
         xs = datasets.inference_examples(3, 0, args.c3_cpu_examples)
@@ -545,6 +809,40 @@ def bench_reference(args, rank, world):
         metric = "inference examples/sec (configs[2] batched CoTM inference)"
         sample = f"{len(xs)}-example prefix per step, {ncpu} threads"
         cores = ncpu
+    elif args.workload == "c4-train":
+        (tx, ty), _ = datasets.bag_of_words(data_seed=4)
+        cfg = oracle.OracleCfg(**datasets.bag_of_words_config_kwargs(seed=0))
+        st = oracle.new_train_state(cfg)
+        x_lit = oracle.augment_literals(tx)
+        order, _ = oracle.shuffle_permutation(len(ty), oracle.derive_stream(0, 0xD157), 0)
+        rates, pos, per_step = [], 0, 8
+        for i in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            oracle.train_steps(cfg, st, x_lit, ty, order[pos:pos + per_step])
+            pos += per_step
+            if i >= args.warmup:
+                rates.append(per_step / (time.perf_counter() - t))
+        value = float(np.mean(rates))
+        metric = "train examples/sec (configs[3] bag-of-words CoTM training)"
+        sample = f"{per_step} consecutive examples of epoch 1 per step, 1 thread"
+        cores = 1
+    elif args.workload == "c5-sparse":
+        d = datasets.sparse_zipf(data_seed=5, n_docs=2000)
+        cfg = datasets.sparse_config_kwargs(seed=0)
+        acts = [d.indices[d.indptr[i]:d.indptr[i + 1]].astype(np.int64) for i in range(2000)]
+        rates, pos, per_step = [], 0, 10
+        for i in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            oracle.sparse_train(oracle.OracleCfg(**cfg), acts[pos:pos + per_step],
+                                d.labels[pos:pos + per_step], n_epochs=1)
+            pos += per_step
+            if i >= args.warmup:
+                rates.append(per_step / (time.perf_counter() - t))
+        value = float(np.mean(rates))
+        metric = "SparseTM train documents/sec (configs[4])"
+        sample = f"{per_step}-document slices trained from the initial model, 1 thread"
+        cores = 1
+        unit = "documents/s"
     else:
         (tx, ty), _ = c2_data(0)
         cfg = oracle.OracleCfg(**datasets.mnist_shaped_config_kwargs(seed=0))
@@ -564,14 +862,14 @@ def bench_reference(args, rank, world):
         sample = (f"{per_step} consecutive examples of epoch 1 per step (warm-up steps "
                   f"advance the model), 1 thread: training is sequential (n_blocks=1)")
         cores = 1
-    return {"metric": metric, "value": value, "unit": "examples/s", "n_gpus": world,
+    return {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "int8 / u64", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.workload},
-            "cpu_baseline": {"value": value, "unit": "examples/s", "cores": cores,
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores,
                              "kind": "port", "sample": sample, "host": model_name},
-            "e2e": {"value": value, "unit": "examples/s", "h2d_bytes_per_step": 0,
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
 
@@ -583,7 +881,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c2-train", choices=["c2-train", "c3-infer"])
+    ap.add_argument("--workload", default="c2-train",
+                    choices=["c2-train", "c3-infer", "c4-train", "c5-sparse"])
     ap.add_argument("--c3-examples", type=int, default=1 << 22)
     ap.add_argument("--c3-e2e-examples", type=int, default=1 << 20)
     ap.add_argument("--c3-cpu-examples", type=int, default=1 << 13)
@@ -613,6 +912,10 @@ def main():
                      "warmup": args.warmup, "dtype": "u8 features / int32 votes",
                      "data": "synthetic (counter-based Bernoulli(0.5) generator)"})
         line["scaling"] = "strong"
+    elif args.workload == "c4-train":
+        line = bench_c4_train(args, rank, world, local)
+    elif args.workload == "c5-sparse":
+        line = bench_c5_sparse(args, rank, world, local)
     else:
         line = bench_c2_train(args, rank, world, local)
     if rank == 0:
