@@ -641,6 +641,9 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
     uint64_t *mb = reinterpret_cast<uint64_t *>(
         reinterpret_cast<uintptr_t>(dirty2 + 2 * kTG + 3) & ~(uintptr_t)7);  // [8]
     uint64_t *full = mb, *empty = mb + 2, *vfull = mb + 4, *vempty = mb + 6;
+    uint64_t *efree = mb + 8, *epushed = mb + 10;  // local: evaluators -> finalizer warp
+    int32_t *pushf = reinterpret_cast<int32_t *>(mb + 12);  // [2] dirty-block masks
+    int32_t *ectr = pushf + 2;                             // [2] next rule chunk (dynamic)
 
     const int r0 = (int)((int64_t)rank * k.R / kCS), r1 = (int)((int64_t)(rank + 1) * k.R / kCS);
     const int rloc = r1 - r0;
@@ -653,6 +656,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
     for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
     if (tid < 2 * kTG) dirty2[tid] = 0;
     if (tid < 2 * kCS) iflag[tid] = 0;
+    if (tid < 2) ectr[tid] = 0;  // (mbarrier area is initialised below, before the cluster sync)
 
     const int64_t tile_n = 32 * kTG;
     const int64_t n_tiles = (k.N + tile_n - 1) / tile_n;
@@ -674,6 +678,10 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
         mbar_init(&vfull[1], kCS);
         mbar_init(&vempty[0], kCS);
         mbar_init(&vempty[1], kCS);
+        mbar_init(&efree[0], 1);
+        mbar_init(&efree[1], 1);
+        mbar_init(&epushed[0], 1);
+        mbar_init(&epushed[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cluster.sync();
@@ -849,7 +857,21 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
         for (int64_t it = 0; it < n_my; ++it) {
             const int64_t t = cid + it * n_clusters;
             const int buf = (int)(it & 1);
-            mbar_wait_cluster(&vfull[buf], (uint32_t)((it >> 1) & 1));
+            const uint32_t par = (uint32_t)((it >> 1) & 1);
+            // forward the evaluators' "buffer free" to the 4 transposer groups
+            mbar_wait(&efree[buf], par);
+            if (lane < kCS) mbar_arrive_remote_relaxed(mapa_u32(smem_u32(&empty[buf]), lane));
+            // forward "partials pushed" to the 4 owners; blocks that received
+            // partials need a releasing arrival (the pushes are the
+            // evaluators' DSMEM stores, observed here through epushed)
+            mbar_wait(&epushed[buf], par);
+            const int pm = pushf[buf];
+            if (lane < kCS) {
+                const uint32_t vb = mapa_u32(smem_u32(&vfull[buf]), lane);
+                if ((pm >> lane) & 1) mbar_arrive_remote(vb);
+                else mbar_arrive_remote_relaxed(vb);
+            }
+            mbar_wait_cluster(&vfull[buf], par);
             const int64_t e = t * tile_n + 32 * rank + lane;
             const bool any = iflag[buf * kCS + 0] | iflag[buf * kCS + 1] | iflag[buf * kCS + 2] |
                              iflag[buf * kCS + 3];
@@ -924,7 +946,11 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
             };
             // two rules per lane (rc*64 + lane and +32): two independent
             // shared-memory chains, early-exit vote every 4 codes
-            for (int rc = ew; rc * 64 < rloc && !(k.dbg & 1); rc += nE) {
+            // 64-rule chunks handed out dynamically: early exits make chunk
+            // costs uneven, and a static split left the evaluator barrier
+            // waiting ~0.7 us per tile for the slowest warp
+            for (int rc = ew;; ) {
+                if (rc * 64 >= rloc || (k.dbg & 1)) break;
                 const int rA = rc * 64 + lane, rB = rA + 32;
                 const uint32_t lA = rA < rloc ? 0xFFFFFFFFu : 0u, lB = rB < rloc ? 0xFFFFFFFFu : 0u;
                 uint32_t A0 = lA, A1 = lA, A2 = lA, A3 = lA, B0 = lB, B1 = lB, B2 = lB, B3 = lB;
@@ -959,12 +985,17 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 }
                 if ((A0 | A1 | A2 | A3) && rA < rloc) finish_rule(rA, A0, A1, A2, A3);
                 if ((B0 | B1 | B2 | B3) && rB < rloc) finish_rule(rB, B0, B1, B2, B3);
+                int nx = 0;
+                if (lane == 0) nx = nE + atomicAdd(&ectr[buf], 1);
+                rc = __shfl_sync(0xffffffffu, nx, 0);
             }
             named_sync(2, 32 * nE);
+            if (etid == 0) ectr[buf] = 0;  // next used by tile it+2
             WPH(5);
-            // buffer `buf` is free as far as this CTA is concerned: tell all
-            // four transposer groups (they refill it for tile it+2)
-            if (etid < kCS) mbar_arrive_remote_relaxed(mapa_u32(smem_u32(&empty[buf]), etid));
+            // buffer `buf` is free as far as this CTA is concerned; the
+            // finalizer warp forwards it to all four transposer groups (a
+            // remote arrival stalls the issuing warp ~0.7 us)
+            if (etid == 0) mbar_arrive_local(&efree[buf]);
             // push the partial sums of example block b to owner b's inbox
             // slot `buf` once the owners consumed slot `buf` of tile it-2
             WPH(6);
@@ -980,17 +1011,11 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 part[i] = 0;
             }
             if (etid < kCS && dirty[etid]) cluster.map_shared_rank(iflag, etid)[buf * kCS + rank] = 1;
+            if (etid == 0) pushf[buf] = dirty[0] | (dirty[1] << 1) | (dirty[2] << 2) | (dirty[3] << 3);
             named_sync(2, 32 * nE);
-            if (etid < kCS) {
-                // owners zero their iflag slots after consuming them; only a
-                // block that received partials needs a releasing arrival
-                const uint32_t vb = mapa_u32(smem_u32(&vfull[buf]), etid);
-                if (dirty[etid]) mbar_arrive_remote(vb);
-                else mbar_arrive_remote_relaxed(vb);
-            }
-            __syncwarp();
+            if (etid == 0) mbar_arrive_local(&epushed[buf]);  // forwarded as vfull arrivals
             if (etid < kTG) dirty[etid] = 0;  // next used by tile it+2
-            WPH(6);
+            WPH(7);
         }
     }
     if (prof && tid == 0)
@@ -1080,7 +1105,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     const int64_t rloc_max = (r->R + kCS - 1) / kCS;
     const size_t smem = 32 * (size_t)rloc_max + 2 * 4 * (size_t)(r->F + 1) * kTG +
                         4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K +
-                        4 * (2 * kCS + 2 * kTG) + 96;
+                        4 * (2 * kCS + 2 * kTG) + 176;
     if (smem > (size_t)max_smem) return TMB_OK;  // generic kernel instead
     InferCK k;
     k.x = x; k.N = N; k.F = r->F; k.heads = r->heads; k.tail_ptr = r->tail_ptr; k.tails = r->tails;
@@ -1153,29 +1178,34 @@ static void balance_heads(const std::vector<int64_t> &ptr, const std::vector<uin
         for (int64_t c0 = s0; c0 < s1; c0 += 32) {
             const int64_t c1 = std::min<int64_t>(c0 + 32, s1);
             for (int q = 0; q < 16; ++q) {
-                int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                // rules with fewer remaining choices pick first
-                std::vector<int64_t> order;
-                for (int64_t i = c0; i < c1; ++i) order.push_back(i);
-                std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-                    return left[a].size() < left[b].size();
-                });
-                for (int64_t i : order) {
-                    auto &L = left[i];
-                    if (L.empty()) {  // padding code reads the all-ones row F
-                        cnt[(F) & 7]++;
-                        continue;
+                // a 16-byte shared load is served a quarter-warp (8 lanes) at a
+                // time: balance the bank quads within each 8-lane group
+                for (int64_t g0 = c0; g0 < c1; g0 += 8) {
+                    const int64_t g1 = std::min<int64_t>(g0 + 8, c1);
+                    int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    // rules with fewer remaining choices pick first
+                    std::vector<int64_t> order;
+                    for (int64_t i = g0; i < g1; ++i) order.push_back(i);
+                    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+                        return left[a].size() < left[b].size();
+                    });
+                    for (int64_t i : order) {
+                        auto &L = left[i];
+                        if (L.empty()) {  // padding code reads the all-ones row F
+                            cnt[(F) & 7]++;
+                            continue;
+                        }
+                        size_t best = 0;
+                        int bc = 1 << 30;
+                        for (size_t j = 0; j < L.size(); ++j) {
+                            const int qd = (int)((L[j] >> 1) & 7);
+                            if (cnt[qd] < bc) { bc = cnt[qd]; best = j; }
+                        }
+                        heads[(size_t)i * 16 + q] = (uint16_t)L[best];
+                        cnt[(L[best] >> 1) & 7]++;
+                        L[best] = L.back();
+                        L.pop_back();
                     }
-                    size_t best = 0;
-                    int bc = 1 << 30;
-                    for (size_t j = 0; j < L.size(); ++j) {
-                        const int qd = (int)((L[j] >> 1) & 7);
-                        if (cnt[qd] < bc) { bc = cnt[qd]; best = j; }
-                    }
-                    heads[(size_t)i * 16 + q] = (uint16_t)L[best];
-                    cnt[(L[best] >> 1) & 7]++;
-                    L[best] = L.back();
-                    L.pop_back();
                 }
             }
         }

@@ -42,7 +42,7 @@ p = ph.cpu().numpy().reshape(148, 8).astype(float) / clk * 1e6
 tiles = (N // 128) / 33
 ws = "--legacy" not in sys.argv
 names = (["T: wait empty", "T: load+transpose", "T: publish", "T: loop", "E: wait full",
-          "E: eval", "E: sync/arrive/push", "E: wait vempty"] if ws else
+          "E: eval+sync", "E: arrive empty", "E: vempty+push+vfull"] if ws else
          ["prefetch", "zero+sync+eval", "sync", "transpose", "publish", "cluster.sync",
           "await", "finalize+loop"])
 for q in range(8):
