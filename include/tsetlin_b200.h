@@ -178,8 +178,8 @@ int tmb_trainer_set_trace(tmb_trainer *t, int64_t *trace);
  * prefetch, all-reduce wait + decision, flag bitmaps, scan + events,
  * per-position feedback.  Grid mode also appends a timeline: %globaltimer
  * (ns) of thread 0 of every CTA at vote arrival, all-reduce detection and
- * step end for steps 64..127 of each launch, [64][n_cta][3] after the
- * [n_cta * 8] phases (size the buffer n_cta * (8 + 192)). */
+ * step end for steps 64..1087 of each launch, [1024][n_cta][3] after the
+ * [n_cta * 8] phases (size the buffer n_cta * (8 + 3072)). */
 int tmb_trainer_set_profile(tmb_trainer *t, uint64_t *phase);
 /* Launch configuration actually used (for reporting). */
 int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_bytes,

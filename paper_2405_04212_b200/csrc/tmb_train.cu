@@ -512,8 +512,9 @@ __device__ __forceinline__ void cluster_wait() {
     } while (0)
 
 // Grid-mode timeline (profiling): %globaltimer of thread 0 at arrival,
-// all-reduce detection and step end for steps [64, 128), stored after the
-// phase array as [64][n_cta][3].
+// all-reduce detection and step end for steps [64, 64 + kTimelineSteps),
+// stored after the phase array as [kTimelineSteps][n_cta][3].
+constexpr int kTimelineSteps = 1024;
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -521,7 +522,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define TIMELINE(i, q)                                                              \
     do {                                                                            \
-        if (prof && warp == 0 && (i) >= 64 && (i) < 128) {                          \
+        if (prof && warp == 0 && (i) >= 64 && (i) < 64 + kTimelineSteps) {                          \
             const unsigned long long g_ = gtimer();                                 \
             if (lane == 0) k.phase[n_cta * 8 + (((i) - 64) * n_cta + rank) * 3 + (q)] = g_; \
         }                                                                           \

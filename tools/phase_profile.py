@@ -39,7 +39,7 @@ for n_cta in args.cta:
     for _ in range(args.epochs - 1):
         sess.run_epoch()
     nc = sess.launch["n_cta"]
-    ph = torch.zeros(nc * (8 + 192), dtype=torch.int64, device="cuda")
+    ph = torch.zeros(nc * (8 + 3072), dtype=torch.int64, device="cuda")
     _lib.call("tmb_trainer_set_profile", sess._h, ptr(ph))
     _lib.call("tmb_set_option", b"train.debug_skip", args.skip)
     trace = torch.zeros(len(ty) * 4, dtype=torch.int64, device="cuda")
@@ -52,7 +52,7 @@ for n_cta in args.cta:
     torch.cuda.synchronize()
     _lib.call("tmb_set_option", b"train.debug_skip", 0)
     ms = st.elapsed_time(en)
-    tl = ph.cpu().numpy()[nc * 8:].reshape(64, nc, 3).astype(np.float64)
+    tl = ph.cpu().numpy()[nc * 8:].reshape(1024, nc, 3).astype(np.float64)
     p = ph.cpu().numpy()[:nc * 8].reshape(-1, 8).astype(np.float64) / clk_hz * 1e6 / len(ty)
     print(f"n_cta={sess.launch['n_cta']} threads={sess.launch['threads']} "
           f"smem_states={sess.launch['states_in_smem']}: {ms * 1e3 / len(ty):.2f} us/example "
@@ -67,7 +67,7 @@ for n_cta in args.cta:
         skew = last - tl[:, :, 0]           # own arrival before the last one
         step = np.diff(tl[:, :, 2].max(axis=1))
         who = np.argmax(tl[:, :, 0], axis=1)
-        print(f"   timeline (ns, steps 64..127): step {np.median(step):.0f} median; "
+        print(f"   timeline (ns, steps 64..1087): step {np.median(step):.0f} median; "
               f"detect-after-last-arrival mean {det.mean():.0f} min {det.min():.0f} "
               f"max {det.max():.0f}; arrival skew mean {skew.mean():.0f} "
               f"max {skew.max():.0f}; last arriver CTAs {np.bincount(who, minlength=nc).argsort()[-5:]}")
@@ -90,11 +90,21 @@ for n_cta in args.cta:
         print("             median end minus median detect     ", q(E - D))
         print("             max end minus median end           ", q(EM - E))
         print("             next median arrival minus med. end ", q(A[1:] - E[:-1]))
-        evs = trace.cpu().numpy().reshape(-1, 4)[64:128, 3]
-        dur = np.diff(np.median(tl[:, :, 1], axis=1))  # detect-to-detect per step
-        ev_next = evs[:-1]
-        for name, m in (("empty", ev_next == 0), ("1-100 events", (ev_next > 0) & (ev_next <= 100)),
-                        (">100 events", ev_next > 100)):
-            if m.any():
-                print(f"   steps with {name:13s}: n={m.sum():3d} median detect-to-detect "
-                      f"{np.median(dur[m]):6.0f} ns mean {dur[m].mean():6.0f}")
+    evs = trace.cpu().numpy().reshape(-1, 4)[64:1088, 3]
+    dur = np.diff(np.median(tl[:, :, 1], axis=1))  # detect-to-detect per step
+    ev_next = evs[:-1]
+    for name, m in (("empty", ev_next == 0), ("1-100 events", (ev_next > 0) & (ev_next <= 100)),
+                    (">100 events", ev_next > 100)):
+        if m.any():
+            print(f"   steps with {name:13s}: n={m.sum():3d} median detect-to-detect "
+                  f"{np.median(dur[m]):6.0f} ns mean {dur[m].mean():6.0f}")
+    if tl[:, :, 0].min() > 0:
+        send, det = tl[:, :, 0], tl[:, :, 1]
+        sh = send[2:] - det[:-2]            # send of A(e) after detection of e-2 (per CTA)
+        q2 = lambda v: f"p10 {np.percentile(v, 10):6.0f} p50 {np.median(v):6.0f} p90 {np.percentile(v, 90):6.0f}"
+        e_empty = (evs[:-2] == 0) & (evs[1:-1] == 0)
+        print("   [empty pairs] send(A e) - det(e-2) per CTA:", q2(sh[e_empty].ravel()))
+        spread = send.max(axis=1) - np.median(send, axis=1)
+        lat = np.median(det, axis=1) - send.max(axis=1)
+        print("   [empty] send spread (max - median):", q2(spread[2:][e_empty]),
+              " det(med) - last send:", q2(lat[2:][e_empty]))
