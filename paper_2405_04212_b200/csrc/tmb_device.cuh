@@ -79,6 +79,16 @@ __device__ __forceinline__ int type_ii(int st, int lit, int out) {
     return (out && !lit && st < 0) ? st + 1 : st;
 }
 
+// feedback.py:33-44: update probability (a / 2T, a in [0, 2T]) -> integer
+// threshold.  The saturated ends are common once the class sums reach T and
+// would take the division's slow path (zero numerator), so they are exact
+// constants here.
+__device__ __forceinline__ uint64_t threshold_of(long long a, long long T) {
+    if (a <= 0) return 0;
+    if (a >= 2 * T) return 1ull << 53;
+    return prob_threshold((double)a / (2.0 * (double)T));
+}
+
 // ---- partitions (executor.py:36-47): block of clause c, block start, CTA ranges
 __host__ __device__ __forceinline__ int block_of(int c, int C, int nb) {
     int base = C / nb, extra = C % nb;

@@ -28,6 +28,8 @@ namespace tmb {
 
 constexpr int kMaxActive = 4096;  // active literals of one document held in smem
 constexpr int kMaxIns = 512;      // Type II insertions per event (per-warp smem)
+constexpr int kStage = 1024;      // per-warp shared staging of a clause list (longer: global)
+constexpr int kPfRegs = 8;        // next document's active ids per thread (prefetch)
 
 struct SparseK {
     int C, K, n_blocks, n_cta, cmax, fmax_words, bmax, slab;
@@ -55,6 +57,7 @@ struct SparseK {
     const uint8_t *x_ut, *x_un, *x_out;
     int x_label, x_neg;
     uint64_t x_counter, x_seed;
+    unsigned long long *phase;  // optional [n_cta][8] clock64 per phase (thread 0; profiling)
 };
 
 __device__ __forceinline__ int32_t *lits_of(const SparseK &k, int c, int which) {
@@ -94,13 +97,35 @@ __device__ __forceinline__ int warp_excl(int f, int lane, int *tot) {
 // Type I on clause c (one warp): domain = stored U active, merged by a merge
 // path (stored first on ties; the active duplicate of a stored literal is
 // skipped).  Returns the new length in the other buffer, -1 on slab overflow.
+// Copy the clause's list into the warp's shared staging buffers (the merge
+// path's binary searches then hit shared memory, not L2); returns the
+// pointers to use.
+__device__ __forceinline__ void stage_list(const int32_t *L, const int8_t *S, int n, int32_t *sL,
+                                           int8_t *sS, int lane, const int32_t *&Lp,
+                                           const int8_t *&Sp) {
+    if (n <= kStage) {
+        for (int q = lane; q < n; q += 32) {
+            sL[q] = L[q];
+            sS[q] = S[q];
+        }
+        __syncwarp();
+        Lp = sL;
+        Sp = sS;
+    } else {
+        Lp = L;
+        Sp = S;
+    }
+}
+
 __device__ int event_type_i(const SparseK &k, int c, int src, const int32_t *act, int n_act,
-                            int out, uint64_t sk, int lane, uint64_t &ndraws) {
-    const int32_t *L = lits_of(k, c, src);
-    const int8_t *S = sts_of(k, c, src);
+                            int out, uint64_t sk, int lane, uint64_t &ndraws, int32_t *sL,
+                            int8_t *sS) {
     int32_t *DL = lits_of(k, c, src ^ 1);
     int8_t *DS = sts_of(k, c, src ^ 1);
     const int n = k.len[c];
+    const int32_t *L;
+    const int8_t *S;
+    stage_list(lits_of(k, c, src), sts_of(k, c, src), n, sL, sS, lane, L, S);
     const int total = n + n_act;
     int emitted = 0, cond_before = 0;
     for (int base = 0; base < total; base += 32) {
@@ -158,12 +183,13 @@ __device__ int event_type_i(const SparseK &k, int c, int src, const int32_t *act
 // up from above the floor); inserted = the first non-stored, non-active
 // candidates x with #stored(<x) + #inserted(<x) < capacity, at floor + 1.
 __device__ int event_type_ii(const SparseK &k, int c, int src, const int32_t *act, int n_act,
-                             int32_t *ins_buf, int lane) {
-    const int32_t *L = lits_of(k, c, src);
-    const int8_t *S = sts_of(k, c, src);
+                             int32_t *ins_buf, int lane, int32_t *sL, int8_t *sS) {
     int32_t *DL = lits_of(k, c, src ^ 1);
     int8_t *DS = sts_of(k, c, src ^ 1);
     const int n = k.len[c];
+    const int32_t *L;
+    const int8_t *S;
+    stage_list(lits_of(k, c, src), sts_of(k, c, src), n, sL, sS, lane, L, S);
     const int cap = k.capacity;
     int ins = 0;
     bool overflow = false;
@@ -212,7 +238,10 @@ __device__ int event_type_ii(const SparseK &k, int c, int src, const int32_t *ac
 }
 
 struct SSmem {
-    int32_t *act;       // [kMaxActive] current document
+    int32_t *act;       // [2][kMaxActive] current / next document
+    int32_t *stL;       // [nwarps][kStage] staged clause literals
+    int8_t *stS;        // [nwarps][kStage] staged clause states
+    int64_t *meta;      // [3][4] prefetched document: a0, a1, label, -
     int32_t *ins;       // [nwarps][kMaxIns]
     uint32_t *ut_bits, *un_bits;
     int32_t *word_cum, *info, *work, *misc;
@@ -231,7 +260,10 @@ __host__ __device__ inline size_t sparse_smem(const SparseK &k, int nwarps, char
         return p;
     };
     SSmem t;
-    t.act = (int32_t *)take(4 * kMaxActive);
+    t.act = (int32_t *)take(4 * 2 * kMaxActive);
+    t.stL = (int32_t *)take(4 * (size_t)kStage * nwarps);
+    t.stS = (int8_t *)take((size_t)kStage * nwarps);
+    t.meta = (int64_t *)take(8 * 12);
     t.ins = (int32_t *)take(4 * (size_t)kMaxIns * nwarps);
     t.ut_bits = (uint32_t *)take(4 * k.fmax_words);
     t.un_bits = (uint32_t *)take(4 * k.fmax_words);
@@ -275,25 +307,81 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
     __syncthreads();
     uint64_t n_draws = 0, n_events = 0, n_t1 = 0, n_t2 = 0;
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
+    const bool prof = k.phase != nullptr;
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long t_mark = clock64();
+#define SPH(n)                                                            \
+    do {                                                                  \
+        if (prof && tid == 0) {                                           \
+            const long long now = clock64();                              \
+            ph[n] += (unsigned long long)(now - t_mark);                  \
+            t_mark = now;                                                 \
+        }                                                                 \
+    } while (0)
+    // document pipeline: meta (range, label) two steps ahead, active ids one
+    // step ahead (registers, committed to act[(it+1)&1] at the step's end)
+    auto load_meta = [&](int64_t d, int slot) {
+        const int ex = explicit_flags ? 0 : __ldg(&k.order[d]);
+        s.meta[slot * 4 + 0] = __ldg(&k.indptr[ex]);
+        s.meta[slot * 4 + 1] = __ldg(&k.indptr[ex + 1]);
+        s.meta[slot * 4 + 2] = explicit_flags ? k.x_label : __ldg(&k.labels[ex]);
+    };
+    if (tid == 0) {
+        load_meta(0, 0);
+        if (k.n_steps > 1) load_meta(1, 1);
+        if (k.n_steps > 2) s.meta[2 * 4 + 3] = __ldg(&k.order[2]);  // example of step 2
+    }
+    __syncthreads();
+    {
+        const int64_t a0 = s.meta[0], a1 = s.meta[1];
+        const int n0 = (int)(a1 - a0 < kMaxActive ? a1 - a0 : kMaxActive);
+        for (int q = tid; q < n0; q += nthr) s.act[q] = __ldg(&k.indices[a0 + q]);
+    }
     for (int64_t it = 0; it < k.n_steps; ++it) {
-        const int ex = explicit_flags ? 0 : __ldg(&k.order[it]);
-        const int64_t a0 = __ldg(&k.indptr[ex]), a1 = __ldg(&k.indptr[ex + 1]);
+        const int cur = (int)(it & 1);
+        const int64_t a0 = s.meta[(it % 3) * 4 + 0], a1 = s.meta[(it % 3) * 4 + 1];
         const int n_act = (int)(a1 - a0 < kMaxActive ? a1 - a0 : kMaxActive);
         if (a1 - a0 > kMaxActive && tid == 0) atomicOr(k.overflow, 2u);
-        for (int q = tid; q < n_act; q += nthr) s.act[q] = __ldg(&k.indices[a0 + q]);
+        const int32_t *act = s.act + cur * kMaxActive;
+        // next document's ids into registers; meta of the one after
+        int32_t pf[kPfRegs];
+        int n_next = 0;
+        if (it + 1 < k.n_steps) {
+            const int64_t b0 = s.meta[((it + 1) % 3) * 4 + 0], b1 = s.meta[((it + 1) % 3) * 4 + 1];
+            n_next = (int)(b1 - b0 < kMaxActive ? b1 - b0 : kMaxActive);
+#pragma unroll
+            for (int r = 0; r < kPfRegs; ++r) {
+                const int q = tid + r * nthr;
+                if (q < n_next) pf[r] = __ldg(&k.indices[b0 + q]);
+            }
+        }
+        // three-stage meta pipeline, no dependent load inside a step: the
+        // example of step it+3, and the range / label of step it+2 (whose
+        // example index was fetched one step earlier)
+        int64_t nm0 = 0, nm1 = 0, nm2 = 0, nx3 = 0;
+        if (tid == nthr - 1) {
+            if (it + 2 < k.n_steps) {
+                const int ex2 = (int)s.meta[((it + 2) % 3) * 4 + 3];
+                nm0 = __ldg(&k.indptr[ex2]);
+                nm1 = __ldg(&k.indptr[ex2 + 1]);
+                nm2 = __ldg(&k.labels[ex2]);
+            }
+            if (it + 3 < k.n_steps) nx3 = __ldg(&k.order[it + 3]);
+        }
         const uint64_t fbc = k.fb_counter0 + (uint64_t)it * step_draws;
         int label, neg;
         if (explicit_flags) {
             label = k.x_label;
             neg = k.x_neg;
         } else {
-            label = __ldg(&k.labels[ex]);
+            label = (int)s.meta[(it % 3) * 4 + 2];
             const double u = u01_from53(draw53(k.fb_seed, fbc));
             neg = label + 1 + (int)(u * (double)(K - 1));
             if (neg >= K) neg -= K;
         }
         if (tid == 0) s.misc[0] = 0;
         __syncthreads();
+        SPH(0);
         // 1. training-mode outputs of own clauses (sparse.py:123-138), warp
         //    per clause: included = stored with state >= 0, all must be active
         for (int j = warp; j < cown; j += nwarps) {
@@ -311,7 +399,7 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                 for (int q = lane; q < n; q += 32) {
                     if (S[q] >= 0) {
                         ++n_inc;
-                        if (!contains(s.act, n_act, L[q])) viol = true;
+                        if (!contains(act, n_act, L[q])) viol = true;
                     }
                 }
                 n_inc = __reduce_add_sync(0xffffffffu, n_inc);
@@ -321,6 +409,7 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
             if (lane == 0) s.info[j] = outv ? SI_OUT : 0;
         }
         __syncthreads();
+        SPH(1);
         uint64_t t_t = 0, t_n = 0;
         if (!explicit_flags) {
             // 2. partial sums of the label / negative class, fence-free exchange
@@ -350,11 +439,12 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                 s.vsum[1] = (long long)(p.y & ((1ull << 40) - 1)) - bias;
             }
             __syncthreads();
+            SPH(2);
             const long long T = k.T, vl = s.vsum[0], vn = s.vsum[1];
             const long long cl = vl < -T ? -T : (vl > T ? T : vl);
             const long long cn2 = vn < -T ? -T : (vn > T ? T : vn);
-            t_t = prob_threshold((double)(T - cl) / (2.0 * (double)T));
-            t_n = prob_threshold((double)(T + cn2) / (2.0 * (double)T));
+            t_t = threshold_of(T - cl, T);
+            t_n = threshold_of(T + cn2, T);
         }
         // 3. update-flag bitmaps over [fs, fe)
         for (int idx = tid; idx < nfw * 32; idx += nthr) {
@@ -376,6 +466,7 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
             }
         }
         __syncthreads();
+        SPH(3);
         // 4. warp 0: event prefix, ordinals, types, weights, work list
         if (warp == 0) {
             int carry = 0;
@@ -445,6 +536,7 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
             }
         }
         __syncthreads();
+        SPH(4);
         // 5. events: warp per clause of the work list, target then negative
         const int n_work = s.misc[0];
         for (int wi = warp; wi < n_work; wi += nwarps) {
@@ -459,10 +551,12 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                 const bool t1 = ev == 0 ? (info & SI_T1) : (info & SI_N1);
                 int nl;
                 if (t1) {
-                    nl = event_type_i(k, c, src, s.act, n_act, out, ev == 0 ? s.sk_t[j] : s.sk_n[j],
-                                      lane, n_draws);
+                    nl = event_type_i(k, c, src, act, n_act, out, ev == 0 ? s.sk_t[j] : s.sk_n[j],
+                                      lane, n_draws, s.stL + (size_t)warp * kStage,
+                                      s.stS + (size_t)warp * kStage);
                 } else if (out) {
-                    nl = event_type_ii(k, c, src, s.act, n_act, s.ins + (size_t)warp * kMaxIns, lane);
+                    nl = event_type_ii(k, c, src, act, n_act, s.ins + (size_t)warp * kMaxIns, lane,
+                                       s.stL + (size_t)warp * kStage, s.stS + (size_t)warp * kStage);
                 } else {
                     continue;  // Type II on output 0: no-op (window still consumed)
                 }
@@ -479,8 +573,28 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                 __syncwarp();
             }
         }
+        // commit the prefetched document (read after the next step's first
+        // barrier)
+#pragma unroll
+        for (int r = 0; r < kPfRegs; ++r) {
+            const int q = tid + r * nthr;
+            if (q < n_next) s.act[(cur ^ 1) * kMaxActive + q] = pf[r];
+        }
+        if (tid == nthr - 1) {
+            if (it + 2 < k.n_steps) {
+                s.meta[((it + 2) % 3) * 4 + 0] = nm0;
+                s.meta[((it + 2) % 3) * 4 + 1] = nm1;
+                s.meta[((it + 2) % 3) * 4 + 2] = nm2;
+            }
+            // slot (it+3)%3 == it%3: this step's meta is no longer read
+            if (it + 3 < k.n_steps) s.meta[((it + 3) % 3) * 4 + 3] = nx3;
+        }
         __syncthreads();
+        SPH(5);
     }
+#undef SPH
+    if (prof && tid == 0)
+        for (int q = 0; q < 8; ++q) k.phase[rank * 8 + q] = ph[q];
     for (int bi = tid; bi <= b1 - b0; bi += nthr) {
         const int b = b0 + bi;
         const int last = block_begin(b + 1, C, k.n_blocks) - 1;
@@ -601,6 +715,8 @@ __global__ void __launch_bounds__(256) k_sparse_infer(SparseInferK k) {
     }
 }
 
+unsigned long long *g_sparse_phase = nullptr;  // tmb_set_option("sparse.phase_buffer")
+
 }  // namespace tmb
 
 using namespace tmb;
@@ -667,7 +783,9 @@ int sparse_fill_k(tmb_sparse *sp) {
     return TMB_OK;
 }
 
+
 int sparse_launch(tmb_sparse *sp, SparseK &k, cudaStream_t st) {
+    k.phase = g_sparse_phase;
     void *args[] = {&k};
     TMB_CUDA(cudaLaunchCooperativeKernel((const void *)k_sparse_train, dim3(sp->n_cta),
                                          dim3(sp->threads), args, sp->smem, st));

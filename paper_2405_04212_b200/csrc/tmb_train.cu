@@ -423,16 +423,6 @@ __device__ __forceinline__ void prologue_ring(const TrainK &k, const Smem &s) {
         s.lit0[w] = __ldg(&k.lit_words[(int64_t)ex * k.W + w]);
 }
 
-// feedback.py:33-44: update probability (a / 2T, a in [0, 2T]) -> integer
-// threshold.  The saturated ends are common once the class sums reach T and
-// would take the division's slow path (zero numerator), so they are exact
-// constants here.
-__device__ __forceinline__ uint64_t threshold_of(long long a, long long T) {
-    if (a <= 0) return 0;
-    if (a >= 2 * T) return 1ull << 53;
-    return prob_threshold((double)a / (2.0 * (double)T));
-}
-
 __device__ __forceinline__ void decide(const TrainK &k, long long vl, long long vn,
                                        uint64_t &t_t, uint64_t &t_n) {
     const long long T = k.T;

@@ -1,0 +1,29 @@
+"""Per-phase clock64 profile of the SparseTM trainer (configs[4] shapes)."""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import paper_2405_04212_b200 as tmb  # noqa: E402
+from paper_2405_04212_b200 import _lib, datasets, sparse_train  # noqa: E402
+n_docs = int(sys.argv[1]) if len(sys.argv) > 1 else 200000
+d = datasets.sparse_zipf(n_docs=n_docs)
+cfg = tmb.Config(**datasets.sparse_config_kwargs(seed=0))
+sess = sparse_train.SparseTrainSession(cfg, d.indptr, d.indices, d.labels)
+sess.run_epoch(max_steps=50000)
+torch.cuda.synchronize()
+nc = 148
+ph = torch.zeros(nc * 8, dtype=torch.int64, device="cuda")
+_lib.call("tmb_set_option", b"sparse.phase_buffer", ph.data_ptr())
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+n = 20000
+a.record()
+sess.run_epoch(max_steps=n)
+b.record()
+torch.cuda.synchronize()
+_lib.call("tmb_set_option", b"sparse.phase_buffer", 0)
+clk = torch.cuda.get_device_properties(0).clock_rate * 1e3
+p = ph.cpu().numpy().reshape(nc, 8).astype(float) / clk * 1e6 / n
+print(f"{a.elapsed_time(b) * 1e3 / n:.2f} us/doc")
+for q, name in enumerate(["loop top (act load, neg)", "eval", "votes+exchange", "flag bitmaps",
+                          "events (warp 0)", "feedback merges"]):
+    print(f"  {name:26s} mean {p[:, q].mean():7.3f}  max {p[:, q].max():7.3f} us/doc")
