@@ -257,14 +257,17 @@ def test_inference_random_models_vs_oracle(gpu, oracle, n_inc, F, K):
     assert np.array_equal(pred, op)
 
 
-@pytest.mark.parametrize("kernel", ["cluster", "generic"])
+@pytest.mark.parametrize("kernel", ["ws", "cluster", "generic"])
 @pytest.mark.parametrize("n_inc,F,K,C,N", [(40, 64, 3, 300, 1000), (17, 784, 10, 2001, 700),
                                            (1, 32, 32, 33, 129), (5, 1000, 2, 5000, 300)])
 def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C, N):
-    """Both inference kernels: rules longer than the 16-code heads (tails),
-    feature widths that are not multiples of 32, K up to 32, ragged tiles."""
+    """All three inference kernels (warp-specialised cluster, alternating
+    cluster, generic): rules longer than the 16-code heads (tails), feature
+    widths that are not multiples of 32, K up to 32, ragged tiles, and
+    firing blocks in many tiles (votes pushed across the cluster)."""
     from paper_2405_04212_b200 import _lib
     _lib.call("tmb_set_option", b"infer.force_generic", int(kernel == "generic"))
+    _lib.call("tmb_set_option", b"infer.warp_specialized", int(kernel == "ws"))
     try:
         rs = np.random.default_rng(n_inc + F + K)
         # satisfiable clauses: n_inc distinct features, random polarity
@@ -298,6 +301,7 @@ def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C,
         assert (ov != 0).any()
     finally:
         _lib.call("tmb_set_option", b"infer.force_generic", 0)
+        _lib.call("tmb_set_option", b"infer.warp_specialized", 1)
 
 
 def test_inference_ties_and_empty(gpu):
