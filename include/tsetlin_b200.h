@@ -217,6 +217,14 @@ int tmb_rules_info(const tmb_rules *r, int64_t *n_rules, int64_t *n_includes);
  * [N,K] and pred int64 [N] are optional (NULL); labels (device int64 [N]) +
  * correct (device uint64 [1], accumulated) optional.  Ties -> lowest class
  * (np.argmax, executor.py:382). */
+/* Batched predict_and_explain (predictor.py:99-124) on device buffers:
+ * x uint8 [N, F] raw features; pred int64 [N] (argmax, ties -> lowest);
+ * votes int64 [N, K] or NULL; scores int64 [N, P] or NULL (P = 2F with
+ * negations, else F): every firing rule adds its weight for the explained
+ * class (for_class >= 0, else the predicted class) to each literal position
+ * it includes.  Feature-level scores = scores[:, :F] - scores[:, F:]. */
+int tmb_explain(const tmb_rules *r, const uint8_t *x, int64_t N, int for_class, int64_t *votes,
+                int64_t *pred, int64_t *scores, void *stream);
 int tmb_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes,
               int64_t *pred, const int64_t *labels, uint64_t *correct, void *stream);
 /* Synchronises `stream` and reports TMB_E_INVALID if any tmb_infer call since

@@ -1031,6 +1031,89 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
     if (bad) atomicOr(k.bad_input, 1u);
 }
 
+
+// ---------------------------------------------------------------------------
+// Batched predict_and_explain (predictor.py:99-124): one warp per example.
+// Pass 1: lane per rule tests the includes against the example's feature
+// bytes (staged in shared memory), marks firing rules and adds their weights
+// to the class sums; argmax (ties -> lowest).  Pass 2: every firing rule adds
+// its weight for the explained class to each literal position it includes
+// (int64 atomics into the example's score row, zeroed first).
+struct ExplainK {
+    const uint8_t *x;
+    int64_t N, F;
+    const uint32_t *inc;
+    const int64_t *ptr;
+    const int32_t *w;
+    int R, K, negations, for_class;
+    int64_t *votes, *pred, *scores;
+};
+
+__global__ void __launch_bounds__(256) k_explain(ExplainK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t F = k.F, P = k.negations ? 2 * F : F;
+    const int fire_words = (k.R + 31) / 32;
+    // per warp: votes [K] int64 | fire bits [fire_words] | feature bytes [F]
+    const size_t per = 8 * (size_t)k.K + 4 * (size_t)fire_words + (size_t)((F + 15) & ~15LL);
+    char *mine = smem_raw + (size_t)wib * ((per + 15) & ~(size_t)15);
+    long long *sv = reinterpret_cast<long long *>(mine);
+    unsigned *fire = reinterpret_cast<unsigned *>(mine + 8 * (size_t)k.K);
+    uint8_t *xr = reinterpret_cast<uint8_t *>(mine + 8 * (size_t)k.K + 4 * (size_t)fire_words);
+    for (int64_t e = (int64_t)blockIdx.x * nw + wib; e < k.N; e += (int64_t)gridDim.x * nw) {
+        for (int q = lane; q < k.K; q += 32) sv[q] = 0;
+        for (int q = lane; q < fire_words; q += 32) fire[q] = 0;
+        for (int64_t f = lane; f < F; f += 32) xr[f] = k.x[e * F + f];
+        int64_t *srow = k.scores ? k.scores + e * P : nullptr;
+        if (srow)
+            for (int64_t p = lane; p < P; p += 32) srow[p] = 0;
+        __syncwarp();
+        for (int r = lane; r < k.R; r += 32) {
+            const int64_t q0 = k.ptr[r], q1 = k.ptr[r + 1];
+            bool f = q1 > q0;  // inference: a rule without includes never fires
+            for (int64_t q = q0; q < q1 && f; ++q) {
+                const uint32_t c = k.inc[q];
+                const uint8_t v = xr[c >> 1];
+                f = (c & 1u) ? v == 0 : v != 0;
+            }
+            if (f) {
+                atomicOr(&fire[r >> 5], 1u << (r & 31));
+                for (int kk = 0; kk < k.K; ++kk) {
+                    const int32_t wv = k.w[(size_t)r * k.K + kk];
+                    if (wv) atomicAdd(reinterpret_cast<unsigned long long *>(&sv[kk]),
+                                      (unsigned long long)(long long)wv);
+                }
+            }
+        }
+        __syncwarp();
+        int best = 0;
+        long long bv = sv[0];
+        for (int kk = 1; kk < k.K; ++kk)
+            if (sv[kk] > bv) {
+                bv = sv[kk];
+                best = kk;
+            }
+        if (lane == 0 && k.pred) k.pred[e] = best;
+        if (k.votes)
+            for (int kk = lane; kk < k.K; kk += 32) k.votes[e * k.K + kk] = sv[kk];
+        const int cls = k.for_class >= 0 ? k.for_class : best;
+        if (srow) {
+            for (int r = lane; r < k.R; r += 32) {
+                if (!((fire[r >> 5] >> (r & 31)) & 1u)) continue;
+                const long long wv = k.w[(size_t)r * k.K + cls];
+                if (!wv) continue;
+                for (int64_t q = k.ptr[r]; q < k.ptr[r + 1]; ++q) {
+                    const uint32_t c = k.inc[q];
+                    const int64_t p = (c & 1u) ? F + (c >> 1) : (int64_t)(c >> 1);
+                    atomicAdd(reinterpret_cast<unsigned long long *>(&srow[p]),
+                              (unsigned long long)wv);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 static unsigned int *g_bad_flag = nullptr;
 
 static int pick_g(int64_t F, int64_t K, int max_smem, int *G_out, size_t *smem_out) {
@@ -1364,6 +1447,34 @@ int tmb_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, i
         return fail(TMB_E_INVALID, "infer: bad arguments");
     cudaStream_t st = as_stream(stream);
     return launch_infer(r, x, N, votes, pred, labels, (unsigned long long *)correct, st);
+}
+
+int tmb_explain(const tmb_rules *r, const uint8_t *x, int64_t N, int for_class, int64_t *votes,
+                int64_t *pred, int64_t *scores, void *stream) {
+    int rc = require_device();
+    if (rc) return rc;
+    if (!r || N < 0 || (N > 0 && !x)) return fail(TMB_E_INVALID, "explain: bad arguments");
+    if (for_class >= (int)r->K) return fail(TMB_E_INVALID, "explain: for_class out of range");
+    if (N == 0) return TMB_OK;
+    ExplainK k;
+    k.x = x; k.N = N; k.F = r->F; k.inc = r->inc; k.ptr = r->ptr; k.w = r->weights;
+    k.R = (int)r->R; k.K = (int)r->K; k.negations = r->negations;
+    k.for_class = for_class < 0 ? -1 : for_class;
+    k.votes = votes; k.pred = pred; k.scores = scores;
+    const int threads = 256, nw = threads / 32;
+    const size_t per = 8 * (size_t)k.K + 4 * (size_t)((k.R + 31) / 32) + (size_t)((r->F + 15) & ~15LL);
+    const size_t smem = nw * ((per + 15) & ~(size_t)15);
+    int dev = 0, max_smem = 0;
+    cudaGetDevice(&dev);
+    TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (smem > (size_t)max_smem)
+        return fail(TMB_E_UNSUPPORTED, "explain: rule set / feature width too large");
+    TMB_CUDA(cudaFuncSetAttribute((const void *)k_explain,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t blocks = std::min<int64_t>((N + nw - 1) / nw, (int64_t)sm_count() * 8);
+    k_explain<<<(unsigned)blocks, threads, smem, as_stream(stream)>>>(k);
+    TMB_LAUNCHED();
+    return TMB_OK;
 }
 
 int tmb_set_option(const char *name, int64_t value) {

@@ -11,7 +11,8 @@ import numpy as np
 
 from .core import Config
 from .executor import TrainRun, train
-from .predictor import RuleSet, compile_ruleset, predict, predict_and_explain, predict_batch
+from .predictor import (RuleSet, compile_ruleset, predict, predict_and_explain,
+                        predict_and_explain_batch, predict_batch)
 
 
 class TsetlinMachine:
@@ -80,6 +81,10 @@ class Predictor:
 
     def predict_and_explain(self, x, level: str = "literal", for_class: int | None = None):
         return predict_and_explain(self.rules, x, level, for_class)
+
+    def predict_and_explain_batch(self, x, level: str = "literal",
+                                  for_class: int | None = None):
+        return predict_and_explain_batch(self.rules, x, level, for_class)
 
     def export_as_program(self, path: str, name: str = "tm"):
         """C99 code generation (export_c.py) is outside the GPU hot path's

@@ -233,6 +233,59 @@ def test_predictor_golden(gpu):
         assert np.array_equal(f.scores, g["feat_scores"][i])
     lit = gpu.augment_literals(g["allx"])
     assert np.array_equal(bank.batch_votes(lit), g["votes"])
+    # the batched device path against the reference's own explanations
+    p64, s64 = gpu.predict_and_explain_batch(rs, g["allx"][:64], level="literal")
+    _, f64 = gpu.predict_and_explain_batch(rs, g["allx"][:64], level="feature")
+    assert np.array_equal(p64, g["preds"])
+    assert np.array_equal(s64, g["lit_scores"]) and np.array_equal(f64, g["feat_scores"])
+
+
+def _explain_reference(includes, weights, n_literals, negations, x, for_class):
+    # predictor.py:99-124 restated (test oracle)
+    lit = np.concatenate([x, 1 - x]) if negations else x
+    votes = np.zeros(weights.shape[1], dtype=np.int64)
+    fired = []
+    for inc, w in zip(includes, weights):
+        if np.all(lit[inc] == 1):
+            votes += w
+            fired.append((inc, w))
+    pred = int(np.argmax(votes))
+    cls = pred if for_class is None else for_class
+    scores = np.zeros(lit.shape[0], dtype=np.int64)
+    for inc, w in fired:
+        scores[inc] += int(w[cls])
+    return pred, scores
+
+
+@pytest.mark.parametrize("negations", [True, False])
+@pytest.mark.parametrize("for_class", [None, 2])
+def test_predict_and_explain_batch_random(gpu, negations, for_class):
+    """Batched explanations on a larger random rule set with planted firing
+    (many rules fire per example), with and without negations, for the
+    predicted class and a fixed class."""
+    rs_ = np.random.default_rng(17 + int(negations))
+    F, R, K, N = 300, 800, 5, 257
+    P = 2 * F if negations else F
+    includes = []
+    for _ in range(R):
+        n = int(rs_.integers(1, 6))
+        feats = rs_.choice(F, size=n, replace=False)
+        pol = rs_.integers(0, 2, size=n) if negations else np.zeros(n, dtype=np.int64)
+        includes.append(np.sort(feats + F * pol).astype(np.int64))
+    weights = rs_.integers(-9, 10, size=(R, K)).astype(np.int32)
+    x = rs_.integers(0, 2, size=(N, F)).astype(np.uint8)
+    for e in range(N):
+        for j in rs_.integers(0, R, size=6):
+            inc = includes[int(j)]
+            x[e, inc[inc < F]] = 1
+            x[e, inc[inc >= F] - F] = 0
+    rset = gpu.RuleSet(F, K, negations, tuple(includes), weights)
+    preds, scores = gpu.predict_and_explain_batch(rset, x, level="literal", for_class=for_class)
+    for e in range(N):
+        p, s = _explain_reference(includes, weights, F, negations, x[e], for_class)
+        assert preds[e] == p, e
+        assert np.array_equal(scores[e], s), e
+    assert (scores != 0).any()
 
 
 @pytest.mark.parametrize("n_inc,F,K", [(1, 37, 3), (2, 64, 10), (3, 300, 4), (20, 4096, 10)])
