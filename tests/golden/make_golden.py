@@ -309,12 +309,46 @@ def tuning_fixture():
     save("tuning", **out)
 
 
+def modelio_fixture():
+    """GTM1 model files written by the reference (dataio.save_model) for a
+    dense bank, a sparse bank and a rule set, with the models' contents."""
+    import io
+    import tempfile
+
+    from tsetlinkit.dataio import save_model
+    out = {}
+    rs = np.random.default_rng(23)
+    x = rs.integers(0, 2, size=(150, 7)).astype(np.uint8)
+    y = (x[:, 1] | x[:, 3]).astype(np.int64)
+    cfg = tk.Config(n_literals=7, n_clauses=6, n_classes=2, s=2.5, threshold=5,
+                    n_literal_budget=4, seed=8, boost_true_positive=True)
+    dense = tk.train(cfg, (x, y), n_epochs=2).model
+    ex = [SparseExample(np.sort(rs.choice(40, size=int(rs.integers(2, 9)), replace=False))
+                        .astype(np.int64), int(rs.integers(0, 2))) for _ in range(80)]
+    scfg = tk.Config(n_literals=40, n_clauses=5, n_classes=2, s=2.0, threshold=4, seed=2,
+                     negated_literals_enabled=False, sparse_capacity=3, sparse_floor=-5)
+    sparse = tk.train(scfg, SparseDataset(40, ex), n_epochs=2).model
+    rset = compile_ruleset(dense)
+    with tempfile.TemporaryDirectory() as td:
+        for name, m in (("dense", dense), ("sparse", sparse), ("ruleset", rset)):
+            path = os.path.join(td, name + ".gtm")
+            save_model(m, path)
+            out[name + "_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    out["dense_states"], out["dense_weights"] = dense.states, dense.weights
+    lens = np.array([a.size for a in sparse.clause_literals], dtype=np.int64)
+    out["sparse_lens"] = lens
+    out["sparse_lits"] = np.concatenate(sparse.clause_literals) if lens.sum() else np.zeros(0, np.int64)
+    out["sparse_sts"] = np.concatenate(sparse.clause_states) if lens.sum() else np.zeros(0, np.int8)
+    out["sparse_weights"] = sparse.weights
+    save("modelio", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "kernels", "feedback", "train", "noisy_xor", "mnist",
-                             "predictor", "sparse", "tuning"]
+                             "predictor", "sparse", "tuning", "modelio"]
     table = {"rng": rng_fixture, "kernels": kernel_fixture, "feedback": feedback_fixture,
              "train": train_fixture, "noisy_xor": noisy_xor_fixture,
              "mnist": mnist_prefix_fixture, "predictor": predictor_fixture,
-             "sparse": sparse_fixture, "tuning": tuning_fixture}
+             "sparse": sparse_fixture, "tuning": tuning_fixture, "modelio": modelio_fixture}
     for name in which:
         table[name]()

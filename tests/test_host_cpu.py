@@ -143,3 +143,52 @@ def test_datasets_shapes():
     a = tmb.datasets.inference_examples(3, 10, 5)
     b = tmb.datasets.inference_examples(3, 12, 2)
     assert np.array_equal(a[2:4], b)
+
+
+def test_gtm1_model_files_byte_identical_to_reference(tmp_path):
+    """GTM1 save/load: the reference's own files for a
+    dense bank, a sparse bank and a rule set are reproduced byte for byte
+    from the same model contents, and load back to the same contents."""
+    import numpy as np
+
+    from conftest import golden
+    from paper_2405_04212_b200 import DenseClauseBank, SparseClauseBank, compile_ruleset
+    from paper_2405_04212_b200.core import Config
+    from paper_2405_04212_b200.modelio import (ModelFormatError, load_model, model_bytes,
+                                               model_from_bytes, save_model)
+    g = golden("modelio")
+    cfg = Config(n_literals=7, n_clauses=6, n_classes=2, s=2.5, threshold=5, n_literal_budget=4,
+                 seed=8, boost_true_positive=True)
+    dense = DenseClauseBank(cfg)
+    dense.states[:] = g["dense_states"]
+    dense.weights[:] = g["dense_weights"]
+    assert model_bytes(dense) == g["dense_bytes"].tobytes()
+    scfg = Config(n_literals=40, n_clauses=5, n_classes=2, s=2.0, threshold=4, seed=2,
+                  negated_literals_enabled=False, sparse_capacity=3, sparse_floor=-5)
+    sparse = SparseClauseBank(scfg)
+    ends = np.cumsum(g["sparse_lens"])
+    starts = ends - g["sparse_lens"]
+    sparse.clause_literals = [g["sparse_lits"][a:b].astype(np.int64) for a, b in zip(starts, ends)]
+    sparse.clause_states = [g["sparse_sts"][a:b].astype(np.int8) for a, b in zip(starts, ends)]
+    sparse.weights = g["sparse_weights"].astype(np.int32)
+    assert model_bytes(sparse) == g["sparse_bytes"].tobytes()
+    rset = compile_ruleset(dense)
+    assert model_bytes(rset) == g["ruleset_bytes"].tobytes()
+    # load the reference's files and re-save them (round trip)
+    for name in ("dense", "sparse", "ruleset"):
+        raw = g[name + "_bytes"].tobytes()
+        m = model_from_bytes(raw)
+        assert model_bytes(m) == raw, name
+        path = tmp_path / f"{name}.gtm"
+        save_model(m, path)
+        assert path.read_bytes() == raw
+        assert model_bytes(load_model(path)) == raw
+    m = model_from_bytes(g["dense_bytes"].tobytes())
+    assert np.array_equal(m.states, g["dense_states"]) and m.cfg == cfg
+    for bad in (b"XXXX" + raw[4:], raw + b"\0", raw[:-1]):
+        try:
+            model_from_bytes(bad)
+        except ModelFormatError:
+            pass
+        else:
+            raise AssertionError("malformed file accepted")
