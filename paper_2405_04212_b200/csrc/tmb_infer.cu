@@ -168,7 +168,6 @@ __global__ void __launch_bounds__(512) k_infer(InferK k) {
 // four partials and writes votes / predictions.  One cluster barrier per tile.
 constexpr int kCS = 4;   // CTAs per cluster
 constexpr int kTG = 4;   // 32-example groups per tile
-constexpr int kHead = 16;
 
 struct InferCK {
     const uint8_t *x;
@@ -905,7 +904,6 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
         const int ew = warp - kWsT, etid = tid - 32 * kWsT;
         const uint32_t haddr = smem_u32(heads);
         for (int64_t it = 0; it < n_my; ++it) {
-            const int64_t t = cid + it * n_clusters;
             const int buf = (int)(it & 1);
             const uint32_t *xt = buf ? xt1 : xt0;
             int32_t *dirty = dirty2 + buf * kTG;
