@@ -472,6 +472,44 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
         _lib.call("tmbh_infer", model._h, ct_ptr(xh), n_e2e, None, np_ptr(ph), 1 << 18)
     e2e_s = max_over_ranks(time.perf_counter() - t, world)
     e2e_value = n_e2e * world * args.steps / e2e_s
+    # the same examples as bit-packed words (feature f = bit f%64 of word
+    # f//64; the generator's raw stream words): device timing + e2e from
+    # pinned host words through the public API
+    xs_cpu = x[:args.c3_cpu_examples].cpu().numpy() if rank == 0 else None
+    del x
+    torch.cuda.empty_cache()
+    W = (F + 63) // 64
+    xb = torch.empty((n, W), dtype=torch.int64, device="cuda")
+    from paper_2405_04212_b200.runtime import ptr, stream_ptr
+    _lib.call("tmb_stream_u64_block", datasets.inference_stream_seed(3), start * W, n * W,
+              ptr(xb), stream_ptr())
+    predb = torch.empty(n, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        model.infer_device_packed(xb, pred_dev=predb)
+    torch.cuda.synchronize()
+    pa = torch.cuda.Event(enable_timing=True)
+    pb = torch.cuda.Event(enable_timing=True)
+    pa.record(stream)
+    for _ in range(args.steps):
+        model.infer_device_packed(xb, pred_dev=predb)
+    pb.record(stream)
+    torch.cuda.synchronize()
+    packed_ms = max_over_ranks(pa.elapsed_time(pb), world) / args.steps
+    packed_same = bool(torch.equal(predb, pred))
+    xbh = xb[:n_e2e].cpu().pin_memory()
+    prh = torch.empty(n_e2e, dtype=torch.int64).pin_memory()
+    barrier(world)
+    pe0 = torch.cuda.Event(enable_timing=True)
+    pe1 = torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    for _ in range(args.steps):
+        xbd = xbh.to("cuda", non_blocking=True)
+        model.infer_device_packed(xbd, pred_dev=predb[:n_e2e])
+        prh.copy_(predb[:n_e2e], non_blocking=True)
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    packed_e2e = n_e2e * world * args.steps / (max_over_ranks(pe0.elapsed_time(pe1), world) / 1e3)
+    del xb
     tr_inf, tr_inf_src = ncu_traffic("k_infer_ws")
     if tr_inf is not None:
         tr_inf *= (N_total / world) / (1 << 22)  # captured on the 2^22-example launch
@@ -491,6 +529,15 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
                      "frac": achieved / HBM_PEAK, "traffic": tr_inf, "traffic_source": tr_inf_src,
                      "peak_source": HBM_PEAK_SRC,
                      "algorithmic_bytes_per_example": bytes_ex, "avg_launch_ms": per_launch_ms},
+        "bit_packed_input": {
+            "note": "same examples and model, features as uint64 words (tmb_infer_packed); "
+                    "not the reference's input format, so not the headline",
+            "value": N_total / (packed_ms / 1e3), "unit": "examples/s", "ms_per_step": packed_ms,
+            "same_predictions_as_uint8": packed_same,
+            "hbm_bytes_per_example": 8 * W + 8,
+            "e2e": {"value": packed_e2e, "unit": "examples/s", "h2d_bytes_per_step": n_e2e * 8 * W,
+                    "d2h_bytes_per_step": n_e2e * 8,
+                    "path": "pinned host uint64 words -> H2D -> tmb_infer_packed -> D2H"}},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "examples/s", "h2d_bytes_per_step": n_e2e * F,
                 "d2h_bytes_per_step": n_e2e * 8,
@@ -500,7 +547,7 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
     if rank == 0 and not args.no_cpu_baseline:
         from oracle import oracle
         _, ncpu = host_desc()
-        xs = x[:args.c3_cpu_examples].cpu().numpy()
+        xs = xs_cpu
         t = time.perf_counter()
         oracle.batch_votes(m.states, m.weights, oracle.augment_literals(xs), nthreads=ncpu,
                            want_votes=False)
@@ -509,7 +556,6 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
                                "kind": "port",
                                "sample": f"oracle C port of batch_votes, {len(xs)}-example "
                                          f"prefix, {ncpu} threads ({dt:.1f}s)"}
-    del x
     torch.cuda.empty_cache()
     return out
 

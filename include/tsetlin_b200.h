@@ -217,6 +217,13 @@ int tmb_rules_info(const tmb_rules *r, int64_t *n_rules, int64_t *n_includes);
  * [N,K] and pred int64 [N] are optional (NULL); labels (device int64 [N]) +
  * correct (device uint64 [1], accumulated) optional.  Ties -> lowest class
  * (np.argmax, executor.py:382). */
+/* Inference on bit-packed features (bit-packed ingestion):
+ * xb uint64 [N, W64], feature f = bit (f % 64) of word f / 64 (W64 >= F/64).
+ * Same outputs as tmb_infer; 8x fewer input bytes than uint8 rows.  Needs a
+ * rule set the cluster kernel supports (else TMB_E_UNSUPPORTED). */
+int tmb_infer_packed(const tmb_rules *r, const uint64_t *xb, int64_t N, int64_t W64,
+                     int64_t *votes, int64_t *pred, const int64_t *labels, uint64_t *correct,
+                     void *stream);
 /* Batched predict_and_explain (predictor.py:99-124) on device buffers:
  * x uint8 [N, F] raw features; pred int64 [N] (argmax, ties -> lowest);
  * votes int64 [N, K] or NULL; scores int64 [N, P] or NULL (P = 2F with

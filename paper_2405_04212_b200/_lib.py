@@ -87,6 +87,7 @@ SIGNATURES = {
     "tmb_infer_status": (i32, [vp]),
     "tmb_set_option": (i32, [ct.c_char_p, i64]),
     "tmb_explain": (i32, [vp, vp, i64, i32, vp, vp, vp, vp]),
+    "tmb_infer_packed": (i32, [vp, vp, i64, i64, vp, vp, vp, vp, vp]),
     "tmb_sparse_create": (i32, [vp, vp, i64, vp]),
     "tmb_sparse_destroy": (i32, [vp]),
     "tmb_sparse_train": (i32, [vp, vp, vp, vp, vp, i64, u64, vp, vp]),

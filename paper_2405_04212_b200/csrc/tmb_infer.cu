@@ -185,6 +185,9 @@ struct InferCK {
     int rloc_max;
     int dbg;  // bit0: skip eval, bit1: skip transpose (timing experiments only)
     unsigned long long *phase;  // optional [grid][8] clock64 per phase (thread 0)
+    const uint64_t *xb;  // bit-packed input [N][W64] (feature f = bit f%64 of word f/64), or null
+    int64_t W64;
+    int xb_vec16;        // 16-byte loads legal (W64 even, base 16-B aligned)
 };
 
 __device__ __forceinline__ uint32_t pack8(unsigned long long q) {
@@ -620,6 +623,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 
 constexpr int kWsT = 8;  // transposer warps per CTA; the last warp finalizes, the rest evaluate
 
+template <bool PACKED>
 __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
     extern __shared__ __align__(16) char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
@@ -701,13 +705,82 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
         }                                                                 \
     } while (0)
 
-    if (warp < kWsT) {
-        // ================= transposer group =================
-        // Each warp owns units u = warp + kWsT*q (q < nq) of every tile
-        // (unit = 32 examples x 128 features; lane (j, c16) loads 16 feature
-        // bytes of 8 example rows).  The loads of the next unit (possibly of
-        // the next tile) are issued before the current unit is transposed,
-        // so HBM latency overlaps the bit work.
+    if (PACKED && warp < kWsT) {
+        // ========== transposer group, bit-packed input ==========
+        // unit = 32 examples x 256 features: lane l holds 256 feature bits
+        // of example 32g + l (two 16-byte loads); eight 32x32 warp bit
+        // transposes leave lane j with the X^T words of features fb+32q+j.
+        const int units = (int)((qf1 - qf0 + 255) / 256) * kTG;
+        const int nq = units > warp ? (units - warp + kWsT - 1) / kWsT : 0;
+        const int g = warp % kTG;
+        const int64_t fb0 = qf0 + (int64_t)(warp / kTG) * 256;
+        auto load_p = [&](int64_t itx, int q, uint32_t (&w)[8]) {
+            const int64_t e = (cid + itx * n_clusters) * tile_n + 32 * g + lane;
+            const int64_t fb = fb0 + (int64_t)q * (kWsT / kTG) * 256;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = 0;
+            if (e >= k.N || fb >= qf1) return;
+            // the row as little-endian 32-bit words: word fb/32 holds
+            // features fb..fb+31 (quarter starts are multiples of 32)
+            const uint32_t *row = reinterpret_cast<const uint32_t *>(k.xb + e * k.W64);
+            const int64_t u0 = fb >> 5, nu = 2 * k.W64;
+            if (k.xb_vec16 && (u0 & 3) == 0 && u0 + 8 <= nu) {
+                const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(row + u0));
+                const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(row + u0 + 4));
+                w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+                w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+            } else {
+#pragma unroll
+                for (int h = 0; h < 8; ++h)
+                    if (u0 + h < nu) w[h] = __ldcs(row + u0 + h);
+            }
+        };
+        auto finish_p = [&](const uint32_t (&w)[8], int q, uint32_t *mine) {
+            const int64_t fb = fb0 + (int64_t)q * (kWsT / kTG) * 256;
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq) {
+                const uint32_t x = warp_transpose32(w[qq], lane);
+                const int64_t f = fb + 32 * qq + lane;
+                if (f < qf1) mine[(size_t)f * kTG + g] = x;
+            }
+        };
+        auto tile_end_p = [&](int64_t it) {
+            const int buf = (int)(it & 1);
+            uint32_t *mine = buf ? xt1 : xt0;
+            named_sync(1, 32 * kWsT);
+            if (tid == 0) {
+                if (my_bytes) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const uint32_t src = smem_u32(mine + (size_t)qf0 * kTG);
+                    for (int p = 0; p < kCS; ++p) {
+                        if (p == rank) continue;
+                        bulk_copy_to_peer(mapa_u32(src, p), src, my_bytes,
+                                          mapa_u32(smem_u32(&full[buf]), p));
+                    }
+                }
+                if (expect_bytes) mbar_arm(&full[buf], expect_bytes);
+                else mbar_arrive_local(&full[buf]);
+            }
+        };
+        uint32_t wa[8], wb[8];
+        for (int64_t it = 0; it < n_my; ++it) {
+            const int buf = (int)(it & 1);
+            uint32_t *mine = buf ? xt1 : xt0;
+            if (it >= 2) mbar_wait(&empty[buf], (uint32_t)(((it >> 1) + 1) & 1));
+            int q = 0;
+            for (; q + 1 < nq; q += 2) {
+                load_p(it, q, wa);
+                load_p(it, q + 1, wb);
+                finish_p(wa, q, mine);
+                finish_p(wb, q + 1, mine);
+            }
+            if (q < nq) {
+                load_p(it, q, wa);
+                finish_p(wa, q, mine);
+            }
+            tile_end_p(it);
+        }
+    } else if (!PACKED && warp < kWsT) {
         const int j = lane >> 3, c16 = lane & 7;
         const int units = nblk * kTG;
         const int nq = units > warp ? (units - warp + kWsT - 1) / kWsT : 0;
@@ -1128,7 +1201,8 @@ static int pick_g(int64_t F, int64_t K, int max_smem, int *G_out, size_t *smem_o
 
 static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes,
                                 int64_t *pred, const int64_t *labels,
-                                unsigned long long *correct, cudaStream_t st, bool *launched);
+                                unsigned long long *correct, cudaStream_t st, bool *launched,
+                                const uint64_t *xb = nullptr, int64_t W64 = 0);
 
 int g_force_generic_infer = 0;
 int g_infer_dbg = 0;
@@ -1177,7 +1251,8 @@ int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes
 
 static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes,
                                 int64_t *pred, const int64_t *labels,
-                                unsigned long long *correct, cudaStream_t st, bool *launched) {
+                                unsigned long long *correct, cudaStream_t st, bool *launched,
+                                const uint64_t *xb, int64_t W64) {
     *launched = false;
     if (r->K > 32 || r->R < 1) return TMB_OK;
     int dev = 0;
@@ -1197,7 +1272,11 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     k.rloc_max = (int)rloc_max;
     k.dbg = g_infer_dbg;
     k.phase = g_infer_phase;
-    const void *fn = g_infer_ws ? (const void *)k_infer_ws : (const void *)k_infer_cluster;
+    k.xb = xb;
+    k.W64 = W64;
+    k.xb_vec16 = xb && (W64 % 2 == 0) && (reinterpret_cast<uintptr_t>(xb) % 16 == 0);
+    const void *fn = k.xb ? (const void *)k_infer_ws<true>
+                   : g_infer_ws ? (const void *)k_infer_ws<false> : (const void *)k_infer_cluster;
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int threads = 512;
     cudaLaunchConfig_t lc = {};
@@ -1445,6 +1524,28 @@ int tmb_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, i
         return fail(TMB_E_INVALID, "infer: bad arguments");
     cudaStream_t st = as_stream(stream);
     return launch_infer(r, x, N, votes, pred, labels, (unsigned long long *)correct, st);
+}
+
+int tmb_infer_packed(const tmb_rules *r, const uint64_t *xb, int64_t N, int64_t W64,
+                     int64_t *votes, int64_t *pred, const int64_t *labels, uint64_t *correct,
+                     void *stream) {
+    int rc = require_device();
+    if (rc) return rc;
+    if (!r || N < 0 || (N > 0 && !xb) || (labels && !correct) || W64 * 64 < r->F)
+        return fail(TMB_E_INVALID, "infer_packed: bad arguments");
+    if (N == 0) return TMB_OK;
+    if (!r->heads_ok) return fail(TMB_E_UNSUPPORTED, "infer_packed: rule set needs the cluster kernel");
+    if (!g_bad_flag) {
+        TMB_CUDA(cudaMalloc(&g_bad_flag, sizeof(unsigned)));
+        TMB_CUDA(cudaMemset(g_bad_flag, 0, sizeof(unsigned)));
+    }
+    bool launched = false;
+    rc = launch_infer_cluster(r, nullptr, N, votes, pred, labels, (unsigned long long *)correct,
+                              as_stream(stream), &launched, xb, W64);
+    if (rc) return rc;
+    if (!launched)
+        return fail(TMB_E_UNSUPPORTED, "infer_packed: shape not supported by the cluster kernel");
+    return TMB_OK;
 }
 
 int tmb_explain(const tmb_rules *r, const uint8_t *x, int64_t N, int for_class, int64_t *votes,

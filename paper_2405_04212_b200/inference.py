@@ -117,3 +117,27 @@ class CompiledModel:
         N = x_dev.shape[0]
         _lib.call("tmb_infer", self._h, ptr(x_dev), N, ptr(votes_dev), ptr(pred_dev),
                   ptr(labels_dev), ptr(correct_dev), stream_ptr())
+
+    # -- bit-packed input (bit-packed ingestion) ---------------
+    def infer_device_packed(self, xb_dev, votes_dev=None, pred_dev=None, labels_dev=None,
+                            correct_dev=None):
+        """Device uint64 [N, W64] bit-packed features (feature f = bit f % 64
+        of word f // 64, e.g. datasets.inference_examples(..., packed=True))
+        on the current stream; same outputs as infer_device."""
+        N, W64 = xb_dev.shape
+        _lib.call("tmb_infer_packed", self._h, ptr(xb_dev), N, W64, ptr(votes_dev),
+                  ptr(pred_dev), ptr(labels_dev), ptr(correct_dev), stream_ptr())
+
+    def votes_and_pred_packed(self, xb: np.ndarray, want_votes: bool = True):
+        """Host bit-packed rows in, host votes / predictions out."""
+        import torch
+        xb = np.ascontiguousarray(xb, dtype=np.uint64)
+        if xb.ndim != 2 or xb.shape[1] * 64 < self.n_features:
+            raise ValueError(f"expected [N, >= {(self.n_features + 63) // 64}] uint64 rows")
+        N = xb.shape[0]
+        xd = torch.from_numpy(xb.view(np.int64)).cuda()
+        votes = torch.empty((N, self.n_classes), dtype=torch.int64, device="cuda") \
+            if want_votes else None
+        pred = torch.empty(N, dtype=torch.int64, device="cuda")
+        self.infer_device_packed(xd, votes, pred)
+        return (votes.cpu().numpy() if want_votes else None), pred.cpu().numpy()

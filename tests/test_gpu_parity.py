@@ -559,3 +559,33 @@ def test_cross_validate_golden(gpu):
     rep = tuning.cross_validate(cfg, (g["cv_x"], g["cv_y"]), 4, 2, seed=9)
     assert np.array_equal(rep.fold_assignments, g["cv_folds"])
     assert np.array_equal(np.array(rep.fold_accuracies), g["cv_acc"])
+
+
+@pytest.mark.parametrize("F,n_inc,N", [(4096, 20, 3000), (300, 3, 1000), (128, 2, 777)])
+def test_inference_bit_packed_input(gpu, oracle, F, n_inc, N):
+    """Bit-packed input (uint64 words, feature f = bit f % 64 of word f // 64)
+    through the packed transposer: identical votes / predictions to the uint8
+    path and to the oracle, including widths that are not multiples of 128
+    (8-byte loads) and ragged tiles."""
+    import torch
+    m = gpu.datasets.inference_model(model_seed=5, n_features=F, n_clauses=2000,
+                                     n_includes=n_inc)
+    bank = gpu.DenseClauseBank(gpu.Config(n_literals=F, n_clauses=2000, n_classes=10, s=2.0,
+                                          threshold=100))
+    bank.states[:] = m.states
+    bank.weights[:] = m.weights
+    model = gpu.CompiledModel.from_bank(bank)
+    xb = gpu.datasets.inference_examples(3, 11, N, n_features=F, packed=True)
+    x = gpu.datasets.inference_examples(3, 11, N, n_features=F)
+    vb, pb = model.votes_and_pred_packed(xb)
+    v8, p8 = model.votes_and_pred(x)
+    assert np.array_equal(vb, v8) and np.array_equal(pb, p8)
+    ov, op = oracle.batch_votes(m.states, m.weights, oracle.augment_literals(x), nthreads=8)
+    assert np.array_equal(vb, ov) and np.array_equal(pb, op)
+    # a base 8 bytes off 16-byte alignment forces the 8-byte load path
+    flat = torch.zeros(xb.size + 1, dtype=torch.int64, device="cuda")
+    xd = flat[1:].view(N, xb.shape[1])
+    xd.copy_(torch.from_numpy(xb.view(np.int64)))
+    pred = torch.empty(N, dtype=torch.int64, device="cuda")
+    model.infer_device_packed(xd, pred_dev=pred)
+    assert np.array_equal(pred.cpu().numpy(), op)
