@@ -621,10 +621,12 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-constexpr int kWsT = 8;  // transposer warps per CTA; the last warp finalizes, the rest evaluate
 
 template <bool PACKED>
 __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
+    // transposer warps per CTA (a multiple of kTG); the last warp finalizes,
+    // the rest evaluate (11 evaluators for bit-packed input measured slower)
+    constexpr int kWsT = 8;
     extern __shared__ __align__(16) char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
@@ -943,10 +945,16 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 if ((pm >> lane) & 1) mbar_arrive_remote(vb);
                 else mbar_arrive_remote_relaxed(vb);
             }
-            mbar_wait_cluster(&vfull[buf], par);
+            // the partials are DSMEM stores into this CTA's shared memory,
+            // performed before the writers' releasing arrivals: a CTA-scope
+            // wait sees them (a cluster-scope acquire adds an L1 invalidate
+            // per tile).  iflag slots carry the tile's tag (it + 1), so they
+            // are never reset and need no release on the way back.
+            mbar_wait(&vfull[buf], par);
+            const int tag = (int)(it + 1);
             const int64_t e = t * tile_n + 32 * rank + lane;
-            const bool any = iflag[buf * kCS + 0] | iflag[buf * kCS + 1] | iflag[buf * kCS + 2] |
-                             iflag[buf * kCS + 3];
+            const bool any = iflag[buf * kCS + 0] == tag || iflag[buf * kCS + 1] == tag ||
+                             iflag[buf * kCS + 2] == tag || iflag[buf * kCS + 3] == tag;
             if (e < k.N) {
                 int best = 0;
                 if (any || k.votes) {
@@ -955,7 +963,8 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                         int32_t sum = 0;
 #pragma unroll
                         for (int p = 0; p < kCS; ++p)
-                            if (iflag[buf * kCS + p]) sum += inbox[((buf * kCS + p) * 32 + lane) * K + kk];
+                            if (iflag[buf * kCS + p] == tag)
+                                sum += inbox[((buf * kCS + p) * 32 + lane) * K + kk];
                         if (kk == 0 || sum > bv) {
                             bv = sum;
                             best = kk;
@@ -967,10 +976,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 if (k.labels) hits += (k.labels[e] == best);
             }
             __syncwarp();
-            if (lane < kCS) {
-                iflag[buf * kCS + lane] = 0;
-                mbar_arrive_remote(mapa_u32(smem_u32(&vempty[buf]), lane));
-            }
+            if (lane < kCS) mbar_arrive_remote_relaxed(mapa_u32(smem_u32(&vempty[buf]), lane));
         }
     } else {
         // ================= evaluator group =================
@@ -1053,6 +1059,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                         }
                     }
                     if (!__any_sync(0xffffffffu, A0 | A1 | A2 | A3 | B0 | B1 | B2 | B3)) break;
+                    if ((k.dbg & 32) && grp == 1) break;  // timing experiment only
                 }
                 if ((A0 | A1 | A2 | A3) && rA < rloc) finish_rule(rA, A0, A1, A2, A3);
                 if ((B0 | B1 | B2 | B3) && rB < rloc) finish_rule(rB, B0, B1, B2, B3);
@@ -1081,7 +1088,8 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 dst[((buf * kCS + rank) * 32) * K + rem] = part[i];
                 part[i] = 0;
             }
-            if (etid < kCS && dirty[etid]) cluster.map_shared_rank(iflag, etid)[buf * kCS + rank] = 1;
+            if (etid < kCS && dirty[etid])
+                cluster.map_shared_rank(iflag, etid)[buf * kCS + rank] = (int)(it + 1);  // tile tag
             if (etid == 0) pushf[buf] = dirty[0] | (dirty[1] << 1) | (dirty[2] << 2) | (dirty[3] << 3);
             named_sync(2, 32 * nE);
             if (etid == 0) mbar_arrive_local(&epushed[buf]);  // forwarded as vfull arrivals
