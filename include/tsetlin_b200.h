@@ -275,6 +275,10 @@ typedef struct tmb_sparse tmb_sparse;
 int tmb_sparse_create(const tmb_sparse_cfg *cfg, const int32_t *candidates,
                       int64_t n_candidates, tmb_sparse **out);
 int tmb_sparse_destroy(tmb_sparse *sp);
+/* Launch layout chosen at create time: out[0] = 1 if the trainer holds the
+ * clause lists in shared memory, out[1] = CTAs, out[2] = threads per CTA,
+ * out[3] = dynamic shared memory bytes.  (No reference counterpart.) */
+int tmb_sparse_layout(const tmb_sparse *sp, int64_t *out4);
 /* Train n_steps documents in `order` (device int32), CSR on device. */
 int tmb_sparse_train(tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
                      const int32_t *labels, const int32_t *order, int64_t n_steps,

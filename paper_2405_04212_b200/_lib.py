@@ -90,6 +90,7 @@ SIGNATURES = {
     "tmb_infer_packed": (i32, [vp, vp, i64, i64, vp, vp, vp, vp, vp]),
     "tmb_sparse_create": (i32, [vp, vp, i64, vp]),
     "tmb_sparse_destroy": (i32, [vp]),
+    "tmb_sparse_layout": (i32, [vp, vp]),
     "tmb_sparse_train": (i32, [vp, vp, vp, vp, vp, i64, u64, vp, vp]),
     "tmb_sparse_feedback": (i32, [vp, vp, i64, vp, i64, i64, vp, vp, u64, u64, vp, vp]),
     "tmb_sparse_get": (i32, [vp, vp, vp, vp, vp, vp, vp]),

@@ -1216,6 +1216,7 @@ int g_force_generic_infer = 0;
 int g_infer_dbg = 0;
 int g_infer_ws = 1;  // tmb_set_option("infer.warp_specialized", 0|1)
 extern unsigned long long *g_sparse_phase;  // tmb_sparse.cu
+extern int g_sparse_resident;                // tmb_sparse.cu
 unsigned long long *g_infer_phase = nullptr;
 
 int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, int64_t *pred,
@@ -1600,6 +1601,10 @@ int tmb_set_option(const char *name, int64_t value) {
     }
     if (std::string(name) == "sparse.phase_buffer") {  // device uint64 [n_cta*8] or 0
         g_sparse_phase = reinterpret_cast<unsigned long long *>(value);
+        return TMB_OK;
+    }
+    if (std::string(name) == "sparse.resident") {  // 0: keep clause lists in global memory
+        g_sparse_resident = (int)value;            // (applies to banks created afterwards)
         return TMB_OK;
     }
     if (std::string(name) == "infer.warp_specialized") {

@@ -82,16 +82,11 @@ __device__ __forceinline__ bool contains(const int32_t *a, int n, int32_t v) {
     return p < n && a[p] == v;
 }
 
-// warp-wide exclusive scan of a 0/1 flag; *tot = warp total
+// warp-wide exclusive scan of a 0/1 flag; *tot = warp total (one ballot)
 __device__ __forceinline__ int warp_excl(int f, int lane, int *tot) {
-    int x = f;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    *tot = __shfl_sync(0xffffffffu, x, 31);
-    return x - f;
+    const unsigned b = __ballot_sync(0xffffffffu, f != 0);
+    *tot = __popc(b);
+    return __popc(b & ((1u << lane) - 1u));
 }
 
 // Type I on clause c (one warp): domain = stored U active, merged by a merge
@@ -117,15 +112,11 @@ __device__ __forceinline__ void stage_list(const int32_t *L, const int8_t *S, in
     }
 }
 
-__device__ int event_type_i(const SparseK &k, int c, int src, const int32_t *act, int n_act,
-                            int out, uint64_t sk, int lane, uint64_t &ndraws, int32_t *sL,
-                            int8_t *sS) {
-    int32_t *DL = lits_of(k, c, src ^ 1);
-    int8_t *DS = sts_of(k, c, src ^ 1);
-    const int n = k.len[c];
-    const int32_t *L;
-    const int8_t *S;
-    stage_list(lits_of(k, c, src), sts_of(k, c, src), n, sL, sS, lane, L, S);
+// L/S: the clause's current list (n pairs), DL/DS: the other buffer.
+__device__ __forceinline__ int event_type_i(const SparseK &k, const int32_t *L, const int8_t *S,
+                                            int n, int32_t *DL, int8_t *DS, const int32_t *act,
+                                            int n_act, int out, uint64_t sk, int lane,
+                                            uint64_t &ndraws) {
     const int total = n + n_act;
     int emitted = 0, cond_before = 0;
     for (int base = 0; base < total; base += 32) {
@@ -182,14 +173,9 @@ __device__ int event_type_i(const SparseK &k, int c, int src, const int32_t *act
 // Type II, output 1 (one warp): every stored pair survives (states only move
 // up from above the floor); inserted = the first non-stored, non-active
 // candidates x with #stored(<x) + #inserted(<x) < capacity, at floor + 1.
-__device__ int event_type_ii(const SparseK &k, int c, int src, const int32_t *act, int n_act,
-                             int32_t *ins_buf, int lane, int32_t *sL, int8_t *sS) {
-    int32_t *DL = lits_of(k, c, src ^ 1);
-    int8_t *DS = sts_of(k, c, src ^ 1);
-    const int n = k.len[c];
-    const int32_t *L;
-    const int8_t *S;
-    stage_list(lits_of(k, c, src), sts_of(k, c, src), n, sL, sS, lane, L, S);
+__device__ __forceinline__ int event_type_ii(const SparseK &k, const int32_t *L, const int8_t *S,
+                                             int n, int32_t *DL, int8_t *DS, const int32_t *act,
+                                             int n_act, int32_t *ins_buf, int ins_cap, int lane) {
     const int cap = k.capacity;
     int ins = 0;
     bool overflow = false;
@@ -209,7 +195,7 @@ __device__ int event_type_ii(const SparseK &k, int c, int src, const int32_t *ac
         const unsigned fail = __ballot_sync(0xffffffffu, cand && !keep);
         const int kpre = warp_excl(keep ? 1 : 0, lane, &ktot) + ins;
         if (keep) {
-            if (kpre < kMaxIns) ins_buf[kpre] = x;
+            if (kpre < ins_cap) ins_buf[kpre] = x;
             else overflow = true;
         }
         ins += ktot;
@@ -239,10 +225,15 @@ __device__ int event_type_ii(const SparseK &k, int c, int src, const int32_t *ac
 
 struct SSmem {
     int32_t *act;       // [2][kMaxActive] current / next document
-    int32_t *stL;       // [nwarps][kStage] staged clause literals
+    int32_t *stL;       // [nwarps][kStage] staged clause literals (global-list mode)
     int8_t *stS;        // [nwarps][kStage] staged clause states
+    int32_t *resL;      // [cmax][2][slab] resident clause lists (resident mode)
+    int8_t *resS;       // [cmax][2][slab]
+    int32_t *rlen;      // [cmax]
+    int32_t *rcur;      // [cmax]
     int64_t *meta;      // [3][4] prefetched document: a0, a1, label, -
-    int32_t *ins;       // [nwarps][kMaxIns]
+    int32_t *ins;       // [nwarps][kMaxIns] (global-list mode; resident mode uses the
+                        // source list's free tail, whose size is exactly the room left)
     uint32_t *ut_bits, *un_bits;
     int32_t *word_cum, *info, *work, *misc;
     uint64_t *sk_t, *sk_n, *blk_ctr, *blk_seed, *draw_t, *draw_n;
@@ -251,7 +242,11 @@ struct SSmem {
 
 __host__ __device__ inline size_t salign(size_t x) { return (x + 15) / 16 * 16; }
 
-__host__ __device__ inline size_t sparse_smem(const SparseK &k, int nwarps, char *base, SSmem *s) {
+// res: every owned clause's two list buffers live in shared memory for the
+// whole launch (loaded at entry, written back at exit); otherwise the lists
+// stay in global memory and events stage the source list per warp.
+__host__ __device__ inline size_t sparse_smem(const SparseK &k, int nwarps, bool res, char *base,
+                                              SSmem *s) {
     size_t off = 0;
     auto take = [&](size_t bytes) -> char * {
         off = salign(off);
@@ -261,10 +256,16 @@ __host__ __device__ inline size_t sparse_smem(const SparseK &k, int nwarps, char
     };
     SSmem t;
     t.act = (int32_t *)take(4 * 2 * kMaxActive);
-    t.stL = (int32_t *)take(4 * (size_t)kStage * nwarps);
-    t.stS = (int8_t *)take((size_t)kStage * nwarps);
+    const size_t stage = res ? 0 : (size_t)kStage * nwarps;
+    const size_t rsz = res ? (size_t)k.cmax * 2 * k.slab : 0;
+    t.stL = (int32_t *)take(4 * stage);
+    t.stS = (int8_t *)take(stage);
+    t.resL = (int32_t *)take(4 * rsz);
+    t.resS = (int8_t *)take(rsz);
+    t.rlen = (int32_t *)take(4 * (size_t)(res ? k.cmax : 0));
+    t.rcur = (int32_t *)take(4 * (size_t)(res ? k.cmax : 0));
     t.meta = (int64_t *)take(8 * 12);
-    t.ins = (int32_t *)take(4 * (size_t)kMaxIns * nwarps);
+    t.ins = (int32_t *)take(res ? 0 : 4 * (size_t)kMaxIns * nwarps);
     t.ut_bits = (uint32_t *)take(4 * k.fmax_words);
     t.un_bits = (uint32_t *)take(4 * k.fmax_words);
     t.word_cum = (int32_t *)take(4 * (k.fmax_words + 1));
@@ -286,12 +287,13 @@ enum : int { SI_TEV = 1, SI_NEV = 2, SI_T1 = 4, SI_N1 = 8, SI_OUT = 16 };
 
 // One cooperative grid; CTA b owns clauses [c0, c1).  k.x_ut != nullptr runs
 // a single example with explicit outputs / flags / counter (bank-level API).
+template <bool RES>
 __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
     extern __shared__ __align__(16) char smem_raw[];
     SSmem s;
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = nthr >> 5;
-    sparse_smem(k, nwarps, smem_raw, &s);
+    sparse_smem(k, nwarps, RES, smem_raw, &s);
     const int rank = blockIdx.x, n_cta = k.n_cta, C = k.C, K = k.K;
     const int c0 = cta_begin(rank, C, n_cta), c1 = cta_begin(rank + 1, C, n_cta);
     const int cown = c1 - c0;
@@ -304,11 +306,32 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
         s.blk_ctr[i] = explicit_flags ? k.x_counter : k.block_counters[b0 + i];
         s.blk_seed[i] = explicit_flags ? k.x_seed : k.block_seeds[b0 + i];
     }
+    // clause list accessors: (literals, states, length) of local clause j's
+    // current list, and the other buffer
+    const int slab = k.slab;
+    if (RES) {
+        for (int j = warp; j < cown; j += nwarps) {
+            const int c = c0 + j, src = k.cur[c], n = k.len[c];
+            const int32_t *gL = lits_of(k, c, src);
+            const int8_t *gS = sts_of(k, c, src);
+            int32_t *rL = s.resL + (size_t)j * 2 * slab;
+            int8_t *rS = s.resS + (size_t)j * 2 * slab;
+            for (int q = lane; q < n; q += 32) {
+                rL[q] = gL[q];
+                rS[q] = gS[q];
+            }
+            if (lane == 0) {
+                s.rlen[j] = n;
+                s.rcur[j] = 0;
+            }
+        }
+    }
     __syncthreads();
     uint64_t n_draws = 0, n_events = 0, n_t1 = 0, n_t2 = 0;
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
     const bool prof = k.phase != nullptr;
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long ev_clk[2] = {0, 0};  // per-warp cycles in Type I / Type II merges
     long long t_mark = clock64();
 #define SPH(n)                                                            \
     do {                                                                  \
@@ -390,10 +413,20 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
             if (explicit_flags) {
                 outv = k.x_out[c];
             } else {
-                const int src = k.cur[c];
-                const int32_t *L = lits_of(k, c, src);
-                const int8_t *S = sts_of(k, c, src);
-                const int n = k.len[c];
+                const int32_t *L;
+                const int8_t *S;
+                int n;
+                if (RES) {
+                    const int b = s.rcur[j];
+                    L = s.resL + ((size_t)j * 2 + b) * slab;
+                    S = s.resS + ((size_t)j * 2 + b) * slab;
+                    n = s.rlen[j];
+                } else {
+                    const int src = k.cur[c];
+                    L = lits_of(k, c, src);
+                    S = sts_of(k, c, src);
+                    n = k.len[c];
+                }
                 int n_inc = 0;
                 bool viol = false;
                 for (int q = lane; q < n; q += 32) {
@@ -544,31 +577,56 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
             const int c = c0 + j;
             const int info = s.info[j];
             const int out = (info & SI_OUT) ? 1 : 0;
-            int src = k.cur[c];
+            int src = RES ? s.rcur[j] : k.cur[c];
+            int n = RES ? s.rlen[j] : k.len[c];
             for (int ev = 0; ev < 2; ++ev) {
                 const bool has = ev == 0 ? (info & SI_TEV) : (info & SI_NEV);
                 if (!has) continue;
                 const bool t1 = ev == 0 ? (info & SI_T1) : (info & SI_N1);
+                if (!t1 && !out) continue;  // Type II on output 0: no-op (window still consumed)
                 int nl;
-                if (t1) {
-                    nl = event_type_i(k, c, src, act, n_act, out, ev == 0 ? s.sk_t[j] : s.sk_n[j],
-                                      lane, n_draws, s.stL + (size_t)warp * kStage,
-                                      s.stS + (size_t)warp * kStage);
-                } else if (out) {
-                    nl = event_type_ii(k, c, src, act, n_act, s.ins + (size_t)warp * kMaxIns, lane,
-                                       s.stL + (size_t)warp * kStage, s.stS + (size_t)warp * kStage);
+                const long long e_t0 = prof ? clock64() : 0;
+                const int32_t *L;
+                const int8_t *S;
+                int32_t *DL;
+                int8_t *DS;
+                if (RES) {
+                    L = s.resL + ((size_t)j * 2 + src) * slab;
+                    S = s.resS + ((size_t)j * 2 + src) * slab;
+                    DL = s.resL + ((size_t)j * 2 + (src ^ 1)) * slab;
+                    DS = s.resS + ((size_t)j * 2 + (src ^ 1)) * slab;
                 } else {
-                    continue;  // Type II on output 0: no-op (window still consumed)
+                    stage_list(lits_of(k, c, src), sts_of(k, c, src), n,
+                               s.stL + (size_t)warp * kStage, s.stS + (size_t)warp * kStage, lane,
+                               L, S);
+                    DL = lits_of(k, c, src ^ 1);
+                    DS = sts_of(k, c, src ^ 1);
                 }
+                if (t1)
+                    nl = event_type_i(k, L, S, n, DL, DS, act, n_act, out,
+                                      ev == 0 ? s.sk_t[j] : s.sk_n[j], lane, n_draws);
+                else if (RES)
+                    nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
+                                       const_cast<int32_t *>(L) + n, slab - n, lane);
+                else
+                    nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
+                                       s.ins + (size_t)warp * kMaxIns, kMaxIns, lane);
+                if (prof) ev_clk[t1 ? 0 : 1] += (unsigned long long)(clock64() - e_t0);
                 if (nl < 0) {
                     if (lane == 0) atomicOr(k.overflow, 1u);
                     nl = 0;
                 }
                 __syncwarp();
                 src ^= 1;
+                n = nl;
                 if (lane == 0) {
-                    k.len[c] = nl;
-                    k.cur[c] = (uint8_t)src;
+                    if (RES) {
+                        s.rlen[j] = nl;
+                        s.rcur[j] = src;
+                    } else {
+                        k.len[c] = nl;
+                        k.cur[c] = (uint8_t)src;
+                    }
                 }
                 __syncwarp();
             }
@@ -594,7 +652,25 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
     }
 #undef SPH
     if (prof && tid == 0)
-        for (int q = 0; q < 8; ++q) k.phase[rank * 8 + q] = ph[q];
+        for (int q = 0; q < 6; ++q) k.phase[rank * 8 + q] = ph[q];
+    if (RES) {  // resident lists back to their global buffers (k.cur unchanged)
+        for (int j = warp; j < cown; j += nwarps) {
+            const int c = c0 + j, n = s.rlen[j], b = s.rcur[j], dst = k.cur[c];
+            const int32_t *rL = s.resL + ((size_t)j * 2 + b) * slab;
+            const int8_t *rS = s.resS + ((size_t)j * 2 + b) * slab;
+            int32_t *gL = lits_of(k, c, dst);
+            int8_t *gS = sts_of(k, c, dst);
+            for (int q = lane; q < n; q += 32) {
+                gL[q] = rL[q];
+                gS[q] = rS[q];
+            }
+            if (lane == 0) k.len[c] = n;
+        }
+    }
+    if (prof && lane == 0) {
+        atomicAdd(&k.phase[rank * 8 + 6], ev_clk[0]);
+        atomicAdd(&k.phase[rank * 8 + 7], ev_clk[1]);
+    }
     for (int bi = tid; bi <= b1 - b0; bi += nthr) {
         const int b = b0 + bi;
         const int last = block_begin(b + 1, C, k.n_blocks) - 1;
@@ -716,6 +792,7 @@ __global__ void __launch_bounds__(256) k_sparse_infer(SparseInferK k) {
 }
 
 unsigned long long *g_sparse_phase = nullptr;  // tmb_set_option("sparse.phase_buffer")
+int g_sparse_resident = 1;                      // tmb_set_option("sparse.resident")
 
 }  // namespace tmb
 
@@ -725,6 +802,7 @@ struct tmb_sparse {
     tmb_sparse_cfg cfg;
     int n_cta = 0, threads = 512;
     size_t smem = 0;
+    bool resident = false;  // clause lists held in shared memory by the trainer
     int32_t *lits[2] = {nullptr, nullptr};
     int8_t *sts[2] = {nullptr, nullptr};
     int32_t *len = nullptr;
@@ -787,7 +865,9 @@ int sparse_fill_k(tmb_sparse *sp) {
 int sparse_launch(tmb_sparse *sp, SparseK &k, cudaStream_t st) {
     k.phase = g_sparse_phase;
     void *args[] = {&k};
-    TMB_CUDA(cudaLaunchCooperativeKernel((const void *)k_sparse_train, dim3(sp->n_cta),
+    const void *fn = sp->resident ? (const void *)k_sparse_train<true>
+                                  : (const void *)k_sparse_train<false>;
+    TMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(sp->n_cta),
                                          dim3(sp->threads), args, sp->smem, st));
     TMB_LAUNCHED();
     return TMB_OK;
@@ -858,20 +938,32 @@ int tmb_sparse_create(const tmb_sparse_cfg *cfg, const int32_t *candidates, int6
     sp->n_cand = n_candidates;
     if ((rc = check_cuda(cudaGetLastError(), "sparse_create"))) return cleanup(rc);
     sparse_fill_k(sp);
-    sp->smem = sparse_smem(sp->k, sp->threads / 32, nullptr, nullptr);
     int max_smem = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    // resident clause lists when every CTA's share (2 buffers x slab) fits
+    const size_t smem_res = sparse_smem(sp->k, sp->threads / 32, true, nullptr, nullptr);
+    sp->resident = g_sparse_resident && smem_res <= (size_t)max_smem;
+    sp->smem = sp->resident ? smem_res : sparse_smem(sp->k, sp->threads / 32, false, nullptr, nullptr);
     if (sp->smem > (size_t)max_smem) return cleanup(fail(TMB_E_UNSUPPORTED, "sparse: smem"));
-    if ((rc = check_cuda(cudaFuncSetAttribute((const void *)k_sparse_train,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const void *fn = sp->resident ? (const void *)k_sparse_train<true>
+                                  : (const void *)k_sparse_train<false>;
+    if ((rc = check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)sp->smem), "cudaFuncSetAttribute")))
         return cleanup(rc);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k_sparse_train,
-                                                  sp->threads, sp->smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, sp->threads, sp->smem);
     if (per_sm * sms < sp->n_cta) return cleanup(fail(TMB_E_UNSUPPORTED, "sparse: co-residency"));
     *out = sp;
+    return TMB_OK;
+}
+
+int tmb_sparse_layout(const tmb_sparse *sp, int64_t *out4) {
+    if (!sp || !out4) return fail(TMB_E_INVALID, "sparse_layout: NULL");
+    out4[0] = sp->resident ? 1 : 0;
+    out4[1] = sp->n_cta;
+    out4[2] = sp->threads;
+    out4[3] = (int64_t)sp->smem;
     return TMB_OK;
 }
 

@@ -47,6 +47,13 @@ class SparseEngine:
         _lib.call("tmb_sparse_create", ct.byref(cs), cands.ctypes.data_as(ct.c_void_p),
                   cands.size, ct.byref(self._h))
 
+    @property
+    def resident(self):
+        """True if the trainer keeps the clause lists in shared memory."""
+        out = (ct.c_int64 * 4)()
+        _lib.call("tmb_sparse_layout", self._h, out)
+        return bool(out[0])
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:

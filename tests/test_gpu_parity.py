@@ -432,6 +432,16 @@ def test_facade_listing(gpu):
 
 # ------------------------------------------------------------------ SparseTM
 
+@pytest.fixture(params=[1, 0], ids=["resident", "global"])
+def sparse_mode(request, gpu):
+    """Both trainer layouts: clause lists resident in shared memory (default
+    when they fit) and lists in global memory with per-event staging."""
+    from paper_2405_04212_b200 import _lib
+    _lib.call("tmb_set_option", b"sparse.resident", request.param)
+    yield request.param
+    _lib.call("tmb_set_option", b"sparse.resident", 1)
+
+
 def _sparse_golden_data(gpu):
     g = golden("sparse")
     ptr, ind = g["indptr"], g["indices"]
@@ -440,7 +450,7 @@ def _sparse_golden_data(gpu):
     return g, gpu.SparseDataset(60, ex)
 
 
-def test_sparse_train_golden(gpu):
+def test_sparse_train_golden(gpu, sparse_mode):
     """SparseClauseBank training incl. capacity rule, floor/evict, candidate
     domain and 3 clause blocks: bit-exact lists, states, weights, votes."""
     g, ds = _sparse_golden_data(gpu)
@@ -460,7 +470,7 @@ def test_sparse_train_golden(gpu):
         assert np.array_equal(m.batch_votes(ds.examples), g[f"r{i}_votes"])
 
 
-def test_sparse_dense_equivalence(gpu):
+def test_sparse_dense_equivalence(gpu, sparse_mode):
     """test_acceptance.py:66-96 oracle: with the floor at the dense clamp and
     no capacity, the sparse engine replays the dense engine exactly."""
     rs = np.random.default_rng(11)
@@ -527,7 +537,7 @@ def test_sparse_bank_feedback_rules(gpu):
     assert b.clause_literals[0].tolist() == [0, 1, 5, 6]
 
 
-def test_sparse_large_vocab_prefix_vs_oracle(gpu, oracle):
+def test_sparse_large_vocab_prefix_vs_oracle(gpu, oracle, sparse_mode):
     """configs[4] shapes on a small slice: 10^6-literal universe, Zipf(1.05)
     documents of 100 tokens, 2000 clauses, capacity 64, floor -15, T=2000,
     s=5 -- 3 training documents against the oracle (its Type II walks all
@@ -548,6 +558,31 @@ def test_sparse_large_vocab_prefix_vs_oracle(gpu, oracle):
         assert np.array_equal(m.clause_states[j], ob.sts[j]), j
     ex = [gpu.SparseExample(a, 0) for a in acts[:200]]
     assert np.array_equal(m.batch_votes(ex), oracle.sparse_batch_votes(banks, acts[:200]))
+
+
+def test_sparse_resident_equals_global_long_run(gpu):
+    """configs[4] shapes, 3000 documents: the shared-memory-resident trainer
+    and the global-list trainer end in byte-identical models."""
+    from paper_2405_04212_b200 import _lib
+    from paper_2405_04212_b200.sparse_train import SparseTrainSession
+    d = gpu.datasets.sparse_zipf(n_docs=3000)
+    cfg = gpu.Config(**gpu.datasets.sparse_config_kwargs(seed=4))
+    models = []
+    for mode in (1, 0):
+        _lib.call("tmb_set_option", b"sparse.resident", mode)
+        try:
+            sess = SparseTrainSession(cfg, d.indptr, d.indices, d.labels)
+            assert sess.engine.resident == bool(mode)
+            sess.run_epoch()
+            models.append((sess.model(), sess.stats_dict()))
+        finally:
+            _lib.call("tmb_set_option", b"sparse.resident", 1)
+    (a, sa), (b, sb) = models
+    assert sa == sb and sa["events"] > 0
+    assert np.array_equal(a.weights, b.weights)
+    for j in range(cfg.n_clauses):
+        assert np.array_equal(a.clause_literals[j], b.clause_literals[j]), j
+        assert np.array_equal(a.clause_states[j], b.clause_states[j]), j
 
 
 def test_cross_validate_golden(gpu):

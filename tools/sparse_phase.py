@@ -14,6 +14,7 @@ torch.cuda.synchronize()
 nc = 148
 ph = torch.zeros(nc * 8, dtype=torch.int64, device="cuda")
 _lib.call("tmb_set_option", b"sparse.phase_buffer", ph.data_ptr())
+st0 = sess.stats_dict()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 n = 20000
 a.record()
@@ -27,3 +28,9 @@ print(f"{a.elapsed_time(b) * 1e3 / n:.2f} us/doc")
 for q, name in enumerate(["loop top (act load, neg)", "eval", "votes+exchange", "flag bitmaps",
                           "events (warp 0)", "feedback merges"]):
     print(f"  {name:26s} mean {p[:, q].mean():7.3f}  max {p[:, q].max():7.3f} us/doc")
+st1 = sess.stats_dict()
+dd = {k: st1[k] - st0[k] for k in st1}
+print("  stats", dd)
+tot = ph.cpu().numpy().reshape(nc, 8).astype(float) / clk * 1e6
+print(f"  Type I merge  {tot[:, 6].sum() / max(dd['type_i'], 1):.3f} us/event  ({dd['type_i'] / n:.1f} per doc)")
+print(f"  Type II merge {tot[:, 7].sum() / max(dd['type_ii'], 1):.3f} us/event  ({dd['type_ii'] / n:.1f} per doc)")
