@@ -65,6 +65,14 @@ uint64_t tmb_launch_count(void);
 int tmb_microbench_allreduce(int n_cta, int threads, int iters, int mode,
                              double *us_per_iter);
 
+/* SparseTM event-merge microbenchmark (design evidence):
+ * one warp per CTA (n_warps warps per CTA) replays one event `reps` times on
+ * synthetic sorted lists of n stored and n_act active literals held in
+ * shared memory.  which: 0 Type I output 0, 1 Type I output 1, 2 Type II.
+ * *us_per_event = mean device time per event per warp. */
+int tmb_microbench_sparse_event(int which, int n, int n_act, int reps, int n_cta, int n_warps,
+                                double *us_per_event);
+
 /* ----------------------------------------------------- RNG (core.py) -- */
 /* core.py:66-95 on the host; used by the host driver and tests. */
 uint64_t tmb_derive_stream(uint64_t seed, uint64_t index);

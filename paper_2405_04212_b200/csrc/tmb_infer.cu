@@ -1599,7 +1599,7 @@ int tmb_set_option(const char *name, int64_t value) {
         g_train_dbg = (int)value;
         return TMB_OK;
     }
-    if (std::string(name) == "sparse.phase_buffer") {  // device uint64 [n_cta*8] or 0
+    if (std::string(name) == "sparse.phase_buffer") {  // device uint64 [n_cta*16] or 0
         g_sparse_phase = reinterpret_cast<unsigned long long *>(value);
         return TMB_OK;
     }

@@ -28,6 +28,8 @@ namespace tmb {
 
 constexpr int kMaxActive = 4096;  // active literals of one document held in smem
 constexpr int kMaxIns = 512;      // Type II insertions per event (per-warp smem)
+constexpr int kCandStage = 1024;  // leading candidates held in smem (every Type II walk
+                                  // starts at candidate 0 and stops at the capacity)
 constexpr int kStage = 1024;      // per-warp shared staging of a clause list (longer: global)
 constexpr int kPfRegs = 8;        // next document's active ids per thread (prefetch)
 
@@ -57,7 +59,7 @@ struct SparseK {
     const uint8_t *x_ut, *x_un, *x_out;
     int x_label, x_neg;
     uint64_t x_counter, x_seed;
-    unsigned long long *phase;  // optional [n_cta][8] clock64 per phase (thread 0; profiling)
+    unsigned long long *phase;  // optional [n_cta][16] clock64 profile (see kPh* below)
 };
 
 __device__ __forceinline__ int32_t *lits_of(const SparseK &k, int c, int which) {
@@ -65,6 +67,19 @@ __device__ __forceinline__ int32_t *lits_of(const SparseK &k, int c, int which) 
 }
 __device__ __forceinline__ int8_t *sts_of(const SparseK &k, int c, int which) {
     return (which ? k.sts1 : k.sts0) + (size_t)c * k.slab;
+}
+
+// number of elements < v in sorted a[0..n), when the answer is usually 0:
+// one probe, then a binary search (warp-uniform v: broadcast loads)
+__device__ __forceinline__ int count_below_gallop(const int32_t *a, int n, int32_t v) {
+    if (n <= 0 || a[0] >= v) return 0;
+    int lo = 1, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
 // number of elements < v in sorted a[0..n)
@@ -112,60 +127,175 @@ __device__ __forceinline__ void stage_list(const int32_t *L, const int8_t *S, in
     }
 }
 
-// L/S: the clause's current list (n pairs), DL/DS: the other buffer.
+// Warp-wide ranks in a sorted 32-window held one value per lane (v): the
+// number of lanes whose v is < x (or <= x), by binary lifting over shuffles.
+__device__ __forceinline__ int window_rank_lt(int32_t v, int32_t x) {
+    int r = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1)
+        if (__shfl_sync(0xffffffffu, v, r + step - 1) < x) r += step;
+    if (__shfl_sync(0xffffffffu, v, r) < x) r += 1;
+    return r;
+}
+__device__ __forceinline__ int window_rank_le(int32_t v, int32_t x) {
+    int r = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1)
+        if (__shfl_sync(0xffffffffu, v, r + step - 1) <= x) r += step;
+    if (__shfl_sync(0xffffffffu, v, r) <= x) r += 1;
+    return r;
+}
+
+// L/S: the clause's current list (n pairs), DL/DS: the other buffer;
+// scratch: 32 x u64 of warp-private shared memory.
+//
+// The merged sequence (stored first on ties) is walked 32 positions per
+// round.  A round's positions come from the next 32 stored and the next 32
+// active elements (windows loaded one per lane); each element's position in
+// the round is its window index plus its rank in the other window (two
+// interleaved 6-step shuffle searches), and the elements that land in
+// [0, 32) are scattered through `scratch` to the lane of their position.
 __device__ __forceinline__ int event_type_i(const SparseK &k, const int32_t *L, const int8_t *S,
                                             int n, int32_t *DL, int8_t *DS, const int32_t *act,
                                             int n_act, int out, uint64_t sk, int lane,
-                                            uint64_t &ndraws) {
+                                            uint64_t &ndraws, uint64_t *scratch) {
+    constexpr int32_t kInf = 0x7fffffff;
     const int total = n + n_act;
     int emitted = 0, cond_before = 0;
-    for (int base = 0; base < total; base += 32) {
-        const int d = base + lane;  // merged position
-        bool valid = d < total;
-        int32_t lit = 0;
-        int st = k.floor_;
-        bool stored = false, active = false;
-        if (valid) {
-            // i = number of stored elements among the first d merged ones
-            int lo = max(0, d - n_act), hi = min(d, n);
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (L[mid] <= act[d - 1 - mid]) lo = mid + 1;
-                else hi = mid;
-            }
-            const int i = lo, a = d - lo;
-            if (i < n && (a >= n_act || L[i] <= act[a])) {
+    if (out == 0) {
+        // Type Ib: every element can only move down, so an active literal that
+        // is not stored (state = floor) is never kept and its draw cannot
+        // matter; the merge reduces to a pass over the stored pairs, in
+        // order, each kept iff it stays above the floor.
+        for (int base = 0; base < n; base += 32) {
+            const int i = base + lane;
+            bool keep = false;
+            int32_t lit = 0;
+            int st = 0;
+            if (i < n) {
                 lit = L[i];
                 st = S[i];
-                stored = true;
-                active = a < n_act && act[a] == lit;
-            } else {
-                lit = act[a];
-                active = true;
-                if (i > 0 && L[i - 1] == lit) valid = false;  // duplicate
+                const uint64_t m = mix64(sk + kGolden * (uint64_t)(uint32_t)lit) >> 11;
+                ++ndraws;
+                if (m < k.fp.t_dec && st > k.floor_) st -= 1;
+                keep = st > k.floor_;
             }
-        }
-        bool cond = false;
-        if (valid) {
-            const uint64_t m = mix64(sk + kGolden * (uint64_t)(uint32_t)lit) >> 11;
-            ++ndraws;
-            if (out == 1 && active) {
-                if ((k.fp.boost || m < k.fp.t_inc) && st < k.smax) st += 1;
-            } else if (m < k.fp.t_dec && st > k.floor_) {
-                st -= 1;
+            int ktot;
+            const int kpre = warp_excl(keep ? 1 : 0, lane, &ktot) + emitted;
+            if (keep && kpre < k.slab) {
+                DL[kpre] = lit;
+                DS[kpre] = (int8_t)st;
             }
-            cond = st > k.floor_;
+            emitted += ktot;
         }
-        int ctot, ktot;
-        const int cpre = warp_excl(cond ? 1 : 0, lane, &ctot) + cond_before;
-        const bool keep = cond && (stored || k.capacity < 0 || cpre < k.capacity);
-        const int kpre = warp_excl(keep ? 1 : 0, lane, &ktot) + emitted;
-        if (keep && kpre < k.slab) {
-            DL[kpre] = lit;
-            DS[kpre] = (int8_t)st;
+        return emitted <= k.slab ? emitted : -1;
+    }
+    // 64 merged positions per round: stored / active windows of 64 held as two
+    // registers per lane (A = window[lane], B = window[32 + lane]); the rank of
+    // a value in a 64-window is the sum of its ranks in the two halves, so the
+    // eight shuffle searches of a round are independent and overlap.
+    int i0 = 0, a0 = 0;
+    int32_t prev_stored = -1;  // last stored literal consumed by earlier rounds
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = 0; base < total; base += 64) {
+        const int lim = min(64, total - base);
+        int32_t lw[2], aw[2];
+        int sw[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int li = i0 + 32 * h + lane, ai = a0 + 32 * h + lane;
+            lw[h] = li < n ? L[li] : kInf;
+            sw[h] = li < n ? (int)S[li] : 0;
+            aw[h] = ai < n_act ? act[ai] : kInf;
         }
-        emitted += ktot;
-        cond_before += ctot;
+        int pl[2], pa[2];
+        bool l_act[2], a_dup[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int ra = window_rank_lt(aw[0], lw[h]) + window_rank_lt(aw[1], lw[h]);
+            const int rl = window_rank_le(lw[0], aw[h]) + window_rank_le(lw[1], aw[h]);
+            const int32_t a0v = __shfl_sync(0xffffffffu, aw[0], ra & 31);
+            const int32_t a1v = __shfl_sync(0xffffffffu, aw[1], ra & 31);
+            const int32_t l0v = __shfl_sync(0xffffffffu, lw[0], (rl - 1) & 31);
+            const int32_t l1v = __shfl_sync(0xffffffffu, lw[1], (rl - 1) & 31);
+            l_act[h] = ra < 64 && (ra < 32 ? a0v : a1v) == lw[h];
+            a_dup[h] = (rl == 0 ? prev_stored : (rl <= 32 ? l0v : l1v)) == aw[h];
+            pl[h] = 32 * h + lane + ra;
+            pa[h] = 32 * h + lane + rl;
+        }
+        // entry: lit << 32 | flags << 8 | (u8)state; flags 1 stored, 2 active, 4 duplicate
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (pl[h] < lim)
+                scratch[pl[h]] = ((uint64_t)(uint32_t)lw[h] << 32) |
+                                 ((1u | (l_act[h] ? 2u : 0u)) << 8) | (uint32_t)(sw[h] & 0xff);
+            if (pa[h] < lim)
+                scratch[pa[h]] = ((uint64_t)(uint32_t)aw[h] << 32) | ((2u | (a_dup[h] ? 4u : 0u)) << 8);
+        }
+        const int nl = __popc(__ballot_sync(0xffffffffu, pl[0] < lim)) +
+                       __popc(__ballot_sync(0xffffffffu, pl[1] < lim));
+        const int na = __popc(__ballot_sync(0xffffffffu, pa[0] < lim)) +
+                       __popc(__ballot_sync(0xffffffffu, pa[1] < lim));
+        {
+            const int32_t p0 = __shfl_sync(0xffffffffu, lw[0], (nl - 1) & 31);
+            const int32_t p1 = __shfl_sync(0xffffffffu, lw[1], (nl - 1) & 31);
+            if (nl > 0) prev_stored = nl <= 32 ? p0 : p1;
+        }
+        __syncwarp();
+        int32_t lit[2];
+        int st[2];
+        bool stored[2];
+        unsigned cm[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int pos = 32 * h + lane;
+            bool valid = pos < lim, active = false;
+            lit[h] = 0;
+            st[h] = k.floor_;
+            stored[h] = false;
+            if (valid) {
+                const uint64_t e = scratch[pos];
+                const unsigned fl = (unsigned)(e >> 8) & 0xffu;
+                lit[h] = (int32_t)(e >> 32);
+                stored[h] = fl & 1u;
+                active = fl & 2u;
+                if (stored[h]) st[h] = (int)(int8_t)(e & 0xffu);
+                if (fl & 4u) valid = false;  // active duplicate of a stored literal
+            }
+            bool cond = false;
+            if (valid) {
+                const uint64_t m = mix64(sk + kGolden * (uint64_t)(uint32_t)lit[h]) >> 11;
+                ++ndraws;
+                if (active) {  // output 1
+                    if ((k.fp.boost || m < k.fp.t_inc) && st[h] < k.smax) st[h] += 1;
+                } else if (m < k.fp.t_dec && st[h] > k.floor_) {
+                    st[h] -= 1;
+                }
+                cond = st[h] > k.floor_;
+            }
+            cm[h] = __ballot_sync(0xffffffffu, cond);
+        }
+        __syncwarp();
+        i0 += nl;
+        a0 += na;
+        // keep_i = cond_i && (stored_i || #cond_true_before_i < capacity)
+        int cpre = cond_before, kpre = emitted;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const bool cond = (cm[h] >> lane) & 1u;
+            const int my_c = cpre + __popc(cm[h] & lt);
+            const bool keep = cond && (stored[h] || k.capacity < 0 || my_c < k.capacity);
+            const unsigned km = __ballot_sync(0xffffffffu, keep);
+            const int my_k = kpre + __popc(km & lt);
+            if (keep && my_k < k.slab) {
+                DL[my_k] = lit[h];
+                DS[my_k] = (int8_t)st[h];
+            }
+            cpre += __popc(cm[h]);
+            kpre += __popc(km);
+        }
+        emitted = kpre;
+        cond_before = cpre;
     }
     return emitted <= k.slab ? emitted : -1;
 }
@@ -173,22 +303,44 @@ __device__ __forceinline__ int event_type_i(const SparseK &k, const int32_t *L, 
 // Type II, output 1 (one warp): every stored pair survives (states only move
 // up from above the floor); inserted = the first non-stored, non-active
 // candidates x with #stored(<x) + #inserted(<x) < capacity, at floor + 1.
+//
+// Candidates, stored literals and active literals are all sorted, so each
+// round of 32 candidates finds its place in L and act with one uniform
+// (broadcast) binary search for the round's first candidate plus
+// shuffle ranks inside the 32-wide windows that follow; a lane whose
+// candidate lies beyond its window (more than 32 stored / active literals
+// inside one candidate round) falls back to a binary search.
 __device__ __forceinline__ int event_type_ii(const SparseK &k, const int32_t *L, const int8_t *S,
                                              int n, int32_t *DL, int8_t *DS, const int32_t *act,
-                                             int n_act, int32_t *ins_buf, int ins_cap, int lane) {
+                                             int n_act, int32_t *ins_buf, int ins_cap,
+                                             const int32_t *cand_s, int lane,
+                                             unsigned long long *pc) {
+    constexpr int32_t kInf = 0x7fffffff;
     const int cap = k.capacity;
     int ins = 0;
     bool overflow = false;
+    long long t0 = pc ? clock64() : 0;
+    int i_lo = 0, a_lo = 0;  // stored / active literals below the round's first candidate
     for (int64_t cb = 0; cb < k.n_cand; cb += 32) {
         const int64_t ci = cb + lane;
-        int32_t x = 0;
-        bool cand = false;
-        int below = 0;
-        if (ci < k.n_cand) {
-            x = __ldg(&k.cands[ci]);
-            below = count_below(L, n, x);
-            cand = !(below < n && L[below] == x) && !contains(act, n_act, x);
+        const bool real = ci < k.n_cand;
+        const int32_t x = real ? (ci < kCandStage ? cand_s[ci] : __ldg(&k.cands[ci])) : kInf;
+        const int32_t x0 = __shfl_sync(0xffffffffu, x, 0);
+        i_lo += count_below_gallop(L + i_lo, n - i_lo, x0);
+        a_lo += count_below_gallop(act + a_lo, n_act - a_lo, x0);
+        const int32_t lw = i_lo + lane < n ? L[i_lo + lane] : kInf;
+        const int32_t aw = a_lo + lane < n_act ? act[a_lo + lane] : kInf;
+        const int rl = window_rank_lt(lw, x), ra = window_rank_lt(aw, x);
+        const int32_t l_at = __shfl_sync(0xffffffffu, lw, rl & 31);
+        const int32_t a_at = __shfl_sync(0xffffffffu, aw, ra & 31);
+        int below = i_lo + rl;
+        bool stored_eq = rl < 32 && l_at == x, in_act = ra < 32 && a_at == x;
+        if (real && rl == 32) {
+            below += count_below(L + below, n - below, x);
+            stored_eq = below < n && L[below] == x;
         }
+        if (real && ra == 32) in_act = contains(act + a_lo + 32, n_act - a_lo - 32, x);
+        const bool cand = real && !stored_eq && !in_act;
         int ctot, ktot;
         const int cpre = warp_excl(cand ? 1 : 0, lane, &ctot) + ins;
         const bool keep = cand && (cap < 0 || below + cpre < cap);
@@ -199,18 +351,42 @@ __device__ __forceinline__ int event_type_ii(const SparseK &k, const int32_t *L,
             else overflow = true;
         }
         ins += ktot;
+        if (pc) pc[0] += 1;
         if (fail) break;  // monotone: every later candidate fails as well
+        // the next round starts past this round's last candidate (lower bounds)
+        i_lo = __shfl_sync(0xffffffffu, below + (stored_eq ? 1 : 0), 31);
+        a_lo = __shfl_sync(0xffffffffu, a_lo + ra + (in_act ? 1 : 0), 31);
+    }
+    if (pc) {
+        const long long t1 = clock64();
+        pc[1] += n;
+        pc[2] += ins;
+        pc[3] += t1 - t0;
     }
     __syncwarp();
     if (__any_sync(0xffffffffu, overflow) || n + ins > k.slab) return -1;
-    // stored pairs: shifted by the insertions below them
-    for (int i = lane; i < n; i += 32) {
-        const int32_t lit = L[i];
-        int st = S[i];
-        if (st < 0 && !contains(act, n_act, lit)) st += 1;
-        const int pos = i + count_below(ins_buf, ins, lit);
-        DL[pos] = lit;
-        DS[pos] = (int8_t)st;
+    // stored pairs: shifted by the insertions below them (window ranks as above)
+    const int32_t iw = lane < ins ? ins_buf[lane] : kInf;
+    a_lo = 0;
+    for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const bool real = i < n;
+        const int32_t lit = real ? L[i] : kInf;
+        const int32_t l0 = L[base];
+        a_lo += count_below_gallop(act + a_lo, n_act - a_lo, l0);
+        const int32_t aw = a_lo + lane < n_act ? act[a_lo + lane] : kInf;
+        const int ra = window_rank_lt(aw, lit);
+        const int32_t a_at = __shfl_sync(0xffffffffu, aw, ra & 31);
+        bool in_act = ra < 32 && a_at == lit;
+        if (real && ra == 32) in_act = contains(act + a_lo + 32, n_act - a_lo - 32, lit);
+        const int ib = ins <= 32 ? window_rank_lt(iw, lit) : 0;
+        if (real) {
+            int st = S[i];
+            if (st < 0 && !in_act) st += 1;
+            const int pos = i + (ins <= 32 ? ib : count_below(ins_buf, ins, lit));
+            DL[pos] = lit;
+            DS[pos] = (int8_t)st;
+        }
     }
     // insertions: shifted by the stored pairs below them
     for (int m = lane; m < ins; m += 32) {
@@ -225,6 +401,7 @@ __device__ __forceinline__ int event_type_ii(const SparseK &k, const int32_t *L,
 
 struct SSmem {
     int32_t *act;       // [2][kMaxActive] current / next document
+    int32_t *cand;      // [kCandStage] leading candidates
     int32_t *stL;       // [nwarps][kStage] staged clause literals (global-list mode)
     int8_t *stS;        // [nwarps][kStage] staged clause states
     int32_t *resL;      // [cmax][2][slab] resident clause lists (resident mode)
@@ -232,6 +409,7 @@ struct SSmem {
     int32_t *rlen;      // [cmax]
     int32_t *rcur;      // [cmax]
     int64_t *meta;      // [3][4] prefetched document: a0, a1, label, -
+    uint64_t *mscr;     // [nwarps][64] Type I merge scatter
     int32_t *ins;       // [nwarps][kMaxIns] (global-list mode; resident mode uses the
                         // source list's free tail, whose size is exactly the room left)
     uint32_t *ut_bits, *un_bits;
@@ -256,6 +434,7 @@ __host__ __device__ inline size_t sparse_smem(const SparseK &k, int nwarps, bool
     };
     SSmem t;
     t.act = (int32_t *)take(4 * 2 * kMaxActive);
+    t.cand = (int32_t *)take(4 * kCandStage);
     const size_t stage = res ? 0 : (size_t)kStage * nwarps;
     const size_t rsz = res ? (size_t)k.cmax * 2 * k.slab : 0;
     t.stL = (int32_t *)take(4 * stage);
@@ -265,6 +444,7 @@ __host__ __device__ inline size_t sparse_smem(const SparseK &k, int nwarps, bool
     t.rlen = (int32_t *)take(4 * (size_t)(res ? k.cmax : 0));
     t.rcur = (int32_t *)take(4 * (size_t)(res ? k.cmax : 0));
     t.meta = (int64_t *)take(8 * 12);
+    t.mscr = (uint64_t *)take(8 * 64 * (size_t)nwarps);
     t.ins = (int32_t *)take(res ? 0 : 4 * (size_t)kMaxIns * nwarps);
     t.ut_bits = (uint32_t *)take(4 * k.fmax_words);
     t.un_bits = (uint32_t *)take(4 * k.fmax_words);
@@ -306,6 +486,8 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
         s.blk_ctr[i] = explicit_flags ? k.x_counter : k.block_counters[b0 + i];
         s.blk_seed[i] = explicit_flags ? k.x_seed : k.block_seeds[b0 + i];
     }
+    if (tid == 0) s.misc[2] = s.misc[3] = 0;
+    for (int q = tid; q < kCandStage && q < k.n_cand; q += nthr) s.cand[q] = __ldg(&k.cands[q]);  // profile: slowest warp's event cycles this step
     // clause list accessors: (literals, states, length) of local clause j's
     // current list, and the other buffer
     const int slab = k.slab;
@@ -331,7 +513,13 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
     const bool prof = k.phase != nullptr;
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    unsigned long long ev_clk[2] = {0, 0};  // per-warp cycles in Type I / Type II merges
+    // profile slots: 0-5 phases (thread 0), 6 Type I (output 0) / 7 Type II /
+    // 8 Type I (output 1) event cycles summed over warps, 9 output-1 Type I
+    // events, 10 sum over steps of the slowest warp's event cycles
+    unsigned long long ev_clk[4] = {0, 0, 0, 0};
+    long long step_ev = 0;
+    unsigned long long crit = 0;
+    unsigned long long pc2[4] = {0, 0, 0, 0};
     long long t_mark = clock64();
 #define SPH(n)                                                            \
     do {                                                                  \
@@ -604,14 +792,22 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                 }
                 if (t1)
                     nl = event_type_i(k, L, S, n, DL, DS, act, n_act, out,
-                                      ev == 0 ? s.sk_t[j] : s.sk_n[j], lane, n_draws);
+                                      ev == 0 ? s.sk_t[j] : s.sk_n[j], lane, n_draws,
+                                      s.mscr + (size_t)warp * 64);
                 else if (RES)
                     nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
-                                       const_cast<int32_t *>(L) + n, slab - n, lane);
+                                       const_cast<int32_t *>(L) + n, slab - n, s.cand, lane,
+                                       prof ? pc2 : nullptr);
                 else
                     nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
-                                       s.ins + (size_t)warp * kMaxIns, kMaxIns, lane);
-                if (prof) ev_clk[t1 ? 0 : 1] += (unsigned long long)(clock64() - e_t0);
+                                       s.ins + (size_t)warp * kMaxIns, kMaxIns, s.cand, lane,
+                                       prof ? pc2 : nullptr);
+                if (prof) {
+                    const long long dt = clock64() - e_t0;
+                    ev_clk[t1 ? (out ? 2 : 0) : 1] += (unsigned long long)dt;
+                    if (t1 && out) ev_clk[3] += 1;
+                    step_ev += dt;
+                }
                 if (nl < 0) {
                     if (lane == 0) atomicOr(k.overflow, 1u);
                     nl = 0;
@@ -631,6 +827,8 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                 __syncwarp();
             }
         }
+        if (prof && lane == 0 && step_ev) atomicMax((unsigned long long *)&s.misc[2], (unsigned long long)step_ev);
+        step_ev = 0;
         // commit the prefetched document (read after the next step's first
         // barrier)
 #pragma unroll
@@ -649,10 +847,18 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
         }
         __syncthreads();
         SPH(5);
+        if (prof && tid == 0) {
+            unsigned long long *mx = (unsigned long long *)&s.misc[2];
+            crit += *mx;
+            *mx = 0;
+        }
     }
 #undef SPH
     if (prof && tid == 0)
-        for (int q = 0; q < 6; ++q) k.phase[rank * 8 + q] = ph[q];
+    {
+        for (int q = 0; q < 6; ++q) k.phase[rank * 16 + q] = ph[q];
+        k.phase[rank * 16 + 10] = crit;
+    }
     if (RES) {  // resident lists back to their global buffers (k.cur unchanged)
         for (int j = warp; j < cown; j += nwarps) {
             const int c = c0 + j, n = s.rlen[j], b = s.rcur[j], dst = k.cur[c];
@@ -668,8 +874,11 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
         }
     }
     if (prof && lane == 0) {
-        atomicAdd(&k.phase[rank * 8 + 6], ev_clk[0]);
-        atomicAdd(&k.phase[rank * 8 + 7], ev_clk[1]);
+        atomicAdd(&k.phase[rank * 16 + 6], ev_clk[0]);
+        atomicAdd(&k.phase[rank * 16 + 7], ev_clk[1]);
+        atomicAdd(&k.phase[rank * 16 + 8], ev_clk[2]);
+        atomicAdd(&k.phase[rank * 16 + 9], ev_clk[3]);
+        for (int q = 0; q < 4; ++q) atomicAdd(&k.phase[rank * 16 + 11 + q], pc2[q]);
     }
     for (int bi = tid; bi <= b1 - b0; bi += nthr) {
         const int b = b0 + bi;
@@ -1165,6 +1374,88 @@ int tmb_sparse_infer(const tmb_sparse *sp, const int64_t *indptr, const int32_t 
                      int64_t N, int64_t *votes, int64_t *pred, void *stream) {
     return sparse_infer_impl(sp, indptr, indices, N, votes, pred, nullptr, stream);
 }
+
+}  // extern "C"
+
+namespace tmb {
+namespace {
+// One warp per event: lists at [0, 3n) step 3 (stored) and [1, 2n_act) step 2
+// (active) so they interleave; states alternate around the floor.
+__global__ void k_sparse_event_bench(SparseK k, int which, int n, int n_act, int reps,
+                                     unsigned long long *cyc) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int slab = k.slab;
+    int32_t *act = (int32_t *)smem_raw;
+    int32_t *cand = act + kMaxActive;
+    char *wb = (char *)(cand + kCandStage) + (size_t)warp * (slab * 10 + 64 * 8 + 16);
+    int32_t *L = (int32_t *)wb, *DL = L + slab;
+    int8_t *S = (int8_t *)(DL + slab), *DS = S + slab;
+    uint64_t *scr = (uint64_t *)(((uintptr_t)(DS + slab) + 15) & ~(uintptr_t)15);
+    for (int q = threadIdx.x; q < n_act; q += blockDim.x) act[q] = 1 + 2 * q;
+    for (int q = threadIdx.x; q < kCandStage; q += blockDim.x) cand[q] = q;
+    for (int q = lane; q < n; q += 32) {
+        L[q] = 3 * q;
+        S[q] = (int8_t)(q & 1 ? k.floor_ + 1 : -1);
+    }
+    __syncthreads();
+    uint64_t nd = 0;
+    int acc = 0;
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+        int nl;
+        const uint64_t sk = 0x9E37ull * (uint64_t)(r + 1);
+        if (which == 2)
+            nl = event_type_ii(k, L, S, n, DL, DS, act, n_act, L + n, slab - n, cand, lane, nullptr);
+        else
+            nl = event_type_i(k, L, S, n, DL, DS, act, n_act, which, sk, lane, nd, scr);
+        acc += nl;
+        __syncwarp();
+    }
+    const long long t1 = clock64();
+    if (lane == 0) {
+        atomicAdd(cyc, (unsigned long long)(t1 - t0));
+        if (acc == -12345) cyc[1] = nd;  // keep the work
+    }
+}
+}  // namespace
+}  // namespace tmb
+
+extern "C" int tmb_microbench_sparse_event(int which, int n, int n_act, int reps, int n_cta,
+                                           int n_warps, double *us_per_event) {
+    int rc = require_device();
+    if (rc) return rc;
+    if (which < 0 || which > 2 || n < 1 || n > 512 || n_act < 1 || n_act > kMaxActive ||
+        reps < 1 || n_cta < 1 || n_warps < 1 || n_warps > 16 || !us_per_event)
+        return fail(TMB_E_INVALID, "microbench_sparse_event: bad arguments");
+    SparseK k{};
+    k.slab = 1024;
+    k.floor_ = -15;
+    k.smax = 127;
+    k.capacity = 64;
+    k.fp = make_fb_params(5.0, 0, -15, 127);
+    k.n_cand = kCandStage;
+    const size_t smem = 4 * (kMaxActive + kCandStage) + (size_t)n_warps * (k.slab * 10 + 64 * 8 + 16);
+    unsigned long long *cyc = nullptr;
+    TMB_CUDA(cudaMalloc(&cyc, 16));
+    cudaMemset(cyc, 0, 16);
+    cudaFuncSetAttribute((const void *)k_sparse_event_bench,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_sparse_event_bench<<<n_cta, 32 * n_warps, smem>>>(k, which, n, n_act, reps, cyc);
+    TMB_LAUNCHED();
+    unsigned long long h[2] = {0, 0};
+    cudaMemcpy(h, cyc, 16, cudaMemcpyDeviceToHost);
+    const cudaError_t e = cudaGetLastError();
+    cudaFree(cyc);
+    if (e != cudaSuccess) return fail(TMB_E_CUDA, cudaGetErrorString(e));
+    int clk_khz = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+    *us_per_event = (double)h[0] / ((double)n_cta * n_warps * reps) / (clk_khz * 1e-3);
+    return TMB_OK;
+}
+
+extern "C" {
 
 int tmb_sparse_outputs(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
                        int64_t N, uint8_t *outputs, void *stream) {
