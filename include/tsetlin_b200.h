@@ -152,7 +152,10 @@ typedef struct {
     int32_t boost;
     int32_t state_min;
     int32_t state_max;
-    int32_t flags;        /* bit 0: keep TA states in HBM even if they fit on chip */
+    int32_t flags;        /* bit 0: keep TA states in HBM even if they fit on chip;
+                             bit 1: generic grid kernel (no step records);
+                             bit 2: HBM-resident states: per-CTA feedback of the
+                             own clauses instead of the grid-balanced split */
     uint64_t seed;        /* model seed; block b uses derive_stream(seed, b) */
 } tmb_train_cfg;
 

@@ -1076,6 +1076,8 @@ int sparse_launch(tmb_sparse *sp, SparseK &k, cudaStream_t st) {
     void *args[] = {&k};
     const void *fn = sp->resident ? (const void *)k_sparse_train<true>
                                   : (const void *)k_sparse_train<false>;
+    // per-function limit: another bank of a different shape may have set it
+    TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp->smem));
     TMB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(sp->n_cta),
                                          dim3(sp->threads), args, sp->smem, st));
     TMB_LAUNCHED();

@@ -61,6 +61,15 @@ struct TrainK {
     uint64_t *block_counters;
     const uint64_t *block_seeds;
     unsigned long long *rec;   // grid mode: [n_steps][2] {arrivals:24 | biased vote sum:40}
+    // grid-balanced feedback (generic grid kernel, HBM-resident states):
+    // every CTA publishes its work list, the union is split evenly over the
+    // CTAs by quads, and the owners pull the rebuilt include masks back
+    int gbal;
+    unsigned *gsync;           // [n_steps][2] arrivals: work lists published / feedback done
+    int *gcount;               // [n_cta] work items per CTA this step
+    int *gw_clause, *gw_info;  // [n_cta][cmax] work items (global clause id, info bits)
+    uint64_t *gw_sk;           // [n_cta][cmax][2] event stream keys (target, negative)
+    uint32_t *gmask;           // [C][W] include masks of the clauses updated this step
     unsigned long long *phase;  // optional [n_cta][8] clock64 per phase (profiling)
     tmb_train_stats *stats;
     long long *trace;  // optional [n_steps][4]: negative, votes[label], votes[neg], events
@@ -111,6 +120,9 @@ struct Smem {
     unsigned long long *vsh;  // fast: [2 parity][2] shadow-time partial sums
     unsigned *wcnt;    // per-warp event counts [32]
     unsigned long long *vacc;  // grid: [2] CTA partial votes (label, negative)
+    int *gpref;                // gbal: [n_cta + 1] prefix of the published work counts
+    int *rc_clause, *rc_info;  // gbal: [cmax + 4] work items of this CTA's quad range
+    uint64_t *rc_sk;           // gbal: [cmax + 4][2]
 };
 
 // Shared-memory carve-up; identical on host (size) and device (pointers).
@@ -153,6 +165,11 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.clo = k.fast ? (long long *)take(8 * 4 * (size_t)k.cmax) : nullptr;
     t.vsh = k.fast ? (unsigned long long *)take(8 * 4) : nullptr;
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
+    const bool gb = k.gbal && !k.fast && !smem_states && mode == MODE_GRID;
+    t.gpref = gb ? (int *)take(4 * (size_t)(k.n_cta + 1)) : nullptr;
+    t.rc_clause = gb ? (int *)take(4 * (size_t)(k.cmax + 4)) : nullptr;
+    t.rc_info = gb ? (int *)take(4 * (size_t)(k.cmax + 4)) : nullptr;
+    t.rc_sk = gb ? (uint64_t *)take(16 * (size_t)(k.cmax + 4)) : nullptr;
     if (s) *s = t;
     return align_up(off, 16);
 }
@@ -297,6 +314,142 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
     }
     cn.draws += nd;
     cn.upd += nupd;
+}
+
+// Grid-balanced feedback (HBM-resident states): this CTA's share
+// [q_begin, q_end) of the quads of all CTAs' work items (the union of the
+// published work lists in CTA order; q_begin, q_end multiples of 32, so a
+// warp's 32 quads lie in one row).  rc_*[g - g_lo] hold the work items.
+// Same per-position arithmetic as feedback_quads; the rebuilt include-mask
+// words go to k.gmask for the owners to pull.
+__device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Smem &s,
+                                                      const uint32_t *lit, int64_t q_begin,
+                                                      int64_t q_end, int64_t g_lo, Counters &cn) {
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
+    const int QP = k.Ppad >> 2;
+    constexpr int B = 4;
+    const uint64_t t_inc = k.fp.t_inc, t_dec = k.fp.t_dec;
+    const int smin = k.fp.smin, smax = k.fp.smax, boost = k.fp.boost ? 1 : 0;
+    unsigned nd = 0, nupd = 0;
+    // quad it = (work item g_lo + gnext, quad rem) advanced by nthr per unit
+    // without a division (nthr < QP is not assumed: a short loop)
+    int gnext = (int)((q_begin + tid) / QP - g_lo);
+    int rnext = (int)((q_begin + tid) % QP);
+    for (int64_t it0 = q_begin + tid; it0 < q_end; it0 += (int64_t)B * nthr) {
+        uint32_t word[B];
+        int gi[B], pp[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int64_t it = it0 + (int64_t)u * nthr;
+            const int g = gnext, rem = rnext;
+            rnext += nthr;
+            while (rnext >= QP) {
+                rnext -= QP;
+                ++gnext;
+            }
+            gi[u] = -1;
+            word[u] = 0xFFFFFFFFu;
+            if (it < q_end) {
+                const int p0 = rem << 2;
+                gi[u] = g;
+                pp[u] = p0;
+                const int8_t *grow = k.states + (int64_t)s.rc_clause[gi[u]] * k.P;
+                if (k.vec4 && p0 + 4 <= k.P) {
+                    word[u] = __ldcg(reinterpret_cast<const unsigned int *>(grow + p0));
+                } else {
+                    for (int b = 0; b < 4; ++b)
+                        if (p0 + b < k.P)
+                            word[u] = (word[u] & ~(0xFFu << (8 * b))) |
+                                      ((uint32_t)(uint8_t)__ldcg(grow + p0 + b) << (8 * b));
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (it0 + (int64_t)u * nthr >= q_end) break;  // warp-uniform
+            const int g = gi[u], p0 = pp[u];
+            const int c = s.rc_clause[g];
+            const int info = s.rc_info[g];
+            const int out = (info & I_OUT) ? 1 : 0;
+            const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
+            const int lim = k.P - p0;
+            int st[4], s0[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) s0[b] = st[b] = (int)(int8_t)(word[u] >> (8 * b));
+            auto type_i = [&](uint64_t z0) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int vb = b < lim ? 1 : 0;
+                    const int inc = out & (int)((litn >> b) & 1u);
+                    const uint64_t thr = inc ? t_inc : t_dec;
+                    const int hit = (mix64(z0 + kGolden * (uint64_t)b) >> 11) < thr ? 1 : 0;
+                    const int room = st[b] < smax ? 1 : 0;
+                    const int above = st[b] > smin ? 1 : 0;
+                    nd += vb & (inc ? (room & (boost ^ 1)) : above);
+                    const int delta = (inc & room & (boost | hit)) - ((inc ^ 1) & above & hit);
+                    st[b] += vb ? delta : 0;
+                }
+            };
+            auto type_ii = [&]() {
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    st[b] += (b < lim ? 1 : 0) & out & (int)(((litn >> b) & 1u) ^ 1u) & (st[b] < 0 ? 1 : 0);
+            };
+            if (info & I_TEV) {
+                if (info & I_T1) type_i(s.rc_sk[2 * g] + kGolden * (uint64_t)p0);
+                else type_ii();
+            }
+            if (info & I_NEV) {
+                if (info & I_N1) type_i(s.rc_sk[2 * g + 1] + kGolden * (uint64_t)p0);
+                else type_ii();
+            }
+            uint32_t nib = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                nupd += st[b] != s0[b] ? 1 : 0;
+                nib |= (uint32_t)(b < lim && st[b] >= 0) << b;
+            }
+            const uint32_t nw = __byte_perm(__byte_perm((uint32_t)st[0], (uint32_t)st[1], 0x0040),
+                                            __byte_perm((uint32_t)st[2], (uint32_t)st[3], 0x0040),
+                                            0x5410);
+            if (nw != word[u]) {
+                int8_t *grow = k.states + (int64_t)c * k.P;
+                if (k.vec4 && p0 + 4 <= k.P) {
+                    __stcg(reinterpret_cast<unsigned int *>(grow + p0), nw);
+                } else {
+                    for (int b = 0; b < 4; ++b)
+                        if (p0 + b < k.P) __stcg(grow + p0 + b, (int8_t)(nw >> (8 * b)));
+                }
+            }
+            // mask word for positions 32w..32w+31: lanes 8g..8g+7 hold its nibbles
+            uint32_t m = nib << ((lane & 7) * 4);
+            m |= __shfl_xor_sync(0xffffffffu, m, 1);
+            m |= __shfl_xor_sync(0xffffffffu, m, 2);
+            m |= __shfl_xor_sync(0xffffffffu, m, 4);
+            if ((lane & 7) == 0) {
+                const int w = p0 >> 5;
+                if (w < k.W) __stcg(&k.gmask[(int64_t)c * k.W + w], m);
+            }
+        }
+    }
+    cn.draws += nd;
+    cn.upd += nupd;
+}
+
+// Grid-wide arrival + wait on a per-step counter (release / acquire; thread 0
+// spins, the CTA waits at a barrier).  Callers: __syncthreads() before.
+__device__ __forceinline__ void grid_arrive_step(unsigned *ctr) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        red_release_add(ctr, 1u);
+    }
+}
+__device__ __forceinline__ void grid_wait_step(const unsigned *ctr, unsigned want) {
+    if (threadIdx.x == 0) {
+        while (ld_acquire_u32(ctr) < want) {
+        }
+    }
+    __syncthreads();
 }
 
 // Load the model slice into shared memory, build include masks and counts.
@@ -553,6 +706,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
     long long t_mark = clock64();
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
 
+    const bool gbal = MODE == MODE_GRID && !SMEM_STATES && k.gbal;
     for (int64_t i = 0; i < k.n_steps; ++i) {
         const uint32_t *lit = (i & 1) ? s.lit1 : s.lit0;
         const int label = s.misc[8 + (int)(i % 3)];
@@ -560,6 +714,25 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         const int neg = negative_class(k, label, fbc);
         Prefetch pf;
         prefetch_issue(k, s, i, pf);
+        if (gbal && i > 0) {
+            // all CTAs' feedback of step i-1 is done: pull the include masks
+            // of the own clauses it updated, recount them
+            grid_wait_step(&k.gsync[(i - 1) * 2 + 1], (unsigned)n_cta);  // arrived below
+            const int n_prev = s.misc[0];
+            for (int q = warp; q < n_prev; q += nwarps) {
+                const int j = s.work[q];
+                const uint32_t *src = k.gmask + (int64_t)(c0 + j) * k.W;
+                int cnt = 0;
+                for (int w = lane; w < k.W; w += 32) {
+                    const uint32_t m = __ldcg(src + w);
+                    s.masks[j * k.W + w] = m;
+                    cnt += __popc(m);
+                }
+                cnt = __reduce_add_sync(0xffffffffu, cnt);
+                if (lane == 0) s.cnt[j] = cnt;
+            }
+            __syncthreads();
+        }
         // 1. training-mode outputs of own clauses (kernels/_numba.py:36-50);
         //    grid mode folds the two class sums the decision reads
         //    (dense.py:153 restricted to label / negative) into the same pass
@@ -743,9 +916,70 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         __syncthreads();
         PHASE(5);
         // 6. per-position Type I / II updates of the work list
-        feedback_quads<SMEM_STATES>(k, s, c0, lit, (k.dbg & 1) ? 0 : s.misc[0], cn);
-        prefetch_commit(k, s, i, pf);
-        __syncthreads();
+        if (gbal) {
+            // publish this CTA's work list, then take an even share of the
+            // union's quads (work items in CTA order, quads in row order)
+            const int n_work = s.misc[0];
+            for (int q = tid; q < n_work; q += nthr) {
+                const int j = s.work[q];
+                const int64_t o = (int64_t)rank * k.cmax + q;
+                __stcg(&k.gw_clause[o], c0 + j);
+                __stcg(&k.gw_info[o], s.info[j]);
+                __stcg(&k.gw_sk[2 * o], (unsigned long long)s.sk_t[j]);
+                __stcg(&k.gw_sk[2 * o + 1], (unsigned long long)s.sk_n[j]);
+            }
+            if (tid == 0) __stcg(&k.gcount[rank], n_work);
+            __syncthreads();
+            grid_arrive_step(&k.gsync[i * 2]);
+            grid_wait_step(&k.gsync[i * 2], (unsigned)n_cta);
+            if (warp == 0) {
+                int carry = 0;
+                for (int base = 0; base < n_cta; base += 32) {
+                    const int r = base + lane;
+                    const int v = r < n_cta ? __ldcg(&k.gcount[r]) : 0;
+                    int x = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (r < n_cta) s.gpref[r] = carry + x - v;
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (lane == 0) s.gpref[n_cta] = carry;
+            }
+            __syncthreads();
+            const int QP = k.Ppad >> 2;
+            const int64_t units = (int64_t)s.gpref[n_cta] * (QP >> 5);
+            const int64_t q_begin = 32 * (units * rank / n_cta);
+            const int64_t q_end = 32 * (units * (rank + 1) / n_cta);
+            const int64_t g_lo = q_begin / QP;
+            const int n_rc = q_end > q_begin ? (int)((q_end - 1) / QP - g_lo + 1) : 0;
+            for (int t = tid; t < n_rc; t += nthr) {
+                const int g = (int)(g_lo + t);
+                int lo = 0, hi = n_cta;  // owner r: gpref[r] <= g < gpref[r + 1]
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s.gpref[mid] <= g) lo = mid;
+                    else hi = mid;
+                }
+                const int64_t o = (int64_t)lo * k.cmax + (g - s.gpref[lo]);
+                s.rc_clause[t] = __ldcg(&k.gw_clause[o]);
+                s.rc_info[t] = __ldcg(&k.gw_info[o]);
+                s.rc_sk[2 * t] = __ldcg(&k.gw_sk[2 * o]);
+                s.rc_sk[2 * t + 1] = __ldcg(&k.gw_sk[2 * o + 1]);
+            }
+            __syncthreads();
+            if (!(k.dbg & 1)) feedback_quads_global(k, s, lit, q_begin, q_end, g_lo, cn);
+            prefetch_commit(k, s, i, pf);
+            __syncthreads();
+            // feedback done: the next step waits on it
+            grid_arrive_step(&k.gsync[i * 2 + 1]);
+        } else {
+            feedback_quads<SMEM_STATES>(k, s, c0, lit, (k.dbg & 1) ? 0 : s.misc[0], cn);
+            prefetch_commit(k, s, i, pf);
+            __syncthreads();
+        }
         PHASE(6);
         if (MODE == MODE_GRID) TIMELINE(i, 2);
     }
@@ -1204,6 +1438,8 @@ struct tmb_trainer {
     int64_t ring_cap = 0;
     uint32_t *recs_d = nullptr;  // fast path: step records [rec_cap][R]
     int64_t rec_cap = 0;
+    unsigned *gsync_d = nullptr;  // gbal: [ring_cap][2] step arrival counters
+    void *gbal_d = nullptr;       // gbal: gcount, gw_*, gmask in one allocation
 };
 
 namespace {
@@ -1292,6 +1528,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     k.Cp = (C + 3) / 4 * 4;
     k.R = 4 + k.Wp + 260 + 2 * k.Cp;
     k.fast = (!cluster && c.n_blocks == 1 && !(c.flags & 2) && C <= 65535) ? 1 : 0;
+    k.gbal = (!cluster && !(c.flags & 4)) ? 1 : 0;  // used by the generic grid kernel, HBM states
     if (cluster && k.cmax > 32 * 1024)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: too many clauses per CTA");
 
@@ -1357,6 +1594,26 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     k.block_seeds = t->block_seeds_d;
 
     k.states = states; k.weights = weights; k.block_counters = block_counters;
+    k.gbal = (k.gbal && !k.fast && !smem_states) ? 1 : 0;
+    if (k.gbal) {
+        const size_t n_w = (size_t)n_cta * k.cmax;
+        const size_t bytes = align_up(4 * (size_t)n_cta, 256) + 2 * align_up(4 * n_w, 256) +
+                             align_up(16 * n_w, 256) + 4 * (size_t)C * W;
+        if ((rc = check_cuda(cudaMalloc(&t->gbal_d, bytes), "cudaMalloc"))) {
+            tmb_trainer_destroy(t);
+            return rc;
+        }
+        char *b = (char *)t->gbal_d;
+        k.gcount = (int *)b;
+        b += align_up(4 * (size_t)n_cta, 256);
+        k.gw_clause = (int *)b;
+        b += align_up(4 * n_w, 256);
+        k.gw_info = (int *)b;
+        b += align_up(4 * n_w, 256);
+        k.gw_sk = (uint64_t *)b;
+        b += align_up(16 * n_w, 256);
+        k.gmask = (uint32_t *)b;
+    }
     t->k = k;
     *out = t;
     return TMB_OK;
@@ -1379,6 +1636,8 @@ int tmb_trainer_destroy(tmb_trainer *t) {
     if (t->block_seeds_d) cudaFree(t->block_seeds_d);
     if (t->ring_d) cudaFree(t->ring_d);
     if (t->recs_d) cudaFree(t->recs_d);
+    if (t->gsync_d) cudaFree(t->gsync_d);
+    if (t->gbal_d) cudaFree(t->gbal_d);
     delete t;
     return TMB_OK;
 }
@@ -1407,6 +1666,12 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     k.dbg = g_train_dbg;
     void *args[] = {&k};
     const void *fn = kernel_for(t->cluster, t->smem_states, k.fast);
+    // the dynamic shared-memory limit is a per-function attribute: another
+    // trainer of a different shape may have lowered it since create
+    TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t->smem));
+    if (k.fast && 2 * k.C > 48 * 1024)
+        TMB_CUDA(cudaFuncSetAttribute((const void *)k_step_records,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * k.C));
     if (t->cluster) {
         cudaLaunchConfig_t lc = {};
         cudaLaunchAttribute at[1];
@@ -1435,9 +1700,11 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         cudaStreamSynchronize(st);
         if (t->ring_d) cudaFree(t->ring_d);
         if (t->recs_d) cudaFree(t->recs_d);
-        t->ring_d = nullptr; t->recs_d = nullptr;
+        if (t->gsync_d) cudaFree(t->gsync_d);
+        t->ring_d = nullptr; t->recs_d = nullptr; t->gsync_d = nullptr;
         t->ring_cap = 0; t->rec_cap = 0;
         TMB_CUDA(cudaMalloc(&t->ring_d, 16 * (size_t)slots));
+        if (k.gbal) TMB_CUDA(cudaMalloc(&t->gsync_d, 8 * (size_t)slots));
         t->ring_cap = slots;
         if (k.fast) {
             TMB_CUDA(cudaMalloc(&t->recs_d, 4 * (size_t)k.R * (size_t)slots));
@@ -1452,6 +1719,10 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         k.fb_counter0 = fb_counter + (uint64_t)off * step_draws;
         k.rec = t->ring_d;
         TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 16 * (size_t)n, st));
+        if (k.gbal) {
+            k.gsync = t->gsync_d;
+            TMB_CUDA(cudaMemsetAsync(t->gsync_d, 0, 8 * (size_t)n, st));
+        }
         if (k.fast) {
             k.recs = t->recs_d;
             k_step_records<<<dim3((unsigned)n, 2), 256, 2 * (size_t)k.C, st>>>(k, t->recs_d);

@@ -115,7 +115,7 @@ class DenseTrainSession:
     def __init__(self, cfg: Config, x: np.ndarray, y: np.ndarray, n_cta: int = 0,
                  threads: int = 0, states: np.ndarray | None = None,
                  weights: np.ndarray | None = None, states_in_hbm: bool = False,
-                 flag_keys: bool = True):
+                 flag_keys: bool = True, balanced_feedback: bool = True):
         import torch
         require_device()
         self.cfg = cfg
@@ -134,7 +134,9 @@ class DenseTrainSession:
         self.set_data(x, y)
         tc = _lib.TrainCfg(F, P, C, K, cfg.n_blocks, cfg.threshold, cfg.effective_budget,
                            float(cfg.s), int(cfg.boost_true_positive), cfg.state_min,
-                           cfg.state_max, int(bool(states_in_hbm)) | (0 if flag_keys else 2),
+                           cfg.state_max,
+                           int(bool(states_in_hbm)) | (0 if flag_keys else 2) |
+                           (0 if balanced_feedback else 4),
                            cfg.seed & (2**64 - 1))
         self._h = ct.c_void_p()
         _lib.call("tmb_trainer_create", ct.byref(tc), ptr(self.states), ptr(self.weights),

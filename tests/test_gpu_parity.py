@@ -128,14 +128,15 @@ def test_train_block_layouts_vs_oracle(gpu, oracle, n_cta, n_blocks):
     y = ((x[:, 0] + x[:, 3] * 2 + x[:, 9]) % 4).astype(np.int64)
     cfg = gpu.Config(n_literals=27, n_clauses=45, n_classes=4, s=2.5, threshold=9, seed=n_cta,
                      n_blocks=n_blocks, n_literal_budget=6)
-    for hbm in (False, True):
-        sess = gpu.DenseTrainSession(cfg, x, y, n_cta=n_cta, states_in_hbm=hbm)
+    ost, _ = oracle.train(cfg, x, y, 2)
+    for hbm, bal in ((False, True), (True, True), (True, False)):
+        sess = gpu.DenseTrainSession(cfg, x, y, n_cta=n_cta, states_in_hbm=hbm,
+                                     balanced_feedback=bal)
         sess.run_epoch()
         sess.run_epoch()
         m = sess.model()
-        ost, _ = oracle.train(cfg, x, y, 2)
-        assert np.array_equal(m.states, ost.states), (n_cta, n_blocks, hbm)
-        assert np.array_equal(m.weights, ost.weights), (n_cta, n_blocks, hbm)
+        assert np.array_equal(m.states, ost.states), (n_cta, n_blocks, hbm, bal)
+        assert np.array_equal(m.weights, ost.weights), (n_cta, n_blocks, hbm, bal)
         assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64),
                               ost.block_counters)
 
@@ -171,13 +172,15 @@ def test_mnist_shaped_prefix_golden(gpu):
 @pytest.mark.parametrize("n_cta,hbm,n_blocks,keys", [
     (0, False, 5, True), (0, True, 5, True), (148, False, 5, True), (148, True, 5, True),
     (5, False, 5, True), (64, True, 5, True),
-    (148, False, 1, True), (148, True, 1, True), (148, False, 1, False), (37, False, 1, True)])
+    (148, False, 1, True), (148, True, 1, True), (148, False, 1, False), (37, False, 1, True),
+    (148, True, 1, False), (23, True, 3, True)])
 def test_mnist_shaped_longer_vs_oracle(gpu, oracle, n_cta, hbm, n_blocks, keys):
     """2 epochs over 1500 examples of the config-2 shapes against the oracle,
     in cluster mode (<= 16 CTAs, DSMEM exchange) and grid mode (cooperative
     grid, global barrier), with per-block counters via n_blocks=5, and with
     one block through both flag paths (precomputed 16-bit keys: ~180 key
-    ties resolved exactly over the run; per-CTA draws)."""
+    ties resolved exactly over the run; per-CTA draws); the generic grid
+    kernel with HBM states splits the feedback over all CTAs."""
     (tx, ty), (ex, ey) = gpu.datasets.mnist_shaped(n_train=1500, n_test=300, data_seed=3)
     kw = gpu.datasets.mnist_shaped_config_kwargs(seed=9)
     kw["n_blocks"] = n_blocks

@@ -10,6 +10,6 @@ cfg = tmb.Config(**datasets.bag_of_words_config_kwargs(seed=0))
 sess = tmb.DenseTrainSession(cfg, tx, ty)
 order = torch.from_numpy(sess.next_order().astype(np.int32)).cuda()
 sess.run_steps(order[:1000])
-sess.run_steps(order[1000:2000])
+sess.run_steps(order[1000:1300])
 torch.cuda.synchronize()
 print("ok", sess.launch)
