@@ -247,6 +247,16 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
             // computed for every position and counted / used only where the
             // reference consumes it.  Type II (:93-98) likewise.
             auto type_i = [&](uint64_t z0) {
+                if (!out) {  // warp-uniform: every position moves down w.p. 1/s
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int above = (b < lim ? 1 : 0) & (st[b] > smin ? 1 : 0);
+                        const int hit = (mix64(z0 + kGolden * (uint64_t)b) >> 11) < t_dec ? 1 : 0;
+                        nd += above;
+                        st[b] -= above & hit;
+                    }
+                    return;
+                }
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
                     const int vb = b < lim ? 1 : 0;
@@ -328,7 +338,6 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int QP = k.Ppad >> 2;
     constexpr int B = 4;
-    const uint64_t t_inc = k.fp.t_inc, t_dec = k.fp.t_dec;
     const int smin = k.fp.smin, smax = k.fp.smax, boost = k.fp.boost ? 1 : 0;
     unsigned nd = 0, nupd = 0;
     // quad it = (work item g_lo + gnext, quad rem) advanced by nthr per unit
@@ -377,12 +386,22 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
 #pragma unroll
             for (int b = 0; b < 4; ++b) s0[b] = st[b] = (int)(int8_t)(word[u] >> (8 * b));
             auto type_i = [&](uint64_t z0) {
+                if (!out) {  // warp-uniform: every position moves down w.p. 1/s
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int above = (b < lim ? 1 : 0) & (st[b] > smin ? 1 : 0);
+                        const int hit = (mix64(z0 + kGolden * (uint64_t)b) >> 11) < k.fp.t_dec ? 1 : 0;
+                        nd += above;
+                        st[b] -= above & hit;
+                    }
+                    return;
+                }
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
                     const int vb = b < lim ? 1 : 0;
-                    const int inc = out & (int)((litn >> b) & 1u);
-                    const uint64_t thr = inc ? t_inc : t_dec;
-                    const int hit = (mix64(z0 + kGolden * (uint64_t)b) >> 11) < thr ? 1 : 0;
+                    const int inc = (int)((litn >> b) & 1u);
+                    const int hit = (mix64(z0 + kGolden * (uint64_t)b) >> 11) <
+                                    (inc ? k.fp.t_inc : k.fp.t_dec) ? 1 : 0;
                     const int room = st[b] < smax ? 1 : 0;
                     const int above = st[b] > smin ? 1 : 0;
                     nd += vb & (inc ? (room & (boost ^ 1)) : above);
