@@ -12,7 +12,8 @@ import ctypes as ct
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtmb200.so")
+# TMB_LIB: an alternative build of the same library (A/B timing experiments)
+LIB_PATH = os.environ.get("TMB_LIB") or os.path.join(_HERE, "libtmb200.so")
 
 u64, i64, i32, f64, vp = ct.c_uint64, ct.c_int64, ct.c_int, ct.c_double, ct.c_void_p
 

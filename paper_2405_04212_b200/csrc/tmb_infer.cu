@@ -188,6 +188,8 @@ struct InferCK {
     const uint64_t *xb;  // bit-packed input [N][W64] (feature f = bit f%64 of word f/64), or null
     int64_t W64;
     int xb_vec16;        // 16-byte loads legal (W64 even, base 16-B aligned)
+    int eval_mode;       // k_infer_ws evaluators: 2 = loads of dead rules skipped from code
+                         // 8 on (default), 3 = same without early-exit votes, 0 = plain
 };
 
 __device__ __forceinline__ uint32_t pack8(unsigned long long q) {
@@ -205,13 +207,17 @@ __device__ __forceinline__ void mbar_arm(uint64_t *mb, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
                  "r"(bytes) : "memory");
 }
+// try_wait suspend-time hint: a waiting warp is parked until the phase
+// completes instead of re-polling (spin loops were ~16% of all issued
+// instructions of the warp-specialised inference kernel)
+constexpr uint32_t kSuspendNs = 0x989680;
 __device__ __forceinline__ void mbar_wait(uint64_t *mb, uint32_t parity) {
     uint32_t done = 0;
     do {
         asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
             " selp.u32 %0, 1, 0, p;\n}"
-            : "=r"(done) : "r"(smem_u32(mb)), "r"(parity) : "memory");
+            : "=r"(done) : "r"(smem_u32(mb)), "r"(parity), "r"(kSuspendNs) : "memory");
     } while (!done);
 }
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
@@ -226,6 +232,19 @@ __device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, uint32_t
         ::"r"(dst_cluster), "r"(src_cta), "r"(bytes), "r"(mbar_cluster) : "memory");
 }
 
+// shared-window atomic (a generic-pointer atomicAdd on a pointer derived from
+// the mbarrier area compiles to a generic ATOM, not ATOMS)
+__device__ __forceinline__ uint32_t atom_add_shared(void *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+    return old;
+}
+// predicated 16-byte shared load into v (v unchanged when !p)
+__device__ __forceinline__ void lds128_if(uint4 &v, bool p, uint32_t addr) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %4, 0;\n"
+                 " @q ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n}"
+                 : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w) : "r"((uint32_t)p), "r"(addr));
+}
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -622,8 +641,19 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 }
 
 
+// 5 warpgroups: 2 transposer warpgroups re-allocated to 128 registers per
+// thread (setmaxnreg), 3 evaluator / finalizer warpgroups to 72 (11
+// evaluator warps instead of 7 at a uniform 128: the evaluators are
+// shared-memory-latency bound and need warps more than registers)
+#ifndef TMB_WS_THREADS
+#define TMB_WS_THREADS 640
+#endif
+constexpr int kWsThreads = TMB_WS_THREADS;
+constexpr int kWsRegsT = 128;
+constexpr int kWsRegsE = kWsThreads == 768 ? 56 : kWsThreads == 640 ? 72 : 128;
+
 template <bool PACKED>
-__global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
+__global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
     // transposer warps per CTA (a multiple of kTG); the last warp finalizes,
     // the rest evaluate (11 evaluators for bit-packed input measured slower)
     constexpr int kWsT = 8;
@@ -707,6 +737,12 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
         }                                                                 \
     } while (0)
 
+    if (kWsThreads > 512) {
+        if (warp < kWsT)
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsRegsT));
+        else
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsE));
+    }
     if (PACKED && warp < kWsT) {
         // ========== transposer group, bit-packed input ==========
         // unit = 32 examples x 256 features: lane l holds 256 feature bits
@@ -832,13 +868,19 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 R[d] = acc;
             }
             bad |= ob & 0xFEFEFEFEu;
-            uint32_t recv[4];
-#pragma unroll
-            for (int sft = 0; sft < 4; ++sft) {
-                const int dd = j ^ sft;
-                const uint32_t send = dd == 0 ? R[0] : dd == 1 ? R[1] : dd == 2 ? R[2] : R[3];
-                recv[sft] = sft ? __shfl_xor_sync(0xffffffffu, send, 8 * sft) : send;
+            // R[d] <- R[d ^ j] by two masked swap stages (a select chain on
+            // the lane-dependent index compiles to divergent branches)
+            {
+                const uint32_t m1 = 0u - (uint32_t)(j & 1), m2 = 0u - (uint32_t)((j >> 1) & 1);
+                uint32_t t0 = (R[0] ^ R[1]) & m1, t1 = (R[2] ^ R[3]) & m1;
+                R[0] ^= t0; R[1] ^= t0; R[2] ^= t1; R[3] ^= t1;
+                t0 = (R[0] ^ R[2]) & m2; t1 = (R[1] ^ R[3]) & m2;
+                R[0] ^= t0; R[2] ^= t0; R[1] ^= t1; R[3] ^= t1;
             }
+            uint32_t recv[4];
+            recv[0] = R[0];
+#pragma unroll
+            for (int sft = 1; sft < 4; ++sft) recv[sft] = __shfl_xor_sync(0xffffffffu, R[sft], 8 * sft);
             // 4x4 byte transpose (word kq gathers byte kq of recv[0..3]),
             // then byte p <- byte p^j (recv[s] came from lane j^s)
             const uint32_t t0 = __byte_perm(recv[0], recv[1], 0x5140);
@@ -852,13 +894,22 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
             wq[3] = __byte_perm(__byte_perm(t2, t3, 0x7632), 0, psel);
             // store round r writes feature 4j + ((r + c16) & 3): the 32
             // lanes of one store then cover all 8 bank quads of the 16-byte
-            // rows (4-way instead of 16-way bank conflicts)
+            // rows (4-way instead of 16-way bank conflicts).  wq is rotated
+            // by c16 & 3 with masked selects (no lane-dependent indexing).
+            {
+                const uint32_t m1 = 0u - (uint32_t)(c16 & 1), m2 = 0u - (uint32_t)((c16 >> 1) & 1);
+                const uint32_t a0 = (wq[0] & ~m1) | (wq[1] & m1), a1 = (wq[1] & ~m1) | (wq[2] & m1);
+                const uint32_t a2 = (wq[2] & ~m1) | (wq[3] & m1), a3 = (wq[3] & ~m1) | (wq[0] & m1);
+                wq[0] = (a0 & ~m2) | (a2 & m2);
+                wq[1] = (a1 & ~m2) | (a3 & m2);
+                wq[2] = (a2 & ~m2) | (a0 & m2);
+                wq[3] = (a3 & ~m2) | (a1 & m2);
+            }
+            uint32_t *dst0 = mine + (size_t)(fb + 4 * j) * kTG + g;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const int kq = (r + c16) & 3;
-                const uint32_t word = kq == 0 ? wq[0] : kq == 1 ? wq[1] : kq == 2 ? wq[2] : wq[3];
-                const int64_t f = fb + 4 * j + kq;
-                if (f < qf1) mine[(size_t)f * kTG + g] = word;
+                if (fb + 4 * j + kq < qf1) dst0[kq * kTG] = wq[r];
             }
         };
         auto tile_begin = [&](int64_t it) {
@@ -1026,7 +1077,7 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
             // 64-rule chunks handed out dynamically: early exits make chunk
             // costs uneven, and a static split left the evaluator barrier
             // waiting ~0.7 us per tile for the slowest warp
-            for (int rc = ew;; ) {
+            for (int rc = ew;;) {
                 if (rc * 64 >= rloc || (k.dbg & 1)) break;
                 const int rA = rc * 64 + lane, rB = rA + 32;
                 const uint32_t lA = rA < rloc ? 0xFFFFFFFFu : 0u, lB = rB < rloc ? 0xFFFFFFFFu : 0u;
@@ -1037,16 +1088,29 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                 const uint4 hb0 = lds128(hB), hb1 = lds128(hB + 16);
                 const uint32_t wa[8] = {ha0.x, ha0.y, ha0.z, ha0.w, ha1.x, ha1.y, ha1.z, ha1.w};
                 const uint32_t wb[8] = {hb0.x, hb0.y, hb0.z, hb0.w, hb1.x, hb1.y, hb1.z, hb1.w};
+                // mode 2: rules already dead for all 128 examples skip their
+                // loads from code 8 on (fewer shared-memory wavefronts), and
+                // the first exit check is after code 8
+                const bool pred2 = k.eval_mode >= 2;
+                const bool no_exit = k.eval_mode == 3;  // all 16 head codes, no warp vote
+                uint4 xa_prev = make_uint4(0, 0, 0, 0), xb_prev = make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int grp = 0; grp < 4; ++grp) {
+                    const bool la = !pred2 || grp < 2 || (A0 | A1 | A2 | A3);
+                    const bool lb = !pred2 || grp < 2 || (B0 | B1 | B2 | B3);
 #pragma unroll
                     for (int q = 2 * grp; q < 2 * grp + 2; ++q) {
 #pragma unroll
                         for (int hh = 0; hh < 2; ++hh) {
                             const uint32_t ca = hh ? (wa[q] >> 16) : (wa[q] & 0xFFFFu);
                             const uint32_t cb = hh ? (wb[q] >> 16) : (wb[q] & 0xFFFFu);
-                            const uint4 xa = lds128(xaddr + (ca >> 1) * 16);
-                            const uint4 xb = lds128(xaddr + (cb >> 1) * 16);
+                            // a dead rule's accumulator stays 0 whatever it is
+                            // ANDed with: its load is skipped, stale registers reused
+                            uint4 xa = xa_prev, xb = xb_prev;
+                            lds128_if(xa, la, xaddr + (ca >> 1) * 16);
+                            lds128_if(xb, lb, xaddr + (cb >> 1) * 16);
+                            xa_prev = xa;
+                            xb_prev = xb;
                             const uint32_t ma = 0u - (ca & 1u), mb2 = 0u - (cb & 1u);
                             A0 &= xa.x ^ ma;
                             A1 &= xa.y ^ ma;
@@ -1058,13 +1122,15 @@ __global__ void __launch_bounds__(512, 1) k_infer_ws(InferCK k) {
                             B3 &= xb.w ^ mb2;
                         }
                     }
-                    if (!__any_sync(0xffffffffu, A0 | A1 | A2 | A3 | B0 | B1 | B2 | B3)) break;
+                    if ((!pred2 || grp > 0) && !no_exit &&
+                        !__any_sync(0xffffffffu, A0 | A1 | A2 | A3 | B0 | B1 | B2 | B3))
+                        break;
                     if ((k.dbg & 32) && grp == 1) break;  // timing experiment only
                 }
                 if ((A0 | A1 | A2 | A3) && rA < rloc) finish_rule(rA, A0, A1, A2, A3);
                 if ((B0 | B1 | B2 | B3) && rB < rloc) finish_rule(rB, B0, B1, B2, B3);
                 int nx = 0;
-                if (lane == 0) nx = nE + atomicAdd(&ectr[buf], 1);
+                if (lane == 0) nx = nE + (int)atom_add_shared(&ectr[buf], 1u);
                 rc = __shfl_sync(0xffffffffu, nx, 0);
             }
             named_sync(2, 32 * nE);
@@ -1215,6 +1281,7 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
 int g_force_generic_infer = 0;
 int g_infer_dbg = 0;
 int g_infer_ws = 1;  // tmb_set_option("infer.warp_specialized", 0|1)
+int g_infer_eval = 2;  // tmb_set_option("infer.eval_mode", 0|2|3): k_infer_ws evaluator
 extern unsigned long long *g_sparse_phase;  // tmb_sparse.cu
 extern int g_sparse_resident;                // tmb_sparse.cu
 unsigned long long *g_infer_phase = nullptr;
@@ -1284,10 +1351,12 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     k.xb = xb;
     k.W64 = W64;
     k.xb_vec16 = xb && (W64 % 2 == 0) && (reinterpret_cast<uintptr_t>(xb) % 16 == 0);
+    k.eval_mode = g_infer_eval;
+    const bool ws = k.xb || g_infer_ws;
     const void *fn = k.xb ? (const void *)k_infer_ws<true>
                    : g_infer_ws ? (const void *)k_infer_ws<false> : (const void *)k_infer_cluster;
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int threads = 512;
+    const int threads = ws ? kWsThreads : 512;
     cudaLaunchConfig_t lc = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1609,6 +1678,10 @@ int tmb_set_option(const char *name, int64_t value) {
     }
     if (std::string(name) == "infer.warp_specialized") {
         g_infer_ws = (int)value;
+        return TMB_OK;
+    }
+    if (std::string(name) == "infer.eval_mode") {
+        g_infer_eval = (int)value;
         return TMB_OK;
     }
     if (std::string(name) == "infer.debug_skip") {  // timing experiments only

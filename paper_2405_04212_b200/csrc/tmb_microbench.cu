@@ -26,6 +26,10 @@ __device__ __forceinline__ unsigned long long mb_ld(const unsigned long long *p)
 // mode 4: the trainer's protocol -- two words in one 16 B slot, both red by
 //         thread 0, warp 0 spins on a 16 B load.
 // mode 5: the two words in different 128 B lines (two loads per spin).
+// mode 6: all-gather, no atomics: every CTA stores a tagged 16 B slot
+//         (ring of 4 steps x n_cta slots); warp 0 polls all slots (lane l
+//         reads slots l, l+32, ...) until every tag matches, then sums them.
+// mode 7: mode 6 with 8 B slots (one tagged word per CTA).
 __global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
                                unsigned long long *cycles) {
     const int n = gridDim.x;
@@ -50,6 +54,43 @@ __global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
                         b = mb_ld(w1);
                     }
                 } while (a < (unsigned long long)n || b < (unsigned long long)n);
+            }
+            __syncthreads();
+            continue;
+        }
+        if (mode == 6 || mode == 7) {
+            // slots: [4][n] x (mode 6: 2 words, mode 7: 1 word)
+            const int ws = mode == 6 ? 2 : 1;
+            unsigned long long *ring = slots + (size_t)(i & 3) * n * ws;
+            const unsigned long long tag = (unsigned long long)(i + 1) << 40;
+            if (threadIdx.x == 0) {
+                unsigned long long *me = ring + (size_t)blockIdx.x * ws;
+                if (ws == 2)
+                    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(me), "l"(tag | 5),
+                                 "l"(tag | 7) : "memory");
+                else
+                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(me), "l"(tag | 5) : "memory");
+            }
+            if (threadIdx.x < 32) {
+                unsigned long long acc = 0;
+                bool done;
+                do {
+                    bool ok = true;
+                    acc = 0;
+                    for (int c = threadIdx.x; c < n; c += 32) {
+                        unsigned long long a, b = tag;
+                        if (ws == 2)
+                            asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                                         : "=l"(a), "=l"(b) : "l"(ring + 2 * c) : "memory");
+                        else
+                            a = mb_ld(ring + c);
+                        ok = ok && (a >> 40) == (tag >> 40) && (b >> 40) == (tag >> 40);
+                        acc += (a & 0xFFFFFFFFFFull) + (b & 0xFFFFFFFFFFull);
+                    }
+                    done = __all_sync(0xffffffffu, ok);
+                } while (!done);
+                for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (threadIdx.x == 0 && acc == 0) slots[0] = 1;  // keep the sum live
             }
             __syncthreads();
             continue;
@@ -90,7 +131,7 @@ extern "C" int tmb_microbench_allreduce(int n_cta, int threads, int iters, int m
     int rc = require_device();
     if (rc) return rc;
     unsigned long long *slots = nullptr, *cyc = nullptr;
-    size_t words = (size_t)iters * (mode == 2 ? 8 * 32 : 32);
+    size_t words = (mode == 6 || mode == 7) ? (size_t)8 * n_cta : (size_t)iters * (mode == 2 ? 8 * 32 : 32);
     TMB_CUDA(cudaMalloc(&slots, 8 * words));
     TMB_CUDA(cudaMalloc(&cyc, 8));
     TMB_CUDA(cudaMemset(slots, 0, 8 * words));

@@ -313,7 +313,7 @@ def test_inference_random_models_vs_oracle(gpu, oracle, n_inc, F, K):
     assert np.array_equal(pred, op)
 
 
-@pytest.mark.parametrize("kernel", ["ws", "cluster", "generic"])
+@pytest.mark.parametrize("kernel", ["ws", "ws_plain", "ws_noexit", "cluster", "generic"])
 @pytest.mark.parametrize("n_inc,F,K,C,N", [(40, 64, 3, 300, 1000), (17, 784, 10, 2001, 700),
                                            (1, 32, 32, 33, 129), (5, 1000, 2, 5000, 300)])
 def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C, N):
@@ -323,7 +323,9 @@ def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C,
     firing blocks in many tiles (votes pushed across the cluster)."""
     from paper_2405_04212_b200 import _lib
     _lib.call("tmb_set_option", b"infer.force_generic", int(kernel == "generic"))
-    _lib.call("tmb_set_option", b"infer.warp_specialized", int(kernel == "ws"))
+    _lib.call("tmb_set_option", b"infer.warp_specialized", int(kernel.startswith("ws")))
+    _lib.call("tmb_set_option", b"infer.eval_mode",
+              {"ws_plain": 0, "ws_noexit": 3}.get(kernel, 2))
     try:
         rs = np.random.default_rng(n_inc + F + K)
         # satisfiable clauses: n_inc distinct features, random polarity
@@ -358,6 +360,7 @@ def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C,
     finally:
         _lib.call("tmb_set_option", b"infer.force_generic", 0)
         _lib.call("tmb_set_option", b"infer.warp_specialized", 1)
+        _lib.call("tmb_set_option", b"infer.eval_mode", 2)
 
 
 def test_inference_ties_and_empty(gpu):

@@ -11,6 +11,8 @@ _lib.call("tmb_set_option", b"infer.warp_specialized", 0 if "--legacy" in sys.ar
 for a in sys.argv[1:]:
     if a.startswith("--dbg="):
         _lib.call("tmb_set_option", b"infer.debug_skip", int(a[6:]))
+    if a.startswith("--mode="):
+        _lib.call("tmb_set_option", b"infer.eval_mode", int(a[7:]))
 N = 1 << 20
 m = datasets.inference_model(model_seed=11)
 bank = tmb.DenseClauseBank(tmb.Config(n_literals=4096, n_clauses=10000, n_classes=10, s=2.0,

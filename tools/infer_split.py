@@ -9,6 +9,9 @@ from paper_2405_04212_b200 import _lib, datasets  # noqa: E402
 
 tmb.runtime.require_device()
 _lib.call("tmb_set_option", b"infer.warp_specialized", 0 if "--legacy" in sys.argv else 1)
+for a in sys.argv[1:]:
+    if a.startswith("--mode="):
+        _lib.call("tmb_set_option", b"infer.eval_mode", int(a[7:]))
 N = 1 << 22
 m = datasets.inference_model(model_seed=11)
 bank = tmb.DenseClauseBank(tmb.Config(n_literals=4096, n_clauses=10000, n_classes=10, s=2.0,
