@@ -83,7 +83,7 @@ __device__ __forceinline__ int type_ii(int st, int lit, int out) {
 // threshold.  The saturated ends are common once the class sums reach T and
 // would take the division's slow path (zero numerator), so they are exact
 // constants here.
-__device__ __forceinline__ uint64_t threshold_of(long long a, long long T) {
+__host__ __device__ __forceinline__ uint64_t threshold_of(long long a, long long T) {
     if (a <= 0) return 0;
     if (a >= 2 * T) return 1ull << 53;
     return prob_threshold((double)a / (2.0 * (double)T));

@@ -73,6 +73,11 @@ struct TrainK {
     unsigned long long *phase;  // optional [n_cta][8] clock64 per phase (profiling)
     tmb_train_stats *stats;
     long long *trace;  // optional [n_steps][4]: negative, votes[label], votes[neg], events
+    // fast path: update thresholds for every numerator a in [0, 2T]
+    // (threshold_of(a, T), feedback.py:33-44) -- copied to shared memory when
+    // it fits, so the decision is one lookup instead of an f64 division
+    const uint64_t *thr_tab;
+    int thr_smem;
 };
 
 // CTA owning clause c (inverse of cta_begin).
@@ -118,6 +123,7 @@ struct Smem {
     int *nout, *oflag; // fast: [2][cmax] next-example outputs; [cmax] own event flags
     long long *clo;    // fast: [2 parity][2 class][cmax] shadow-time vote contributions
     unsigned long long *vsh;  // fast: [2 parity][2] shadow-time partial sums
+    uint64_t *thr_tab;        // fast: [2T + 1] update thresholds (k.thr_smem)
     unsigned *wcnt;    // per-warp event counts [32]
     unsigned long long *vacc;  // grid: [2] CTA partial votes (label, negative)
     int *gpref;                // gbal: [n_cta + 1] prefix of the published work counts
@@ -164,6 +170,7 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.vacc = (unsigned long long *)take(8 * 2);
     t.clo = k.fast ? (long long *)take(8 * 4 * (size_t)k.cmax) : nullptr;
     t.vsh = k.fast ? (unsigned long long *)take(8 * 4) : nullptr;
+    t.thr_tab = k.fast && k.thr_smem ? (uint64_t *)take(8 * (size_t)(2 * k.T + 1)) : nullptr;
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
     const bool gb = k.gbal && !k.fast && !smem_states && mode == MODE_GRID;
     t.gpref = gb ? (int *)take(4 * (size_t)(k.n_cta + 1)) : nullptr;
@@ -1186,6 +1193,8 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
     auto REC = [&](int64_t e) { return s.rec3 + (int)(e & (kRecRing - 1)) * k.R; };
 
     load_slice<SMEM_STATES>(k, s, c0, cown);
+    if (k.thr_smem)
+        for (int64_t a = tid; a <= 2 * k.T; a += nthr) s.thr_tab[a] = k.thr_tab[a];
     if (tid == 0) {
         s.blk_ctr[0] = k.block_counters[0];
         s.blk_seed[0] = k.block_seeds[0];
@@ -1247,8 +1256,9 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                 const long long T = k.T;
                 const long long v = lane == 0 ? gl : gn;
                 const long long cv = v < -T ? -T : (v > T ? T : v);
+                const long long a = lane == 0 ? T - cv : T + cv;
                 s.thr[lane] = (k.dbg & 4) ? 0 : (k.dbg & 32) ? (1ull << 50)
-                                               : threshold_of(lane == 0 ? T - cv : T + cv, T);
+                            : k.thr_smem ? s.thr_tab[a] : threshold_of(a, T);
             }
             if (k.trace && rank == 0 && lane == 0) {
                 k.trace[i * 4 + 0] = neg;
@@ -1459,6 +1469,7 @@ struct tmb_trainer {
     int64_t rec_cap = 0;
     unsigned *gsync_d = nullptr;  // gbal: [ring_cap][2] step arrival counters
     void *gbal_d = nullptr;       // gbal: gcount, gw_*, gmask in one allocation
+    uint64_t *thr_d = nullptr;    // fast path: threshold table [2T + 1]
 };
 
 namespace {
@@ -1560,7 +1571,15 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     const size_t need_off = smem_layout(k, false, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
     // flags bit 0 forces HBM-resident states (tests the streaming path)
     const int smem_states = (need_on <= (size_t)max_smem && !(c.flags & 1)) ? 1 : 0;
-    const size_t need = smem_states ? need_on : need_off;
+    size_t need = smem_states ? need_on : need_off;
+    // fast path: the threshold table in shared memory if it fits next to
+    // everything else (it never displaces resident states)
+    if (k.fast && c.threshold <= 8192) {
+        k.thr_smem = 1;
+        const size_t with_tab = smem_layout(k, smem_states, MODE_GRID, nullptr, nullptr);
+        if (with_tab <= (size_t)max_smem) need = with_tab;
+        else k.thr_smem = 0;
+    }
     if (need > (size_t)max_smem)
         return fail(TMB_E_UNSUPPORTED,
                     "trainer_create: per-CTA include masks exceed shared memory (" +
@@ -1611,6 +1630,17 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
         return rc;
     }
     k.block_seeds = t->block_seeds_d;
+    if (k.thr_smem) {
+        std::vector<uint64_t> tab((size_t)(2 * c.threshold + 1));
+        for (int64_t a = 0; a <= 2 * c.threshold; ++a) tab[a] = threshold_of(a, c.threshold);
+        if ((rc = check_cuda(cudaMalloc(&t->thr_d, 8 * tab.size()), "cudaMalloc")) ||
+            (rc = check_cuda(cudaMemcpy(t->thr_d, tab.data(), 8 * tab.size(),
+                                        cudaMemcpyHostToDevice), "cudaMemcpy"))) {
+            tmb_trainer_destroy(t);
+            return rc;
+        }
+        k.thr_tab = t->thr_d;
+    }
 
     k.states = states; k.weights = weights; k.block_counters = block_counters;
     k.gbal = (k.gbal && !k.fast && !smem_states) ? 1 : 0;
@@ -1657,6 +1687,7 @@ int tmb_trainer_destroy(tmb_trainer *t) {
     if (t->recs_d) cudaFree(t->recs_d);
     if (t->gsync_d) cudaFree(t->gsync_d);
     if (t->gbal_d) cudaFree(t->gbal_d);
+    if (t->thr_d) cudaFree(t->thr_d);
     delete t;
     return TMB_OK;
 }
