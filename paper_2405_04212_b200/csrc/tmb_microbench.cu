@@ -30,6 +30,9 @@ __device__ __forceinline__ unsigned long long mb_ld(const unsigned long long *p)
 //         (ring of 4 steps x n_cta slots); warp 0 polls all slots (lane l
 //         reads slots l, l+32, ...) until every tag matches, then sums them.
 // mode 7: mode 6 with 8 B slots (one tagged word per CTA).
+// mode 8+q: mode 4 with q in {2, 3, 4} polling loads in flight, staggered by
+//         `spacing` cycles (a poll samples the slot ~L/2 after issue; q
+//         loads spaced L/q apart cut the detection delay from ~L to ~L/2 + L/2q).
 __global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
                                unsigned long long *cycles) {
     const int n = gridDim.x;
@@ -54,6 +57,38 @@ __global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
                         b = mb_ld(w1);
                     }
                 } while (a < (unsigned long long)n || b < (unsigned long long)n);
+            }
+            __syncthreads();
+            continue;
+        }
+        if (mode >= 10 && mode <= 12) {
+            const int q = mode - 8;
+            const long long spacing = 700 / q;
+            unsigned long long *w0 = slots + (size_t)i * 32;
+            if (threadIdx.x < 2) mb_red(threadIdx.x == 0 ? w0 : w0 + 1, 1ull);
+            if (threadIdx.x < 32) {
+                ulonglong2 v[4];
+                auto ld2 = [&](ulonglong2 &r) {
+                    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                                 : "=l"(r.x), "=l"(r.y) : "l"(w0) : "memory");
+                };
+                auto done = [&](const ulonglong2 &r) {
+                    return r.x >= (unsigned long long)n && r.y >= (unsigned long long)n;
+                };
+                for (int u = 0; u < q; ++u) {
+                    ld2(v[u]);
+                    if (u + 1 < q) {
+                        const long long t = clock64();
+                        while (clock64() - t < spacing) {}
+                    }
+                }
+                bool fin = false;
+                while (!fin) {
+                    for (int u = 0; u < q && !fin; ++u) {
+                        if (done(v[u])) fin = true;
+                        else ld2(v[u]);
+                    }
+                }
             }
             __syncthreads();
             continue;

@@ -1177,7 +1177,9 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 
 constexpr int kRecRing = 4;  // step records in shared memory (i & 3)
 
-template <bool SMEM_STATES>
+// PROF: the phase-profiling build (tools/phase_profile.py); its per-step
+// accumulators cost registers the production build cannot spare
+template <bool SMEM_STATES, bool PROF>
 __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
     extern __shared__ __align__(16) char smem_raw[];
     Smem s;
@@ -1222,8 +1224,36 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
     }
 
     Counters cn;
-    const bool prof = k.phase != nullptr;
+    const bool prof = PROF && k.phase != nullptr;
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // per-step phase deltas, flushed into ph (empty / light steps) or phh
+    // (steps with > 64 candidate flag entries) at the step's end
+    unsigned long long cur[8] = {0, 0, 0, 0, 0, 0, 0, 0}, phh[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long n_heavy = 0;
+#define PHASEF(n)                                                         \
+    do {                                                                  \
+        if (prof && warp == 0) {                                          \
+            const long long now = clock64();                              \
+            cur[n] += (unsigned long long)(now - t_mark);                 \
+            t_mark = now;                                                 \
+        }                                                                 \
+    } while (0)
+#define PHASE_FLUSH(heavy)                                                \
+    do {                                                                  \
+        if (prof && warp == 0) {                                          \
+            for (int q_ = 0; q_ < 8; ++q_) {                              \
+                if (heavy) phh[q_] += cur[q_]; else ph[q_] += cur[q_];    \
+                cur[q_] = 0;                                              \
+            }                                                             \
+            n_heavy += (heavy) ? 1 : 0;                                   \
+        }                                                                 \
+    } while (0)
+    // decision constants (loop-invariant, kept in registers): lane 0 of warp
+    // 0 turns the label sum into T - v, lane 1 the negative sum into T + v
+    const long long dec_bias = (long long)n_cta * kVoteBias;
+    const long long dec_c0 = lane == 0 ? k.T + dec_bias : k.T - dec_bias;
+    const long long dec_2T = 2 * k.T;
+    const bool dec_tab = k.thr_smem != 0, dec_dbg = (k.dbg & 36) != 0;
     long long t_mark = clock64();
     for (int64_t i = 0; i < n; ++i) {
         uint32_t *rc = REC(i);
@@ -1236,7 +1266,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
         const int label1 = more ? (int)rn[1] : 0, neg1 = more ? (int)rn[2] : 0;
         // 1. arrival (issued at the end of the previous step, or in the
         //    prologue for step 0)
-        PHASE(0);
+        PHASEF(0);
         if (warp == 0) {
             // 2. all-reduce, then the decision (feedback.py:33-53): lane 0
             //    the target threshold, lane 1 the negative one.  The whole
@@ -1248,24 +1278,27 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                 p = ld_relaxed_v2u64(&k.rec[i * 2]);
             } while ((p.x >> 40) != want || (p.y >> 40) != want);
             TIMELINE(i, 1);
-            PHASE(1);
-            const long long bias = (long long)n_cta * kVoteBias;
-            const long long gl = (long long)(p.x & ((1ull << 40) - 1)) - bias;
-            const long long gn = (long long)(p.y & ((1ull << 40) - 1)) - bias;
+            PHASEF(1);
+            // lane 0: a = T - clip(v_label), lane 1: a = T + clip(v_neg), as
+            // one add on the biased 40-bit sum and one clamp to [0, 2T]
+            // (the decision is on the critical path of every step)
             if (lane < 2) {
-                const long long T = k.T;
-                const long long v = lane == 0 ? gl : gn;
-                const long long cv = v < -T ? -T : (v > T ? T : v);
-                const long long a = lane == 0 ? T - cv : T + cv;
-                s.thr[lane] = (k.dbg & 4) ? 0 : (k.dbg & 32) ? (1ull << 50)
-                            : k.thr_smem ? s.thr_tab[a] : threshold_of(a, T);
+                const long long v40 = (long long)((lane == 0 ? p.x : p.y) & ((1ull << 40) - 1));
+                long long a = lane == 0 ? dec_c0 - v40 : dec_c0 + v40;
+                a = a < 0 ? 0 : (a > dec_2T ? dec_2T : a);
+                uint64_t th = dec_tab ? s.thr_tab[a] : threshold_of(a, dec_2T >> 1);
+                if (dec_dbg) th = (k.dbg & 4) ? 0 : (k.dbg & 32) ? (1ull << 50) : th;
+                s.thr[lane] = th;
             }
             if (k.trace && rank == 0 && lane == 0) {
+                const long long bias = (long long)n_cta * kVoteBias;
+                const long long gl = (long long)(p.x & ((1ull << 40) - 1)) - bias;
+                const long long gn = (long long)(p.y & ((1ull << 40) - 1)) - bias;
                 k.trace[i * 4 + 0] = neg;
                 k.trace[i * 4 + 1] = gl;
                 k.trace[i * 4 + 2] = gn;
             }
-            PHASE(2);
+            PHASEF(2);
         } else {
             // shadow of the all-reduce: record i+3 in flight; outputs of
             // example i into info (read by this step's events); outputs of
@@ -1297,7 +1330,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
             cp_async_wait_1();  // record i+2 landed (this thread's part); B1 publishes it
         }
         __syncthreads();
-        PHASE(3);
+        PHASEF(3);
         const uint64_t tt = s.thr[0], tn = s.thr[1];
         if ((tt | tn) == 0) {
             // both update probabilities are 0 (the example is learned): no
@@ -1314,7 +1347,8 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                 TIMELINE(i, 2);
                 if (more) TIMELINE(i + 1, 0);
             }
-            PHASE(7);
+            PHASEF(7);
+            PHASE_FLUSH(false);
             continue;
         }
         // 3. the step's events: every entry of the buckets up to the
@@ -1403,7 +1437,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
             }
         }
         __syncthreads();
-        PHASE(4);
+        PHASEF(4);
         // 6. per-position Type I / II updates of the work list, then the
         //    re-evaluation for example i+1 of the clauses they changed (with
         //    the correction of its class sums)
@@ -1411,7 +1445,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
         if (n_work > 0) {
             feedback_quads<SMEM_STATES>(k, s, c0, lit, n_work, cn);
             __syncthreads();
-            PHASE(5);
+            PHASEF(5);
             if (more) {
                 int *no = s.nout + par * k.cmax;
                 const long long *cl = s.clo + par * 2 * k.cmax;
@@ -1428,7 +1462,7 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
                 }
                 __syncthreads();
             }
-            PHASE(6);
+            PHASEF(6);
         }
         TIMELINE(i, 2);
         // 7. thread 0: class sums of example i+1 -> its arrival
@@ -1439,10 +1473,18 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
             red_relaxed_add_u64(&k.rec[(i + 1) * 2 + lane], (1ull << 40) + (unsigned long long)(v + kVoteBias));
         }
         if (more) TIMELINE(i + 1, 0);
-        PHASE(7);
+        PHASEF(7);
+        PHASE_FLUSH(ne > 64);
     }
-    if (prof && tid == 0)
+#undef PHASEF
+#undef PHASE_FLUSH
+    if (prof && tid == 0) {
         for (int q = 0; q < 8; ++q) k.phase[rank * 8 + q] = ph[q];
+        // after the timeline: heavy-step phases [n_cta][8], then counts [n_cta]
+        unsigned long long *hp = k.phase + n_cta * 8 + (size_t)kTimelineSteps * n_cta * 3;
+        for (int q = 0; q < 8; ++q) hp[rank * 8 + q] = phh[q];
+        hp[n_cta * 8 + rank] = n_heavy;
+    }
     cp_async_wait_all();
     __syncthreads();
     store_slice<SMEM_STATES>(k, s, c0, cown);
@@ -1489,12 +1531,15 @@ void per_cta_maxima(TrainK &k) {
     k.bmax = bmax;
 }
 
-const void *kernel_for(bool cluster, bool smem_states, bool fast) {
+const void *kernel_for(bool cluster, bool smem_states, bool fast, bool prof = false) {
     if (cluster)
         return smem_states ? (const void *)k_train<MODE_CLUSTER, true>
                            : (const void *)k_train<MODE_CLUSTER, false>;
     if (fast)
-        return smem_states ? (const void *)k_train_fast<true> : (const void *)k_train_fast<false>;
+        return prof ? (smem_states ? (const void *)k_train_fast<true, true>
+                                   : (const void *)k_train_fast<false, true>)
+                    : (smem_states ? (const void *)k_train_fast<true, false>
+                                   : (const void *)k_train_fast<false, false>);
     return smem_states ? (const void *)k_train<MODE_GRID, true> : (const void *)k_train<MODE_GRID, false>;
 }
 
@@ -1715,7 +1760,7 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     k.n_steps = n_steps; k.fb_counter0 = fb_counter; k.stats = stats;
     k.dbg = g_train_dbg;
     void *args[] = {&k};
-    const void *fn = kernel_for(t->cluster, t->smem_states, k.fast);
+    const void *fn = kernel_for(t->cluster, t->smem_states, k.fast, k.phase != nullptr);
     // the dynamic shared-memory limit is a per-function attribute: another
     // trainer of a different shape may have lowered it since create
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t->smem));

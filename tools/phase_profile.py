@@ -39,7 +39,7 @@ for n_cta in args.cta:
     for _ in range(args.epochs - 1):
         sess.run_epoch()
     nc = sess.launch["n_cta"]
-    ph = torch.zeros(nc * (8 + 3072), dtype=torch.int64, device="cuda")
+    ph = torch.zeros(nc * (8 + 3072 + 9), dtype=torch.int64, device="cuda")
     _lib.call("tmb_trainer_set_profile", sess._h, ptr(ph))
     _lib.call("tmb_set_option", b"train.debug_skip", args.skip)
     trace = torch.zeros(len(ty) * 4, dtype=torch.int64, device="cuda")
@@ -52,7 +52,7 @@ for n_cta in args.cta:
     torch.cuda.synchronize()
     _lib.call("tmb_set_option", b"train.debug_skip", 0)
     ms = st.elapsed_time(en)
-    tl = ph.cpu().numpy()[nc * 8:].reshape(1024, nc, 3).astype(np.float64)
+    tl = ph.cpu().numpy()[nc * 8:nc * (8 + 3072)].reshape(1024, nc, 3).astype(np.float64)
     p = ph.cpu().numpy()[:nc * 8].reshape(-1, 8).astype(np.float64) / clk_hz * 1e6 / len(ty)
     print(f"n_cta={sess.launch['n_cta']} threads={sess.launch['threads']} "
           f"smem_states={sess.launch['states_in_smem']}: {ms * 1e3 / len(ty):.2f} us/example "
@@ -61,6 +61,19 @@ for n_cta in args.cta:
         name = (NAMES if args.no_keys else NAMES_FAST)[q]
         print(f"   {name:22s} mean {p[:, q].mean():6.3f}  max {p[:, q].max():6.3f}  "
               f"cta0 {p[0, q]:6.3f} us/ex")
+    if not args.no_keys:
+        raw = ph.cpu().numpy().astype(np.float64)
+        hp = raw[nc * (8 + 3072):nc * (8 + 3072 + 8)].reshape(nc, 8)
+        nh = raw[nc * (8 + 3072 + 8):nc * (8 + 3072 + 9)]
+        nl = len(ty) - nh
+        lp = raw[:nc * 8].reshape(nc, 8)
+        print(f"   per step, warp 0 of each CTA (light / empty steps n={nl.mean():.0f}, "
+              f"heavy steps (> 64 flag entries) n={nh.mean():.0f}):")
+        for q in range(8):
+            lt = lp[:, q] / np.maximum(nl, 1) / clk_hz * 1e9
+            hv = hp[:, q] / np.maximum(nh, 1) / clk_hz * 1e9
+            print(f"     {NAMES_FAST[q]:22s} light mean {lt.mean():7.0f} ns   heavy mean {hv.mean():7.0f} "
+                  f"max {hv.max():7.0f} ns")
     if tl[:, :, 0].min() > 0:
         last = tl[:, :, 0].max(axis=1, keepdims=True)
         det = tl[:, :, 1] - last            # detection after the last arrival
