@@ -309,6 +309,39 @@ def tuning_fixture():
     save("tuning", **out)
 
 
+def search_fixture():
+    """tuning.SearchSpace parse / sample draws and a random_search ranking
+    (holdout split and cv_k variants) on a small XOR-shaped problem."""
+    from tsetlinkit.tuning import SearchSpace, random_search
+    from tsetlinkit.core import RngStream as RS
+    text = ("# comment line\n"
+            "s loguniform 1.5 6.0\n"
+            "threshold int 5 25\n"
+            "n_clauses cat 6,8,10\n"
+            "boost_true_positive cat true,false\n"
+            "state_max uniform 50 127\n")
+    space = SearchSpace.parse(text)
+    rng = RS.derive(123, 0x5EA7)
+    draws = [space.sample(rng) for _ in range(40)]
+    out = {"space_text": np.frombuffer(text.encode(), dtype=np.uint8)}
+    for name in ("s", "threshold", "n_clauses", "boost_true_positive", "state_max"):
+        out["draw_" + name] = np.array([d[name] for d in draws], dtype=np.float64)
+    rs = np.random.default_rng(23)
+    x = rs.integers(0, 2, size=(200, 6)).astype(np.uint8)
+    y = (x[:, 0] ^ x[:, 1]).astype(np.int64)
+    base = tk.Config(n_literals=6, n_clauses=8, n_classes=2, s=2.0, threshold=10, seed=0)
+    small = SearchSpace.parse("s uniform 1.5 4.0\nthreshold int 5 20\nn_clauses cat 6,10")
+    for tag, kw in (("hold", dict()), ("cv", dict(cv_k=3))):
+        trials = random_search(small, base, (x, y), n_trials=5, n_epochs=2, seed=31, **kw)
+        out[tag + "_index"] = np.array([t.index for t in trials], dtype=np.int64)
+        out[tag + "_acc"] = np.array([t.accuracy for t in trials], dtype=np.float64)
+        out[tag + "_s"] = np.array([t.config.s for t in trials], dtype=np.float64)
+        out[tag + "_T"] = np.array([t.config.threshold for t in trials], dtype=np.int64)
+        out[tag + "_C"] = np.array([t.config.n_clauses for t in trials], dtype=np.int64)
+    out["x"], out["y"] = x, y
+    save("search", **out)
+
+
 def modelio_fixture():
     """GTM1 model files written by the reference (dataio.save_model) for a
     dense bank, a sparse bank and a rule set, with the models' contents."""
@@ -345,10 +378,11 @@ def modelio_fixture():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "kernels", "feedback", "train", "noisy_xor", "mnist",
-                             "predictor", "sparse", "tuning", "modelio"]
+                             "predictor", "sparse", "tuning", "modelio", "search"]
     table = {"rng": rng_fixture, "kernels": kernel_fixture, "feedback": feedback_fixture,
              "train": train_fixture, "noisy_xor": noisy_xor_fixture,
              "mnist": mnist_prefix_fixture, "predictor": predictor_fixture,
-             "sparse": sparse_fixture, "tuning": tuning_fixture, "modelio": modelio_fixture}
+             "sparse": sparse_fixture, "tuning": tuning_fixture, "modelio": modelio_fixture,
+             "search": search_fixture}
     for name in which:
         table[name]()

@@ -602,6 +602,21 @@ def test_cross_validate_golden(gpu):
     assert np.array_equal(np.array(rep.fold_accuracies), g["cv_acc"])
 
 
+@pytest.mark.parametrize("tag", ["hold", "cv"])
+def test_random_search_golden(gpu, tag):
+    """tuning.random_search on the GPU trainer == the reference's ranked
+    trials (tuning.py:194-227), holdout and cv_k variants."""
+    g = golden("search")
+    base = gpu.Config(n_literals=6, n_clauses=8, n_classes=2, s=2.0, threshold=10, seed=0)
+    small = gpu.SearchSpace.parse("s uniform 1.5 4.0\nthreshold int 5 20\nn_clauses cat 6,10")
+    kw = {"cv_k": 3} if tag == "cv" else {}
+    trials = gpu.random_search(small, base, (g["x"], g["y"]), n_trials=5, n_epochs=2, seed=31,
+                               **kw)
+    assert [t.index for t in trials] == g[tag + "_index"].tolist()
+    assert np.array_equal([t.accuracy for t in trials], g[tag + "_acc"])
+    assert np.array_equal([t.config.s for t in trials], g[tag + "_s"])
+
+
 @pytest.mark.parametrize("F,n_inc,N", [(4096, 20, 3000), (300, 3, 1000), (128, 2, 777)])
 def test_inference_bit_packed_input(gpu, oracle, F, n_inc, N):
     """Bit-packed input (uint64 words, feature f = bit f % 64 of word f // 64)

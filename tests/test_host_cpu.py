@@ -192,3 +192,56 @@ def test_gtm1_model_files_byte_identical_to_reference(tmp_path):
             pass
         else:
             raise AssertionError("malformed file accepted")
+
+
+# ---------------------------------------------------------------- search --
+def _oracle_train(cfg, data, n_epochs):
+    from oracle import oracle
+    x, y = data
+    st, _ = oracle.train(cfg, x, y, n_epochs)
+    return st
+
+
+def _oracle_eval(st, data):
+    from oracle import oracle
+    x, y = data
+    _, pred = oracle.batch_votes(st.states, st.weights, oracle.augment_literals(x))
+    return float(np.mean(pred == np.asarray(y)))
+
+
+def test_search_space_parse_and_sample_match_reference():
+    """SearchSpace.parse / sample draws == the reference's (tuning.py:34-101)."""
+    from paper_2405_04212_b200 import RngStream, SearchSpace
+    g = np.load(os.path.join(REPO, "tests", "golden", "search.npz"))
+    space = SearchSpace.parse(bytes(g["space_text"]).decode())
+    rng = RngStream.derive(123, 0x5EA7)
+    draws = [space.sample(rng) for _ in range(40)]
+    for name in ("s", "threshold", "n_clauses", "boost_true_positive", "state_max"):
+        assert np.array_equal(np.array([d[name] for d in draws], dtype=np.float64),
+                              g["draw_" + name]), name
+    with pytest.raises(ValueError):
+        SearchSpace.parse("s uniform 3 1")
+    with pytest.raises(ValueError):
+        SearchSpace.parse("s loguniform 0 1")
+    with pytest.raises(ValueError):
+        SearchSpace.parse("s gaussian 0 1")
+
+
+@pytest.mark.parametrize("tag", ["hold", "cv"])
+def test_random_search_ranking_matches_reference(tag):
+    """random_search host logic (trial draws, coercion, holdout split, CV,
+    ranking with ties by index) with the oracle as trainer == the
+    reference's trials (tuning.py:194-227)."""
+    from paper_2405_04212_b200 import Config, SearchSpace, random_search
+    g = np.load(os.path.join(REPO, "tests", "golden", "search.npz"))
+    base = Config(n_literals=6, n_clauses=8, n_classes=2, s=2.0, threshold=10, seed=0)
+    small = SearchSpace.parse("s uniform 1.5 4.0\nthreshold int 5 20\nn_clauses cat 6,10")
+    kw = {"cv_k": 3} if tag == "cv" else {}
+    trials = random_search(small, base, (g["x"], g["y"]), n_trials=5, n_epochs=2, seed=31,
+                           train_fn=_oracle_train, evaluate_fn=_oracle_eval, **kw)
+    assert [t.index for t in trials] == g[tag + "_index"].tolist()
+    assert np.array_equal([t.accuracy for t in trials], g[tag + "_acc"])
+    assert np.array_equal([t.config.s for t in trials], g[tag + "_s"])
+    assert [t.config.threshold for t in trials] == g[tag + "_T"].tolist()
+    assert [t.config.n_clauses for t in trials] == g[tag + "_C"].tolist()
+    assert all(isinstance(t.config.threshold, int) for t in trials)

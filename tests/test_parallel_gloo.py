@@ -53,11 +53,16 @@ def _worker(rank, world, port, out_dir):
     # CV over the ranks
     rep = tuning.cross_validate(cfgs[0], (tx, ty), 3, 1, seed=5, train_fn=_oracle_train,
                                 evaluate_fn=_oracle_eval)
+    # random search: 5 trials over the ranks
+    space = tuning.SearchSpace.parse("s uniform 1.5 5.0\nthreshold int 5 20")
+    trials = tuning.random_search(space, cfgs[0], (tx, ty), n_trials=5, n_epochs=1, seed=8,
+                                  train_fn=_oracle_train, evaluate_fn=_oracle_eval)
     # sharded rows
     lo, hi = parallel.shard_range(101, world, rank)
     rows = parallel.gather_rows(np.arange(lo, hi), 101)
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), accs=np.array(accs),
-             cv=np.array(rep.fold_accuracies), folds=rep.fold_assignments, rows=rows)
+             cv=np.array(rep.fold_accuracies), folds=rep.fold_assignments, rows=rows,
+             search=np.array([[t.index, t.accuracy] for t in trials]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -67,7 +72,7 @@ def test_sweep_cv_and_sharding_over_two_gloo_ranks(tmp_path):
     mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     r0 = np.load(tmp_path / "r0.npz")
     r1 = np.load(tmp_path / "r1.npz")
-    for key in ("accs", "cv", "folds", "rows"):
+    for key in ("accs", "cv", "folds", "rows", "search"):
         assert np.array_equal(r0[key], r1[key]), key
     assert np.array_equal(r0["rows"], np.arange(101))
     # single-process reference for the same jobs
@@ -83,6 +88,10 @@ def test_sweep_cv_and_sharding_over_two_gloo_ranks(tmp_path):
     rep = tuning.cross_validate(cfgs[0], (tx, ty), 3, 1, seed=5, train_fn=_oracle_train,
                                 evaluate_fn=_oracle_eval)
     assert np.array_equal(r0["cv"], np.array(rep.fold_accuracies))
+    space = tuning.SearchSpace.parse("s uniform 1.5 5.0\nthreshold int 5 20")
+    trials = tuning.random_search(space, cfgs[0], (tx, ty), n_trials=5, n_epochs=1, seed=8,
+                                  train_fn=_oracle_train, evaluate_fn=_oracle_eval)
+    assert np.array_equal(r0["search"], np.array([[t.index, t.accuracy] for t in trials]))
 
 
 def test_shard_and_job_assignment():
