@@ -155,6 +155,15 @@ class SparseTrainSession:
                   ptr(self.stats), stream_ptr())
         self.fb_counter += n * (1 + 2 * self.cfg.n_clauses)
 
+    def run_steps_on(self, indptr_dev, indices_dev, labels_dev, order_dev):
+        """Like run_steps, on caller-provided device CSR rows / labels (a
+        batch staged by a data loader) instead of the session's own copy."""
+        n = int(order_dev.shape[0])
+        _lib.call("tmb_sparse_train", self.engine._h, ptr(indptr_dev), ptr(indices_dev),
+                  ptr(labels_dev), ptr(order_dev), n, self.fb_counter & (2 ** 64 - 1),
+                  ptr(self.stats), stream_ptr())
+        self.fb_counter += n * (1 + 2 * self.cfg.n_clauses)
+
     def run_epoch(self, max_steps=None):
         import torch
         from .executor import shuffle_permutation
