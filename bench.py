@@ -66,6 +66,32 @@ def ncu_traffic(kernel: str):
     return None, None
 
 
+def ncu_pipes(kernel: str):
+    """Pipe utilisation of `kernel` from the same committed ncu summary as
+    ncu_traffic: ALU / FMA pipe activity, issue-slot use and shared-memory
+    wavefronts, each as % of its peak (the integer-pipe roofline of a
+    kernel that is neither HBM- nor tensor-bound), or None."""
+    import glob
+    keys = {"alu_pipe_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+            "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+            "issue_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed"}
+    for f in sorted(glob.glob(os.path.join(REPO, "profiles", "*_ncu_full_summary.json")),
+                    reverse=True):
+        try:
+            data = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        for rec in data.values():
+            if kernel in rec.get("Kernel Name", ""):
+                out = {"source": os.path.basename(f), "kernel": rec["Kernel Name"]}
+                for name, key in keys.items():
+                    if key in rec:
+                        out[name] = float(rec[key].split()[0])
+                return out
+    return None
+
+
 # ---------------------------------------------------------------- infra --
 
 def dist_init():
@@ -352,6 +378,7 @@ def bench_c2_train(args, rank, world, local):
                          "frac": int_achieved / int_peak,
                          "ops_per_example": int_ops_ex,
                          "us_per_example": us_ex},
+        "pipes_ncu": ncu_pipes("k_train_fast"),
         "roofline_latency": {"bound": "one grid all-reduce per example (sequential training)",
                              "floor_us_per_example": floor.value, "achieved_us_per_example": us_ex,
                              "frac": floor.value / us_ex,
@@ -529,6 +556,7 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
                      "frac": achieved / HBM_PEAK, "traffic": tr_inf, "traffic_source": tr_inf_src,
                      "peak_source": HBM_PEAK_SRC,
                      "algorithmic_bytes_per_example": bytes_ex, "avg_launch_ms": per_launch_ms},
+        "pipes_ncu": ncu_pipes("k_infer_ws"),
         "bit_packed_input": {
             "note": "same examples and model, features as uint64 words (tmb_infer_packed); "
                     "not the reference's input format, so not the headline",
