@@ -596,6 +596,18 @@ def ct_ptr(t):
 
 # ------------------------------------------------------- c4 / c5 rows --
 
+def c4_ncu_sample():
+    """DRAM bytes per example of the generic grid trainer from the committed
+    ncu capture of tools/c4_once.py (one 1000-step launch, examples 0..999 of
+    epoch 1: more events per example than the bench's later steps, so this
+    is a traffic-per-example sample, not the bench launch)."""
+    tot, src = ncu_traffic("k_train<")
+    if tot is None:
+        return None
+    return {"dram_bytes_per_example": tot / 1000.0, "source": src,
+            "sample": "tools/c4_once.py: 1000 steps from a fresh model"}
+
+
 def bench_c4_train(args, rank, world, local):
     """configs[3]: bag-of-words CoTM training, 10^4 clauses x 2*10^4 literal
     positions (states HBM-resident, 200 MB).  Step = 5000 consecutive
@@ -704,7 +716,9 @@ def bench_c4_train(args, rank, world, local):
                      "bound": "hbm", "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
                      "frac": achieved / HBM_PEAK, "traffic": None, "peak_source": HBM_PEAK_SRC,
                      "algorithmic_bytes_per_example": bytes_ex,
-                     "avg_launch_ms": per_launch_ms},
+                     "avg_launch_ms": per_launch_ms,
+                     "traffic_ncu_sample": c4_ncu_sample()},
+        "pipes_ncu": ncu_pipes("k_train<"),
         "roofline_int": {"bound": "int (ALU+FMA issue)",
                          "achieved": int_ops_ex * step_n / (per_launch_ms / 1e3) / 1e12,
                          "peak": int_peak / 1e12, "unit": "Tops/s",
