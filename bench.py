@@ -390,7 +390,7 @@ def bench_c2_train(args, rank, world, local):
                 "path": "pinned host features/labels -> H2D -> tmb_pack_literals -> host "
                         "Fisher-Yates -> tmb_trainer_run -> D2H model"},
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         from oracle import oracle
         x_lit = oracle.augment_literals(tx)
         rate, n_done, dt = oracle_train_rate(cfg, st0, w0, c0, fb0, x_lit, ty,
@@ -572,7 +572,7 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
                 "path": f"pinned host uint8 [{n_e2e}, 4096] -> tmbh_infer (2-deep chunked "
                         "H2D/compute overlap) -> host int64 predictions"},
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         from oracle import oracle
         _, ncpu = host_desc()
         xs = xs_cpu
@@ -731,7 +731,7 @@ def bench_c4_train(args, rank, world, local):
                 "path": "pinned host features -> H2D -> tmb_pack_literals -> tmb_trainer_run "
                         "-> D2H model"},
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         from oracle import oracle
         x_lit = oracle.augment_literals(tx)
         rate, n_done, dt = oracle_train_rate(cfg, st0, w0, c0, fb0, x_lit, ty,
@@ -896,7 +896,7 @@ def bench_c5_sparse(args, rank, world, local):
                                    "traffic": None,
                                    "algorithmic_bytes_per_example": csr_bytes + 8}},
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         from oracle import oracle
         model_name, ncpu = host_desc()
         acts = [d.indices[d.indptr[i]:d.indptr[i + 1]].astype(np.int64) for i in range(200)]
