@@ -641,10 +641,13 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 }
 
 
-// 5 warpgroups: 2 transposer warpgroups re-allocated to 128 registers per
-// thread (setmaxnreg), 3 evaluator / finalizer warpgroups to 72 (11
-// evaluator warps instead of 7 at a uniform 128: the evaluators are
-// shared-memory-latency bound and need warps more than registers)
+// 5 warpgroups: warpgroups 0-1 re-allocated to 128 registers per thread
+// (setmaxnreg) -- 6 transposer warps, whose loads in flight live in
+// registers, and 2 evaluator warps -- and warpgroups 2-4 to 72 (11 more
+// evaluators and the finalizer).  13 evaluator warps instead of 7 at a
+// uniform 128: the evaluators are the bound and need warps more than
+// registers.  Transposer warps measured per 2^22 configs[2] examples:
+// 4: 8.74 ms, 5: 7.44, 6: 7.15, 7: 7.29, 8: 7.88.
 #ifndef TMB_WS_THREADS
 #define TMB_WS_THREADS 640
 #endif
@@ -656,7 +659,13 @@ template <bool PACKED>
 __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
     // transposer warps per CTA (a multiple of kTG); the last warp finalizes,
     // the rest evaluate (11 evaluators for bit-packed input measured slower)
-    constexpr int kWsT = 8;
+#ifndef TMB_WS_T
+#define TMB_WS_T 6
+#endif
+    // bit-packed input: the transposer's 32x32 warp bit transposes cost more
+    // per byte, 8 transposer warps measured best (6.8 vs 7.0 ms with 6)
+    constexpr int kWsT = PACKED ? 8 : TMB_WS_T;
+    static_assert(kWsT <= 8, "transposer warps must fit the two 128-register warpgroups");
     extern __shared__ __align__(16) char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
@@ -738,7 +747,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
     } while (0)
 
     if (kWsThreads > 512) {
-        if (warp < kWsT)
+        if (warp < 8)  // warpgroups 0-1 (transposers; evaluators if kWsT < 8)
             asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsRegsT));
         else
             asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsRegsE));
@@ -750,11 +759,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
         // transposes leave lane j with the X^T words of features fb+32q+j.
         const int units = (int)((qf1 - qf0 + 255) / 256) * kTG;
         const int nq = units > warp ? (units - warp + kWsT - 1) / kWsT : 0;
-        const int g = warp % kTG;
-        const int64_t fb0 = qf0 + (int64_t)(warp / kTG) * 256;
+        // unit U = warp + q*kWsT: example group U % kTG, feature block U / kTG
+        auto ug = [&](int q) { return (warp + q * kWsT) % kTG; };
+        auto ufb = [&](int q) { return qf0 + (int64_t)((warp + q * kWsT) / kTG) * 256; };
         auto load_p = [&](int64_t itx, int q, uint32_t (&w)[8]) {
-            const int64_t e = (cid + itx * n_clusters) * tile_n + 32 * g + lane;
-            const int64_t fb = fb0 + (int64_t)q * (kWsT / kTG) * 256;
+            const int64_t e = (cid + itx * n_clusters) * tile_n + 32 * ug(q) + lane;
+            const int64_t fb = ufb(q);
 #pragma unroll
             for (int i = 0; i < 8; ++i) w[i] = 0;
             if (e >= k.N || fb >= qf1) return;
@@ -774,7 +784,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
             }
         };
         auto finish_p = [&](const uint32_t (&w)[8], int q, uint32_t *mine) {
-            const int64_t fb = fb0 + (int64_t)q * (kWsT / kTG) * 256;
+            const int64_t fb = ufb(q);
+            const int g = ug(q);
 #pragma unroll
             for (int qq = 0; qq < 8; ++qq) {
                 const uint32_t x = warp_transpose32(w[qq], lane);
@@ -822,14 +833,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
         const int j = lane >> 3, c16 = lane & 7;
         const int units = nblk * kTG;
         const int nq = units > warp ? (units - warp + kWsT - 1) / kWsT : 0;
-        const int g = warp % kTG;  // every unit of this warp has group warp % 4
-        const int64_t fb0 = qf0 + (int64_t)(warp / kTG) * 128 + 16 * c16;
+        // unit U = warp + q*kWsT: example group U % kTG, feature block U / kTG
+        auto ug = [&](int q) { return (warp + q * kWsT) % kTG; };
+        auto ufb = [&](int q) {
+            return qf0 + (int64_t)((warp + q * kWsT) / kTG) * 128 + 16 * c16;
+        };
         const uint32_t psel = (uint32_t)(j | ((1 ^ j) << 4) | ((2 ^ j) << 8) | ((3 ^ j) << 12));
         const bool do_t = !(k.dbg & 2);
         // item (tile itx, unit q): my 8 rows x 16 bytes
         auto load_item = [&](int64_t itx, int q, uint4 (&w)[8]) {
-            const int64_t er = (cid + itx * n_clusters) * tile_n + 32 * g + 8 * j;
-            const int64_t fb = fb0 + (int64_t)q * (kWsT / kTG) * 128;
+            const int64_t er = (cid + itx * n_clusters) * tile_n + 32 * ug(q) + 8 * j;
+            const int64_t fb = ufb(q);
             if (k.vec_ok && fb + 16 <= qf1 && er + 7 < k.N) {
                 const uint8_t *src = k.x + er * F + fb;
 #pragma unroll
@@ -850,7 +864,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
             }
         };
         auto finish_item = [&](const uint4 (&w)[8], int q, uint32_t *mine) {
-            const int64_t fb = fb0 + (int64_t)q * (kWsT / kTG) * 128;
+            const int64_t fb = ufb(q);
+            const int g = ug(q);
             // bytes are 0/1 (anything else is flagged and aborts the call),
             // so OR-ing row i shifted by i builds, in byte b of R_d, the 8
             // row bits of feature 4d + b: the byte -> bit transpose is 7
