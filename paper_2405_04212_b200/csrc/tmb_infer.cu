@@ -652,8 +652,14 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 #define TMB_WS_THREADS 640
 #endif
 constexpr int kWsThreads = TMB_WS_THREADS;
-constexpr int kWsRegsT = 128;
-constexpr int kWsRegsE = kWsThreads == 768 ? 56 : kWsThreads == 640 ? 72 : 128;
+#ifndef TMB_WS_REGS_T
+#define TMB_WS_REGS_T 128
+#endif
+constexpr int kWsRegsT = TMB_WS_REGS_T;
+// the rest of the 640 x 96 pool (warpgroups 2-4)
+constexpr int kWsRegsE = kWsThreads == 768 ? 56
+                       : kWsThreads == 640 ? ((61440 - 2 * 128 * kWsRegsT) / (3 * 128)) / 8 * 8
+                                           : 128;
 
 template <bool PACKED>
 __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
