@@ -166,7 +166,7 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.rec3 = k.fast ? (uint32_t *)take(4 * 4 * (size_t)k.R) : nullptr;
     t.nout = k.fast ? (int *)take(4 * 2 * (size_t)k.cmax) : nullptr;
     t.oflag = k.fast ? (int *)take(4 * (size_t)k.cmax) : nullptr;
-    t.wcnt = (unsigned *)take(4 * 32);
+    t.wcnt = (unsigned *)take(4 * 64);  // [0, 32): per-warp prefix counts, [32, 64): totals
     t.vacc = (unsigned long long *)take(8 * 2);
     t.clo = k.fast ? (long long *)take(8 * 4 * (size_t)k.cmax) : nullptr;
     t.vsh = k.fast ? (unsigned long long *)take(8 * 4) : nullptr;
@@ -1177,10 +1177,17 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 
 constexpr int kRecRing = 4;  // step records in shared memory (i & 3)
 
+// Largest CTA of the fast trainer (more warps: more shadow evaluation and
+// feedback throughput per CTA, fewer registers per thread)
+#ifndef TMB_FAST_MAX_THREADS
+#define TMB_FAST_MAX_THREADS 512
+#endif
+constexpr int kFastMaxThreads = TMB_FAST_MAX_THREADS;
+
 // PROF: the phase-profiling build (tools/phase_profile.py); its per-step
 // accumulators cost registers the production build cannot spare
 template <bool SMEM_STATES, bool PROF>
-__global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
+__global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_fast(TrainK k) {
     extern __shared__ __align__(16) char smem_raw[];
     Smem s;
     smem_layout(k, SMEM_STATES, MODE_GRID, smem_raw, &s);
@@ -1425,12 +1432,12 @@ __global__ void __launch_bounds__(512, 1) k_train_fast(TrainK k) {
             tot = __reduce_add_sync(0xffffffffu, tot);
             if (lane == 0) {
                 s.wcnt[warp] = pre;
-                s.wcnt[16 + warp] = tot;
+                s.wcnt[32 + warp] = tot;
             }
             __syncthreads();
             if (warp == 0) {
                 unsigned pv = lane < nwarps ? s.wcnt[lane] : 0u;
-                unsigned tv = lane < nwarps ? s.wcnt[16 + lane] : 0u;
+                unsigned tv = lane < nwarps ? s.wcnt[32 + lane] : 0u;
                 pv = __reduce_add_sync(0xffffffffu, pv);
                 tv = __reduce_add_sync(0xffffffffu, tv);
                 own_events(pv, tv);
@@ -1585,7 +1592,9 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     if (!cluster && n_cta >= 256)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: grid mode supports < 256 CTAs");
     if (threads <= 0) threads = (n_cta == 1 && work <= 16384) ? 256 : 512;
-    threads = std::max(64, std::min(512, threads / 32 * 32));
+    threads = std::max(64, std::min(std::max(512, kFastMaxThreads), threads / 32 * 32));
+    if (threads > 512 && !(!cluster && c.n_blocks == 1 && !(c.flags & 2) && C <= 65535))
+        threads = 512;  // only the fast grid kernel is built for more than 512 threads
 
     if (W > kRowRegs * threads)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: literal rows wider than 4*threads words");
