@@ -684,16 +684,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
     uint4 *heads = reinterpret_cast<uint4 *>(smem_raw);
     uint32_t *xt0 = reinterpret_cast<uint32_t *>(heads + 2 * (size_t)k.rloc_max);
     uint32_t *xt1 = xt0 + (size_t)xrows * kTG;
-    int32_t *part = reinterpret_cast<int32_t *>(xt1 + (size_t)xrows * kTG);  // [32*kTG][K]
-    int32_t *inbox = part + 32 * kTG * K;                                    // [2][kCS][32][K]
+    // partial class sums, one set per X^T buffer: the evaluators of tile
+    // it+1 accumulate while the finalizer warp pushes tile it's
+    int32_t *part2 = reinterpret_cast<int32_t *>(xt1 + (size_t)xrows * kTG);  // [2][32*kTG][K]
+    int32_t *inbox = part2 + 2 * 32 * kTG * K;                                // [2][kCS][32][K]
     int32_t *iflag = inbox + 2 * kCS * 32 * K;                               // [2][kCS]
     int32_t *dirty2 = iflag + 2 * kCS;                                       // [2][kTG]
     uint64_t *mb = reinterpret_cast<uint64_t *>(
         reinterpret_cast<uintptr_t>(dirty2 + 2 * kTG + 3) & ~(uintptr_t)7);  // [8]
     uint64_t *full = mb, *empty = mb + 2, *vfull = mb + 4, *vempty = mb + 6;
-    uint64_t *efree = mb + 8, *epushed = mb + 10;  // local: evaluators -> finalizer warp
-    int32_t *pushf = reinterpret_cast<int32_t *>(mb + 12);  // [2] dirty-block masks
-    int32_t *ectr = pushf + 2;                             // [2] next rule chunk (dynamic)
+    uint64_t *efree = mb + 8;  // local: evaluators -> finalizer (tile evaluated)
+    uint64_t *pfree = mb + 10; // local: finalizer -> evaluators (partials of the buffer pushed)
+    int32_t *ectr = reinterpret_cast<int32_t *>(mb + 12);  // [2] next rule chunk (dynamic)
 
     const int r0 = (int)((int64_t)rank * k.R / kCS), r1 = (int)((int64_t)(rank + 1) * k.R / kCS);
     const int rloc = r1 - r0;
@@ -703,7 +705,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
         xt0[(size_t)F * kTG + tid] = 0xFFFFFFFFu;
         xt1[(size_t)F * kTG + tid] = 0xFFFFFFFFu;
     }
-    for (int i = tid; i < 32 * kTG * K; i += blockDim.x) part[i] = 0;
+    for (int i = tid; i < 2 * 32 * kTG * K; i += blockDim.x) part2[i] = 0;
     if (tid < 2 * kTG) dirty2[tid] = 0;
     if (tid < 2 * kCS) iflag[tid] = 0;
     if (tid < 2) ectr[tid] = 0;  // (mbarrier area is initialised below, before the cluster sync)
@@ -730,8 +732,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
         mbar_init(&vempty[1], kCS);
         mbar_init(&efree[0], 1);
         mbar_init(&efree[1], 1);
-        mbar_init(&epushed[0], 1);
-        mbar_init(&epushed[1], 1);
+        mbar_init(&pfree[0], 1);
+        mbar_init(&pfree[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cluster.sync();
@@ -1004,14 +1006,36 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
             const int64_t t = cid + it * n_clusters;
             const int buf = (int)(it & 1);
             const uint32_t par = (uint32_t)((it >> 1) & 1);
-            // forward the evaluators' "buffer free" to the 4 transposer groups
+            // the evaluators are done with tile it (part / dirty of buffer buf
+            // are final): push the partial sums of example block b to owner
+            // b's inbox slot `buf` once the owners consumed that slot (tile
+            // it-2) -- the evaluators move on to tile it+1 meanwhile
             mbar_wait(&efree[buf], par);
+            // X^T buffer `buf` is free as far as this CTA is concerned:
+            // forward to all four transposer groups at once (the partials
+            // have their own release, pfree, below)
             if (lane < kCS) mbar_arrive_remote_relaxed(mapa_u32(smem_u32(&empty[buf]), lane));
+            int32_t *pbuf = part2 + buf * 32 * kTG * K;
+            int32_t *dbuf = dirty2 + buf * kTG;
+            const int pm = dbuf[0] | (dbuf[1] << 1) | (dbuf[2] << 2) | (dbuf[3] << 3);
+            if (it >= 2) mbar_wait(&vempty[buf], (uint32_t)(((it >> 1) + 1) & 1));
+            if (pm) {
+                for (int i = lane; i < 32 * kTG * K; i += 32) {
+                    const int b = i / (32 * K);
+                    if (!((pm >> b) & 1)) continue;
+                    const int rem = i - b * 32 * K;
+                    int32_t *dst = cluster.map_shared_rank(inbox, b);
+                    dst[((buf * kCS + rank) * 32) * K + rem] = pbuf[i];
+                    pbuf[i] = 0;
+                }
+                if (lane < kCS && ((pm >> lane) & 1))
+                    cluster.map_shared_rank(iflag, lane)[buf * kCS + rank] = (int)(it + 1);  // tile tag
+            }
+            if (lane < kTG) dbuf[lane] = 0;  // next used by tile it+2
+            __syncwarp();
+            if (lane == 0) mbar_arrive_local(&pfree[buf]);  // tile it+2's evaluators may accumulate
             // forward "partials pushed" to the 4 owners; blocks that received
-            // partials need a releasing arrival (the pushes are the
-            // evaluators' DSMEM stores, observed here through epushed)
-            mbar_wait(&epushed[buf], par);
-            const int pm = pushf[buf];
+            // partials need a releasing arrival (this warp's DSMEM stores)
             if (lane < kCS) {
                 const uint32_t vb = mapa_u32(smem_u32(&vfull[buf]), lane);
                 if ((pm >> lane) & 1) mbar_arrive_remote(vb);
@@ -1058,10 +1082,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
             const int buf = (int)(it & 1);
             const uint32_t *xt = buf ? xt1 : xt0;
             int32_t *dirty = dirty2 + buf * kTG;
+            int32_t *part = part2 + buf * 32 * kTG * K;
             WPH(6);
             // the peers' quarters arrive by bulk copy (complete_tx), so the
             // phase completion makes them visible: CTA-scope wait
             mbar_wait(&full[buf], (uint32_t)((it >> 1) & 1));
+            // the finalizer has pushed (and zeroed) tile it-2's partials of
+            // this buffer -- normally long before the transposers are done
+            if (it >= 2) mbar_wait(&pfree[buf], (uint32_t)(((it >> 1) + 1) & 1));
             WPH(4);
             const uint32_t xaddr = smem_u32(xt);
             // a rule's tail codes (CSR, global) and its votes into part[]
@@ -1155,32 +1183,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
                 rc = __shfl_sync(0xffffffffu, nx, 0);
             }
             named_sync(2, 32 * nE);
-            if (etid == 0) ectr[buf] = 0;  // next used by tile it+2
             WPH(5);
-            // buffer `buf` is free as far as this CTA is concerned; the
-            // finalizer warp forwards it to all four transposer groups (a
-            // remote arrival stalls the issuing warp ~0.7 us)
-            if (etid == 0) mbar_arrive_local(&efree[buf]);
-            // push the partial sums of example block b to owner b's inbox
-            // slot `buf` once the owners consumed slot `buf` of tile it-2
-            WPH(6);
-            if (it >= 2) mbar_wait(&vempty[buf], (uint32_t)(((it >> 1) + 1) & 1));
-            WPH(7);
-            const bool anyd = dirty[0] | dirty[1] | dirty[2] | dirty[3];
-            for (int i = etid; anyd && i < 32 * kTG * K; i += 32 * nE) {
-                const int b = i / (32 * K);
-                if (!dirty[b]) continue;
-                const int rem = i - b * 32 * K;
-                int32_t *dst = cluster.map_shared_rank(inbox, b);
-                dst[((buf * kCS + rank) * 32) * K + rem] = part[i];
-                part[i] = 0;
+            // tile it is evaluated: the finalizer warp pushes its partials
+            // and forwards the buffer to the transposers (a remote arrival
+            // stalls the issuing warp ~0.7 us), the evaluators go on to tile
+            // it+1
+            if (etid == 0) {
+                ectr[buf] = 0;  // next used by tile it+2
+                mbar_arrive_local(&efree[buf]);
             }
-            if (etid < kCS && dirty[etid])
-                cluster.map_shared_rank(iflag, etid)[buf * kCS + rank] = (int)(it + 1);  // tile tag
-            if (etid == 0) pushf[buf] = dirty[0] | (dirty[1] << 1) | (dirty[2] << 2) | (dirty[3] << 3);
-            named_sync(2, 32 * nE);
-            if (etid == 0) mbar_arrive_local(&epushed[buf]);  // forwarded as vfull arrivals
-            if (etid < kTG) dirty[etid] = 0;  // next used by tile it+2
             WPH(7);
         }
     }
@@ -1357,9 +1368,10 @@ static int launch_infer_cluster(const tmb_rules *r, const uint8_t *x, int64_t N,
     int max_smem = 0;
     TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const int64_t rloc_max = (r->R + kCS - 1) / kCS;
+    const bool ws_kernel = xb || g_infer_ws;
     const size_t smem = 32 * (size_t)rloc_max + 2 * 4 * (size_t)(r->F + 1) * kTG +
-                        4 * (size_t)32 * kTG * r->K + 4 * (size_t)2 * kCS * 32 * r->K +
-                        4 * (2 * kCS + 2 * kTG) + 176;
+                        (ws_kernel ? 2 : 1) * 4 * (size_t)32 * kTG * r->K +
+                        4 * (size_t)2 * kCS * 32 * r->K + 4 * (2 * kCS + 2 * kTG) + 176;
     if (smem > (size_t)max_smem) return TMB_OK;  // generic kernel instead
     InferCK k;
     k.x = x; k.N = N; k.F = r->F; k.heads = r->heads; k.tail_ptr = r->tail_ptr; k.tails = r->tails;
