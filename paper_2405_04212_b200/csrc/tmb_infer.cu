@@ -719,8 +719,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
     const int64_t qf0 = (int64_t)ch0 * 32;
     const int64_t qf1 = std::min<int64_t>((int64_t)ch1 * 32, F);
     const int nblk = (int)((qf1 - qf0 + 127) / 128);
-    const uint32_t my_bytes = (uint32_t)((qf1 > qf0 ? qf1 - qf0 : 0) * 16);
-    const uint32_t expect_bytes = (uint32_t)(F * 16) - my_bytes;
+    // debug bit 64 (timing experiment only, wrong results): no peer copies
+    const uint32_t my_bytes = (k.dbg & 64) ? 0u : (uint32_t)((qf1 > qf0 ? qf1 - qf0 : 0) * 16);
+    const uint32_t expect_bytes = (k.dbg & 64) ? 0u : (uint32_t)(F * 16) - my_bytes;
     if (tid == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
@@ -730,8 +731,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
         mbar_init(&vfull[1], kCS);
         mbar_init(&vempty[0], kCS);
         mbar_init(&vempty[1], kCS);
-        mbar_init(&efree[0], 1);
-        mbar_init(&efree[1], 1);
+        mbar_init(&efree[0], nE);  // every evaluator warp arrives when its chunks are done
+        mbar_init(&efree[1], nE);
         mbar_init(&pfree[0], 1);
         mbar_init(&pfree[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -949,7 +950,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
             named_sync(1, 32 * kWsT);
             if (tid == 0) {
                 // my quarter to the 3 peers (complete_tx on their full[buf]),
-                // then my own arrival (+ the bytes the peers will send me)
+                // then my own arrival (+ the bytes the peers will send me).
+                // (Copying each feature block as soon as a round of units
+                // completes it needs a transposer barrier per round, which
+                // stalls the load pipeline: 9.1 vs 7.0 ms, measured.)
                 if (my_bytes) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     const uint32_t src = smem_u32(mine + (size_t)qf0 * kTG);
@@ -1076,7 +1080,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
         }
     } else {
         // ================= evaluator group =================
-        const int ew = warp - kWsT, etid = tid - 32 * kWsT;
+        const int ew = warp - kWsT;
         const uint32_t haddr = smem_u32(heads);
         for (int64_t it = 0; it < n_my; ++it) {
             const int buf = (int)(it & 1);
@@ -1126,6 +1130,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
             // 64-rule chunks handed out dynamically: early exits make chunk
             // costs uneven, and a static split left the evaluator barrier
             // waiting ~0.7 us per tile for the slowest warp
+            const int n_chunks = (rloc + 63) / 64;
+            const uint32_t ebase = (uint32_t)(it >> 1) * (uint32_t)n_chunks;
             for (int rc = ew;;) {
                 if (rc * 64 >= rloc || (k.dbg & 1)) break;
                 const int rA = rc * 64 + lane, rB = rA + 32;
@@ -1179,19 +1185,21 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
                 if ((A0 | A1 | A2 | A3) && rA < rloc) finish_rule(rA, A0, A1, A2, A3);
                 if ((B0 | B1 | B2 | B3) && rB < rloc) finish_rule(rB, B0, B1, B2, B3);
                 int nx = 0;
-                if (lane == 0) nx = nE + (int)atom_add_shared(&ectr[buf], 1u);
+                // ectr[buf] is never reset: each use of the buffer advances it
+                // by exactly n_chunks (one atomic per evaluated chunk), so use
+                // u = it >> 1 numbers its chunks from u * n_chunks
+                if (lane == 0) nx = nE + (int)(atom_add_shared(&ectr[buf], 1u) - ebase);
                 rc = __shfl_sync(0xffffffffu, nx, 0);
             }
-            named_sync(2, 32 * nE);
             WPH(5);
-            // tile it is evaluated: the finalizer warp pushes its partials
+            // this warp's share of tile it is evaluated: arrive (releasing its
+            // lanes' partial-sum atomics, ordered by the warp barrier) and go
+            // on to tile it+1 without waiting for the other evaluator warps.
+            // When all have arrived, the finalizer warp pushes the partials
             // and forwards the buffer to the transposers (a remote arrival
-            // stalls the issuing warp ~0.7 us), the evaluators go on to tile
-            // it+1
-            if (etid == 0) {
-                ectr[buf] = 0;  // next used by tile it+2
-                mbar_arrive_local(&efree[buf]);
-            }
+            // stalls the issuing warp ~0.7 us).
+            __syncwarp();
+            if (lane == 0) mbar_arrive_local(&efree[buf]);
             WPH(7);
         }
     }
