@@ -645,3 +645,22 @@ def test_inference_bit_packed_input(gpu, oracle, F, n_inc, N):
     pred = torch.empty(N, dtype=torch.int64, device="cuda")
     model.infer_device_packed(xd, pred_dev=pred)
     assert np.array_equal(pred.cpu().numpy(), op)
+
+
+def test_configs1_three_full_epochs_vs_oracle(gpu):
+    """The bench workload itself: 3 full configs[1] epochs (180 000 examples,
+    2000 clauses x 1568 literal positions x 10 classes, T=5000, s=10) through
+    the production fused trainer == the oracle's model, RNG counters and
+    shuffle position after the same 3 epochs (tests/golden/c2_epoch3.npz,
+    written by tests/golden/make_c2_epoch3.py)."""
+    g = golden("c2_epoch3")
+    (tx, ty), _ = gpu.datasets.mnist_shaped(data_seed=7)
+    cfg = gpu.Config(**gpu.datasets.mnist_shaped_config_kwargs(seed=0))
+    sess = gpu.DenseTrainSession(cfg, tx, ty)
+    for _ in range(3):
+        sess.run_epoch()
+    states, weights, counters, fb, sh = sess.snapshot()
+    assert np.array_equal(states.cpu().numpy(), g["states"])
+    assert np.array_equal(weights.cpu().numpy(), g["weights"])
+    assert np.array_equal(counters.cpu().numpy().view(np.uint64), g["block_counters"])
+    assert fb == int(g["fb_counter"]) and sh == int(g["shuffle_counter"])
