@@ -642,12 +642,13 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 
 
 // 5 warpgroups: warpgroups 0-1 re-allocated to 128 registers per thread
-// (setmaxnreg) -- 6 transposer warps, whose loads in flight live in
-// registers, and 2 evaluator warps -- and warpgroups 2-4 to 72 (11 more
-// evaluators and the finalizer).  13 evaluator warps instead of 7 at a
-// uniform 128: the evaluators are the bound and need warps more than
-// registers.  Transposer warps measured per 2^22 configs[2] examples:
-// 4: 8.74 ms, 5: 7.44, 6: 7.15, 7: 7.29, 8: 7.88.
+// (setmaxnreg) -- 7 transposer warps, whose loads in flight live in
+// registers, and 1 evaluator warp -- and warpgroups 2-4 to 72 (11 more
+// evaluators and the finalizer).  12 evaluator warps instead of 7 at a
+// uniform 128.  Transposer warps measured per 2^22 configs[2] examples with
+// the evaluators' tile barrier: 4: 8.74 ms, 5: 7.44, 6: 7.15, 7: 7.29,
+// 8: 7.88; after the push moved to the finalizer and the barrier went:
+// 6: 7.06, 7: 7.01, 8: 7.16.
 #ifndef TMB_WS_THREADS
 #define TMB_WS_THREADS 640
 #endif
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_infer_ws(InferCK k) {
     // transposer warps per CTA (a multiple of kTG); the last warp finalizes,
     // the rest evaluate (11 evaluators for bit-packed input measured slower)
 #ifndef TMB_WS_T
-#define TMB_WS_T 6
+#define TMB_WS_T 7
 #endif
     // bit-packed input: the transposer's 32x32 warp bit transposes cost more
     // per byte, 8 transposer warps measured best (6.8 vs 7.0 ms with 6)
