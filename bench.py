@@ -407,29 +407,129 @@ def bench_c2_train(args, rank, world, local):
     return line
 
 
+# ------------------------------------------------------- c1 training --
+
+def bench_c1_train(args, rank, world, local):
+    """configs[0]: Noisy-XOR CoTM (12 features, 10 clauses, 2 classes, T=15,
+    s=3.9), 5000 training examples, 20 epochs.  Step = one complete 20-epoch
+    training of one model seed (seeds 0..4 in turn; 100 000 examples); the
+    timed region is the 20 fused-kernel launches of each step (epoch orders
+    from the host shuffle precomputed).  e2e = the public
+    train(cfg, train, eval, n_epochs=20) call per step (H2D of the data,
+    per-epoch test accuracy, D2H of the model).  N > 1: replicas."""
+    import torch
+
+    import paper_2405_04212_b200 as tmb
+    from paper_2405_04212_b200 import _lib, datasets
+    (tx, ty), (ex, ey) = datasets.noisy_xor()
+    n_epochs, N = 20, len(ty)
+    stream = torch.cuda.current_stream()
+
+    def seed_of(i):
+        return (i + 5 * rank) % 5 if world == 1 else 5 * rank + i % 5
+
+    def prepare(i):
+        cfg = tmb.Config(**datasets.noisy_xor_config_kwargs(seed=seed_of(i)))
+        sess = tmb.DenseTrainSession(cfg, tx, ty)
+        orders = [torch.from_numpy(sess.next_order().astype(np.int32)).cuda()
+                  for _ in range(n_epochs)]
+        return sess, orders
+
+    for i in range(args.warmup):
+        sess, orders = prepare(i)
+        for o in orders:
+            sess.run_steps(o)
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    preps = [prepare(args.warmup + i) for i in range(args.steps)]
+    torch.cuda.synchronize()
+    ev = []
+    barrier(world)
+    with ClockSampler(local) as clk:
+        for sess, orders in preps:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for o in orders:
+                sess.run_steps(o)
+            b.record(stream)
+            ev.append((a, b))
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = _lib.launch_count() - launches0
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), world)
+    n_ex = args.steps * n_epochs * N
+    value = n_ex * world / (ms / 1e3)
+    us_step = ms * 1e3 / n_ex
+    accs = []
+    for sess, _ in preps:
+        accs.append(tmb.evaluate(sess.model(), (ex, ey)))
+    # e2e through the public train() (per-epoch evaluation included, as the
+    # reference's train(eval_data=...) does)
+    barrier(world)
+    t0 = time.perf_counter()
+    e2e_acc = []
+    for i in range(args.steps):
+        cfg = tmb.Config(**datasets.noisy_xor_config_kwargs(seed=seed_of(args.warmup + i)))
+        run = tmb.train(cfg, (tx, ty), (ex, ey), n_epochs=n_epochs)
+        e2e_acc.append(run.epoch_metrics[-1].accuracy)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    line = {
+        "metric": "train examples/sec (configs[0] Noisy-XOR CoTM training)",
+        "value": value, "unit": "examples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "us_per_example": us_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int8 TA states / int32 weights / u64 SplitMix64",
+        "data": "synthetic (datasets.noisy_xor: 12 Bernoulli(0.5) features, 40% train "
+                "label noise)",
+        "config": {"workload": "configs[0]: Noisy-XOR, 10 clauses, T=15, s=3.9; step = one "
+                               "20-epoch training of 5000 examples (model seeds 0..4 in turn)",
+                   "launch": preps[0][0].launch,
+                   "parallelism": f"replicas x{world} (online training is sequential)",
+                   "l2": "model and data (60 KB) are L2/SMEM-resident by design; nothing to "
+                         "flush that the workload re-reads"},
+        "gpu_launches": int(launches),
+        "accuracy": {"test_accuracy_per_step": accs, "mean": float(np.mean(accs))},
+        "roofline": {"kernel": "k_train (cluster mode, one CTA)", "bound": "latency",
+                     "achieved": 1e6 / us_step, "unit": "examples/s",
+                     "note": "single-CTA sequential steps: the per-example dependency chain "
+                             "(eval -> class sums -> decision -> feedback) is barrier/latency "
+                             "bound; see DESIGN.md"},
+        "clocks": clk.summary(),
+        "e2e": {"value": n_ex * world / e2e_s, "unit": "examples/s",
+                "h2d_bytes_per_step": int(tx.nbytes + ex.nbytes + 4 * N),
+                "d2h_bytes_per_step": int(n_epochs * 8 * len(ey) + 10 * 24 + 10 * 2 * 4),
+                "path": "tmb.train(cfg, (x, y), (x_test, y_test), n_epochs=20): host arrays in, "
+                        "per-epoch test predictions and the model out",
+                "test_accuracy_per_step": e2e_acc},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
+        from oracle import oracle
+        model_name, ncpu = host_desc()
+        t = time.perf_counter()
+        o_acc = []
+        for sd in range(5):
+            cfg = tmb.Config(**datasets.noisy_xor_config_kwargs(seed=sd))
+            st, acc = oracle.train(cfg, tx, ty, n_epochs)
+            _, pred = oracle.batch_votes(st.states, st.weights, oracle.augment_literals(ex))
+            o_acc.append(float(np.mean(pred == ey)))
+        dt = time.perf_counter() - t
+        line["cpu_baseline"] = {"value": 5 * n_epochs * N / dt, "unit": "examples/s",
+                                "cores": 1, "kind": "port",
+                                "sample": f"oracle C port of executor.train, seeds 0..4 x 20 "
+                                          f"epochs x 5000 examples ({dt:.1f}s, 1 thread)",
+                                "host": model_name, "host_cores": ncpu,
+                                "mean_test_accuracy_seeds_0_4": float(np.mean(o_acc))}
+    return line
+
+
 # -------------------------------------------------------- c3 inference --
 
 def c3_inputs_device(n: int, start: int, data_seed: int = 3, F: int = 4096):
     """Device-side synthesis of the counter-based C3 inputs (same bits as
     datasets.inference_examples)."""
-    import torch
-
-    from paper_2405_04212_b200 import _lib, datasets
-    from paper_2405_04212_b200.runtime import ptr, stream_ptr
-    W = (F + 63) // 64
-    x = torch.empty((n, F), dtype=torch.uint8, device="cuda")
-    seed = datasets.inference_stream_seed(data_seed)
-    chunk = 1 << 18
-    shifts = torch.arange(8, device="cuda", dtype=torch.uint8)
-    for lo in range(0, n, chunk):
-        m = min(chunk, n - lo)
-        words = torch.empty(m * W, dtype=torch.int64, device="cuda")
-        _lib.call("tmb_stream_u64_block", seed, (start + lo) * W, m * W, ptr(words), stream_ptr())
-        b = words.view(torch.uint8).view(m, W * 8)
-        bits = (b.unsqueeze(-1) >> shifts) & 1
-        x[lo:lo + m] = bits.view(m, W * 64)[:, :F]
-        del words, b, bits
-    return x
+    from paper_2405_04212_b200 import datasets
+    return datasets.inference_examples_device(data_seed, start, n, F)
 
 
 def bench_c3_infer(args, rank, world, local, embedded=False):
@@ -746,27 +846,186 @@ def bench_c4_train(args, rank, world, local):
     return line
 
 
-def bench_c5_sparse(args, rank, world, local):
-    """configs[4]: SparseTM on 10^6 Zipf documents (10^6-literal vocabulary,
-    2000 clauses, capacity 64).  Headline = training documents/s, step =
-    100000 consecutive documents of the epoch; secondary = inverted-index
-    inference over all 10^6 documents per step."""
+def bench_c4_sweep(args, rank, world, local):
+    """configs[3] sweep: the 8-point grid s in {1.5, 2, 3, 5} x T in {5000,
+    10000} (datasets.SWEEP_GRID) of independent bag-of-words trainings, job j
+    on rank j mod world (parallel.jobs_of; tuning.py:176-227 runs them one
+    after another).  Step = every job trains its next --sweep-examples
+    examples of epoch 1 (sessions persist across steps).  value = examples
+    of all jobs / max-over-ranks time: total work is fixed, so scaling is
+    strong.  The jobs' test accuracies (the sweep's result) are reported."""
     import torch
 
     import paper_2405_04212_b200 as tmb
-    from paper_2405_04212_b200 import _lib, datasets, sparse_train
-    d = datasets.sparse_zipf(data_seed=5 + rank)
-    cfg = tmb.Config(**datasets.sparse_config_kwargs(seed=rank))
+    from paper_2405_04212_b200 import _lib, datasets, parallel
+    (tx, ty), (ex, ey) = datasets.bag_of_words(data_seed=4)
+    grid = datasets.SWEEP_GRID
+    mine = parallel.jobs_of(len(grid), world, rank)
+    step_n = args.sweep_examples
+    jobs = []
+    for j in mine:
+        s_, t_ = grid[j]
+        cfg = tmb.Config(**datasets.bag_of_words_config_kwargs(seed=j, s=s_, threshold=t_))
+        sess = tmb.DenseTrainSession(cfg, tx, ty)
+        order = torch.from_numpy(sess.next_order().astype(np.int32)).cuda()
+        jobs.append([j, cfg, sess, order, 0])
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(job):
+        j, cfg, sess, order, pos = job
+        if pos + step_n > sess.N:  # next epoch
+            job[3] = order = torch.from_numpy(sess.next_order().astype(np.int32)).cuda()
+            pos = 0
+        sess.run_steps(order[pos:pos + step_n])
+        job[4] = pos + step_n
+
+    for _ in range(args.warmup):
+        for job in jobs:
+            step(job)
+    torch.cuda.synchronize()
+    stats0 = [job[2].stats_dict() for job in jobs]
+    launches0 = _lib.launch_count()
+    barrier(world)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            flush_l2(flush)
+            for job in jobs:
+                step(job)
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = _lib.launch_count() - launches0
+    ms = max_over_ranks(a.elapsed_time(b), world)
+    n_total = len(grid) * step_n * args.steps
+    value = n_total / (ms / 1e3)
+    ev = sum(job[2].stats_dict()["events"] - s0["events"] for job, s0 in zip(jobs, stats0))
+    n_mine = len(jobs) * step_n * args.steps
+    # the sweep's result: test accuracy of every grid point (gathered)
+    acc_mine = {job[0]: tmb.evaluate(job[2].model(), (ex, ey)) for job in jobs}
+    if world > 1:
+        import torch.distributed as dist
+        parts = [None] * world
+        dist.all_gather_object(parts, acc_mine)
+        acc = {}
+        for p in parts:
+            acc.update(p)
+    else:
+        acc = acc_mine
+    # e2e: per step and job, pinned host features -> H2D -> pack -> trainer ->
+    # D2H model (a sweep driver that keeps no device state between steps)
+    from paper_2405_04212_b200.runtime import ptr, stream_ptr
+    xp = torch.from_numpy(np.ascontiguousarray(tx)).pin_memory()
+    st_host = torch.empty(jobs[0][2].states.shape, dtype=torch.int8).pin_memory() if jobs else None
+    w_host = torch.empty(jobs[0][2].weights.shape, dtype=torch.int32).pin_memory() if jobs else None
+    barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        for job in jobs:
+            sess = job[2]
+            xd = xp.to("cuda", non_blocking=True)
+            _lib.call("tmb_pack_literals", ptr(xd), xp.shape[0], job[1].n_literals, 1,
+                      ptr(sess.lit_words), stream_ptr())
+            step(job)
+            st_host.copy_(sess.states, non_blocking=True)
+            w_host.copy_(sess.weights, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    line = {
+        "metric": "sweep train examples/sec (configs[3] 8-point s x T grid)",
+        "value": value, "unit": "examples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "int8 TA states (HBM) / int32 weights / u64 SplitMix64",
+        "data": "synthetic (datasets.bag_of_words: Zipf(1.1) documents, planted sets)",
+        "config": {"workload": f"configs[3] sweep: 8 independent bag-of-words trainings "
+                               f"(10000 clauses x 20000 positions), job j on rank j mod "
+                               f"{world}; step = {step_n} examples of every job",
+                   "grid": [list(g) for g in grid], "jobs_on_rank0": mine,
+                   "parallelism": f"jobs round-robin over {world} GPU(s); no collective on "
+                                  "the hot path",
+                   "l2": "256 MiB buffer written before every timed step"},
+        "gpu_launches": int(launches),
+        "work": {"events_per_example_rank0": ev / max(n_mine, 1)},
+        "sweep_result": {"test_accuracy": {f"s={grid[j][0]},T={grid[j][1]}": acc[j]
+                                           for j in sorted(acc)},
+                         "note": f"after {args.warmup + args.steps} steps of {step_n} "
+                                 "examples per job"},
+        "roofline": {"kernel": "k_train<1, false> (grid mode, HBM-resident states)",
+                     "bound": "hbm", "note": "see the c4-train line: same kernel"},
+        "clocks": clk.summary(),
+        "e2e": {"value": n_total / (e2e_ms / 1e3), "unit": "examples/s",
+                "h2d_bytes_per_step": int(len(jobs) * tx.nbytes),
+                "d2h_bytes_per_step": int(len(jobs) * (jobs[0][2].states.numel()
+                                                       + 4 * jobs[0][2].weights.numel()))
+                if jobs else 0,
+                "path": "per job and step: pinned host features -> H2D -> tmb_pack_literals "
+                        "-> tmb_trainer_run -> D2H model"},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
+        from oracle import oracle
+        model_name, ncpu = host_desc()
+        x_lit = oracle.augment_literals(tx)
+        per, t = 6, time.perf_counter()
+        for j, (s_, t_) in enumerate(grid):
+            cfg = oracle.OracleCfg(**datasets.bag_of_words_config_kwargs(seed=j, s=s_,
+                                                                          threshold=t_))
+            st = oracle.new_train_state(cfg)
+            order, _ = oracle.shuffle_permutation(len(ty), oracle.derive_stream(j, 0xD157), 0)
+            oracle.train_steps(cfg, st, x_lit, ty, order[:per])
+        dt = time.perf_counter() - t
+        line["cpu_baseline"] = {"value": len(grid) * per / dt, "unit": "examples/s",
+                                "cores": 1, "kind": "port",
+                                "sample": f"oracle C port of executor.train, the first {per} "
+                                          f"examples of each of the 8 grid points, run one "
+                                          f"after another as tuning does ({dt:.1f}s, 1 thread)",
+                                "host": model_name, "host_cores": ncpu}
+    return line
+
+
+def bench_c5_sparse(args, rank, world, local):
+    """configs[4]: SparseTM on 10^6 Zipf documents (10^6-literal vocabulary,
+    2000 clauses, capacity 64).  Headline = training documents/s, step =
+    100000 consecutive documents of the epoch (the next epoch's shuffle when
+    one runs out); every rank trains the same replica (same data and seed:
+    training is sequential, "replicas only").  Secondary = inference over
+    all 10^6 documents per step, the CSR rows SHARDED over the ranks by
+    non-zeros (parallel.csr_shard), predictions gathered once."""
+    import torch
+
+    import paper_2405_04212_b200 as tmb
+    from paper_2405_04212_b200 import _lib, datasets, parallel, sparse_train
+    from paper_2405_04212_b200.executor import shuffle_permutation
+    d = datasets.sparse_zipf(data_seed=5)
+    cfg = tmb.Config(**datasets.sparse_config_kwargs(seed=0))
     sess = sparse_train.SparseTrainSession(cfg, d.indptr, d.indices, d.labels)
     step_n = 100_000
-    from paper_2405_04212_b200.executor import shuffle_permutation
-    order = torch.from_numpy(shuffle_permutation(sess.N, sess.shuffle_rng).astype(np.int32)).cuda()
+    cur = {"order": shuffle_permutation(sess.N, sess.shuffle_rng).astype(np.int32), "pos": 0}
+
+    def next_slice():
+        if cur["pos"] + step_n > sess.N:  # the next epoch's order
+            cur["order"] = shuffle_permutation(sess.N, sess.shuffle_rng).astype(np.int32)
+            cur["pos"] = 0
+        o = cur["order"][cur["pos"]:cur["pos"] + step_n]
+        cur["pos"] += step_n
+        return o
+
     stream = torch.cuda.current_stream()
-    pos = 0
     for _ in range(args.warmup):
-        sess.run_steps(order[pos:pos + step_n])
-        pos += step_n
+        sess.run_steps(torch.from_numpy(next_slice()).cuda())
     torch.cuda.synchronize()
+    timed = [next_slice() for _ in range(args.steps)]
+    timed_dev = [torch.from_numpy(o).cuda() for o in timed]
+    # model at the start of the timed region (CPU baseline starts from it)
+    lits0, sts0, w0, bc0 = sess.engine.get_lists()
+    fb0 = sess.fb_counter
     stats0 = sess.stats_dict()
     launches0 = _lib.launch_count()
     barrier(world)
@@ -774,9 +1033,8 @@ def bench_c5_sparse(args, rank, world, local):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for i in range(args.steps):
-            sess.run_steps(order[pos:pos + step_n])
-            pos += step_n
+        for od in timed_dev:
+            sess.run_steps(od)
         b.record(stream)
         torch.cuda.synchronize()
         barrier(world)
@@ -788,33 +1046,39 @@ def bench_c5_sparse(args, rank, world, local):
     nnz = 100
     csr_bytes = 4 * nnz + 8
     ev_doc = dd["events"] / max(dd["examples"], 1)
-    # inference over all documents (the trained model)
+    # ---- sharded inference over all documents with the trained model
     eng = sess.engine
+    lo, hi = parallel.csr_shard(d.indptr, world, rank)
+    n_loc = hi - lo
+    ip_loc = sess.indptr[lo:hi + 1] - sess.indptr[lo]
+    ix_loc = sess.indices[int(d.indptr[lo]):int(d.indptr[hi])]
     for _ in range(2):
-        eng.votes_and_pred(sess.indptr, sess.indices, sess.N)
+        eng.votes_and_pred(ip_loc, ix_loc, n_loc)
     torch.cuda.synchronize()
+    barrier(world)
     ia = torch.cuda.Event(enable_timing=True)
     ib = torch.cuda.Event(enable_timing=True)
     ia.record(stream)
     for _ in range(args.steps):
-        votes, pred = eng.votes_and_pred(sess.indptr, sess.indices, sess.N)
+        votes, pred = eng.votes_and_pred(ip_loc, ix_loc, n_loc)
     ib.record(stream)
     torch.cuda.synchronize()
-    inf_ms = ia.elapsed_time(ib)
+    inf_ms = max_over_ranks(ia.elapsed_time(ib), world)
     inf_value = sess.N * args.steps / (inf_ms / 1e3)
-    acc = float((pred.cpu().numpy() == d.labels).mean())
-    # e2e training: the next args.steps chunks of the epoch, each chunk's CSR
-    # rows staged (in consumption order) in pinned host memory by the data
-    # loader before the timed region; timed per step: H2D of the chunk, the
-    # trainer, D2H of the step's statistics
-    order_h = order.cpu().numpy()
+    per_launch_inf_ms = ia.elapsed_time(ib) / args.steps
+    tg = time.perf_counter()
+    pred_all = parallel.gather_rows(pred.cpu().numpy(), sess.N)
+    gather_s = time.perf_counter() - tg
+    acc = float((pred_all == d.labels).mean())
+    # e2e training: the timed chunks again from the same model, each chunk's
+    # CSR rows staged (in consumption order) in pinned host memory by the
+    # data loader before the timed region; timed per step: H2D of the chunk,
+    # the trainer, D2H of the step's statistics
+    eng.set_lists(lits0, sts0, w0, bc0)
+    sess.fb_counter = fb0
     staged = []
-    for _ in range(args.steps):
-        if pos + step_n > sess.N:  # next epoch's order
-            order_h = shuffle_permutation(sess.N, sess.shuffle_rng).astype(np.int32)
-            pos = 0
-        o = order_h[pos:pos + step_n].astype(np.int64)
-        pos += step_n
+    for o in timed:
+        o = o.astype(np.int64)
         lens = d.indptr[o + 1] - d.indptr[o]
         ip = np.zeros(step_n + 1, dtype=np.int64)
         ip[1:] = np.cumsum(lens)
@@ -824,7 +1088,7 @@ def bench_c5_sparse(args, rank, world, local):
                        torch.from_numpy(d.labels[o].astype(np.int32)).pin_memory()))
     seq = torch.arange(step_n, dtype=torch.int32, device="cuda")
     st_h = torch.empty(6, dtype=torch.int64).pin_memory()
-    h2d_tr = sum(int(a.numel() * a.element_size()) for a in staged[0])
+    h2d_tr = sum(int(x.numel() * x.element_size()) for x in staged[0])
     torch.cuda.synchronize()
     barrier(world)
     ta = torch.cuda.Event(enable_timing=True)
@@ -837,22 +1101,28 @@ def bench_c5_sparse(args, rank, world, local):
     tb.record(stream)
     torch.cuda.synchronize()
     e2e_train = step_n * args.steps * world / (max_over_ranks(ta.elapsed_time(tb), world) / 1e3)
-    # e2e inference: host CSR -> device -> infer -> host predictions
-    ip_h = torch.from_numpy(d.indptr).pin_memory()
-    ix_h = torch.from_numpy(d.indices).pin_memory()
-    pr_h = torch.empty(sess.N, dtype=torch.int64).pin_memory()
+    lits1, sts1, w1, bc1 = eng.get_lists()
+    e2e_same = bool(np.array_equal(bc1, sess.engine.get_lists()[3]))
+    # e2e inference: this rank's host CSR shard -> device -> infer -> host
+    a0, a1 = int(d.indptr[lo]), int(d.indptr[hi])
+    ip_h = torch.from_numpy(np.ascontiguousarray(d.indptr[lo:hi + 1] - a0)).pin_memory()
+    ix_h = torch.from_numpy(np.ascontiguousarray(d.indices[a0:a1])).pin_memory()
+    pr_h = torch.empty(n_loc, dtype=torch.int64).pin_memory()
+    barrier(world)
     ea = torch.cuda.Event(enable_timing=True)
     eb = torch.cuda.Event(enable_timing=True)
     ea.record(stream)
     for _ in range(args.steps):
         ipd = ip_h.to("cuda", non_blocking=True)
         ixd = ix_h.to("cuda", non_blocking=True)
-        _, pd = eng.votes_and_pred(ipd, ixd, sess.N)
+        _, pd = eng.votes_and_pred(ipd, ixd, n_loc)
         pr_h.copy_(pd, non_blocking=True)
     eb.record(stream)
     torch.cuda.synchronize()
-    e2e_inf = sess.N * args.steps / (ea.elapsed_time(eb) / 1e3)
+    e2e_inf = sess.N * args.steps / (max_over_ranks(ea.elapsed_time(eb), world) / 1e3)
     launches = _lib.launch_count() - launches0
+    tr_tr, tr_tr_src = ncu_traffic("k_sparse_train")
+    tr_in, tr_in_src = ncu_traffic("k_sparse_infer")
     line = {
         "metric": "SparseTM train documents/sec (configs[4])",
         "value": value, "unit": "documents/s", "n_gpus": world, "steps": args.steps,
@@ -862,155 +1132,355 @@ def bench_c5_sparse(args, rank, world, local):
         "data": "synthetic (datasets.sparse_zipf: 10^6 Zipf(1.05) documents x 100 ids)",
         "config": {"workload": "configs[4]: SparseTM, 10^6-literal vocabulary, 2000 clauses, "
                                "capacity 64; step = 100000 consecutive training documents",
-                   "parallelism": f"replicas x{world} (online training is sequential)"},
+                   "parallelism": f"replicas x{world} (online training is sequential; every "
+                                  "rank trains the same replica)",
+                   "l2": "per-step CSR chunk (40 MB) and the clause lists; each step streams "
+                         "new documents"},
         "gpu_launches": int(launches),
         "work": {"events_per_document": ev_doc,
                  "draws_per_document": dd["draws"] / max(dd["examples"], 1)},
-        "roofline": {"kernel": "k_sparse_train", "bound": "hbm",
-                     "achieved": csr_bytes * value / world / 1e9, "peak": HBM_PEAK,
-                     "unit": "GB/s", "frac": csr_bytes * value / world / 1e9 / HBM_PEAK,
-                     "traffic": None, "peak_source": HBM_PEAK_SRC,
+        "roofline": {"kernel": "k_sparse_train", "bound": "latency",
+                     "achieved": value / world, "unit": "documents/s",
+                     "traffic": tr_tr, "traffic_source": tr_tr_src,
+                     "hbm_gbs": csr_bytes * value / world / 1e9,
+                     "hbm_frac": csr_bytes * value / world / 1e9 / HBM_PEAK,
                      "algorithmic_bytes_per_example": csr_bytes,
-                     "note": "latency-bound sequential training (one all-reduce per document); "
-                             "clause lists are on chip, HBM carries the document's CSR row"},
+                     "note": "sequential training: one grid all-reduce per document plus the "
+                             "per-event list merges; HBM carries only the document's CSR row"},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_train, "unit": "documents/s",
                 "h2d_bytes_per_step": h2d_tr, "d2h_bytes_per_step": 48,
+                "same_model_as_device_run": e2e_same,
                 "path": "per step: pinned host CSR chunk (100000 documents in consumption "
                         "order) + labels -> H2D -> tmb_sparse_train -> D2H step statistics"},
-        "secondary": {"metric": "SparseTM inference documents/sec (configs[4])",
-                      "value": inf_value, "unit": "documents/s",
+        "secondary": {"metric": "SparseTM inference documents/sec (configs[4], sharded)",
+                      "value": inf_value, "unit": "documents/s", "n_gpus": world,
+                      "scaling": "strong",
+                      "sharding": f"CSR rows balanced by nnz over {world} rank(s) "
+                                  "(parallel.csr_shard); predictions gathered once "
+                                  f"({gather_s * 1e3:.1f} ms, outside the timed step)",
+                      "rows_rank0": [lo, hi],
                       "e2e": {"value": e2e_inf, "unit": "documents/s",
-                              "h2d_bytes_per_step": int(d.indptr.nbytes + d.indices.nbytes),
-                              "d2h_bytes_per_step": int(8 * sess.N),
-                              "path": "pinned host CSR -> H2D -> tmb_sparse_infer -> host "
-                                      "predictions"},
-                      "accuracy_note": "1 partial epoch of training; C5 states no accuracy "
-                                       "target (throughput workload; training is bit-exact "
-                                       "vs the oracle on slices, tests/test_gpu_parity.py)",
+                              "h2d_bytes_per_step": int(ip_h.numel() * 8 + ix_h.numel() * 4),
+                              "d2h_bytes_per_step": int(8 * n_loc),
+                              "path": "this rank's pinned host CSR shard -> H2D -> "
+                                      "tmb_sparse_infer -> host predictions"},
                       "ms_per_step": inf_ms / args.steps, "accuracy_after_train": acc,
                       "roofline": {"kernel": "k_sparse_infer (inverted index)", "bound": "hbm",
-                                   "achieved": inf_value * (csr_bytes + 8) / 1e9,
+                                   "achieved": n_loc * (csr_bytes + 8) / (per_launch_inf_ms / 1e3)
+                                   / 1e9,
                                    "peak": HBM_PEAK, "unit": "GB/s",
-                                   "frac": inf_value * (csr_bytes + 8) / 1e9 / HBM_PEAK,
-                                   "traffic": None,
+                                   "frac": n_loc * (csr_bytes + 8) / (per_launch_inf_ms / 1e3)
+                                   / 1e9 / HBM_PEAK,
+                                   "traffic": tr_in, "traffic_source": tr_in_src,
                                    "algorithmic_bytes_per_example": csr_bytes + 8}},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         from oracle import oracle
         model_name, ncpu = host_desc()
-        acts = [d.indices[d.indptr[i]:d.indptr[i + 1]].astype(np.int64) for i in range(200)]
-        t0 = time.perf_counter()
-        n_tr = 40
-        oracle.sparse_train(cfg, acts[:n_tr], d.labels[:n_tr], n_epochs=1)
+        # the oracle from the SAME model state on the same documents, with the
+        # real candidate set (the whole training set's actives)
+        ob = oracle.SparseOracleBank(cfg, candidates=sess.candidates)
+        ob.lits, ob.sts, ob.weights = lits0, sts0, w0.copy()
+        docs = [d.row(int(i)) for i in timed[0]]
+        labels = d.labels[timed[0]].astype(np.int64)
+        n_tr, t0 = 0, time.perf_counter()
+        bctr = [int(bc0[0])]
+        fb = fb0
+        while time.perf_counter() - t0 < args.cpu_seconds and n_tr < len(docs):
+            _, bctr, fb = oracle.sparse_train_from(cfg, [ob], bctr, fb, docs[n_tr:n_tr + 1],
+                                                   labels[n_tr:n_tr + 1])
+            n_tr += 1
         dt = time.perf_counter() - t0
         line["cpu_baseline"] = {"value": n_tr / dt, "unit": "documents/s", "cores": 1,
                                 "kind": "port",
                                 "sample": f"oracle C port of executor.train (sparse), the first "
-                                          f"{n_tr} documents of a 40-document dataset from the "
-                                          f"initial model ({dt:.1f}s, 1 thread)",
+                                          f"{n_tr} documents of the first timed step from the "
+                                          f"same model state, real candidate set "
+                                          f"({len(sess.candidates)} literals) ({dt:.1f}s, "
+                                          f"1 thread)",
                                 "host": model_name, "host_cores": ncpu}
     return line
 
 # -------------------------------------------------------- reference arm --
 
+def ref_package():
+    """The UNMODIFIED reference (tsetlinkit) from baseline/_ref (pip-installed
+    from /root/reference), with its default numba backend.
+    Returns the module or None when it is not installed / numba is absent."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "tsetlinkit")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "numba_cache"))
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import tsetlinkit
+        from tsetlinkit import kernels
+    except Exception:  # noqa: BLE001 - fall back to the port
+        return None
+    if kernels.BACKEND_NAME != "numba":
+        return None
+    kernels.warmup()
+    return tsetlinkit
+
+
+class RefTrainer:
+    """executor.train's serial driver (executor.py:296-330: eval_block /
+    decide / update_block, one clause block) driving the reference's own
+    DenseClauseBank, update_probabilities, sample_updates and numba kernels,
+    started from a saved training state so it can time any epoch."""
+
+    def __init__(self, tk, cfg_kwargs, x, state=None):
+        from tsetlinkit.core import (FEEDBACK_STREAM, SHUFFLE_STREAM, Config, RngStream,
+                                     augment_literals)
+        from tsetlinkit.dense import DenseClauseBank
+        self.tk = tk
+        self.cfg = Config(**cfg_kwargs)
+        self.bank = DenseClauseBank(self.cfg)
+        self.blk_rng = RngStream.derive(self.cfg.seed, 0)
+        self.fb_rng = RngStream.derive(self.cfg.seed, FEEDBACK_STREAM)
+        self.sh_rng = RngStream.derive(self.cfg.seed, SHUFFLE_STREAM)
+        if state is not None:
+            self.bank.states[:] = state["states"]
+            self.bank.weights[:] = state["weights"]
+            self.blk_rng.counter = int(state["block_counters"][0])
+            self.fb_rng.counter = int(state["fb_counter"])
+            self.sh_rng.counter = int(state["shuffle_counter"])
+        self.x_lit = augment_literals(x, self.cfg.negated_literals_enabled)
+        self.votes_parts = np.zeros((1, self.cfg.n_classes), dtype=np.int64)
+
+    def next_order(self):
+        from tsetlinkit.executor import shuffle_permutation
+        return shuffle_permutation(self.x_lit.shape[0], self.sh_rng)
+
+    def steps(self, labels, order):
+        from tsetlinkit.dense import EvalMode
+        from tsetlinkit.feedback import sample_updates, update_probabilities
+        bank, cfg, vp = self.bank, self.cfg, self.votes_parts
+        for idx in order:
+            lits = self.x_lit[idx]
+            label = int(labels[idx])
+            out = bank.clause_outputs(lits, EvalMode.TRAINING)
+            vp[0] = bank.votes(out)
+            dec = update_probabilities(vp.sum(axis=0), label, cfg.threshold, self.fb_rng)
+            ut, un = sample_updates(dec, cfg.n_clauses, self.fb_rng)
+            bank.apply_feedback(lits, out, label, dec.negative_class, ut, un, self.blk_rng)
+
+
+
+
+def _c2_checkpoint(warmup: int):
+    """Latest committed oracle checkpoint of the configs[1] bench model at or
+    before the GPU arm's last warm-up epoch (tests/golden/c2_epoch{3,5}.npz)."""
+    best = None
+    for e in (3, 5):
+        f = os.path.join(REPO, "tests", "golden", f"c2_epoch{e}.npz")
+        if e <= warmup and os.path.exists(f):
+            best = (e, f)
+    if best is None:
+        return 0, None
+    g = np.load(best[1])
+    return best[0], {k: g[k] for k in g.files}
+
+
 def bench_reference(args, rank, world):
-    """The reference's own CPU algorithm on the host cores: the oracle port
-    (a C restatement of tsetlinkit's numba loops; the Python reference does
-    not exist on the GPU box).  Rank 0 only."""
+    """The reference's own CPU implementation on the host cores, rank 0 only.
+
+    When baseline/_ref holds the unmodified reference (pip-installed from
+    /root/reference) and numba imports, its own code runs ("kind":
+    "reference"): the executor's serial-driver loop over its DenseClauseBank
+    / feedback functions / numba kernels (training), its public train()
+    (configs[0]), its numba clause_outputs_batch sharded over host threads
+    (inference).  Otherwise, and for SparseTM (pure-Python reference, ~minutes
+    per configs[4] document), the oracle's C restatement ("kind": "port")."""
     if rank != 0:
         return None
     from oracle import oracle
 
     from paper_2405_04212_b200 import datasets
     model_name, ncpu = host_desc()
+    tk = None if args.ref_port else ref_package()
+    kind = "reference" if tk is not None else "port"
     unit = "examples/s"
-    if args.workload == "c3-infer":
+    extra = {}
+    if args.workload == "c1-train":
+        (tx, ty), (ex, ey) = datasets.noisy_xor()
+        rates, accs = [], []
+        for i in range(args.warmup + args.steps):
+            kw = datasets.noisy_xor_config_kwargs(seed=i % 5)
+            t = time.perf_counter()
+            if tk is not None:
+                run = tk.train(tk.Config(**kw), (tx, ty), n_epochs=20)
+                st, w = run.model.states, run.model.weights
+            else:
+                ost, _ = oracle.train(oracle.OracleCfg(**kw), tx, ty, 20)
+                st, w = ost.states, ost.weights
+            dt = time.perf_counter() - t
+            if i >= args.warmup:
+                rates.append(20 * len(ty) / dt)
+                _, pred = oracle.batch_votes(st, w, oracle.augment_literals(ex))
+                accs.append(float(np.mean(pred == ey)))
+        value = float(np.mean(rates))
+        metric = "train examples/sec (configs[0] Noisy-XOR CoTM training)"
+        sample = ("one 20-epoch train() of 5000 examples per step (model seeds 0..4 in turn), "
+                  "1 thread" + (" (tsetlinkit.train, numba backend)" if tk else ""))
+        cores = 1
+        extra["test_accuracy_per_step"] = accs
+    elif args.workload == "c3-infer":
         m = datasets.inference_model(model_seed=11)
         xs = datasets.inference_examples(3, 0, args.c3_cpu_examples)
         x_lit = oracle.augment_literals(xs)
+        if tk is not None:
+            from concurrent.futures import ThreadPoolExecutor
+
+            from tsetlinkit.core import Config as RCfg
+            from tsetlinkit.dense import DenseClauseBank as RBank
+            bank = RBank(RCfg(n_literals=4096, n_clauses=10000, n_classes=10, s=2.0,
+                              threshold=100))
+            bank.states[:] = m.states
+            bank.weights[:] = m.weights
+            parts = np.array_split(np.arange(len(xs)), ncpu)
+            pool = ThreadPoolExecutor(ncpu)
+
+            def run_all():
+                # batch_votes (dense.py:171-174; numba nogil kernel) per
+                # thread shard, then argmax (executor.py:382)
+                res = list(pool.map(lambda p: bank.batch_votes(x_lit[p]), parts))
+                return np.argmax(np.concatenate(res), axis=1)
+        else:
+            def run_all():
+                return oracle.batch_votes(m.states, m.weights, x_lit, nthreads=ncpu,
+                                          want_votes=False)[1]
         rates = []
         for i in range(args.warmup + args.steps):
             t = time.perf_counter()
-            oracle.batch_votes(m.states, m.weights, x_lit, nthreads=ncpu, want_votes=False)
+            run_all()
             if i >= args.warmup:
                 rates.append(len(xs) / (time.perf_counter() - t))
         value = float(np.mean(rates))
         metric = "inference examples/sec (configs[2] batched CoTM inference)"
-        sample = f"{len(xs)}-example prefix per step, {ncpu} threads"
+        sample = (f"{len(xs)}-example prefix per step, {ncpu} threads"
+                  + (" (DenseClauseBank.batch_votes, numba nogil kernel per thread shard)"
+                     if tk else ""))
         cores = ncpu
-    elif args.workload == "c4-train":
+    elif args.workload in ("c4-train", "c4-sweep"):
         (tx, ty), _ = datasets.bag_of_words(data_seed=4)
-        cfg = oracle.OracleCfg(**datasets.bag_of_words_config_kwargs(seed=0))
-        st = oracle.new_train_state(cfg)
-        x_lit = oracle.augment_literals(tx)
-        order, _ = oracle.shuffle_permutation(len(ty), oracle.derive_stream(0, 0xD157), 0)
-        rates, pos, per_step = [], 0, 8
+        grid = datasets.SWEEP_GRID if args.workload == "c4-sweep" else [(2.0, 10000)]
+        per_step = 8 if args.workload == "c4-train" else 2
+        trainers = []
+        for j, (s_, t_) in enumerate(grid):
+            kw = datasets.bag_of_words_config_kwargs(seed=j if len(grid) > 1 else 0, s=s_,
+                                                     threshold=t_)
+            if tk is not None:
+                tr = RefTrainer(tk, kw, tx)
+                trainers.append((tr, tr.next_order(), None))
+            else:
+                cfg = oracle.OracleCfg(**kw)
+                st = oracle.new_train_state(cfg)
+                order, _ = oracle.shuffle_permutation(len(ty), oracle.derive_stream(cfg.seed,
+                                                                                    0xD157), 0)
+                trainers.append((cfg, order, st))
+        x_lit = None if tk is not None else oracle.augment_literals(tx)
+        rates, pos = [], 0
         for i in range(args.warmup + args.steps):
             t = time.perf_counter()
-            oracle.train_steps(cfg, st, x_lit, ty, order[pos:pos + per_step])
+            for a, order, st in trainers:
+                if tk is not None:
+                    a.steps(ty, order[pos:pos + per_step])
+                else:
+                    oracle.train_steps(a, st, x_lit, ty, order[pos:pos + per_step])
             pos += per_step
             if i >= args.warmup:
-                rates.append(per_step / (time.perf_counter() - t))
+                rates.append(per_step * len(trainers) / (time.perf_counter() - t))
         value = float(np.mean(rates))
-        metric = "train examples/sec (configs[3] bag-of-words CoTM training)"
-        sample = f"{per_step} consecutive examples of epoch 1 per step, 1 thread"
+        if args.workload == "c4-sweep":
+            metric = "sweep train examples/sec (configs[3] 8-point s x T grid)"
+            sample = (f"{per_step} consecutive examples of epoch 1 of each of the 8 grid points "
+                      f"per step, run one after another as tuning does, 1 thread")
+        else:
+            metric = "train examples/sec (configs[3] bag-of-words CoTM training)"
+            sample = f"{per_step} consecutive examples of epoch 1 per step, 1 thread"
         cores = 1
     elif args.workload == "c5-sparse":
-        d = datasets.sparse_zipf(data_seed=5, n_docs=2000)
-        cfg = datasets.sparse_config_kwargs(seed=0)
-        acts = [d.indices[d.indptr[i]:d.indptr[i + 1]].astype(np.int64) for i in range(2000)]
-        rates, pos, per_step = [], 0, 10
+        kind = "port"
+        d = datasets.sparse_zipf(data_seed=5)
+        cfg = oracle.OracleCfg(**datasets.sparse_config_kwargs(seed=0))
+        cands = np.unique(d.indices).astype(np.int64)
+        order, _ = oracle.shuffle_permutation(len(d), oracle.derive_stream(0, 0xD157), 0)
+        banks = [oracle.SparseOracleBank(cfg, candidates=cands)]
+        bctr, fb = [0], 0
+        rates, pos, per_step = [], 0, 1
         for i in range(args.warmup + args.steps):
+            docs = [d.row(int(k)) for k in order[pos:pos + per_step]]
             t = time.perf_counter()
-            oracle.sparse_train(oracle.OracleCfg(**cfg), acts[pos:pos + per_step],
-                                d.labels[pos:pos + per_step], n_epochs=1)
+            banks, bctr, fb = oracle.sparse_train_from(cfg, banks, bctr, fb, docs,
+                                                       d.labels[order[pos:pos + per_step]])
             pos += per_step
             if i >= args.warmup:
                 rates.append(per_step / (time.perf_counter() - t))
         value = float(np.mean(rates))
         metric = "SparseTM train documents/sec (configs[4])"
-        sample = f"{per_step}-document slices trained from the initial model, 1 thread"
+        sample = (f"{per_step} document(s) of epoch 1 per step with the full training set's "
+                  f"candidate set ({cands.size} literals), 1 thread; the reference's "
+                  "SparseClauseBank is pure Python, so its C restatement runs")
         cores = 1
         unit = "documents/s"
     else:
         (tx, ty), _ = c2_data(0)
-        cfg = oracle.OracleCfg(**datasets.mnist_shaped_config_kwargs(seed=0))
-        st = oracle.new_train_state(cfg)
-        x_lit = oracle.augment_literals(tx)
-        # the GPU arm times epochs 4..6; start from the same model after 3
-        # epochs (tests/golden/c2_epoch3.npz, trained by the oracle itself and
-        # matched bit for bit by the GPU trainer in the parity tests)
-        epoch = 1
-        fx = os.path.join(REPO, "tests", "golden", "c2_epoch3.npz")
-        if os.path.exists(fx):
-            g = np.load(fx)
-            st = oracle.OracleTrainState(g["states"].copy(), g["weights"].copy(),
-                                         g["block_counters"].copy(), int(g["fb_counter"]),
-                                         int(g["shuffle_counter"]))
-            epoch = 4
-        order, _ = oracle.shuffle_permutation(len(ty), oracle.derive_stream(0, 0xD157),
-                                              st.shuffle_counter)
+        kw = datasets.mnist_shaped_config_kwargs(seed=0)
+        # the GPU arm times epochs W+1..: start from the committed oracle
+        # checkpoint of epoch W (bit-identical to the GPU arm's model there,
+        # tests/test_gpu_parity.py) so the reference times the same epoch
+        ep, ck = _c2_checkpoint(args.warmup)
+        if tk is not None:
+            tr = RefTrainer(tk, kw, tx, ck)
+            order = tr.next_order()
+        else:
+            cfg = oracle.OracleCfg(**kw)
+            if ck is not None:
+                st = oracle.OracleTrainState(ck["states"].copy(), ck["weights"].copy(),
+                                             ck["block_counters"].copy(), int(ck["fb_counter"]),
+                                             int(ck["shuffle_counter"]))
+            else:
+                st = oracle.new_train_state(cfg)
+            x_lit = oracle.augment_literals(tx)
+            order, _ = oracle.shuffle_permutation(len(ty), oracle.derive_stream(0, 0xD157),
+                                                  st.shuffle_counter)
         rates, pos = [], 0
         per_step = args.ref_examples
         for i in range(args.warmup + args.steps):
+            if pos + per_step > len(ty):
+                break
             t = time.perf_counter()
-            oracle.train_steps(cfg, st, x_lit, ty, order[pos:pos + per_step])
+            if tk is not None:
+                tr.steps(ty, order[pos:pos + per_step])
+            else:
+                oracle.train_steps(cfg, st, x_lit, ty, order[pos:pos + per_step])
             pos += per_step
             if i >= args.warmup:
                 rates.append(per_step / (time.perf_counter() - t))
         value = float(np.mean(rates))
         metric = "train examples/sec (configs[1] MNIST-shaped CoTM training)"
-        sample = (f"{per_step} consecutive examples of epoch {epoch} per step (warm-up steps "
-                  f"advance the model), 1 thread: training is sequential (n_blocks=1)")
+        sample = (f"{per_step} consecutive examples of epoch {ep + 1} per step (warm-up steps "
+                  f"advance the model; the GPU arm's first timed epoch is {args.warmup + 1}), "
+                  f"from the committed epoch-{ep} checkpoint, 1 thread: training is "
+                  f"sequential (n_blocks=1)"
+                  + (" (tsetlinkit serial-driver loop, numba backend)" if tk else ""))
         cores = 1
+    cpu = {"value": value, "unit": unit, "cores": cores, "kind": kind, "sample": sample,
+           "host": model_name}
+    if tk is not None and kind == "reference":
+        from tsetlinkit import kernels as rk
+        cpu["reference"] = {"package": "tsetlinkit (baseline/_ref, unmodified)",
+                            "backend": rk.BACKEND_NAME}
+    cpu.update(extra)
     return {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "int8 / u64", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.workload},
-            "cpu_baseline": {"value": value, "unit": unit, "cores": cores,
-                             "kind": "port", "sample": sample, "host": model_name},
+            "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -1024,16 +1494,20 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2-train",
-                    choices=["c2-train", "c3-infer", "c4-train", "c5-sparse"])
+                    choices=["c1-train", "c2-train", "c3-infer", "c4-train", "c4-sweep",
+                             "c5-sparse"])
     ap.add_argument("--c3-examples", type=int, default=1 << 22)
     ap.add_argument("--c3-e2e-examples", type=int, default=1 << 20)
     ap.add_argument("--c3-cpu-examples", type=int, default=1 << 13)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-examples", type=int, default=1500)
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--sweep-examples", type=int, default=2500)
     ap.add_argument("--train-cta", type=int, default=0, help="0 = auto")
     ap.add_argument("--train-threads", type=int, default=0, help="0 = auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-port", action="store_true",
+                    help="reference arm: time the oracle port even when baseline/_ref exists")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -1054,8 +1528,12 @@ def main():
                      "warmup": args.warmup, "dtype": "u8 features / int32 votes",
                      "data": "synthetic (counter-based Bernoulli(0.5) generator)"})
         line["scaling"] = "strong"
+    elif args.workload == "c1-train":
+        line = bench_c1_train(args, rank, world, local)
     elif args.workload == "c4-train":
         line = bench_c4_train(args, rank, world, local)
+    elif args.workload == "c4-sweep":
+        line = bench_c4_sweep(args, rank, world, local)
     elif args.workload == "c5-sparse":
         line = bench_c5_sparse(args, rank, world, local)
     else:

@@ -65,6 +65,18 @@ uint64_t tmb_launch_count(void);
 int tmb_microbench_allreduce(int n_cta, int threads, int iters, int mode,
                              double *us_per_iter);
 
+/* Integer-pipe issue-rate microbenchmark (roofline denominators measured on
+ * the box): n_cta CTAs of `threads` threads run 8 dependent chains of one
+ * SASS opcode.  op: 0 LOP3, 1 IADD3, 2 SHF, 3 IMAD, 4 IMAD.WIDE, 5 POPC,
+ * 6 PRMT, 7 LOP3+IMAD interleaved, 8 SplitMix64 draw + compare.  Returns
+ * per-SM ops (lane-ops) per SM clock and the SM clock the CTAs saw. */
+int tmb_microbench_pipe(int op, int n_cta, int threads, int iters,
+                        double *ops_per_clk_per_sm, double *sm_mhz);
+/* Cross-SM signal latency through L2: two CTAs on different SMs bounce a
+ * counter (mode 0: st.relaxed.gpu, 1: red.relaxed.gpu.add); one hop = one
+ * write observed by the peer's ld.relaxed.gpu poll. */
+int tmb_microbench_pingpong(int mode, int hops, double *ns_per_hop, double *cycles_per_hop);
+
 /* SparseTM event-merge microbenchmark (design evidence):
  * one warp per CTA (n_warps warps per CTA) replays one event `reps` times on
  * synthetic sorted lists of n stored and n_act active literals held in

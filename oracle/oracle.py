@@ -425,14 +425,23 @@ class SparseOracleBank:
         return counter
 
 
-def sparse_train(cfg, examples_active, labels, n_epochs=1, max_steps=None):
+def sparse_train(cfg, examples_active, labels, n_epochs=1, max_steps=None, candidates=None,
+                 order=None, progress=None):
     """executor.train for a SparseDataset (executor.py:275-340 with the
-    sparse branches at :88-97, :287-289).  examples_active: list of sorted
-    int64 arrays.  Returns (banks per block, block counters, fb counter)."""
+    sparse branches at :88-97, :287-289).  examples_active: list (or any
+    indexable) of sorted int64 arrays.  candidates: the training set's
+    candidate literals when examples_active is only part of it (default: the
+    union of examples_active, sparse.py:65-69).  order: explicit example
+    order of ONE epoch instead of the shuffle (the caller applied
+    shuffle_permutation itself).  Returns (banks per block, block counters,
+    fb counter)."""
     ocfg = as_oracle_cfg(cfg)
     labels = np.asarray(labels, dtype=np.int64)
-    cands = (np.unique(np.concatenate(examples_active)) if len(examples_active)
-             else np.empty(0, np.int64))
+    if candidates is not None:
+        cands = np.asarray(candidates, dtype=np.int64)
+    else:
+        cands = (np.unique(np.concatenate(list(examples_active))) if len(examples_active)
+                 else np.empty(0, np.int64))
     ranges = partition_clauses(ocfg.n_clauses, ocfg.n_blocks)
     banks = [SparseOracleBank(ocfg, len(r), cands) for r in ranges]
     bseeds = [derive_stream(ocfg.seed, b) for b in range(ocfg.n_blocks)]
@@ -440,27 +449,51 @@ def sparse_train(cfg, examples_active, labels, n_epochs=1, max_steps=None):
     fb_seed = derive_stream(ocfg.seed, FEEDBACK_STREAM)
     sh_seed = derive_stream(ocfg.seed, SHUFFLE_STREAM)
     fb, sh = 0, 0
-    C, K = ocfg.n_clauses, ocfg.n_classes
     steps = 0
     for _ in range(n_epochs):
-        order, sh = shuffle_permutation(len(labels), sh_seed, sh)
-        for idx in order:
+        if order is None:
+            ep_order, sh = shuffle_permutation(len(labels), sh_seed, sh)
+        else:
+            ep_order = order
+        for idx in ep_order:
             if max_steps is not None and steps >= max_steps:
                 return banks, bctr, fb
-            act = examples_active[idx]
-            label = int(labels[idx])
-            outs = [bk.clause_outputs(act, True) for bk in banks]
-            votes = sum(o.astype(np.int64) @ bk.weights.astype(np.int64)
-                        for o, bk in zip(outs, banks))
-            u = stream_u01(fb_seed, fb)
-            neg, pt, pn = update_probabilities(votes, label, ocfg.threshold, u)
-            ut, un = sample_updates(pt, pn, C, fb_seed, fb + 1)
-            fb += 1 + 2 * C
-            for b, (bk, r) in enumerate(zip(banks, ranges)):
-                sl = slice(r.start, r.stop)
-                bctr[b] = bk.apply_feedback(act, outs[b], label, neg, ut[sl], un[sl],
-                                            bseeds[b], bctr[b])
+            if progress is not None:
+                progress(steps)
+            fb = _sparse_step(ocfg, banks, ranges, bseeds, bctr, fb_seed, fb,
+                              examples_active[idx], int(labels[idx]))
             steps += 1
+    return banks, bctr, fb
+
+
+def _sparse_step(ocfg, banks, ranges, bseeds, bctr, fb_seed, fb, act, label):
+    """One example of executor.py:326-330 on sparse banks; updates bctr in
+    place, returns the new feedback counter."""
+    C = ocfg.n_clauses
+    outs = [bk.clause_outputs(act, True) for bk in banks]
+    votes = sum(o.astype(np.int64) @ bk.weights.astype(np.int64)
+                for o, bk in zip(outs, banks))
+    u = stream_u01(fb_seed, fb)
+    neg, pt, pn = update_probabilities(votes, label, ocfg.threshold, u)
+    ut, un = sample_updates(pt, pn, C, fb_seed, fb + 1)
+    fb += 1 + 2 * C
+    for b, (bk, r) in enumerate(zip(banks, ranges)):
+        sl = slice(r.start, r.stop)
+        bctr[b] = bk.apply_feedback(act, outs[b], label, neg, ut[sl], un[sl],
+                                    bseeds[b], bctr[b])
+    return fb
+
+
+def sparse_train_from(cfg, banks, bctr, fb, docs, labels):
+    """Continue sparse training from a given state (banks per block, block
+    counters, feedback counter) over docs in the given order."""
+    ocfg = as_oracle_cfg(cfg)
+    ranges = partition_clauses(ocfg.n_clauses, ocfg.n_blocks)
+    bseeds = [derive_stream(ocfg.seed, b) for b in range(ocfg.n_blocks)]
+    fb_seed = derive_stream(ocfg.seed, FEEDBACK_STREAM)
+    bctr = [int(c) for c in bctr]
+    for act, label in zip(docs, labels):
+        fb = _sparse_step(ocfg, banks, ranges, bseeds, bctr, fb_seed, fb, act, int(label))
     return banks, bctr, fb
 
 

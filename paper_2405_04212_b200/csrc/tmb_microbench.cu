@@ -93,6 +93,36 @@ __global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
             __syncthreads();
             continue;
         }
+        if (mode >= 20 && mode < 64) {
+            // mode 20 + G: the trainer's packed (count << 40 | biased sum)
+            // arrival, spread over G groups (CTA r -> group r % G), each a
+            // 16 B slot in its own 256 B line; lanes 0..G-1 poll one slot
+            // each, the warp reduces the G partial words
+            const int G = mode - 20;
+            unsigned long long *base = slots + (size_t)i * G * 32;
+            if (threadIdx.x < 2)
+                mb_red(base + (blockIdx.x % G) * 32 + threadIdx.x, (1ull << 40) + 12345ull);
+            if (threadIdx.x < 32) {
+                const int g = threadIdx.x;
+                const unsigned long long want = g < G ? (unsigned long long)((n - g + G - 1) / G) : 0;
+                unsigned long long a = 0, b = 0;
+                bool done;
+                do {
+                    if (g < G)
+                        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                                     : "=l"(a), "=l"(b) : "l"(base + g * 32) : "memory");
+                    done = __all_sync(0xffffffffu, (a >> 40) == want && (b >> 40) == want);
+                } while (!done);
+                unsigned long long sa = a & 0xFFFFFFFFFFull, sb = b & 0xFFFFFFFFFFull;
+                for (int o = 16; o; o >>= 1) {
+                    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+                    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+                }
+                if (threadIdx.x == 0 && sa + sb == 1) slots[0] = 1;  // keep the sums live
+            }
+            __syncthreads();
+            continue;
+        }
         if (mode == 6 || mode == 7) {
             // slots: [4][n] x (mode 6: 2 words, mode 7: 1 word)
             const int ws = mode == 6 ? 2 : 1;
@@ -157,6 +187,80 @@ __global__ void k_mb_allreduce(unsigned long long *slots, int iters, int mode,
     if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = (unsigned long long)(clock64() - t0);
 }
 
+
+// ---------------------------------------------------------------------------
+// Integer-pipe issue rates (roofline denominators, measured on the box).
+// Every thread runs 8 interleaved dependent chains of ONE SASS opcode
+// (chains feed each other so nothing folds); 64 ops per loop trip.  One CTA
+// per SM; clock64 gives the SM clocks the CTA ran for.
+//   op 0 LOP3   1 IADD3   2 SHF   3 IMAD   4 IMAD.WIDE   5 POPC   6 PRMT
+//   op 7 LOP3 + IMAD interleaved (ALU and FMA pipes issuing together)
+//   op 8 one SplitMix64 draw + threshold compare per "op" (the trainers'
+//        per-literal unit of work)
+template <int OP>
+__global__ void k_mb_pipe(int iters, unsigned seed, unsigned long long *sink,
+                          unsigned long long *cycles) {
+    unsigned x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = seed * (threadIdx.x + 1) + c * 0x9E3779B9u + blockIdx.x;
+    const unsigned y = seed ^ threadIdx.x, sel = 0x3210u + (seed & 0x1111u);
+    unsigned long long w[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) w[c] = x[c];
+    unsigned long long acc = 0;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const unsigned o = x[(c + 1) & 7];
+                if (OP == 0) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(o), "r"(y));
+                if (OP == 1) asm volatile("{.reg .u32 t; add.u32 t, %0, %1; add.u32 %0, t, %2;}" : "+r"(x[c]) : "r"(o), "r"(y));
+                if (OP == 2) asm volatile("shf.l.wrap.b32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(o), "r"(y));
+                if (OP == 3) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(o), "r"(y));
+                if (OP == 4) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[c]) : "r"((unsigned)w[(c + 1) & 7]), "r"(y));
+                if (OP == 5) asm volatile("popc.b32 %0, %1;" : "=r"(x[c]) : "r"(o));
+                if (OP == 6) asm volatile("prmt.b32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(o), "r"(sel));
+                if (OP == 7) {
+                    if (c & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(o), "r"(y));
+                    else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(o), "r"(y));
+                }
+                if (OP == 8) {
+                    w[c] += 0x9E3779B97F4A7C15ull;
+                    acc += (mix64(w[c]) >> 11) < 0x1999999999999ull;
+                }
+            }
+        }
+    }
+    const long long t1 = clock64();
+    unsigned long long r = acc;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) r += x[c] + w[c];
+    if (r == 0x1234567ull) sink[0] = r;
+    if (threadIdx.x == 0) cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+}
+
+// Cross-SM signal latency through L2 (the hardware floor under any
+// per-example grid exchange): CTA 0 and CTA 1 (different SMs) bounce a
+// counter through one global word: each waits for its turn with
+// ld.relaxed.gpu polls and answers with st.relaxed.gpu (mode 0) or
+// red.relaxed.gpu.add (mode 1).  One hop = one write observed by the peer.
+__global__ void k_mb_pingpong(unsigned long long *word, int hops, int mode,
+                              unsigned long long *cycles) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long me = blockIdx.x;
+    const long long t0 = clock64();
+    for (unsigned long long h = me; h < (unsigned long long)hops; h += 2) {
+        while (mb_ld(word) != h) {}
+        if (mode == 0)
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(word), "l"(h + 1) : "memory");
+        else
+            mb_red(word, 1ull);
+    }
+    if (me == 0) *cycles = (unsigned long long)(clock64() - t0);
+}
+
 }  // namespace tmb
 
 using namespace tmb;
@@ -166,7 +270,9 @@ extern "C" int tmb_microbench_allreduce(int n_cta, int threads, int iters, int m
     int rc = require_device();
     if (rc) return rc;
     unsigned long long *slots = nullptr, *cyc = nullptr;
-    size_t words = (mode == 6 || mode == 7) ? (size_t)8 * n_cta : (size_t)iters * (mode == 2 ? 8 * 32 : 32);
+    size_t words = (mode == 6 || mode == 7) ? (size_t)8 * n_cta
+                   : (mode >= 20 && mode < 64) ? (size_t)iters * (mode - 20) * 32
+                   : (size_t)iters * (mode == 2 ? 8 * 32 : 32);
     TMB_CUDA(cudaMalloc(&slots, 8 * words));
     TMB_CUDA(cudaMalloc(&cyc, 8));
     TMB_CUDA(cudaMemset(slots, 0, 8 * words));
@@ -185,6 +291,92 @@ extern "C" int tmb_microbench_allreduce(int n_cta, int threads, int iters, int m
     if (!rc) *us_per_iter = (double)ms * 1e3 / iters;
     cudaFree(slots);
     cudaFree(cyc);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return rc;
+}
+
+template <int OP>
+static int run_pipe(int n_cta, int threads, int iters, double *ops_per_clk_per_sm, double *sm_mhz) {
+    unsigned long long *buf = nullptr;
+    TMB_CUDA(cudaMalloc(&buf, 8 * (size_t)(n_cta + 1)));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    int rc = 0;
+    float ms = 0;
+    for (int rep = 0; rep < 2 && !rc; ++rep) {  // rep 0 warms up
+        cudaEventRecord(a);
+        k_mb_pipe<OP><<<n_cta, threads>>>(iters, 0x2545F491u, buf, buf + 1);
+        cudaEventRecord(b);
+        rc = check_cuda(cudaEventSynchronize(b), "pipe microbench");
+        cudaEventElapsedTime(&ms, a, b);
+    }
+    if (!rc) {
+        unsigned long long *cyc = (unsigned long long *)malloc(8 * (size_t)n_cta);
+        rc = check_cuda(cudaMemcpy(cyc, buf + 1, 8 * (size_t)n_cta, cudaMemcpyDeviceToHost), "copy");
+        double mean = 0;
+        for (int i = 0; i < n_cta; ++i) mean += (double)cyc[i];
+        mean /= n_cta;
+        const double ops_per_cta = (double)threads * iters * 64;
+        *ops_per_clk_per_sm = ops_per_cta / mean;
+        *sm_mhz = mean / ((double)ms * 1e3);  // cycles per us, the busy SMs' clock
+        free(cyc);
+    }
+    cudaFree(buf);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return rc;
+}
+
+extern "C" int tmb_microbench_pipe(int op, int n_cta, int threads, int iters,
+                                   double *ops_per_clk_per_sm, double *sm_mhz) {
+    int rc = require_device();
+    if (rc) return rc;
+    switch (op) {
+        case 0: return run_pipe<0>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        case 1: return run_pipe<1>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        case 2: return run_pipe<2>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        case 3: return run_pipe<3>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        case 4: return run_pipe<4>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        case 5: return run_pipe<5>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        case 6: return run_pipe<6>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        case 7: return run_pipe<7>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        case 8: return run_pipe<8>(n_cta, threads, iters, ops_per_clk_per_sm, sm_mhz);
+        default: return fail(TMB_E_INVALID, "tmb_microbench_pipe: op must be 0..8");
+    }
+}
+
+extern "C" int tmb_microbench_pingpong(int mode, int hops, double *ns_per_hop,
+                                       double *cycles_per_hop) {
+    int rc = require_device();
+    if (rc) return rc;
+    unsigned long long *buf = nullptr;
+    TMB_CUDA(cudaMalloc(&buf, 16));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float ms = 0;
+    for (int rep = 0; rep < 2 && !rc; ++rep) {
+        cudaMemset(buf, 0, 16);
+        void *args[] = {&buf, &hops, &mode, (void *)nullptr};
+        unsigned long long *cyc = buf + 1;
+        args[3] = &cyc;
+        cudaEventRecord(a);
+        // cooperative launch: both CTAs are guaranteed co-resident
+        rc = check_cuda(cudaLaunchCooperativeKernel((const void *)k_mb_pingpong, dim3(2), dim3(32),
+                                                    args, 0, 0), "pingpong launch");
+        cudaEventRecord(b);
+        if (!rc) rc = check_cuda(cudaEventSynchronize(b), "pingpong");
+        cudaEventElapsedTime(&ms, a, b);
+    }
+    if (!rc) {
+        unsigned long long cyc = 0;
+        rc = check_cuda(cudaMemcpy(&cyc, buf + 1, 8, cudaMemcpyDeviceToHost), "copy");
+        *ns_per_hop = (double)ms * 1e6 / hops;
+        *cycles_per_hop = (double)cyc / hops;
+    }
+    cudaFree(buf);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     return rc;

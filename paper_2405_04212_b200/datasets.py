@@ -125,6 +125,36 @@ def inference_examples(data_seed: int, start: int, count: int, n_features: int =
     return np.ascontiguousarray(bits[:, :n_features])
 
 
+def inference_examples_device(data_seed: int, start: int, count: int, n_features: int = 4096,
+                              packed: bool = False):
+    """Device twin of ``inference_examples`` (same bits): the stream words are
+    filled by tmb_stream_u64_block on the current stream and expanded to
+    uint8 [count, F] (or returned as int64 [count, W] words when packed)."""
+    import torch
+
+    from . import _lib
+    from .runtime import ptr, stream_ptr
+    W = (n_features + 63) // 64
+    seed = inference_stream_seed(data_seed)
+    if packed:
+        words = torch.empty((count, W), dtype=torch.int64, device="cuda")
+        _lib.call("tmb_stream_u64_block", seed, start * W, count * W, ptr(words), stream_ptr())
+        return words
+    x = torch.empty((count, n_features), dtype=torch.uint8, device="cuda")
+    chunk = 1 << 18
+    shifts = torch.arange(8, device="cuda", dtype=torch.uint8)
+    for lo in range(0, count, chunk):
+        m = min(chunk, count - lo)
+        words = torch.empty(m * W, dtype=torch.int64, device="cuda")
+        _lib.call("tmb_stream_u64_block", seed, (start + lo) * W, m * W, ptr(words),
+                  stream_ptr())
+        b = words.view(torch.uint8).view(m, W * 8)
+        bits = (b.unsqueeze(-1) >> shifts) & 1
+        x[lo:lo + m] = bits.view(m, W * 64)[:, :n_features]
+        del words, b, bits
+    return x
+
+
 @dataclass
 class InferenceModel:
     states: np.ndarray   # int8 [C, 2F]: 0 = include, -1 = exclude

@@ -23,6 +23,28 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def csr_shard(indptr: np.ndarray, world: int, rank: int) -> tuple[int, int]:
+    """Row range [lo, hi) of a CSR matrix for `rank` of `world`, balanced by
+    non-zeros (the work of sparse inference is per posting): rank r starts
+    at the first row whose prefix nnz reaches r/world of the total."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world / rank")
+    indptr = np.asarray(indptr, dtype=np.int64)
+    n = indptr.size - 1
+    nnz = int(indptr[-1]) if n > 0 else 0
+
+    def start(r):
+        if r <= 0:
+            return 0
+        if r >= world:
+            return n
+        if nnz == 0:
+            return n * r // world
+        return int(np.searchsorted(indptr[:n], nnz * r // world, side="left"))
+
+    return start(rank), start(rank + 1)
+
+
 def jobs_of(n_jobs: int, world: int, rank: int) -> list[int]:
     """Round-robin job assignment (job j -> rank j mod world)."""
     return list(range(rank, n_jobs, world))
@@ -103,3 +125,18 @@ def sharded_predict(model, x: np.ndarray, group=None) -> np.ndarray:
     lo, hi = shard_range(x.shape[0], world, rank)
     _, pred = model.votes_and_pred(x[lo:hi], want_votes=False)
     return gather_rows(pred, x.shape[0], group)
+
+
+def sharded_sparse_predict(engine, indptr: np.ndarray, indices: np.ndarray, group=None):
+    """Predictions of a device sparse model (sparse_train.SparseEngine) for a
+    CSR document set, rows split over the ranks by csr_shard (each rank
+    evaluates only its rows on its GPU), gathered once."""
+    import torch
+    world, rank = world_info(group)
+    lo, hi = csr_shard(indptr, world, rank)
+    a, b = int(indptr[lo]), int(indptr[hi])
+    ip = torch.from_numpy(np.ascontiguousarray(indptr[lo:hi + 1] - a, dtype=np.int64)).cuda()
+    ix = torch.from_numpy(np.ascontiguousarray(
+        indices[a:b] if b > a else np.zeros(1, np.int32), dtype=np.int32)).cuda()
+    _, pred = engine.votes_and_pred(ip, ix, hi - lo)
+    return gather_rows(pred.cpu().numpy(), indptr.size - 1, group)

@@ -1,0 +1,187 @@
+"""GPU parity at the BENCHMARKED sizes (BASELINE.json configs[2]/[3]/[4]):
+every number bench.py reports rides on these.
+
+* configs[2]: all 2^22 examples of the bench workload (data_seed 3,
+  model_seed 11) against the oracle's votes for every example
+  (tests/golden/c3_full.npz, written once by tests/golden/make_c3_full.py).
+* configs[3]: the full 10^4-clause x 2*10^4-position bag-of-words trainer
+  against the oracle, and trainers whose block counters start just below
+  2^32 so the Type I window base (counter << 32, core.py:141-145) wraps
+  mod 2^64 inside the run.
+* configs[4]: SparseTM at the full shape (10^6-literal universe, the
+  candidate set of the whole 10^6-document training set) against a
+  one-time oracle fixture (tests/golden/c5_prefix.npz).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _have(name):
+    return os.path.exists(os.path.join(GOLDEN, name + ".npz"))
+
+
+# ------------------------------------------------------------ configs[2] --
+
+@pytest.mark.skipif(not _have("c3_full"), reason="c3_full fixture not generated")
+def test_configs2_all_2pow22_examples_vs_oracle(gpu):
+    """Votes and predictions of all 2^22 configs[2] examples equal the
+    oracle's (DenseClauseBank.batch_votes, dense.py:171-174, + argmax with
+    ties to the lowest class, executor.py:382).  The fixture stores the
+    oracle's votes of every example with a non-zero vote row; all others are
+    zero rows with prediction 0."""
+    import torch
+    g = golden("c3_full")
+    N = int(g["n"])
+    F, C, K = 4096, 10000, 10
+    m = gpu.datasets.inference_model(model_seed=int(g["model_seed"]), n_features=F,
+                                     n_clauses=C, n_classes=K)
+    bank = gpu.DenseClauseBank(gpu.Config(n_literals=F, n_clauses=C, n_classes=K, s=2.0,
+                                          threshold=100))
+    bank.states[:] = m.states
+    bank.weights[:] = m.weights
+    model = gpu.CompiledModel.from_bank(bank)
+    idx = torch.from_numpy(g["index"].astype(np.int64)).cuda()
+    want = torch.from_numpy(g["votes"].astype(np.int64)).cuda()
+    chunk = 1 << 20
+    n_nonzero = 0
+    pred_sums = []
+    for lo in range(0, N, chunk):
+        cnt = min(chunk, N - lo)
+        x = gpu.datasets.inference_examples_device(int(g["data_seed"]), lo, cnt, F)
+        votes = torch.empty((cnt, K), dtype=torch.int64, device="cuda")
+        pred = torch.empty(cnt, dtype=torch.int64, device="cuda")
+        model.infer_device(x, votes_dev=votes, pred_dev=pred)
+        sel = (idx >= lo) & (idx < lo + cnt)
+        li = idx[sel] - lo
+        assert torch.equal(votes[li], want[sel]), f"votes differ in [{lo}, {lo + cnt})"
+        nz = torch.zeros(cnt, dtype=torch.bool, device="cuda")
+        nz[li] = True
+        assert not votes[~nz].any(), f"unexpected non-zero votes in [{lo}, {lo + cnt})"
+        assert torch.equal(pred, torch.argmax(votes, dim=1)), "prediction is not argmax"
+        n_nonzero += int(li.numel())
+        ps = pred.view(-1, int(g["chunk"])).sum(dim=1) if cnt % int(g["chunk"]) == 0 else None
+        if ps is not None:
+            pred_sums.extend(ps.cpu().tolist())
+        del x, votes, pred
+    assert n_nonzero == g["index"].size
+    assert pred_sums == g["pred_chunk_sums"].tolist()
+    # the packed-input kernel gives the same predictions on a full-size slice
+    xb = gpu.datasets.inference_examples_device(int(g["data_seed"]), 0, chunk, F, packed=True)
+    pb = torch.empty(chunk, dtype=torch.int64, device="cuda")
+    vb = torch.empty((chunk, K), dtype=torch.int64, device="cuda")
+    model.infer_device_packed(xb, votes_dev=vb, pred_dev=pb)
+    sel = idx < chunk
+    assert torch.equal(vb[idx[sel]], want[sel])
+    assert int((vb != 0).any(dim=1).sum()) == int(sel.sum())
+
+
+# ------------------------------------------------------------ configs[3] --
+
+@pytest.fixture(scope="module")
+def bow():
+    import paper_2405_04212_b200 as tmb
+    return tmb.datasets.bag_of_words(n_train=400, n_test=10)
+
+
+def _oracle_state(oracle, cfg, counter0):
+    st = oracle.new_train_state(cfg)
+    st.block_counters[:] = np.uint64(counter0)
+    return st
+
+
+def test_configs3_full_shape_vs_oracle(gpu, oracle, bow):
+    """configs[3] model (10^4 clauses, 2*10^4 positions, K=2, T=10^4, s=2):
+    the first 60 steps of epoch 1 through the production trainer (states
+    HBM-resident, grid-balanced feedback) equal the oracle's model and
+    counters."""
+    (tx, ty), _ = bow
+    cfg = gpu.Config(**gpu.datasets.bag_of_words_config_kwargs(seed=3))
+    sess = gpu.DenseTrainSession(cfg, tx, ty)
+    order = sess.next_order()[:60]
+    import torch
+    sess.run_steps(torch.from_numpy(order.astype(np.int32)).cuda())
+    m = sess.model()
+    st = oracle.new_train_state(cfg)
+    oracle.train_steps(cfg, st, oracle.augment_literals(tx), ty, order.astype(np.int64))
+    assert np.array_equal(m.states, st.states)
+    assert np.array_equal(m.weights, st.weights)
+    assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64), st.block_counters)
+    assert sess.fb_counter == st.fb_counter
+    ev = sess.stats_dict()["events"]
+    assert ev == int(st.block_counters[0]) and ev > 60 * 1000  # thousands of events per step
+
+
+@pytest.mark.parametrize("shape,n_blocks,n_cta", [
+    ("c4", 1, 0), ("c2", 1, 148), ("c2", 3, 148), ("c2", 1, 8)])
+def test_window_base_wraps_at_2pow32(gpu, oracle, bow, shape, n_blocks, n_cta):
+    """Block counters start at 2^32 - 3: the Type I window base
+    (counter << 32) wraps mod 2^64 after three events (core.py:141-145,
+    kernels/_numba.py:110,121; SURVEY A.1 -- configs[3] reaches it after
+    ~17 epochs).  Production trainers (configs[3] generic grid kernel;
+    configs[1] fast kernel with 1 block, generic with 3 blocks, cluster mode)
+    against the oracle."""
+    import torch
+    if shape == "c4":
+        (tx, ty), _ = bow
+        kw = gpu.datasets.bag_of_words_config_kwargs(seed=5)
+        steps = 20
+    else:
+        (tx, ty), _ = gpu.datasets.mnist_shaped(n_train=600, n_test=10, data_seed=3)
+        kw = gpu.datasets.mnist_shaped_config_kwargs(seed=6)
+        steps = 600
+    kw["n_blocks"] = n_blocks
+    cfg = gpu.Config(**kw)
+    c0 = (1 << 32) - 3
+    sess = gpu.DenseTrainSession(cfg, tx, ty, n_cta=n_cta)
+    sess.block_counters.fill_(c0)
+    order = sess.next_order()[:steps]
+    sess.run_steps(torch.from_numpy(order.astype(np.int32)).cuda())
+    m = sess.model()
+    st = _oracle_state(oracle, cfg, c0)
+    oracle.train_steps(cfg, st, oracle.augment_literals(tx), ty, order.astype(np.int64))
+    got_ctr = sess.block_counters.cpu().numpy().view(np.uint64)
+    assert np.array_equal(got_ctr, st.block_counters)
+    assert (got_ctr > np.uint64(1 << 32)).all(), "the run must cross the wrap"
+    assert np.array_equal(m.weights, st.weights)
+    assert np.array_equal(m.states, st.states)
+
+
+# ------------------------------------------------------------ configs[4] --
+
+@pytest.mark.skipif(not _have("c5_prefix"), reason="c5_prefix fixture not generated")
+def test_configs4_full_shape_prefix_vs_oracle(gpu):
+    """configs[4] at the bench's full shape: the 10^6-document Zipf(1.05)
+    training set's candidate set (~10^6 literals), 2000 clauses, capacity 64,
+    floor -15, T=2000, s=5: the first documents of epoch 1 against the
+    oracle's model (lists, states, weights, counters), and the accuracy both
+    models reach on held-out documents (tests/golden/make_c5_prefix.py)."""
+    import torch
+
+    from paper_2405_04212_b200.sparse_train import SparseTrainSession
+    g = golden("c5_prefix")
+    cfg = gpu.Config(**gpu.datasets.sparse_config_kwargs(seed=int(g["seed"])))
+    cands = np.flatnonzero(np.unpackbits(g["cand_bits"], bitorder="little"))
+    cands = cands[cands < cfg.n_literals]
+    sess = SparseTrainSession(cfg, g["indptr"], g["indices"], g["labels"], candidates=cands)
+    sess.run_steps(torch.arange(len(g["labels"]), dtype=torch.int32, device="cuda"))
+    m = sess.model()
+    ptr_, lits, sts = g["m_ptr"], g["m_lits"], g["m_sts"]
+    for j in range(cfg.n_clauses):
+        a, b = ptr_[j], ptr_[j + 1]
+        assert np.array_equal(m.clause_literals[j], lits[a:b]), j
+        assert np.array_equal(m.clause_states[j], sts[a:b]), j
+    assert np.array_equal(m.weights, g["weights"])
+    _, _, _, bc = sess.engine.get_lists()
+    assert np.array_equal(bc, g["bctr"])
+    # held-out accuracy of the trained model: identical predictions
+    ex = [gpu.SparseExample(g["t_indices"][g["t_indptr"][i]:g["t_indptr"][i + 1]], 0)
+          for i in range(len(g["t_labels"]))]
+    votes = m.batch_votes(ex)
+    assert np.array_equal(votes, g["t_votes"])

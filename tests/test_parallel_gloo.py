@@ -34,6 +34,23 @@ def _oracle_eval(st, data):
     return float(np.mean(pred == np.asarray(y)))
 
 
+def _sparse_case():
+    """A trained oracle sparse bank and ragged documents (some empty)."""
+    from oracle import oracle
+
+    from paper_2405_04212_b200.core import Config
+    rng = np.random.default_rng(3)
+    docs = []
+    for i in range(90):
+        n = 0 if i % 17 == 0 else int(rng.integers(1, 40))
+        docs.append(np.sort(rng.choice(300, size=n, replace=False)).astype(np.int64))
+    labels = np.array([int(np.isin(d, np.arange(20)).sum() > 1) for d in docs])
+    cfg = Config(n_literals=300, n_clauses=12, n_classes=2, s=3.0, threshold=10, seed=4,
+                 negated_literals_enabled=False, sparse_capacity=8)
+    banks, _, _ = oracle.sparse_train(cfg, docs, labels, n_epochs=2)
+    return banks[0], docs
+
+
 def _worker(rank, world, port, out_dir):
     import sys
     sys.path.insert(0, REPO)
@@ -60,9 +77,20 @@ def _worker(rank, world, port, out_dir):
     # sharded rows
     lo, hi = parallel.shard_range(101, world, rank)
     rows = parallel.gather_rows(np.arange(lo, hi), 101)
+    # sharded sparse inference (configs[4] path): nnz-balanced CSR row shards,
+    # each rank votes its rows (oracle bank standing in for the device engine),
+    # predictions gathered once
+    bank, docs = _sparse_case()
+    ip = np.zeros(len(docs) + 1, dtype=np.int64)
+    np.cumsum([len(a) for a in docs], out=ip[1:])
+    slo, shi = parallel.csr_shard(ip, world, rank)
+    from oracle import oracle
+    v = oracle.sparse_batch_votes([bank], docs[slo:shi])
+    spred = parallel.gather_rows(np.argmax(v, axis=1), len(docs))
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), accs=np.array(accs),
              cv=np.array(rep.fold_accuracies), folds=rep.fold_assignments, rows=rows,
-             search=np.array([[t.index, t.accuracy] for t in trials]))
+             search=np.array([[t.index, t.accuracy] for t in trials]), spred=spred,
+             sshard=np.array([slo, shi]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -72,9 +100,15 @@ def test_sweep_cv_and_sharding_over_two_gloo_ranks(tmp_path):
     mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     r0 = np.load(tmp_path / "r0.npz")
     r1 = np.load(tmp_path / "r1.npz")
-    for key in ("accs", "cv", "folds", "rows", "search"):
+    for key in ("accs", "cv", "folds", "rows", "search", "spred"):
         assert np.array_equal(r0[key], r1[key]), key
     assert np.array_equal(r0["rows"], np.arange(101))
+    # the two shards tile the documents; gathered predictions == unsharded
+    assert r0["sshard"][0] == 0 and r0["sshard"][1] == r1["sshard"][0]
+    bank, docs = _sparse_case()
+    assert r1["sshard"][1] == len(docs)
+    from oracle import oracle
+    assert np.array_equal(r0["spred"], np.argmax(oracle.sparse_batch_votes([bank], docs), axis=1))
     # single-process reference for the same jobs
     import sys
     sys.path.insert(0, REPO)
@@ -101,6 +135,19 @@ def test_shard_and_job_assignment():
             ranges = [parallel.shard_range(n, world, r) for r in range(world)]
             assert ranges[0][0] == 0 and ranges[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    # nnz-balanced CSR shards: contiguous, covering, within one row of balance
+    rng = np.random.default_rng(1)
+    for n in (0, 1, 5, 1000):
+        lens = rng.integers(0, 200, size=n)
+        ip = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(lens, out=ip[1:])
+        for world in (1, 2, 3, 8):
+            rs = [parallel.csr_shard(ip, world, r) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            if n:
+                loads = [ip[b] - ip[a] for a, b in rs]
+                assert max(loads) - ip[-1] / world <= lens.max(initial=0) + 1
     jobs = [parallel.jobs_of(8, 3, r) for r in range(3)]
     assert sorted(j for js in jobs for j in js) == list(range(8))
 
