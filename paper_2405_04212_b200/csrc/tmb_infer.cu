@@ -18,24 +18,10 @@
 
 #include "tmb_common.cuh"
 #include "tmb_device.cuh"
+#include "tmb_infer.cuh"
 
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
-
-struct tmb_rules {
-    int64_t R = 0, K = 0, F = 0, n_inc = 0;
-    int negations = 0;
-    uint32_t *inc = nullptr;     // device [n_inc]: (feature << 1) | negated
-    int64_t *ptr = nullptr;      // device [R+1]
-    int32_t *weights = nullptr;  // device [R, K]
-    // head/tail form for the cluster kernel (uint16 codes; F + 1 < 32768):
-    // the first 16 include codes of every rule, padded with the always-true
-    // code (F << 1) that addresses an all-ones X^T row; the rest in a CSR tail
-    uint16_t *heads = nullptr;   // device [R, 16]
-    int32_t *tail_ptr = nullptr; // device [R+1]
-    uint16_t *tails = nullptr;   // device [n_tail]
-    int heads_ok = 0;
-};
 
 namespace tmb {
 
@@ -191,105 +177,6 @@ struct InferCK {
     int eval_mode;       // k_infer_ws evaluators: 2 = loads of dead rules skipped from code
                          // 8 on (default), 3 = same without early-exit votes, 0 = plain
 };
-
-__device__ __forceinline__ uint32_t pack8(unsigned long long q) {
-    return (uint32_t)(((q & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56);
-}
-
-// ---- mbarrier / bulk-copy helpers (shared::cta / shared::cluster, sm_90+)
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *mb, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arm(uint64_t *mb, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
-                 "r"(bytes) : "memory");
-}
-// try_wait suspend-time hint: a waiting warp is parked until the phase
-// completes instead of re-polling (spin loops were ~16% of all issued
-// instructions of the warp-specialised inference kernel)
-constexpr uint32_t kSuspendNs = 0x989680;
-__device__ __forceinline__ void mbar_wait(uint64_t *mb, uint32_t parity) {
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
-            " selp.u32 %0, 1, 0, p;\n}"
-            : "=r"(done) : "r"(smem_u32(mb)), "r"(parity), "r"(kSuspendNs) : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, uint32_t src_cta,
-                                                  uint32_t bytes, uint32_t mbar_cluster) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"(dst_cluster), "r"(src_cta), "r"(bytes), "r"(mbar_cluster) : "memory");
-}
-
-// shared-window atomic (a generic-pointer atomicAdd on a pointer derived from
-// the mbarrier area compiles to a generic ATOM, not ATOMS)
-__device__ __forceinline__ uint32_t atom_add_shared(void *p, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
-    return old;
-}
-// predicated 16-byte shared load into v (v unchanged when !p)
-__device__ __forceinline__ void lds128_if(uint4 &v, bool p, uint32_t addr) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %4, 0;\n"
-                 " @q ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n}"
-                 : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w) : "r"((uint32_t)p), "r"(addr));
-}
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-    return v;
-}
-
-// 4 bytes of 0/1 -> 4 bits (bit t = byte t)
-__device__ __forceinline__ uint32_t pack4(uint32_t w) {
-    return ((w & 0x01010101u) * 0x01020408u) >> 24;
-}
-
-// 8x8 bit-matrix transpose: byte i = row i (bit t = column t) -> byte t =
-// column t (bit i = row i)
-__device__ __forceinline__ unsigned long long transpose8x8(unsigned long long x) {
-    unsigned long long t;
-    t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
-    x = x ^ t ^ (t << 7);
-    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
-    x = x ^ t ^ (t << 14);
-    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
-    x = x ^ t ^ (t << 28);
-    return x;
-}
-
-// up to 8 feature bytes starting at column f (bounds-checked against F)
-__device__ __forceinline__ unsigned long long load8_tail(const uint8_t *src, int64_t f, int64_t F) {
-    unsigned long long v = 0;
-    for (int bb = 0; bb < 8; ++bb)
-        if (f + bb < F) v |= (unsigned long long)src[bb] << (8 * bb);
-    return v;
-}
-
-// 32x32 bit transpose across the warp: lane i holds row i (bit j = A[i][j]);
-// afterwards lane j holds column j (bit i = A[i][j]).
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
-#pragma unroll
-    for (int j = 16; j >= 1; j >>= 1) {
-        const uint32_t m0 = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
-                          : j == 2 ? 0x33333333u : 0x55555555u;
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-        x = (lane & j) ? ((x & ~m0) | ((y >> j) & m0)) : ((x & m0) | ((y << j) & ~m0));
-    }
-    return x;
-}
 
 __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
     extern __shared__ __align__(16) char smem_raw[];
@@ -615,32 +502,6 @@ __global__ void __launch_bounds__(512, 1) k_infer_cluster(InferCK k) {
 //   empty[b]  (per CTA)  the 4 CTAs' evaluator groups are done with buffer b
 //   vfull[b]  (owner)    the 4 CTAs pushed their partial sums for block b
 //   vempty[b] (writer)   the 4 owners consumed this CTA's partials of slot b
-__device__ __forceinline__ void mbar_arrive_local(uint64_t *mb) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mb)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t mb_cluster) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mb_cluster)
-                 : "memory");
-}
-// arrival that publishes nothing (the barrier only orders reads before it)
-__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t mb_cluster) {
-    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mb_cluster)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *mb, uint32_t parity) {
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}"
-            : "=r"(done) : "r"(smem_u32(mb)), "r"(parity) : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-
 // 5 warpgroups: warpgroups 0-1 re-allocated to 128 registers per thread
 // (setmaxnreg) -- 7 transposer warps, whose loads in flight live in
 // registers, and 1 evaluator warp -- and warpgroups 2-4 to 72 (11 more
@@ -1334,6 +1195,12 @@ int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes
         TMB_CUDA(cudaMalloc(&g_bad_flag, sizeof(unsigned)));
         TMB_CUDA(cudaMemset(g_bad_flag, 0, sizeof(unsigned)));
     }
+    if (!g_force_generic_infer && r->sheads_ok) {
+        bool launched = false;
+        int rc = launch_infer_solo(r, x, nullptr, 0, N, votes, pred, labels, correct, g_bad_flag,
+                                   st, &launched);
+        if (rc || launched) return rc;
+    }
     if (!g_force_generic_infer && r->heads_ok) {
         bool launched = false;
         int rc = launch_infer_cluster(r, x, N, votes, pred, labels, correct, st, &launched);
@@ -1542,6 +1409,10 @@ static int upload_rules(const std::vector<int64_t> &ptr, const std::vector<uint3
         if (!tails.empty()) cudaMemcpy(r->tails, tails.data(), 2 * tails.size(), cudaMemcpyHostToDevice);
         r->heads_ok = 1;
     }
+    if ((rc = build_solo_heads(ptr, inc, r->R, F, r))) {
+        tmb_rules_destroy(r);
+        return rc;
+    }
     cudaMemcpy(r->ptr, ptr.data(), 8 * ptr.size(), cudaMemcpyHostToDevice);
     if (!inc.empty()) cudaMemcpy(r->inc, inc.data(), 4 * inc.size(), cudaMemcpyHostToDevice);
     if (!w.empty()) cudaMemcpy(r->weights, w.data(), 4 * w.size(), cudaMemcpyHostToDevice);
@@ -1625,6 +1496,9 @@ int tmb_rules_destroy(tmb_rules *r) {
     if (r->heads) cudaFree(r->heads);
     if (r->tail_ptr) cudaFree(r->tail_ptr);
     if (r->tails) cudaFree(r->tails);
+    if (r->sheads) cudaFree(r->sheads);
+    if (r->stail_ptr) cudaFree(r->stail_ptr);
+    if (r->stails) cudaFree(r->stails);
     delete r;
     return TMB_OK;
 }
@@ -1654,12 +1528,16 @@ int tmb_infer_packed(const tmb_rules *r, const uint64_t *xb, int64_t N, int64_t 
     if (!r || N < 0 || (N > 0 && !xb) || (labels && !correct) || W64 * 64 < r->F)
         return fail(TMB_E_INVALID, "infer_packed: bad arguments");
     if (N == 0) return TMB_OK;
-    if (!r->heads_ok) return fail(TMB_E_UNSUPPORTED, "infer_packed: rule set needs the cluster kernel");
+    if (!r->heads_ok && !r->sheads_ok)
+        return fail(TMB_E_UNSUPPORTED, "infer_packed: rule set needs the cluster or solo kernel");
     if (!g_bad_flag) {
         TMB_CUDA(cudaMalloc(&g_bad_flag, sizeof(unsigned)));
         TMB_CUDA(cudaMemset(g_bad_flag, 0, sizeof(unsigned)));
     }
     bool launched = false;
+    rc = launch_infer_solo(r, nullptr, xb, W64, N, votes, pred, labels,
+                           (unsigned long long *)correct, g_bad_flag, as_stream(stream), &launched);
+    if (rc || launched) return rc;
     rc = launch_infer_cluster(r, nullptr, N, votes, pred, labels, (unsigned long long *)correct,
                               as_stream(stream), &launched, xb, W64);
     if (rc) return rc;
@@ -1716,6 +1594,10 @@ int tmb_set_option(const char *name, int64_t value) {
     }
     if (std::string(name) == "sparse.resident") {  // 0: keep clause lists in global memory
         g_sparse_resident = (int)value;            // (applies to banks created afterwards)
+        return TMB_OK;
+    }
+    if (std::string(name) == "infer.solo") {  // 0: the 4-CTA cluster kernels instead
+        g_infer_solo = (int)value;
         return TMB_OK;
     }
     if (std::string(name) == "infer.warp_specialized") {

@@ -313,16 +313,17 @@ def test_inference_random_models_vs_oracle(gpu, oracle, n_inc, F, K):
     assert np.array_equal(pred, op)
 
 
-@pytest.mark.parametrize("kernel", ["ws", "ws_plain", "ws_noexit", "cluster", "generic"])
+@pytest.mark.parametrize("kernel", ["solo", "ws", "ws_plain", "ws_noexit", "cluster", "generic"])
 @pytest.mark.parametrize("n_inc,F,K,C,N", [(40, 64, 3, 300, 1000), (17, 784, 10, 2001, 700),
                                            (1, 32, 32, 33, 129), (5, 1000, 2, 5000, 300)])
 def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C, N):
-    """All three inference kernels (warp-specialised cluster, alternating
-    cluster, generic): rules longer than the 16-code heads (tails), feature
+    """All inference kernels (per-CTA solo, warp-specialised cluster,
+    alternating cluster, generic): rules longer than the 16-code heads (tails), feature
     widths that are not multiples of 32, K up to 32, ragged tiles, and
     firing blocks in many tiles (votes pushed across the cluster)."""
     from paper_2405_04212_b200 import _lib
     _lib.call("tmb_set_option", b"infer.force_generic", int(kernel == "generic"))
+    _lib.call("tmb_set_option", b"infer.solo", int(kernel == "solo"))
     _lib.call("tmb_set_option", b"infer.warp_specialized", int(kernel.startswith("ws")))
     _lib.call("tmb_set_option", b"infer.eval_mode",
               {"ws_plain": 0, "ws_noexit": 3}.get(kernel, 2))
@@ -359,6 +360,7 @@ def test_inference_kernels_tails_and_shapes(gpu, oracle, kernel, n_inc, F, K, C,
         assert (ov != 0).any()
     finally:
         _lib.call("tmb_set_option", b"infer.force_generic", 0)
+        _lib.call("tmb_set_option", b"infer.solo", 1)
         _lib.call("tmb_set_option", b"infer.warp_specialized", 1)
         _lib.call("tmb_set_option", b"infer.eval_mode", 2)
 
@@ -617,8 +619,16 @@ def test_random_search_golden(gpu, tag):
     assert np.array_equal([t.config.s for t in trials], g[tag + "_s"])
 
 
+@pytest.fixture(params=[1, 0], ids=["solo", "cluster"])
+def infer_kernel(request, gpu):
+    from paper_2405_04212_b200 import _lib
+    _lib.call("tmb_set_option", b"infer.solo", request.param)
+    yield request.param
+    _lib.call("tmb_set_option", b"infer.solo", 1)
+
+
 @pytest.mark.parametrize("F,n_inc,N", [(4096, 20, 3000), (300, 3, 1000), (128, 2, 777)])
-def test_inference_bit_packed_input(gpu, oracle, F, n_inc, N):
+def test_inference_bit_packed_input(gpu, oracle, infer_kernel, F, n_inc, N):
     """Bit-packed input (uint64 words, feature f = bit f % 64 of word f // 64)
     through the packed transposer: identical votes / predictions to the uint8
     path and to the oracle, including widths that are not multiples of 128
