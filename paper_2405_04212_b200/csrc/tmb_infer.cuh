@@ -170,5 +170,6 @@ int launch_infer_solo(const tmb_rules *r, const uint8_t *x, const uint64_t *xb, 
                       unsigned long long *correct, unsigned int *bad_flag, cudaStream_t st,
                       bool *launched);
 extern int g_infer_solo;  // tmb_set_option("infer.solo", 0|1)
+extern int g_infer_dbg;   // tmb_set_option("infer.debug_skip", ...)
 
 }  // namespace tmb

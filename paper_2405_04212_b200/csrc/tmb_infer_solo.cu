@@ -40,12 +40,20 @@ int g_infer_solo = 1;
 
 constexpr int kSoTG = 4;  // 32-example groups per tile (128 examples)
 #ifndef TMB_SOLO_T
-#define TMB_SOLO_T 5
+#define TMB_SOLO_T 7
 #endif
 #ifndef TMB_SOLO_THREADS
 #define TMB_SOLO_THREADS 512
 #endif
 constexpr int kSoThreads = TMB_SOLO_THREADS;
+// > 512 threads: warpgroups 0-1 (the transposers; warps 0..7) re-allocated
+// to TMB_SOLO_REGS_T registers per thread, the rest share what is left
+#ifndef TMB_SOLO_REGS_T
+#define TMB_SOLO_REGS_T 104
+#endif
+constexpr int kSoRegsT = TMB_SOLO_REGS_T;
+constexpr int kSoRegsE = kSoThreads <= 512 ? 128
+    : ((65536 / kSoThreads / 8 * 8) * kSoThreads - 256 * kSoRegsT) / (kSoThreads - 256) / 8 * 8;
 
 struct InferSK {
     const uint8_t *x;    // raw features [N][F] (uint8 path)
@@ -63,6 +71,7 @@ struct InferSK {
     unsigned long long *correct;
     unsigned int *bad_input;
     int vec_ok;
+    int dbg;  // timing experiments only (wrong results): bit0 skip eval, bit1 skip transpose
 };
 
 __device__ __forceinline__ uint4 ldg_heads(const uint4 *p) {
@@ -72,9 +81,28 @@ __device__ __forceinline__ uint4 ldg_heads(const uint4 *p) {
     return v;
 }
 
+// X^T row addresses of the two 16-bit row indices of a head word: one
+// extraction + one LEA each (written out: left to itself the compiler spends
+// three instructions per index)
+__device__ __forceinline__ uint32_t row_lo(uint32_t w, uint32_t base) {
+    uint32_t a;
+    asm("{\n .reg .u32 t;\n and.b32 t, %1, 0xFFFF;\n mad.lo.u32 %0, t, 16, %2;\n}"
+        : "=r"(a) : "r"(w), "r"(base));
+    return a;
+}
+__device__ __forceinline__ uint32_t row_hi(uint32_t w, uint32_t base) {
+    uint32_t a;
+    asm("{\n .reg .u32 t;\n shr.u32 t, %1, 16;\n mad.lo.u32 %0, t, 16, %2;\n}"
+        : "=r"(a) : "r"(w), "r"(base));
+    return a;
+}
+
 template <bool PACKED>
 __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
-    constexpr int kT = PACKED ? 6 : TMB_SOLO_T;  // transposer warps
+#ifndef TMB_SOLO_TP
+#define TMB_SOLO_TP 6
+#endif
+    constexpr int kT = PACKED ? TMB_SOLO_TP : TMB_SOLO_T;  // transposer warps
     extern __shared__ __align__(16) char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int nE = nwarps - kT - 1;  // evaluator warps (the last warp finalizes)
@@ -110,6 +138,13 @@ __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
     }
     __syncthreads();
 
+    if (kSoThreads > 512) {
+        static_assert(kSoThreads <= 512 || (kSoRegsE >= 24 && kSoRegsE <= 256), "register split");
+        if (warp < 8)
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoRegsT));
+        else
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kSoRegsE));
+    }
     const int64_t tile_n = 32 * kSoTG;
     const int64_t n_tiles = (k.N + tile_n - 1) / tile_n;
     const int64_t n_my = blockIdx.x < n_tiles
@@ -131,7 +166,7 @@ __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
             // of example 32g + l; eight 32x32 warp bit transposes leave lane j
             // with the X^T words of features fb + 32q + j
             const int units = (int)((F + 255) / 256) * kSoTG;
-            const int nq = units > warp ? (units - warp + kT - 1) / kT : 0;
+            const int nq = (k.dbg & 2) ? 0 : units > warp ? (units - warp + kT - 1) / kT : 0;
             auto ug = [&](int q) { return (warp + q * kT) % kSoTG; };
             auto ufb = [&](int q) { return (int64_t)((warp + q * kT) / kSoTG) * 256; };
             auto load_p = [&](int64_t itx, int q, uint32_t (&w)[8]) {
@@ -268,7 +303,7 @@ __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
                     if (fb + 4 * j + kq < F) dst0[kq * kSoTG] = wq[r];
                 }
             };
-            if (nq == 0) {
+            if (nq == 0 || (k.dbg & 2)) {
                 for (int64_t it = 0; it < n_my; ++it) {
                     tile_begin(it);
                     tile_end(it);
@@ -388,7 +423,7 @@ __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
             // evaluated chunk hands out the next; ectr[buf] is never reset
             // (use u = it >> 1 numbers its chunks from u * n_chunks)
             const uint32_t ebase = (uint32_t)(it >> 1) * (uint32_t)n_chunks;
-            int rc = ew;
+            int rc = (k.dbg & 1) ? n_chunks : ew;
             uint4 hA0 = make_uint4(0, 0, 0, 0), hA1 = hA0, hB0 = hA0, hB1 = hA0;
             if (rc < n_chunks) {
                 const uint4 *hp = k.heads + (size_t)(rc * 64 + lane) * 2;
@@ -422,10 +457,10 @@ __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
                 auto pair = [&](const uint32_t ha, const uint32_t hb, const bool pred) {
                     const bool la = !pred || (A0 | A1 | A2 | A3);
                     const bool lb = !pred || (B0 | B1 | B2 | B3);
-                    lds128_if(pa, la, xaddr + (ha & 0xFFFFu) * 16);
-                    lds128_if(na, la, xaddr + (ha >> 16) * 16);
-                    lds128_if(pb, lb, xaddr + (hb & 0xFFFFu) * 16);
-                    lds128_if(nb, lb, xaddr + (hb >> 16) * 16);
+                    lds128_if(pa, la, row_lo(ha, xaddr));
+                    lds128_if(na, la, row_hi(ha, xaddr));
+                    lds128_if(pb, lb, row_lo(hb, xaddr));
+                    lds128_if(nb, lb, row_hi(hb, xaddr));
                     A0 &= pa.x & ~na.x;
                     A1 &= pa.y & ~na.y;
                     A2 &= pa.z & ~na.z;
@@ -566,6 +601,7 @@ int launch_infer_solo(const tmb_rules *r, const uint8_t *x, const uint64_t *xb, 
     k.votes = votes; k.pred = pred; k.labels = labels; k.correct = correct;
     k.bad_input = bad_flag;
     k.vec_ok = (r->F % 16 == 0) && x && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+    k.dbg = g_infer_dbg;
     const void *fn = xb ? (const void *)k_infer_solo<true> : (const void *)k_infer_solo<false>;
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t tiles = (N + 32 * kSoTG - 1) / (32 * kSoTG);

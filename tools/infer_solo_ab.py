@@ -20,8 +20,10 @@ model = tmb.CompiledModel.from_bank(bank)
 x = bench.c3_inputs_device(N, 0)
 xb = datasets.inference_examples_device(3, 0, N, 4096, packed=True)
 ref = None
-for solo in (1, 0):
+dbgs = [int(a) for a in sys.argv[1:]] or [0]
+for solo, dbg in [(1, d) for d in dbgs] + ([(0, 0)] if dbgs == [0] else []):
     _lib.call("tmb_set_option", b"infer.solo", solo)
+    _lib.call("tmb_set_option", b"infer.debug_skip", dbg)
     for packed in (False, True):
         pred = torch.empty(N, dtype=torch.int64, device="cuda")
         run = (lambda: model.infer_device_packed(xb, pred_dev=pred)) if packed else \
@@ -38,7 +40,7 @@ for solo in (1, 0):
         gbs = N * 4104 / (ms / 1e3) / 1e9 if not packed else N * 520 / (ms / 1e3) / 1e9
         if ref is None:
             ref = pred.clone()
-        print(f"solo={solo} packed={packed}: {ms:8.3f} ms  {N / ms / 1e3:8.1f} M ex/s  "
+        print(f"solo={solo} dbg={dbg} packed={packed}: {ms:8.3f} ms  {N / ms / 1e3:8.1f} M ex/s  "
               f"{gbs:7.1f} GB/s  same={bool(torch.equal(ref, pred))}", flush=True)
 _lib.call("tmb_set_option", b"infer.solo", 1)
-_lib.call("tmb_tmb_status", None) if False else None
+_lib.call("tmb_set_option", b"infer.debug_skip", 0)
