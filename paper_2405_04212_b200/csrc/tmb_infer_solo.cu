@@ -46,6 +46,16 @@ constexpr int kSoTG = 4;  // 32-example groups per tile (128 examples)
 #define TMB_SOLO_THREADS 512
 #endif
 constexpr int kSoThreads = TMB_SOLO_THREADS;
+#ifndef TMB_SOLO_PD
+#define TMB_SOLO_PD 3
+#endif
+constexpr int kSoPD = TMB_SOLO_PD;  // transposer L2 prefetch distance (items)
+// evaluator load predication of slots 8..15: 0 none, 1 liveness before
+// every pair, 2 liveness before each group of two pairs
+#ifndef TMB_SOLO_PRED
+#define TMB_SOLO_PRED 1
+#endif
+constexpr int kSoPred = TMB_SOLO_PRED;
 // > 512 threads: warpgroups 0-1 (the transposers; warps 0..7) re-allocated
 // to TMB_SOLO_REGS_T registers per thread, the rest share what is left
 #ifndef TMB_SOLO_REGS_T
@@ -322,16 +332,36 @@ __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
                         ++itn;
                     }
                 };
+                // L2 prefetch kSoPD items beyond the one in registers: the
+                // register loads then hit L2 instead of waiting out the HBM
+                // latency (bytes in flight without registers or smem)
+                int64_t ipf = 0;
+                int qpf = 0;
+                auto prefetch_next = [&]() {
+                    if (ipf >= n_my) return;
+                    const int64_t e = tile_of(ipf) * tile_n + 32 * ug(qpf) + lane;
+                    const int64_t f0 = (int64_t)((warp + qpf * kT) / kSoTG) * 128;
+                    if (e < k.N && f0 < F)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(k.x + e * F + f0));
+                    next_of(ipf, qpf, ipf, qpf);
+                };
+                for (int d = 0; d <= kSoPD && n_my > 0; ++d) prefetch_next();
                 if (n_my > 0) load_item(0, 0, wa);
                 while (ia < n_my) {
                     next_of(ia, qa, ib, qb);
-                    if (ib < n_my) load_item(ib, qb, wb);
+                    if (ib < n_my) {
+                        load_item(ib, qb, wb);
+                        prefetch_next();
+                    }
                     if (qa == 0) tile_begin(ia);
                     finish_item(wa, qa, (ia & 1) ? xt1 : xt0);
                     if (qa == nq - 1) tile_end(ia);
                     if (ib >= n_my) break;
                     next_of(ib, qb, ia, qa);
-                    if (ia < n_my) load_item(ia, qa, wa);
+                    if (ia < n_my) {
+                        load_item(ia, qa, wa);
+                        prefetch_next();
+                    }
                     if (qb == 0) tile_begin(ib);
                     finish_item(wb, qb, (ib & 1) ? xt1 : xt0);
                     if (qb == nq - 1) tile_end(ib);
@@ -448,15 +478,13 @@ __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
                 const int rA = rc * 64 + lane, rB = rA + 32;
                 const uint32_t lA = rA < k.R ? 0xFFFFFFFFu : 0u, lB = rB < k.R ? 0xFFFFFFFFu : 0u;
                 uint32_t A0 = lA, A1 = lA, A2 = lA, A3 = lA, B0 = lB, B1 = lB, B2 = lB, B3 = lB;
-                const uint32_t wa[8] = {hA0.x, hA0.y, hA0.z, hA0.w, hA1.x, hA1.y, hA1.z, hA1.w};
-                const uint32_t wb[8] = {hB0.x, hB0.y, hB0.z, hB0.w, hB1.x, hB1.y, hB1.z, hB1.w};
                 uint4 pa = make_uint4(0, 0, 0, 0), na = pa, pb = pa, nb = pa;
                 // slot pair q: slots 8..15 of a rule dead for all 128 examples
                 // skip their loads (its accumulator stays 0 whatever stale
                 // registers it is ANDed with)
-                auto pair = [&](const uint32_t ha, const uint32_t hb, const bool pred) {
-                    const bool la = !pred || (A0 | A1 | A2 | A3);
-                    const bool lb = !pred || (B0 | B1 | B2 | B3);
+                // la / lb: load predicates (liveness sampled before a group
+                // of pairs, so the group's loads issue back to back)
+                auto pair = [&](const uint32_t ha, const uint32_t hb, const bool la, const bool lb) {
                     lds128_if(pa, la, row_lo(ha, xaddr));
                     lds128_if(na, la, row_hi(ha, xaddr));
                     lds128_if(pb, lb, row_lo(hb, xaddr));
@@ -470,15 +498,29 @@ __global__ void __launch_bounds__(kSoThreads, 1) k_infer_solo(InferSK k) {
                     B2 &= pb.z & ~nb.z;
                     B3 &= pb.w & ~nb.w;
                 };
-                pair(hA0.x, hB0.x, false);
-                pair(hA0.y, hB0.y, false);
-                pair(hA0.z, hB0.z, false);
-                pair(hA0.w, hB0.w, false);
-                pair(hA1.x, hB1.x, true);
-                pair(hA1.y, hB1.y, true);
+                auto alive_a = [&]() { return kSoPred == 0 || (A0 | A1 | A2 | A3) != 0; };
+                auto alive_b = [&]() { return kSoPred == 0 || (B0 | B1 | B2 | B3) != 0; };
+                pair(hA0.x, hB0.x, true, true);
+                pair(hA0.y, hB0.y, true, true);
+                pair(hA0.z, hB0.z, true, true);
+                pair(hA0.w, hB0.w, true, true);
+                if (kSoPred == 1) {
+                    pair(hA1.x, hB1.x, alive_a(), alive_b());
+                    pair(hA1.y, hB1.y, alive_a(), alive_b());
+                } else {
+                    const bool la = alive_a(), lb = alive_b();
+                    pair(hA1.x, hB1.x, la, lb);
+                    pair(hA1.y, hB1.y, la, lb);
+                }
                 if (__any_sync(0xffffffffu, A0 | A1 | A2 | A3 | B0 | B1 | B2 | B3)) {
-                    pair(hA1.z, hB1.z, true);
-                    pair(hA1.w, hB1.w, true);
+                    if (kSoPred == 1) {
+                        pair(hA1.z, hB1.z, alive_a(), alive_b());
+                        pair(hA1.w, hB1.w, alive_a(), alive_b());
+                    } else {
+                        const bool la = alive_a(), lb = alive_b();
+                        pair(hA1.z, hB1.z, la, lb);
+                        pair(hA1.w, hB1.w, la, lb);
+                    }
                 }
                 if (A0 | A1 | A2 | A3) finish_rule(rA, A0, A1, A2, A3);
                 if (B0 | B1 | B2 | B3) finish_rule(rB, B0, B1, B2, B3);
