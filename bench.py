@@ -211,6 +211,38 @@ def host_desc():
 
 # --------------------------------------------------------- c2 training --
 
+_LIVE = {}
+
+
+def live_peaks():
+    """Integer-pipe and cross-SM latency peaks measured on THIS box right now
+    (tmb_microbench_pipe / tmb_microbench_pingpong; tools/int_peaks.py
+    writes the full table, profiles/r02_int_peaks.json): LOP3 and full
+    SplitMix64 draw+compare rates per SM per clock, the SM clock they ran
+    at, and one L2 hop (a red.relaxed.gpu observed by a peer SM's poll)."""
+    if _LIVE:
+        return _LIVE
+    import ctypes as ct
+
+    import torch
+
+    from paper_2405_04212_b200 import _lib
+    sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    out = {"sm_count": sm, "source": "measured live (tmb_microbench_pipe, tmb_microbench_pingpong)"}
+    for op, name in ((0, "lop3"), (8, "draw")):
+        r, mhz = ct.c_double(), ct.c_double()
+        _lib.call("tmb_microbench_pipe", op, sm, 1024, 256, ct.byref(r), ct.byref(mhz))
+        out[f"{name}_per_clk_per_sm"] = r.value
+        out[f"{name}_sm_mhz"] = mhz.value
+        out[f"{name}_peak_per_s"] = r.value * sm * mhz.value * 1e6
+    ns, cyc = ct.c_double(), ct.c_double()
+    _lib.call("tmb_microbench_pingpong", 1, 20000, ct.byref(ns), ct.byref(cyc))
+    out["l2_hop_ns"] = ns.value
+    out["l2_hop_cycles"] = cyc.value
+    _LIVE.update(out)
+    return _LIVE
+
+
 def c2_data(rank: int):
     from paper_2405_04212_b200 import datasets
     return datasets.mnist_shaped(data_seed=7)
@@ -327,18 +359,20 @@ def bench_c2_train(args, rank, world, local):
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     clocks = clk.summary()
     f_sm = (clocks["sm_mhz"] or 1965.0) * 1e6
-    # integer-pipe roofline: SplitMix64 draw = ~30 SASS integer ops
-    # (see DESIGN.md); eval = C*W LOP3 (+popc) per example.
-    int_ops_ex = draws_per_ex * 30 + C * W * 3
-    int_peak = sm_count * 128 * f_sm  # ALU + FMA pipes, 64 lanes/clk each
-    int_achieved = int_ops_ex * ex_per_launch / (per_launch_ms / 1e3)
+    # integer work per example at the measured peaks: every reference draw
+    # (one SplitMix64 + threshold compare each; the kernel evaluates all of
+    # them branch-free) plus the bit-packed clause evaluation (C*W LOP3)
+    lp = live_peaks()
+    int_s_ex = draws_per_ex / lp["draw_peak_per_s"] + C * W / lp["lop3_peak_per_s"]
     tr_train, tr_train_src = ncu_traffic("k_train_fast")
-    # latency floor of sequential online training: one grid-wide all-reduce
-    # per example, measured live by the same relaxed-atomic scheme in isolation
+    # latency floors of sequential online training: (hardware) one L2 hop
+    # between SMs per example -- every example's decision needs every CTA's
+    # partial class sums; (protocol) the trainer's own exchange with no work
     import ctypes as ct
     floor = ct.c_double()
     _lib.call("tmb_microbench_allreduce", sess.launch["n_cta"], 512, 20000, 4, ct.byref(floor))
     us_ex = per_launch_ms * 1e3 / ex_per_launch
+    hop_us = lp["l2_hop_ns"] / 1e3
 
     line = {
         "metric": "train examples/sec (configs[1] MNIST-shaped CoTM training)",
@@ -359,31 +393,37 @@ def bench_c2_train(args, rank, world, local):
                  "type_i_per_example": dstats["type_i"] / max(dstats["examples"], 1),
                  "state_updates_per_example": dstats["state_updates"] / max(dstats["examples"], 1)},
         "roofline": {"kernel": "k_train_fast (fused persistent trainer)",
-                     "bound": "hbm",
-                     "achieved": achieved_gbs, "peak": HBM_PEAK, "unit": "GB/s",
-                     "frac": achieved_gbs / HBM_PEAK, "traffic": tr_train,
+                     "bound": "latency",
+                     "achieved": 1e6 / us_ex, "peak": 1e6 / hop_us, "unit": "examples/s",
+                     "frac": hop_us / us_ex, "traffic": tr_train,
                      "traffic_source": tr_train_src,
-                     "traffic_note": "ncu DRAM bytes of one k_train_fast launch (one epoch): "
-                                     "the per-step records (literal row + bucketed 16-bit "
-                                     "flag keys, ~17 KB/step) read once from HBM, then "
-                                     "L2 hits for the other 147 CTAs",
-                     "peak_source": HBM_PEAK_SRC,
-                     "algorithmic_bytes_per_example": hbm_bytes_ex,
-                     "avg_launch_ms": per_launch_ms,
-                     "note": "model is SMEM-resident for the whole launch; HBM carries only "
-                             "the packed literal rows, so this kernel is latency / "
-                             "integer-pipe bound -- see roofline_int"},
-        "roofline_int": {"bound": "int (ALU+FMA issue)", "achieved": int_achieved / 1e12,
-                         "peak": int_peak / 1e12, "unit": "Tops/s",
-                         "frac": int_achieved / int_peak,
-                         "ops_per_example": int_ops_ex,
-                         "us_per_example": us_ex},
+                     "achieved_us_per_example": us_ex, "floor_us_per_example": hop_us,
+                     "floor": "one cross-SM L2 hop per example (red.relaxed.gpu observed by "
+                              "a peer SM's ld.relaxed.gpu poll), measured live by "
+                              "tmb_microbench_pingpong: online training needs every CTA's "
+                              "partial class sums before any CTA's feedback (SPEC.md:360)",
+                     "peak_source": lp["source"], "avg_launch_ms": per_launch_ms},
+        "roofline_int": {"bound": "int (SplitMix64 draws + LOP3 evaluation at measured "
+                                  "per-SM rates)",
+                         "frac": int_s_ex * 1e6 / us_ex,
+                         "int_us_per_example": int_s_ex * 1e6, "achieved_us_per_example": us_ex,
+                         "draw_peak_per_s": lp["draw_peak_per_s"],
+                         "lop3_peak_per_s": lp["lop3_peak_per_s"],
+                         "ops_per_example": {"draws": draws_per_ex, "lop3": C * W}},
+        "roofline_hbm": {"achieved": achieved_gbs, "peak": HBM_PEAK, "unit": "GB/s",
+                         "frac": achieved_gbs / HBM_PEAK, "peak_source": HBM_PEAK_SRC,
+                         "algorithmic_bytes_per_example": hbm_bytes_ex,
+                         "traffic": tr_train,
+                         "traffic_note": "ncu DRAM bytes of one launch (one epoch): the per-step "
+                                         "records (literal row + bucketed 16-bit flag keys, "
+                                         "~17 KB/step) read once from HBM (the other 147 CTAs "
+                                         "hit L2) -- a deliberate trade, ~10 GB/s, not binding"},
         "pipes_ncu": ncu_pipes("k_train_fast"),
-        "roofline_latency": {"bound": "one grid all-reduce per example (sequential training)",
+        "roofline_latency": {"bound": "the trainer's own exchange protocol, no work",
                              "floor_us_per_example": floor.value, "achieved_us_per_example": us_ex,
                              "frac": floor.value / us_ex,
-                             "floor_source": "tmb_microbench_allreduce mode 4 (the trainer's two-word "
-                                            "relaxed red + warp spin, no work), same CTA count"},
+                             "floor_source": "tmb_microbench_allreduce mode 4 (two-word relaxed "
+                                             "red + warp spin), same CTA count"},
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "examples/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
@@ -637,7 +677,7 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
     torch.cuda.synchronize()
     packed_e2e = n_e2e * world * args.steps / (max_over_ranks(pe0.elapsed_time(pe1), world) / 1e3)
     del xb
-    tr_inf, tr_inf_src = ncu_traffic("k_infer_ws")
+    tr_inf, tr_inf_src = ncu_traffic("k_infer_solo<0>")
     if tr_inf is not None:
         tr_inf *= (N_total / world) / (1 << 22)  # captured on the 2^22-example launch
     out = {
@@ -650,13 +690,14 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
                    "rules": model.n_rules, "l2": "inputs (17 GB) far larger than L2"},
         "gpu_launches": int(launches),
         "parity_sample_1024": parity,
-        "roofline": {"kernel": "k_infer_ws (warp-specialised bit-sliced rule evaluation)",
+        "roofline": {"kernel": "k_infer_solo (per-CTA bit-sliced rule evaluation, rule heads "
+                               "streamed from L2)",
                      "bound": "hbm",
                      "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
                      "frac": achieved / HBM_PEAK, "traffic": tr_inf, "traffic_source": tr_inf_src,
                      "peak_source": HBM_PEAK_SRC,
                      "algorithmic_bytes_per_example": bytes_ex, "avg_launch_ms": per_launch_ms},
-        "pipes_ncu": ncu_pipes("k_infer_ws"),
+        "pipes_ncu": ncu_pipes("k_infer_solo<0>"),
         "bit_packed_input": {
             "note": "same examples and model, features as uint64 words (tmb_infer_packed); "
                     "not the reference's input format, so not the headline",
@@ -773,8 +814,8 @@ def bench_c4_train(args, rank, world, local):
     clocks = clk.summary()
     f_sm = (clocks["sm_mhz"] or 1965.0) * 1e6
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
-    int_ops_ex = draws_ex * 22
-    int_peak = sm_count * 128 * f_sm
+    lp = live_peaks()
+    int_s_ex = draws_ex / lp["draw_peak_per_s"]
     # e2e: the same slices from the same state through host buffers
     sess.restore(snap)
     from paper_2405_04212_b200.runtime import ptr, stream_ptr
@@ -819,11 +860,12 @@ def bench_c4_train(args, rank, world, local):
                      "avg_launch_ms": per_launch_ms,
                      "traffic_ncu_sample": c4_ncu_sample()},
         "pipes_ncu": ncu_pipes("k_train<"),
-        "roofline_int": {"bound": "int (ALU+FMA issue)",
-                         "achieved": int_ops_ex * step_n / (per_launch_ms / 1e3) / 1e12,
-                         "peak": int_peak / 1e12, "unit": "Tops/s",
-                         "frac": int_ops_ex * step_n / (per_launch_ms / 1e3) / int_peak,
-                         "ops_per_example": int_ops_ex},
+        "roofline_int": {"bound": "int (SplitMix64 draws at the measured per-SM rate)",
+                         "frac": int_s_ex * step_n / (per_launch_ms / 1e3),
+                         "int_us_per_example": int_s_ex * 1e6,
+                         "achieved_us_per_example": per_launch_ms * 1e3 / step_n,
+                         "draw_peak_per_s": lp["draw_peak_per_s"],
+                         "peak_source": lp["source"]},
         "clocks": clocks,
         "e2e": {"value": n_ex * world / (e2e_ms / 1e3), "unit": "examples/s",
                 "h2d_bytes_per_step": int(tx.nbytes + 4 * step_n),
