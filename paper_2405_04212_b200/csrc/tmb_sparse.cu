@@ -904,98 +904,116 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
 }
 
 // ---------------------------------------------------------- inference --
-// Inverted index: post_ptr [n_literals + 1] (int32) -> post_clause [n_post];
-// n_inc[c] = included literals of clause c (0: never fires in inference).
+// Key-literal index (sparse.py:123-147 semantics: a clause fires in
+// inference iff it has >= 1 included literal and all of them are active).
+// Every clause with includes is filed under ONE of its included literals,
+// its key (the one the query documents contain least often, estimated on a
+// sample of them), so a document's candidates are the clauses keyed by its
+// own tokens -- each clause at most once -- and each candidate is verified
+// include by include against the document's sorted ids (binary search in
+// global memory, L1-resident).  No per-document hit buffer, no limit on
+// document length, hits or classes.  One warp per document.
 struct SparseInferK {
     const int64_t *indptr;
     const int32_t *indices;
     int64_t N;
-    const int32_t *post_ptr, *post_clause, *n_inc;
+    const int32_t *key_ptr;     // [n_literals + 1]
+    const int32_t *key_clause;  // clauses by key literal
+    const int32_t *inc_ptr;     // [C + 1]
+    const int32_t *inc_lits;    // included literals per clause, sorted
     int64_t n_literals;
     const int32_t *weights;
     int C, K;
     int64_t *votes, *pred;
-    const int32_t *outputs_mode;  // unused
-    uint8_t *outputs;             // optional [N, C] inference-mode outputs
-    unsigned int *overflow;
+    uint8_t *outputs;  // optional [N, C] inference-mode outputs
 };
 
-constexpr int kMaxHits = 1024;  // clause hits of one document (per-warp smem)
+__device__ __forceinline__ bool doc_has(const int32_t *doc, int n, int32_t v) {
+    int lo = 0, hi = n;  // first index with doc[i] >= v
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(&doc[mid]) < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && __ldg(&doc[lo]) == v;
+}
 
 __global__ void __launch_bounds__(256) k_sparse_infer(SparseInferK k) {
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    int32_t *hits = reinterpret_cast<int32_t *>(smem_raw) + (size_t)warp * kMaxHits;
-    long long *vacc = reinterpret_cast<long long *>(
-        reinterpret_cast<int32_t *>(smem_raw) + (size_t)nwarps * kMaxHits) + (size_t)warp * 32;
+    long long *vacc = reinterpret_cast<long long *>(smem_raw) + (size_t)warp * k.K;
     for (int64_t d = (int64_t)blockIdx.x * nwarps + warp; d < k.N; d += (int64_t)gridDim.x * nwarps) {
         const int64_t a0 = k.indptr[d], a1 = k.indptr[d + 1];
-        // gather clause hits of the document's active literals
-        int nh = 0;
-        bool ovf = false;
-        for (int64_t base = a0; base < a1; base += 32) {
-            const int64_t q = base + lane;
-            int p0 = 0, p1 = 0;
-            if (q < a1) {
-                const int32_t lit = k.indices[q];
-                if (lit >= 0 && lit < k.n_literals) {
-                    p0 = k.post_ptr[lit];
-                    p1 = k.post_ptr[lit + 1];
+        const int32_t *doc = k.indices + a0;
+        const int n = (int)(a1 - a0);
+        for (int kk = lane; kk < k.K; kk += 32) vacc[kk] = 0;
+        __syncwarp();
+        for (int base = 0; base < n; base += 32) {
+            int p0 = 0, cnt = 0;
+            if (base + lane < n) {
+                const int32_t lit = __ldg(&doc[base + lane]);
+                // (a repeated id would make its clauses candidates twice)
+                const bool dup = base + lane > 0 && __ldg(&doc[base + lane - 1]) == lit;
+                if (lit >= 0 && lit < k.n_literals && !dup) {
+                    p0 = __ldg(&k.key_ptr[lit]);
+                    cnt = __ldg(&k.key_ptr[lit + 1]) - p0;
                 }
             }
-            int tot;
-            int x = p1 - p0;
-            int incl = x;
+            int incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            tot = __shfl_sync(0xffffffffu, incl, 31);
-            const int off = nh + incl - x;
-            for (int m = 0; m < x; ++m) {
-                if (off + m < kMaxHits) hits[off + m] = k.post_clause[p0 + m];
-                else ovf = true;
-            }
-            nh += tot;
-        }
-        __syncwarp();
-        if (__any_sync(0xffffffffu, ovf)) {
-            if (lane == 0) atomicOr(k.overflow, 4u);
-            nh = kMaxHits;
-        }
-        // clause c fires iff it was hit n_inc[c] times (distinct includes);
-        // count with the first occurrence of every clause
-        for (int kk = lane; kk < 32; kk += 32) vacc[kk] = 0;
-        __syncwarp();
-        for (int m = lane; m < nh; m += 32) {
-            const int32_t c = hits[m];
-            int cnt = 0;
-            bool first = true;
-            for (int q = 0; q < nh; ++q) {
-                const int32_t o = hits[q];
-                if (o == c) {
-                    ++cnt;
-                    if (q < m) first = false;
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            for (int s0 = 0; s0 < total; s0 += 32) {
+                const int slot = s0 + lane;
+                // owner token: the first lane whose inclusive count exceeds slot
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+                    if (v <= slot) lo += step;
+                }
+                const int j = lo;
+                const int pj = __shfl_sync(0xffffffffu, p0, j & 31);
+                const int ej = __shfl_sync(0xffffffffu, incl - cnt, j & 31);
+                if (slot >= total) continue;
+                const int c = __ldg(&k.key_clause[pj + slot - ej]);
+                bool fire = true;
+                for (int q = __ldg(&k.inc_ptr[c]), qe = __ldg(&k.inc_ptr[c + 1]); q < qe && fire; ++q)
+                    fire = doc_has(doc, n, __ldg(&k.inc_lits[q]));
+                if (fire) {
+                    for (int kk = 0; kk < k.K; ++kk) {
+                        const int32_t wv = __ldg(&k.weights[(size_t)c * k.K + kk]);
+                        if (wv) atomicAdd((unsigned long long *)&vacc[kk], (unsigned long long)(long long)wv);
+                    }
+                    if (k.outputs) k.outputs[d * k.C + c] = 1;
                 }
             }
-            if (first && cnt == k.n_inc[c]) {
-                for (int kk = 0; kk < k.K; ++kk) {
-                    const int32_t wv = k.weights[(size_t)c * k.K + kk];
-                    if (wv) atomicAdd((unsigned long long *)&vacc[kk], (unsigned long long)(long long)wv);
-                }
-                if (k.outputs) k.outputs[d * k.C + c] = 1;
-            }
         }
         __syncwarp();
-        if (lane == 0) {
-            int best = 0;
-            for (int kk = 0; kk < k.K; ++kk) {
-                if (k.votes) k.votes[d * k.K + kk] = vacc[kk];
-                if (vacc[kk] > vacc[best]) best = kk;
+        // argmax, ties to the lowest class (np.argmax); lanes stripe the classes
+        long long bv = 0;
+        int best = 0x7FFFFFFF;
+        for (int kk = lane; kk < k.K; kk += 32) {
+            const long long v = vacc[kk];
+            if (k.votes) k.votes[d * k.K + kk] = v;
+            if (best == 0x7FFFFFFF || v > bv) {
+                bv = v;
+                best = kk;
             }
-            if (k.pred) k.pred[d] = best;
         }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const long long ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+            if (ob != 0x7FFFFFFF && (best == 0x7FFFFFFF || ov > bv || (ov == bv && ob < best))) {
+                bv = ov;
+                best = ob;
+            }
+        }
+        if (lane == 0 && k.pred) k.pred[d] = best;
         __syncwarp();
     }
 }
@@ -1092,9 +1110,9 @@ int sparse_check_overflow(tmb_sparse *sp, cudaStream_t st) {
         cudaMemsetAsync(sp->overflow, 0, 4, st);
         return fail(TMB_E_UNSUPPORTED,
                     std::string("sparse: ") +
-                        ((v & 1) ? "a clause list exceeded the device slab; raise cfg.slab" :
-                         (v & 2) ? "a document has more than 4096 active literals" :
-                                   "a document hit more than 1024 clause postings"));
+                        ((v & 1) ? "a clause list exceeded the device slab (pass a larger "
+                                   "slab= to the training session)" :
+                                   "a document has more than 4096 active literals"));
     }
     return TMB_OK;
 }
@@ -1309,13 +1327,24 @@ static int sparse_infer_impl(const tmb_sparse *sp, const int64_t *indptr, const 
     cudaStream_t st = as_stream(stream);
     const int64_t C = sp->cfg.n_clauses, slab = sp->cfg.slab, K = sp->cfg.n_classes;
     const int64_t L = sp->cfg.n_literals;
-    // build the inverted index on the host from the device lists (model
-    // compile step, once per call: a few MB)
+    // model compile step (once per call, a few MB): the included literals
+    // of every clause from the device lists
     std::vector<uint8_t> cur(C);
     std::vector<int32_t> len(C);
     TMB_CUDA(cudaMemcpyAsync(cur.data(), sp->cur, C, cudaMemcpyDeviceToHost, st));
     TMB_CUDA(cudaMemcpyAsync(len.data(), sp->len, 4 * C, cudaMemcpyDeviceToHost, st));
+    // a sample of the query's ids (up to 2^20) estimates literal frequencies
+    int64_t nnz = 0;
+    TMB_CUDA(cudaMemcpyAsync(&nnz, indptr + N, 8, cudaMemcpyDeviceToHost, st));
     TMB_CUDA(cudaStreamSynchronize(st));
+    int64_t a_first = 0;
+    TMB_CUDA(cudaMemcpyAsync(&a_first, indptr, 8, cudaMemcpyDeviceToHost, st));
+    TMB_CUDA(cudaStreamSynchronize(st));
+    const int64_t n_sample = std::max<int64_t>(0, std::min<int64_t>(nnz - a_first, 1 << 20));
+    std::vector<int32_t> sample((size_t)n_sample);
+    if (n_sample)
+        TMB_CUDA(cudaMemcpyAsync(sample.data(), indices + a_first, 4 * n_sample,
+                                 cudaMemcpyDeviceToHost, st));
     std::vector<int32_t> hl(C * slab);
     std::vector<int8_t> hs(C * slab);
     for (int b = 0; b < 2; ++b) {
@@ -1331,45 +1360,92 @@ static int sparse_infer_impl(const tmb_sparse *sp, const int64_t *indptr, const 
                     hs[c * slab + q] = ts[c * slab + q];
                 }
     }
-    std::vector<int32_t> n_inc(C, 0), cnt(L + 1, 0);
-    for (int64_t c = 0; c < C; ++c)
-        for (int q = 0; q < len[c]; ++q)
-            if (hs[c * slab + q] >= 0) {
-                ++n_inc[c];
-                ++cnt[hl[c * slab + q] + 1];
+    std::vector<int32_t> inc_ptr(C + 1, 0), inc_lits;
+    std::vector<int32_t> n_clauses_of;  // literal -> number of clauses including it
+    std::vector<uint32_t> freq;         // literal -> occurrences in the sample
+    std::vector<std::pair<int32_t, int32_t>> keyed;  // (key literal, clause)
+    {
+        std::vector<int32_t> ids;
+        for (int64_t c = 0; c < C; ++c) {
+            for (int q = 0; q < len[c]; ++q)
+                if (hs[c * slab + q] >= 0) inc_lits.push_back(hl[c * slab + q]);
+            inc_ptr[c + 1] = (int32_t)inc_lits.size();
+        }
+        // sparse per-literal statistics over the literals that are included
+        ids = inc_lits;
+        std::sort(ids.begin(), ids.end());
+        ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+        n_clauses_of.assign(ids.size(), 0);
+        freq.assign(ids.size(), 0);
+        auto idx = [&](int32_t lit) {
+            return (size_t)(std::lower_bound(ids.begin(), ids.end(), lit) - ids.begin());
+        };
+        for (int32_t lit : inc_lits) ++n_clauses_of[idx(lit)];
+        for (int32_t v : sample) {
+            const size_t i = idx(v);
+            if (i < ids.size() && ids[i] == v) ++freq[i];
+        }
+        for (int64_t c = 0; c < C; ++c) {
+            if (inc_ptr[c + 1] == inc_ptr[c]) continue;  // no includes: never fires
+            int32_t key = -1;
+            size_t best = 0;
+            for (int32_t q = inc_ptr[c]; q < inc_ptr[c + 1]; ++q) {
+                const size_t i = idx(inc_lits[q]);
+                if (key < 0 || freq[i] < freq[best] ||
+                    (freq[i] == freq[best] && n_clauses_of[i] < n_clauses_of[best])) {
+                    key = inc_lits[q];
+                    best = i;
+                }
             }
-    for (int64_t l = 0; l < L; ++l) cnt[l + 1] += cnt[l];
-    std::vector<int32_t> post(cnt[L]);
-    std::vector<int32_t> fillp(cnt.begin(), cnt.end() - 1);
-    for (int64_t c = 0; c < C; ++c)
-        for (int q = 0; q < len[c]; ++q)
-            if (hs[c * slab + q] >= 0) post[fillp[hl[c * slab + q]]++] = (int32_t)c;
-    int32_t *d_ptr = nullptr, *d_post = nullptr, *d_ninc = nullptr;
-    TMB_CUDA(cudaMallocAsync(&d_ptr, 4 * (L + 1), st));
-    TMB_CUDA(cudaMallocAsync(&d_post, 4 * std::max<size_t>(post.size(), 1), st));
-    TMB_CUDA(cudaMallocAsync(&d_ninc, 4 * C, st));
-    TMB_CUDA(cudaMemcpyAsync(d_ptr, cnt.data(), 4 * (L + 1), cudaMemcpyHostToDevice, st));
-    if (!post.empty())
-        TMB_CUDA(cudaMemcpyAsync(d_post, post.data(), 4 * post.size(), cudaMemcpyHostToDevice, st));
-    TMB_CUDA(cudaMemcpyAsync(d_ninc, n_inc.data(), 4 * C, cudaMemcpyHostToDevice, st));
+            keyed.emplace_back(key, (int32_t)c);
+        }
+    }
+    std::vector<int32_t> key_ptr(L + 1, 0), key_clause(keyed.size());
+    for (auto &kc : keyed) ++key_ptr[kc.first + 1];
+    for (int64_t l = 0; l < L; ++l) key_ptr[l + 1] += key_ptr[l];
+    {
+        std::vector<int32_t> fillp(key_ptr.begin(), key_ptr.end() - 1);
+        for (auto &kc : keyed) key_clause[fillp[kc.first]++] = kc.second;
+    }
+    int32_t *d_kptr = nullptr, *d_kcl = nullptr, *d_iptr = nullptr, *d_ilit = nullptr;
+    TMB_CUDA(cudaMallocAsync(&d_kptr, 4 * (L + 1), st));
+    TMB_CUDA(cudaMallocAsync(&d_kcl, 4 * std::max<size_t>(key_clause.size(), 1), st));
+    TMB_CUDA(cudaMallocAsync(&d_iptr, 4 * (C + 1), st));
+    TMB_CUDA(cudaMallocAsync(&d_ilit, 4 * std::max<size_t>(inc_lits.size(), 1), st));
+    int rc = TMB_OK;
+    auto h2d = [&](void *dst, const void *src, size_t bytes) {
+        if (!rc && bytes) rc = check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
+    };
+    h2d(d_kptr, key_ptr.data(), 4 * key_ptr.size());
+    h2d(d_kcl, key_clause.data(), 4 * key_clause.size());
+    h2d(d_iptr, inc_ptr.data(), 4 * inc_ptr.size());
+    h2d(d_ilit, inc_lits.data(), 4 * inc_lits.size());
     SparseInferK k{};
     k.indptr = indptr; k.indices = indices; k.N = N;
-    k.post_ptr = d_ptr; k.post_clause = d_post; k.n_inc = d_ninc; k.n_literals = L;
-    k.weights = sp->weights; k.C = (int)C; k.K = (int)K; k.votes = votes; k.pred = pred;
-    k.outputs = outputs; k.overflow = sp->overflow;
-    if (outputs) TMB_CUDA(cudaMemsetAsync(outputs, 0, (size_t)N * C, st));
-    if (K > 32) return fail(TMB_E_UNSUPPORTED, "sparse_infer: K > 32");
+    k.key_ptr = d_kptr; k.key_clause = d_kcl; k.inc_ptr = d_iptr; k.inc_lits = d_ilit;
+    k.n_literals = L; k.weights = sp->weights; k.C = (int)C; k.K = (int)K;
+    k.votes = votes; k.pred = pred; k.outputs = outputs;
+    if (!rc && outputs) rc = check_cuda(cudaMemsetAsync(outputs, 0, (size_t)N * C, st), "memset");
     const int threads = 256;
-    const size_t smem = 4 * (size_t)kMaxHits * (threads / 32) + 8 * 32 * (threads / 32);
-    TMB_CUDA(cudaFuncSetAttribute((const void *)k_sparse_infer,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t grid = std::min<int64_t>((N + 7) / 8, (int64_t)sm_count() * 8);
-    k_sparse_infer<<<(unsigned)grid, threads, smem, st>>>(k);
-    TMB_LAUNCHED();
-    cudaFreeAsync(d_ptr, st);
-    cudaFreeAsync(d_post, st);
-    cudaFreeAsync(d_ninc, st);
-    return sparse_check_overflow(const_cast<tmb_sparse *>(sp), st);
+    const size_t smem = 8 * (size_t)K * (threads / 32);
+    int dev = 0, max_smem = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (!rc && smem > (size_t)max_smem) rc = fail(TMB_E_UNSUPPORTED, "sparse_infer: too many classes");
+    if (!rc) rc = check_cuda(cudaFuncSetAttribute((const void *)k_sparse_infer,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)smem), "smem attribute");
+    if (!rc) {
+        const int64_t grid = std::min<int64_t>((N + 7) / 8, (int64_t)sm_count() * 8);
+        k_sparse_infer<<<(unsigned)grid, threads, smem, st>>>(k);
+        note_launch();
+        rc = check_cuda(cudaGetLastError(), "kernel launch");
+    }
+    cudaFreeAsync(d_kptr, st);
+    cudaFreeAsync(d_kcl, st);
+    cudaFreeAsync(d_iptr, st);
+    cudaFreeAsync(d_ilit, st);
+    return rc;
 }
 
 int tmb_sparse_infer(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,

@@ -674,3 +674,48 @@ def test_configs1_three_full_epochs_vs_oracle(gpu):
     assert np.array_equal(weights.cpu().numpy(), g["weights"])
     assert np.array_equal(counters.cpu().numpy().view(np.uint64), g["block_counters"])
     assert fb == int(g["fb_counter"]) and sh == int(g["shuffle_counter"])
+
+
+@pytest.mark.parametrize("K,n_docs,doc_len", [(40, 300, 60), (3, 200, 500), (2, 50, 5000)])
+def test_sparse_inference_no_hit_or_class_limits(gpu, oracle, K, n_docs, doc_len):
+    """Key-literal sparse inference has no per-document buffers: thousands of
+    clause postings per document (clauses over a small pool of common
+    literals), more than 32 classes, documents longer than 4096 ids, empty
+    clauses and empty documents -- votes and outputs equal the oracle's
+    SparseClauseBank (sparse.py:123-147)."""
+    rs = np.random.default_rng(K + doc_len)
+    L, C = 20000, 3000
+    cfg = gpu.Config(n_literals=L, n_clauses=C, n_classes=K, s=3.0, threshold=10,
+                     negated_literals_enabled=False)
+    bank = gpu.SparseClauseBank(cfg, candidate_literals=np.arange(L))
+    pool = rs.choice(L, size=40, replace=False)
+    ob = oracle.SparseOracleBank(cfg, candidates=np.arange(L))
+    for j in range(C):
+        if j % 97 == 0:
+            lits = np.empty(0, np.int64)
+        else:
+            m = int(rs.integers(1, 4))
+            lits = np.unique(np.concatenate([rs.choice(pool, size=m, replace=False),
+                                             rs.integers(0, L, size=int(rs.integers(0, 3)))]))
+        sts = rs.integers(-5, 3, size=lits.size).astype(np.int8)
+        if lits.size:
+            sts[0] = 0
+        bank.clause_literals[j] = lits.astype(np.int64)
+        bank.clause_states[j] = sts
+        ob.lits[j], ob.sts[j] = lits.astype(np.int64), sts
+    w = rs.integers(-9, 10, size=(C, K)).astype(np.int32)
+    bank.weights[:] = w
+    ob.weights = w.copy()
+    docs = []
+    for i in range(n_docs):
+        n = 0 if i % 41 == 0 else int(rs.integers(1, doc_len))
+        d = np.unique(np.concatenate([rs.choice(pool, size=int(rs.integers(0, 40)), replace=False),
+                                      rs.integers(0, L, size=n)]))
+        docs.append(d.astype(np.int64))
+    ex = [gpu.SparseExample(d, 0) for d in docs]
+    votes = bank.batch_votes(ex)
+    assert np.array_equal(votes, oracle.sparse_batch_votes([ob], docs))
+    from paper_2405_04212_b200.sparse_train import sparse_outputs
+    outs = sparse_outputs(bank, ex[:40], gpu.EvalMode.INFERENCE)
+    for i in range(40):
+        assert np.array_equal(outs[i], ob.clause_outputs(docs[i], False)), i
