@@ -551,9 +551,10 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
     for (int64_t it = 0; it < k.n_steps; ++it) {
         const int cur = (int)(it & 1);
         const int64_t a0 = s.meta[(it % 3) * 4 + 0], a1 = s.meta[(it % 3) * 4 + 1];
-        const int n_act = (int)(a1 - a0 < kMaxActive ? a1 - a0 : kMaxActive);
-        if (a1 - a0 > kMaxActive && tid == 0) atomicOr(k.overflow, 2u);
-        const int32_t *act = s.act + cur * kMaxActive;
+        // a document longer than the shared-memory stage is read in place
+        // (its CSR row is sorted, like the staged copy)
+        const int n_act = (int)(a1 - a0);
+        const int32_t *act = n_act > kMaxActive ? k.indices + a0 : s.act + cur * kMaxActive;
         // next document's ids into registers; meta of the one after
         int32_t pf[kPfRegs];
         int n_next = 0;
@@ -798,9 +799,16 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                     nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
                                        const_cast<int32_t *>(L) + n, slab - n, s.cand, lane,
                                        prof ? pc2 : nullptr);
-                else
+                else if (k.capacity >= 0 && k.capacity <= kMaxIns)
+                    // insertions per event < capacity: the shared buffer holds them
                     nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
                                        s.ins + (size_t)warp * kMaxIns, kMaxIns, s.cand, lane,
+                                       prof ? pc2 : nullptr);
+                else
+                    // unbounded insertions (sparse_capacity None): the unused
+                    // tail of the source list's global slab is the buffer
+                    nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
+                                       lits_of(k, c, src) + n, slab - n, s.cand, lane,
                                        prof ? pc2 : nullptr);
                 if (prof) {
                     const long long dt = clock64() - e_t0;

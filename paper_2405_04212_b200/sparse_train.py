@@ -19,7 +19,24 @@ from .core import FEEDBACK_STREAM, SHUFFLE_STREAM, RngStream
 from .dense import EvalMode
 from .runtime import ptr, require_device, stream_ptr
 
-DEFAULT_SLAB = 1024  # max (literal, state) pairs per clause held on the device
+DEFAULT_SLAB = 1024  # (literal, state) pairs per clause held on the device (initial)
+
+
+def auto_slab(cfg, candidates, longest: int = 0) -> int:
+    """Device slab (pairs per clause) for a bank over `candidates`.  With
+    sparse_capacity=None a Type II event stores every candidate that is not
+    active (sparse.py:192-210), so a list can hold the whole candidate set:
+    size for it.  With a capacity, lists stay near it (stored pairs are kept,
+    SURVEY 0.8) and start at DEFAULT_SLAB; training sessions grow the slab
+    and replay the epoch if a list ever outgrows it."""
+    n = DEFAULT_SLAB
+    if cfg.sparse_capacity is None:
+        n = max(n, int(len(candidates)) + 32)
+    return max(n, int(longest) + 2 * (cfg.sparse_capacity or 64) + 64)
+
+
+def _is_slab_overflow(err) -> bool:
+    return isinstance(err, _lib.TmbError) and "slab" in str(err)
 
 
 def _cfg_struct(cfg, n_clauses=None, n_blocks=None, slab=DEFAULT_SLAB):
@@ -130,7 +147,7 @@ def _csr_dev(examples):
 class SparseTrainSession:
     """Device-resident sparse training (model, CSR data, RNG counters)."""
 
-    def __init__(self, cfg, indptr, indices, labels, candidates=None, slab=DEFAULT_SLAB):
+    def __init__(self, cfg, indptr, indices, labels, candidates=None, slab=None):
         import torch
         require_device()
         self.cfg = cfg
@@ -139,7 +156,8 @@ class SparseTrainSession:
         if candidates is None:
             candidates = np.unique(indices)
         self.candidates = np.asarray(candidates, dtype=np.int64)
-        self.engine = SparseEngine(cfg, self.candidates, slab=slab)
+        self.engine = SparseEngine(cfg, self.candidates,
+                                   slab=auto_slab(cfg, self.candidates) if slab is None else slab)
         self.N = labels.shape[0]
         self.indptr = torch.from_numpy(indptr).cuda()
         self.indices = torch.from_numpy(indices if indices.size else np.zeros(1, np.int32)).cuda()
@@ -174,6 +192,32 @@ class SparseTrainSession:
         self.run_steps(od)
         return od
 
+    def snapshot(self):
+        """Host copy of the training state (lists, weights, counters)."""
+        return self.engine.get_lists(), self.fb_counter, self.shuffle_rng.counter
+
+    def restore(self, snap, slab=None):
+        """Back to a snapshot, optionally on a new engine with a larger slab."""
+        (lits, sts, w, bc), fb, sh = snap
+        if slab is not None and slab != self.engine.slab:
+            self.engine = SparseEngine(self.cfg, self.candidates, slab=slab)
+        self.engine.set_lists(lits, sts, w, bc)
+        self.fb_counter = fb
+        self.shuffle_rng.counter = sh
+
+    def run_epoch_growing(self, max_steps=None):
+        """run_epoch that survives a clause list outgrowing the device slab:
+        the epoch is replayed from its start on a slab twice as large (the
+        result is the same model; only the storage grew)."""
+        snap = self.snapshot()
+        while True:
+            try:
+                return self.run_epoch(max_steps)
+            except _lib.TmbError as err:
+                if not _is_slab_overflow(err):
+                    raise
+                self.restore(snap, slab=2 * self.engine.slab)
+
     def model(self):
         from .sparse import SparseClauseBank
         lits, sts, w, _ = self.engine.get_lists()
@@ -205,7 +249,7 @@ def train_sparse(cfg, inp, evl, n_epochs, epoch_callback, observer, TrainRun, Ep
         ev = _csr_dev(evl.data.examples)
     for epoch in range(n_epochs):
         t0 = time.perf_counter()
-        sess.run_epoch()
+        sess.run_epoch_growing()
         if observer:
             torch.cuda.current_stream().synchronize()
             for step in range(len(inp)):
@@ -227,8 +271,8 @@ def train_sparse(cfg, inp, evl, n_epochs, epoch_callback, observer, TrainRun, Ep
 
 def _engine_for_bank(bank):
     eng = SparseEngine(bank.cfg, bank.candidates, n_clauses=bank.n_clauses, n_blocks=1,
-                       slab=max(DEFAULT_SLAB, max((len(a) for a in bank.clause_literals),
-                                                  default=0) + 2 * (bank.capacity or 64) + 64))
+                       slab=auto_slab(bank.cfg, bank.candidates,
+                                      max((len(a) for a in bank.clause_literals), default=0)))
     eng.set_lists(bank.clause_literals, bank.clause_states, bank.weights)
     return eng
 

@@ -719,3 +719,66 @@ def test_sparse_inference_no_hit_or_class_limits(gpu, oracle, K, n_docs, doc_len
     outs = sparse_outputs(bank, ex[:40], gpu.EvalMode.INFERENCE)
     for i in range(40):
         assert np.array_equal(outs[i], ob.clause_outputs(docs[i], False)), i
+
+
+def _sparse_docs(rs, n_docs, vocab, lo, hi, planted):
+    docs, labels = [], []
+    for i in range(n_docs):
+        n = int(rs.integers(lo, hi))
+        d = np.unique(rs.integers(0, vocab, size=n))
+        docs.append(d.astype(np.int64))
+        labels.append(int(np.isin(d, planted).sum() % 2))
+    return docs, np.array(labels)
+
+
+def _sparse_vs_oracle(gpu, oracle, cfg, docs, labels, n_epochs, slab=None):
+    from paper_2405_04212_b200.sparse_train import SparseTrainSession
+    ip = np.zeros(len(docs) + 1, dtype=np.int64)
+    np.cumsum([len(d) for d in docs], out=ip[1:])
+    sess = SparseTrainSession(cfg, ip, np.concatenate(docs).astype(np.int32), labels, slab=slab)
+    for _ in range(n_epochs):
+        sess.run_epoch_growing()
+    m = sess.model()
+    banks, bctr, _ = oracle.sparse_train(cfg, docs, labels, n_epochs=n_epochs)
+    ob = banks[0]
+    assert np.array_equal(m.weights, ob.weights)
+    for j in range(cfg.n_clauses):
+        assert np.array_equal(m.clause_literals[j], ob.lits[j]), j
+        assert np.array_equal(m.clause_states[j], ob.sts[j]), j
+    return sess
+
+
+def test_sparse_capacity_none_large_candidate_set(gpu, oracle):
+    """sparse_capacity=None (the reference default) with 2500+ candidates:
+    a Type II event stores every non-active candidate (sparse.py:192-210), so
+    lists far exceed the initial 1024-pair slab; the session sizes the slab
+    from the candidate set and the model equals the oracle's."""
+    rs = np.random.default_rng(5)
+    docs, labels = _sparse_docs(rs, 60, 3000, 20, 80, np.arange(0, 3000, 7))
+    cfg = gpu.Config(n_literals=3000, n_clauses=12, n_classes=2, s=3.0, threshold=8, seed=2,
+                     negated_literals_enabled=False)
+    sess = _sparse_vs_oracle(gpu, oracle, cfg, docs, labels, 2)
+    assert sess.engine.slab > 1024
+    assert max(len(a) for a in sess.model().clause_literals) > 1024
+
+
+def test_sparse_slab_grows_and_replays(gpu, oracle):
+    """A slab too small for the lists the run builds: the epoch is replayed on
+    a larger slab and the model equals the oracle's."""
+    rs = np.random.default_rng(6)
+    docs, labels = _sparse_docs(rs, 80, 400, 10, 40, np.arange(0, 400, 5))
+    cfg = gpu.Config(n_literals=400, n_clauses=10, n_classes=2, s=3.0, threshold=8, seed=3,
+                     negated_literals_enabled=False, sparse_capacity=12)
+    sess = _sparse_vs_oracle(gpu, oracle, cfg, docs, labels, 2, slab=16)
+    assert sess.engine.slab > 16
+
+
+def test_sparse_train_documents_longer_than_stage(gpu, oracle):
+    """Training documents with more than 4096 active literals (read in place
+    from the CSR row instead of the shared-memory stage)."""
+    rs = np.random.default_rng(7)
+    docs, labels = _sparse_docs(rs, 12, 30000, 4500, 9000, np.arange(0, 30000, 3))
+    assert max(len(d) for d in docs) > 4096
+    cfg = gpu.Config(n_literals=30000, n_clauses=8, n_classes=2, s=3.0, threshold=8, seed=4,
+                     negated_literals_enabled=False, sparse_capacity=16)
+    _sparse_vs_oracle(gpu, oracle, cfg, docs, labels, 2)
