@@ -625,18 +625,31 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
         xs = x[:1024].cpu().numpy()
         _, op = oracle.batch_votes(m.states, m.weights, oracle.augment_literals(xs), nthreads=8)
         parity = bool(np.array_equal(pred[:1024].cpu().numpy(), op))
-    # e2e: host (pinned) uint8 features -> tmbh_infer (chunked H2D overlapped
-    # with the kernel) -> host predictions
+    # e2e: host (pinned) uint8 features -> tmbh_infer (3-deep pipeline of
+    # ~48 MB chunks: H2D / kernel / D2H overlap) -> host predictions; beside
+    # it the pinned H2D copy peak of the same bytes (one cudaMemcpyAsync)
     n_e2e = min(n, args.c3_e2e_examples)
     xh = torch.empty((n_e2e, F), dtype=torch.uint8).pin_memory()
     xh.copy_(x[:n_e2e])
     ph = np.empty(n_e2e, dtype=np.int64)
     from paper_2405_04212_b200.runtime import np_ptr
-    _lib.call("tmbh_infer", model._h, ct_ptr(xh), n_e2e, None, np_ptr(ph), 1 << 18)
+    _lib.call("tmbh_infer", model._h, ct_ptr(xh), n_e2e, None, np_ptr(ph), 0)
+    xd_copy = torch.empty_like(xh, device="cuda")
+    for _ in range(2):
+        xd_copy.copy_(xh, non_blocking=True)
+    torch.cuda.synchronize()
+    ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ca.record(stream)
+    for _ in range(3):
+        xd_copy.copy_(xh, non_blocking=True)
+    cb.record(stream)
+    torch.cuda.synchronize()
+    h2d_peak = 3 * xh.numel() / (ca.elapsed_time(cb) / 1e3) / 1e9
+    del xd_copy
     barrier(world)
     t = time.perf_counter()
     for _ in range(args.steps):
-        _lib.call("tmbh_infer", model._h, ct_ptr(xh), n_e2e, None, np_ptr(ph), 1 << 18)
+        _lib.call("tmbh_infer", model._h, ct_ptr(xh), n_e2e, None, np_ptr(ph), 0)
     e2e_s = max_over_ranks(time.perf_counter() - t, world)
     e2e_value = n_e2e * world * args.steps / e2e_s
     # the same examples as bit-packed words (feature f = bit f%64 of word
@@ -710,8 +723,11 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "examples/s", "h2d_bytes_per_step": n_e2e * F,
                 "d2h_bytes_per_step": n_e2e * 8,
-                "path": f"pinned host uint8 [{n_e2e}, 4096] -> tmbh_infer (2-deep chunked "
-                        "H2D/compute overlap) -> host int64 predictions"},
+                "path": f"pinned host uint8 [{n_e2e}, 4096] -> tmbh_infer (3-deep pipeline of "
+                        "~48 MB chunks, buffers kept with the rule set) -> host int64 predictions",
+                "h2d_gbs": n_e2e * F * args.steps / e2e_s / 1e9,
+                "h2d_pinned_copy_peak_gbs": h2d_peak,
+                "h2d_frac_of_peak": n_e2e * F * args.steps / e2e_s / 1e9 / h2d_peak},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # N=1 only (contract)
         from oracle import oracle

@@ -1424,6 +1424,25 @@ static int upload_rules(const std::vector<int64_t> &ptr, const std::vector<uint3
     return TMB_OK;
 }
 
+static void host_pipe_free(HostPipe *hp) {
+    if (!hp) return;
+    if (hp->ks) cudaStreamSynchronize(hp->ks);
+    if (hp->cs) cudaStreamSynchronize(hp->cs);
+    for (int b = 0; b < kPipe; ++b) {
+        if (hp->dx[b]) cudaFree(hp->dx[b]);
+        if (hp->dp[b]) cudaFree(hp->dp[b]);
+        if (hp->dv[b]) cudaFree(hp->dv[b]);
+        if (hp->hp[b]) cudaFreeHost(hp->hp[b]);
+        if (hp->hv[b]) cudaFreeHost(hp->hv[b]);
+        if (hp->kdone[b]) cudaEventDestroy(hp->kdone[b]);
+        if (hp->copied[b]) cudaEventDestroy(hp->copied[b]);
+        if (hp->done[b]) cudaEventDestroy(hp->done[b]);
+    }
+    if (hp->cs) cudaStreamDestroy(hp->cs);
+    if (hp->ks) cudaStreamDestroy(hp->ks);
+    delete hp;
+}
+
 static inline uint32_t encode_inc(int64_t p, int64_t F, int negations) {
     if (negations && p >= F) return (uint32_t)(((p - F) << 1) | 1);
     return (uint32_t)(p << 1);
@@ -1496,6 +1515,7 @@ int tmb_rules_destroy(tmb_rules *r) {
     if (r->heads) cudaFree(r->heads);
     if (r->tail_ptr) cudaFree(r->tail_ptr);
     if (r->tails) cudaFree(r->tails);
+    if (r->pipe) host_pipe_free(r->pipe);
     if (r->sheads) cudaFree(r->sheads);
     if (r->stail_ptr) cudaFree(r->stail_ptr);
     if (r->stails) cudaFree(r->stails);
@@ -1631,67 +1651,70 @@ int tmbh_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, 
     if (rc) return rc;
     if (!r || N < 0 || (N > 0 && !x)) return fail(TMB_E_INVALID, "infer: bad arguments");
     if (N == 0) return TMB_OK;
-    if (chunk <= 0) chunk = 1 << 18;
-    chunk = std::min(chunk, N);
     const int64_t F = r->F, K = r->K;
-    cudaStream_t cs, ks;
-    TMB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    TMB_CUDA(cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking));
-    uint8_t *dx[2] = {nullptr, nullptr};
-    int64_t *dv[2] = {nullptr, nullptr}, *dp[2] = {nullptr, nullptr};
-    int64_t *hv[2] = {nullptr, nullptr}, *hp[2] = {nullptr, nullptr};
-    cudaEvent_t copied[2], done[2];
-    rc = TMB_OK;
-    for (int b = 0; b < 2 && !rc; ++b) {
-        rc = check_cuda(cudaMalloc(&dx[b], chunk * F), "cudaMalloc");
-        if (!rc && votes) rc = check_cuda(cudaMalloc(&dv[b], 8 * chunk * K), "cudaMalloc");
-        if (!rc && votes) rc = check_cuda(cudaMallocHost(&hv[b], 8 * chunk * K), "cudaMallocHost");
-        if (!rc && pred) rc = check_cuda(cudaMalloc(&dp[b], 8 * chunk), "cudaMalloc");
-        if (!rc && pred) rc = check_cuda(cudaMallocHost(&hp[b], 8 * chunk), "cudaMallocHost");
-        cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
+    // ~48 MB of raw input per chunk: long enough copies for the PCIe / DMA
+    // engine, enough chunks for a 3-deep copy / compute / drain pipeline
+    if (chunk <= 0) chunk = std::max<int64_t>(128, ((48 << 20) / std::max<int64_t>(F, 1)) / 128 * 128);
+    chunk = std::min(chunk, N);
+    HostPipe *hp = r->pipe;
+    if (!hp || hp->chunk < chunk || (votes && !hp->votes)) {
+        if (hp) host_pipe_free(hp);
+        hp = new HostPipe();
+        const_cast<tmb_rules *>(r)->pipe = hp;
+        hp->chunk = chunk;
+        hp->votes = votes != nullptr;
+        TMB_CUDA(cudaStreamCreateWithFlags(&hp->cs, cudaStreamNonBlocking));
+        TMB_CUDA(cudaStreamCreateWithFlags(&hp->ks, cudaStreamNonBlocking));
+        for (int b = 0; b < kPipe; ++b) {
+            TMB_CUDA(cudaMalloc(&hp->dx[b], chunk * F));
+            TMB_CUDA(cudaMalloc(&hp->dp[b], 8 * chunk));
+            TMB_CUDA(cudaMallocHost(&hp->hp[b], 8 * chunk));
+            if (hp->votes) {
+                TMB_CUDA(cudaMalloc(&hp->dv[b], 8 * chunk * K));
+                TMB_CUDA(cudaMallocHost(&hp->hv[b], 8 * chunk * K));
+            }
+            TMB_CUDA(cudaEventCreateWithFlags(&hp->kdone[b], cudaEventDisableTiming));
+            TMB_CUDA(cudaEventCreateWithFlags(&hp->copied[b], cudaEventDisableTiming));
+            TMB_CUDA(cudaEventCreateWithFlags(&hp->done[b], cudaEventDisableTiming));
+        }
     }
-    int64_t prev_off[2] = {-1, -1}, prev_n[2] = {0, 0};
+    int64_t prev_off[kPipe], prev_n[kPipe];
+    for (int b = 0; b < kPipe; ++b) prev_off[b] = -1, prev_n[b] = 0;
     auto drain = [&](int b) {
         if (prev_off[b] < 0) return;
-        cudaEventSynchronize(done[b]);
-        if (votes) memcpy(votes + prev_off[b] * K, hv[b], 8 * prev_n[b] * K);
-        if (pred) memcpy(pred + prev_off[b], hp[b], 8 * prev_n[b]);
+        cudaEventSynchronize(hp->done[b]);
+        if (votes) memcpy(votes + prev_off[b] * K, hp->hv[b], 8 * prev_n[b] * K);
+        if (pred) memcpy(pred + prev_off[b], hp->hp[b], 8 * prev_n[b]);
         prev_off[b] = -1;
     };
     int64_t idx = 0;
+    rc = TMB_OK;
     for (int64_t off = 0; off < N && !rc; off += chunk, ++idx) {
-        const int b = (int)(idx & 1);
+        const int b = (int)(idx % kPipe);
         const int64_t n = std::min(chunk, N - off);
-        drain(b);  // buffer b's previous results are on the host and it is free
-        rc = check_cuda(cudaMemcpyAsync(dx[b], x + off * F, n * F, cudaMemcpyHostToDevice, cs),
-                        "H2D");
-        cudaEventRecord(copied[b], cs);
-        cudaStreamWaitEvent(ks, copied[b], 0);
-        if (!rc) rc = launch_infer(r, dx[b], n, dv[b], dp[b], nullptr, nullptr, ks);
+        drain(b);  // chunk idx - kPipe's results are on the host; buffer b is free
+        // the copy into dx[b] waits for the kernel that last read it
+        if (idx >= kPipe) cudaStreamWaitEvent(hp->cs, hp->kdone[b], 0);
+        rc = check_cuda(cudaMemcpyAsync(hp->dx[b], x + off * F, n * F, cudaMemcpyHostToDevice,
+                                        hp->cs), "H2D");
+        cudaEventRecord(hp->copied[b], hp->cs);
+        cudaStreamWaitEvent(hp->ks, hp->copied[b], 0);
+        if (!rc) rc = launch_infer(r, hp->dx[b], n, votes ? hp->dv[b] : nullptr, hp->dp[b],
+                                   nullptr, nullptr, hp->ks);
+        cudaEventRecord(hp->kdone[b], hp->ks);
         if (!rc && votes)
-            rc = check_cuda(cudaMemcpyAsync(hv[b], dv[b], 8 * n * K, cudaMemcpyDeviceToHost, ks), "D2H");
+            rc = check_cuda(cudaMemcpyAsync(hp->hv[b], hp->dv[b], 8 * n * K, cudaMemcpyDeviceToHost,
+                                            hp->ks), "D2H");
         if (!rc && pred)
-            rc = check_cuda(cudaMemcpyAsync(hp[b], dp[b], 8 * n, cudaMemcpyDeviceToHost, ks), "D2H");
-        cudaEventRecord(done[b], ks);
+            rc = check_cuda(cudaMemcpyAsync(hp->hp[b], hp->dp[b], 8 * n, cudaMemcpyDeviceToHost,
+                                            hp->ks), "D2H");
+        cudaEventRecord(hp->done[b], hp->ks);
         prev_off[b] = off;
         prev_n[b] = n;
     }
-    drain(0);
-    drain(1);
-    if (!rc) rc = check_cuda(cudaStreamSynchronize(ks), "sync");
-    if (!rc) rc = check_bad_input(ks);
-    for (int b = 0; b < 2; ++b) {
-        cudaFree(dx[b]);
-        if (dv[b]) cudaFree(dv[b]);
-        if (dp[b]) cudaFree(dp[b]);
-        if (hv[b]) cudaFreeHost(hv[b]);
-        if (hp[b]) cudaFreeHost(hp[b]);
-        cudaEventDestroy(copied[b]);
-        cudaEventDestroy(done[b]);
-    }
-    cudaStreamDestroy(cs);
-    cudaStreamDestroy(ks);
+    for (int b = 0; b < kPipe; ++b) drain(b);
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(hp->ks), "sync");
+    if (!rc) rc = check_bad_input(hp->ks);
     return rc;
 }
 

@@ -8,6 +8,20 @@
 
 #include "tmb_common.cuh"
 
+// Host-buffer inference pipeline state (tmbh_infer), kept with the rule set
+// between calls: kPipe device input / output buffers, pinned output staging,
+// a copy stream and a compute stream.
+constexpr int kPipe = 3;
+struct HostPipe {
+    int64_t chunk = 0;
+    bool votes = false;
+    uint8_t *dx[kPipe] = {};
+    int64_t *dp[kPipe] = {}, *dv[kPipe] = {};
+    int64_t *hp[kPipe] = {}, *hv[kPipe] = {};
+    cudaEvent_t kdone[kPipe] = {}, copied[kPipe] = {}, done[kPipe] = {};
+    cudaStream_t cs = nullptr, ks = nullptr;
+};
+
 struct tmb_rules {
     int64_t R = 0, K = 0, F = 0, n_inc = 0;
     int negations = 0;
@@ -32,6 +46,7 @@ struct tmb_rules {
     uint16_t *stails = nullptr;    // device [n_stail]
     int64_t R_pad = 0;
     int sheads_ok = 0;
+    HostPipe *pipe = nullptr;  // tmbh_infer buffers (lazily created)
 };
 
 namespace tmb {

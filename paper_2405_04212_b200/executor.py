@@ -152,6 +152,10 @@ class DenseTrainSession:
         device (tmb_pack_literals: [N, ceil(P/32)] uint32)."""
         import torch
         x = np.ascontiguousarray(x, dtype=np.uint8)
+        if x.size and int(x.max()) > 1:
+            # the device packs literal bits; the inference and explain paths
+            # reject non-0/1 bytes the same way
+            raise DataError("train data: features must be 0/1")
         dev = self.states.device
         xd = torch.from_numpy(x).pin_memory().to(dev, non_blocking=True)
         self.lit_words = torch.empty((x.shape[0], self.W), dtype=torch.int32, device=dev)

@@ -97,9 +97,11 @@ class CompiledModel:
 
     # -- evaluation -----------------------------------------------------
     def votes_and_pred(self, x: np.ndarray, want_votes: bool = True, want_pred: bool = True,
-                       chunk: int = 1 << 18):
-        """Host arrays in, host arrays out (tmbh_infer: chunked H2D with
-        copy/compute overlap)."""
+                       chunk: int = 0):
+        """Host arrays in, host arrays out (tmbh_infer: a 3-deep pipeline of
+        ~48 MB chunks -- H2D copy / kernel / D2H of the predictions overlap;
+        chunk = examples per chunk, 0 = auto).  The device and pinned
+        buffers stay with the rule set between calls (one call at a time)."""
         x = np.ascontiguousarray(x, dtype=np.uint8)
         if x.ndim != 2 or x.shape[1] != self.n_features:
             raise ValueError(f"expected [N, {self.n_features}] input, got {x.shape}")

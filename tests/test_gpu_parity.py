@@ -782,3 +782,12 @@ def test_sparse_train_documents_longer_than_stage(gpu, oracle):
     cfg = gpu.Config(n_literals=30000, n_clauses=8, n_classes=2, s=3.0, threshold=8, seed=4,
                      negated_literals_enabled=False, sparse_capacity=16)
     _sparse_vs_oracle(gpu, oracle, cfg, docs, labels, 2)
+
+
+def test_train_rejects_non_binary_features(gpu):
+    """The device packs literal bits; non-0/1 training bytes raise DataError
+    (as the inference and explain paths reject them)."""
+    cfg = gpu.Config(n_literals=4, n_clauses=4, n_classes=2, s=3.0, threshold=5)
+    x = np.array([[0, 1, 2, 0], [1, 0, 0, 1]], dtype=np.uint8)
+    with pytest.raises(gpu.DataError):
+        gpu.train(cfg, (x, np.array([0, 1])), n_epochs=1)
