@@ -2,6 +2,7 @@
 // kernels.clause_outputs / clause_outputs_batch / bank_feedback
 // (kernels/_numba.py:53-125) plus the explicit-draws test hook, literal
 // packing and include-mask construction shared with the fused trainer.
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -224,7 +225,7 @@ int feedback_dev(int8_t *states, int32_t *weights, int64_t C, int64_t P, int64_t
                  const uint8_t *lits, const uint8_t *outputs, int64_t label, int64_t negative,
                  const uint8_t *ut, const uint8_t *un, double s, int boost, int smin, int smax,
                  uint64_t seed, uint64_t counter, const double *draws, int64_t n_rows,
-                 uint64_t *counter_out, cudaStream_t st) {
+                 uint64_t *counter_out, cudaStream_t st, uint64_t *total_pinned = nullptr) {
     if (C < 1 || P < 1 || K < 2 || label < 0 || label >= K || negative < 0 || negative >= K)
         return fail(TMB_E_INVALID, "bank_feedback: bad shape or class index");
     if (!(s > 1.0) && !draws) return fail(TMB_E_INVALID, "bank_feedback: s must exceed 1");
@@ -243,6 +244,11 @@ int feedback_dev(int8_t *states, int32_t *weights, int64_t C, int64_t P, int64_t
                                                  prefix.as<int64_t>(), fp, seed, counter, draws,
                                                  n_rows);
     TMB_LAUNCHED();
+    if (total_pinned) {  // the caller synchronises and adds the counter
+        TMB_CUDA(cudaMemcpyAsync(total_pinned, total.as<uint64_t>(), sizeof(uint64_t),
+                                 cudaMemcpyDeviceToHost, st));
+        return TMB_OK;
+    }
     uint64_t tot = 0;
     TMB_CUDA(cudaMemcpyAsync(&tot, total.as<uint64_t>(), sizeof(uint64_t),
                              cudaMemcpyDeviceToHost, st));
@@ -311,32 +317,62 @@ int tmb_bank_feedback_draws(int8_t *states, int32_t *weights, int64_t C, int64_t
 }
 
 // ------------------------------------------------------- host variants --
+}  // extern "C"
+
+namespace {
+// Per host thread: one stream, a device arena and a pinned staging buffer,
+// kept between calls (the reference calls the plugin once per example per
+// block, so per-call stream / allocation setup would dominate).  Inputs are
+// packed into the staging buffer and moved with ONE host->device copy.
+struct PluginCtx {
+    cudaStream_t st = nullptr;
+    char *dev = nullptr, *pin = nullptr;
+    size_t dev_cap = 0, pin_cap = 0;
+    int ensure(size_t dbytes, size_t pbytes) {
+        if (!st) TMB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        if (dbytes > dev_cap) {
+            if (dev) cudaFree(dev);
+            dev_cap = std::max(dbytes, 2 * dev_cap);
+            TMB_CUDA(cudaMalloc(&dev, dev_cap));
+        }
+        if (pbytes > pin_cap) {
+            if (pin) cudaFreeHost(pin);
+            pin_cap = std::max(pbytes, 2 * pin_cap);
+            TMB_CUDA(cudaMallocHost(&pin, pin_cap));
+        }
+        return TMB_OK;
+    }
+};
+thread_local PluginCtx *t_pc = nullptr;  // never freed: outlives the CUDA runtime at exit
+PluginCtx &plugin_ctx() {
+    if (!t_pc) t_pc = new PluginCtx();
+    return *t_pc;
+}
+inline size_t al16(size_t n) { return (n + 15) & ~(size_t)15; }
+}  // namespace
+
+extern "C" {
+
 int tmbh_clause_outputs_batch(const int8_t *states, int64_t C, int64_t P, const uint8_t *x_lit,
                               int64_t N, int training, int64_t budget, uint8_t *out) {
     int rc = require_device();
     if (rc) return rc;
     if (C < 1 || P < 1 || N < 0 || !states || (N > 0 && (!x_lit || !out)))
         return fail(TMB_E_INVALID, "clause_outputs_batch: bad arguments");
-    cudaStream_t st;
-    TMB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    {
-        DevBuf ds, dx, dout;
-        if ((rc = ds.alloc(C * P, st)) || (rc = dx.alloc(N * P, st)) ||
-            (rc = dout.alloc(N * C, st))) {
-            cudaStreamDestroy(st);
-            return rc;
-        }
-        cudaMemcpyAsync(ds.p, states, C * P, cudaMemcpyHostToDevice, st);
-        if (N > 0) cudaMemcpyAsync(dx.p, x_lit, N * P, cudaMemcpyHostToDevice, st);
-        rc = outputs_batch_dev(ds.as<int8_t>(), C, P, dx.as<uint8_t>(), N, training, budget,
-                               dout.as<uint8_t>(), st);
-        if (!rc && N > 0)
-            rc = check_cuda(cudaMemcpyAsync(out, dout.p, N * C, cudaMemcpyDeviceToHost, st),
-                            "copy out");
-        if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync");
-    }
-    cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
+    PluginCtx &pc = plugin_ctx();
+    const size_t o_s = 0, o_x = al16(C * P), o_out = o_x + al16(N * P), tot_in = o_out;
+    if ((rc = pc.ensure(o_out + al16(N * C), std::max(tot_in, (size_t)(N * C))))) return rc;
+    memcpy(pc.pin + o_s, states, C * P);
+    if (N > 0) memcpy(pc.pin + o_x, x_lit, N * P);
+    TMB_CUDA(cudaMemcpyAsync(pc.dev, pc.pin, tot_in, cudaMemcpyHostToDevice, pc.st));
+    rc = outputs_batch_dev(reinterpret_cast<int8_t *>(pc.dev + o_s), C, P,
+                           reinterpret_cast<uint8_t *>(pc.dev + o_x), N, training, budget,
+                           reinterpret_cast<uint8_t *>(pc.dev + o_out), pc.st);
+    if (!rc && N > 0)
+        rc = check_cuda(cudaMemcpyAsync(pc.pin, pc.dev + o_out, N * C, cudaMemcpyDeviceToHost,
+                                        pc.st), "copy out");
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(pc.st), "sync");
+    if (!rc && N > 0) memcpy(out, pc.pin, N * C);
     return rc;
 }
 
@@ -354,34 +390,33 @@ int tmbh_bank_feedback(int8_t *states, int32_t *weights, int64_t C, int64_t P, i
     if (rc) return rc;
     if (C < 1 || P < 1 || K < 2 || !states || !weights || !lits || !outputs || !ut || !un)
         return fail(TMB_E_INVALID, "bank_feedback: bad arguments");
-    cudaStream_t st;
-    TMB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    {
-        DevBuf ds, dw, dl, dout, dut, dun;
-        if ((rc = ds.alloc(C * P, st)) || (rc = dw.alloc(4 * C * K, st)) ||
-            (rc = dl.alloc(P, st)) || (rc = dout.alloc(C, st)) || (rc = dut.alloc(C, st)) ||
-            (rc = dun.alloc(C, st))) {
-            cudaStreamDestroy(st);
-            return rc;
-        }
-        cudaMemcpyAsync(ds.p, states, C * P, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(dw.p, weights, 4 * C * K, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(dl.p, lits, P, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(dout.p, outputs, C, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(dut.p, ut, C, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(dun.p, un, C, cudaMemcpyHostToDevice, st);
-        rc = feedback_dev(ds.as<int8_t>(), dw.as<int32_t>(), C, P, K, dl.as<uint8_t>(),
-                          dout.as<uint8_t>(), label, negative, dut.as<uint8_t>(),
-                          dun.as<uint8_t>(), s, boost, state_min, state_max, seed, counter,
-                          nullptr, 0, counter_out, st);
-        if (!rc) {
-            cudaMemcpyAsync(states, ds.p, C * P, cudaMemcpyDeviceToHost, st);
-            cudaMemcpyAsync(weights, dw.p, 4 * C * K, cudaMemcpyDeviceToHost, st);
-            rc = check_cuda(cudaStreamSynchronize(st), "sync");
-        }
+    PluginCtx &pc = plugin_ctx();
+    // staging layout: states | weights | lits | outputs | ut | un
+    const size_t o_s = 0, o_w = al16(C * P), o_l = o_w + al16(4 * C * K), o_o = o_l + al16(P),
+                 o_t = o_o + al16(C), o_n = o_t + al16(C), tot = o_n + al16(C);
+    if ((rc = pc.ensure(tot, tot + 16))) return rc;
+    uint64_t *ev_total = reinterpret_cast<uint64_t *>(pc.pin + tot);
+    memcpy(pc.pin + o_s, states, C * P);
+    memcpy(pc.pin + o_w, weights, 4 * C * K);
+    memcpy(pc.pin + o_l, lits, P);
+    memcpy(pc.pin + o_o, outputs, C);
+    memcpy(pc.pin + o_t, ut, C);
+    memcpy(pc.pin + o_n, un, C);
+    TMB_CUDA(cudaMemcpyAsync(pc.dev, pc.pin, tot, cudaMemcpyHostToDevice, pc.st));
+    char *d = pc.dev;
+    rc = feedback_dev(reinterpret_cast<int8_t *>(d + o_s), reinterpret_cast<int32_t *>(d + o_w),
+                      C, P, K, reinterpret_cast<uint8_t *>(d + o_l),
+                      reinterpret_cast<uint8_t *>(d + o_o), label, negative,
+                      reinterpret_cast<uint8_t *>(d + o_t), reinterpret_cast<uint8_t *>(d + o_n),
+                      s, boost, state_min, state_max, seed, counter, nullptr, 0, counter_out,
+                      pc.st, ev_total);
+    if (!rc) rc = check_cuda(cudaMemcpyAsync(pc.pin, d, o_l, cudaMemcpyDeviceToHost, pc.st), "D2H");
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(pc.st), "sync");
+    if (!rc) {
+        if (counter_out) *counter_out = counter + *ev_total;
+        memcpy(states, pc.pin + o_s, C * P);
+        memcpy(weights, pc.pin + o_w, 4 * C * K);
     }
-    cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
     return rc;
 }
 

@@ -56,6 +56,16 @@ int require_device() {
             } else {
                 g_dev_state = TMB_OK;
                 g_sm_count = prop.multiProcessorCount;
+                // stream-ordered scratch (cudaMallocAsync) stays mapped between
+                // calls: with the default release threshold of 0 every
+                // synchronisation unmapped it and the next per-example plugin
+                // call paid ~1 ms to map it again
+                cudaMemPool_t pool;
+                if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                    uint64_t keep = UINT64_MAX;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+                }
+                cudaGetLastError();
             }
         }
     }
