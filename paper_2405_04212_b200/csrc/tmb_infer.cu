@@ -1186,6 +1186,7 @@ int g_infer_ws = 1;  // tmb_set_option("infer.warp_specialized", 0|1)
 int g_infer_eval = 2;  // tmb_set_option("infer.eval_mode", 0|2|3): k_infer_ws evaluator
 extern unsigned long long *g_sparse_phase;  // tmb_sparse.cu
 extern int g_sparse_resident;                // tmb_sparse.cu
+extern int g_sparse_infer_key;               // tmb_sparse.cu
 unsigned long long *g_infer_phase = nullptr;
 
 int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, int64_t *pred,
@@ -1610,6 +1611,10 @@ int tmb_set_option(const char *name, int64_t value) {
     }
     if (std::string(name) == "sparse.phase_buffer") {  // device uint64 [n_cta*16] or 0
         g_sparse_phase = reinterpret_cast<unsigned long long *>(value);
+        return TMB_OK;
+    }
+    if (std::string(name) == "sparse.infer_key") {  // 1: key-literal sparse inference kernel
+        g_sparse_infer_key = (int)value;
         return TMB_OK;
     }
     if (std::string(name) == "sparse.resident") {  // 0: keep clause lists in global memory

@@ -934,7 +934,141 @@ struct SparseInferK {
     int C, K;
     int64_t *votes, *pred;
     uint8_t *outputs;  // optional [N, C] inference-mode outputs
+    // counting variant: the full inverted index and include counts
+    const int32_t *post_ptr;     // [n_literals + 1]
+    const int32_t *post_clause;  // clauses including each literal
+    const int32_t *n_inc;        // [C]
 };
+
+// votes (argmax ties to the lowest class, np.argmax) of document d from the
+// warp's int64 class sums; lanes stripe the classes
+__device__ __forceinline__ void finish_doc(const SparseInferK &k, int64_t d, const long long *vacc,
+                                           int lane) {
+    long long bv = 0;
+    int best = 0x7FFFFFFF;
+    for (int kk = lane; kk < k.K; kk += 32) {
+        const long long v = vacc[kk];
+        if (k.votes) k.votes[d * k.K + kk] = v;
+        if (best == 0x7FFFFFFF || v > bv) {
+            bv = v;
+            best = kk;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const long long ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+        if (ob != 0x7FFFFFFF && (best == 0x7FFFFFFF || ov > bv || (ov == bv && ob < best))) {
+            bv = ov;
+            best = ob;
+        }
+    }
+    if (lane == 0 && k.pred) k.pred[d] = best;
+}
+
+// Counting variant (clause count small enough for a per-warp counter array
+// in shared memory): every (token, including clause) posting of the
+// document increments the clause's counter; the posting that brings it to
+// the clause's include count fires it.  Linear in the postings, no buffer.
+// Class sums of fired clauses: KR > 0 (K <= KR) accumulates per lane in
+// registers and reduces once per document -- a clause fires on most
+// postings of a trained configs[4] model (1.2 includes per clause), and
+// shared atomics from all lanes onto the same K sums serialise; KR = 0 keeps
+// per-warp shared int64 sums.
+template <int KR>
+struct VoteAcc {
+    long long r[KR > 0 ? KR : 1];
+    __device__ __forceinline__ void clear() {
+#pragma unroll
+        for (int kk = 0; kk < (KR > 0 ? KR : 1); ++kk) r[kk] = 0;
+    }
+    __device__ __forceinline__ void add(const SparseInferK &k, int c, long long *vacc) {
+        const int32_t *wr = k.weights + (size_t)c * k.K;
+        if (KR > 0) {
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk)
+                if (kk < k.K) r[kk] += __ldg(&wr[kk]);
+        } else {
+            for (int kk = 0; kk < k.K; ++kk) {
+                const int32_t wv = __ldg(&wr[kk]);
+                if (wv) atomicAdd((unsigned long long *)&vacc[kk], (unsigned long long)(long long)wv);
+            }
+        }
+    }
+    // lane sums -> vacc (KR > 0); call with the whole warp
+    __device__ __forceinline__ void flush(const SparseInferK &k, long long *vacc, int lane) {
+        if (KR > 0) {
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk) {
+                long long v = r[kk];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && kk < k.K) vacc[kk] = v;
+            }
+        }
+    }
+};
+
+template <int KR>
+__global__ void __launch_bounds__(256) k_sparse_infer_count(SparseInferK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int Cp = (k.C + 3) & ~3;
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(smem_raw) + (size_t)warp * Cp;
+    long long *vacc = reinterpret_cast<long long *>(
+        reinterpret_cast<uint32_t *>(smem_raw) + (size_t)nwarps * Cp) + (size_t)warp * k.K;
+    for (int64_t d = (int64_t)blockIdx.x * nwarps + warp; d < k.N; d += (int64_t)gridDim.x * nwarps) {
+        const int64_t a0 = k.indptr[d], a1 = k.indptr[d + 1];
+        const int32_t *doc = k.indices + a0;
+        const int n = (int)(a1 - a0);
+        for (int q = lane; q < Cp / 4; q += 32) reinterpret_cast<uint4 *>(cnt)[q] = make_uint4(0, 0, 0, 0);
+        for (int kk = lane; kk < k.K; kk += 32) vacc[kk] = 0;
+        VoteAcc<KR> acc;
+        acc.clear();
+        __syncwarp();
+        for (int base = 0; base < n; base += 32) {
+            int p0 = 0, np = 0;
+            if (base + lane < n) {
+                const int32_t lit = __ldg(&doc[base + lane]);
+                const bool dup = base + lane > 0 && __ldg(&doc[base + lane - 1]) == lit;
+                if (lit >= 0 && lit < k.n_literals && !dup) {
+                    p0 = __ldg(&k.post_ptr[lit]);
+                    np = __ldg(&k.post_ptr[lit + 1]) - p0;
+                }
+            }
+            int incl = np;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            for (int s0 = 0; s0 < total; s0 += 32) {
+                const int slot = s0 + lane;
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+                    if (v <= slot) lo += step;
+                }
+                const int pj = __shfl_sync(0xffffffffu, p0, lo & 31);
+                const int ej = __shfl_sync(0xffffffffu, incl - np, lo & 31);
+                if (slot >= total) continue;
+                const int c = __ldg(&k.post_clause[pj + slot - ej]);
+                const uint32_t old = atomicAdd(&cnt[c], 1u);
+                if ((int)old + 1 == __ldg(&k.n_inc[c])) {
+                    acc.add(k, c, vacc);
+                    if (k.outputs) k.outputs[d * k.C + c] = 1;
+                }
+            }
+        }
+        __syncwarp();
+        acc.flush(k, vacc, lane);
+        __syncwarp();
+        finish_doc(k, d, vacc, lane);
+        __syncwarp();
+    }
+}
 
 __device__ __forceinline__ bool doc_has(const int32_t *doc, int n, int32_t v) {
     int lo = 0, hi = n;  // first index with doc[i] >= v
@@ -946,6 +1080,7 @@ __device__ __forceinline__ bool doc_has(const int32_t *doc, int n, int32_t v) {
     return lo < n && __ldg(&doc[lo]) == v;
 }
 
+template <int KR>
 __global__ void __launch_bounds__(256) k_sparse_infer(SparseInferK k) {
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -955,6 +1090,8 @@ __global__ void __launch_bounds__(256) k_sparse_infer(SparseInferK k) {
         const int32_t *doc = k.indices + a0;
         const int n = (int)(a1 - a0);
         for (int kk = lane; kk < k.K; kk += 32) vacc[kk] = 0;
+        VoteAcc<KR> acc;
+        acc.clear();
         __syncwarp();
         for (int base = 0; base < n; base += 32) {
             int p0 = 0, cnt = 0;
@@ -992,40 +1129,20 @@ __global__ void __launch_bounds__(256) k_sparse_infer(SparseInferK k) {
                 for (int q = __ldg(&k.inc_ptr[c]), qe = __ldg(&k.inc_ptr[c + 1]); q < qe && fire; ++q)
                     fire = doc_has(doc, n, __ldg(&k.inc_lits[q]));
                 if (fire) {
-                    for (int kk = 0; kk < k.K; ++kk) {
-                        const int32_t wv = __ldg(&k.weights[(size_t)c * k.K + kk]);
-                        if (wv) atomicAdd((unsigned long long *)&vacc[kk], (unsigned long long)(long long)wv);
-                    }
+                    acc.add(k, c, vacc);
                     if (k.outputs) k.outputs[d * k.C + c] = 1;
                 }
             }
         }
         __syncwarp();
-        // argmax, ties to the lowest class (np.argmax); lanes stripe the classes
-        long long bv = 0;
-        int best = 0x7FFFFFFF;
-        for (int kk = lane; kk < k.K; kk += 32) {
-            const long long v = vacc[kk];
-            if (k.votes) k.votes[d * k.K + kk] = v;
-            if (best == 0x7FFFFFFF || v > bv) {
-                bv = v;
-                best = kk;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const long long ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int ob = __shfl_xor_sync(0xffffffffu, best, o);
-            if (ob != 0x7FFFFFFF && (best == 0x7FFFFFFF || ov > bv || (ov == bv && ob < best))) {
-                bv = ov;
-                best = ob;
-            }
-        }
-        if (lane == 0 && k.pred) k.pred[d] = best;
+        acc.flush(k, vacc, lane);
+        __syncwarp();
+        finish_doc(k, d, vacc, lane);
         __syncwarp();
     }
 }
 
+int g_sparse_infer_key = 0;  // tmb_set_option("sparse.infer_key"): force the key-literal kernel
 unsigned long long *g_sparse_phase = nullptr;  // tmb_set_option("sparse.phase_buffer")
 int g_sparse_resident = 1;                      // tmb_set_option("sparse.resident")
 
@@ -1033,8 +1150,30 @@ int g_sparse_resident = 1;                      // tmb_set_option("sparse.reside
 
 using namespace tmb;
 
+// compiled inference index (device arrays), see build_infer_index
+struct SparseIndex {
+    uint64_t version = ~0ull;
+    bool counting = false;
+    int cnt_warps = 0;
+    int32_t *pptr = nullptr, *pcl = nullptr, *ninc = nullptr;             // counting
+    int32_t *kptr = nullptr, *kcl = nullptr, *iptr = nullptr, *ilit = nullptr;  // key literal
+    void release() {
+        for (int32_t **p : {&pptr, &pcl, &ninc, &kptr, &kcl, &iptr, &ilit}) {
+            if (*p) cudaFree(*p);
+            *p = nullptr;
+        }
+        version = ~0ull;
+    }
+    void release_after(cudaStream_t st) {  // after the kernels queued on st
+        cudaStreamSynchronize(st);
+        release();
+    }
+};
+
 struct tmb_sparse {
     tmb_sparse_cfg cfg;
+    uint64_t version = 0;  // bumped whenever the model changes (train / feedback / set)
+    SparseIndex ix;
     int n_cta = 0, threads = 512;
     size_t smem = 0;
     bool resident = false;  // clause lists held in shared memory by the trainer
@@ -1205,6 +1344,7 @@ int tmb_sparse_layout(const tmb_sparse *sp, int64_t *out4) {
 }
 
 int tmb_sparse_destroy(tmb_sparse *sp) {
+    if (sp) sp->ix.release();
     if (!sp) return TMB_OK;
     for (int b = 0; b < 2; ++b) {
         if (sp->lits[b]) cudaFree(sp->lits[b]);
@@ -1221,6 +1361,7 @@ int tmb_sparse_destroy(tmb_sparse *sp) {
 int tmb_sparse_train(tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
                      const int32_t *labels, const int32_t *order, int64_t n_steps,
                      uint64_t fb_counter, tmb_train_stats *stats, void *stream) {
+    if (sp) ++sp->version;  // the compiled inference index is stale
     if (!sp) return fail(TMB_E_INVALID, "sparse_train: NULL");
     if (n_steps <= 0) return TMB_OK;
     if (!indptr || !indices || !labels || !order) return fail(TMB_E_INVALID, "sparse_train: NULL data");
@@ -1249,6 +1390,7 @@ int tmb_sparse_feedback(tmb_sparse *sp, const int32_t *active, int64_t n_active,
                         const uint8_t *outputs, int64_t label, int64_t negative,
                         const uint8_t *ut, const uint8_t *un, uint64_t stream_seed,
                         uint64_t counter, uint64_t *counter_out, void *stream) {
+    if (sp) ++sp->version;  // the compiled inference index is stale
     if (!sp) return fail(TMB_E_INVALID, "sparse_feedback: NULL");
     if (sp->cfg.n_blocks != 1) return fail(TMB_E_UNSUPPORTED, "sparse_feedback: one block only");
     if (!outputs || !ut || !un || (n_active > 0 && !active) || label < 0 ||
@@ -1310,6 +1452,7 @@ int tmb_sparse_get(const tmb_sparse *sp, int32_t *lens, int32_t *lits, int8_t *s
 
 int tmb_sparse_set(tmb_sparse *sp, const int32_t *lens, const int32_t *lits, const int8_t *states,
                    const int32_t *weights, const uint64_t *block_counters, void *stream) {
+    if (sp) ++sp->version;  // the compiled inference index is stale
     if (!sp) return fail(TMB_E_INVALID, "sparse_set: NULL");
     cudaStream_t st = as_stream(stream);
     const int64_t C = sp->cfg.n_clauses, slab = sp->cfg.slab, K = sp->cfg.n_classes;
@@ -1326,65 +1469,86 @@ int tmb_sparse_set(tmb_sparse *sp, const int32_t *lens, const int32_t *lits, con
     return TMB_OK;
 }
 
-static int sparse_infer_impl(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
-                             int64_t N, int64_t *votes, int64_t *pred, uint8_t *outputs,
-                             void *stream) {
-    if (!sp) return fail(TMB_E_INVALID, "sparse_infer: NULL");
-    if (N < 0 || (N > 0 && (!indptr || !indices))) return fail(TMB_E_INVALID, "sparse_infer: bad args");
-    if (N == 0) return TMB_OK;
-    cudaStream_t st = as_stream(stream);
+// Compiled inference index of a sparse model (the included literals of
+// every clause), kept in the handle and rebuilt only when the model changed
+// (tmb_sparse::version) -- except the key-literal form, whose keys depend
+// on the query's id frequencies and are rebuilt per call.
+static int build_infer_index(tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,
+                             int64_t N, cudaStream_t st) {
+    SparseIndex &ix = sp->ix;
     const int64_t C = sp->cfg.n_clauses, slab = sp->cfg.slab, K = sp->cfg.n_classes;
     const int64_t L = sp->cfg.n_literals;
-    // model compile step (once per call, a few MB): the included literals
-    // of every clause from the device lists
+    int dev = 0, max_smem = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t per_warp_cnt = 4 * (size_t)((C + 3) & ~3LL) + 8 * (size_t)K;
+    const int cnt_warps =
+        (int)std::min<size_t>(8, (size_t)std::min(max_smem, 200 * 1024) / per_warp_cnt);
+    const bool counting = cnt_warps >= 2 && !g_sparse_infer_key;
+    ix.release();
     std::vector<uint8_t> cur(C);
     std::vector<int32_t> len(C);
     TMB_CUDA(cudaMemcpyAsync(cur.data(), sp->cur, C, cudaMemcpyDeviceToHost, st));
     TMB_CUDA(cudaMemcpyAsync(len.data(), sp->len, 4 * C, cudaMemcpyDeviceToHost, st));
-    // a sample of the query's ids (up to 2^20) estimates literal frequencies
-    int64_t nnz = 0;
-    TMB_CUDA(cudaMemcpyAsync(&nnz, indptr + N, 8, cudaMemcpyDeviceToHost, st));
-    TMB_CUDA(cudaStreamSynchronize(st));
-    int64_t a_first = 0;
-    TMB_CUDA(cudaMemcpyAsync(&a_first, indptr, 8, cudaMemcpyDeviceToHost, st));
-    TMB_CUDA(cudaStreamSynchronize(st));
-    const int64_t n_sample = std::max<int64_t>(0, std::min<int64_t>(nnz - a_first, 1 << 20));
-    std::vector<int32_t> sample((size_t)n_sample);
-    if (n_sample)
-        TMB_CUDA(cudaMemcpyAsync(sample.data(), indices + a_first, 4 * n_sample,
-                                 cudaMemcpyDeviceToHost, st));
-    std::vector<int32_t> hl(C * slab);
-    std::vector<int8_t> hs(C * slab);
-    for (int b = 0; b < 2; ++b) {
-        std::vector<int32_t> tl(C * slab);
-        std::vector<int8_t> ts(C * slab);
-        TMB_CUDA(cudaMemcpyAsync(tl.data(), sp->lits[b], 4 * C * slab, cudaMemcpyDeviceToHost, st));
-        TMB_CUDA(cudaMemcpyAsync(ts.data(), sp->sts[b], C * slab, cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> sample;
+    if (!counting) {  // a sample of the query's ids (up to 2^20) estimates frequencies
+        int64_t ends[2] = {0, 0};
+        TMB_CUDA(cudaMemcpyAsync(&ends[0], indptr, 8, cudaMemcpyDeviceToHost, st));
+        TMB_CUDA(cudaMemcpyAsync(&ends[1], indptr + N, 8, cudaMemcpyDeviceToHost, st));
         TMB_CUDA(cudaStreamSynchronize(st));
-        for (int64_t c = 0; c < C; ++c)
-            if (cur[c] == b)
-                for (int q = 0; q < len[c]; ++q) {
-                    hl[c * slab + q] = tl[c * slab + q];
-                    hs[c * slab + q] = ts[c * slab + q];
-                }
+        const int64_t n_sample = std::max<int64_t>(0, std::min<int64_t>(ends[1] - ends[0], 1 << 20));
+        sample.resize((size_t)n_sample);
+        if (n_sample)
+            TMB_CUDA(cudaMemcpyAsync(sample.data(), indices + ends[0], 4 * n_sample,
+                                     cudaMemcpyDeviceToHost, st));
     }
+    TMB_CUDA(cudaStreamSynchronize(st));
     std::vector<int32_t> inc_ptr(C + 1, 0), inc_lits;
-    std::vector<int32_t> n_clauses_of;  // literal -> number of clauses including it
-    std::vector<uint32_t> freq;         // literal -> occurrences in the sample
-    std::vector<std::pair<int32_t, int32_t>> keyed;  // (key literal, clause)
     {
-        std::vector<int32_t> ids;
+        std::vector<int32_t> tl[2];
+        std::vector<int8_t> ts[2];
+        for (int b = 0; b < 2; ++b) {
+            tl[b].resize(C * slab);
+            ts[b].resize(C * slab);
+            TMB_CUDA(cudaMemcpyAsync(tl[b].data(), sp->lits[b], 4 * C * slab, cudaMemcpyDeviceToHost, st));
+            TMB_CUDA(cudaMemcpyAsync(ts[b].data(), sp->sts[b], C * slab, cudaMemcpyDeviceToHost, st));
+        }
+        TMB_CUDA(cudaStreamSynchronize(st));
         for (int64_t c = 0; c < C; ++c) {
+            const int b = cur[c];
             for (int q = 0; q < len[c]; ++q)
-                if (hs[c * slab + q] >= 0) inc_lits.push_back(hl[c * slab + q]);
+                if (ts[b][c * slab + q] >= 0) inc_lits.push_back(tl[b][c * slab + q]);
             inc_ptr[c + 1] = (int32_t)inc_lits.size();
         }
-        // sparse per-literal statistics over the literals that are included
-        ids = inc_lits;
+    }
+    int rc = TMB_OK;
+    auto up = [&](int32_t **dst, const std::vector<int32_t> &v) {
+        if (rc) return;
+        rc = check_cuda(cudaMalloc(dst, 4 * std::max<size_t>(v.size(), 1)), "cudaMalloc");
+        if (!rc && !v.empty())
+            rc = check_cuda(cudaMemcpyAsync(*dst, v.data(), 4 * v.size(), cudaMemcpyHostToDevice, st), "H2D");
+    };
+    if (counting) {
+        std::vector<int32_t> post_ptr(L + 1, 0), n_inc(C, 0);
+        for (int64_t c = 0; c < C; ++c) {
+            n_inc[c] = inc_ptr[c + 1] - inc_ptr[c];
+            for (int32_t q = inc_ptr[c]; q < inc_ptr[c + 1]; ++q) ++post_ptr[inc_lits[q] + 1];
+        }
+        for (int64_t l = 0; l < L; ++l) post_ptr[l + 1] += post_ptr[l];
+        std::vector<int32_t> post_clause(inc_lits.size()), fillp(post_ptr.begin(), post_ptr.end() - 1);
+        for (int64_t c = 0; c < C; ++c)
+            for (int32_t q = inc_ptr[c]; q < inc_ptr[c + 1]; ++q)
+                post_clause[fillp[inc_lits[q]]++] = (int32_t)c;
+        up(&ix.pptr, post_ptr);
+        up(&ix.pcl, post_clause);
+        up(&ix.ninc, n_inc);
+    } else {
+        // key = the included literal the sample contains least often (ties:
+        // the one fewest clauses include)
+        std::vector<int32_t> ids(inc_lits);
         std::sort(ids.begin(), ids.end());
         ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
-        n_clauses_of.assign(ids.size(), 0);
-        freq.assign(ids.size(), 0);
+        std::vector<uint32_t> freq(ids.size(), 0), n_clauses_of(ids.size(), 0);
         auto idx = [&](int32_t lit) {
             return (size_t)(std::lower_bound(ids.begin(), ids.end(), lit) - ids.begin());
         };
@@ -1393,6 +1557,7 @@ static int sparse_infer_impl(const tmb_sparse *sp, const int64_t *indptr, const 
             const size_t i = idx(v);
             if (i < ids.size() && ids[i] == v) ++freq[i];
         }
+        std::vector<std::pair<int32_t, int32_t>> keyed;
         for (int64_t c = 0; c < C; ++c) {
             if (inc_ptr[c + 1] == inc_ptr[c]) continue;  // no includes: never fires
             int32_t key = -1;
@@ -1407,53 +1572,70 @@ static int sparse_infer_impl(const tmb_sparse *sp, const int64_t *indptr, const 
             }
             keyed.emplace_back(key, (int32_t)c);
         }
-    }
-    std::vector<int32_t> key_ptr(L + 1, 0), key_clause(keyed.size());
-    for (auto &kc : keyed) ++key_ptr[kc.first + 1];
-    for (int64_t l = 0; l < L; ++l) key_ptr[l + 1] += key_ptr[l];
-    {
+        std::vector<int32_t> key_ptr(L + 1, 0), key_clause(keyed.size());
+        for (auto &kc : keyed) ++key_ptr[kc.first + 1];
+        for (int64_t l = 0; l < L; ++l) key_ptr[l + 1] += key_ptr[l];
         std::vector<int32_t> fillp(key_ptr.begin(), key_ptr.end() - 1);
         for (auto &kc : keyed) key_clause[fillp[kc.first]++] = kc.second;
+        up(&ix.kptr, key_ptr);
+        up(&ix.kcl, key_clause);
+        up(&ix.iptr, inc_ptr);
+        up(&ix.ilit, inc_lits);
     }
-    int32_t *d_kptr = nullptr, *d_kcl = nullptr, *d_iptr = nullptr, *d_ilit = nullptr;
-    TMB_CUDA(cudaMallocAsync(&d_kptr, 4 * (L + 1), st));
-    TMB_CUDA(cudaMallocAsync(&d_kcl, 4 * std::max<size_t>(key_clause.size(), 1), st));
-    TMB_CUDA(cudaMallocAsync(&d_iptr, 4 * (C + 1), st));
-    TMB_CUDA(cudaMallocAsync(&d_ilit, 4 * std::max<size_t>(inc_lits.size(), 1), st));
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "index upload");
+    if (rc) {
+        ix.release();
+        return rc;
+    }
+    ix.counting = counting;
+    ix.cnt_warps = cnt_warps;
+    ix.version = counting ? sp->version : ~0ull;
+    return TMB_OK;
+}
+
+static int sparse_infer_impl(const tmb_sparse *csp, const int64_t *indptr, const int32_t *indices,
+                             int64_t N, int64_t *votes, int64_t *pred, uint8_t *outputs,
+                             void *stream) {
+    if (!csp) return fail(TMB_E_INVALID, "sparse_infer: NULL");
+    if (N < 0 || (N > 0 && (!indptr || !indices))) return fail(TMB_E_INVALID, "sparse_infer: bad args");
+    if (N == 0) return TMB_OK;
+    tmb_sparse *sp = const_cast<tmb_sparse *>(csp);  // the index cache only
+    cudaStream_t st = as_stream(stream);
+    const int64_t C = sp->cfg.n_clauses, K = sp->cfg.n_classes;
     int rc = TMB_OK;
-    auto h2d = [&](void *dst, const void *src, size_t bytes) {
-        if (!rc && bytes) rc = check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
-    };
-    h2d(d_kptr, key_ptr.data(), 4 * key_ptr.size());
-    h2d(d_kcl, key_clause.data(), 4 * key_clause.size());
-    h2d(d_iptr, inc_ptr.data(), 4 * inc_ptr.size());
-    h2d(d_ilit, inc_lits.data(), 4 * inc_lits.size());
+    if (!(sp->ix.counting && sp->ix.version == sp->version && !g_sparse_infer_key))
+        if ((rc = build_infer_index(sp, indptr, indices, N, st))) return rc;
+    const SparseIndex &ix = sp->ix;
     SparseInferK k{};
     k.indptr = indptr; k.indices = indices; k.N = N;
-    k.key_ptr = d_kptr; k.key_clause = d_kcl; k.inc_ptr = d_iptr; k.inc_lits = d_ilit;
-    k.n_literals = L; k.weights = sp->weights; k.C = (int)C; k.K = (int)K;
+    k.key_ptr = ix.kptr; k.key_clause = ix.kcl; k.inc_ptr = ix.iptr; k.inc_lits = ix.ilit;
+    k.post_ptr = ix.pptr; k.post_clause = ix.pcl; k.n_inc = ix.ninc;
+    k.n_literals = sp->cfg.n_literals; k.weights = sp->weights; k.C = (int)C; k.K = (int)K;
     k.votes = votes; k.pred = pred; k.outputs = outputs;
-    if (!rc && outputs) rc = check_cuda(cudaMemsetAsync(outputs, 0, (size_t)N * C, st), "memset");
-    const int threads = 256;
-    const size_t smem = 8 * (size_t)K * (threads / 32);
+    if (outputs) TMB_CUDA(cudaMemsetAsync(outputs, 0, (size_t)N * C, st));
+    const bool counting = ix.counting;
+    const int threads = counting ? 32 * ix.cnt_warps : 256;
+    const size_t smem = counting ? (4 * (size_t)((C + 3) & ~3LL) + 8 * (size_t)K) * ix.cnt_warps
+                                 : 8 * (size_t)K * (threads / 32);
     int dev = 0, max_smem = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (!rc && smem > (size_t)max_smem) rc = fail(TMB_E_UNSUPPORTED, "sparse_infer: too many classes");
-    if (!rc) rc = check_cuda(cudaFuncSetAttribute((const void *)k_sparse_infer,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)smem), "smem attribute");
-    if (!rc) {
-        const int64_t grid = std::min<int64_t>((N + 7) / 8, (int64_t)sm_count() * 8);
-        k_sparse_infer<<<(unsigned)grid, threads, smem, st>>>(k);
-        note_launch();
-        rc = check_cuda(cudaGetLastError(), "kernel launch");
-    }
-    cudaFreeAsync(d_kptr, st);
-    cudaFreeAsync(d_kcl, st);
-    cudaFreeAsync(d_iptr, st);
-    cudaFreeAsync(d_ilit, st);
-    return rc;
+    if (smem > (size_t)max_smem) return fail(TMB_E_UNSUPPORTED, "sparse_infer: too many classes");
+    const void *fn = counting ? (K <= 2 ? (const void *)k_sparse_infer_count<2>
+                                 : K <= 8 ? (const void *)k_sparse_infer_count<8>
+                                          : (const void *)k_sparse_infer_count<0>)
+                              : (K <= 2 ? (const void *)k_sparse_infer<2>
+                                 : K <= 8 ? (const void *)k_sparse_infer<8>
+                                          : (const void *)k_sparse_infer<0>);
+    TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t per_cta = threads / 32;
+    const int64_t per_sm = counting ? std::max<int64_t>(1, (220 * 1024) / (int64_t)smem) : 8;
+    const int64_t grid = std::min<int64_t>((N + per_cta - 1) / per_cta, (int64_t)sm_count() * per_sm);
+    void *args[] = {&k};
+    TMB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(threads), args, smem, st));
+    TMB_LAUNCHED();
+    if (!counting) sp->ix.release_after(st);  // key-literal index: per call
+    return TMB_OK;
 }
 
 int tmb_sparse_infer(const tmb_sparse *sp, const int64_t *indptr, const int32_t *indices,

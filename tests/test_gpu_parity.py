@@ -676,9 +676,12 @@ def test_configs1_three_full_epochs_vs_oracle(gpu):
     assert fb == int(g["fb_counter"]) and sh == int(g["shuffle_counter"])
 
 
+@pytest.mark.parametrize("kernel", ["count", "key"])
 @pytest.mark.parametrize("K,n_docs,doc_len", [(40, 300, 60), (3, 200, 500), (2, 50, 5000)])
-def test_sparse_inference_no_hit_or_class_limits(gpu, oracle, K, n_docs, doc_len):
-    """Key-literal sparse inference has no per-document buffers: thousands of
+def test_sparse_inference_no_hit_or_class_limits(gpu, oracle, kernel, K, n_docs, doc_len):
+    """Both sparse inference kernels (per-warp clause counters; key-literal
+    candidates for clause counts too large for the counters) have no
+    per-document buffers: thousands of
     clause postings per document (clauses over a small pool of common
     literals), more than 32 classes, documents longer than 4096 ids, empty
     clauses and empty documents -- votes and outputs equal the oracle's
@@ -713,12 +716,16 @@ def test_sparse_inference_no_hit_or_class_limits(gpu, oracle, K, n_docs, doc_len
                                       rs.integers(0, L, size=n)]))
         docs.append(d.astype(np.int64))
     ex = [gpu.SparseExample(d, 0) for d in docs]
-    votes = bank.batch_votes(ex)
-    assert np.array_equal(votes, oracle.sparse_batch_votes([ob], docs))
-    from paper_2405_04212_b200.sparse_train import sparse_outputs
-    outs = sparse_outputs(bank, ex[:40], gpu.EvalMode.INFERENCE)
-    for i in range(40):
-        assert np.array_equal(outs[i], ob.clause_outputs(docs[i], False)), i
+    gpu._lib.call("tmb_set_option", b"sparse.infer_key", int(kernel == "key"))
+    try:
+        votes = bank.batch_votes(ex)
+        assert np.array_equal(votes, oracle.sparse_batch_votes([ob], docs))
+        from paper_2405_04212_b200.sparse_train import sparse_outputs
+        outs = sparse_outputs(bank, ex[:40], gpu.EvalMode.INFERENCE)
+        for i in range(40):
+            assert np.array_equal(outs[i], ob.clause_outputs(docs[i], False)), i
+    finally:
+        gpu._lib.call("tmb_set_option", b"sparse.infer_key", 0)
 
 
 def _sparse_docs(rs, n_docs, vocab, lo, hi, planted):
