@@ -63,7 +63,7 @@ for f in sorted(glob.glob(f"gpurun_out/{TAG}_*_launches.csv")):
                                    for k, v in sorted(per.items(), key=lambda x: -x[1][1])}
     os.system(f"cp {f} profiles/")
 json.dump(shares, open(f"profiles/{TAG}_launch_shares.json", "w"), indent=1)
-for b in glob.glob(f"gpurun_out/{TAG}_bench.json"):
+for b in glob.glob(f"gpurun_out/{TAG}_bench*.json") + glob.glob(f"gpurun_out/{TAG}_int_peaks.json"):
     os.system(f"cp {b} profiles/")
 print(json.dumps(summary, indent=1))
 print(json.dumps(shares, indent=1))
