@@ -755,14 +755,14 @@ def ct_ptr(t):
 
 def c4_ncu_sample():
     """DRAM bytes per example of the generic grid trainer from the committed
-    ncu capture of tools/c4_once.py (one 1000-step launch, examples 0..999 of
+    ncu capture of tools/probes/c4_once.py (one 1000-step launch, examples 0..999 of
     epoch 1: more events per example than the bench's later steps, so this
     is a traffic-per-example sample, not the bench launch)."""
     tot, src = ncu_traffic("k_train<")
     if tot is None:
         return None
     return {"dram_bytes_per_example": tot / 1000.0, "source": src,
-            "sample": "tools/c4_once.py: 1000 steps from a fresh model"}
+            "sample": "tools/probes/c4_once.py: 1000 steps from a fresh model"}
 
 
 def bench_c4_train(args, rank, world, local):
