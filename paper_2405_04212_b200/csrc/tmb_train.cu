@@ -1499,6 +1499,174 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_fast(TrainK k) {
     flush_stats(k, cn, rank == 0);
 }
 
+// --------------------------------------------------------- tiny banks --
+// One warp trains the whole bank (C <= 32 clauses, P <= 1024 positions,
+// K <= 32): lane c owns clause c (output, flag draws, event ordinals, event
+// types, weights); the lanes sweep the positions of each event together.
+// No block barrier, no exchange -- the per-example dependency chain of
+// executor.py:326-330 is a handful of shuffles.  Same arithmetic as the
+// other trainers (kernels/_numba.py:36-125, feedback.py:33-53).
+constexpr int kWarpMaxC = 32, kWarpMaxW = 32;
+
+__global__ void __launch_bounds__(32, 1) k_train_warp(TrainK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x;
+    const int C = k.C, P = k.P, K = k.K, W = k.W, nb = k.n_blocks;
+    const int Pp = (P + 3) & ~3;
+    int8_t *st = reinterpret_cast<int8_t *>(smem_raw);                        // [C][Pp]
+    uint32_t *masks = reinterpret_cast<uint32_t *>(st + align_up((size_t)C * Pp, 16));  // [C][W]
+    int32_t *wts = reinterpret_cast<int32_t *>(masks + (size_t)C * W);        // [C][K]
+    uint64_t *bctr = reinterpret_cast<uint64_t *>(
+        align_up(reinterpret_cast<uintptr_t>(wts + (size_t)C * K), 8));       // [nb]
+    for (int i = lane; i < C * P; i += 32) st[(i / P) * Pp + i % P] = k.states[i];
+    for (int i = lane; i < C * K; i += 32) wts[i] = k.weights[i];
+    for (int i = lane; i < nb; i += 32) bctr[i] = k.block_counters[i];
+    __syncwarp();
+    // include masks / counts of clause c from its states (warp-collective)
+    auto rebuild = [&](int c) {
+        int n = 0;
+        for (int r = 0; r < W; ++r) {
+            const int p = 32 * r + lane;
+            const unsigned m = __ballot_sync(0xffffffffu, p < P && st[c * Pp + p] >= 0);
+            if (lane == 0) masks[c * W + r] = m;
+            n += __popc(m);
+        }
+        return n;
+    };
+    int cnt = 0;  // lane c: include count of clause c
+    for (int c = 0; c < C; ++c) {
+        const int n = rebuild(c);
+        if (lane == c) cnt = n;
+    }
+    __syncwarp();
+    const int c = lane;
+    const bool real = c < C;
+    const int b = real ? block_of(c, C, nb) : 0;
+    const int bstart = block_begin(b, C, nb);
+    const bool blast = real && (c == C - 1 || block_of(c + 1, C, nb) != b);
+    const uint64_t bseed = real ? k.block_seeds[b] : 0;
+    const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
+    Counters cn;
+    // the next example's index, label and literal row are loaded one step
+    // ahead (the dependent global loads would otherwise open every step)
+    int ex_n = k.n_steps > 0 ? __ldg(&k.order[0]) : 0;
+    int label_n = k.n_steps > 0 ? __ldg(&k.labels[ex_n]) : 0;
+    uint32_t litw_n = (k.n_steps > 0 && lane < W) ? __ldg(&k.lit_words[(int64_t)ex_n * W + lane]) : 0u;
+    int ex_nn = k.n_steps > 1 ? __ldg(&k.order[1]) : 0;
+    for (int64_t i = 0; i < k.n_steps; ++i) {
+        const int label = label_n;
+        const uint32_t litw = litw_n;
+        if (i + 1 < k.n_steps) {
+            label_n = __ldg(&k.labels[ex_nn]);
+            litw_n = lane < W ? __ldg(&k.lit_words[(int64_t)ex_nn * W + lane]) : 0u;
+            ex_nn = i + 2 < k.n_steps ? __ldg(&k.order[i + 2]) : 0;
+        }
+        const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
+        const int neg = negative_class(k, label, fbc);
+        // 1. training-mode outputs (kernels/_numba.py:36-50)
+        uint32_t viol = 0;
+        for (int r = 0; r < W; ++r) {
+            const uint32_t lw = __shfl_sync(0xffffffffu, litw, r);
+            if (real) viol |= masks[c * W + r] & ~lw;
+        }
+        const bool out = real && viol == 0 && cnt <= k.budget;
+        // 2. class sums of the label and the negative class (dense.py:153)
+        long long vl, vn;
+        warp_sum2(out ? wts[c * K + label] : 0, out ? wts[c * K + neg] : 0, vl, vn);
+        // 3. decision and update flags (feedback.py:33-53)
+        uint64_t tt, tn;
+        if (k.thr_tab) {  // threshold_of(a, T) for a in [0, 2T], precomputed
+            const long long T = k.T;
+            const long long cl = vl < -T ? -T : (vl > T ? T : vl);
+            const long long cv = vn < -T ? -T : (vn > T ? T : vn);
+            tt = __ldg(&k.thr_tab[T - cl]);
+            tn = __ldg(&k.thr_tab[T + cv]);
+        } else {
+            decide(k, vl, vn, tt, tn);
+        }
+        const bool ut = real && draw53(k.fb_seed, fbc + 1 + (uint64_t)c) < tt;
+        const bool un = real && draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)c) < tn;
+        // 4. event ordinals within the clause block (kernels/_numba.py:101-125)
+        const int e = (ut ? 1 : 0) + (un ? 1 : 0);
+        int incl = e;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int before_block = __shfl_sync(0xffffffffu, incl - e, bstart & 31);
+        const uint64_t ord = real ? bctr[b] + (uint64_t)(incl - e - before_block) : 0;
+        // 5. event types, weights (feedback first, then weight: SPEC.md:171)
+        bool t1 = false, n1 = false;
+        if (real && e) {
+            int32_t *w = wts + c * K;
+            t1 = w[label] >= 0;
+            n1 = w[neg] < 0;
+            if (ut) { ++cn.events; if (t1) ++cn.t1; else if (out) ++cn.t2; }
+            if (un) { ++cn.events; if (n1) ++cn.t1; else if (out) ++cn.t2; }
+            if (out) {
+                if (ut) w[label] += 1;
+                if (un) w[neg] -= 1;
+            }
+        }
+        __syncwarp();
+        if (blast) bctr[b] += (uint64_t)(incl - before_block);
+        // 6. per-position feedback of the clauses whose states can move
+        const bool work = (ut && (t1 || out)) || (un && (n1 || out));
+        unsigned todo = __ballot_sync(0xffffffffu, work);
+        unsigned nd = 0, nupd = 0;
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int jo = __shfl_sync(0xffffffffu, out ? 1 : 0, j);
+            const bool jt = __shfl_sync(0xffffffffu, ut, j), jn = __shfl_sync(0xffffffffu, un, j);
+            const bool jt1 = __shfl_sync(0xffffffffu, t1, j), jn1 = __shfl_sync(0xffffffffu, n1, j);
+            const uint64_t jord = __shfl_sync(0xffffffffu, ord, j);
+            const uint64_t jseed = __shfl_sync(0xffffffffu, bseed, j);
+            for (int r = 0; r < W; ++r) {
+                const int p = 32 * r + lane;
+                const uint32_t lw = __shfl_sync(0xffffffffu, litw, r);
+                if (p >= P) continue;
+                const int lit = (lw >> lane) & 1;
+                int s0 = st[j * Pp + p], sv = s0;
+                uint64_t d = 0;
+                for (int ev = 0; ev < 2; ++ev) {
+                    const bool has = ev == 0 ? jt : jn;
+                    if (!has) continue;
+                    const bool ti = ev == 0 ? jt1 : jn1;
+                    if (ti) {
+                        const uint64_t o = jord + (uint64_t)(ev == 1 && jt ? 1 : 0);
+                        const uint64_t sk = jseed + kGolden * ((o << 32) + 1);
+                        sv = type_i_stream(sv, lit, jo, k.fp, sk, (uint32_t)p, d);
+                    } else {
+                        sv = type_ii(sv, lit, jo);
+                    }
+                }
+                nd += (unsigned)d;
+                nupd += sv != s0 ? 1u : 0u;
+                st[j * Pp + p] = (int8_t)sv;
+            }
+            __syncwarp();
+            const int n = rebuild(j);
+            if (lane == j) cnt = n;
+            __syncwarp();
+        }
+        cn.draws += nd;
+        cn.upd += nupd;
+    }
+    __syncwarp();
+    for (int i = lane; i < C * P; i += 32) k.states[i] = st[(i / P) * Pp + i % P];
+    for (int i = lane; i < C * K; i += 32) k.weights[i] = wts[i];
+    for (int i = lane; i < nb; i += 32) k.block_counters[i] = bctr[i];
+    flush_stats(k, cn, true);
+}
+
+size_t warp_kernel_smem(int C, int P, int K, int W, int nb) {
+    const size_t Pp = (size_t)((P + 3) & ~3);
+    return align_up(align_up((size_t)C * Pp, 16) + 4 * (size_t)C * W + 4 * (size_t)C * K, 8) +
+           8 * (size_t)nb + 16;
+}
+
 }  // namespace tmb
 
 using namespace tmb;
@@ -1509,6 +1677,7 @@ struct tmb_trainer {
     int32_t *weights;
     uint64_t *block_counters;
     int n_cta, threads, smem, smem_states, cluster;
+    int warp = 0;  // k_train_warp (one warp, tiny banks)
     uint64_t launches = 0;
     TrainK k;
     uint64_t *block_seeds_d = nullptr;
@@ -1669,8 +1838,18 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
             return fail(TMB_E_UNSUPPORTED, "trainer_create: grid cannot be co-resident");
     }
 
+    // tiny banks (C, K <= 32, literal rows of <= 32 words) on one CTA: the
+    // single-warp trainer (flags bit 3 keeps the generic cluster kernel)
+    const size_t warp_smem = warp_kernel_smem(C, P, K, W, (int)c.n_blocks);
+    const bool warp_k = n_cta == 1 && C <= kWarpMaxC && K <= 32 && W <= kWarpMaxW &&
+                        !(c.flags & 8) && warp_smem <= (size_t)max_smem;
+    if (warp_k && warp_smem > 48 * 1024)
+        TMB_CUDA(cudaFuncSetAttribute((const void *)k_train_warp,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_smem));
+
     tmb_trainer *t = new tmb_trainer();
     t->cfg = c;
+    t->warp = warp_k ? 1 : 0;
     t->states = states; t->weights = weights; t->block_counters = block_counters;
     t->n_cta = n_cta; t->threads = threads; t->smem = (int)need;
     t->smem_states = smem_states; t->cluster = cluster;
@@ -1684,7 +1863,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
         return rc;
     }
     k.block_seeds = t->block_seeds_d;
-    if (k.thr_smem) {
+    if (k.thr_smem || (t->warp && c.threshold <= (1 << 20))) {
         std::vector<uint64_t> tab((size_t)(2 * c.threshold + 1));
         for (int64_t a = 0; a <= 2 * c.threshold; ++a) tab[a] = threshold_of(a, c.threshold);
         if ((rc = check_cuda(cudaMalloc(&t->thr_d, 8 * tab.size()), "cudaMalloc")) ||
@@ -1750,7 +1929,7 @@ int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_b
                      int *states_in_smem) {
     if (!t) return fail(TMB_E_INVALID, "trainer_info: NULL");
     if (n_cta) *n_cta = t->n_cta;
-    if (threads) *threads = t->threads;
+    if (threads) *threads = t->warp ? 32 : t->threads;
     if (smem_bytes) *smem_bytes = t->smem;
     if (states_in_smem) *states_in_smem = t->smem_states;
     return TMB_OK;
@@ -1769,6 +1948,15 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     k.n_steps = n_steps; k.fb_counter0 = fb_counter; k.stats = stats;
     k.dbg = g_train_dbg;
     void *args[] = {&k};
+    if (t->warp) {
+        const size_t sm = warp_kernel_smem(k.C, k.P, k.K, k.W, k.n_blocks);
+        if (sm > 48 * 1024)
+            TMB_CUDA(cudaFuncSetAttribute((const void *)k_train_warp,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_train_warp<<<1, 32, sm, st>>>(k);
+        TMB_LAUNCHED();
+        return TMB_OK;
+    }
     const void *fn = kernel_for(t->cluster, t->smem_states, k.fast, k.phase != nullptr);
     // the dynamic shared-memory limit is a per-function attribute: another
     // trainer of a different shape may have lowered it since create

@@ -115,7 +115,8 @@ class DenseTrainSession:
     def __init__(self, cfg: Config, x: np.ndarray, y: np.ndarray, n_cta: int = 0,
                  threads: int = 0, states: np.ndarray | None = None,
                  weights: np.ndarray | None = None, states_in_hbm: bool = False,
-                 flag_keys: bool = True, balanced_feedback: bool = True):
+                 flag_keys: bool = True, balanced_feedback: bool = True,
+                 warp_kernel: bool = True):
         import torch
         require_device()
         self.cfg = cfg
@@ -136,7 +137,7 @@ class DenseTrainSession:
                            float(cfg.s), int(cfg.boost_true_positive), cfg.state_min,
                            cfg.state_max,
                            int(bool(states_in_hbm)) | (0 if flag_keys else 2) |
-                           (0 if balanced_feedback else 4),
+                           (0 if balanced_feedback else 4) | (0 if warp_kernel else 8),
                            cfg.seed & (2**64 - 1))
         self._h = ct.c_void_p()
         _lib.call("tmb_trainer_create", ct.byref(tc), ptr(self.states), ptr(self.weights),

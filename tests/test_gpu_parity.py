@@ -798,3 +798,31 @@ def test_train_rejects_non_binary_features(gpu):
     x = np.array([[0, 1, 2, 0], [1, 0, 0, 1]], dtype=np.uint8)
     with pytest.raises(gpu.DataError):
         gpu.train(cfg, (x, np.array([0, 1])), n_epochs=1)
+
+
+@pytest.mark.parametrize("F,C,K,nb,boost,budget", [
+    (12, 10, 2, 1, False, None), (6, 8, 2, 2, True, 3), (500, 32, 10, 3, False, 40),
+    (31, 17, 4, 5, True, None)])
+def test_single_warp_trainer_vs_oracle(gpu, oracle, F, C, K, nb, boost, budget):
+    """Tiny banks (C, K <= 32, literal rows <= 32 words) run on the
+    single-warp trainer; the generic one-CTA cluster kernel (warp_kernel=
+    False) and the oracle give the same model, counters and statistics."""
+    rs = np.random.default_rng(F + C + K)
+    x = rs.integers(0, 2, size=(400, F)).astype(np.uint8)
+    y = ((x[:, 0] ^ x[:, 1]) + 2 * x[:, 2] * (K > 2)).astype(np.int64) % K
+    cfg = gpu.Config(n_literals=F, n_clauses=C, n_classes=K, s=2.7, threshold=9, seed=C,
+                     n_blocks=nb, boost_true_positive=boost, n_literal_budget=budget)
+    ost, _ = oracle.train(cfg, x, y, 3)
+    stats = []
+    for warp in (True, False):
+        sess = gpu.DenseTrainSession(cfg, x, y, warp_kernel=warp)
+        assert sess.launch["threads"] == (32 if warp else sess.launch["threads"])
+        for _ in range(3):
+            sess.run_epoch()
+        m = sess.model()
+        assert np.array_equal(m.states, ost.states), warp
+        assert np.array_equal(m.weights, ost.weights), warp
+        assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64),
+                              ost.block_counters), warp
+        stats.append(sess.stats_dict())
+    assert stats[0] == stats[1]
