@@ -9,6 +9,12 @@ if REPO not in sys.path:
     sys.path.insert(0, REPO)
 GOLDEN = os.path.join(REPO, "tests", "golden")
 
+# tests/reference_backend/ holds the INTEGRATION.md stub and a reference-side
+# test module; they import `tsetlinkit` and only run inside the patched
+# reference copy tools/run_reference_suite.py builds (via
+# tests/test_reference_suite_b200.py), never from this tree.
+collect_ignore = ["reference_backend"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libtmb200.so")
