@@ -74,6 +74,7 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int sm_count();
 extern int64_t g_train_key_chunk;
 extern int g_train_dbg;  // trainer timing ablations (tmb_train.cu)
+extern int g_train_spec;  // speculative window of the fast grid trainer (tmb_train.cu)
 //  // keyed trainer: steps per launch override (tmb_train.cu)
 
 }  // namespace tmb

@@ -1605,6 +1605,11 @@ int tmb_set_option(const char *name, int64_t value) {
         g_train_key_chunk = value;
         return TMB_OK;
     }
+    if (std::string(name) == "train.spec_window") {  // 0: k_train_fast; 1..16: k_train_spec
+        if (value < 0 || value > 16) return fail(TMB_E_INVALID, "set_option: train.spec_window must be 0..16");
+        g_train_spec = (int)value;                   // (applies to trainers created afterwards)
+        return TMB_OK;
+    }
     if (std::string(name) == "train.debug_skip") {  // timing ablations only (not bit-exact)
         g_train_dbg = (int)value;
         return TMB_OK;

@@ -78,6 +78,8 @@ struct TrainK {
     // it fits, so the decision is one lookup instead of an f64 division
     const uint64_t *thr_tab;
     int thr_smem;
+    // speculative windows (k_train_spec): examples per window, 0 = k_train_fast
+    int spec;
 };
 
 // CTA owning clause c (inverse of cta_begin).
@@ -126,6 +128,9 @@ struct Smem {
     uint64_t *thr_tab;        // fast: [2T + 1] update thresholds (k.thr_smem)
     unsigned *wcnt;    // per-warp event counts [32]
     unsigned long long *vacc;  // grid: [2] CTA partial votes (label, negative)
+    uint32_t *hring;           // spec: [3 * spec][spec_hsz] staged step heads (ring i % HR)
+    uint32_t *obits;           // spec: [2 parity][cmax] clause outputs of a window (bit q)
+    unsigned long long *vwin;  // spec: [2 parity][spec][2] window partial class sums
     int *gpref;                // gbal: [n_cta + 1] prefix of the published work counts
     int *rc_clause, *rc_info;  // gbal: [cmax + 4] work items of this CTA's quad range
     uint64_t *rc_sk;           // gbal: [cmax + 4][2]
@@ -163,13 +168,19 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     const bool pre = 32 * k.fmax_words <= kMaxPrecompute;
     t.draw_t = pre && !k.fast ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
     t.draw_n = pre && !k.fast ? (uint64_t *)take(8 * 32 * k.fmax_words) : nullptr;
-    t.rec3 = k.fast ? (uint32_t *)take(4 * 4 * (size_t)k.R) : nullptr;
-    t.nout = k.fast ? (int *)take(4 * 2 * (size_t)k.cmax) : nullptr;
+    const bool fs = k.fast && !k.spec;  // k_train_fast's record ring and shadow sums
+    t.rec3 = fs ? (uint32_t *)take(4 * 4 * (size_t)k.R) : nullptr;
+    t.nout = fs ? (int *)take(4 * 2 * (size_t)k.cmax) : nullptr;
     t.oflag = k.fast ? (int *)take(4 * (size_t)k.cmax) : nullptr;
     t.wcnt = (unsigned *)take(4 * 64);  // [0, 32): per-warp prefix counts, [32, 64): totals
     t.vacc = (unsigned long long *)take(8 * 2);
-    t.clo = k.fast ? (long long *)take(8 * 4 * (size_t)k.cmax) : nullptr;
-    t.vsh = k.fast ? (unsigned long long *)take(8 * 4) : nullptr;
+    t.clo = fs ? (long long *)take(8 * 4 * (size_t)k.cmax) : nullptr;
+    t.vsh = fs ? (unsigned long long *)take(8 * 4) : nullptr;
+    const bool sp = k.fast && k.spec;
+    t.hring = sp ? (uint32_t *)take(4 * (size_t)(3 * k.spec) * (size_t)(4 + k.Wp + 260 + 2 * 64))
+                 : nullptr;
+    t.obits = sp ? (uint32_t *)take(4 * 2 * (size_t)k.cmax) : nullptr;
+    t.vwin = sp ? (unsigned long long *)take(8 * 2 * 2 * (size_t)k.spec) : nullptr;
     t.thr_tab = k.fast && k.thr_smem ? (uint64_t *)take(8 * (size_t)(2 * k.T + 1)) : nullptr;
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
     const bool gb = k.gbal && !k.fast && !smem_states && mode == MODE_GRID;
@@ -1499,6 +1510,361 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_fast(TrainK k) {
     flush_stats(k, cn, rank == 0);
 }
 
+// ------------------------------------------------- speculative windows --
+// k_train_spec: the fast path's records and feedback, with the per-example
+// grid exchange amortised over windows of up to k.spec consecutive steps.
+//
+// From epoch ~3 on, 80-90% of the steps are empty (both update probabilities
+// 0, feedback.py:33-44): nothing changes, so the next example's class sums
+// are already final.  Every CTA therefore evaluates a whole window of
+// examples with its current clauses and publishes all of their partial sums
+// at once; after ONE exchange every CTA knows the sums of every step of the
+// window and finds (identically) its first non-empty step.  Steps before it
+// are done; that step's events are applied exactly as in k_train_fast; the
+// next window starts right after it.  While warp 0 waits for window w, the
+// other warps already evaluate and publish window w+1 under the assumption
+// that w is all-empty (true most of the time), so runs of empty steps cost
+// max(exchange, evaluation) per window instead of one exchange per step.
+// A window whose speculation failed is simply abandoned: window numbers are
+// never reused (each has its own slots in k.rec), so stale partial sums can
+// never be mistaken for current ones.  The result is bit-identical to the
+// sequential loop (executor.py:275-340): every applied step sees exactly
+// the states the steps before it produced.
+constexpr int kSpecEnt = 64;  // flag entries per stream staged with each head
+__host__ __device__ inline int spec_hsz(const TrainK &k) { return 4 + k.Wp + 260 + 2 * kSpecEnt; }
+
+// Stage the heads of steps [from, to) -- example, label, negative class,
+// literal row, bucket starts and the first kSpecEnt flag entries of each
+// stream -- into ring slots i % (3 * spec), 16-B cp.async units spread over
+// threads t0, t0 + nt, ...
+__device__ __forceinline__ void spec_issue(const TrainK &k, const Smem &s, int64_t from, int64_t to,
+                                           int t0, int nt) {
+    const int nh = (4 + k.Wp + 260) / 4;
+    const int ne = min(kSpecEnt, k.Cp) / 4;
+    const int per = nh + 2 * ne;
+    const int HR = 3 * k.spec, HSZ = spec_hsz(k);
+    const int total = (int)(to - from) * per;
+    for (int u = t0; u < total; u += nt) {
+        const int st = u / per, q = u - st * per;
+        const int64_t i = from + st;
+        const uint32_t *src = k.recs + i * (int64_t)k.R;
+        uint32_t *dst = s.hring + (int)(i % HR) * HSZ;
+        if (q < nh) {
+            cp_async16(dst + 4 * q, src + 4 * q);
+        } else {
+            const int r = q - nh, str = r >= ne ? 1 : 0, e = r - str * ne;
+            cp_async16(dst + 4 * nh + str * kSpecEnt + 4 * e, src + rec_entries(k) + str * k.Cp + 4 * e);
+        }
+    }
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Outputs of own clause j (warp-collective) for the kk <= 16 examples of the
+// window whose first head sits in ring slot sb: lane q + 16h tests example q
+// on words h, h + 2, ...; bit q of ob[j]; the example's label / negative
+// class-sum contributions are added into vw[q][2].
+__device__ __forceinline__ void spec_eval_clause(const TrainK &k, const Smem &s, int j, int sb, int kk,
+                                                 uint32_t *ob, unsigned long long *vw) {
+    const int lane = threadIdx.x & 31, q = lane & 15, h = lane >> 4;
+    const int HR = 3 * k.spec, HSZ = spec_hsz(k);
+    const bool act = q < kk;
+    int slot = sb + (act ? q : 0);
+    if (slot >= HR) slot -= HR;
+    const uint32_t *hd = s.hring + slot * HSZ;
+    const uint32_t *lit = hd + 4;
+    const uint32_t *m = s.masks + j * k.W;
+    uint32_t viol = 0;
+#pragma unroll 4
+    for (int w = h; w < k.W; w += 2) viol |= m[w] & ~lit[w];
+    viol |= __shfl_xor_sync(0xffffffffu, viol, 16);
+    const bool o = act && viol == 0 && s.cnt[j] <= k.budget;
+    const unsigned bits = __ballot_sync(0xffffffffu, o) & 0xFFFFu;
+    if (lane == 0) ob[j] = bits;
+    if (h == 0 && o) {
+        const int32_t *w = s.weights + j * k.K;
+        const long long a = w[hd[1]], b = w[hd[2]];
+        if (a) atomicAdd(&vw[q * 2 + 0], (unsigned long long)a);
+        if (b) atomicAdd(&vw[q * 2 + 1], (unsigned long long)b);
+    }
+}
+
+// Event bookkeeping of own clause j for the applied step (fast_events
+// without the next-example correction: the next window is evaluated anew).
+__device__ __forceinline__ void spec_events(const TrainK &k, const Smem &s, Counters &cn, int j,
+                                            bool t_ev, bool n_ev, uint64_t ord, int label, int neg) {
+    int info = s.info[j] & I_OUT;
+    const bool out = info & I_OUT;
+    int32_t *w = s.weights + j * k.K;
+    const bool t1 = w[label] >= 0, n1 = w[neg] < 0;
+    const uint64_t bseed = s.blk_seed[0];
+    if (t_ev) {
+        info |= I_TEV | (t1 ? I_T1 : 0);
+        s.sk_t[j] = bseed + kGolden * ((ord << 32) + 1);
+        ++cn.events;
+        if (t1) ++cn.t1; else if (out) ++cn.t2;
+    }
+    if (n_ev) {
+        const uint64_t o2 = ord + (t_ev ? 1 : 0);
+        info |= I_NEV | (n1 ? I_N1 : 0);
+        s.sk_n[j] = bseed + kGolden * ((o2 << 32) + 1);
+        ++cn.events;
+        if (n1) ++cn.t1; else if (out) ++cn.t2;
+    }
+    if (out) {
+        if (t_ev) w[label] += 1;
+        if (n_ev) w[neg] -= 1;
+    }
+    s.info[j] = info;
+    if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
+        s.work[atomicAdd(&s.misc[0], 1)] = j;
+}
+
+template <bool SMEM_STATES>
+__global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    Smem s;
+    smem_layout(k, SMEM_STATES, MODE_GRID, smem_raw, &s);
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = nthr >> 5;
+    const int rank = blockIdx.x;
+    const int C = k.C, n_cta = k.n_cta;
+    const int c0 = cta_begin(rank, C, n_cta), c1 = cta_begin(rank + 1, C, n_cta);
+    const int cown = c1 - c0;
+    const int64_t n = k.n_steps;
+    const int KW = k.spec, HR = 3 * KW, HSZ = spec_hsz(k);
+    const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
+
+    load_slice<SMEM_STATES>(k, s, c0, cown);
+    if (k.thr_smem)
+        for (int64_t a = tid; a <= 2 * k.T; a += nthr) s.thr_tab[a] = k.thr_tab[a];
+    if (tid == 0) {
+        s.blk_ctr[0] = k.block_counters[0];
+        s.blk_seed[0] = k.block_seeds[0];
+        s.misc[0] = 0;
+    }
+    for (int j = tid; j < cown; j += nthr) s.oflag[j] = 0;
+    for (int q = tid; q < 4 * KW; q += nthr) s.vwin[q] = 0;
+    int64_t issued = n < (int64_t)HR ? n : (int64_t)HR;
+    spec_issue(k, s, 0, issued, tid, nthr);
+    cp_async_commit();
+    cp_async_wait_0();
+    __syncthreads();
+
+    // window 0: every warp evaluates, then publish
+    int64_t i0 = 0, wn = 0;
+    {
+        const int kk = (int)(n < (int64_t)KW ? n : (int64_t)KW);
+        for (int j = warp; j < cown; j += nwarps) spec_eval_clause(k, s, j, 0, kk, s.obits, s.vwin);
+        __syncthreads();
+        if (tid < 2 * kk) {
+            const long long v = (long long)s.vwin[tid];
+            s.vwin[tid] = 0;
+            red_relaxed_add_u64(&k.rec[tid], (1ull << 40) + (unsigned long long)(v + kVoteBias));
+        }
+    }
+
+    Counters cn;
+    const long long dec_bias = (long long)n_cta * kVoteBias;
+    const long long dec_2T = 2 * k.T;
+    const bool dec_tab = k.thr_smem != 0;
+    while (i0 < n) {
+        const int kk = (int)(n - i0 < (int64_t)KW ? n - i0 : (int64_t)KW);
+        const int par = (int)(wn & 1);
+        const int64_t i1 = i0 + kk;
+        const int kk1 = (int)(n - i1 < (int64_t)KW ? n - i1 : (int64_t)KW);
+        if (warp == 0) {
+            // exchange of window wn: lane t < 2kk holds step t >> 1's label
+            // (t even) or negative (t odd) class sum once all CTAs arrived
+            const unsigned long long *slot = k.rec + (size_t)wn * 2 * KW;
+            unsigned long long p = 0;
+            const bool mine = lane < 2 * kk;
+            for (;;) {
+                if (mine) p = ld_relaxed_u64(slot + lane);
+                if (__all_sync(0xffffffffu, !mine || (p >> 40) == (unsigned long long)n_cta)) break;
+            }
+            // decision (feedback.py:33-44) of every step of the window
+            uint64_t th = 0;
+            const long long v40 = (long long)(p & ((1ull << 40) - 1));
+            if (mine) {
+                long long a = (lane & 1) ? k.T - dec_bias + v40 : k.T + dec_bias - v40;
+                a = a < 0 ? 0 : (a > dec_2T ? dec_2T : a);
+                th = dec_tab ? s.thr_tab[a] : threshold_of(a, dec_2T >> 1);
+            }
+            const unsigned busy = __ballot_sync(0xffffffffu, th != 0);
+            const int first = busy ? (__ffs(busy) - 1) >> 1 : kk;
+            if (mine && (lane >> 1) == first) s.thr[lane & 1] = th;
+            if (lane == 0) s.misc[1] = first;
+            if (k.trace && rank == 0 && mine && (lane >> 1) <= first) {
+                const int64_t i = i0 + (lane >> 1);
+                const uint32_t *hd = s.hring + (int)(i % HR) * HSZ;
+                if ((lane & 1) == 0) k.trace[i * 4 + 0] = (long long)hd[2];
+                k.trace[i * 4 + 1 + (lane & 1)] = v40 - dec_bias;
+                if ((lane >> 1) < first) k.trace[i * 4 + 3] = 0;
+            }
+        } else {
+            // speculative evaluation + publication of window wn + 1
+            cp_async_wait_0();
+            named_bar(1, nthr - 32);
+            if (kk1 > 0) {
+                const int sb = (int)(i1 % HR);
+                uint32_t *ob = s.obits + (par ^ 1) * k.cmax;
+                unsigned long long *vw = s.vwin + (par ^ 1) * 2 * KW;
+                for (int j = warp - 1; j < cown; j += nwarps - 1) spec_eval_clause(k, s, j, sb, kk1, ob, vw);
+                named_bar(1, nthr - 32);
+                const int t = tid - 32;
+                if (t < 2 * kk1) {
+                    const long long v = (long long)vw[t];
+                    vw[t] = 0;
+                    red_relaxed_add_u64(k.rec + (size_t)(wn + 1) * 2 * KW + t,
+                                        (1ull << 40) + (unsigned long long)(v + kVoteBias));
+                }
+            }
+            const int64_t want = i0 + HR < n ? i0 + HR : n;
+            if (want > issued) spec_issue(k, s, issued, want, tid - 32, nthr - 32);
+            cp_async_commit();
+        }
+        {
+            const int64_t want = i0 + HR < n ? i0 + HR : n;
+            if (want > issued) issued = want;
+        }
+        __syncthreads();
+        const int first = s.misc[1];
+        if (first >= kk) {  // all-empty window: the next one is already published
+            i0 = i1;
+            wn += 1;
+            continue;
+        }
+        // the window's first non-empty step i: k_train_fast's steps 3-6
+        const int64_t i = i0 + first;
+        const uint32_t *rc = s.hring + (int)(i % HR) * HSZ;
+        const uint32_t *lit = rc + 4;
+        const int label = (int)rc[1], neg = (int)rc[2];
+        const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
+        const uint64_t tt = s.thr[0], tn = s.thr[1];
+        {
+            const uint32_t *ob = s.obits + par * k.cmax;
+            for (int j = tid; j < cown; j += nthr) s.info[j] = ((ob[j] >> first) & 1u) ? I_OUT : 0;
+        }
+        const unsigned tbt = (unsigned)(tt >> 37), tbn = (unsigned)(tn >> 37);
+        int hi_t, hi_n;
+        {
+            const uint16_t *off = reinterpret_cast<const uint16_t *>(rc + 4 + k.Wp);
+            hi_t = tbt >= 65536u ? C : off[(tbt >> 8) + 1];
+            hi_n = tbn >= 65536u ? C : off[260 + (tbn >> 8) + 1];
+        }
+        const bool staged = hi_t <= kSpecEnt && hi_n <= kSpecEnt;
+        const uint32_t *ent = staged ? rc + 4 + k.Wp + 260 : k.recs + i * (int64_t)k.R + rec_entries(k);
+        const int estr = staged ? kSpecEnt : k.Cp;
+        const int ne = hi_t + hi_n;
+        __syncthreads();  // info[] written
+        auto count_entries = [&](int t0, int nt, unsigned &pre, unsigned &tot) {
+            for (int e = t0; e < ne; e += nt) {
+                const int str = e >= hi_t ? 1 : 0;
+                const uint32_t v = ent[str * estr + e - str * hi_t];
+                const unsigned key = v >> 16, c = v & 0xFFFFu;
+                const unsigned tb = str ? tbn : tbt;
+                bool q = key < tb;
+                if (key == tb)
+                    q = draw53(k.fb_seed, fbc + 1 + (str ? (uint64_t)C : 0) + c) < (str ? tn : tt);
+                if (q) {
+                    ++tot;
+                    pre += c < (unsigned)c0 ? 1u : 0u;
+                    if (c >= (unsigned)c0 && c < (unsigned)c1) atomicOr(&s.oflag[c - c0], 1 << str);
+                }
+            }
+        };
+        auto own_events = [&](unsigned pv, unsigned tv) {
+            if (lane == 0) s.misc[0] = 0;
+            __syncwarp();
+            const uint64_t obase = s.blk_ctr[0] + pv;
+            unsigned carry = 0;
+            for (int jb = 0; jb < cown; jb += 32) {
+                const int j = jb + lane;
+                const int f = j < cown ? s.oflag[j] : 0;
+                const unsigned v = (unsigned)(f & 1) + (unsigned)(f >> 1);
+                unsigned x = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (f) {
+                    s.oflag[j] = 0;
+                    spec_events(k, s, cn, j, f & 1, f & 2, obase + carry + (x - v), label, neg);
+                }
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                s.blk_ctr[0] += (uint64_t)tv;
+                if (k.trace && rank == 0) k.trace[i * 4 + 3] = tv;
+            }
+        };
+        if (ne <= 64) {
+            if (warp == 0) {
+                unsigned pre = 0, tot = 0;
+                count_entries(lane, 32, pre, tot);
+                pre = __reduce_add_sync(0xffffffffu, pre);
+                tot = __reduce_add_sync(0xffffffffu, tot);
+                __syncwarp();
+                own_events(pre, tot);
+            }
+        } else {
+            unsigned pre = 0, tot = 0;
+            count_entries(tid, nthr, pre, tot);
+            pre = __reduce_add_sync(0xffffffffu, pre);
+            tot = __reduce_add_sync(0xffffffffu, tot);
+            if (lane == 0) {
+                s.wcnt[warp] = pre;
+                s.wcnt[32 + warp] = tot;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                unsigned pv = lane < nwarps ? s.wcnt[lane] : 0u;
+                unsigned tv = lane < nwarps ? s.wcnt[32 + lane] : 0u;
+                pv = __reduce_add_sync(0xffffffffu, pv);
+                tv = __reduce_add_sync(0xffffffffu, tv);
+                own_events(pv, tv);
+            }
+        }
+        __syncthreads();
+        const int n_work = (k.dbg & 1) ? 0 : s.misc[0];
+        if (n_work > 0) {
+            feedback_quads<SMEM_STATES>(k, s, c0, lit, n_work, cn);
+            __syncthreads();
+        }
+        // next window right after step i, evaluated by every warp
+        i0 = i + 1;
+        wn += 2;
+        if (i0 < n) {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
+            const int kn = (int)(n - i0 < (int64_t)KW ? n - i0 : (int64_t)KW);
+            const int pn = (int)(wn & 1);
+            unsigned long long *vw = s.vwin + pn * 2 * KW;
+            const int sb = (int)(i0 % HR);
+            for (int j = warp; j < cown; j += nwarps)
+                spec_eval_clause(k, s, j, sb, kn, s.obits + pn * k.cmax, vw);
+            __syncthreads();
+            if (tid < 2 * kn) {
+                const long long v = (long long)vw[tid];
+                vw[tid] = 0;
+                red_relaxed_add_u64(k.rec + (size_t)wn * 2 * KW + tid,
+                                    (1ull << 40) + (unsigned long long)(v + kVoteBias));
+            }
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    store_slice<SMEM_STATES>(k, s, c0, cown);
+    if (tid == 0 && rank == n_cta - 1) k.block_counters[0] = s.blk_ctr[0];
+    flush_stats(k, cn, rank == 0);
+}
+
 // --------------------------------------------------------- tiny banks --
 // One warp trains the whole bank (C <= 32 clauses, P <= 1024 positions,
 // K <= 32): lane c owns clause c (output, flag draws, event ordinals, event
@@ -1707,7 +2073,9 @@ void per_cta_maxima(TrainK &k) {
     k.bmax = bmax;
 }
 
-const void *kernel_for(bool cluster, bool smem_states, bool fast, bool prof = false) {
+const void *kernel_for(bool cluster, bool smem_states, bool fast, bool prof = false, bool spec = false) {
+    if (fast && spec)
+        return smem_states ? (const void *)k_train_spec<true> : (const void *)k_train_spec<false>;
     if (cluster)
         return smem_states ? (const void *)k_train<MODE_CLUSTER, true>
                            : (const void *)k_train<MODE_CLUSTER, false>;
@@ -1727,6 +2095,9 @@ constexpr size_t kRecordBufferBytes = size_t(2) << 30;
 namespace tmb {
 int64_t g_train_key_chunk = 0;  // tmb_set_option("train.key_chunk"): test override
 int g_train_dbg = 0;            // tmb_set_option("train.debug_skip"): timing ablations
+// tmb_set_option("train.spec_window"): examples per speculative window of the
+// fast grid trainer (k_train_spec, 1..16), 0 = k_train_fast; read at create
+int g_train_spec = 16;
 }
 
 namespace {
@@ -1781,6 +2152,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     k.Cp = (C + 3) / 4 * 4;
     k.R = 4 + k.Wp + 260 + 2 * k.Cp;
     k.fast = (!cluster && c.n_blocks == 1 && !(c.flags & 2) && C <= 65535) ? 1 : 0;
+    k.spec = k.fast ? std::max(0, std::min(16, g_train_spec)) : 0;
     k.gbal = (!cluster && !(c.flags & 4)) ? 1 : 0;  // used by the generic grid kernel, HBM states
     if (cluster && k.cmax > 32 * 1024)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: too many clauses per CTA");
@@ -1789,6 +2161,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     cudaGetDevice(&dev);
     int max_smem = 0;
     TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (k.spec && smem_layout(k, false, MODE_GRID, nullptr, nullptr) > (size_t)max_smem) k.spec = 0;
     if (k.fast && smem_layout(k, false, MODE_GRID, nullptr, nullptr) > (size_t)max_smem) k.fast = 0;
     const size_t need_on = smem_layout(k, true, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
     const size_t need_off = smem_layout(k, false, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
@@ -1807,7 +2180,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
         return fail(TMB_E_UNSUPPORTED,
                     "trainer_create: per-CTA include masks exceed shared memory (" +
                         std::to_string(need) + " B); use more CTAs");
-    const void *fn = kernel_for(cluster, smem_states, k.fast);
+    const void *fn = kernel_for(cluster, smem_states, k.fast, false, k.spec != 0);
     if (k.fast && 2 * C > 48 * 1024)
         TMB_CUDA(cudaFuncSetAttribute((const void *)k_step_records,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * C));
@@ -1957,7 +2330,9 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         TMB_LAUNCHED();
         return TMB_OK;
     }
-    const void *fn = kernel_for(t->cluster, t->smem_states, k.fast, k.phase != nullptr);
+    if (k.spec && k.phase)
+        return fail(TMB_E_UNSUPPORTED, "trainer_run: phase profiling needs train.spec_window=0");
+    const void *fn = kernel_for(t->cluster, t->smem_states, k.fast, k.phase != nullptr, k.spec != 0);
     // the dynamic shared-memory limit is a per-function attribute: another
     // trainer of a different shape may have lowered it since create
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t->smem));
@@ -1988,6 +2363,10 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         if (g_train_key_chunk > 0) chunk = std::min(chunk, g_train_key_chunk);
     }
     const int64_t slots = std::min(n_steps, chunk);
+    // vote slots: 2 per step, or (spec) 2 * spec per window number (< 2n + 2)
+    auto ring_words = [&](int64_t nn) -> size_t {
+        return k.spec ? (size_t)(2 * nn + 2) * 2 * (size_t)k.spec : 2 * (size_t)nn;
+    };
     if (t->ring_cap < slots || (k.fast && t->rec_cap < slots)) {
         cudaStreamSynchronize(st);
         if (t->ring_d) cudaFree(t->ring_d);
@@ -1995,7 +2374,7 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         if (t->gsync_d) cudaFree(t->gsync_d);
         t->ring_d = nullptr; t->recs_d = nullptr; t->gsync_d = nullptr;
         t->ring_cap = 0; t->rec_cap = 0;
-        TMB_CUDA(cudaMalloc(&t->ring_d, 16 * (size_t)slots));
+        TMB_CUDA(cudaMalloc(&t->ring_d, 8 * ring_words(slots)));
         if (k.gbal) TMB_CUDA(cudaMalloc(&t->gsync_d, 8 * (size_t)slots));
         t->ring_cap = slots;
         if (k.fast) {
@@ -2010,7 +2389,7 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         k.n_steps = n;
         k.fb_counter0 = fb_counter + (uint64_t)off * step_draws;
         k.rec = t->ring_d;
-        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 16 * (size_t)n, st));
+        TMB_CUDA(cudaMemsetAsync(t->ring_d, 0, 8 * ring_words(n), st));
         if (k.gbal) {
             k.gsync = t->gsync_d;
             TMB_CUDA(cudaMemsetAsync(t->gsync_d, 0, 8 * (size_t)n, st));
