@@ -48,6 +48,7 @@ struct TrainK {
     int C, P, K, W, Ppad, n_blocks, n_cta, cmax, fmax_words, bmax;
     int vec4;  // states rows 4-byte addressable in global memory
     int fast, Wp, Cp, R;  // fast path: padded literal words / clauses, record words
+    int MW;         // include-mask row stride in shared memory (W, or Wp for k_train_spec)
     int dbg;        // timing ablations only (tmb_set_option "train.debug_skip")
     int64_t budget, T;
     FbParams fp;
@@ -129,8 +130,9 @@ struct Smem {
     unsigned *wcnt;    // per-warp event counts [32]
     unsigned long long *vacc;  // grid: [2] CTA partial votes (label, negative)
     uint32_t *hring;           // spec: [3 * spec][spec_hsz] staged step heads (ring i % HR)
-    uint32_t *obits;           // spec: [2 parity][cmax] clause outputs of a window (bit q)
-    unsigned long long *vwin;  // spec: [2 parity][spec][2] window partial class sums
+    uint32_t *obs;             // spec: [3 * spec][cmax / 32] clause-output bitset per kept step
+    long long *vst;            // spec: [3 * spec][2] partial class sums per kept step
+    long long *part;           // spec: [warp][lane] per-warp class-sum partials of a window
     int *gpref;                // gbal: [n_cta + 1] prefix of the published work counts
     int *rc_clause, *rc_info;  // gbal: [cmax + 4] work items of this CTA's quad range
     uint64_t *rc_sk;           // gbal: [cmax + 4][2]
@@ -156,7 +158,7 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.vsum = (long long *)take(8 * 2);
     t.lit0 = (uint32_t *)take(4 * k.W);
     t.lit1 = (uint32_t *)take(4 * k.W);
-    t.masks = (uint32_t *)take(4 * (size_t)k.cmax * k.W);
+    t.masks = (uint32_t *)take(4 * (size_t)k.cmax * k.MW);
     t.weights = (int32_t *)take(4 * (size_t)k.cmax * k.K);
     t.work = (int32_t *)take(4 * k.cmax);
     t.info = (int32_t *)take(4 * k.cmax);
@@ -179,8 +181,9 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     const bool sp = k.fast && k.spec;
     t.hring = sp ? (uint32_t *)take(4 * (size_t)(3 * k.spec) * (size_t)(4 + k.Wp + 260 + 2 * 64))
                  : nullptr;
-    t.obits = sp ? (uint32_t *)take(4 * 2 * (size_t)k.cmax) : nullptr;
-    t.vwin = sp ? (unsigned long long *)take(8 * 2 * 2 * (size_t)k.spec) : nullptr;
+    t.obs = sp ? (uint32_t *)take(4 * (size_t)(3 * k.spec) * (size_t)((k.cmax + 31) / 32)) : nullptr;
+    t.vst = sp ? (long long *)take(8 * 2 * (size_t)(3 * k.spec)) : nullptr;
+    t.part = sp ? (long long *)take(8 * 32 * 32) : nullptr;
     t.thr_tab = k.fast && k.thr_smem ? (uint64_t *)take(8 * (size_t)(2 * k.T + 1)) : nullptr;
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
     const bool gb = k.gbal && !k.fast && !smem_states && mode == MODE_GRID;
@@ -331,9 +334,9 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
             if ((lane & 7) == 0) {
                 const int w = p0 >> 5;
                 if (w < k.W) {
-                    const uint32_t old = s.masks[j * k.W + w];
+                    const uint32_t old = s.masks[j * k.MW + w];
                     if (old != m) {
-                        s.masks[j * k.W + w] = m;
+                        s.masks[j * k.MW + w] = m;
                         atomicAdd(&s.cnt[j], __popc(m) - __popc(old));
                     }
                 }
@@ -496,6 +499,9 @@ __device__ __forceinline__ void load_slice(const TrainK &k, const Smem &s, int c
     const int warp = tid >> 5, nwarps = nthr >> 5;
     for (int i = tid; i < cown * k.K; i += nthr) s.weights[i] = k.weights[(int64_t)c0 * k.K + i];
     for (int i = tid; i < cown; i += nthr) s.cnt[i] = 0;
+    if (k.MW > k.W)  // row padding of the masks stays 0 (never an include)
+        for (int i = tid; i < cown * (k.MW - k.W); i += nthr)
+            s.masks[(i / (k.MW - k.W)) * k.MW + k.W + i % (k.MW - k.W)] = 0u;
     if (SMEM_STATES) {
         for (int i = tid; i < cown * k.Ppad; i += nthr) {
             int j = i / k.Ppad, p = i - j * k.Ppad;
@@ -511,7 +517,7 @@ __device__ __forceinline__ void load_slice(const TrainK &k, const Smem &s, int c
         else st = p < k.P ? k.states[(int64_t)(c0 + j) * k.P + p] : -1;
         unsigned m = __ballot_sync(0xffffffffu, st >= 0);
         if (lane == 0) {
-            s.masks[j * k.W + w] = m;
+            s.masks[j * k.MW + w] = m;
             if (m) atomicAdd(&s.cnt[j], __popc(m));
         }
     }
@@ -668,7 +674,7 @@ __device__ __forceinline__ void apply_events(const TrainK &k, const Smem &s, Cou
 __device__ __forceinline__ bool clause_out(const TrainK &k, const Smem &s, int j,
                                            const uint32_t *lit) {
     uint32_t viol = 0;
-    for (int w = (int)(threadIdx.x & 31); w < k.W; w += 32) viol |= s.masks[j * k.W + w] & ~lit[w];
+    for (int w = (int)(threadIdx.x & 31); w < k.W; w += 32) viol |= s.masks[j * k.MW + w] & ~lit[w];
     viol = __reduce_or_sync(0xffffffffu, viol);
     return viol == 0 && s.cnt[j] <= k.budget;
 }
@@ -762,7 +768,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 int cnt = 0;
                 for (int w = lane; w < k.W; w += 32) {
                     const uint32_t m = __ldcg(src + w);
-                    s.masks[j * k.W + w] = m;
+                    s.masks[j * k.MW + w] = m;
                     cnt += __popc(m);
                 }
                 cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -775,7 +781,7 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
         //    (dense.py:153 restricted to label / negative) into the same pass
         for (int j = warp; j < ((k.dbg & 2) ? 0 : cown); j += nwarps) {
             uint32_t viol = 0;
-            for (int w = lane; w < k.W; w += 32) viol |= s.masks[j * k.W + w] & ~lit[w];
+            for (int w = lane; w < k.W; w += 32) viol |= s.masks[j * k.MW + w] & ~lit[w];
             viol = __reduce_or_sync(0xffffffffu, viol);
             if (lane == 0) {
                 const bool out = viol == 0 && s.cnt[j] <= k.budget;
@@ -1527,33 +1533,52 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_fast(TrainK k) {
 // max(exchange, evaluation) per window instead of one exchange per step.
 // A window whose speculation failed is simply abandoned: window numbers are
 // never reused (each has its own slots in k.rec), so stale partial sums can
-// never be mistaken for current ones.  The result is bit-identical to the
-// sequential loop (executor.py:275-340): every applied step sees exactly
-// the states the steps before it produced.
+// never be mistaken for current ones.
+//
+// Every evaluated step keeps, per CTA, its clause-output bitset and its two
+// partial class sums (obs / vst, ring slot i % HR).  After a non-empty step
+// only the clauses on the work list changed (states, masks, weights), so
+// the next window -- which lies inside the two windows already evaluated --
+// is published from the kept sums corrected by the work-list clauses alone.
+// The result is bit-identical to the sequential loop (executor.py:275-340):
+// every applied step sees exactly the states the steps before it produced.
 constexpr int kSpecEnt = 64;  // flag entries per stream staged with each head
 __host__ __device__ inline int spec_hsz(const TrainK &k) { return 4 + k.Wp + 260 + 2 * kSpecEnt; }
 
-// Stage the heads of steps [from, to) -- example, label, negative class,
-// literal row, bucket starts and the first kSpecEnt flag entries of each
-// stream -- into ring slots i % (3 * spec), 16-B cp.async units spread over
-// threads t0, t0 + nt, ...
-__device__ __forceinline__ void spec_issue(const TrainK &k, const Smem &s, int64_t from, int64_t to,
-                                           int t0, int nt) {
+__device__ __forceinline__ int spec_wrap(int x, int HR) { return x >= HR ? x - HR : x; }
+
+// Stage the heads of cnt <= HR steps from step `from` (ring slot fslot) --
+// example, label, negative class, literal row, bucket starts and the first
+// kSpecEnt flag entries of each stream -- one warp per step (warps wrel,
+// wrel + nw, ...), 16-B cp.async units over the lanes.  k.dbg & 64 also
+// prefetches the step's remaining flag entries into L2 (this CTA takes the
+// 128-B lines l = rank - i mod n_cta).
+__device__ __forceinline__ void spec_issue(const TrainK &k, const Smem &s, int64_t from, int fslot,
+                                           int cnt, int wrel, int nw) {
+    const int lane = threadIdx.x & 31;
     const int nh = (4 + k.Wp + 260) / 4;
     const int ne = min(kSpecEnt, k.Cp) / 4;
     const int per = nh + 2 * ne;
     const int HR = 3 * k.spec, HSZ = spec_hsz(k);
-    const int total = (int)(to - from) * per;
-    for (int u = t0; u < total; u += nt) {
-        const int st = u / per, q = u - st * per;
+    for (int st = wrel; st < cnt; st += nw) {
         const int64_t i = from + st;
         const uint32_t *src = k.recs + i * (int64_t)k.R;
-        uint32_t *dst = s.hring + (int)(i % HR) * HSZ;
-        if (q < nh) {
-            cp_async16(dst + 4 * q, src + 4 * q);
-        } else {
-            const int r = q - nh, str = r >= ne ? 1 : 0, e = r - str * ne;
-            cp_async16(dst + 4 * nh + str * kSpecEnt + 4 * e, src + rec_entries(k) + str * k.Cp + 4 * e);
+        uint32_t *dst = s.hring + spec_wrap(fslot + st, HR) * HSZ;
+        for (int q = lane; q < per; q += 32) {
+            if (q < nh) {
+                cp_async16(dst + 4 * q, src + 4 * q);
+            } else {
+                const int r = q - nh, str = r >= ne ? 1 : 0, e = r - str * ne;
+                cp_async16(dst + 4 * nh + str * kSpecEnt + 4 * e, src + rec_entries(k) + str * k.Cp + 4 * e);
+            }
+        }
+        if ((k.dbg & 64) && lane == 0) {
+            const int lines = (2 * k.Cp * 4 + 127) / 128;
+            const int n_cta = k.n_cta;
+            for (int l = ((int)blockIdx.x - (int)(i % n_cta) + n_cta) % n_cta; l < lines; l += n_cta) {
+                const char *p = reinterpret_cast<const char *>(src + rec_entries(k)) + 128 * l;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+            }
         }
     }
 }
@@ -1563,37 +1588,117 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Outputs of own clause j (warp-collective) for the kk <= 16 examples of the
-// window whose first head sits in ring slot sb: lane q + 16h tests example q
-// on words h, h + 2, ...; bit q of ob[j]; the example's label / negative
-// class-sum contributions are added into vw[q][2].
-__device__ __forceinline__ void spec_eval_clause(const TrainK &k, const Smem &s, int j, int sb, int kk,
-                                                 uint32_t *ob, unsigned long long *vw) {
-    const int lane = threadIdx.x & 31, q = lane & 15, h = lane >> 4;
-    const int HR = 3 * k.spec, HSZ = spec_hsz(k);
-    const bool act = q < kk;
-    int slot = sb + (act ? q : 0);
-    if (slot >= HR) slot -= HR;
+// Fresh evaluation of a window: warp w (= wrel, wrel + nw, ...) takes own
+// clauses 2w', 2w' + 1 against the kk <= 16 examples whose heads sit in ring
+// slots sb, sb + 1, ...; lane c2 * 16 + q on (clause 2w' + c2, example q)
+// ORs mask & ~literal over the row in 16-B shared loads (rows padded to Wp
+// words; the mask is a 2-address broadcast).  A firing (clause, example)
+// sets its bit in the example's output bitset obs[slot] (zeroed before);
+// the lanes' label / negative weights are summed over the pair into
+// part[warp][lane] (lane q: label sum of example q, lane 16 + q: negative).
+__device__ __forceinline__ void spec_eval(const TrainK &k, const Smem &s, int wrel, int nw, int cown,
+                                          int sb, int kk) {
+    const int lane = threadIdx.x & 31, q = lane & 15, c2 = lane >> 4;
+    const int HR = 3 * k.spec, HSZ = spec_hsz(k), MW = k.MW, CW = (k.cmax + 31) >> 5;
+    const int slot = spec_wrap(sb + (q < kk ? q : 0), HR);
     const uint32_t *hd = s.hring + slot * HSZ;
-    const uint32_t *lit = hd + 4;
-    const uint32_t *m = s.masks + j * k.W;
-    uint32_t viol = 0;
+    const uint4 *lit = reinterpret_cast<const uint4 *>(hd + 4);
+    const int label = (int)hd[1], neg = (int)hd[2];
+    const int n4 = MW >> 2;
+    uint32_t *ob = s.obs + slot * CW;
+    long long a = 0, b = 0;
+    for (int jp = 2 * wrel; jp < cown; jp += 2 * nw) {
+        const int j = jp + c2;
+        const bool real = j < cown;
+        const int jj = real ? j : jp;
+        const uint4 *m = reinterpret_cast<const uint4 *>(s.masks + jj * MW);
+        uint32_t v = 0;
 #pragma unroll 4
-    for (int w = h; w < k.W; w += 2) viol |= m[w] & ~lit[w];
-    viol |= __shfl_xor_sync(0xffffffffu, viol, 16);
-    const bool o = act && viol == 0 && s.cnt[j] <= k.budget;
-    const unsigned bits = __ballot_sync(0xffffffffu, o) & 0xFFFFu;
-    if (lane == 0) ob[j] = bits;
-    if (h == 0 && o) {
-        const int32_t *w = s.weights + j * k.K;
-        const long long a = w[hd[1]], b = w[hd[2]];
-        if (a) atomicAdd(&vw[q * 2 + 0], (unsigned long long)a);
-        if (b) atomicAdd(&vw[q * 2 + 1], (unsigned long long)b);
+        for (int u = 0; u < n4; ++u) {
+            const uint4 mm = m[u], ll = lit[u];
+            v |= (mm.x & ~ll.x) | (mm.y & ~ll.y) | (mm.z & ~ll.z) | (mm.w & ~ll.w);
+        }
+        if (real && q < kk && v == 0 && s.cnt[jj] <= k.budget) {
+            atomicOr(&ob[j >> 5], 1u << (j & 31));
+            a += s.weights[j * k.K + label];
+            b += s.weights[j * k.K + neg];
+        }
     }
+    a += __shfl_xor_sync(0xffffffffu, a, 16);
+    b += __shfl_xor_sync(0xffffffffu, b, 16);
+    s.part[(threadIdx.x >> 5) * 32 + lane] = c2 ? b : a;
+}
+
+// After a non-empty step (label li, negative ni): the kk examples from ring
+// slot sb were evaluated before it; only work-list clauses changed.  Warp w
+// takes work items 2w', 2w' + 1: each (clause, example) lane re-tests the
+// clause, flips its bit in obs[slot] if the output changed, and adds
+// new - old contribution (old weights = new minus the step's +1 / -1 on li /
+// ni when the clause fired on it, kernels/_numba.py:117-122) into part.
+__device__ __forceinline__ void spec_correct(const TrainK &k, const Smem &s, int wrel, int nw,
+                                             int n_work, int sb, int kk, int li, int ni) {
+    const int lane = threadIdx.x & 31, q = lane & 15, c2 = lane >> 4;
+    const int HR = 3 * k.spec, HSZ = spec_hsz(k), MW = k.MW, CW = (k.cmax + 31) >> 5;
+    const int slot = spec_wrap(sb + (q < kk ? q : 0), HR);
+    const uint32_t *hd = s.hring + slot * HSZ;
+    const uint4 *lit = reinterpret_cast<const uint4 *>(hd + 4);
+    const int label = (int)hd[1], neg = (int)hd[2];
+    const int n4 = MW >> 2;
+    uint32_t *ob = s.obs + slot * CW;
+    long long a = 0, b = 0;
+    for (int wp = 2 * wrel; wp < n_work; wp += 2 * nw) {
+        const int idx = wp + c2;
+        const bool real = idx < n_work;
+        const int j = s.work[real ? idx : wp];
+        const uint4 *m = reinterpret_cast<const uint4 *>(s.masks + j * MW);
+        uint32_t v = 0;
+#pragma unroll 4
+        for (int u = 0; u < n4; ++u) {
+            const uint4 mm = m[u], ll = lit[u];
+            v |= (mm.x & ~ll.x) | (mm.y & ~ll.y) | (mm.z & ~ll.z) | (mm.w & ~ll.w);
+        }
+        if (real && q < kk) {
+            const bool on = v == 0 && s.cnt[j] <= k.budget;
+            const bool oo = (ob[j >> 5] >> (j & 31)) & 1u;
+            const int info = s.info[j];
+            const int fired = (info & I_OUT) ? 1 : 0;
+            const int dt = (info & I_TEV) ? fired : 0, dn = (info & I_NEV) ? fired : 0;
+            const int32_t *w = s.weights + j * k.K;
+            const long long wl = w[label], wg = w[neg];
+            const long long wl0 = wl - (label == li ? dt : 0) + (label == ni ? dn : 0);
+            const long long wg0 = wg - (neg == li ? dt : 0) + (neg == ni ? dn : 0);
+            a += (on ? wl : 0) - (oo ? wl0 : 0);
+            b += (on ? wg : 0) - (oo ? wg0 : 0);
+            if (on != oo) atomicXor(&ob[j >> 5], 1u << (j & 31));
+        }
+    }
+    a += __shfl_xor_sync(0xffffffffu, a, 16);
+    b += __shfl_xor_sync(0xffffffffu, b, 16);
+    s.part[(threadIdx.x >> 5) * 32 + lane] = c2 ? b : a;
+}
+
+// Vote slot t of window wn.  Slots are interleaved across windows (slot t
+// of every window, then slot t + 1, ...) so the 2 * spec words of one window
+// sit in distinct 128-B lines (the L2 serialises atomics per line).
+__device__ __forceinline__ size_t spec_slot(const TrainK &k, int64_t wn, int t) {
+    return (size_t)t * (size_t)(2 * k.n_steps + 2) + (size_t)wn;
+}
+
+// Thread t < 2kk publishes step t >> 1's label (t even) / negative (t odd)
+// partial class sum of window wn: the kept sum (add_kept) plus the partials
+// of warps w0 .. w0 + nw - 1; the result is kept for later corrections.
+__device__ __forceinline__ void spec_push(const TrainK &k, const Smem &s, int t, int w0, int nw,
+                                          int sb, bool add_kept, int64_t wn) {
+    long long v = 0;
+    for (int w = w0; w < w0 + nw; ++w) v += s.part[w * 32 + (t >> 1) + 16 * (t & 1)];
+    long long *kept = s.vst + spec_wrap(sb + (t >> 1), 3 * k.spec) * 2 + (t & 1);
+    if (add_kept) v += *kept;
+    *kept = v;
+    red_relaxed_add_u64(k.rec + spec_slot(k, wn, t), (1ull << 40) + (unsigned long long)(v + kVoteBias));
 }
 
 // Event bookkeeping of own clause j for the applied step (fast_events
-// without the next-example correction: the next window is evaluated anew).
+// without the next-example correction).
 __device__ __forceinline__ void spec_events(const TrainK &k, const Smem &s, Counters &cn, int j,
                                             bool t_ev, bool n_ev, uint64_t ord, int label, int neg) {
     int info = s.info[j] & I_OUT;
@@ -1623,7 +1728,29 @@ __device__ __forceinline__ void spec_events(const TrainK &k, const Smem &s, Coun
         s.work[atomicAdd(&s.misc[0], 1)] = j;
 }
 
-template <bool SMEM_STATES>
+__device__ __forceinline__ int mine_lane(int lane, int kk) { return lane < 2 * kk ? lane : 0; }
+
+// PROF timeline: %globaltimer of this CTA's publication (thread 32) and poll
+// completion (thread 0) of windows [kSpecTl0, kSpecTl0 + kSpecTlN), stored
+// after the counters as [n_cta][kSpecTlN][2].
+// Per polled window wn: [0] %globaltimer when the next window was published
+// after wn's non-empty step, [1] %globaltimer at wn's poll completion, then
+// clock64 at [2] poll completion, [3] events done, [4] feedback done, [5]
+// publication; stored after the counters as [n_cta][kSpecTlN][kSpecTlQ].
+constexpr int kSpecTl0 = 2000, kSpecTlN = 2048, kSpecTlQ = 6;
+#define SPEC_TL(wn_, q_, v_)                                                                          \
+    do {                                                                                              \
+        if (PROF && (wn_) >= kSpecTl0 && (wn_) < kSpecTl0 + kSpecTlN)                                  \
+            k.phase[n_cta * 16 + ((size_t)rank * kSpecTlN + ((wn_) - kSpecTl0)) * kSpecTlQ + (q_)] = \
+                (unsigned long long)(v_);                                                             \
+    } while (0)
+
+// PROF: k.phase[rank * 16 + q] accumulates (thread 0, clock64) 0 poll, 1
+// decision + barrier, 2 event preparation, 15 entries + own events, 3
+// feedback, 13 next-window wait, 14 correction, 4 publication; counts 8
+// windows, 9 non-empty steps, 10 steps with > 64 flag entries, 11 steps
+// whose entries were staged, 12 whole loop
+template <bool SMEM_STATES, bool PROF>
 __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
     extern __shared__ __align__(16) char smem_raw[];
     Smem s;
@@ -1635,7 +1762,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
     const int c0 = cta_begin(rank, C, n_cta), c1 = cta_begin(rank + 1, C, n_cta);
     const int cown = c1 - c0;
     const int64_t n = k.n_steps;
-    const int KW = k.spec, HR = 3 * KW, HSZ = spec_hsz(k);
+    const int KW = k.spec, HR = 3 * KW, HSZ = spec_hsz(k), CW = (k.cmax + 31) >> 5;
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
 
     load_slice<SMEM_STATES>(k, s, c0, cown);
@@ -1647,44 +1774,59 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
         s.misc[0] = 0;
     }
     for (int j = tid; j < cown; j += nthr) s.oflag[j] = 0;
-    for (int q = tid; q < 4 * KW; q += nthr) s.vwin[q] = 0;
-    int64_t issued = n < (int64_t)HR ? n : (int64_t)HR;
-    spec_issue(k, s, 0, issued, tid, nthr);
+    for (int q = tid; q < HR * CW; q += nthr) s.obs[q] = 0;
+    int64_t issued = n < (int64_t)HR ? n : (int64_t)HR;  // heads staged or in flight: [0, issued)
+    int islot = spec_wrap((int)issued, HR);              // issued % HR
+    spec_issue(k, s, 0, 0, (int)issued, warp, nwarps);
     cp_async_commit();
     cp_async_wait_0();
     __syncthreads();
 
-    // window 0: every warp evaluates, then publish
+    // window 0: every warp evaluates, then warp 1 publishes
     int64_t i0 = 0, wn = 0;
+    int s0 = 0;  // i0 % HR
     {
         const int kk = (int)(n < (int64_t)KW ? n : (int64_t)KW);
-        for (int j = warp; j < cown; j += nwarps) spec_eval_clause(k, s, j, 0, kk, s.obits, s.vwin);
+        spec_eval(k, s, warp, nwarps, cown, 0, kk);
         __syncthreads();
-        if (tid < 2 * kk) {
-            const long long v = (long long)s.vwin[tid];
-            s.vwin[tid] = 0;
-            red_relaxed_add_u64(&k.rec[tid], (1ull << 40) + (unsigned long long)(v + kVoteBias));
-        }
+        if (tid >= 32 && tid - 32 < 2 * kk) spec_push(k, s, tid - 32, 0, nwarps, 0, false, 0);
     }
 
     Counters cn;
+    unsigned long long ph[16] = {0};
+    long long t_mark = clock64();
+    const long long t_loop0 = t_mark;
+#define SPH(q)                                                   \
+    do {                                                         \
+        if (PROF && tid == 0) {                                  \
+            const long long now_ = clock64();                    \
+            ph[q] += (unsigned long long)(now_ - t_mark);        \
+            t_mark = now_;                                       \
+        }                                                        \
+    } while (0)
     const long long dec_bias = (long long)n_cta * kVoteBias;
     const long long dec_2T = 2 * k.T;
     const bool dec_tab = k.thr_smem != 0;
     while (i0 < n) {
         const int kk = (int)(n - i0 < (int64_t)KW ? n - i0 : (int64_t)KW);
-        const int par = (int)(wn & 1);
         const int64_t i1 = i0 + kk;
+        const int s1 = spec_wrap(s0 + kk, HR);
         const int kk1 = (int)(n - i1 < (int64_t)KW ? n - i1 : (int64_t)KW);
+        const int64_t want = i0 + HR < n ? i0 + HR : n;
         if (warp == 0) {
             // exchange of window wn: lane t < 2kk holds step t >> 1's label
             // (t even) or negative (t odd) class sum once all CTAs arrived
-            const unsigned long long *slot = k.rec + (size_t)wn * 2 * KW;
+            const unsigned long long *slot = k.rec + spec_slot(k, wn, mine_lane(lane, kk));
             unsigned long long p = 0;
             const bool mine = lane < 2 * kk;
             for (;;) {
-                if (mine) p = ld_relaxed_u64(slot + lane);
+                if (mine) p = ld_relaxed_u64(slot);
                 if (__all_sync(0xffffffffu, !mine || (p >> 40) == (unsigned long long)n_cta)) break;
+            }
+            SPH(0);
+            if (lane == 0) {
+                SPEC_TL(wn, 1, gtimer());
+                SPEC_TL(wn, 2, clock64());
             }
             // decision (feedback.py:33-44) of every step of the window
             uint64_t th = 0;
@@ -1700,7 +1842,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
             if (lane == 0) s.misc[1] = first;
             if (k.trace && rank == 0 && mine && (lane >> 1) <= first) {
                 const int64_t i = i0 + (lane >> 1);
-                const uint32_t *hd = s.hring + (int)(i % HR) * HSZ;
+                const uint32_t *hd = s.hring + spec_wrap(s0 + (lane >> 1), HR) * HSZ;
                 if ((lane & 1) == 0) k.trace[i * 4 + 0] = (long long)hd[2];
                 k.trace[i * 4 + 1 + (lane & 1)] = v40 - dec_bias;
                 if ((lane >> 1) < first) k.trace[i * 4 + 3] = 0;
@@ -1708,46 +1850,45 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
         } else {
             // speculative evaluation + publication of window wn + 1
             cp_async_wait_0();
+            for (int q = tid - 32; q < kk1 * CW; q += nthr - 32) {
+                const int st = q / CW;
+                s.obs[spec_wrap(s1 + st, HR) * CW + (q - st * CW)] = 0;
+            }
             named_bar(1, nthr - 32);
             if (kk1 > 0) {
-                const int sb = (int)(i1 % HR);
-                uint32_t *ob = s.obits + (par ^ 1) * k.cmax;
-                unsigned long long *vw = s.vwin + (par ^ 1) * 2 * KW;
-                for (int j = warp - 1; j < cown; j += nwarps - 1) spec_eval_clause(k, s, j, sb, kk1, ob, vw);
+                spec_eval(k, s, warp - 1, nwarps - 1, cown, s1, kk1);
                 named_bar(1, nthr - 32);
-                const int t = tid - 32;
-                if (t < 2 * kk1) {
-                    const long long v = (long long)vw[t];
-                    vw[t] = 0;
-                    red_relaxed_add_u64(k.rec + (size_t)(wn + 1) * 2 * KW + t,
-                                        (1ull << 40) + (unsigned long long)(v + kVoteBias));
-                }
+                if (tid - 32 < 2 * kk1) spec_push(k, s, tid - 32, 1, nwarps - 1, s1, false, wn + 1);
             }
-            const int64_t want = i0 + HR < n ? i0 + HR : n;
-            if (want > issued) spec_issue(k, s, issued, want, tid - 32, nthr - 32);
+            if (want > issued) spec_issue(k, s, issued, islot, (int)(want - issued), warp - 1, nwarps - 1);
             cp_async_commit();
         }
-        {
-            const int64_t want = i0 + HR < n ? i0 + HR : n;
-            if (want > issued) issued = want;
+        if (want > issued) {
+            islot = spec_wrap(islot + (int)(want - issued), HR);
+            issued = want;
         }
         __syncthreads();
+        SPH(1);
+        if (PROF && tid == 0) ph[8] += 1;
         const int first = s.misc[1];
         if (first >= kk) {  // all-empty window: the next one is already published
             i0 = i1;
+            s0 = s1;
             wn += 1;
             continue;
         }
+        if (PROF && tid == 0) ph[9] += 1;
         // the window's first non-empty step i: k_train_fast's steps 3-6
         const int64_t i = i0 + first;
-        const uint32_t *rc = s.hring + (int)(i % HR) * HSZ;
+        const int si = spec_wrap(s0 + first, HR);
+        const uint32_t *rc = s.hring + si * HSZ;
         const uint32_t *lit = rc + 4;
         const int label = (int)rc[1], neg = (int)rc[2];
         const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
         const uint64_t tt = s.thr[0], tn = s.thr[1];
         {
-            const uint32_t *ob = s.obits + par * k.cmax;
-            for (int j = tid; j < cown; j += nthr) s.info[j] = ((ob[j] >> first) & 1u) ? I_OUT : 0;
+            const uint32_t *ob = s.obs + si * CW;
+            for (int j = tid; j < cown; j += nthr) s.info[j] = ((ob[j >> 5] >> (j & 31)) & 1u) ? I_OUT : 0;
         }
         const unsigned tbt = (unsigned)(tt >> 37), tbn = (unsigned)(tn >> 37);
         int hi_t, hi_n;
@@ -1757,10 +1898,15 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
             hi_n = tbn >= 65536u ? C : off[260 + (tbn >> 8) + 1];
         }
         const bool staged = hi_t <= kSpecEnt && hi_n <= kSpecEnt;
+        if (PROF && tid == 0) {
+            ph[10] += (hi_t + hi_n > 64) ? 1 : 0;
+            ph[11] += staged ? 1 : 0;
+        }
         const uint32_t *ent = staged ? rc + 4 + k.Wp + 260 : k.recs + i * (int64_t)k.R + rec_entries(k);
         const int estr = staged ? kSpecEnt : k.Cp;
         const int ne = hi_t + hi_n;
         __syncthreads();  // info[] written
+        SPH(2);
         auto count_entries = [&](int t0, int nt, unsigned &pre, unsigned &tot) {
             for (int e = t0; e < ne; e += nt) {
                 const int str = e >= hi_t ? 1 : 0;
@@ -1804,59 +1950,68 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
                 if (k.trace && rank == 0) k.trace[i * 4 + 3] = tv;
             }
         };
-        if (ne <= 64) {
+        {
+            // few entries: warp 0 alone; else all warps count, warp 0 assigns
+            const bool few = ne <= 64;
+            unsigned pre = 0, tot = 0;
+            if (!few || warp == 0) count_entries(few ? lane : tid, few ? 32 : nthr, pre, tot);
+            pre = __reduce_add_sync(0xffffffffu, pre);
+            tot = __reduce_add_sync(0xffffffffu, tot);
+            if (!few) {
+                if (lane == 0) {
+                    s.wcnt[warp] = pre;
+                    s.wcnt[32 + warp] = tot;
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    pre = __reduce_add_sync(0xffffffffu, lane < nwarps ? s.wcnt[lane] : 0u);
+                    tot = __reduce_add_sync(0xffffffffu, lane < nwarps ? s.wcnt[32 + lane] : 0u);
+                }
+            }
             if (warp == 0) {
-                unsigned pre = 0, tot = 0;
-                count_entries(lane, 32, pre, tot);
-                pre = __reduce_add_sync(0xffffffffu, pre);
-                tot = __reduce_add_sync(0xffffffffu, tot);
                 __syncwarp();
                 own_events(pre, tot);
             }
-        } else {
-            unsigned pre = 0, tot = 0;
-            count_entries(tid, nthr, pre, tot);
-            pre = __reduce_add_sync(0xffffffffu, pre);
-            tot = __reduce_add_sync(0xffffffffu, tot);
-            if (lane == 0) {
-                s.wcnt[warp] = pre;
-                s.wcnt[32 + warp] = tot;
-            }
-            __syncthreads();
-            if (warp == 0) {
-                unsigned pv = lane < nwarps ? s.wcnt[lane] : 0u;
-                unsigned tv = lane < nwarps ? s.wcnt[32 + lane] : 0u;
-                pv = __reduce_add_sync(0xffffffffu, pv);
-                tv = __reduce_add_sync(0xffffffffu, tv);
-                own_events(pv, tv);
-            }
         }
         __syncthreads();
+        SPH(15);
+        if (tid == 0) SPEC_TL(wn, 3, clock64());
         const int n_work = (k.dbg & 1) ? 0 : s.misc[0];
         if (n_work > 0) {
             feedback_quads<SMEM_STATES>(k, s, c0, lit, n_work, cn);
             __syncthreads();
         }
-        // next window right after step i, evaluated by every warp
+        SPH(3);
+        if (tid == 0) SPEC_TL(wn, 4, clock64());
+        // next window right after step i: the kept sums of its steps,
+        // corrected by the work-list clauses
         i0 = i + 1;
+        s0 = spec_wrap(si + 1, HR);
         wn += 2;
         if (i0 < n) {
             asm volatile("cp.async.wait_group 1;" ::: "memory");
-            __syncthreads();
+            SPH(13);
             const int kn = (int)(n - i0 < (int64_t)KW ? n - i0 : (int64_t)KW);
-            const int pn = (int)(wn & 1);
-            unsigned long long *vw = s.vwin + pn * 2 * KW;
-            const int sb = (int)(i0 % HR);
-            for (int j = warp; j < cown; j += nwarps)
-                spec_eval_clause(k, s, j, sb, kn, s.obits + pn * k.cmax, vw);
+            if (n_work > 0) {
+                spec_correct(k, s, warp, nwarps, n_work, s0, kn, label, neg);
+            } else if (tid < 64) {
+                s.part[tid] = 0;  // warps 0-1: nothing to correct
+            }
             __syncthreads();
-            if (tid < 2 * kn) {
-                const long long v = (long long)vw[tid];
-                vw[tid] = 0;
-                red_relaxed_add_u64(k.rec + (size_t)wn * 2 * KW + tid,
-                                    (1ull << 40) + (unsigned long long)(v + kVoteBias));
+            SPH(14);
+            const int used = n_work > 0 ? nwarps : 2;  // warps whose partials count
+            if (tid >= 32 && tid - 32 < 2 * kn) spec_push(k, s, tid - 32, 0, used, s0, true, wn);
+            if (tid == 32) {
+                SPEC_TL(wn - 2, 0, gtimer());
+                SPEC_TL(wn - 2, 5, clock64());
             }
         }
+        SPH(4);
+    }
+#undef SPH
+    if (PROF && tid == 0) {
+        ph[12] = (unsigned long long)(clock64() - t_loop0);
+        for (int q = 0; q < 16; ++q) k.phase[rank * 16 + q] = ph[q];
     }
     cp_async_wait_all();
     __syncthreads();
@@ -2075,7 +2230,10 @@ void per_cta_maxima(TrainK &k) {
 
 const void *kernel_for(bool cluster, bool smem_states, bool fast, bool prof = false, bool spec = false) {
     if (fast && spec)
-        return smem_states ? (const void *)k_train_spec<true> : (const void *)k_train_spec<false>;
+        return prof ? (smem_states ? (const void *)k_train_spec<true, true>
+                                   : (const void *)k_train_spec<false, true>)
+                    : (smem_states ? (const void *)k_train_spec<true, false>
+                                   : (const void *)k_train_spec<false, false>);
     if (cluster)
         return smem_states ? (const void *)k_train<MODE_CLUSTER, true>
                            : (const void *)k_train<MODE_CLUSTER, false>;
@@ -2152,7 +2310,9 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     k.Cp = (C + 3) / 4 * 4;
     k.R = 4 + k.Wp + 260 + 2 * k.Cp;
     k.fast = (!cluster && c.n_blocks == 1 && !(c.flags & 2) && C <= 65535) ? 1 : 0;
-    k.spec = k.fast ? std::max(0, std::min(16, g_train_spec)) : 0;
+    // (window evaluation holds two literal words per lane: rows of <= 64 words)
+    k.spec = (k.fast && W <= 64) ? std::max(0, std::min(16, g_train_spec)) : 0;
+    k.MW = k.spec ? k.Wp : W;
     k.gbal = (!cluster && !(c.flags & 4)) ? 1 : 0;  // used by the generic grid kernel, HBM states
     if (cluster && k.cmax > 32 * 1024)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: too many clauses per CTA");
@@ -2161,7 +2321,10 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     cudaGetDevice(&dev);
     int max_smem = 0;
     TMB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    if (k.spec && smem_layout(k, false, MODE_GRID, nullptr, nullptr) > (size_t)max_smem) k.spec = 0;
+    if (k.spec && smem_layout(k, false, MODE_GRID, nullptr, nullptr) > (size_t)max_smem) {
+        k.spec = 0;
+        k.MW = W;
+    }
     if (k.fast && smem_layout(k, false, MODE_GRID, nullptr, nullptr) > (size_t)max_smem) k.fast = 0;
     const size_t need_on = smem_layout(k, true, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
     const size_t need_off = smem_layout(k, false, cluster ? MODE_CLUSTER : MODE_GRID, nullptr, nullptr);
@@ -2330,8 +2493,6 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         TMB_LAUNCHED();
         return TMB_OK;
     }
-    if (k.spec && k.phase)
-        return fail(TMB_E_UNSUPPORTED, "trainer_run: phase profiling needs train.spec_window=0");
     const void *fn = kernel_for(t->cluster, t->smem_states, k.fast, k.phase != nullptr, k.spec != 0);
     // the dynamic shared-memory limit is a per-function attribute: another
     // trainer of a different shape may have lowered it since create

@@ -22,6 +22,9 @@ def main():
     ap.add_argument("--windows", type=int, nargs="+", default=[0, 16])
     ap.add_argument("--epochs", type=int, default=3)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--dbg", type=int, default=0, help="train.debug_skip bits (timing ablations)")
+    ap.add_argument("--prof", action="store_true",
+                    help="k_train_spec phase counters (clock64 per CTA, see tmb_train.cu)")
     args = ap.parse_args()
     import torch
 
@@ -33,6 +36,7 @@ def main():
     g = np.load(os.path.join(REPO, "tests", "golden", "c2_epoch3.npz"))
     ref = None
     out = []
+    _lib.call("tmb_set_option", b"train.debug_skip", args.dbg)
     for wsz in args.windows:
         _lib.call("tmb_set_option", b"train.spec_window", wsz)
         sess = tmb.DenseTrainSession(cfg, tx, ty, threads=args.threads,
@@ -41,9 +45,20 @@ def main():
         sess.fb_counter = int(g["fb_counter"])
         sess.shuffle_rng.counter = int(g["shuffle_counter"])
         ms = []
+        prof = None
+        if args.prof and wsz > 0:
+            ncta = sess.launch["n_cta"]
+            prof = torch.zeros(ncta * 16 + ncta * 2048 * 6, dtype=torch.int64, device="cuda")
+            _lib.call("tmb_trainer_set_profile", sess._h, prof.data_ptr())
+
+        def reset():
+            if prof is not None:
+                prof.zero_()
+        phases = []
         for _ in range(args.epochs):
             order = sess.next_order().astype(np.int32)
             od = torch.from_numpy(order).cuda()
+            reset()
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
@@ -52,6 +67,44 @@ def main():
             b.record()
             torch.cuda.synchronize()
             ms.append(a.elapsed_time(b))
+            if prof is not None:
+                allp = prof.cpu().numpy()
+                p = allp[:ncta * 16].reshape(-1, 16).astype(np.float64)
+                tl = allp[ncta * 16:].reshape(ncta, 2048, 6).astype(np.float64)
+                heavy = (tl[:, :, 0] > 0).all(axis=0) & (tl[:, :, 1] > 0).all(axis=0)
+                polled = (tl[:, :, 1] > 0).all(axis=0)
+                h = tl[:, heavy, :]
+                cyc = 1.9  # cycles per ns (approx.)
+                ev = (h[:, :, 3] - h[:, :, 2]) / cyc
+                fb = (h[:, :, 4] - h[:, :, 3]) / cyc
+                pb = (h[:, :, 5] - h[:, :, 4]) / cyc
+                chain = (h[:, :, 5] - h[:, :, 2]) / cyc
+                # latency: next polled window's earliest completion - latest publication
+                idx = np.nonzero(heavy)[0]
+                lat = []
+                for w in idx:
+                    nxt = w + 2
+                    if nxt < 2048 and polled[nxt]:
+                        lat.append(tl[:, nxt, 1].min() - tl[:, w, 0].max())
+                med = lambda a: float(np.median(a))
+                timeline = dict(
+                    heavy_windows=int(heavy.sum()),
+                    chain_ns=dict(median_cta=med(np.median(chain, axis=0)), max_cta=med(chain.max(axis=0))),
+                    events_ns=dict(median_cta=med(np.median(ev, axis=0)), max_cta=med(ev.max(axis=0))),
+                    feedback_ns=dict(median_cta=med(np.median(fb, axis=0)), max_cta=med(fb.max(axis=0))),
+                    correct_push_ns=dict(median_cta=med(np.median(pb, axis=0)), max_cta=med(pb.max(axis=0))),
+                    done_spread_ns=med(h[:, :, 1].max(axis=0) - h[:, :, 1].min(axis=0)),
+                    pub_skew_ns=med(h[:, :, 0].max(axis=0) - np.median(h[:, :, 0], axis=0)),
+                    next_latency_ns=np.percentile(lat, [10, 50, 90]).round().tolist() if lat else None)
+                names = {0: "poll", 1: "decide", 2: "ev_prep", 15: "ev_count_own", 3: "feedback",
+                         13: "nw_wait", 14: "nw_eval", 4: "nw_push"}
+                nne = max(1.0, p[0, 9])
+                tot = p[:, 12].mean()
+                phases.append(dict(
+                    share={n: round(p[:, q].mean() / tot, 4) for q, n in names.items()},
+                    ns_per_nonempty={n: round(p[:, q].mean() / nne / 1.9, 1) for q, n in names.items()},
+                    windows=int(p[0, 8]), nonempty=int(p[0, 9]), heavy=int(p[0, 10]),
+                    staged=int(p[0, 11]), loop_cycles=int(tot), timeline=timeline))
         st = sess.states.cpu().numpy()
         w = sess.weights.cpu().numpy()
         bc = sess.block_counters.cpu().numpy()
@@ -63,7 +116,7 @@ def main():
                         and np.array_equal(bc, ref[2]))
         rec = dict(window=wsz, launch=sess.launch, ms_per_epoch=ms,
                    us_per_example=[m * 1e3 / len(ty) for m in ms], identical_to_first=same,
-                   stats=sess.stats_dict())
+                   stats=sess.stats_dict(), phases=phases)
         out.append(rec)
         print(json.dumps(rec), flush=True)
         del sess
