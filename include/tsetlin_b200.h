@@ -85,6 +85,17 @@ int tmb_microbench_pingpong(int mode, int hops, double *ns_per_hop, double *cycl
 int tmb_microbench_sparse_event(int which, int n, int n_act, int reps, int n_cta, int n_warps,
                                 double *us_per_event);
 
+/* Trainer feedback microbenchmark (design evidence): one CTA
+ * of `threads` threads with the configs[1] per-CTA slice (14 clauses x 1568
+ * positions, states in shared memory) applies Type I feedback to n_work
+ * firing clauses (two_events: target and negative event on each) `iters`
+ * times.  variant 0: feedback_quads (k_train_fast), 1: feedback_compact;
+ * 2-5: compact ablations (no mask rebuild / cheap hash / no state access / all);
+ * 6: feedback_simd (k_train_spec).
+ * *cycles_per_call = mean SM cycles per call including its barrier. */
+int tmb_microbench_feedback(int variant, int n_work, int two_events, int threads, int iters,
+                            double *cycles_per_call);
+
 /* ----------------------------------------------------- RNG (core.py) -- */
 /* core.py:66-95 on the host; used by the host driver and tests. */
 uint64_t tmb_derive_stream(uint64_t seed, uint64_t index);

@@ -347,6 +347,226 @@ __device__ __forceinline__ void feedback_quads(const TrainK &k, const Smem &s, i
     cn.upd += nupd;
 }
 
+// Compact per-position feedback for k_train_spec: the arithmetic of
+// feedback_quads (kernels/_numba.py:71-98, target event then negative event,
+// SPEC.md:369) with one quad per thread and iteration and both events
+// through one code path -- a fraction of the instructions.  The non-empty-
+// step path runs every few microseconds with its code fetched cold, so code
+// size is latency here.  Type I with the clause not firing is the general
+// rule with inc = 0 (every position decrements w.p. 1/s).
+// ABL (microbenchmark ablations only): 1 no mask rebuild, 2 a cheap hash
+// instead of SplitMix64, 4 no state load / store
+template <bool SMEM_STATES, int ABL = 0>
+__device__ __forceinline__ void feedback_compact(const TrainK &k, const Smem &s, int c0,
+                                                 const uint32_t *lit, int n_work, Counters &cn) {
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
+    const int QP = k.Ppad >> 2;  // quads per (padded) row; multiple of 32
+    const int total = n_work * QP;
+    int wc = tid / QP, rem = tid - (tid / QP) * QP;
+    const uint64_t t_inc = k.fp.t_inc, t_dec = k.fp.t_dec;
+    const int smin = k.fp.smin, smax = k.fp.smax, boost = k.fp.boost ? 1 : 0;
+    unsigned nd = 0, nupd = 0;
+    for (int it = tid; it < total; it += nthr) {  // warp-uniform: a warp's quads share a row
+        const int j = s.work[wc], p0 = rem << 2;
+        uint32_t word = 0xFFFFFFFFu;
+        int8_t *grow = SMEM_STATES ? nullptr : k.states + (int64_t)(c0 + j) * k.P;
+        if (ABL & 4) {
+            word = (uint32_t)(it * 0x9E3779B9u);
+        } else if (SMEM_STATES) {
+            word = *reinterpret_cast<const uint32_t *>(s.states + (size_t)j * k.Ppad + p0);
+        } else if (k.vec4 && p0 + 4 <= k.P) {
+            word = __ldcg(reinterpret_cast<const unsigned int *>(grow + p0));
+        } else {
+            for (int b = 0; b < 4; ++b)
+                if (p0 + b < k.P)
+                    word = (word & ~(0xFFu << (8 * b))) | ((uint32_t)(uint8_t)grow[p0 + b] << (8 * b));
+        }
+        const int info = s.info[j];
+        const int out = (info & I_OUT) ? 1 : 0;
+        const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
+        const int lim = k.P - p0;
+        int st[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) st[b] = (int)(int8_t)(word >> (8 * b));
+#pragma unroll 1
+        for (int ev = 0; ev < 2; ++ev) {
+            if (!(info & (ev ? I_NEV : I_TEV))) continue;
+            if (info & (ev ? I_N1 : I_T1)) {  // Type I
+                const uint64_t z0 = (ev ? s.sk_n[j] : s.sk_t[j]) + kGolden * (uint64_t)p0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int vb = b < lim ? 1 : 0;
+                    const int inc = out & (int)((litn >> b) & 1u);
+                    const uint64_t zz = (ABL & 2) ? (z0 + kGolden * (uint64_t)b) * kMixC1
+                                                  : mix64(z0 + kGolden * (uint64_t)b);
+                    const int hit = (zz >> 11) < (inc ? t_inc : t_dec) ? 1 : 0;
+                    const int room = st[b] < smax ? 1 : 0;
+                    const int above = st[b] > smin ? 1 : 0;
+                    nd += vb & (inc ? (room & (boost ^ 1)) : above);
+                    const int delta = (inc & room & (boost | hit)) - ((inc ^ 1) & above & hit);
+                    st[b] += vb ? delta : 0;
+                }
+            } else {  // Type II
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    st[b] += (b < lim ? 1 : 0) & out & (int)(((litn >> b) & 1u) ^ 1u) & (st[b] < 0 ? 1 : 0);
+            }
+        }
+        uint32_t nib = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            nupd += st[b] != (int)(int8_t)(word >> (8 * b)) ? 1 : 0;
+            nib |= (uint32_t)(b < lim && st[b] >= 0) << b;
+        }
+        const uint32_t nw = __byte_perm(__byte_perm((uint32_t)st[0], (uint32_t)st[1], 0x0040),
+                                        __byte_perm((uint32_t)st[2], (uint32_t)st[3], 0x0040), 0x5410);
+        if (nw != word && !(ABL & 4)) {
+            if (SMEM_STATES) {
+                *reinterpret_cast<uint32_t *>(s.states + (size_t)j * k.Ppad + p0) = nw;
+            } else if (k.vec4 && p0 + 4 <= k.P) {
+                __stcg(reinterpret_cast<unsigned int *>(grow + p0), nw);
+            } else {
+                for (int b = 0; b < 4; ++b)
+                    if (p0 + b < k.P) grow[p0 + b] = (int8_t)(nw >> (8 * b));
+            }
+        }
+        // mask word for positions 32w..32w+31: lanes 8g..8g+7 hold its nibbles
+        if (!(ABL & 1)) {
+            uint32_t m = nib << ((lane & 7) * 4);
+            m |= __shfl_xor_sync(0xffffffffu, m, 1);
+            m |= __shfl_xor_sync(0xffffffffu, m, 2);
+            m |= __shfl_xor_sync(0xffffffffu, m, 4);
+            if ((lane & 7) == 0) {
+                const int w = p0 >> 5;
+                if (w < k.W) {
+                    const uint32_t old = s.masks[j * k.MW + w];
+                    if (old != m) {
+                        s.masks[j * k.MW + w] = m;
+                        atomicAdd(&s.cnt[j], __popc(m) - __popc(old));
+                    }
+                }
+            }
+        } else {
+            cn.t2 += nib;
+        }
+        rem += nthr;
+        while (rem >= QP) {
+            rem -= QP;
+            ++wc;
+        }
+    }
+    cn.draws += nd;
+    cn.upd += nupd;
+}
+
+// Byte-SIMD per-quad feedback for k_train_spec: feedback_compact's
+// arithmetic (kernels/_numba.py:71-98, target then negative event) on the
+// four int8 states of a 32-bit word at once -- per-byte compares, the
+// +1 / -1 applied by carry-free SWAR add / subtract (states stay in
+// [state_min, state_max] within int8, so no byte over/underflows).  Only the
+// SplitMix64 draws remain per position; u < p is tested as z < t << 11 on
+// the full 64-bit draw (t < 2^53, exact).
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) {  // bit b -> byte b = 0xFF
+    return ((nib * 0x204081u) & 0x01010101u) * 0xFFu;
+}
+__device__ __forceinline__ uint32_t swar_inc(uint32_t w, uint32_t one) {  // bytes + {0,1}
+    return ((w & 0x7F7F7F7Fu) + one) ^ (w & 0x80808080u);
+}
+__device__ __forceinline__ uint32_t swar_dec(uint32_t w, uint32_t one) {  // bytes - {0,1}
+    return ((w | 0x80808080u) - one) ^ ((w ^ ~one) & 0x80808080u);
+}
+
+template <bool SMEM_STATES>
+__device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, int c0,
+                                              const uint32_t *lit, int n_work, Counters &cn) {
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
+    const int QP = k.Ppad >> 2;  // quads per (padded) row; multiple of 32
+    const int total = n_work * QP;
+    int wc = tid / QP, rem = tid - (tid / QP) * QP;
+    const uint64_t T_inc = k.fp.t_inc << 11, T_dec = k.fp.t_dec << 11;
+    const uint32_t smin4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smin;
+    const uint32_t smax4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smax;
+    const uint32_t boostm = k.fp.boost ? 0xFFFFFFFFu : 0u;
+    unsigned nd = 0, nupd = 0;
+    for (int it = tid; it < total; it += nthr) {  // warp-uniform: a warp's quads share a row
+        const int j = s.work[wc], p0 = rem << 2;
+        uint32_t word = 0xFFFFFFFFu;
+        int8_t *grow = SMEM_STATES ? nullptr : k.states + (int64_t)(c0 + j) * k.P;
+        if (SMEM_STATES) {
+            word = *reinterpret_cast<const uint32_t *>(s.states + (size_t)j * k.Ppad + p0);
+        } else if (k.vec4 && p0 + 4 <= k.P) {
+            word = __ldcg(reinterpret_cast<const unsigned int *>(grow + p0));
+        } else {
+            for (int b = 0; b < 4; ++b)
+                if (p0 + b < k.P)
+                    word = (word & ~(0xFFu << (8 * b))) | ((uint32_t)(uint8_t)grow[p0 + b] << (8 * b));
+        }
+        const int info = s.info[j];
+        const uint32_t outm = (info & I_OUT) ? 0xFFFFFFFFu : 0u;
+        const int lim = k.P - p0;
+        const uint32_t vb = lim >= 4 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
+        const uint32_t litb = spread4(p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u);
+        const uint32_t incb = litb & outm & vb;  // Type I: positions that may increment
+        uint32_t w = word;
+#pragma unroll 1
+        for (int ev = 0; ev < 2; ++ev) {
+            if (!(info & (ev ? I_NEV : I_TEV))) continue;
+            if (info & (ev ? I_N1 : I_T1)) {  // Type I
+                const uint64_t z0 = (ev ? s.sk_n[j] : s.sk_t[j]) + kGolden * (uint64_t)p0;
+                uint32_t hitn = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint64_t z = mix64(z0 + kGolden * (uint64_t)b);
+                    hitn |= (z < (((incb >> (8 * b)) & 1u) ? T_inc : T_dec) ? 1u : 0u) << b;
+                }
+                const uint32_t hit = spread4(hitn);
+                const uint32_t room = __vcmplts4(w, smax4), above = __vcmpgts4(w, smin4);
+                nd += __popc(((incb & room & ~boostm) | (~incb & above & vb)) & 0x01010101u);
+                const uint32_t up = incb & room & (boostm | hit);
+                const uint32_t dn = ~incb & vb & above & hit;
+                w = swar_dec(swar_inc(w, up & 0x01010101u), dn & 0x01010101u);
+            } else {  // Type II
+                const uint32_t neg = __vcmplts4(w, 0u);
+                w = swar_inc(w, outm & ~litb & vb & neg & 0x01010101u);
+            }
+        }
+        nupd += __popc(__vcmpne4(w, word) & 0x01010101u);
+        const uint32_t nib = (((~w & 0x80808080u) >> 7) & vb & 0x01010101u) * 0x01020408u >> 24;
+        if (w != word) {
+            if (SMEM_STATES) {
+                *reinterpret_cast<uint32_t *>(s.states + (size_t)j * k.Ppad + p0) = w;
+            } else if (k.vec4 && p0 + 4 <= k.P) {
+                __stcg(reinterpret_cast<unsigned int *>(grow + p0), w);
+            } else {
+                for (int b = 0; b < 4; ++b)
+                    if (p0 + b < k.P) grow[p0 + b] = (int8_t)(w >> (8 * b));
+            }
+        }
+        // mask word for positions 32w..32w+31: lanes 8g..8g+7 hold its nibbles
+        uint32_t m = nib << ((lane & 7) * 4);
+        m |= __shfl_xor_sync(0xffffffffu, m, 1);
+        m |= __shfl_xor_sync(0xffffffffu, m, 2);
+        m |= __shfl_xor_sync(0xffffffffu, m, 4);
+        if ((lane & 7) == 0) {
+            const int wd = p0 >> 5;
+            if (wd < k.W) {
+                const uint32_t old = s.masks[j * k.MW + wd];
+                if (old != m) {
+                    s.masks[j * k.MW + wd] = m;
+                    atomicAdd(&s.cnt[j], __popc(m) - __popc(old));
+                }
+            }
+        }
+        rem += nthr;
+        while (rem >= QP) {
+            rem -= QP;
+            ++wc;
+        }
+    }
+    cn.draws += nd;
+    cn.upd += nupd;
+}
+
 // Grid-balanced feedback (HBM-resident states): this CTA's share
 // [q_begin, q_end) of the quads of all CTAs' work items (the union of the
 // published work lists in CTA order; q_begin, q_end multiples of 32, so a
@@ -1572,13 +1792,10 @@ __device__ __forceinline__ void spec_issue(const TrainK &k, const Smem &s, int64
                 cp_async16(dst + 4 * nh + str * kSpecEnt + 4 * e, src + rec_entries(k) + str * k.Cp + 4 * e);
             }
         }
-        if ((k.dbg & 64) && lane == 0) {
-            const int lines = (2 * k.Cp * 4 + 127) / 128;
-            const int n_cta = k.n_cta;
-            for (int l = ((int)blockIdx.x - (int)(i % n_cta) + n_cta) % n_cta; l < lines; l += n_cta) {
-                const char *p = reinterpret_cast<const char *>(src + rec_entries(k)) + 128 * l;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-            }
+        if ((k.dbg & 64) && lane == 0 && (int)(i % k.n_cta) == (int)blockIdx.x) {
+            // one CTA per step: the step's flag entries into L2 (one bulk op)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         ::"l"(src + rec_entries(k)), "r"(8 * k.Cp) : "memory");
         }
     }
 }
@@ -1736,8 +1953,10 @@ __device__ __forceinline__ int mine_lane(int lane, int kk) { return lane < 2 * k
 // Per polled window wn: [0] %globaltimer when the next window was published
 // after wn's non-empty step, [1] %globaltimer at wn's poll completion, then
 // clock64 at [2] poll completion, [3] events done, [4] feedback done, [5]
-// publication; stored after the counters as [n_cta][kSpecTlN][kSpecTlQ].
-constexpr int kSpecTl0 = 2000, kSpecTlN = 2048, kSpecTlQ = 6;
+// publication, [6] work-list length, [7] flag entries of the step, [8]
+// clock64 after the decision barrier, [9] after the preparation barrier; stored
+// after the counters as [n_cta][kSpecTlN][kSpecTlQ].
+constexpr int kSpecTl0 = 2000, kSpecTlN = 2048, kSpecTlQ = 10;
 #define SPEC_TL(wn_, q_, v_)                                                                          \
     do {                                                                                              \
         if (PROF && (wn_) >= kSpecTl0 && (wn_) < kSpecTl0 + kSpecTlN)                                  \
@@ -1806,7 +2025,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
     } while (0)
     const long long dec_bias = (long long)n_cta * kVoteBias;
     const long long dec_2T = 2 * k.T;
-    const bool dec_tab = k.thr_smem != 0;
+    const bool dec_tab = k.thr_smem != 0;  // exact thresholds by table lookup (feedback.py:33-44)
     while (i0 < n) {
         const int kk = (int)(n - i0 < (int64_t)KW ? n - i0 : (int64_t)KW);
         const int64_t i1 = i0 + kk;
@@ -1828,17 +2047,19 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
                 SPEC_TL(wn, 1, gtimer());
                 SPEC_TL(wn, 2, clock64());
             }
-            // decision (feedback.py:33-44) of every step of the window
-            uint64_t th = 0;
+            // decision (feedback.py:33-44) of every step of the window: the
+            // update probability a / 2T is 0 iff a == 0; the exact threshold
+            // ceil(p * 2^53) only for the first non-empty step
+            long long a = 0;
             const long long v40 = (long long)(p & ((1ull << 40) - 1));
             if (mine) {
-                long long a = (lane & 1) ? k.T - dec_bias + v40 : k.T + dec_bias - v40;
+                a = (lane & 1) ? k.T - dec_bias + v40 : k.T + dec_bias - v40;
                 a = a < 0 ? 0 : (a > dec_2T ? dec_2T : a);
-                th = dec_tab ? s.thr_tab[a] : threshold_of(a, dec_2T >> 1);
             }
-            const unsigned busy = __ballot_sync(0xffffffffu, th != 0);
+            const unsigned busy = __ballot_sync(0xffffffffu, a != 0);
             const int first = busy ? (__ffs(busy) - 1) >> 1 : kk;
-            if (mine && (lane >> 1) == first) s.thr[lane & 1] = th;
+            if (mine && (lane >> 1) == first)
+                s.thr[lane & 1] = dec_tab ? s.thr_tab[a] : threshold_of(a, dec_2T >> 1);
             if (lane == 0) s.misc[1] = first;
             if (k.trace && rank == 0 && mine && (lane >> 1) <= first) {
                 const int64_t i = i0 + (lane >> 1);
@@ -1869,6 +2090,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
         }
         __syncthreads();
         SPH(1);
+        if (tid == 0) SPEC_TL(wn, 8, clock64());
         if (PROF && tid == 0) ph[8] += 1;
         const int first = s.misc[1];
         if (first >= kk) {  // all-empty window: the next one is already published
@@ -1907,6 +2129,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
         const int ne = hi_t + hi_n;
         __syncthreads();  // info[] written
         SPH(2);
+        if (tid == 0) SPEC_TL(wn, 9, clock64());
         auto count_entries = [&](int t0, int nt, unsigned &pre, unsigned &tot) {
             for (int e = t0; e < ne; e += nt) {
                 const int str = e >= hi_t ? 1 : 0;
@@ -1978,11 +2201,15 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
         if (tid == 0) SPEC_TL(wn, 3, clock64());
         const int n_work = (k.dbg & 1) ? 0 : s.misc[0];
         if (n_work > 0) {
-            feedback_quads<SMEM_STATES>(k, s, c0, lit, n_work, cn);
+            feedback_simd<SMEM_STATES>(k, s, c0, lit, n_work, cn);
             __syncthreads();
         }
         SPH(3);
-        if (tid == 0) SPEC_TL(wn, 4, clock64());
+        if (tid == 0) {
+            SPEC_TL(wn, 4, clock64());
+            SPEC_TL(wn, 6, n_work);
+            SPEC_TL(wn, 7, ne);
+        }
         // next window right after step i: the kept sums of its steps,
         // corrected by the work-list clauses
         i0 = i + 1;
@@ -2568,3 +2795,74 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
 }
 
 }  // extern "C"
+
+// ------------------------------------------------- feedback microbench --
+namespace tmb {
+template <int VARIANT>
+__global__ void __launch_bounds__(1024, 1) k_mb_feedback(TrainK k, int n_work, int two, int iters,
+                                                          unsigned long long *cyc) {
+    extern __shared__ __align__(16) char smem_raw[];
+    Smem s;
+    smem_layout(k, true, MODE_GRID, smem_raw, &s);
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    for (int i = tid; i < k.cmax * k.Ppad; i += nthr)
+        s.states[i] = (int8_t)((int)(mix64((uint64_t)i) & 255) - 128);
+    for (int i = tid; i < k.cmax * k.MW; i += nthr) s.masks[i] = 0;
+    for (int j = tid; j < k.cmax; j += nthr) {
+        s.work[j] = j;
+        s.info[j] = I_OUT | I_TEV | I_T1 | (two ? (I_NEV | I_N1) : 0);
+        s.sk_t[j] = mix64(j);
+        s.sk_n[j] = mix64(j + 100);
+        s.cnt[j] = 0;
+    }
+    uint32_t *lit = s.lit0;
+    for (int w = tid; w < k.W; w += nthr) lit[w] = (uint32_t)mix64(w + 7);
+    __syncthreads();
+    Counters cn;
+    unsigned long long tot = 0;
+    for (int it = 0; it < iters; ++it) {
+        const long long t0 = clock64();
+        if (VARIANT == 0) feedback_quads<true>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 1) feedback_compact<true>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 2) feedback_compact<true, 1>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 3) feedback_compact<true, 2>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 4) feedback_compact<true, 4>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 5) feedback_compact<true, 7>(k, s, 0, lit, n_work, cn);
+        else feedback_simd<true>(k, s, 0, lit, n_work, cn);
+        __syncthreads();
+        tot += (unsigned long long)(clock64() - t0);
+    }
+    if (tid == 0) cyc[0] = tot + ((cn.draws + cn.t2) & 1);  // keep the work alive
+}
+}  // namespace tmb
+
+extern "C" int tmb_microbench_feedback(int variant, int n_work, int two_events, int threads,
+                                       int iters, double *cycles_per_call) {
+    using namespace tmb;
+    int rc = require_device();
+    if (rc) return rc;
+    if (n_work < 0 || n_work > 14 || iters < 1 || !cycles_per_call)
+        return fail(TMB_E_INVALID, "microbench_feedback: bad arguments");
+    TrainK k{};
+    k.C = 2000; k.P = 1568; k.K = 10; k.W = 49; k.Ppad = 1664; k.n_blocks = 1; k.n_cta = 148;
+    k.cmax = 14; k.fmax_words = 1; k.bmax = 1; k.vec4 = 1; k.fast = 1; k.Wp = 52; k.Cp = 2000;
+    k.R = 4 + k.Wp + 260 + 2 * k.Cp; k.MW = 52; k.budget = 1 << 30; k.T = 5000;
+    k.fp = make_fb_params(10.0, 0, -128, 127);
+    const size_t sm = smem_layout(k, true, MODE_GRID, nullptr, nullptr);
+    unsigned long long *cyc = nullptr;
+    TMB_CUDA(cudaMalloc(&cyc, 8));
+    const void *fns[7] = {(const void *)k_mb_feedback<0>, (const void *)k_mb_feedback<1>,
+                          (const void *)k_mb_feedback<2>, (const void *)k_mb_feedback<3>,
+                          (const void *)k_mb_feedback<4>, (const void *)k_mb_feedback<5>,
+                          (const void *)k_mb_feedback<6>};
+    if (variant < 0 || variant > 6) return fail(TMB_E_INVALID, "microbench_feedback: variant 0..6");
+    TMB_CUDA(cudaFuncSetAttribute(fns[variant], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    void *args[] = {&k, &n_work, &two_events, &iters, &cyc};
+    TMB_CUDA(cudaLaunchKernel(fns[variant], dim3(1), dim3(threads), args, sm, 0));
+    rc = check_cuda(cudaGetLastError(), "microbench launch");
+    unsigned long long c = 0;
+    if (!rc) rc = check_cuda(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    cudaFree(cyc);
+    if (!rc) *cycles_per_call = (double)c / iters;
+    return rc;
+}

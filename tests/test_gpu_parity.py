@@ -826,3 +826,37 @@ def test_single_warp_trainer_vs_oracle(gpu, oracle, F, C, K, nb, boost, budget):
                               ost.block_counters), warp
         stats.append(sess.stats_dict())
     assert stats[0] == stats[1]
+
+
+@pytest.mark.parametrize("window,n_cta,n_train", [(1, 148, 700), (5, 148, 703), (16, 37, 1500),
+                                                  (16, 20, 333), (7, 148, 5)])
+def test_speculative_windows_vs_oracle(gpu, oracle, window, n_cta, n_train):
+    """k_train_spec (one exchange per window of up to `window` steps, kept
+    per-step sums corrected by the work list) against the oracle and against
+    k_train_fast (train.spec_window=0): models, block counters and the
+    per-step trace (negative class, both class sums, events) are identical --
+    window sizes that do not divide the run, runs shorter than one window,
+    more than 32 clauses per CTA (multi-word output bitsets)."""
+    import torch
+    (tx, ty), _ = gpu.datasets.mnist_shaped(n_train=n_train, n_test=10, data_seed=6)
+    cfg = gpu.Config(**gpu.datasets.mnist_shaped_config_kwargs(seed=4))
+    ost, _ = oracle.train(cfg, tx, ty, 2)
+    got = {}
+    try:
+        for w in (window, 0):
+            gpu._lib.call("tmb_set_option", b"train.spec_window", w)
+            sess = gpu.DenseTrainSession(cfg, tx, ty, n_cta=n_cta)
+            trace = torch.zeros((2, n_train, 4), dtype=torch.int64, device="cuda")
+            for e in range(2):
+                gpu._lib.call("tmb_trainer_set_trace", sess._h, trace[e].data_ptr())
+                sess.run_epoch()
+            m = sess.model()
+            assert np.array_equal(m.states, ost.states), w
+            assert np.array_equal(m.weights, ost.weights), w
+            assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64),
+                                  ost.block_counters), w
+            got[w] = trace.cpu().numpy()
+    finally:
+        gpu._lib.call("tmb_set_option", b"train.spec_window", 16)
+    assert np.array_equal(got[window], got[0])
+    assert got[0][:, :, 3].sum() > 0  # the run has events

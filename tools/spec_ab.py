@@ -48,7 +48,7 @@ def main():
         prof = None
         if args.prof and wsz > 0:
             ncta = sess.launch["n_cta"]
-            prof = torch.zeros(ncta * 16 + ncta * 2048 * 6, dtype=torch.int64, device="cuda")
+            prof = torch.zeros(ncta * 16 + ncta * 2048 * 10, dtype=torch.int64, device="cuda")
             _lib.call("tmb_trainer_set_profile", sess._h, prof.data_ptr())
 
         def reset():
@@ -70,7 +70,7 @@ def main():
             if prof is not None:
                 allp = prof.cpu().numpy()
                 p = allp[:ncta * 16].reshape(-1, 16).astype(np.float64)
-                tl = allp[ncta * 16:].reshape(ncta, 2048, 6).astype(np.float64)
+                tl = allp[ncta * 16:].reshape(ncta, 2048, 10).astype(np.float64)
                 heavy = (tl[:, :, 0] > 0).all(axis=0) & (tl[:, :, 1] > 0).all(axis=0)
                 polled = (tl[:, :, 1] > 0).all(axis=0)
                 h = tl[:, heavy, :]
@@ -87,6 +87,11 @@ def main():
                     if nxt < 2048 and polled[nxt]:
                         lat.append(tl[:, nxt, 1].min() - tl[:, w, 0].max())
                 med = lambda a: float(np.median(a))
+                nw = h[:, :, 6]
+                fb_by_nwork = {int(v): round(float(np.median(fb[nw == v])), 1)
+                               for v in range(0, 12) if (nw == v).sum() > 20}
+                nw_max = nw.max(axis=0)
+                ent = h[0, :, 7]
                 timeline = dict(
                     heavy_windows=int(heavy.sum()),
                     chain_ns=dict(median_cta=med(np.median(chain, axis=0)), max_cta=med(chain.max(axis=0))),
@@ -95,6 +100,17 @@ def main():
                     correct_push_ns=dict(median_cta=med(np.median(pb, axis=0)), max_cta=med(pb.max(axis=0))),
                     done_spread_ns=med(h[:, :, 1].max(axis=0) - h[:, :, 1].min(axis=0)),
                     pub_skew_ns=med(h[:, :, 0].max(axis=0) - np.median(h[:, :, 0], axis=0)),
+                    decide_ns=med(np.median((h[:, :, 8] - h[:, :, 2]) / cyc, axis=0)),
+                    prep_ns=med(np.median((h[:, :, 9] - h[:, :, 8]) / cyc, axis=0)),
+                    count_own_ns=med(np.median((h[:, :, 3] - h[:, :, 9]) / cyc, axis=0)),
+                    fb_ns_by_nwork=fb_by_nwork,
+                    nwork_max_cta=np.percentile(nw_max, [10, 50, 90]).tolist(),
+                    nwork_mean_cta=float(nw.mean()),
+                    entries=np.percentile(ent, [10, 50, 90]).tolist(),
+                    events_ns_by_entries={b: round(float(np.median(ev[:, (ent >= lo) & (ent < hi)])), 1)
+                                          for b, (lo, hi) in {"<=64": (0, 65), "65-512": (65, 513),
+                                                              "513-2048": (513, 2049), ">2048": (2049, 1e9)}.items()
+                                          if ((ent >= lo) & (ent < hi)).sum() > 5},
                     next_latency_ns=np.percentile(lat, [10, 50, 90]).round().tolist() if lat else None)
                 names = {0: "poll", 1: "decide", 2: "ev_prep", 15: "ev_count_own", 3: "feedback",
                          13: "nw_wait", 14: "nw_eval", 4: "nw_push"}
