@@ -207,6 +207,9 @@ int tmb_trainer_destroy(tmb_trainer *t);
  * only when n_blocks == 1) for its example i.  Device int64 [n_steps*4]. */
 int tmb_trainer_set_trace(tmb_trainer *t, int64_t *trace);
 /* Phase profiling: when non-NULL, every launch writes, per CTA, the clock64
+ * cycles of its phases.  k_train_spec: [n_cta * 16] counters (see
+ * tmb_train.cu) then a per-window timeline [n_cta][2048][10] (size the
+ * buffer n_cta * (16 + 20480)).  Other grid-mode kernels: the clock64
  * cycles thread 0 spent in each of 8 kernel phases (device uint64
  * [n_cta * 8]): eval, partial votes + arrive, flag-draw precompute +
  * prefetch, all-reduce wait + decision, flag bitmaps, scan + events,
@@ -218,6 +221,10 @@ int tmb_trainer_set_profile(tmb_trainer *t, uint64_t *phase);
 /* Launch configuration actually used (for reporting). */
 int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_bytes,
                      int *states_in_smem);
+/* Which fused trainer runs (for reporting): *kind 0 k_train_warp (one warp),
+ * 1 k_train cluster mode, 2 k_train grid mode, 3 k_train_fast, 4 k_train_spec
+ * (speculative windows of *window steps, else 0). */
+int tmb_trainer_kernel(const tmb_trainer *t, int *kind, int *window);
 /* Run n_steps examples: example i uses literal row lit_words[order[i]] (device
  * uint32 [N, W]) and label labels[order[i]] (device int32); the feedback
  * stream counter of example i is fb_counter + i*(1+2C) (feedback.py:33-53).

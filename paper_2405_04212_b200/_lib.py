@@ -82,6 +82,7 @@ SIGNATURES = {
     "tmb_trainer_set_trace": (i32, [vp, vp]),
     "tmb_trainer_set_profile": (i32, [vp, vp]),
     "tmb_trainer_info": (i32, [vp, vp, vp, vp, vp]),
+    "tmb_trainer_kernel": (i32, [vp, vp, vp]),
     "tmb_trainer_run": (i32, [vp, vp, vp, vp, i64, u64, vp, vp]),
     "tmb_rules_from_bank": (i32, [vp, vp, i64, i64, i64, i64, i32, vp, vp]),
     "tmb_rules_from_csr": (i32, [vp, vp, i64, vp, i64, i64, i32, vp]),

@@ -2698,6 +2698,14 @@ int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_b
     return TMB_OK;
 }
 
+int tmb_trainer_kernel(const tmb_trainer *t, int *kind, int *window) {
+    if (!t) return fail(TMB_E_INVALID, "trainer_kernel: NULL");
+    const int kd = t->warp ? 0 : t->cluster ? 1 : !t->k.fast ? 2 : t->k.spec ? 4 : 3;
+    if (kind) *kind = kd;
+    if (window) *window = kd == 4 ? t->k.spec : 0;
+    return TMB_OK;
+}
+
 int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *labels,
                     const int32_t *order, int64_t n_steps, uint64_t fb_counter,
                     tmb_train_stats *stats, void *stream) {

@@ -105,6 +105,11 @@ def _resolve_jobs(n_jobs: int, n_blocks: int) -> int:
     return min(n_jobs, n_blocks)
 
 
+# tmb_trainer_kernel kinds
+TRAINER_KERNELS = ("k_train_warp", "k_train (cluster)", "k_train (grid)", "k_train_fast",
+                   "k_train_spec")
+
+
 class DenseTrainSession:
     """Device-resident dense training state: the model (states, weights,
     per-block counters), the packed dataset and the fused-kernel trainer.
@@ -145,8 +150,11 @@ class DenseTrainSession:
         a, b, c, d = ct.c_int(), ct.c_int(), ct.c_int(), ct.c_int()
         _lib.call("tmb_trainer_info", self._h, ct.byref(a), ct.byref(b), ct.byref(c),
                   ct.byref(d))
+        kind, win = ct.c_int(), ct.c_int()
+        _lib.call("tmb_trainer_kernel", self._h, ct.byref(kind), ct.byref(win))
         self.launch = dict(n_cta=a.value, threads=b.value, smem_bytes=c.value,
-                           states_in_smem=bool(d.value))
+                           states_in_smem=bool(d.value),
+                           kernel=TRAINER_KERNELS[kind.value], spec_window=win.value)
 
     def set_data(self, x: np.ndarray, y: np.ndarray):
         """Upload raw features once and pack them to literal bit rows on the
