@@ -17,7 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 1 --warmup 3 --no-secondary --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/${TAG}_c3_infer_launches.csv \
     python bench.py --workload c3-infer --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_train_fast -s 3 -c 1 \
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_train_spec -s 3 -c 1 \
     -o $OUT/${TAG}_prof_train python bench.py --steps 1 --warmup 3 --no-secondary --no-cpu-baseline > $OUT/${TAG}_ncu_train.log 2>&1
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_infer_solo -s 3 -c 1 \
     -o $OUT/${TAG}_prof_infer python bench.py --workload c3-infer --steps 1 --warmup 3 --no-cpu-baseline > $OUT/${TAG}_ncu_infer.log 2>&1
