@@ -783,15 +783,18 @@ def ct_ptr(t):
 # ------------------------------------------------------- c4 / c5 rows --
 
 def c4_ncu_sample():
-    """DRAM bytes per example of the generic grid trainer from the committed
-    ncu capture of tools/probes/c4_once.py (one 1000-step launch, examples 0..999 of
-    epoch 1: more events per example than the bench's later steps, so this
-    is a traffic-per-example sample, not the bench launch)."""
+    """DRAM bytes per example of the generic grid trainer from the newest
+    committed ncu capture: tools/profile_round.sh captures the bench's own
+    first timed c4-train launch (5000 steps after 3 warm-up launches); the
+    round-1 summaries hold a 1000-step launch from a fresh model
+    (tools/probes/c4_once.py)."""
     tot, src = ncu_traffic("k_train<")
     if tot is None:
         return None
-    return {"dram_bytes_per_example": tot / 1000.0, "source": src,
-            "sample": "tools/probes/c4_once.py: 1000 steps from a fresh model"}
+    steps = 1000 if src.startswith("r01") else 5000
+    return {"dram_bytes_per_example": tot / steps, "dram_bytes_per_launch": tot, "source": src,
+            "sample": ("tools/probes/c4_once.py: 1000 steps from a fresh model" if steps == 1000
+                       else "tools/profile_round.sh: the bench's first timed 5000-step launch")}
 
 
 def bench_c4_train(args, rank, world, local):
@@ -812,9 +815,20 @@ def bench_c4_train(args, rank, world, local):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     pos = 0
-    for _ in range(args.warmup):
-        sess.run_steps(order[pos:pos + step_n])
+
+    def next_slice():
+        # the next step_n examples of the running epoch (the next epoch's
+        # shuffle once this one is used up: a step never trains fewer)
+        nonlocal order, pos
+        if pos + step_n > sess.N:
+            order = torch.from_numpy(sess.next_order().astype(np.int32)).cuda()
+            pos = 0
+        sl = order[pos:pos + step_n]
         pos += step_n
+        return sl
+
+    for _ in range(args.warmup):
+        sess.run_steps(next_slice())
     torch.cuda.synchronize()
     st0 = sess.states.cpu().numpy().copy()
     w0 = sess.weights.cpu().numpy().copy()
@@ -822,10 +836,10 @@ def bench_c4_train(args, rank, world, local):
     fb0 = sess.fb_counter
     stats0 = sess.stats_dict()
     snap = sess.snapshot()
-    pos0 = pos
     launches0 = _lib.launch_count()
     barrier(world)
     k_ms = []
+    timed_slices = []
     with ClockSampler(local) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
@@ -834,11 +848,12 @@ def bench_c4_train(args, rank, world, local):
             flush_l2(flush)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
+            sl = next_slice()
+            timed_slices.append(sl)
             a.record(stream)
-            sess.run_steps(order[pos:pos + step_n])
+            sess.run_steps(sl)
             b.record(stream)
             k_ms.append((a, b))
-            pos += step_n
         t_end.record(stream)
         torch.cuda.synchronize()
         barrier(world)
@@ -867,21 +882,19 @@ def bench_c4_train(args, rank, world, local):
     xp = torch.from_numpy(np.ascontiguousarray(tx)).pin_memory()
     st_host = torch.empty(sess.states.shape, dtype=torch.int8).pin_memory()
     w_host = torch.empty(sess.weights.shape, dtype=torch.int32).pin_memory()
-    ordh = order.cpu().pin_memory()
+    slices_h = [sl.cpu().pin_memory() for sl in timed_slices]
     barrier(world)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    pos = pos0
     for i in range(args.steps):
         xd = xp.to("cuda", non_blocking=True)
         _lib.call("tmb_pack_literals", ptr(xd), xp.shape[0], cfg.n_literals, 1,
                   ptr(sess.lit_words), stream_ptr())
-        od = ordh[pos:pos + step_n].to("cuda", non_blocking=True)
+        od = slices_h[i].to("cuda", non_blocking=True)
         sess.run_steps(od)
         st_host.copy_(sess.states, non_blocking=True)
         w_host.copy_(sess.weights, non_blocking=True)
-        pos += step_n
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
@@ -898,19 +911,25 @@ def bench_c4_train(args, rank, world, local):
                    "l2": "256 MiB buffer written before every timed step"},
         "gpu_launches": int(launches),
         "work": {"events_per_example": ev_ex, "draws_per_example": draws_ex},
-        "roofline": {"kernel": "k_train<1, false> (grid mode, HBM-resident states)",
-                     "bound": "hbm", "achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
-                     "frac": achieved / HBM_PEAK, "traffic": None, "peak_source": HBM_PEAK_SRC,
-                     "algorithmic_bytes_per_example": bytes_ex,
-                     "avg_launch_ms": per_launch_ms,
-                     "traffic_ncu_sample": c4_ncu_sample()},
+        # the binding resource is the integer pipe: every reference draw is
+        # one SplitMix64 (two 64-bit multiplies) + compare, at the measured
+        # per-SM draw rate; the HBM traffic of the states is secondary
+        "roofline": {"kernel": "k_train<1, false> (grid mode, HBM-resident states, "
+                               "grid-balanced byte-SIMD feedback)",
+                     "bound": "int (SplitMix64 draws at the measured per-SM rate)",
+                     "achieved": draws_ex * step_n / (per_launch_ms / 1e3) / 1e9,
+                     "peak": lp["draw_peak_per_s"] / 1e9, "unit": "G draws/s",
+                     "frac": int_s_ex * step_n / (per_launch_ms / 1e3),
+                     "traffic": c4_ncu_sample(), "peak_source": lp["source"],
+                     "draws_per_example": draws_ex,
+                     "int_us_per_example": int_s_ex * 1e6,
+                     "achieved_us_per_example": per_launch_ms * 1e3 / step_n,
+                     "avg_launch_ms": per_launch_ms},
         "pipes_ncu": ncu_pipes("k_train<"),
-        "roofline_int": {"bound": "int (SplitMix64 draws at the measured per-SM rate)",
-                         "frac": int_s_ex * step_n / (per_launch_ms / 1e3),
-                         "int_us_per_example": int_s_ex * 1e6,
-                         "achieved_us_per_example": per_launch_ms * 1e3 / step_n,
-                         "draw_peak_per_s": lp["draw_peak_per_s"],
-                         "peak_source": lp["source"]},
+        "roofline_hbm": {"achieved": achieved, "peak": HBM_PEAK, "unit": "GB/s",
+                         "frac": achieved / HBM_PEAK, "peak_source": HBM_PEAK_SRC,
+                         "algorithmic_bytes_per_example": bytes_ex,
+                         "traffic_ncu_sample": c4_ncu_sample()},
         "clocks": clocks,
         "e2e": {"value": n_ex * world / (e2e_ms / 1e3), "unit": "examples/s",
                 "h2d_bytes_per_step": int(tx.nbytes + 4 * step_n),
@@ -922,7 +941,7 @@ def bench_c4_train(args, rank, world, local):
         from oracle import oracle
         x_lit = oracle.augment_literals(tx)
         rate, n_done, dt = oracle_train_rate(cfg, st0, w0, c0, fb0, x_lit, ty,
-                                             order[pos0:pos0 + step_n].cpu().numpy().astype(np.int64),
+                                             timed_slices[0].cpu().numpy().astype(np.int64),
                                              args.cpu_seconds)
         model_name, ncpu = host_desc()
         line["cpu_baseline"] = {"value": rate, "unit": "examples/s", "cores": 1, "kind": "port",

@@ -75,6 +75,7 @@ int sm_count();
 extern int64_t g_train_key_chunk;
 extern int g_train_dbg;  // trainer timing ablations (tmb_train.cu)
 extern int g_train_spec;  // speculative window of the fast grid trainer (tmb_train.cu)
+extern int g_train_spec_ent;  // staged flag entries per step head (0 = auto)
 //  // keyed trainer: steps per launch override (tmb_train.cu)
 
 }  // namespace tmb

@@ -1610,6 +1610,10 @@ int tmb_set_option(const char *name, int64_t value) {
         g_train_spec = (int)value;                   // (applies to trainers created afterwards)
         return TMB_OK;
     }
+    if (std::string(name) == "train.spec_entries") {  // 0 auto, else 64..256 (multiple of 32; default 64)
+        g_train_spec_ent = (int)value;
+        return TMB_OK;
+    }
     if (std::string(name) == "train.debug_skip") {  // timing ablations only (not bit-exact)
         g_train_dbg = (int)value;
         return TMB_OK;

@@ -81,6 +81,8 @@ struct TrainK {
     int thr_smem;
     // speculative windows (k_train_spec): examples per window, 0 = k_train_fast
     int spec;
+    int spec_ent;              // spec: flag entries per stream staged with each step head
+    const uint32_t *thr32;     // spec: threshold_of(a, T) >> 21 for a in [0, 2T] (k.thr_smem)
 };
 
 // CTA owning clause c (inverse of cta_begin).
@@ -179,12 +181,15 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
     t.clo = fs ? (long long *)take(8 * 4 * (size_t)k.cmax) : nullptr;
     t.vsh = fs ? (unsigned long long *)take(8 * 4) : nullptr;
     const bool sp = k.fast && k.spec;
-    t.hring = sp ? (uint32_t *)take(4 * (size_t)(3 * k.spec) * (size_t)(4 + k.Wp + 260 + 2 * 64))
+    t.hring = sp ? (uint32_t *)take(4 * (size_t)(3 * k.spec) * (size_t)(4 + k.Wp + 260 + 2 * k.spec_ent))
                  : nullptr;
     t.obs = sp ? (uint32_t *)take(4 * (size_t)(3 * k.spec) * (size_t)((k.cmax + 31) / 32)) : nullptr;
     t.vst = sp ? (long long *)take(8 * 2 * (size_t)(3 * k.spec)) : nullptr;
     t.part = sp ? (long long *)take(8 * 32 * 32) : nullptr;
-    t.thr_tab = k.fast && k.thr_smem ? (uint64_t *)take(8 * (size_t)(2 * k.T + 1)) : nullptr;
+    // k_train_spec keeps the table in 32 bits (bucket + all but the low 21
+    // bits of each threshold; the exact value is recomputed on a key tie)
+    t.thr_tab = k.fast && k.thr_smem ? (uint64_t *)take((k.spec ? 4 : 8) * (size_t)(2 * k.T + 1))
+                                     : nullptr;
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
     const bool gb = k.gbal && !k.fast && !smem_states && mode == MODE_GRID;
     t.gpref = gb ? (int *)take(4 * (size_t)(k.n_cta + 1)) : nullptr;
@@ -476,6 +481,52 @@ __device__ __forceinline__ uint32_t swar_dec(uint32_t w, uint32_t one) {  // byt
     return ((w | 0x80808080u) - one) ^ ((w ^ ~one) & 0x80808080u);
 }
 
+// One quad of feedback_simd: the four states of word w after the clause's
+// events (info bits), literal nibble litn, valid positions lim; zt / zn =
+// event key + kGolden * p0 of the target / negative event.  Adds the
+// reference's draw count to nd.
+__device__ __forceinline__ uint32_t quad_update_simd(const TrainK &k, uint32_t w, int info,
+                                                     uint32_t litn, int lim, uint64_t zt,
+                                                     uint64_t zn, unsigned &nd) {
+    const uint64_t T_inc = k.fp.t_inc << 11, T_dec = k.fp.t_dec << 11;
+    const uint32_t smin4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smin;
+    const uint32_t smax4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smax;
+    const uint32_t boostm = k.fp.boost ? 0xFFFFFFFFu : 0u;
+    const uint32_t outm = (info & I_OUT) ? 0xFFFFFFFFu : 0u;
+    const uint32_t vb = lim >= 4 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
+    const uint32_t litb = spread4(litn);
+    const uint32_t incb = litb & outm & vb;  // Type I: positions that may increment
+#pragma unroll 1
+    for (int ev = 0; ev < 2; ++ev) {
+        if (!(info & (ev ? I_NEV : I_TEV))) continue;
+        if (info & (ev ? I_N1 : I_T1)) {  // Type I
+            const uint64_t z0 = ev ? zn : zt;
+            uint32_t hitn = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint64_t z = mix64(z0 + kGolden * (uint64_t)b);
+                hitn |= (z < (((incb >> (8 * b)) & 1u) ? T_inc : T_dec) ? 1u : 0u) << b;
+            }
+            const uint32_t hit = spread4(hitn);
+            const uint32_t room = __vcmplts4(w, smax4), above = __vcmpgts4(w, smin4);
+            nd += __popc(((incb & room & ~boostm) | (~incb & above & vb)) & 0x01010101u);
+            const uint32_t up = incb & room & (boostm | hit);
+            const uint32_t dn = ~incb & vb & above & hit;
+            w = swar_dec(swar_inc(w, up & 0x01010101u), dn & 0x01010101u);
+        } else {  // Type II
+            const uint32_t neg = __vcmplts4(w, 0u);
+            w = swar_inc(w, outm & ~litb & vb & neg & 0x01010101u);
+        }
+    }
+    return w;
+}
+
+// Include bits (state >= 0) of the valid positions of a quad, as a nibble.
+__device__ __forceinline__ uint32_t quad_include_nibble(uint32_t w, int lim) {
+    const uint32_t vb = lim >= 4 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
+    return (((~w & 0x80808080u) >> 7) & vb & 0x01010101u) * 0x01020408u >> 24;
+}
+
 template <bool SMEM_STATES>
 __device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, int c0,
                                               const uint32_t *lit, int n_work, Counters &cn) {
@@ -483,10 +534,6 @@ __device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, in
     const int QP = k.Ppad >> 2;  // quads per (padded) row; multiple of 32
     const int total = n_work * QP;
     int wc = tid / QP, rem = tid - (tid / QP) * QP;
-    const uint64_t T_inc = k.fp.t_inc << 11, T_dec = k.fp.t_dec << 11;
-    const uint32_t smin4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smin;
-    const uint32_t smax4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smax;
-    const uint32_t boostm = k.fp.boost ? 0xFFFFFFFFu : 0u;
     unsigned nd = 0, nupd = 0;
     for (int it = tid; it < total; it += nthr) {  // warp-uniform: a warp's quads share a row
         const int j = s.work[wc], p0 = rem << 2;
@@ -502,36 +549,14 @@ __device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, in
                     word = (word & ~(0xFFu << (8 * b))) | ((uint32_t)(uint8_t)grow[p0 + b] << (8 * b));
         }
         const int info = s.info[j];
-        const uint32_t outm = (info & I_OUT) ? 0xFFFFFFFFu : 0u;
         const int lim = k.P - p0;
-        const uint32_t vb = lim >= 4 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
-        const uint32_t litb = spread4(p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u);
-        const uint32_t incb = litb & outm & vb;  // Type I: positions that may increment
-        uint32_t w = word;
-#pragma unroll 1
-        for (int ev = 0; ev < 2; ++ev) {
-            if (!(info & (ev ? I_NEV : I_TEV))) continue;
-            if (info & (ev ? I_N1 : I_T1)) {  // Type I
-                const uint64_t z0 = (ev ? s.sk_n[j] : s.sk_t[j]) + kGolden * (uint64_t)p0;
-                uint32_t hitn = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const uint64_t z = mix64(z0 + kGolden * (uint64_t)b);
-                    hitn |= (z < (((incb >> (8 * b)) & 1u) ? T_inc : T_dec) ? 1u : 0u) << b;
-                }
-                const uint32_t hit = spread4(hitn);
-                const uint32_t room = __vcmplts4(w, smax4), above = __vcmpgts4(w, smin4);
-                nd += __popc(((incb & room & ~boostm) | (~incb & above & vb)) & 0x01010101u);
-                const uint32_t up = incb & room & (boostm | hit);
-                const uint32_t dn = ~incb & vb & above & hit;
-                w = swar_dec(swar_inc(w, up & 0x01010101u), dn & 0x01010101u);
-            } else {  // Type II
-                const uint32_t neg = __vcmplts4(w, 0u);
-                w = swar_inc(w, outm & ~litb & vb & neg & 0x01010101u);
-            }
-        }
+        const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
+        const uint64_t zp = kGolden * (uint64_t)p0;
+        const uint32_t w = quad_update_simd(k, word, info, litn, lim,
+                                            (info & I_TEV) ? s.sk_t[j] + zp : 0,
+                                            (info & I_NEV) ? s.sk_n[j] + zp : 0, nd);
         nupd += __popc(__vcmpne4(w, word) & 0x01010101u);
-        const uint32_t nib = (((~w & 0x80808080u) >> 7) & vb & 0x01010101u) * 0x01020408u >> 24;
+        const uint32_t nib = quad_include_nibble(w, lim);
         if (w != word) {
             if (SMEM_STATES) {
                 *reinterpret_cast<uint32_t *>(s.states + (size_t)j * k.Ppad + p0) = w;
@@ -579,7 +604,6 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int QP = k.Ppad >> 2;
     constexpr int B = 4;
-    const int smin = k.fp.smin, smax = k.fp.smax, boost = k.fp.boost ? 1 : 0;
     unsigned nd = 0, nupd = 0;
     // quad it = (work item g_lo + gnext, quad rem) advanced by nthr per unit
     // without a division (nthr < QP is not assumed: a short loop)
@@ -620,58 +644,14 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
             const int g = gi[u], p0 = pp[u];
             const int c = s.rc_clause[g];
             const int info = s.rc_info[g];
-            const int out = (info & I_OUT) ? 1 : 0;
             const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
             const int lim = k.P - p0;
-            int st[4], s0[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) s0[b] = st[b] = (int)(int8_t)(word[u] >> (8 * b));
-            auto type_i = [&](uint64_t z0) {
-                if (!out) {  // warp-uniform: every position moves down w.p. 1/s
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int above = (b < lim ? 1 : 0) & (st[b] > smin ? 1 : 0);
-                        const int hit = (mix64(z0 + kGolden * (uint64_t)b) >> 11) < k.fp.t_dec ? 1 : 0;
-                        nd += above;
-                        st[b] -= above & hit;
-                    }
-                    return;
-                }
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int vb = b < lim ? 1 : 0;
-                    const int inc = (int)((litn >> b) & 1u);
-                    const int hit = (mix64(z0 + kGolden * (uint64_t)b) >> 11) <
-                                    (inc ? k.fp.t_inc : k.fp.t_dec) ? 1 : 0;
-                    const int room = st[b] < smax ? 1 : 0;
-                    const int above = st[b] > smin ? 1 : 0;
-                    nd += vb & (inc ? (room & (boost ^ 1)) : above);
-                    const int delta = (inc & room & (boost | hit)) - ((inc ^ 1) & above & hit);
-                    st[b] += vb ? delta : 0;
-                }
-            };
-            auto type_ii = [&]() {
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    st[b] += (b < lim ? 1 : 0) & out & (int)(((litn >> b) & 1u) ^ 1u) & (st[b] < 0 ? 1 : 0);
-            };
-            if (info & I_TEV) {
-                if (info & I_T1) type_i(s.rc_sk[2 * g] + kGolden * (uint64_t)p0);
-                else type_ii();
-            }
-            if (info & I_NEV) {
-                if (info & I_N1) type_i(s.rc_sk[2 * g + 1] + kGolden * (uint64_t)p0);
-                else type_ii();
-            }
-            uint32_t nib = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                nupd += st[b] != s0[b] ? 1 : 0;
-                nib |= (uint32_t)(b < lim && st[b] >= 0) << b;
-            }
-            const uint32_t nw = __byte_perm(__byte_perm((uint32_t)st[0], (uint32_t)st[1], 0x0040),
-                                            __byte_perm((uint32_t)st[2], (uint32_t)st[3], 0x0040),
-                                            0x5410);
+            const uint64_t zp = kGolden * (uint64_t)p0;
+            const uint32_t nw = quad_update_simd(k, word[u], info, litn, lim,
+                                                 (info & I_TEV) ? s.rc_sk[2 * g] + zp : 0,
+                                                 (info & I_NEV) ? s.rc_sk[2 * g + 1] + zp : 0, nd);
+            nupd += __popc(__vcmpne4(nw, word[u]) & 0x01010101u);
+            const uint32_t nib = quad_include_nibble(nw, lim);
             if (nw != word[u]) {
                 int8_t *grow = k.states + (int64_t)c * k.P;
                 if (k.vec4 && p0 + 4 <= k.P) {
@@ -1239,7 +1219,10 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
             // feedback done: the next step waits on it
             grid_arrive_step(&k.gsync[i * 2 + 1]);
         } else {
-            feedback_quads<SMEM_STATES>(k, s, c0, lit, (k.dbg & 1) ? 0 : s.misc[0], cn);
+            // shared-memory states: the byte-SIMD body; HBM states keep the
+            // 4-word-in-flight body (its loads go to L2 / HBM)
+            if (SMEM_STATES) feedback_simd<true>(k, s, c0, lit, (k.dbg & 1) ? 0 : s.misc[0], cn);
+            else feedback_quads<false>(k, s, c0, lit, (k.dbg & 1) ? 0 : s.misc[0], cn);
             prefetch_commit(k, s, i, pf);
             __syncthreads();
         }
@@ -1687,7 +1670,8 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_fast(TrainK k) {
         //    the correction of its class sums)
         const int n_work = (k.dbg & 1) ? 0 : s.misc[0];
         if (n_work > 0) {
-            feedback_quads<SMEM_STATES>(k, s, c0, lit, n_work, cn);
+            if (SMEM_STATES) feedback_simd<true>(k, s, c0, lit, n_work, cn);
+            else feedback_quads<false>(k, s, c0, lit, n_work, cn);
             __syncthreads();
             PHASEF(5);
             if (more) {
@@ -1762,14 +1746,15 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_fast(TrainK k) {
 // is published from the kept sums corrected by the work-list clauses alone.
 // The result is bit-identical to the sequential loop (executor.py:275-340):
 // every applied step sees exactly the states the steps before it produced.
-constexpr int kSpecEnt = 64;  // flag entries per stream staged with each head
-__host__ __device__ inline int spec_hsz(const TrainK &k) { return 4 + k.Wp + 260 + 2 * kSpecEnt; }
+// flag entries per stream staged with each head: k.spec_ent (the largest of
+// 256, 224, ... 64 that fits next to everything else)
+__host__ __device__ inline int spec_hsz(const TrainK &k) { return 4 + k.Wp + 260 + 2 * k.spec_ent; }
 
 __device__ __forceinline__ int spec_wrap(int x, int HR) { return x >= HR ? x - HR : x; }
 
 // Stage the heads of cnt <= HR steps from step `from` (ring slot fslot) --
 // example, label, negative class, literal row, bucket starts and the first
-// kSpecEnt flag entries of each stream -- one warp per step (warps wrel,
+// k.spec_ent flag entries of each stream -- one warp per step (warps wrel,
 // wrel + nw, ...), 16-B cp.async units over the lanes.  k.dbg & 64 also
 // prefetches the step's remaining flag entries into L2 (this CTA takes the
 // 128-B lines l = rank - i mod n_cta).
@@ -1777,7 +1762,7 @@ __device__ __forceinline__ void spec_issue(const TrainK &k, const Smem &s, int64
                                            int cnt, int wrel, int nw) {
     const int lane = threadIdx.x & 31;
     const int nh = (4 + k.Wp + 260) / 4;
-    const int ne = min(kSpecEnt, k.Cp) / 4;
+    const int ne = min(k.spec_ent, k.Cp) / 4;
     const int per = nh + 2 * ne;
     const int HR = 3 * k.spec, HSZ = spec_hsz(k);
     for (int st = wrel; st < cnt; st += nw) {
@@ -1789,7 +1774,7 @@ __device__ __forceinline__ void spec_issue(const TrainK &k, const Smem &s, int64
                 cp_async16(dst + 4 * q, src + 4 * q);
             } else {
                 const int r = q - nh, str = r >= ne ? 1 : 0, e = r - str * ne;
-                cp_async16(dst + 4 * nh + str * kSpecEnt + 4 * e, src + rec_entries(k) + str * k.Cp + 4 * e);
+                cp_async16(dst + 4 * nh + str * k.spec_ent + 4 * e, src + rec_entries(k) + str * k.Cp + 4 * e);
             }
         }
         if ((k.dbg & 64) && lane == 0 && (int)(i % k.n_cta) == (int)blockIdx.x) {
@@ -1954,9 +1939,10 @@ __device__ __forceinline__ int mine_lane(int lane, int kk) { return lane < 2 * k
 // after wn's non-empty step, [1] %globaltimer at wn's poll completion, then
 // clock64 at [2] poll completion, [3] events done, [4] feedback done, [5]
 // publication, [6] work-list length, [7] flag entries of the step, [8]
-// clock64 after the decision barrier, [9] after the preparation barrier; stored
+// clock64 after the decision barrier, [9] after the preparation barrier,
+// [10] after its warm repetition (profiling build only); stored
 // after the counters as [n_cta][kSpecTlN][kSpecTlQ].
-constexpr int kSpecTl0 = 2000, kSpecTlN = 2048, kSpecTlQ = 10;
+constexpr int kSpecTl0 = 2000, kSpecTlN = 2048, kSpecTlQ = 11;
 #define SPEC_TL(wn_, q_, v_)                                                                          \
     do {                                                                                              \
         if (PROF && (wn_) >= kSpecTl0 && (wn_) < kSpecTl0 + kSpecTlN)                                  \
@@ -1985,8 +1971,9 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
 
     load_slice<SMEM_STATES>(k, s, c0, cown);
+    uint32_t *thr32 = reinterpret_cast<uint32_t *>(s.thr_tab);
     if (k.thr_smem)
-        for (int64_t a = tid; a <= 2 * k.T; a += nthr) s.thr_tab[a] = k.thr_tab[a];
+        for (int64_t a = tid; a <= 2 * k.T; a += nthr) thr32[a] = k.thr32[a];
     if (tid == 0) {
         s.blk_ctr[0] = k.block_counters[0];
         s.blk_seed[0] = k.block_seeds[0];
@@ -2058,8 +2045,14 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
             }
             const unsigned busy = __ballot_sync(0xffffffffu, a != 0);
             const int first = busy ? (__ffs(busy) - 1) >> 1 : kk;
-            if (mine && (lane >> 1) == first)
-                s.thr[lane & 1] = dec_tab ? s.thr_tab[a] : threshold_of(a, dec_2T >> 1);
+            // the first non-empty step: its bucket (thresholds >> 37) from
+            // the 32-bit table, a for the exact threshold on a key tie
+            if (mine && (lane >> 1) == first) {
+                s.thr[lane & 1] = (uint64_t)a;
+                s.thr[2 + (lane & 1)] = a == dec_2T ? 65536u
+                                        : dec_tab   ? (uint64_t)(thr32[a] >> 16)
+                                                    : threshold_of(a, dec_2T >> 1) >> 37;
+            }
             if (lane == 0) s.misc[1] = first;
             if (k.trace && rank == 0 && mine && (lane >> 1) <= first) {
                 const int64_t i = i0 + (lane >> 1);
@@ -2107,29 +2100,28 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
         const uint32_t *lit = rc + 4;
         const int label = (int)rc[1], neg = (int)rc[2];
         const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
-        const uint64_t tt = s.thr[0], tn = s.thr[1];
-        {
+        const long long at = (long long)s.thr[0], an = (long long)s.thr[1];
+        const unsigned tbt = (unsigned)s.thr[2], tbn = (unsigned)s.thr[3];
+        int hi_t = 0, hi_n = 0;
+        // (the profiling build runs this block twice: cold vs warm code)
+        for (int rep = 0; rep < (PROF ? 2 : 1); ++rep) {
             const uint32_t *ob = s.obs + si * CW;
             for (int j = tid; j < cown; j += nthr) s.info[j] = ((ob[j >> 5] >> (j & 31)) & 1u) ? I_OUT : 0;
-        }
-        const unsigned tbt = (unsigned)(tt >> 37), tbn = (unsigned)(tn >> 37);
-        int hi_t, hi_n;
-        {
             const uint16_t *off = reinterpret_cast<const uint16_t *>(rc + 4 + k.Wp);
             hi_t = tbt >= 65536u ? C : off[(tbt >> 8) + 1];
             hi_n = tbn >= 65536u ? C : off[260 + (tbn >> 8) + 1];
+            __syncthreads();  // info[] written
+            if (tid == 0) SPEC_TL(wn, rep ? 10 : 9, clock64());
         }
-        const bool staged = hi_t <= kSpecEnt && hi_n <= kSpecEnt;
+        const bool staged = hi_t <= k.spec_ent && hi_n <= k.spec_ent;
         if (PROF && tid == 0) {
             ph[10] += (hi_t + hi_n > 64) ? 1 : 0;
             ph[11] += staged ? 1 : 0;
         }
         const uint32_t *ent = staged ? rc + 4 + k.Wp + 260 : k.recs + i * (int64_t)k.R + rec_entries(k);
-        const int estr = staged ? kSpecEnt : k.Cp;
+        const int estr = staged ? k.spec_ent : k.Cp;
         const int ne = hi_t + hi_n;
-        __syncthreads();  // info[] written
         SPH(2);
-        if (tid == 0) SPEC_TL(wn, 9, clock64());
         auto count_entries = [&](int t0, int nt, unsigned &pre, unsigned &tot) {
             for (int e = t0; e < ne; e += nt) {
                 const int str = e >= hi_t ? 1 : 0;
@@ -2137,8 +2129,9 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
                 const unsigned key = v >> 16, c = v & 0xFFFFu;
                 const unsigned tb = str ? tbn : tbt;
                 bool q = key < tb;
-                if (key == tb)
-                    q = draw53(k.fb_seed, fbc + 1 + (str ? (uint64_t)C : 0) + c) < (str ? tn : tt);
+                if (key == tb)  // a tie on the 16-bit key: the exact draw and threshold
+                    q = draw53(k.fb_seed, fbc + 1 + (str ? (uint64_t)C : 0) + c) <
+                        threshold_of(str ? an : at, k.T);
                 if (q) {
                     ++tot;
                     pre += c < (unsigned)c0 ? 1u : 0u;
@@ -2483,6 +2476,10 @@ int g_train_dbg = 0;            // tmb_set_option("train.debug_skip"): timing ab
 // tmb_set_option("train.spec_window"): examples per speculative window of the
 // fast grid trainer (k_train_spec, 1..16), 0 = k_train_fast; read at create
 int g_train_spec = 16;
+// tmb_set_option("train.spec_entries"): flag entries staged per step head,
+// 0 = as many as fit (256 measured no faster than 64: the entry loads are
+// not what the non-empty path waits on)
+int g_train_spec_ent = 64;
 }
 
 namespace {
@@ -2540,6 +2537,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     // (window evaluation holds two literal words per lane: rows of <= 64 words)
     k.spec = (k.fast && W <= 64) ? std::max(0, std::min(16, g_train_spec)) : 0;
     k.MW = k.spec ? k.Wp : W;
+    k.spec_ent = 64;
     k.gbal = (!cluster && !(c.flags & 4)) ? 1 : 0;  // used by the generic grid kernel, HBM states
     if (cluster && k.cmax > 32 * 1024)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: too many clauses per CTA");
@@ -2565,6 +2563,22 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
         const size_t with_tab = smem_layout(k, smem_states, MODE_GRID, nullptr, nullptr);
         if (with_tab <= (size_t)max_smem) need = with_tab;
         else k.thr_smem = 0;
+    }
+    // k_train_spec: stage as many flag entries per step head as fit
+    // (tmb_set_option("train.spec_entries") fixes the count for A/B runs)
+    if (k.spec && need <= (size_t)max_smem) {
+        const int want[] = {256, 224, 192, 160, 128, 96, 64};
+        for (int e : want) {
+            if (g_train_spec_ent > 0 && e != g_train_spec_ent) continue;
+            k.spec_ent = e;
+            const size_t n2 = smem_layout(k, smem_states, MODE_GRID, nullptr, nullptr);
+            if (n2 <= (size_t)max_smem) {
+                need = n2;
+                break;
+            }
+            k.spec_ent = 64;
+        }
+        need = smem_layout(k, smem_states, MODE_GRID, nullptr, nullptr);
     }
     if (need > (size_t)max_smem)
         return fail(TMB_E_UNSUPPORTED,
@@ -2629,13 +2643,22 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     if (k.thr_smem || (t->warp && c.threshold <= (1 << 20))) {
         std::vector<uint64_t> tab((size_t)(2 * c.threshold + 1));
         for (int64_t a = 0; a <= 2 * c.threshold; ++a) tab[a] = threshold_of(a, c.threshold);
-        if ((rc = check_cuda(cudaMalloc(&t->thr_d, 8 * tab.size()), "cudaMalloc")) ||
+        // k_train_spec: 32-bit entries (threshold >> 21; a == 2T is p == 1)
+        std::vector<uint32_t> tab32(tab.size());
+        for (size_t a = 0; a < tab.size(); ++a)
+            tab32[a] = (uint32_t)std::min<uint64_t>(tab[a] >> 21, 0xFFFFFFFFull);
+        if ((rc = check_cuda(cudaMalloc(&t->thr_d, 12 * tab.size()), "cudaMalloc")) ||
             (rc = check_cuda(cudaMemcpy(t->thr_d, tab.data(), 8 * tab.size(),
-                                        cudaMemcpyHostToDevice), "cudaMemcpy"))) {
+                                        cudaMemcpyHostToDevice), "cudaMemcpy")) ||
+            (rc = check_cuda(cudaMemcpy(reinterpret_cast<char *>(t->thr_d) + 8 * tab.size(),
+                                        tab32.data(), 4 * tab.size(), cudaMemcpyHostToDevice),
+                             "cudaMemcpy"))) {
             tmb_trainer_destroy(t);
             return rc;
         }
         k.thr_tab = t->thr_d;
+        k.thr32 = reinterpret_cast<const uint32_t *>(reinterpret_cast<char *>(t->thr_d) +
+                                                     8 * tab.size());
     }
 
     k.states = states; k.weights = weights; k.block_counters = block_counters;

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--epochs", type=int, default=3)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--dbg", type=int, default=0, help="train.debug_skip bits (timing ablations)")
+    ap.add_argument("--ents", type=int, default=64, help="train.spec_entries (0 = auto)")
     ap.add_argument("--prof", action="store_true",
                     help="k_train_spec phase counters (clock64 per CTA, see tmb_train.cu)")
     args = ap.parse_args()
@@ -37,6 +38,7 @@ def main():
     ref = None
     out = []
     _lib.call("tmb_set_option", b"train.debug_skip", args.dbg)
+    _lib.call("tmb_set_option", b"train.spec_entries", args.ents)
     for wsz in args.windows:
         _lib.call("tmb_set_option", b"train.spec_window", wsz)
         sess = tmb.DenseTrainSession(cfg, tx, ty, threads=args.threads,
@@ -48,7 +50,7 @@ def main():
         prof = None
         if args.prof and wsz > 0:
             ncta = sess.launch["n_cta"]
-            prof = torch.zeros(ncta * 16 + ncta * 2048 * 10, dtype=torch.int64, device="cuda")
+            prof = torch.zeros(ncta * 16 + ncta * 2048 * 11, dtype=torch.int64, device="cuda")
             _lib.call("tmb_trainer_set_profile", sess._h, prof.data_ptr())
 
         def reset():
@@ -70,7 +72,7 @@ def main():
             if prof is not None:
                 allp = prof.cpu().numpy()
                 p = allp[:ncta * 16].reshape(-1, 16).astype(np.float64)
-                tl = allp[ncta * 16:].reshape(ncta, 2048, 10).astype(np.float64)
+                tl = allp[ncta * 16:].reshape(ncta, 2048, 11).astype(np.float64)
                 heavy = (tl[:, :, 0] > 0).all(axis=0) & (tl[:, :, 1] > 0).all(axis=0)
                 polled = (tl[:, :, 1] > 0).all(axis=0)
                 h = tl[:, heavy, :]
@@ -102,7 +104,8 @@ def main():
                     pub_skew_ns=med(h[:, :, 0].max(axis=0) - np.median(h[:, :, 0], axis=0)),
                     decide_ns=med(np.median((h[:, :, 8] - h[:, :, 2]) / cyc, axis=0)),
                     prep_ns=med(np.median((h[:, :, 9] - h[:, :, 8]) / cyc, axis=0)),
-                    count_own_ns=med(np.median((h[:, :, 3] - h[:, :, 9]) / cyc, axis=0)),
+                    prep_warm_ns=med(np.median((h[:, :, 10] - h[:, :, 9]) / cyc, axis=0)),
+                    count_own_ns=med(np.median((h[:, :, 3] - h[:, :, 10]) / cyc, axis=0)),
                     fb_ns_by_nwork=fb_by_nwork,
                     nwork_max_cta=np.percentile(nw_max, [10, 50, 90]).tolist(),
                     nwork_mean_cta=float(nw.mean()),
@@ -137,6 +140,7 @@ def main():
         print(json.dumps(rec), flush=True)
         del sess
     _lib.call("tmb_set_option", b"train.spec_window", 16)
+    _lib.call("tmb_set_option", b"train.spec_entries", 64)
 
 
 if __name__ == "__main__":
