@@ -96,6 +96,13 @@ int tmb_microbench_sparse_event(int which, int n, int n_act, int reps, int n_cta
 int tmb_microbench_feedback(int variant, int n_work, int two_events, int threads, int iters,
                             double *cycles_per_call);
 
+/* Instruction-fetch microbenchmark (design evidence): one
+ * CTA of `warps` warps loops a straight-line block of `kbytes` KB of
+ * independent IADDs `iters` times; *cycles_per_instr = SM cycles per
+ * instruction of one warp's stream (kbytes: 8, 16, 32, 64, 96, 128, 192,
+ * 256). */
+int tmb_microbench_icache(int kbytes, int warps, int iters, double *cycles_per_instr);
+
 /* ----------------------------------------------------- RNG (core.py) -- */
 /* core.py:66-95 on the host; used by the host driver and tests. */
 uint64_t tmb_derive_stream(uint64_t seed, uint64_t index);

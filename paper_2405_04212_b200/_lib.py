@@ -61,6 +61,7 @@ SIGNATURES = {
     "tmb_microbench_allreduce": (i32, [i32, i32, i32, i32, vp]),
     "tmb_microbench_sparse_event": (i32, [i32, i32, i32, i32, i32, i32, vp]),
     "tmb_microbench_feedback": (i32, [i32, i32, i32, i32, i32, vp]),
+    "tmb_microbench_icache": (i32, [i32, i32, i32, vp]),
     "tmb_microbench_pipe": (i32, [i32, i32, i32, i32, vp, vp]),
     "tmb_microbench_pingpong": (i32, [i32, i32, vp, vp]),
     "tmb_derive_stream": (u64, [u64, u64]),

@@ -381,3 +381,62 @@ extern "C" int tmb_microbench_pingpong(int mode, int hops, double *ns_per_hop,
     cudaEventDestroy(b);
     return rc;
 }
+
+// ------------------------------------------------ instruction fetch --
+// Straight-line blocks of N independent IADDs (16 B of SASS each, 8
+// rotating registers so the chain never stalls) looped `iters` times by
+// `warps` warps of one CTA: cycles per instruction show where the block
+// stops fitting the instruction caches and what a refetch costs.
+namespace tmb {
+template <int N>
+__global__ void __launch_bounds__(1024, 1) k_mb_icache(int iters, unsigned long long *out) {
+    unsigned r0 = threadIdx.x, r1 = r0 + 1, r2 = r0 + 2, r3 = r0 + 3, r4 = r0 + 4, r5 = r0 + 5,
+             r6 = r0 + 6, r7 = r0 + 7;
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < N / 8; ++i) {
+            // register-only xor / add ring: nothing for ptxas to fold
+            asm volatile(
+                "xor.b32 %0, %0, %1;\n\tadd.u32 %1, %1, %2;\n\txor.b32 %2, %2, %3;\n\tadd.u32 %3, %3, %4;\n\t"
+                "xor.b32 %4, %4, %5;\n\tadd.u32 %5, %5, %6;\n\txor.b32 %6, %6, %7;\n\tadd.u32 %7, %7, %0;"
+                : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3), "+r"(r4), "+r"(r5), "+r"(r6), "+r"(r7));
+        }
+    }
+    __syncthreads();
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
+    if ((r0 ^ r1 ^ r2 ^ r3 ^ r4 ^ r5 ^ r6 ^ r7) == 0xFFFFFFFFu) out[1] = 1;  // keep the chains
+}
+}  // namespace tmb
+
+extern "C" int tmb_microbench_icache(int kbytes, int warps, int iters, double *cycles_per_instr) {
+    using namespace tmb;
+    int rc = require_device();
+    if (rc) return rc;
+    const void *fn = nullptr;
+    int n = 0;
+    switch (kbytes) {
+        case 8: fn = (const void *)k_mb_icache<512>; n = 512; break;
+        case 16: fn = (const void *)k_mb_icache<1024>; n = 1024; break;
+        case 32: fn = (const void *)k_mb_icache<2048>; n = 2048; break;
+        case 64: fn = (const void *)k_mb_icache<4096>; n = 4096; break;
+        case 96: fn = (const void *)k_mb_icache<6144>; n = 6144; break;
+        case 128: fn = (const void *)k_mb_icache<8192>; n = 8192; break;
+        case 192: fn = (const void *)k_mb_icache<12288>; n = 12288; break;
+        case 256: fn = (const void *)k_mb_icache<16384>; n = 16384; break;
+        default: return fail(TMB_E_INVALID, "microbench_icache: kbytes in 8,16,32,64,96,128,192,256");
+    }
+    if (warps < 1 || warps > 32 || iters < 1 || !cycles_per_instr)
+        return fail(TMB_E_INVALID, "microbench_icache: bad arguments");
+    unsigned long long *out = nullptr;
+    TMB_CUDA(cudaMalloc(&out, 16));
+    void *args[] = {&iters, &out};
+    rc = check_cuda(cudaLaunchKernel(fn, dim3(1), dim3(32 * warps), args, 0, 0), "icache launch");
+    unsigned long long c = 0;
+    if (!rc) rc = check_cuda(cudaMemcpy(&c, out, 8, cudaMemcpyDeviceToHost), "copy");
+    cudaFree(out);
+    if (!rc) *cycles_per_instr = (double)c / ((double)iters * n);
+    return rc;
+}
