@@ -531,8 +531,15 @@ def bench_c1_train(args, rank, world, local):
     value = n_ex * world / (ms / 1e3)
     us_step = ms * 1e3 / n_ex
     accs = []
+    draws = sum(sess.stats_dict()["draws"] for sess, _ in preps)
     for sess, _ in preps:
         accs.append(tmb.evaluate(sess.model(), (ex, ey)))
+    draws_ex = draws / n_ex
+    lp = live_peaks()
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    # one warp issues on one of the SM's four schedulers: its share of the
+    # measured per-SM SplitMix64 draw rate is the integer peak it can reach
+    warp_draw_peak = lp["draw_peak_per_s"] / sm_count / 4
     # e2e through the public train() (per-epoch evaluation included, as the
     # reference's train(eval_data=...) does)
     barrier(world)
@@ -559,11 +566,16 @@ def bench_c1_train(args, rank, world, local):
                          "flush that the workload re-reads"},
         "gpu_launches": int(launches),
         "accuracy": {"test_accuracy_per_step": accs, "mean": float(np.mean(accs))},
-        "roofline": {"kernel": "k_train (cluster mode, one CTA)", "bound": "latency",
+        "roofline": {"kernel": preps[0][0].launch.get("kernel", "k_train_warp"),
+                     "bound": "latency (one warp: the per-example chain eval -> class sums "
+                              "-> decision -> feedback; no parallelism across examples)",
                      "achieved": 1e6 / us_step, "unit": "examples/s",
-                     "note": "single-CTA sequential steps: the per-example dependency chain "
-                             "(eval -> class sums -> decision -> feedback) is barrier/latency "
-                             "bound; see DESIGN.md"},
+                     "peak": warp_draw_peak / max(draws_ex, 1e-9),
+                     "frac": (1e6 / us_step) * draws_ex / warp_draw_peak,
+                     "draws_per_example": draws_ex,
+                     "peak_note": "the reference draws of one example at one warp's share "
+                                  "(one scheduler) of the measured per-SM SplitMix64 draw rate",
+                     "peak_source": lp["source"]},
         "clocks": clk.summary(),
         "e2e": {"value": n_ex * world / e2e_s, "unit": "examples/s",
                 "h2d_bytes_per_step": int(tx.nbytes + ex.nbytes + 4 * N),
@@ -1010,6 +1022,7 @@ def bench_c4_sweep(args, rank, world, local):
     n_total = len(grid) * step_n * args.steps
     value = n_total / (ms / 1e3)
     ev = sum(job[2].stats_dict()["events"] - s0["events"] for job, s0 in zip(jobs, stats0))
+    sweep_draws = sum(job[2].stats_dict()["draws"] - s0["draws"] for job, s0 in zip(jobs, stats0))
     n_mine = len(jobs) * step_n * args.steps
     # the sweep's result: test accuracy of every grid point (gathered)
     acc_mine = {job[0]: tmb.evaluate(job[2].model(), (ex, ey)) for job in jobs}
@@ -1064,8 +1077,15 @@ def bench_c4_sweep(args, rank, world, local):
                                            for j in sorted(acc)},
                          "note": f"after {args.warmup + args.steps} steps of {step_n} "
                                  "examples per job"},
-        "roofline": {"kernel": "k_train<1, false> (grid mode, HBM-resident states)",
-                     "bound": "hbm", "note": "see the c4-train line: same kernel"},
+        "roofline": {"kernel": "k_train<1, false> (grid mode, HBM-resident states, "
+                               "grid-balanced byte-SIMD feedback)",
+                     "bound": "int (SplitMix64 draws at the measured per-SM rate)",
+                     "achieved": sweep_draws / (ms / 1e3) / 1e9,
+                     "peak": live_peaks()["draw_peak_per_s"] / 1e9, "unit": "G draws/s",
+                     "frac": sweep_draws / (ms / 1e3) / live_peaks()["draw_peak_per_s"],
+                     "draws_per_example_rank0": sweep_draws / max(n_mine, 1),
+                     "peak_source": live_peaks()["source"],
+                     "note": "the c4-train kernel; draws of rank 0's jobs over its timed region"},
         "clocks": clk.summary(),
         "e2e": {"value": n_total / (e2e_ms / 1e3), "unit": "examples/s",
                 "h2d_bytes_per_step": int(len(jobs) * tx.nbytes),
@@ -1247,6 +1267,11 @@ def bench_c5_sparse(args, rank, world, local):
                  "draws_per_document": dd["draws"] / max(dd["examples"], 1)},
         "roofline": {"kernel": "k_sparse_train", "bound": "latency",
                      "achieved": value / world, "unit": "documents/s",
+                     "peak": 1e9 / live_peaks()["l2_hop_ns"],
+                     "frac": (value / world) * live_peaks()["l2_hop_ns"] / 1e9,
+                     "floor": "one cross-SM L2 hop per document (every document is non-empty: "
+                              "~1 100 applied events each, so no window of documents can be "
+                              "decided together), measured live by tmb_microbench_pingpong",
                      "traffic": tr_tr, "traffic_source": tr_tr_src,
                      "hbm_gbs": csr_bytes * value / world / 1e9,
                      "hbm_frac": csr_bytes * value / world / 1e9 / HBM_PEAK,
@@ -1272,7 +1297,10 @@ def bench_c5_sparse(args, rank, world, local):
                               "path": "this rank's pinned host CSR shard -> H2D -> "
                                       "tmb_sparse_infer -> host predictions"},
                       "ms_per_step": inf_ms / args.steps, "accuracy_after_train": acc,
-                      "roofline": {"kernel": "k_sparse_infer (inverted index)", "bound": "hbm",
+                      "roofline": {"kernel": "k_sparse_infer (inverted index)",
+                                   "bound": "hbm (nominal; the binding cost is the postings' "
+                                            "gathers from the L2-resident index and the "
+                                            "per-warp shared counters, DESIGN.md 5.4)",
                                    "achieved": n_loc * (csr_bytes + 8) / (per_launch_inf_ms / 1e3)
                                    / 1e9,
                                    "peak": HBM_PEAK, "unit": "GB/s",
