@@ -1668,6 +1668,8 @@ def main():
     ap.add_argument("--train-cta", type=int, default=0, help="0 = auto")
     ap.add_argument("--train-threads", type=int, default=0, help="0 = auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--set-option", action="append", default=[], metavar="NAME=INT",
+                    help="tmb_set_option before the workload (A/B runs)")
     ap.add_argument("--ref-port", action="store_true",
                     help="reference arm: time the oracle port even when baseline/_ref exists")
     args = ap.parse_args()
@@ -1684,6 +1686,9 @@ def main():
     rank, world, local = dist_init()
     import paper_2405_04212_b200 as tmb
     tmb.runtime.require_device()
+    for opt in args.set_option:
+        name, val = opt.split("=")
+        tmb._lib.call("tmb_set_option", name.encode(), int(val))
     if args.workload == "c3-infer":
         line = bench_c3_infer(args, rank, world, local)
         line.update({"higher_is_better": True, "scaling": "weak", "vs_baseline": None,

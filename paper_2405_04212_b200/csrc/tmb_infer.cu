@@ -1610,6 +1610,11 @@ int tmb_set_option(const char *name, int64_t value) {
         g_train_spec = (int)value;                   // (applies to trainers created afterwards)
         return TMB_OK;
     }
+    if (std::string(name) == "train.hbm_threads") {  // 512 | 1024 (applies at create)
+        if (value != 512 && value != 1024) return fail(TMB_E_INVALID, "set_option: train.hbm_threads must be 512 or 1024");
+        g_train_hbm_threads = (int)value;
+        return TMB_OK;
+    }
     if (std::string(name) == "train.spec_entries") {  // 0 auto, else 64..256 (multiple of 32; default 64)
         g_train_spec_ent = (int)value;
         return TMB_OK;

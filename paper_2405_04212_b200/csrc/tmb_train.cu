@@ -598,12 +598,12 @@ __device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, in
 // warp's 32 quads lie in one row).  rc_*[g - g_lo] hold the work items.
 // Same per-position arithmetic as feedback_quads; the rebuilt include-mask
 // words go to k.gmask for the owners to pull.
+template <int B>  // state words in flight per thread
 __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Smem &s,
                                                       const uint32_t *lit, int64_t q_begin,
                                                       int64_t q_end, int64_t g_lo, Counters &cn) {
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int QP = k.Ppad >> 2;
-    constexpr int B = 4;
     unsigned nd = 0, nupd = 0;
     // quad it = (work item g_lo + gnext, quad rem) advanced by nthr per unit
     // without a division (nthr < QP is not assumed: a short loop)
@@ -915,8 +915,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     } while (0)
 
 // One fused kernel, two synchronisation domains (see the header comment).
-template <int MODE, bool SMEM_STATES>
-__global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
+// NT: the CTA size the build is bounded for (1024: the HBM-state grid
+// kernel with twice the warps to hide its feedback's dependency latency)
+template <int MODE, bool SMEM_STATES, int NT = 512>
+__global__ void __launch_bounds__(NT, 1) k_train(TrainK k) {
     extern __shared__ __align__(16) char smem_raw[];
     Smem s;
     smem_layout(k, SMEM_STATES, MODE, smem_raw, &s);
@@ -1213,7 +1215,8 @@ __global__ void __launch_bounds__(512, 1) k_train(TrainK k) {
                 s.rc_sk[2 * t + 1] = __ldcg(&k.gw_sk[2 * o + 1]);
             }
             __syncthreads();
-            if (!(k.dbg & 1)) feedback_quads_global(k, s, lit, q_begin, q_end, g_lo, cn);
+            if (!(k.dbg & 1))  // 1024 threads: half the words in flight per thread
+                feedback_quads_global<(NT > 512 ? 2 : 4)>(k, s, lit, q_begin, q_end, g_lo, cn);
             prefetch_commit(k, s, i, pf);
             __syncthreads();
             // feedback done: the next step waits on it
@@ -2448,7 +2451,8 @@ void per_cta_maxima(TrainK &k) {
     k.bmax = bmax;
 }
 
-const void *kernel_for(bool cluster, bool smem_states, bool fast, bool prof = false, bool spec = false) {
+const void *kernel_for(bool cluster, bool smem_states, bool fast, bool prof = false, bool spec = false,
+                       int threads = 512) {
     if (fast && spec)
         return prof ? (smem_states ? (const void *)k_train_spec<true, true>
                                    : (const void *)k_train_spec<false, true>)
@@ -2462,6 +2466,7 @@ const void *kernel_for(bool cluster, bool smem_states, bool fast, bool prof = fa
                                    : (const void *)k_train_fast<false, true>)
                     : (smem_states ? (const void *)k_train_fast<true, false>
                                    : (const void *)k_train_fast<false, false>);
+    if (!smem_states && threads > 512) return (const void *)k_train<MODE_GRID, false, 1024>;
     return smem_states ? (const void *)k_train<MODE_GRID, true> : (const void *)k_train<MODE_GRID, false>;
 }
 
@@ -2480,6 +2485,10 @@ int g_train_spec = 16;
 // 0 = as many as fit (256 measured no faster than 64: the entry loads are
 // not what the non-empty path waits on)
 int g_train_spec_ent = 64;
+// tmb_set_option("train.hbm_threads"): CTA size of the HBM-state generic
+// grid trainer when the caller leaves it to the library (512 | 1024, read at
+// create); 1024 measured 9% faster on configs[3] (2.44 -> 2.65 k ex/s)
+int g_train_hbm_threads = 1024;
 }
 
 namespace {
@@ -2513,6 +2522,7 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
     const bool cluster = n_cta <= 16;
     if (!cluster && n_cta >= 256)
         return fail(TMB_E_UNSUPPORTED, "trainer_create: grid mode supports < 256 CTAs");
+    const bool auto_threads = threads <= 0;
     if (threads <= 0) threads = (n_cta == 1 && work <= 16384) ? 256 : 512;
     threads = std::max(64, std::min(std::max(512, kFastMaxThreads), threads / 32 * 32));
     if (threads > 512 && !(!cluster && c.n_blocks == 1 && !(c.flags & 2) && C <= 65535))
@@ -2584,7 +2594,11 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
         return fail(TMB_E_UNSUPPORTED,
                     "trainer_create: per-CTA include masks exceed shared memory (" +
                         std::to_string(need) + " B); use more CTAs");
-    const void *fn = kernel_for(cluster, smem_states, k.fast, false, k.spec != 0);
+    // HBM-resident states on the generic grid kernel: optionally 1024 threads
+    // (tmb_set_option("train.hbm_threads")), twice the warps to hide latency
+    if (auto_threads && !smem_states && !cluster && !k.fast && g_train_hbm_threads > 512)
+        threads = 1024;
+    const void *fn = kernel_for(cluster, smem_states, k.fast, false, k.spec != 0, threads);
     if (k.fast && 2 * C > 48 * 1024)
         TMB_CUDA(cudaFuncSetAttribute((const void *)k_step_records,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * C));
@@ -2751,7 +2765,8 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
         TMB_LAUNCHED();
         return TMB_OK;
     }
-    const void *fn = kernel_for(t->cluster, t->smem_states, k.fast, k.phase != nullptr, k.spec != 0);
+    const void *fn = kernel_for(t->cluster, t->smem_states, k.fast, k.phase != nullptr, k.spec != 0,
+                                t->threads);
     // the dynamic shared-memory limit is a per-function attribute: another
     // trainer of a different shape may have lowered it since create
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t->smem));

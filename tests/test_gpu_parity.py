@@ -860,3 +860,28 @@ def test_speculative_windows_vs_oracle(gpu, oracle, window, n_cta, n_train):
         gpu._lib.call("tmb_set_option", b"train.spec_window", 16)
     assert np.array_equal(got[window], got[0])
     assert got[0][:, :, 3].sum() > 0  # the run has events
+
+
+@pytest.mark.parametrize("n_blocks,keys", [(5, True), (1, False), (3, False)])
+def test_hbm_state_trainer_1024_threads_vs_oracle(gpu, oracle, n_blocks, keys):
+    """The HBM-state generic grid trainer built for 1024-thread CTAs
+    (train.hbm_threads=1024: twice the warps, two state words in flight per
+    thread, grid-balanced SIMD feedback) against the oracle (one block with
+    16-bit flag keys takes the fast trainers instead)."""
+    (tx, ty), _ = gpu.datasets.mnist_shaped(n_train=800, n_test=10, data_seed=8)
+    kw = gpu.datasets.mnist_shaped_config_kwargs(seed=12)
+    kw["n_blocks"] = n_blocks
+    cfg = gpu.Config(**kw)
+    try:
+        gpu._lib.call("tmb_set_option", b"train.hbm_threads", 1024)
+        sess = gpu.DenseTrainSession(cfg, tx, ty, states_in_hbm=True, flag_keys=keys)
+        assert sess.launch["threads"] == 1024 and not sess.launch["states_in_smem"]
+        for _ in range(2):
+            sess.run_epoch()
+        m = sess.model()
+    finally:
+        gpu._lib.call("tmb_set_option", b"train.hbm_threads", 1024)
+    ost, _ = oracle.train(cfg, tx, ty, 2)
+    assert np.array_equal(m.states, ost.states)
+    assert np.array_equal(m.weights, ost.weights)
+    assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64), ost.block_counters)
