@@ -513,7 +513,8 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
     const bool prof = k.phase != nullptr;
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    // profile slots: 0-5 phases (thread 0), 6 Type I (output 0) / 7 Type II /
+    // profile slots: 0-5 phases (thread 0; 15: the part of phase 0 up to the
+    // next document's prefetch issue), 6 Type I (output 0) / 7 Type II /
     // 8 Type I (output 1) event cycles summed over warps, 9 output-1 Type I
     // events, 10 sum over steps of the slowest warp's event cycles
     unsigned long long ev_clk[4] = {0, 0, 0, 0};
@@ -579,6 +580,10 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                 nm2 = __ldg(&k.labels[ex2]);
             }
             if (it + 3 < k.n_steps) nx3 = __ldg(&k.order[it + 3]);
+        }
+        if (prof && tid == 0) {  // loop top up to here (prefetch issue) -> slot 15
+            const long long now = clock64();
+            ph[6] += (unsigned long long)(now - t_mark);
         }
         const uint64_t fbc = k.fb_counter0 + (uint64_t)it * step_draws;
         int label, neg;
@@ -866,6 +871,7 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
     {
         for (int q = 0; q < 6; ++q) k.phase[rank * 16 + q] = ph[q];
         k.phase[rank * 16 + 10] = crit;
+        k.phase[rank * 16 + 15] = ph[6];
     }
     if (RES) {  // resident lists back to their global buffers (k.cur unchanged)
         for (int j = warp; j < cown; j += nwarps) {

@@ -45,4 +45,5 @@ print(f"  Type I out=1  {tot[:, 8].sum() / max(n1, 1):.3f} us/event  ({n1 / n:.1
 print(f"  Type II       {tot[:, 7].sum() / max(dd['type_ii'], 1):.3f} us/event  ({dd['type_ii'] / n:.1f} per doc)")
 print(f"  slowest warp's events per step: mean over CTAs {p[:, 10].mean():.3f}  max {p[:, 10].max():.3f} us/doc")
 nii = max(dd['type_ii'], 1)
+print(f"  loop top up to the prefetch issue: mean {p[:, 15].mean():.3f} us/doc")
 print(f"  Type II: cand rounds {raw[:, 11].sum() / nii:.2f}  stored n {raw[:, 12].sum() / nii:.1f}  ins {raw[:, 13].sum() / nii:.1f}  cand-loop {raw[:, 14].sum() / clk * 1e6 / nii:.3f} us")
