@@ -796,25 +796,32 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                     DL = lits_of(k, c, src ^ 1);
                     DS = sts_of(k, c, src ^ 1);
                 }
-                if (t1)
+                if (t1) {
                     nl = event_type_i(k, L, S, n, DL, DS, act, n_act, out,
                                       ev == 0 ? s.sk_t[j] : s.sk_n[j], lane, n_draws,
                                       s.mscr + (size_t)warp * 64);
-                else if (RES)
-                    nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
-                                       const_cast<int32_t *>(L) + n, slab - n, s.cand, lane,
+                } else {
+                    // insertion buffer: resident lists use their own slab's
+                    // free tail; with a capacity <= kMaxIns the warp's shared
+                    // buffer; unbounded insertions (sparse_capacity None) the
+                    // unused tail of the source list's global slab.  One call
+                    // site: the merge is inlined once (its code is fetched
+                    // for every document)
+                    int32_t *ib;
+                    int icap;
+                    if (RES) {
+                        ib = const_cast<int32_t *>(L) + n;
+                        icap = slab - n;
+                    } else if (k.capacity >= 0 && k.capacity <= kMaxIns) {
+                        ib = s.ins + (size_t)warp * kMaxIns;
+                        icap = kMaxIns;
+                    } else {
+                        ib = lits_of(k, c, src) + n;
+                        icap = slab - n;
+                    }
+                    nl = event_type_ii(k, L, S, n, DL, DS, act, n_act, ib, icap, s.cand, lane,
                                        prof ? pc2 : nullptr);
-                else if (k.capacity >= 0 && k.capacity <= kMaxIns)
-                    // insertions per event < capacity: the shared buffer holds them
-                    nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
-                                       s.ins + (size_t)warp * kMaxIns, kMaxIns, s.cand, lane,
-                                       prof ? pc2 : nullptr);
-                else
-                    // unbounded insertions (sparse_capacity None): the unused
-                    // tail of the source list's global slab is the buffer
-                    nl = event_type_ii(k, L, S, n, DL, DS, act, n_act,
-                                       lits_of(k, c, src) + n, slab - n, s.cand, lane,
-                                       prof ? pc2 : nullptr);
+                }
                 if (prof) {
                     const long long dt = clock64() - e_t0;
                     ev_clk[t1 ? (out ? 2 : 0) : 1] += (unsigned long long)dt;
