@@ -2113,7 +2113,11 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
             const uint16_t *off = reinterpret_cast<const uint16_t *>(rc + 4 + k.Wp);
             hi_t = tbt >= 65536u ? C : off[(tbt >> 8) + 1];
             hi_n = tbn >= 65536u ? C : off[260 + (tbn >> 8) + 1];
-            __syncthreads();  // info[] written
+            // info[] of own clauses is read by warp 0 (own events) before the
+            // next block barrier: a block barrier only when other warps wrote
+            // part of it
+            if (cown > 32) __syncthreads();
+            else __syncwarp();
             if (tid == 0) SPEC_TL(wn, rep ? 10 : 9, clock64());
         }
         const bool staged = hi_t <= k.spec_ent && hi_n <= k.spec_ent;
