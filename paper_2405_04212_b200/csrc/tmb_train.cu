@@ -2798,6 +2798,9 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     int64_t chunk = n_steps;
     if (k.fast) {
         chunk = std::max<int64_t>(1, (int64_t)(kRecordBufferBytes / (4 * (size_t)k.R)));
+        // k_train_spec's vote slots grow with the launch ((2n + 2) windows x
+        // 2 * spec words): at most 2^18 steps per launch (128 MB of slots)
+        if (k.spec) chunk = std::min<int64_t>(chunk, int64_t(1) << 18);
         if (g_train_key_chunk > 0) chunk = std::min(chunk, g_train_key_chunk);
     }
     const int64_t slots = std::min(n_steps, chunk);
