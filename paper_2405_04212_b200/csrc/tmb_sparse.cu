@@ -951,6 +951,9 @@ struct SparseInferK {
     const int32_t *post_ptr;     // [n_literals + 1]
     const int32_t *post_clause;  // clauses including each literal
     const int32_t *n_inc;        // [C]
+    // K <= 2: the same postings as {clause, include count, w0, w1} -- one
+    // 16-byte load per posting instead of three dependent gathers
+    const int4 *post_ent;
 };
 
 // votes (argmax ties to the lowest class, np.argmax) of document d from the
@@ -1067,6 +1070,16 @@ __global__ void __launch_bounds__(256) k_sparse_infer_count(SparseInferK k) {
                 const int pj = __shfl_sync(0xffffffffu, p0, lo & 31);
                 const int ej = __shfl_sync(0xffffffffu, incl - np, lo & 31);
                 if (slot >= total) continue;
+                if (KR == 2 && k.post_ent) {
+                    const int4 e = __ldg(&k.post_ent[pj + slot - ej]);
+                    const uint32_t old = atomicAdd(&cnt[e.x], 1u);
+                    if ((int)old + 1 == e.y) {
+                        acc.r[0] += e.z;
+                        acc.r[KR > 1 ? 1 : 0] += e.w;
+                        if (k.outputs) k.outputs[d * k.C + e.x] = 1;
+                    }
+                    continue;
+                }
                 const int c = __ldg(&k.post_clause[pj + slot - ej]);
                 const uint32_t old = atomicAdd(&cnt[c], 1u);
                 if ((int)old + 1 == __ldg(&k.n_inc[c])) {
@@ -1169,12 +1182,15 @@ struct SparseIndex {
     bool counting = false;
     int cnt_warps = 0;
     int32_t *pptr = nullptr, *pcl = nullptr, *ninc = nullptr;             // counting
+    int4 *pent = nullptr;                                                 // counting, K <= 2
     int32_t *kptr = nullptr, *kcl = nullptr, *iptr = nullptr, *ilit = nullptr;  // key literal
     void release() {
         for (int32_t **p : {&pptr, &pcl, &ninc, &kptr, &kcl, &iptr, &ilit}) {
             if (*p) cudaFree(*p);
             *p = nullptr;
         }
+        if (pent) cudaFree(pent);
+        pent = nullptr;
         version = ~0ull;
     }
     void release_after(cudaStream_t st) {  // after the kernels queued on st
@@ -1555,6 +1571,22 @@ static int build_infer_index(tmb_sparse *sp, const int64_t *indptr, const int32_
         up(&ix.pptr, post_ptr);
         up(&ix.pcl, post_clause);
         up(&ix.ninc, n_inc);
+        if (K <= 2) {  // packed postings {clause, include count, weights}
+            std::vector<int32_t> w(C * K);
+            if (!rc) rc = check_cuda(cudaMemcpyAsync(w.data(), sp->weights, 4 * C * K,
+                                                     cudaMemcpyDeviceToHost, st), "D2H");
+            if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "weights");
+            std::vector<int4> ent(post_clause.size());
+            for (size_t q = 0; q < post_clause.size(); ++q) {
+                const int32_t c = post_clause[q];
+                ent[q] = make_int4(c, n_inc[c], w[(size_t)c * K], K > 1 ? w[(size_t)c * K + 1] : 0);
+            }
+            if (!rc) rc = check_cuda(cudaMalloc(&ix.pent, 16 * std::max<size_t>(ent.size(), 1)),
+                                     "cudaMalloc");
+            if (!rc && !ent.empty())
+                rc = check_cuda(cudaMemcpyAsync(ix.pent, ent.data(), 16 * ent.size(),
+                                                cudaMemcpyHostToDevice, st), "H2D");
+        }
     } else {
         // key = the included literal the sample contains least often (ties:
         // the one fewest clauses include)
@@ -1622,7 +1654,7 @@ static int sparse_infer_impl(const tmb_sparse *csp, const int64_t *indptr, const
     SparseInferK k{};
     k.indptr = indptr; k.indices = indices; k.N = N;
     k.key_ptr = ix.kptr; k.key_clause = ix.kcl; k.inc_ptr = ix.iptr; k.inc_lits = ix.ilit;
-    k.post_ptr = ix.pptr; k.post_clause = ix.pcl; k.n_inc = ix.ninc;
+    k.post_ptr = ix.pptr; k.post_clause = ix.pcl; k.n_inc = ix.ninc; k.post_ent = ix.pent;
     k.n_literals = sp->cfg.n_literals; k.weights = sp->weights; k.C = (int)C; k.K = (int)K;
     k.votes = votes; k.pred = pred; k.outputs = outputs;
     if (outputs) TMB_CUDA(cudaMemsetAsync(outputs, 0, (size_t)N * C, st));
