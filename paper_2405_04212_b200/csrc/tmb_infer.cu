@@ -1187,6 +1187,7 @@ int g_infer_eval = 2;  // tmb_set_option("infer.eval_mode", 0|2|3): k_infer_ws e
 extern unsigned long long *g_sparse_phase;  // tmb_sparse.cu
 extern int g_sparse_resident;                // tmb_sparse.cu
 extern int g_sparse_infer_key;               // tmb_sparse.cu
+extern int g_sparse_cnt32;                   // tmb_sparse.cu
 unsigned long long *g_infer_phase = nullptr;
 
 int launch_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes, int64_t *pred,
@@ -1625,6 +1626,10 @@ int tmb_set_option(const char *name, int64_t value) {
     }
     if (std::string(name) == "sparse.phase_buffer") {  // device uint64 [n_cta*16] or 0
         g_sparse_phase = reinterpret_cast<unsigned long long *>(value);
+        return TMB_OK;
+    }
+    if (std::string(name) == "sparse.counters32") {  // 1: 32-bit counters in the counting kernel
+        g_sparse_cnt32 = (int)value;
         return TMB_OK;
     }
     if (std::string(name) == "sparse.infer_key") {  // 1: key-literal sparse inference kernel

@@ -954,6 +954,7 @@ struct SparseInferK {
     // K <= 2: the same postings as {clause, include count, w0, w1} -- one
     // 16-byte load per posting instead of three dependent gathers
     const int4 *post_ent;
+    int cnt8;  // every include count <= 255: byte counters (4x the warps per SM)
 };
 
 // votes (argmax ties to the lowest class, np.argmax) of document d from the
@@ -1029,10 +1030,18 @@ template <int KR>
 __global__ void __launch_bounds__(256) k_sparse_infer_count(SparseInferK k) {
     extern __shared__ __align__(16) char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int Cp = (k.C + 3) & ~3;
+    // counter words per warp: one per clause, or (cnt8) one byte per clause
+    const int Cp = k.cnt8 ? ((k.C + 15) & ~15) / 4 : (k.C + 3) & ~3;
     uint32_t *cnt = reinterpret_cast<uint32_t *>(smem_raw) + (size_t)warp * Cp;
     long long *vacc = reinterpret_cast<long long *>(
         reinterpret_cast<uint32_t *>(smem_raw) + (size_t)nwarps * Cp) + (size_t)warp * k.K;
+    auto bump = [&](int c) -> int {  // this posting's count before it
+        if (k.cnt8) {
+            const uint32_t sh = 8u * (uint32_t)(c & 3);
+            return (int)((atomicAdd(&cnt[c >> 2], 1u << sh) >> sh) & 0xFFu);
+        }
+        return (int)atomicAdd(&cnt[c], 1u);
+    };
     for (int64_t d = (int64_t)blockIdx.x * nwarps + warp; d < k.N; d += (int64_t)gridDim.x * nwarps) {
         const int64_t a0 = k.indptr[d], a1 = k.indptr[d + 1];
         const int32_t *doc = k.indices + a0;
@@ -1072,8 +1081,7 @@ __global__ void __launch_bounds__(256) k_sparse_infer_count(SparseInferK k) {
                 if (slot >= total) continue;
                 if (KR == 2 && k.post_ent) {
                     const int4 e = __ldg(&k.post_ent[pj + slot - ej]);
-                    const uint32_t old = atomicAdd(&cnt[e.x], 1u);
-                    if ((int)old + 1 == e.y) {
+                    if (bump(e.x) + 1 == e.y) {
                         acc.r[0] += e.z;
                         acc.r[KR > 1 ? 1 : 0] += e.w;
                         if (k.outputs) k.outputs[d * k.C + e.x] = 1;
@@ -1081,8 +1089,7 @@ __global__ void __launch_bounds__(256) k_sparse_infer_count(SparseInferK k) {
                     continue;
                 }
                 const int c = __ldg(&k.post_clause[pj + slot - ej]);
-                const uint32_t old = atomicAdd(&cnt[c], 1u);
-                if ((int)old + 1 == __ldg(&k.n_inc[c])) {
+                if (bump(c) + 1 == __ldg(&k.n_inc[c])) {
                     acc.add(k, c, vacc);
                     if (k.outputs) k.outputs[d * k.C + c] = 1;
                 }
@@ -1169,6 +1176,7 @@ __global__ void __launch_bounds__(256) k_sparse_infer(SparseInferK k) {
 }
 
 int g_sparse_infer_key = 0;  // tmb_set_option("sparse.infer_key"): force the key-literal kernel
+int g_sparse_cnt32 = 0;      // tmb_set_option("sparse.counters32"): 32-bit clause counters
 unsigned long long *g_sparse_phase = nullptr;  // tmb_set_option("sparse.phase_buffer")
 int g_sparse_resident = 1;                      // tmb_set_option("sparse.resident")
 
@@ -1183,6 +1191,7 @@ struct SparseIndex {
     int cnt_warps = 0;
     int32_t *pptr = nullptr, *pcl = nullptr, *ninc = nullptr;             // counting
     int4 *pent = nullptr;                                                 // counting, K <= 2
+    bool cnt8 = false;                                                    // max include count <= 255
     int32_t *kptr = nullptr, *kcl = nullptr, *iptr = nullptr, *ilit = nullptr;  // key literal
     void release() {
         for (int32_t **p : {&pptr, &pcl, &ninc, &kptr, &kcl, &iptr, &ilit}) {
@@ -1571,6 +1580,7 @@ static int build_infer_index(tmb_sparse *sp, const int64_t *indptr, const int32_
         up(&ix.pptr, post_ptr);
         up(&ix.pcl, post_clause);
         up(&ix.ninc, n_inc);
+        ix.cnt8 = C == 0 || *std::max_element(n_inc.begin(), n_inc.end()) <= 255;
         if (K <= 2) {  // packed postings {clause, include count, weights}
             std::vector<int32_t> w(C * K);
             if (!rc) rc = check_cuda(cudaMemcpyAsync(w.data(), sp->weights, 4 * C * K,
@@ -1655,12 +1665,14 @@ static int sparse_infer_impl(const tmb_sparse *csp, const int64_t *indptr, const
     k.indptr = indptr; k.indices = indices; k.N = N;
     k.key_ptr = ix.kptr; k.key_clause = ix.kcl; k.inc_ptr = ix.iptr; k.inc_lits = ix.ilit;
     k.post_ptr = ix.pptr; k.post_clause = ix.pcl; k.n_inc = ix.ninc; k.post_ent = ix.pent;
+    k.cnt8 = ix.counting && ix.cnt8 && !g_sparse_cnt32 ? 1 : 0;
     k.n_literals = sp->cfg.n_literals; k.weights = sp->weights; k.C = (int)C; k.K = (int)K;
     k.votes = votes; k.pred = pred; k.outputs = outputs;
     if (outputs) TMB_CUDA(cudaMemsetAsync(outputs, 0, (size_t)N * C, st));
     const bool counting = ix.counting;
     const int threads = counting ? 32 * ix.cnt_warps : 256;
-    const size_t smem = counting ? (4 * (size_t)((C + 3) & ~3LL) + 8 * (size_t)K) * ix.cnt_warps
+    const size_t cnt_bytes = k.cnt8 ? (size_t)((C + 15) & ~15LL) : 4 * (size_t)((C + 3) & ~3LL);
+    const size_t smem = counting ? (cnt_bytes + 8 * (size_t)K) * ix.cnt_warps
                                  : 8 * (size_t)K * (threads / 32);
     int dev = 0, max_smem = 0;
     cudaGetDevice(&dev);
@@ -1674,7 +1686,9 @@ static int sparse_infer_impl(const tmb_sparse *csp, const int64_t *indptr, const
                                           : (const void *)k_sparse_infer<0>);
     TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t per_cta = threads / 32;
-    const int64_t per_sm = counting ? std::max<int64_t>(1, (220 * 1024) / (int64_t)smem) : 8;
+    const int64_t per_sm = counting ? std::max<int64_t>(1, std::min<int64_t>(64 / ix.cnt_warps,
+                                                                              (220 * 1024) / (int64_t)smem))
+                                    : 8;
     const int64_t grid = std::min<int64_t>((N + per_cta - 1) / per_cta, (int64_t)sm_count() * per_sm);
     void *args[] = {&k};
     TMB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(threads), args, smem, st));
