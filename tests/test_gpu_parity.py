@@ -885,3 +885,21 @@ def test_hbm_state_trainer_1024_threads_vs_oracle(gpu, oracle, n_blocks, keys):
     assert np.array_equal(m.states, ost.states)
     assert np.array_equal(m.weights, ost.weights)
     assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64), ost.block_counters)
+
+
+def test_speculative_trainer_large_threshold_vs_oracle(gpu, oracle):
+    """k_train_spec with T > 8192 (no threshold table in shared memory: the
+    window decision computes the exact thresholds in f64) against the
+    oracle."""
+    (tx, ty), _ = gpu.datasets.mnist_shaped(n_train=600, n_test=10, data_seed=9)
+    kw = gpu.datasets.mnist_shaped_config_kwargs(seed=13)
+    kw["threshold"] = 9000
+    cfg = gpu.Config(**kw)
+    sess = gpu.DenseTrainSession(cfg, tx, ty)
+    assert sess.launch["kernel"] == "k_train_spec"
+    for _ in range(2):
+        sess.run_epoch()
+    m = sess.model()
+    ost, _ = oracle.train(cfg, tx, ty, 2)
+    assert np.array_equal(m.states, ost.states)
+    assert np.array_equal(m.weights, ost.weights)
