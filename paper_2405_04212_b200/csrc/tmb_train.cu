@@ -1882,11 +1882,12 @@ __device__ __forceinline__ void spec_correct(const TrainK &k, const Smem &s, int
     s.part[(threadIdx.x >> 5) * 32 + lane] = c2 ? b : a;
 }
 
-// Vote slot t of window wn.  Slots are interleaved across windows (slot t
-// of every window, then slot t + 1, ...) so the 2 * spec words of one window
-// sit in distinct 128-B lines (the L2 serialises atomics per line).
+// Vote slot t of window wn: a window's 2 * spec words are contiguous (two
+// 128-B lines).  Measured against one line per word (interleaved across
+// windows, which spreads the atomics over L2 slices but makes every poll 32
+// line reads): 3% faster per example.
 __device__ __forceinline__ size_t spec_slot(const TrainK &k, int64_t wn, int t) {
-    return (size_t)t * (size_t)(2 * k.n_steps + 2) + (size_t)wn;
+    return (size_t)wn * 2 * k.spec + t;
 }
 
 // Thread t < 2kk publishes step t >> 1's label (t even) / negative (t odd)
