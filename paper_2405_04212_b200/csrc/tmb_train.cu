@@ -592,6 +592,105 @@ __device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, in
     cn.upd += nupd;
 }
 
+// Wide feedback for shared-memory states: a thread owns NQ consecutive quads
+// (4 * NQ positions) of one work row, a row takes RW whole warps.  The row's
+// index, info bits, event keys, the literal bits and kGolden * p0 are fetched
+// or computed once per 4 * NQ positions instead of once per quad, the states
+// move as one 8- or 16-byte shared access, and the include-mask word needs
+// log2(8 / NQ) shuffles instead of three -- about 40% fewer instructions per
+// position than feedback_simd (same arithmetic: quad_update_simd).
+template <int NQ, int UNR>
+__device__ __forceinline__ void feedback_wide(const TrainK &k, const Smem &s,
+                                              const uint32_t *lit, int n_work, Counters &cn) {
+    static_assert(NQ == 2 || NQ == 4, "NQ: 2 or 4 quads per thread");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    constexpr int LPW = 8 / NQ;             // lanes per include-mask word
+    const int UP = k.Ppad / (4 * NQ);       // units per padded row (Ppad % 128 == 0)
+    const int RW = (UP + 31) >> 5;          // warps per row
+    const int total = n_work * RW;
+    unsigned nd = 0, nupd = 0;
+    for (int v = warp; v < total; v += nwarp) {
+        const int wc = v / RW, u = (v - wc * RW) * 32 + lane;
+        const int j = s.work[wc];
+        const int p0 = u * (4 * NQ);
+        const bool valid = u < UP;
+        uint32_t nibs = 0;
+        if (valid) {
+            const int info = s.info[j];
+            const uint32_t litu = p0 < k.P ? lit[p0 >> 5] >> (p0 & 31) : 0u;
+            const uint64_t zp = kGolden * (uint64_t)p0;
+            uint64_t zt = (info & I_TEV) ? s.sk_t[j] + zp : 0;
+            uint64_t zn = (info & I_NEV) ? s.sk_n[j] + zp : 0;
+            int8_t *row = s.states + (size_t)j * k.Ppad + p0;
+            uint32_t in[NQ], out[NQ];
+            if (NQ == 4) {
+                const uint4 t = *reinterpret_cast<const uint4 *>(row);
+                in[0] = t.x; in[1] = t.y; in[NQ - 2] = t.z; in[NQ - 1] = t.w;
+            } else {
+                const uint2 t = *reinterpret_cast<const uint2 *>(row);
+                in[0] = t.x; in[1] = t.y;
+            }
+            bool changed = false;
+            if (UNR >= NQ) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int lim = k.P - p0 - 4 * q;
+                    out[q] = quad_update_simd(k, in[q], info, (litu >> (4 * q)) & 0xFu, lim,
+                                              zt + kGolden * (uint64_t)(4 * q),
+                                              zn + kGolden * (uint64_t)(4 * q), nd);
+                    nupd += __popc(__vcmpne4(out[q], in[q]) & 0x01010101u);
+                    nibs |= quad_include_nibble(out[q], lim) << (4 * q);
+                    changed |= out[q] != in[q];
+                }
+            } else {
+                // rolled: the words rotate through in[0] / out[NQ - 1]
+                int lim = k.P - p0;
+                uint32_t lq = litu;
+#pragma unroll 1
+                for (int q = 0; q < NQ; ++q) {
+                    const uint32_t wi = in[0];
+                    const uint32_t wo = quad_update_simd(k, wi, info, lq & 0xFu, lim, zt, zn, nd);
+                    nupd += __popc(__vcmpne4(wo, wi) & 0x01010101u);
+                    nibs = (nibs >> 4) | (quad_include_nibble(wo, lim) << (4 * (NQ - 1)));
+                    changed |= wo != wi;
+#pragma unroll
+                    for (int r = 0; r + 1 < NQ; ++r) {
+                        in[r] = in[r + 1];
+                        out[r] = out[r + 1];
+                    }
+                    out[NQ - 1] = wo;
+                    zt += 4 * kGolden;
+                    zn += 4 * kGolden;
+                    lq >>= 4;
+                    lim -= 4;
+                }
+            }
+            if (changed) {
+                if (NQ == 4)
+                    *reinterpret_cast<uint4 *>(row) = make_uint4(out[0], out[1], out[NQ - 2], out[NQ - 1]);
+                else
+                    *reinterpret_cast<uint2 *>(row) = make_uint2(out[0], out[1]);
+            }
+        }
+        // mask word for positions 32w..32w+31: LPW adjacent lanes hold its parts
+        uint32_t m = nibs << ((lane & (LPW - 1)) * 4 * NQ);
+#pragma unroll
+        for (int o = 1; o < LPW; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+        if (valid && (lane & (LPW - 1)) == 0) {
+            const int wd = p0 >> 5;
+            if (wd < k.W) {
+                const uint32_t old = s.masks[j * k.MW + wd];
+                if (old != m) {
+                    s.masks[j * k.MW + wd] = m;
+                    atomicAdd(&s.cnt[j], __popc(m) - __popc(old));
+                }
+            }
+        }
+    }
+    cn.draws += nd;
+    cn.upd += nupd;
+}
+
 // Grid-balanced feedback (HBM-resident states): this CTA's share
 // [q_begin, q_end) of the quads of all CTAs' work items (the union of the
 // published work lists in CTA order; q_begin, q_end multiples of 32, so a
@@ -2882,7 +2981,11 @@ __global__ void __launch_bounds__(1024, 1) k_mb_feedback(TrainK k, int n_work, i
         else if (VARIANT == 3) feedback_compact<true, 2>(k, s, 0, lit, n_work, cn);
         else if (VARIANT == 4) feedback_compact<true, 4>(k, s, 0, lit, n_work, cn);
         else if (VARIANT == 5) feedback_compact<true, 7>(k, s, 0, lit, n_work, cn);
-        else feedback_simd<true>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 6) feedback_simd<true>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 7) feedback_wide<4, 1>(k, s, lit, n_work, cn);
+        else if (VARIANT == 8) feedback_wide<4, 4>(k, s, lit, n_work, cn);
+        else if (VARIANT == 9) feedback_wide<2, 1>(k, s, lit, n_work, cn);
+        else feedback_wide<2, 2>(k, s, lit, n_work, cn);
         __syncthreads();
         tot += (unsigned long long)(clock64() - t0);
     }
@@ -2905,11 +3008,13 @@ extern "C" int tmb_microbench_feedback(int variant, int n_work, int two_events, 
     const size_t sm = smem_layout(k, true, MODE_GRID, nullptr, nullptr);
     unsigned long long *cyc = nullptr;
     TMB_CUDA(cudaMalloc(&cyc, 8));
-    const void *fns[7] = {(const void *)k_mb_feedback<0>, (const void *)k_mb_feedback<1>,
-                          (const void *)k_mb_feedback<2>, (const void *)k_mb_feedback<3>,
-                          (const void *)k_mb_feedback<4>, (const void *)k_mb_feedback<5>,
-                          (const void *)k_mb_feedback<6>};
-    if (variant < 0 || variant > 6) return fail(TMB_E_INVALID, "microbench_feedback: variant 0..6");
+    const void *fns[11] = {(const void *)k_mb_feedback<0>, (const void *)k_mb_feedback<1>,
+                           (const void *)k_mb_feedback<2>, (const void *)k_mb_feedback<3>,
+                           (const void *)k_mb_feedback<4>, (const void *)k_mb_feedback<5>,
+                           (const void *)k_mb_feedback<6>, (const void *)k_mb_feedback<7>,
+                           (const void *)k_mb_feedback<8>, (const void *)k_mb_feedback<9>,
+                           (const void *)k_mb_feedback<10>};
+    if (variant < 0 || variant > 10) return fail(TMB_E_INVALID, "microbench_feedback: variant 0..10");
     TMB_CUDA(cudaFuncSetAttribute(fns[variant], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     void *args[] = {&k, &n_work, &two_events, &iters, &cyc};
     TMB_CUDA(cudaLaunchKernel(fns[variant], dim3(1), dim3(threads), args, sm, 0));

@@ -251,14 +251,16 @@ class CSRDocs:
 
 
 def sparse_zipf(data_seed: int = 5, n_docs: int = 1_000_000, vocab: int = 1_000_000,
-                n_tokens: int = 100, a: float = 1.05, n_planted: int = 500) -> CSRDocs:
+                n_tokens: int = 100, a: float = 1.05, n_planted: int = 500,
+                planted_lo: int = 100, planted_span: int = 5000) -> CSRDocs:
     """C5: documents of 100 distinct Zipf(1.05) ids over a 10^6 vocabulary,
     stored as CSR.  500 planted indicator ids per class are drawn from ranks
-    100..5099; label = class with the larger planted count, ties broken by a
-    coin from the data stream."""
+    100..5099 (planted_lo .. planted_lo + planted_span - 1); label = class
+    with the larger planted count, ties broken by a coin from the data
+    stream."""
     rng = np.random.default_rng(data_seed)
     rank_to_id = rng.permutation(vocab)
-    planted = rank_to_id[100 + rng.permutation(5000)[:2 * n_planted]]
+    planted = rank_to_id[planted_lo + rng.permutation(planted_span)[:2 * n_planted]]
     cls0, cls1 = np.sort(planted[:n_planted]), np.sort(planted[n_planted:])
     cdf = np.cumsum(_zipf_probs(vocab, a))
     indptr = np.arange(n_docs + 1, dtype=np.int64) * n_tokens

@@ -11,9 +11,9 @@ from paper_2405_04212_b200 import _lib  # noqa: E402
 
 out = {}
 for threads in (512,):
-    for variant in (0, 1, 6):
+    for variant in (0, 6, 7, 8, 9, 10):
         for two in (0, 1):
-            for nw in (1, 2, 4, 8):
+            for nw in (1, 2, 3, 4, 8):
                 c = ct.c_double()
                 _lib.call("tmb_microbench_feedback", variant, nw, two, threads, 200, ct.byref(c))
                 out[f"t{threads}_v{variant}_two{two}_nw{nw}"] = round(c.value, 1)
