@@ -43,6 +43,27 @@ HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
 HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
 
 
+# config.workload of every workload: the b200 arm and the reference arm print
+# the same string (the reference arm times a bounded sample of it)
+WORKLOADS = {
+    "c2-train": "configs[1]: MNIST-shaped CoTM training, step = 1 epoch",
+    "c1-train": ("configs[0]: Noisy-XOR, 10 clauses, T=15, s=3.9; step = the 5-seed study: five "
+                 "20-epoch trainings of 5000 examples (model seeds 0..4), concurrent on five "
+                 "streams / SMs"),
+    "c3-infer": ("configs[2]: 2^22 examples x 4096 features, 10000 clauses x 20 includes, 10 "
+                 "classes; step = one pass over all examples"),
+    "c4-train": ("configs[3]: bag-of-words training, 10000 clauses x 20000 literal positions, "
+                 "step = 5000 consecutive examples of the epoch"),
+    "c5-sparse": ("configs[4]: SparseTM, 10^6-literal vocabulary, 2000 clauses, capacity 64; "
+                  "step = 100000 consecutive training documents"),
+}
+
+
+def sweep_workload(world: int, step_n: int) -> str:
+    return (f"configs[3] sweep: 8 independent bag-of-words trainings (10000 clauses x 20000 "
+            f"positions), job j on rank j mod {world}; step = {step_n} examples of every job")
+
+
 def ncu_traffic(kernel: str):
     """DRAM bytes (read + write) per launch of `kernel` from the newest
     committed `ncu --set full` summary under profiles/ (captured on the same
@@ -398,7 +419,7 @@ def bench_c2_train(args, rank, world, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int8 TA states / int32 weights / u64 SplitMix64",
         "data": "synthetic (seeded MNIST-shaped generator, datasets.mnist_shaped)",
-        "config": {"workload": "configs[1]: MNIST-shaped CoTM training, step = 1 epoch",
+        "config": {"workload": WORKLOADS["c2-train"],
                    "n_features": 784, "n_literals": P, "n_clauses": C, "n_classes": 10,
                    "threshold": cfg.threshold, "s": cfg.s, "examples_per_epoch": N,
                    "epochs_timed": f"{args.warmup + 1}..{args.warmup + args.steps}",
@@ -582,9 +603,7 @@ def bench_c1_train(args, rank, world, local):
         "dtype": "int8 TA states / int32 weights / u64 SplitMix64",
         "data": "synthetic (datasets.noisy_xor: 12 Bernoulli(0.5) features, 40% train "
                 "label noise)",
-        "config": {"workload": "configs[0]: Noisy-XOR, 10 clauses, T=15, s=3.9; step = the "
-                               "5-seed study: five 20-epoch trainings of 5000 examples (model "
-                               "seeds 0..4), concurrent on five streams / SMs",
+        "config": {"workload": WORKLOADS["c1-train"],
                    "latency_us_per_example_one_training": us_training_example,
                    "launch": preps[0][0].launch,
                    "parallelism": f"replicas x{world} (online training is sequential)",
@@ -766,8 +785,7 @@ def bench_c3_infer(args, rank, world, local, embedded=False):
         "metric": "inference examples/sec (configs[2] batched CoTM inference)",
         "value": value, "unit": "examples/s", "n_gpus": world, "steps": args.steps,
         "ms_per_step": ms / args.steps,
-        "config": {"workload": "configs[2]: 2^22 examples x 4096 features, 10000 clauses x 20 "
-                               "includes, 10 classes; step = one pass over all examples",
+        "config": {"workload": WORKLOADS["c3-infer"],
                    "examples": N_total, "sharding": f"contiguous example ranges over {world}",
                    "rules": model.n_rules, "l2": "inputs (17 GB) far larger than L2"},
         "gpu_launches": int(launches),
@@ -945,8 +963,7 @@ def bench_c4_train(args, rank, world, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int8 TA states (HBM) / int32 weights / u64 SplitMix64",
         "data": "synthetic (datasets.bag_of_words: Zipf(1.1) documents, planted sets)",
-        "config": {"workload": "configs[3]: bag-of-words training, 10000 clauses x 20000 literal "
-                               "positions, step = 5000 consecutive examples of the epoch",
+        "config": {"workload": WORKLOADS["c4-train"],
                    "launch": sess.launch, "parallelism": f"replicas x{world}",
                    "l2": "256 MiB buffer written before every timed step"},
         "gpu_launches": int(launches),
@@ -1092,9 +1109,7 @@ def bench_c4_sweep(args, rank, world, local):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int8 TA states (HBM) / int32 weights / u64 SplitMix64",
         "data": "synthetic (datasets.bag_of_words: Zipf(1.1) documents, planted sets)",
-        "config": {"workload": f"configs[3] sweep: 8 independent bag-of-words trainings "
-                               f"(10000 clauses x 20000 positions), job j on rank j mod "
-                               f"{world}; step = {step_n} examples of every job",
+        "config": {"workload": sweep_workload(world, step_n),
                    "grid": [list(g) for g in grid], "jobs_on_rank0": mine,
                    "parallelism": f"jobs round-robin over {world} GPU(s); no collective on "
                                   "the hot path",
@@ -1284,8 +1299,7 @@ def bench_c5_sparse(args, rank, world, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int32 literal ids / int8 states / u64 SplitMix64",
         "data": "synthetic (datasets.sparse_zipf: 10^6 Zipf(1.05) documents x 100 ids)",
-        "config": {"workload": "configs[4]: SparseTM, 10^6-literal vocabulary, 2000 clauses, "
-                               "capacity 64; step = 100000 consecutive training documents",
+        "config": {"workload": WORKLOADS["c5-sparse"],
                    "parallelism": f"replicas x{world} (online training is sequential; every "
                                   "rank trains the same replica)",
                    "l2": "per-step CSR chunk (40 MB) and the clause lists; each step streams "
@@ -1466,6 +1480,7 @@ def bench_reference(args, rank, world):
     kind = "reference" if tk is not None else "port"
     unit = "examples/s"
     extra = {}
+    secs = []  # wall seconds of every timed step (a bounded sample of the workload's step)
     if args.workload == "c1-train":
         (tx, ty), (ex, ey) = datasets.noisy_xor()
         rates, accs = [], []
@@ -1480,6 +1495,7 @@ def bench_reference(args, rank, world):
                 st, w = ost.states, ost.weights
             dt = time.perf_counter() - t
             if i >= args.warmup:
+                secs.append(dt)
                 rates.append(20 * len(ty) / dt)
                 _, pred = oracle.batch_votes(st, w, oracle.augment_literals(ex))
                 accs.append(float(np.mean(pred == ey)))
@@ -1519,7 +1535,8 @@ def bench_reference(args, rank, world):
             t = time.perf_counter()
             run_all()
             if i >= args.warmup:
-                rates.append(len(xs) / (time.perf_counter() - t))
+                secs.append(time.perf_counter() - t)
+                rates.append(len(xs) / secs[-1])
         value = float(np.mean(rates))
         metric = "inference examples/sec (configs[2] batched CoTM inference)"
         sample = (f"{len(xs)}-example prefix per step, {ncpu} threads"
@@ -1554,7 +1571,8 @@ def bench_reference(args, rank, world):
                     oracle.train_steps(a, st, x_lit, ty, order[pos:pos + per_step])
             pos += per_step
             if i >= args.warmup:
-                rates.append(per_step * len(trainers) / (time.perf_counter() - t))
+                secs.append(time.perf_counter() - t)
+                rates.append(per_step * len(trainers) / secs[-1])
         value = float(np.mean(rates))
         if args.workload == "c4-sweep":
             metric = "sweep train examples/sec (configs[3] 8-point s x T grid)"
@@ -1580,7 +1598,8 @@ def bench_reference(args, rank, world):
                                                        d.labels[order[pos:pos + per_step]])
             pos += per_step
             if i >= args.warmup:
-                rates.append(per_step / (time.perf_counter() - t))
+                secs.append(time.perf_counter() - t)
+                rates.append(per_step / secs[-1])
         value = float(np.mean(rates))
         metric = "SparseTM train documents/sec (configs[4])"
         sample = (f"{per_step} document(s) of epoch 1 per step with the full training set's "
@@ -1621,7 +1640,8 @@ def bench_reference(args, rank, world):
                 oracle.train_steps(cfg, st, x_lit, ty, order[pos:pos + per_step])
             pos += per_step
             if i >= args.warmup:
-                rates.append(per_step / (time.perf_counter() - t))
+                secs.append(time.perf_counter() - t)
+                rates.append(per_step / secs[-1])
         value = float(np.mean(rates))
         metric = "train examples/sec (configs[1] MNIST-shaped CoTM training)"
         sample = (f"{per_step} consecutive examples of epoch {ep + 1} per step (warm-up steps "
@@ -1638,10 +1658,13 @@ def bench_reference(args, rank, world):
                             "backend": rk.BACKEND_NAME}
     cpu.update(extra)
     return {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.mean(secs)) if secs else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "int8 / u64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.workload},
+            "config": {"workload": (sweep_workload(world, args.sweep_examples)
+                                    if args.workload == "c4-sweep" else WORKLOADS[args.workload]),
+                       "sample_per_step": sample},
             "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
