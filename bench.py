@@ -967,7 +967,10 @@ def bench_c4_train(args, rank, world, local):
                    "launch": sess.launch, "parallelism": f"replicas x{world}",
                    "l2": "256 MiB buffer written before every timed step"},
         "gpu_launches": int(launches),
-        "work": {"events_per_example": ev_ex, "draws_per_example": draws_ex},
+        "work": {"events_per_example": ev_ex, "draws_per_example": draws_ex,
+                 "type_i_per_example": d["type_i"] / max(d["examples"], 1),
+                 "type_ii_per_example": d["type_ii"] / max(d["examples"], 1),
+                 "state_updates_per_example": d["state_updates"] / max(d["examples"], 1)},
         # the binding resource is the integer pipe: every reference draw is
         # one SplitMix64 (two 64-bit multiplies) + compare, at the measured
         # per-SM draw rate; the HBM traffic of the states is secondary

@@ -88,10 +88,12 @@ int tmb_microbench_sparse_event(int which, int n, int n_act, int reps, int n_cta
 /* Trainer feedback microbenchmark (design evidence): one CTA
  * of `threads` threads with the configs[1] per-CTA slice (14 clauses x 1568
  * positions, states in shared memory) applies Type I feedback to n_work
- * firing clauses (two_events: target and negative event on each) `iters`
- * times.  variant 0: feedback_quads (k_train_fast), 1: feedback_compact;
- * 2-5: compact ablations (no mask rebuild / cheap hash / no state access / all);
- * 6: feedback_simd (k_train_spec).
+ * clauses (two_events bit 0: target and negative event on each; bit 1: the
+ * clauses are silent instead of firing) `iters` times.  variant 0:
+ * feedback_quads, 1: feedback_compact; 2-5: compact ablations (no mask rebuild
+ * / cheap hash / no state access / all); 6: feedback_simd_v1 (byte-SIMD);
+ * 7-10: feedback_wide; 11: feedback_simd (k_train_spec: silent Type I fast
+ * path, include-mask rebuild gated on sign flips).
  * *cycles_per_call = mean SM cycles per call including its barrier. */
 int tmb_microbench_feedback(int variant, int n_work, int two_events, int threads, int iters,
                             double *cycles_per_call);

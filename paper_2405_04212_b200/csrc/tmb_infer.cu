@@ -1616,6 +1616,10 @@ int tmb_set_option(const char *name, int64_t value) {
         g_train_hbm_threads = (int)value;
         return TMB_OK;
     }
+    if (std::string(name) == "train.gbal_weights") {  // packed bytes: Type II, Type I silent, Type I firing
+        g_train_gbw = (int)value;
+        return TMB_OK;
+    }
     if (std::string(name) == "train.spec_entries") {  // 0 auto, else 64..256 (multiple of 32; default 64)
         g_train_spec_ent = (int)value;
         return TMB_OK;

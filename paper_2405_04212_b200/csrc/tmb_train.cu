@@ -67,10 +67,12 @@ struct TrainK {
     // CTAs by quads, and the owners pull the rebuilt include masks back
     int gbal;
     unsigned *gsync;           // [n_steps][2] arrivals: work lists published / feedback done
-    int *gcount;               // [n_cta] work items per CTA this step
+    int *gcount;               // [2][n_cta] work items per CTA this step, their summed cost weights
+    int gbw[3];                // gbal cost weights of an event: Type II (firing), Type I silent, Type I firing
+    unsigned *gdirty;          // [C] gbal: an include bit of the clause flipped since its owner's last pull
     int *gw_clause, *gw_info;  // [n_cta][cmax] work items (global clause id, info bits)
     uint64_t *gw_sk;           // [n_cta][cmax][2] event stream keys (target, negative)
-    uint32_t *gmask;           // [C][W] include masks of the clauses updated this step
+    uint32_t *gmask;           // [C][W] every clause's include mask (gbal: rewritten where include bits flip)
     unsigned long long *phase;  // optional [n_cta][8] clock64 per phase (profiling)
     tmb_train_stats *stats;
     long long *trace;  // optional [n_steps][4]: negative, votes[label], votes[neg], events
@@ -136,6 +138,8 @@ struct Smem {
     long long *vst;            // spec: [3 * spec][2] partial class sums per kept step
     long long *part;           // spec: [warp][lane] per-warp class-sum partials of a window
     int *gpref;                // gbal: [n_cta + 1] prefix of the published work counts
+    int *gwpref;               // gbal: [n_cta + 1] prefix of the published cost weights
+    long long *gcut;           // gbal: [2] this CTA's share [q_begin, q_end) of the union's quads
     int *rc_clause, *rc_info;  // gbal: [cmax + 4] work items of this CTA's quad range
     uint64_t *rc_sk;           // gbal: [cmax + 4][2]
 };
@@ -192,7 +196,9 @@ __host__ __device__ inline size_t smem_layout(const TrainK &k, bool smem_states,
                                      : nullptr;
     t.states = smem_states ? (int8_t *)take((size_t)k.cmax * k.Ppad) : nullptr;
     const bool gb = k.gbal && !k.fast && !smem_states && mode == MODE_GRID;
+    t.gcut = gb ? (long long *)take(16) : nullptr;
     t.gpref = gb ? (int *)take(4 * (size_t)(k.n_cta + 1)) : nullptr;
+    t.gwpref = gb ? (int *)take(4 * (size_t)(k.n_cta + 1)) : nullptr;
     t.rc_clause = gb ? (int *)take(4 * (size_t)(k.cmax + 4)) : nullptr;
     t.rc_info = gb ? (int *)take(4 * (size_t)(k.cmax + 4)) : nullptr;
     t.rc_sk = gb ? (uint64_t *)take(16 * (size_t)(k.cmax + 4)) : nullptr;
@@ -481,6 +487,24 @@ __device__ __forceinline__ uint32_t swar_dec(uint32_t w, uint32_t one) {  // byt
     return ((w | 0x80808080u) - one) ^ ((w ^ ~one) & 0x80808080u);
 }
 
+// The four draws z0 + kGolden * b (b = 0..3) against 64-bit thresholds, as a
+// 0x01-per-byte mask of the positions with draw < threshold.  SELECT: byte b
+// uses T_inc where bit 8b of incb is set, else T_dec.  (Measured and rejected,
+// tmb_microbench_feedback on the silent path, cycles per clause: deciding on
+// the high word alone with a full compare on ties +5%, the same with the
+// high-word shifts as IMAD.HI on the FMA pipe +12%.)
+template <bool SELECT>
+__device__ __forceinline__ uint32_t quad_hits(uint64_t z0, uint64_t T_dec, uint64_t T_inc,
+                                              uint32_t incb) {
+    uint32_t h = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint64_t t = SELECT && ((incb >> (8 * b)) & 1u) ? T_inc : T_dec;
+        h |= mix64(z0 + kGolden * (uint64_t)b) < t ? (1u << (8 * b)) : 0u;
+    }
+    return h;
+}
+
 // One quad of feedback_simd: the four states of word w after the clause's
 // events (info bits), literal nibble litn, valid positions lim; zt / zn =
 // event key + kGolden * p0 of the target / negative event.  Adds the
@@ -500,14 +524,7 @@ __device__ __forceinline__ uint32_t quad_update_simd(const TrainK &k, uint32_t w
     for (int ev = 0; ev < 2; ++ev) {
         if (!(info & (ev ? I_NEV : I_TEV))) continue;
         if (info & (ev ? I_N1 : I_T1)) {  // Type I
-            const uint64_t z0 = ev ? zn : zt;
-            uint32_t hitn = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const uint64_t z = mix64(z0 + kGolden * (uint64_t)b);
-                hitn |= (z < (((incb >> (8 * b)) & 1u) ? T_inc : T_dec) ? 1u : 0u) << b;
-            }
-            const uint32_t hit = spread4(hitn);
+            const uint32_t hit = quad_hits<true>(ev ? zn : zt, T_dec, T_inc, incb);  // 0x01 bytes
             const uint32_t room = __vcmplts4(w, smax4), above = __vcmpgts4(w, smin4);
             nd += __popc(((incb & room & ~boostm) | (~incb & above & vb)) & 0x01010101u);
             const uint32_t up = incb & room & (boostm | hit);
@@ -528,7 +545,7 @@ __device__ __forceinline__ uint32_t quad_include_nibble(uint32_t w, int lim) {
 }
 
 template <bool SMEM_STATES>
-__device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, int c0,
+__device__ __forceinline__ void feedback_simd_v1(const TrainK &k, const Smem &s, int c0,
                                               const uint32_t *lit, int n_work, Counters &cn) {
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int QP = k.Ppad >> 2;  // quads per (padded) row; multiple of 32
@@ -579,6 +596,147 @@ __device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, in
                 if (old != m) {
                     s.masks[j * k.MW + wd] = m;
                     atomicAdd(&s.cnt[j], __popc(m) - __popc(old));
+                }
+            }
+        }
+        rem += nthr;
+        while (rem >= QP) {
+            rem -= QP;
+            ++wc;
+        }
+    }
+    cn.draws += nd;
+    cn.upd += nupd;
+}
+
+// feedback_simd, second cut.  A warp's 32 quads share a work row, so the row's
+// event class is warp-uniform and the common one gets its own straight-line
+// path: ONE Type I event on a silent clause (kernels/_numba.py:84-90 with
+// clause_out == 0: every valid position above state_min decrements w.p. 1/s)
+// needs no literal bits, no threshold selection and no increment arithmetic.
+// The pre-shifted thresholds are loop invariants, and the include-mask word is
+// rebuilt only when some state of the warp's 128 positions crossed the include
+// boundary (the sign byte changed) -- the masks always equal the states' signs,
+// so an unchanged sign pattern means an unchanged word.  Same results as
+// feedback_simd_v1 (the microbenchmark compares cycles, the trainers' parity
+// tests the states).
+__device__ __forceinline__ uint32_t quad_silent_type1(uint32_t w, uint32_t vb, uint32_t smin4,
+                                                      uint64_t T_dec, uint64_t z0, unsigned &nd,
+                                                      unsigned &nupd) {
+    const uint32_t above = __vcmpgts4(w, smin4) & vb & 0x01010101u;
+    const uint32_t dn = above & quad_hits<false>(z0, T_dec, T_dec, 0u);
+    nd += __popc(above);
+    nupd += __popc(dn);
+    return swar_dec(w, dn);
+}
+
+// ONE Type I event on a firing clause (kernels/_numba.py:71-83): positions
+// whose literal is 1 increment w.p. (s-1)/s (always with boost), the others
+// decrement w.p. 1/s -- quad_update_simd's Type I branch without the event loop.
+__device__ __forceinline__ uint32_t quad_firing_type1(const TrainK &k, uint32_t w, uint32_t litn,
+                                                      uint32_t vb, uint64_t z0, unsigned &nd,
+                                                      unsigned &nupd) {
+    const uint32_t smin4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smin;
+    const uint32_t smax4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smax;
+    const uint32_t boostm = k.fp.boost ? 0xFFFFFFFFu : 0u;
+    const uint32_t incb = spread4(litn) & vb;
+    const uint32_t hit = quad_hits<true>(z0, k.fp.t_dec << 11, k.fp.t_inc << 11, incb);
+    const uint32_t room = __vcmplts4(w, smax4), above = __vcmpgts4(w, smin4);
+    nd += __popc(((incb & room & ~boostm) | (~incb & above & vb)) & 0x01010101u);
+    const uint32_t up = incb & room & (boostm | hit) & 0x01010101u;
+    const uint32_t dn = ~incb & vb & above & hit & 0x01010101u;
+    nupd += __popc(up | dn);
+    return swar_dec(swar_inc(w, up), dn);
+}
+// ONE Type II event on a firing clause (kernels/_numba.py:93-98): excluded
+// positions whose literal is 0 move one step towards inclusion; no draws.
+__device__ __forceinline__ uint32_t quad_type2(uint32_t w, uint32_t litn, uint32_t vb,
+                                               unsigned &nupd) {
+    const uint32_t up = ~spread4(litn) & vb & __vcmplts4(w, 0u) & 0x01010101u;
+    nupd += __popc(up);
+    return swar_inc(w, up);
+}
+// Warp-uniform class of a work row's events: 1 one Type I event on a silent
+// clause, 2 one Type I event on a firing clause, 3 one Type II event (firing),
+// 0 anything else (both events) -- the general quad_update_simd.
+__device__ __forceinline__ int fb_class(int info) {
+    const int e = info & (I_TEV | I_NEV);
+    if (e == (I_TEV | I_NEV) || e == 0) return 0;
+    const bool t1 = e == I_TEV ? (info & I_T1) : (info & I_N1);
+    if (!(info & I_OUT)) return t1 ? 1 : 0;
+    return t1 ? 2 : 3;
+}
+
+template <bool SMEM_STATES>
+__device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, int c0,
+                                              const uint32_t *lit, int n_work, Counters &cn) {
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
+    const int QP = k.Ppad >> 2;  // quads per (padded) row; multiple of 32
+    const int total = n_work * QP;
+    int wc = tid / QP, rem = tid - (tid / QP) * QP;
+    const uint64_t T_dec = k.fp.t_dec << 11;
+    const uint32_t smin4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smin;
+    unsigned nd = 0, nupd = 0;
+    for (int it = tid; it < total; it += nthr) {  // warp-uniform: a warp's quads share a row
+        const int j = s.work[wc], p0 = rem << 2;
+        uint32_t word = 0xFFFFFFFFu;
+        int8_t *grow = SMEM_STATES ? nullptr : k.states + (int64_t)(c0 + j) * k.P;
+        if (SMEM_STATES) {
+            word = *reinterpret_cast<const uint32_t *>(s.states + (size_t)j * k.Ppad + p0);
+        } else if (k.vec4 && p0 + 4 <= k.P) {
+            word = __ldcg(reinterpret_cast<const unsigned int *>(grow + p0));
+        } else {
+            for (int b = 0; b < 4; ++b)
+                if (p0 + b < k.P)
+                    word = (word & ~(0xFFu << (8 * b))) | ((uint32_t)(uint8_t)grow[p0 + b] << (8 * b));
+        }
+        const int info = s.info[j];
+        const int lim = k.P - p0;
+        const uint64_t zp = kGolden * (uint64_t)p0;
+        uint32_t w;
+        const int cls = fb_class(info);
+        const uint32_t vb = lim >= 4 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
+        if (cls == 1) {
+            w = quad_silent_type1(word, vb, smin4, T_dec, ((info & I_TEV) ? s.sk_t[j] : s.sk_n[j]) + zp,
+                                  nd, nupd);
+        } else {
+            const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
+            if (cls == 2) {
+                w = quad_firing_type1(k, word, litn, vb, ((info & I_TEV) ? s.sk_t[j] : s.sk_n[j]) + zp,
+                                      nd, nupd);
+            } else if (cls == 3) {
+                w = quad_type2(word, litn, vb, nupd);
+            } else {
+                w = quad_update_simd(k, word, info, litn, lim, (info & I_TEV) ? s.sk_t[j] + zp : 0,
+                                     (info & I_NEV) ? s.sk_n[j] + zp : 0, nd);
+                nupd += __popc(__vcmpne4(w, word) & 0x01010101u);
+            }
+        }
+        if (w != word) {
+            if (SMEM_STATES) {
+                *reinterpret_cast<uint32_t *>(s.states + (size_t)j * k.Ppad + p0) = w;
+            } else if (k.vec4 && p0 + 4 <= k.P) {
+                __stcg(reinterpret_cast<unsigned int *>(grow + p0), w);
+            } else {
+                for (int b = 0; b < 4; ++b)
+                    if (p0 + b < k.P) grow[p0 + b] = (int8_t)(w >> (8 * b));
+            }
+        }
+        // mask word for positions 32w..32w+31 (lanes 8g..8g+7 hold its
+        // nibbles), only when an include bit of the warp's positions flipped
+        if (__any_sync(0xffffffffu, ((w ^ word) & 0x80808080u) != 0)) {
+            uint32_t m = quad_include_nibble(w, lim) << ((lane & 7) * 4);
+            m |= __shfl_xor_sync(0xffffffffu, m, 1);
+            m |= __shfl_xor_sync(0xffffffffu, m, 2);
+            m |= __shfl_xor_sync(0xffffffffu, m, 4);
+            if ((lane & 7) == 0) {
+                const int wd = p0 >> 5;
+                if (wd < k.W) {
+                    const uint32_t old = s.masks[j * k.MW + wd];
+                    if (old != m) {
+                        s.masks[j * k.MW + wd] = m;
+                        atomicAdd(&s.cnt[j], __popc(m) - __popc(old));
+                    }
                 }
             }
         }
@@ -691,6 +849,17 @@ __device__ __forceinline__ void feedback_wide(const TrainK &k, const Smem &s,
     cn.upd += nupd;
 }
 
+// Cost weight of a work item for the balanced split (relative SM time of its
+// quads: a Type II event has no draws, Type I on a silent clause runs the
+// straight-line decrement path, Type I on a firing clause the general one).
+__device__ __forceinline__ int gbal_weight(const TrainK &k, int info) {
+    const int out = (info & I_OUT) ? 1 : 0;
+    int w = 0;
+    if (info & I_TEV) w += (info & I_T1) ? k.gbw[1 + out] : out * k.gbw[0];
+    if (info & I_NEV) w += (info & I_N1) ? k.gbw[1 + out] : out * k.gbw[0];
+    return w > 0 ? w : 1;
+}
+
 // Grid-balanced feedback (HBM-resident states): this CTA's share
 // [q_begin, q_end) of the quads of all CTAs' work items (the union of the
 // published work lists in CTA order; q_begin, q_end multiples of 32, so a
@@ -704,6 +873,8 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int QP = k.Ppad >> 2;
     unsigned nd = 0, nupd = 0;
+    const uint64_t T_dec = k.fp.t_dec << 11;
+    const uint32_t smin4 = 0x01010101u * (uint32_t)(uint8_t)k.fp.smin;
     // quad it = (work item g_lo + gnext, quad rem) advanced by nthr per unit
     // without a division (nthr < QP is not assumed: a short loop)
     int gnext = (int)((q_begin + tid) / QP - g_lo);
@@ -743,14 +914,30 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
             const int g = gi[u], p0 = pp[u];
             const int c = s.rc_clause[g];
             const int info = s.rc_info[g];
-            const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
             const int lim = k.P - p0;
             const uint64_t zp = kGolden * (uint64_t)p0;
-            const uint32_t nw = quad_update_simd(k, word[u], info, litn, lim,
-                                                 (info & I_TEV) ? s.rc_sk[2 * g] + zp : 0,
-                                                 (info & I_NEV) ? s.rc_sk[2 * g + 1] + zp : 0, nd);
-            nupd += __popc(__vcmpne4(nw, word[u]) & 0x01010101u);
-            const uint32_t nib = quad_include_nibble(nw, lim);
+            const int cls = fb_class(info);
+            const uint32_t vb = lim >= 4 ? 0xFFFFFFFFu
+                                         : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
+            uint32_t nw;
+            // warp-uniform: a warp's quads share a work item (see feedback_simd)
+            if (cls == 1) {
+                nw = quad_silent_type1(word[u], vb, smin4, T_dec,
+                                       s.rc_sk[2 * g + ((info & I_TEV) ? 0 : 1)] + zp, nd, nupd);
+            } else {
+                const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
+                if (cls == 2) {
+                    nw = quad_firing_type1(k, word[u], litn, vb,
+                                           s.rc_sk[2 * g + ((info & I_TEV) ? 0 : 1)] + zp, nd, nupd);
+                } else if (cls == 3) {
+                    nw = quad_type2(word[u], litn, vb, nupd);
+                } else {
+                    nw = quad_update_simd(k, word[u], info, litn, lim,
+                                          (info & I_TEV) ? s.rc_sk[2 * g] + zp : 0,
+                                          (info & I_NEV) ? s.rc_sk[2 * g + 1] + zp : 0, nd);
+                    nupd += __popc(__vcmpne4(nw, word[u]) & 0x01010101u);
+                }
+            }
             if (nw != word[u]) {
                 int8_t *grow = k.states + (int64_t)c * k.P;
                 if (k.vec4 && p0 + 4 <= k.P) {
@@ -760,14 +947,20 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
                         if (p0 + b < k.P) __stcg(grow + p0 + b, (int8_t)(nw >> (8 * b)));
                 }
             }
-            // mask word for positions 32w..32w+31: lanes 8g..8g+7 hold its nibbles
-            uint32_t m = nib << ((lane & 7) * 4);
-            m |= __shfl_xor_sync(0xffffffffu, m, 1);
-            m |= __shfl_xor_sync(0xffffffffu, m, 2);
-            m |= __shfl_xor_sync(0xffffffffu, m, 4);
-            if ((lane & 7) == 0) {
-                const int w = p0 >> 5;
-                if (w < k.W) __stcg(&k.gmask[(int64_t)c * k.W + w], m);
+            // mask word for positions 32w..32w+31 (lanes 8g..8g+7 hold its
+            // nibbles), only when an include bit of the warp's positions
+            // flipped: k.gmask holds every clause's current mask (k_train
+            // writes the own rows at launch), so an unchanged word is current
+            if (__any_sync(0xffffffffu, ((nw ^ word[u]) & 0x80808080u) != 0)) {
+                uint32_t m = quad_include_nibble(nw, lim) << ((lane & 7) * 4);
+                m |= __shfl_xor_sync(0xffffffffu, m, 1);
+                m |= __shfl_xor_sync(0xffffffffu, m, 2);
+                m |= __shfl_xor_sync(0xffffffffu, m, 4);
+                if ((lane & 7) == 0) {
+                    const int w = p0 >> 5;
+                    if (w < k.W) __stcg(&k.gmask[(int64_t)c * k.W + w], m);
+                }
+                if (lane == 0) __stcg(&k.gdirty[c], 1u);
             }
         }
     }
@@ -1051,6 +1244,17 @@ __global__ void __launch_bounds__(NT, 1) k_train(TrainK k) {
     const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
 
     const bool gbal = MODE == MODE_GRID && !SMEM_STATES && k.gbal;
+    if (gbal) {
+        // k.gmask mirrors every clause's include mask from the start (the
+        // balanced feedback rewrites only the words whose include bits flip);
+        // ordered before any peer's write by this CTA's first release arrival
+        for (int q = tid; q < cown * k.W; q += nthr) {
+            const int j = q / k.W, w = q - j * k.W;
+            __stcg(&k.gmask[(int64_t)(c0 + j) * k.W + w], s.masks[j * k.MW + w]);
+        }
+        for (int j = tid; j < cown; j += nthr) __stcg(&k.gdirty[c0 + j], 0u);
+        if (tid == 0) s.misc[2] = 0;
+    }
     for (int64_t i = 0; i < k.n_steps; ++i) {
         const uint32_t *lit = (i & 1) ? s.lit1 : s.lit0;
         const int label = s.misc[8 + (int)(i % 3)];
@@ -1060,11 +1264,15 @@ __global__ void __launch_bounds__(NT, 1) k_train(TrainK k) {
         prefetch_issue(k, s, i, pf);
         if (gbal && i > 0) {
             // all CTAs' feedback of step i-1 is done: pull the include masks
-            // of the own clauses it updated, recount them
+            // of the own clauses whose include bits it flipped, recount them
             grid_wait_step(&k.gsync[(i - 1) * 2 + 1], (unsigned)n_cta);  // arrived below
+            PHASE(7);
             const int n_prev = s.misc[0];
             for (int q = warp; q < n_prev; q += nwarps) {
                 const int j = s.work[q];
+                if (__ldcg(&k.gdirty[c0 + j]) == 0u) continue;  // no include bit flipped
+                __syncwarp();
+                if (lane == 0) __stcg(&k.gdirty[c0 + j], 0u);
                 const uint32_t *src = k.gmask + (int64_t)(c0 + j) * k.W;
                 int cnt = 0;
                 for (int w = lane; w < k.W; w += 32) {
@@ -1272,50 +1480,114 @@ __global__ void __launch_bounds__(NT, 1) k_train(TrainK k) {
                 __stcg(&k.gw_sk[2 * o], (unsigned long long)s.sk_t[j]);
                 __stcg(&k.gw_sk[2 * o + 1], (unsigned long long)s.sk_n[j]);
             }
-            if (tid == 0) __stcg(&k.gcount[rank], n_work);
+            {   // summed cost weight of the own work list
+                int wsum = 0;
+                for (int q = tid; q < n_work; q += nthr) wsum += gbal_weight(k, s.info[s.work[q]]);
+                wsum = __reduce_add_sync(0xffffffffu, wsum);
+                if (lane == 0 && wsum) atomicAdd(&s.misc[2], wsum);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __stcg(&k.gcount[rank], n_work);
+                __stcg(&k.gcount[n_cta + rank], s.misc[2]);
+                s.misc[2] = 0;
+            }
             __syncthreads();
             grid_arrive_step(&k.gsync[i * 2]);
             grid_wait_step(&k.gsync[i * 2], (unsigned)n_cta);
-            if (warp == 0) {
+            if (warp < 2) {  // warp 0: prefix of the counts, warp 1: of the cost weights
+                int *pref = warp == 0 ? s.gpref : s.gwpref;
                 int carry = 0;
                 for (int base = 0; base < n_cta; base += 32) {
                     const int r = base + lane;
-                    const int v = r < n_cta ? __ldcg(&k.gcount[r]) : 0;
+                    const int v = r < n_cta ? __ldcg(&k.gcount[warp * n_cta + r]) : 0;
                     int x = v;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const int y = __shfl_up_sync(0xffffffffu, x, o);
                         if (lane >= o) x += y;
                     }
-                    if (r < n_cta) s.gpref[r] = carry + x - v;
+                    if (r < n_cta) pref[r] = carry + x - v;
                     carry += __shfl_sync(0xffffffffu, x, 31);
                 }
-                if (lane == 0) s.gpref[n_cta] = carry;
+                if (lane == 0) pref[n_cta] = carry;
             }
             __syncthreads();
-            const int QP = k.Ppad >> 2;
-            const int64_t units = (int64_t)s.gpref[n_cta] * (QP >> 5);
-            const int64_t q_begin = 32 * (units * rank / n_cta);
-            const int64_t q_end = 32 * (units * (rank + 1) / n_cta);
-            const int64_t g_lo = q_begin / QP;
-            const int n_rc = q_end > q_begin ? (int)((q_end - 1) / QP - g_lo + 1) : 0;
-            for (int t = tid; t < n_rc; t += nthr) {
-                const int g = (int)(g_lo + t);
-                int lo = 0, hi = n_cta;  // owner r: gpref[r] <= g < gpref[r + 1]
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (s.gpref[mid] <= g) lo = mid;
-                    else hi = mid;
+            // This CTA's share: the union's 32-quad units (work items in CTA
+            // order, quads in row order), each unit weighted by its item's
+            // cost, cut at the weighted positions X(rank), X(rank + 1) -- every
+            // CTA computes the same cuts.  Warp 0 locates X(rank), warp 1
+            // X(rank + 1): owner CTA by the weight prefix, item by a scan of
+            // that CTA's published infos, unit = offset / item weight.
+            const int QP = k.Ppad >> 2, U = QP >> 5;
+            if (warp < 2) {
+                const int64_t wt = (int64_t)s.gwpref[n_cta] * U;
+                const int64_t X = wt * (rank + warp) / n_cta;
+                int64_t q = (int64_t)s.gpref[n_cta] * QP;  // X == wt: the end
+                if (X < wt) {
+                    int lo = 0, hi = n_cta;  // owner: gwpref[lo] * U <= X < gwpref[lo + 1] * U
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if ((int64_t)s.gwpref[mid] * U <= X) lo = mid;
+                        else hi = mid;
+                    }
+                    const int cnt = s.gpref[lo + 1] - s.gpref[lo];
+                    int64_t off = X - (int64_t)s.gwpref[lo] * U;  // weighted offset inside the owner's list
+                    int found = -1, unit = 0;
+                    for (int base = 0; base < cnt && found < 0; base += 32) {
+                        const int t = base + lane;
+                        const int w = t < cnt ? gbal_weight(k, __ldcg(&k.gw_info[(int64_t)lo * k.cmax + t])) : 0;
+                        int x = w;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y = __shfl_up_sync(0xffffffffu, x, o);
+                            if (lane >= o) x += y;
+                        }
+                        const int64_t before = (int64_t)(x - w) * U;  // weighted start of item t in this group
+                        const bool here = t < cnt && off >= before && off < before + (int64_t)w * U;
+                        const unsigned bal = __ballot_sync(0xffffffffu, here);
+                        if (bal) {
+                            const int src = __ffs(bal) - 1;
+                            found = base + src;
+                            unit = (int)((off - __shfl_sync(0xffffffffu, before, src)) /
+                                         __shfl_sync(0xffffffffu, w, src));
+                        } else {
+                            off -= (int64_t)__shfl_sync(0xffffffffu, x, 31) * U;
+                        }
+                    }
+                    if (found >= 0) q = ((int64_t)s.gpref[lo] + found) * QP + 32 * (int64_t)unit;
                 }
-                const int64_t o = (int64_t)lo * k.cmax + (g - s.gpref[lo]);
-                s.rc_clause[t] = __ldcg(&k.gw_clause[o]);
-                s.rc_info[t] = __ldcg(&k.gw_info[o]);
-                s.rc_sk[2 * t] = __ldcg(&k.gw_sk[2 * o]);
-                s.rc_sk[2 * t + 1] = __ldcg(&k.gw_sk[2 * o + 1]);
+                if (lane == 0) s.gcut[warp] = q;
             }
             __syncthreads();
-            if (!(k.dbg & 1))  // 1024 threads: half the words in flight per thread
-                feedback_quads_global<(NT > 512 ? 2 : 4)>(k, s, lit, q_begin, q_end, g_lo, cn);
+            const int64_t q_begin = s.gcut[0], q_end = s.gcut[1];
+            // the share's work items are staged cmax + 4 at a time (a share of
+            // cheap items can hold more items than any CTA owns)
+            const int rc_cap = k.cmax + 4;
+            for (int64_t g_lo = q_begin / QP; g_lo * QP < q_end; g_lo += rc_cap) {
+                const int64_t g_hi = (q_end - 1) / QP;  // last item of the share
+                const int n_rc = (int)((g_hi - g_lo + 1) < rc_cap ? (g_hi - g_lo + 1) : rc_cap);
+                for (int t = tid; t < n_rc; t += nthr) {
+                    const int g = (int)(g_lo + t);
+                    int lo = 0, hi = n_cta;  // owner r: gpref[r] <= g < gpref[r + 1]
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (s.gpref[mid] <= g) lo = mid;
+                        else hi = mid;
+                    }
+                    const int64_t o = (int64_t)lo * k.cmax + (g - s.gpref[lo]);
+                    s.rc_clause[t] = __ldcg(&k.gw_clause[o]);
+                    s.rc_info[t] = __ldcg(&k.gw_info[o]);
+                    s.rc_sk[2 * t] = __ldcg(&k.gw_sk[2 * o]);
+                    s.rc_sk[2 * t + 1] = __ldcg(&k.gw_sk[2 * o + 1]);
+                }
+                __syncthreads();
+                const int64_t qa = q_begin > g_lo * QP ? q_begin : g_lo * QP;
+                const int64_t qb = q_end < (g_lo + n_rc) * QP ? q_end : (g_lo + n_rc) * QP;
+                if (!(k.dbg & 1))  // 1024 threads: half the words in flight per thread
+                    feedback_quads_global<(NT > 512 ? 2 : 4)>(k, s, lit, qa, qb, g_lo, cn);
+                __syncthreads();
+            }
             prefetch_commit(k, s, i, pf);
             __syncthreads();
             // feedback done: the next step waits on it
@@ -2593,6 +2865,9 @@ int g_train_spec_ent = 64;
 // grid trainer when the caller leaves it to the library (512 | 1024, read at
 // create); 1024 measured 9% faster on configs[3] (2.44 -> 2.65 k ex/s)
 int g_train_hbm_threads = 1024;
+// tmb_set_option("train.gbal_weights"): cost weights of the balanced feedback's
+// split, bytes 0..2 = Type II / Type I silent / Type I firing (0 = unweighted)
+int g_train_gbw = 2 | (5 << 8) | (6 << 16);
 }
 
 namespace {
@@ -2781,23 +3056,27 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
 
     k.states = states; k.weights = weights; k.block_counters = block_counters;
     k.gbal = (k.gbal && !k.fast && !smem_states) ? 1 : 0;
+    for (int q = 0; q < 3; ++q) k.gbw[q] = g_train_gbw ? ((g_train_gbw >> (8 * q)) & 255) : 1;
+    for (int q = 0; q < 3; ++q) k.gbw[q] = k.gbw[q] > 0 ? k.gbw[q] : 1;
     if (k.gbal) {
         const size_t n_w = (size_t)n_cta * k.cmax;
-        const size_t bytes = align_up(4 * (size_t)n_cta, 256) + 2 * align_up(4 * n_w, 256) +
-                             align_up(16 * n_w, 256) + 4 * (size_t)C * W;
+        const size_t bytes = align_up(8 * (size_t)n_cta, 256) + 2 * align_up(4 * n_w, 256) +
+                             align_up(16 * n_w, 256) + align_up(4 * (size_t)C, 256) + 4 * (size_t)C * W;
         if ((rc = check_cuda(cudaMalloc(&t->gbal_d, bytes), "cudaMalloc"))) {
             tmb_trainer_destroy(t);
             return rc;
         }
         char *b = (char *)t->gbal_d;
         k.gcount = (int *)b;
-        b += align_up(4 * (size_t)n_cta, 256);
+        b += align_up(8 * (size_t)n_cta, 256);
         k.gw_clause = (int *)b;
         b += align_up(4 * n_w, 256);
         k.gw_info = (int *)b;
         b += align_up(4 * n_w, 256);
         k.gw_sk = (uint64_t *)b;
         b += align_up(16 * n_w, 256);
+        k.gdirty = (unsigned *)b;
+        b += align_up(4 * (size_t)C, 256);
         k.gmask = (uint32_t *)b;
     }
     t->k = k;
@@ -2963,7 +3242,7 @@ __global__ void __launch_bounds__(1024, 1) k_mb_feedback(TrainK k, int n_work, i
     for (int i = tid; i < k.cmax * k.MW; i += nthr) s.masks[i] = 0;
     for (int j = tid; j < k.cmax; j += nthr) {
         s.work[j] = j;
-        s.info[j] = I_OUT | I_TEV | I_T1 | (two ? (I_NEV | I_N1) : 0);
+        s.info[j] = ((two & 2) ? 0 : I_OUT) | I_TEV | I_T1 | ((two & 1) ? (I_NEV | I_N1) : 0);
         s.sk_t[j] = mix64(j);
         s.sk_n[j] = mix64(j + 100);
         s.cnt[j] = 0;
@@ -2981,7 +3260,8 @@ __global__ void __launch_bounds__(1024, 1) k_mb_feedback(TrainK k, int n_work, i
         else if (VARIANT == 3) feedback_compact<true, 2>(k, s, 0, lit, n_work, cn);
         else if (VARIANT == 4) feedback_compact<true, 4>(k, s, 0, lit, n_work, cn);
         else if (VARIANT == 5) feedback_compact<true, 7>(k, s, 0, lit, n_work, cn);
-        else if (VARIANT == 6) feedback_simd<true>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 6) feedback_simd_v1<true>(k, s, 0, lit, n_work, cn);
+        else if (VARIANT == 11) feedback_simd<true>(k, s, 0, lit, n_work, cn);
         else if (VARIANT == 7) feedback_wide<4, 1>(k, s, lit, n_work, cn);
         else if (VARIANT == 8) feedback_wide<4, 4>(k, s, lit, n_work, cn);
         else if (VARIANT == 9) feedback_wide<2, 1>(k, s, lit, n_work, cn);
@@ -3008,13 +3288,13 @@ extern "C" int tmb_microbench_feedback(int variant, int n_work, int two_events, 
     const size_t sm = smem_layout(k, true, MODE_GRID, nullptr, nullptr);
     unsigned long long *cyc = nullptr;
     TMB_CUDA(cudaMalloc(&cyc, 8));
-    const void *fns[11] = {(const void *)k_mb_feedback<0>, (const void *)k_mb_feedback<1>,
+    const void *fns[12] = {(const void *)k_mb_feedback<0>, (const void *)k_mb_feedback<1>,
                            (const void *)k_mb_feedback<2>, (const void *)k_mb_feedback<3>,
                            (const void *)k_mb_feedback<4>, (const void *)k_mb_feedback<5>,
                            (const void *)k_mb_feedback<6>, (const void *)k_mb_feedback<7>,
                            (const void *)k_mb_feedback<8>, (const void *)k_mb_feedback<9>,
-                           (const void *)k_mb_feedback<10>};
-    if (variant < 0 || variant > 10) return fail(TMB_E_INVALID, "microbench_feedback: variant 0..10");
+                           (const void *)k_mb_feedback<10>, (const void *)k_mb_feedback<11>};
+    if (variant < 0 || variant > 11) return fail(TMB_E_INVALID, "microbench_feedback: variant 0..11");
     TMB_CUDA(cudaFuncSetAttribute(fns[variant], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     void *args[] = {&k, &n_work, &two_events, &iters, &cyc};
     TMB_CUDA(cudaLaunchKernel(fns[variant], dim3(1), dim3(threads), args, sm, 0));

@@ -11,8 +11,8 @@ from paper_2405_04212_b200 import _lib  # noqa: E402
 
 out = {}
 for threads in (512,):
-    for variant in (0, 6, 7, 8, 9, 10):
-        for two in (0, 1):
+    for variant in [int(v) for v in sys.argv[1:]] or (0, 6, 7, 8, 9, 10, 11):
+        for two in (0, 1, 2):
             for nw in (1, 2, 3, 4, 8):
                 c = ct.c_double()
                 _lib.call("tmb_microbench_feedback", variant, nw, two, threads, 200, ct.byref(c))

@@ -14,7 +14,7 @@ for a in sys.argv[1:]:
     _lib.load()
     _lib.call("tmb_set_option", n.encode(), int(v))
 NAMES = ["eval(+votes)", "arrive", "precompute", "wait+decide", "flag bitmaps",
-         "scan+events", "feedback", "-"]
+         "scan+events", "feedback", "wait for all CTAs' feedback"]
 (tx, ty), _ = datasets.bag_of_words(n_train=6000, n_test=10)
 cfg = tmb.Config(**datasets.bag_of_words_config_kwargs(seed=0))
 sess = tmb.DenseTrainSession(cfg, tx, ty)
