@@ -21,7 +21,7 @@ timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_t
     -o $OUT/${TAG}_prof_train python bench.py --steps 1 --warmup 3 --no-secondary --no-cpu-baseline > $OUT/${TAG}_ncu_train.log 2>&1
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_infer_solo -s 3 -c 1 \
     -o $OUT/${TAG}_prof_infer python bench.py --workload c3-infer --steps 1 --warmup 3 --no-cpu-baseline > $OUT/${TAG}_ncu_infer.log 2>&1
-timeout 1500 ncu --set full --import-source on --clock-control none -k k_train -s 3 -c 1 \
+[ -n "${SKIP_C4_NCU:-}" ] || timeout 1500 ncu --set full --import-source on --clock-control none -k k_train -s 3 -c 1 \
     -o $OUT/${TAG}_prof_c4train python bench.py --workload c4-train --steps 1 --warmup 3 --no-cpu-baseline > $OUT/${TAG}_ncu_c4.log 2>&1
 timeout 1500 ncu --set full --import-source on --clock-control none -k regex:k_sparse_train -s 3 -c 1 \
     -o $OUT/${TAG}_prof_c5train python bench.py --workload c5-sparse --steps 1 --warmup 3 --no-cpu-baseline > $OUT/${TAG}_ncu_c5train.log 2>&1
