@@ -232,7 +232,8 @@ int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_b
                      int *states_in_smem);
 /* Which fused trainer runs (for reporting): *kind 0 k_train_warp (one warp),
  * 1 k_train cluster mode, 2 k_train grid mode, 3 k_train_fast, 4 k_train_spec
- * (speculative windows of *window steps, else 0). */
+ * (speculative windows of *window steps, else 0), 5 k_train_tiny (tiny banks,
+ * one warp per clause). */
 int tmb_trainer_kernel(const tmb_trainer *t, int *kind, int *window);
 /* Run n_steps examples: example i uses literal row lit_words[order[i]] (device
  * uint32 [N, W]) and label labels[order[i]] (device int32); the feedback

@@ -77,6 +77,7 @@ extern int g_train_dbg;  // trainer timing ablations (tmb_train.cu)
 extern int g_train_spec;  // speculative window of the fast grid trainer (tmb_train.cu)
 extern int g_train_spec_ent;  // staged flag entries per step head (0 = auto)
 extern int g_train_hbm_threads;  // CTA size of the HBM-state grid trainer
+extern int g_train_tiny;         // tiny banks: one warp per clause (k_train_tiny) instead of one warp
 extern int g_train_gbw;          // balanced-feedback cost weights (packed bytes)
 //  // keyed trainer: steps per launch override (tmb_train.cu)
 

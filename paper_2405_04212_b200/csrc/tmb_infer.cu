@@ -1616,6 +1616,10 @@ int tmb_set_option(const char *name, int64_t value) {
         g_train_hbm_threads = (int)value;
         return TMB_OK;
     }
+    if (std::string(name) == "train.tiny") {  // 1 (default): k_train_tiny for tiny banks, 0: k_train_warp
+        g_train_tiny = (int)value;
+        return TMB_OK;
+    }
     if (std::string(name) == "train.gbal_weights") {  // packed bytes: Type II, Type I silent, Type I firing
         g_train_gbw = (int)value;
         return TMB_OK;

@@ -1121,6 +1121,9 @@ __device__ __forceinline__ void decide(const TrainK &k, long long vl, long long 
 }
 
 __device__ __forceinline__ int negative_class(const TrainK &k, int label, uint64_t fbc) {
+    // two classes: u * (K - 1) < 1 whatever the draw, so it need not be
+    // evaluated (the stream is random-access, core.py:7-10)
+    if (k.K == 2) return label ^ 1;
     const double u = u01_from53(draw53(k.fb_seed, fbc));
     int neg = label + 1 + (int)(u * (double)(k.K - 1));  // < 2K
     return neg >= k.K ? neg - k.K : neg;
@@ -2781,6 +2784,152 @@ __global__ void __launch_bounds__(32, 1) k_train_warp(TrainK k) {
     flush_stats(k, cn, true);
 }
 
+// One warp per clause for the same tiny banks (C <= 32 clauses -> a CTA of C
+// warps, K <= 32, literal rows <= 32 words), ONE block barrier per example.
+// Warp c owns clause c: lane r keeps include-mask word r, lane kk the weight
+// of class kk, the states live in the warp's own shared-memory row.  Per
+// step every warp publishes its clause's contribution to the label / negative
+// class sums (double-buffered by step parity), the barrier, then every warp
+// derives -- redundantly, lane per clause -- the sums, the thresholds, all 2C
+// update flags and the event ordinals (feedback.py:33-53,
+// kernels/_numba.py:101-125) and applies its own clause's events over the
+// lanes.  k_train_warp serialises the step's events (a dependent chain of
+// ~5 000 instructions on one warp); here they run side by side.  Same
+// arithmetic and draw addressing, bit-identical results.
+__global__ void __launch_bounds__(32 * kWarpMaxC, 1) k_train_tiny(TrainK k) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+    const int C = k.C, P = k.P, K = k.K, W = k.W, nb = k.n_blocks;
+    const int Pp = (P + 3) & ~3;
+    int8_t *st = reinterpret_cast<int8_t *>(smem_raw) + (size_t)c * Pp;  // own row
+    int2 *pub = reinterpret_cast<int2 *>(smem_raw + align_up((size_t)C * Pp, 16));  // [2][32]
+    for (int p = lane; p < P; p += 32) st[p] = k.states[(int64_t)c * P + p];
+    int wreg = lane < K ? k.weights[c * K + lane] : 0;
+    __syncwarp();
+    uint32_t mword = 0;  // lane r: include-mask word r
+    int cnt = 0;
+    auto rebuild = [&]() {
+        int n = 0;
+        for (int r = 0; r < W; ++r) {
+            const int p = 32 * r + lane;
+            const unsigned m = __ballot_sync(0xffffffffu, p < P && st[p] >= 0);
+            if (lane == r) mword = m;
+            n += __popc(m);
+        }
+        cnt = n;
+    };
+    rebuild();
+    // lane c2 stands for clause c2: every warp derives every clause's flags
+    // and the ordinals of its own block
+    const bool real = lane < C;
+    const int myb = block_of(c, C, nb);
+    const int mybs = block_begin(myb, C, nb), mybe = block_begin(myb + 1, C, nb);
+    const uint64_t bseed = k.block_seeds[myb];
+    uint64_t myctr = k.block_counters[myb];  // event counter of the own clause's block
+    const unsigned long long step_draws = 1ull + 2ull * (unsigned long long)C;
+    Counters cn;
+    int ex_n = k.n_steps > 0 ? __ldg(&k.order[0]) : 0;
+    int label_n = k.n_steps > 0 ? __ldg(&k.labels[ex_n]) : 0;
+    uint32_t litw_n = (k.n_steps > 0 && lane < W) ? __ldg(&k.lit_words[(int64_t)ex_n * W + lane]) : 0u;
+    int ex_nn = k.n_steps > 1 ? __ldg(&k.order[1]) : 0;
+    for (int64_t i = 0; i < k.n_steps; ++i) {
+        const int label = label_n;
+        const uint32_t litw = litw_n;
+        if (i + 1 < k.n_steps) {
+            label_n = __ldg(&k.labels[ex_nn]);
+            litw_n = lane < W ? __ldg(&k.lit_words[(int64_t)ex_nn * W + lane]) : 0u;
+            ex_nn = i + 2 < k.n_steps ? __ldg(&k.order[i + 2]) : 0;
+        }
+        const uint64_t fbc = k.fb_counter0 + (uint64_t)i * step_draws;
+        const int neg = negative_class(k, label, fbc);
+        // 1. own clause's training-mode output (kernels/_numba.py:36-50) and
+        //    its contribution to the two class sums (dense.py:153)
+        const bool out = !__any_sync(0xffffffffu, lane < W && (mword & ~litw) != 0u) && cnt <= k.budget;
+        const int w_l = __shfl_sync(0xffffffffu, wreg, label), w_n = __shfl_sync(0xffffffffu, wreg, neg);
+        int2 *pb = pub + (i & 1) * 32;
+        if (lane == 0) pb[c] = make_int2(out ? w_l : 0, out ? w_n : 0);
+        // the flag draws do not depend on the sums: before the barrier
+        const uint64_t d_t = real ? draw53(k.fb_seed, fbc + 1 + (uint64_t)lane) : ~0ull;
+        const uint64_t d_n = real ? draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)lane) : ~0ull;
+        __syncthreads();
+        // 2. class sums, decision, every clause's flags (feedback.py:33-53)
+        const int2 pv = real ? pb[lane] : make_int2(0, 0);
+        long long vl, vn;
+        warp_sum2(pv.x, pv.y, vl, vn);
+        uint64_t tt, tn;
+        if (k.thr_tab) {
+            const long long T = k.T;
+            const long long cl = vl < -T ? -T : (vl > T ? T : vl);
+            const long long cv = vn < -T ? -T : (vn > T ? T : vn);
+            tt = __ldg(&k.thr_tab[T - cl]);
+            tn = __ldg(&k.thr_tab[T + cv]);
+        } else {
+            decide(k, vl, vn, tt, tn);
+        }
+        // 3. every clause's flags as two ballots; event ordinals within the
+        //    clause block (kernels/_numba.py:101-125) by population counts
+        const unsigned bt = __ballot_sync(0xffffffffu, real && d_t < tt);
+        const unsigned bn = __ballot_sync(0xffffffffu, real && d_n < tn);
+        const unsigned below_me = (1u << c) - 1u, below_blk = (1u << mybs) - 1u;
+        const unsigned blk = (mybe >= 32 ? 0xFFFFFFFFu : (1u << mybe) - 1u) & ~below_blk;
+        const uint64_t ord = myctr + (uint64_t)(__popc(bt & below_me & ~below_blk) +
+                                                __popc(bn & below_me & ~below_blk));
+        myctr += (uint64_t)(__popc(bt & blk) + __popc(bn & blk));
+        const bool ut = (bt >> c) & 1u, un = (bn >> c) & 1u;
+        if (!(ut || un)) continue;
+        // 4. own clause's event types and weights (feedback first: SPEC.md:171)
+        const bool t1 = w_l >= 0, n1 = w_n < 0;
+        if (lane == 0) {
+            if (ut) { ++cn.events; if (t1) ++cn.t1; else if (out) ++cn.t2; }
+            if (un) { ++cn.events; if (n1) ++cn.t1; else if (out) ++cn.t2; }
+        }
+        if (out) {
+            if (ut && lane == label) wreg += 1;
+            if (un && lane == neg) wreg -= 1;
+        }
+        // 5. per-position feedback when a state can move
+        if (!((ut && (t1 || out)) || (un && (n1 || out)))) continue;
+        unsigned nd = 0, nupd = 0;
+        const int jo = out ? 1 : 0;
+        for (int r = 0; r < W; ++r) {
+            const int p = 32 * r + lane;
+            const uint32_t lw = __shfl_sync(0xffffffffu, litw, r);
+            if (p >= P) continue;
+            const int lit = (lw >> lane) & 1;
+            const int s0 = st[p];
+            int sv = s0;
+            uint64_t d = 0;
+            if (ut) {
+                if (t1) sv = type_i_stream(sv, lit, jo, k.fp, bseed + kGolden * ((ord << 32) + 1),
+                                           (uint32_t)p, d);
+                else sv = type_ii(sv, lit, jo);
+            }
+            if (un) {
+                const uint64_t o2 = ord + (ut ? 1 : 0);
+                if (n1) sv = type_i_stream(sv, lit, jo, k.fp, bseed + kGolden * ((o2 << 32) + 1),
+                                           (uint32_t)p, d);
+                else sv = type_ii(sv, lit, jo);
+            }
+            nd += (unsigned)d;
+            nupd += sv != s0 ? 1u : 0u;
+            st[p] = (int8_t)sv;
+        }
+        __syncwarp();
+        rebuild();
+        cn.draws += nd;
+        cn.upd += nupd;
+    }
+    __syncwarp();
+    for (int p = lane; p < P; p += 32) k.states[(int64_t)c * P + p] = st[p];
+    if (lane < K) k.weights[c * K + lane] = wreg;
+    if (lane == 0 && c == mybe - 1) k.block_counters[myb] = myctr;
+    flush_stats(k, cn, threadIdx.x == 0);
+}
+
+size_t tiny_kernel_smem(int C, int P) {
+    return align_up((size_t)C * (size_t)((P + 3) & ~3), 16) + 2 * 32 * sizeof(int2);
+}
+
 size_t warp_kernel_smem(int C, int P, int K, int W, int nb) {
     const size_t Pp = (size_t)((P + 3) & ~3);
     return align_up(align_up((size_t)C * Pp, 16) + 4 * (size_t)C * W + 4 * (size_t)C * K, 8) +
@@ -2797,7 +2946,7 @@ struct tmb_trainer {
     int32_t *weights;
     uint64_t *block_counters;
     int n_cta, threads, smem, smem_states, cluster;
-    int warp = 0;  // k_train_warp (one warp, tiny banks)
+    int warp = 0;  // tiny banks: 1 k_train_warp (one warp), 2 k_train_tiny (one warp per clause)
     uint64_t launches = 0;
     TrainK k;
     uint64_t *block_seeds_d = nullptr;
@@ -2865,6 +3014,7 @@ int g_train_spec_ent = 64;
 // grid trainer when the caller leaves it to the library (512 | 1024, read at
 // create); 1024 measured 9% faster on configs[3] (2.44 -> 2.65 k ex/s)
 int g_train_hbm_threads = 1024;
+int g_train_tiny = 1;  // tmb_set_option("train.tiny"): tiny banks on k_train_tiny (0: k_train_warp)
 // tmb_set_option("train.gbal_weights"): cost weights of the balanced feedback's
 // split, bytes 0..2 = Type II / Type I silent / Type I firing (0 = unweighted)
 int g_train_gbw = 2 | (5 << 8) | (6 << 16);
@@ -3017,9 +3167,17 @@ int tmb_trainer_create(const tmb_train_cfg *cfg, int8_t *states, int32_t *weight
         TMB_CUDA(cudaFuncSetAttribute((const void *)k_train_warp,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_smem));
 
+    // ... by default with one warp per clause (k_train_tiny); train.tiny 0
+    // keeps the single-warp kernel
+    const bool tiny_k = warp_k && g_train_tiny && tiny_kernel_smem(C, P) <= (size_t)max_smem;
+    if (tiny_k && tiny_kernel_smem(C, P) > 48 * 1024)
+        TMB_CUDA(cudaFuncSetAttribute((const void *)k_train_tiny,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)tiny_kernel_smem(C, P)));
+
     tmb_trainer *t = new tmb_trainer();
     t->cfg = c;
-    t->warp = warp_k ? 1 : 0;
+    t->warp = tiny_k ? 2 : warp_k ? 1 : 0;
     t->states = states; t->weights = weights; t->block_counters = block_counters;
     t->n_cta = n_cta; t->threads = threads; t->smem = (int)need;
     t->smem_states = smem_states; t->cluster = cluster;
@@ -3112,7 +3270,7 @@ int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_b
                      int *states_in_smem) {
     if (!t) return fail(TMB_E_INVALID, "trainer_info: NULL");
     if (n_cta) *n_cta = t->n_cta;
-    if (threads) *threads = t->warp ? 32 : t->threads;
+    if (threads) *threads = t->warp == 2 ? 32 * t->k.C : t->warp ? 32 : t->threads;
     if (smem_bytes) *smem_bytes = t->smem;
     if (states_in_smem) *states_in_smem = t->smem_states;
     return TMB_OK;
@@ -3120,7 +3278,7 @@ int tmb_trainer_info(const tmb_trainer *t, int *n_cta, int *threads, int *smem_b
 
 int tmb_trainer_kernel(const tmb_trainer *t, int *kind, int *window) {
     if (!t) return fail(TMB_E_INVALID, "trainer_kernel: NULL");
-    const int kd = t->warp ? 0 : t->cluster ? 1 : !t->k.fast ? 2 : t->k.spec ? 4 : 3;
+    const int kd = t->warp == 2 ? 5 : t->warp ? 0 : t->cluster ? 1 : !t->k.fast ? 2 : t->k.spec ? 4 : 3;
     if (kind) *kind = kd;
     if (window) *window = kd == 4 ? t->k.spec : 0;
     return TMB_OK;
@@ -3139,6 +3297,15 @@ int tmb_trainer_run(tmb_trainer *t, const uint32_t *lit_words, const int32_t *la
     k.n_steps = n_steps; k.fb_counter0 = fb_counter; k.stats = stats;
     k.dbg = g_train_dbg;
     void *args[] = {&k};
+    if (t->warp == 2) {
+        const size_t sm = tiny_kernel_smem(k.C, k.P);
+        if (sm > 48 * 1024)
+            TMB_CUDA(cudaFuncSetAttribute((const void *)k_train_tiny,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_train_tiny<<<1, 32 * k.C, sm, st>>>(k);
+        TMB_LAUNCHED();
+        return TMB_OK;
+    }
     if (t->warp) {
         const size_t sm = warp_kernel_smem(k.C, k.P, k.K, k.W, k.n_blocks);
         if (sm > 48 * 1024)

@@ -107,7 +107,7 @@ def _resolve_jobs(n_jobs: int, n_blocks: int) -> int:
 
 # tmb_trainer_kernel kinds
 TRAINER_KERNELS = ("k_train_warp", "k_train (cluster)", "k_train (grid)", "k_train_fast",
-                   "k_train_spec")
+                   "k_train_spec", "k_train_tiny")
 
 
 class DenseTrainSession:

@@ -804,9 +804,11 @@ def test_train_rejects_non_binary_features(gpu):
     (12, 10, 2, 1, False, None), (6, 8, 2, 2, True, 3), (500, 32, 10, 3, False, 40),
     (31, 17, 4, 5, True, None)])
 def test_single_warp_trainer_vs_oracle(gpu, oracle, F, C, K, nb, boost, budget):
-    """Tiny banks (C, K <= 32, literal rows <= 32 words) run on the
-    single-warp trainer; the generic one-CTA cluster kernel (warp_kernel=
-    False) and the oracle give the same model, counters and statistics."""
+    """Tiny banks (C, K <= 32, literal rows <= 32 words) run on
+    k_train_tiny (one warp per clause, one block barrier per example) or,
+    with train.tiny 0, on the single-warp k_train_warp; both, the generic
+    one-CTA cluster kernel (warp_kernel=False) and the oracle give the same
+    model, counters and statistics."""
     rs = np.random.default_rng(F + C + K)
     x = rs.integers(0, 2, size=(400, F)).astype(np.uint8)
     y = ((x[:, 0] ^ x[:, 1]) + 2 * x[:, 2] * (K > 2)).astype(np.int64) % K
@@ -814,18 +816,24 @@ def test_single_warp_trainer_vs_oracle(gpu, oracle, F, C, K, nb, boost, budget):
                      n_blocks=nb, boost_true_positive=boost, n_literal_budget=budget)
     ost, _ = oracle.train(cfg, x, y, 3)
     stats = []
-    for warp in (True, False):
-        sess = gpu.DenseTrainSession(cfg, x, y, warp_kernel=warp)
-        assert sess.launch["threads"] == (32 if warp else sess.launch["threads"])
-        for _ in range(3):
-            sess.run_epoch()
-        m = sess.model()
-        assert np.array_equal(m.states, ost.states), warp
-        assert np.array_equal(m.weights, ost.weights), warp
-        assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64),
-                              ost.block_counters), warp
-        stats.append(sess.stats_dict())
-    assert stats[0] == stats[1]
+    try:
+        for kernel in ("k_train_tiny", "k_train_warp", None):
+            gpu._lib.call("tmb_set_option", b"train.tiny", int(kernel == "k_train_tiny"))
+            sess = gpu.DenseTrainSession(cfg, x, y, warp_kernel=kernel is not None)
+            if kernel:
+                assert sess.launch["kernel"] == kernel
+                assert sess.launch["threads"] == (32 * C if kernel == "k_train_tiny" else 32)
+            for _ in range(3):
+                sess.run_epoch()
+            m = sess.model()
+            assert np.array_equal(m.states, ost.states), kernel
+            assert np.array_equal(m.weights, ost.weights), kernel
+            assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64),
+                                  ost.block_counters), kernel
+            stats.append(sess.stats_dict())
+    finally:
+        gpu._lib.call("tmb_set_option", b"train.tiny", 1)
+    assert stats[0] == stats[1] == stats[2]
 
 
 @pytest.mark.parametrize("window,n_cta,n_train", [(1, 148, 700), (5, 148, 703), (16, 37, 1500),
