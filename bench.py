@@ -504,7 +504,7 @@ def bench_c1_train(args, rank, world, local):
     s=3.9), 5000 training examples, 20 epochs, evaluated over model seeds
     0..4 (the north star's 5-seed criterion).  Step = the whole 5-seed study:
     five complete 20-epoch trainings, run concurrently -- each session's
-    single-warp trainer on its own CUDA stream, so the five land on five SMs
+    tiny-bank trainer (k_train_tiny) on its own CUDA stream, so the five land on five SMs
     (500 000 examples per step); epoch orders from the host shuffle are
     precomputed.  The per-training latency (one seed's 20 epochs alone on its
     stream) is reported beside it.  e2e = the public train(cfg, train, eval,
@@ -612,15 +612,18 @@ def bench_c1_train(args, rank, world, local):
         "gpu_launches": int(launches),
         "accuracy": {"test_accuracy_per_step": accs, "mean": float(np.mean(accs))},
         "roofline": {"kernel": preps[0][0].launch.get("kernel", "k_train_warp"),
-                     "bound": "latency (one warp: the per-example chain eval -> class sums "
-                              "-> decision -> feedback; no parallelism across examples)",
+                     "bound": "latency (one CTA per training, one warp per clause: the "
+                              "per-example chain eval -> block barrier -> class sums -> "
+                              "decision -> feedback; no parallelism across examples)",
                      "achieved": 1e6 / us_step, "unit": "examples/s",
                      "peak": n_seeds * warp_draw_peak / max(draws_ex, 1e-9),
                      "frac": (1e6 / us_step) * draws_ex / (n_seeds * warp_draw_peak),
                      "draws_per_example": draws_ex,
-                     "peak_note": "the reference draws of an example at the five warps' share "
-                                  "(one scheduler each) of the measured per-SM SplitMix64 draw "
-                                  "rate",
+                     "peak_note": "the reference draws of an example at one scheduler's share "
+                                  "per training of the measured per-SM SplitMix64 draw rate "
+                                  "(k_train_warp's footprint; k_train_tiny spreads a training "
+                                  "over its SM's four schedulers, so the fraction is of a "
+                                  "quarter of the five SMs it occupies)",
                      "peak_source": lp["source"]},
         "clocks": clk.summary(),
         "e2e": {"value": n_ex * world / e2e_s, "unit": "examples/s",
