@@ -289,9 +289,21 @@ int tmb_infer(const tmb_rules *r, const uint8_t *x, int64_t N, int64_t *votes,
  * the last check saw a feature byte other than 0 / 1 (the device path
  * requires binary inputs); clears the flag. */
 int tmb_infer_status(void *stream);
-/* Library options (tests / tuning): "infer.force_generic" = 1 routes
- * tmb_infer to the generic one-CTA-per-tile kernel instead of the 4-CTA
- * cluster kernel. */
+/* Library options (tests / tuning; defaults in brackets).  Inference:
+ * "infer.solo" [1] per-CTA kernel k_infer_solo, 0 the 4-CTA cluster kernels;
+ * "infer.force_generic" [0] 1 routes tmb_infer to the generic
+ * one-CTA-per-tile kernel; "infer.warp_specialized", "infer.eval_mode",
+ * "infer.debug_skip" (timing only), "infer.phase_buffer" (profiling).
+ * Training, read at tmb_trainer_create:
+ * "train.spec_window" [16] steps per speculative window of k_train_spec (0:
+ * k_train_fast); "train.spec_entries" [64] staged flag entries per head;
+ * "train.hbm_threads" [1024] CTA size of the HBM-state grid trainer (512 or
+ * 1024); "train.gbal_weights" [2 | 5 << 8 | 6 << 16] cost weights of the
+ * balanced feedback split (bytes: Type II, Type I silent, Type I firing; 0 =
+ * unweighted); "train.tiny" [1] tiny banks on k_train_tiny (0: k_train_warp);
+ * "train.key_chunk" (tests), "train.debug_skip" (timing only, not
+ * bit-exact).  SparseTM: "sparse.resident", "sparse.infer_key",
+ * "sparse.counters32", "sparse.phase_buffer" (profiling). */
 int tmb_set_option(const char *name, int64_t value);
 /* End-to-end variant with HOST buffers: streams x (host, ideally pinned)
  * through the device in chunks with copy/compute overlap and returns host
