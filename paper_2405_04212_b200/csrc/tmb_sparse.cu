@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
             neg = label + 1 + (int)(u * (double)(K - 1));
             if (neg >= K) neg -= K;
         }
-        if (tid == 0) s.misc[0] = s.misc[1] = 0;
+        if (tid == 0) s.misc[0] = 0;
         __syncthreads();
         SPH(0);
         // 1. training-mode outputs of own clauses (sparse.py:123-138), warp
@@ -750,14 +750,8 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
                         if (t_ev) w[label] += 1;
                         if (n_ev) w[neg] -= 1;
                     }
-                    if ((t_ev && ((info & SI_T1) || out)) || (n_ev && ((info & SI_N1) || out))) {
-                        // firing clauses (Type I with insertions / Type II: the
-                        // long merges) fill the list from the front, silent
-                        // ones from the back: when a CTA has more events than
-                        // warps, a warp's second event is a short one
-                        if (out) s.work[atomicAdd(&s.misc[0], 1)] = j;
-                        else s.work[k.cmax - 1 - atomicAdd(&s.misc[1], 1)] = j;
-                    }
+                    if ((t_ev && ((info & SI_T1) || out)) || (n_ev && ((info & SI_N1) || out)))
+                        s.work[atomicAdd(&s.misc[0], 1)] = j;
                 }
                 s.info[j] = info;
             }
@@ -771,9 +765,9 @@ __global__ void __launch_bounds__(512, 1) k_sparse_train(SparseK k) {
         __syncthreads();
         SPH(4);
         // 5. events: warp per clause of the work list, target then negative
-        const int n_heavy = s.misc[0], n_work = n_heavy + s.misc[1];
+        const int n_work = s.misc[0];
         for (int wi = warp; wi < n_work; wi += nwarps) {
-            const int j = wi < n_heavy ? s.work[wi] : s.work[k.cmax - 1 - (wi - n_heavy)];
+            const int j = s.work[wi];
             const int c = c0 + j;
             const int info = s.info[j];
             const int out = (info & SI_OUT) ? 1 : 0;
