@@ -895,6 +895,33 @@ def test_hbm_state_trainer_1024_threads_vs_oracle(gpu, oracle, n_blocks, keys):
     assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64), ost.block_counters)
 
 
+@pytest.mark.parametrize("weights", [0, 1 | (50 << 8) | (50 << 16), 255 | (1 << 8) | (255 << 16)])
+def test_balanced_feedback_weighted_split_vs_oracle(gpu, oracle, weights):
+    """HBM-state grid trainer, balanced feedback: the union of the CTAs' work
+    lists is cut at cost-weighted positions (train.gbal_weights).  Whatever
+    the weights -- unweighted, Type II nearly free, silent Type I rows 255
+    times cheaper than firing ones (a share of cheap rows then holds more work
+    items than the cmax + 4 staging buffer: the chunked path) -- every quad is
+    applied exactly once, so the model equals the oracle's.  First epoch of the MNIST-shaped config: every step is
+    non-empty with ~2 000 events."""
+    (tx, ty), _ = gpu.datasets.mnist_shaped(n_train=240, n_test=10, data_seed=11)
+    cfg = gpu.Config(**gpu.datasets.mnist_shaped_config_kwargs(seed=15))
+    try:
+        gpu._lib.call("tmb_set_option", b"train.gbal_weights", weights)
+        sess = gpu.DenseTrainSession(cfg, tx, ty, states_in_hbm=True, flag_keys=False)
+        assert sess.launch["kernel"] == "k_train (grid)" and not sess.launch["states_in_smem"]
+        sess.run_epoch()
+        m = sess.model()
+        stats = sess.stats_dict()
+    finally:
+        gpu._lib.call("tmb_set_option", b"train.gbal_weights", 2 | (5 << 8) | (6 << 16))
+    ost, _ = oracle.train(cfg, tx, ty, 1)
+    assert np.array_equal(m.states, ost.states)
+    assert np.array_equal(m.weights, ost.weights)
+    assert np.array_equal(sess.block_counters.cpu().numpy().view(np.uint64), ost.block_counters)
+    assert stats["events"] > 100 * len(ty)
+
+
 def test_speculative_trainer_large_threshold_vs_oracle(gpu, oracle):
     """k_train_spec with T > 8192 (no threshold table in shared memory: the
     window decision computes the exact thresholds in f64) against the
