@@ -2529,18 +2529,17 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
             for (int jb = 0; jb < cown; jb += 32) {
                 const int j = jb + lane;
                 const int f = j < cown ? s.oflag[j] : 0;
-                const unsigned v = (unsigned)(f & 1) + (unsigned)(f >> 1);
-                unsigned x = v;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
+                // events before lane's clause within the chunk: two ballots
+                const unsigned bt = __ballot_sync(0xffffffffu, f & 1);
+                const unsigned bn = __ballot_sync(0xffffffffu, f & 2);
+                const unsigned below = (1u << lane) - 1u;
                 if (f) {
                     s.oflag[j] = 0;
-                    spec_events(k, s, cn, j, f & 1, f & 2, obase + carry + (x - v), label, neg);
+                    spec_events(k, s, cn, j, f & 1, f & 2,
+                                obase + carry + (unsigned)(__popc(bt & below) + __popc(bn & below)),
+                                label, neg);
                 }
-                carry += __shfl_sync(0xffffffffu, x, 31);
+                carry += (unsigned)(__popc(bt) + __popc(bn));
             }
             __syncwarp();
             if (lane == 0) {
