@@ -2848,9 +2848,9 @@ __global__ void __launch_bounds__(32 * kWarpMaxC, 1) k_train_tiny(TrainK k) {
         int2 *pb = pub + (i & 1) * 32;
         if (lane == 0) pb[c] = make_int2(out ? w_l : 0, out ? w_n : 0);
         // the flag draws do not depend on the sums: before the barrier
-        const uint64_t d_t = real ? draw53(k.fb_seed, fbc + 1 + (uint64_t)lane) : ~0ull;
-        const uint64_t d_n = real ? draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)lane) : ~0ull;
-        __syncthreads();
+        const uint64_t d_t = (k.dbg & 2) ? fbc * 0x9E3779B9ull >> 11 : real ? draw53(k.fb_seed, fbc + 1 + (uint64_t)lane) : ~0ull;
+        const uint64_t d_n = (k.dbg & 2) ? fbc * 0x7F4A7C15ull >> 11 : real ? draw53(k.fb_seed, fbc + 1 + (uint64_t)C + (uint64_t)lane) : ~0ull;
+        if (!(k.dbg & 4)) __syncthreads();
         // 2. class sums, decision, every clause's flags (feedback.py:33-53)
         const int2 pv = real ? pb[lane] : make_int2(0, 0);
         long long vl, vn;
@@ -2887,7 +2887,7 @@ __global__ void __launch_bounds__(32 * kWarpMaxC, 1) k_train_tiny(TrainK k) {
             if (un && lane == neg) wreg -= 1;
         }
         // 5. per-position feedback when a state can move
-        if (!((ut && (t1 || out)) || (un && (n1 || out)))) continue;
+        if (!((ut && (t1 || out)) || (un && (n1 || out))) || (k.dbg & 1)) continue;
         unsigned nd = 0, nupd = 0;
         const int jo = out ? 1 : 0;
         for (int r = 0; r < W; ++r) {
@@ -2898,15 +2898,17 @@ __global__ void __launch_bounds__(32 * kWarpMaxC, 1) k_train_tiny(TrainK k) {
             const int s0 = st[p];
             int sv = s0;
             uint64_t d = 0;
+            // (branch-free Type I: the lanes hold different literals and
+            // states, the mixer must not run once per diverged path)
             if (ut) {
-                if (t1) sv = type_i_stream(sv, lit, jo, k.fp, bseed + kGolden * ((ord << 32) + 1),
-                                           (uint32_t)p, d);
+                if (t1) sv = type_i_bf(sv, lit, jo, k.fp,
+                                       bseed + kGolden * (((ord << 32) + 1) + (uint64_t)p), d);
                 else sv = type_ii(sv, lit, jo);
             }
             if (un) {
                 const uint64_t o2 = ord + (ut ? 1 : 0);
-                if (n1) sv = type_i_stream(sv, lit, jo, k.fp, bseed + kGolden * ((o2 << 32) + 1),
-                                           (uint32_t)p, d);
+                if (n1) sv = type_i_bf(sv, lit, jo, k.fp,
+                                       bseed + kGolden * (((o2 << 32) + 1) + (uint64_t)p), d);
                 else sv = type_ii(sv, lit, jo);
             }
             nd += (unsigned)d;
