@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--windows", type=int, nargs="+", default=[0, 16])
     ap.add_argument("--epochs", type=int, default=3)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--n-cta", type=int, default=0, help="CTAs (0 = one per SM)")
     ap.add_argument("--dbg", type=int, default=0, help="train.debug_skip bits (timing ablations)")
     ap.add_argument("--ents", type=int, default=64, help="train.spec_entries (0 = auto)")
     ap.add_argument("--prof", action="store_true",
@@ -41,7 +42,7 @@ def main():
     _lib.call("tmb_set_option", b"train.spec_entries", args.ents)
     for wsz in args.windows:
         _lib.call("tmb_set_option", b"train.spec_window", wsz)
-        sess = tmb.DenseTrainSession(cfg, tx, ty, threads=args.threads,
+        sess = tmb.DenseTrainSession(cfg, tx, ty, threads=args.threads, n_cta=args.n_cta,
                                      states=g["states"], weights=g["weights"])
         sess.block_counters.copy_(torch.from_numpy(g["block_counters"].view(np.int64)))
         sess.fb_counter = int(g["fb_counter"])
