@@ -2318,9 +2318,10 @@ __device__ __forceinline__ int mine_lane(int lane, int kk) { return lane < 2 * k
 // clock64 at [2] poll completion, [3] events done, [4] feedback done, [5]
 // publication, [6] work-list length, [7] flag entries of the step, [8]
 // clock64 after the decision barrier, [9] after the preparation barrier,
-// [10] after its warm repetition (profiling build only); stored
+// [10] after its warm repetition, [11] entries counted (warp 0), [12] own
+// events assigned, [13] own flagged clauses (profiling build only); stored
 // after the counters as [n_cta][kSpecTlN][kSpecTlQ].
-constexpr int kSpecTl0 = 2000, kSpecTlN = 2048, kSpecTlQ = 11;
+constexpr int kSpecTl0 = 2000, kSpecTlN = 2048, kSpecTlQ = 14;
 #define SPEC_TL(wn_, q_, v_)                                                                          \
     do {                                                                                              \
         if (PROF && (wn_) >= kSpecTl0 && (wn_) < kSpecTl0 + kSpecTlN)                                  \
@@ -2567,7 +2568,12 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
             }
             if (warp == 0) {
                 __syncwarp();
+                if (lane == 0) SPEC_TL(wn, 11, clock64());
                 own_events(pre, tot);
+                if (lane == 0) {
+                    SPEC_TL(wn, 12, clock64());
+                    SPEC_TL(wn, 13, s.misc[0]);
+                }
             }
         }
         __syncthreads();

@@ -51,7 +51,7 @@ def main():
         prof = None
         if args.prof and wsz > 0:
             ncta = sess.launch["n_cta"]
-            prof = torch.zeros(ncta * 16 + ncta * 2048 * 11, dtype=torch.int64, device="cuda")
+            prof = torch.zeros(ncta * 16 + ncta * 2048 * 14, dtype=torch.int64, device="cuda")
             _lib.call("tmb_trainer_set_profile", sess._h, prof.data_ptr())
 
         def reset():
@@ -73,7 +73,7 @@ def main():
             if prof is not None:
                 allp = prof.cpu().numpy()
                 p = allp[:ncta * 16].reshape(-1, 16).astype(np.float64)
-                tl = allp[ncta * 16:].reshape(ncta, 2048, 11).astype(np.float64)
+                tl = allp[ncta * 16:].reshape(ncta, 2048, 14).astype(np.float64)
                 heavy = (tl[:, :, 0] > 0).all(axis=0) & (tl[:, :, 1] > 0).all(axis=0)
                 polled = (tl[:, :, 1] > 0).all(axis=0)
                 h = tl[:, heavy, :]
@@ -107,6 +107,11 @@ def main():
                     prep_ns=med(np.median((h[:, :, 9] - h[:, :, 8]) / cyc, axis=0)),
                     prep_warm_ns=med(np.median((h[:, :, 10] - h[:, :, 9]) / cyc, axis=0)),
                     count_own_ns=med(np.median((h[:, :, 3] - h[:, :, 10]) / cyc, axis=0)),
+                    count_ns=med(np.median((h[:, :, 11] - h[:, :, 10]) / cyc, axis=0)),
+                    own_events_ns=med(np.median((h[:, :, 12] - h[:, :, 11]) / cyc, axis=0)),
+                    own_events_max_ns=med(((h[:, :, 12] - h[:, :, 11]) / cyc).max(axis=0)),
+                    count_max_ns=med(((h[:, :, 11] - h[:, :, 10]) / cyc).max(axis=0)),
+                    events_barrier_ns=med(np.median((h[:, :, 3] - h[:, :, 12]) / cyc, axis=0)),
                     fb_ns_by_nwork=fb_by_nwork,
                     nwork_max_cta=np.percentile(nw_max, [10, 50, 90]).tolist(),
                     nwork_mean_cta=float(nw.mean()),
