@@ -866,6 +866,9 @@ __device__ __forceinline__ int gbal_weight(const TrainK &k, int info) {
 // warp's 32 quads lie in one row).  rc_*[g - g_lo] hold the work items.
 // Same per-position arithmetic as feedback_quads; the rebuilt include-mask
 // words go to k.gmask for the owners to pull.
+#ifndef TMB_GB_B
+#define TMB_GB_B 1  // state words in flight per thread of the 1024-thread build (2: +5% time, 3: +4%)
+#endif
 template <int B>  // state words in flight per thread
 __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Smem &s,
                                                       const uint32_t *lit, int64_t q_begin,
@@ -1588,7 +1591,7 @@ __global__ void __launch_bounds__(NT, 1) k_train(TrainK k) {
                 const int64_t qa = q_begin > g_lo * QP ? q_begin : g_lo * QP;
                 const int64_t qb = q_end < (g_lo + n_rc) * QP ? q_end : (g_lo + n_rc) * QP;
                 if (!(k.dbg & 1))  // 1024 threads: half the words in flight per thread
-                    feedback_quads_global<(NT > 512 ? 2 : 4)>(k, s, lit, qa, qb, g_lo, cn);
+                    feedback_quads_global<(NT > 512 ? TMB_GB_B : 4)>(k, s, lit, qa, qb, g_lo, cn);
                 __syncthreads();
             }
             prefetch_commit(k, s, i, pf);
