@@ -885,6 +885,7 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
     for (int64_t it0 = q_begin + tid; it0 < q_end; it0 += (int64_t)B * nthr) {
         uint32_t word[B];
         int gi[B], pp[B];
+        int8_t *gp[B];  // the quad's states in HBM
 #pragma unroll
         for (int u = 0; u < B; ++u) {
             const int64_t it = it0 + (int64_t)u * nthr;
@@ -900,14 +901,14 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
                 const int p0 = rem << 2;
                 gi[u] = g;
                 pp[u] = p0;
-                const int8_t *grow = k.states + (int64_t)s.rc_clause[gi[u]] * k.P;
+                gp[u] = k.states + (int64_t)s.rc_clause[gi[u]] * k.P + p0;
                 if (k.vec4 && p0 + 4 <= k.P) {
-                    word[u] = __ldcg(reinterpret_cast<const unsigned int *>(grow + p0));
+                    word[u] = __ldcg(reinterpret_cast<const unsigned int *>(gp[u]));
                 } else {
                     for (int b = 0; b < 4; ++b)
                         if (p0 + b < k.P)
                             word[u] = (word[u] & ~(0xFFu << (8 * b))) |
-                                      ((uint32_t)(uint8_t)__ldcg(grow + p0 + b) << (8 * b));
+                                      ((uint32_t)(uint8_t)__ldcg(gp[u] + b) << (8 * b));
                 }
             }
         }
@@ -916,22 +917,21 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
             if (it0 + (int64_t)u * nthr >= q_end) break;  // warp-uniform
             const int g = gi[u], p0 = pp[u];
             const int c = s.rc_clause[g];
-            const int info = s.rc_info[g];
+            const int info = s.rc_info[g] & 0xFF, cls = s.rc_info[g] >> 8;
             const int lim = k.P - p0;
             const uint64_t zp = kGolden * (uint64_t)p0;
-            const int cls = fb_class(info);
-            const uint32_t vb = lim >= 4 ? 0xFFFFFFFFu
-                                         : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
+            // valid-position byte mask: all ones except in a row's last warp
+            uint32_t vb = 0xFFFFFFFFu;
+            if (__any_sync(0xffffffffu, lim < 4))
+                vb = lim >= 4 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
             uint32_t nw;
             // warp-uniform: a warp's quads share a work item (see feedback_simd)
             if (cls == 1) {
-                nw = quad_silent_type1(word[u], vb, smin4, T_dec,
-                                       s.rc_sk[2 * g + ((info & I_TEV) ? 0 : 1)] + zp, nd, nupd);
+                nw = quad_silent_type1(word[u], vb, smin4, T_dec, s.rc_sk[2 * g] + zp, nd, nupd);
             } else {
                 const uint32_t litn = p0 < k.P ? (lit[p0 >> 5] >> (p0 & 31)) & 0xFu : 0u;
                 if (cls == 2) {
-                    nw = quad_firing_type1(k, word[u], litn, vb,
-                                           s.rc_sk[2 * g + ((info & I_TEV) ? 0 : 1)] + zp, nd, nupd);
+                    nw = quad_firing_type1(k, word[u], litn, vb, s.rc_sk[2 * g] + zp, nd, nupd);
                 } else if (cls == 3) {
                     nw = quad_type2(word[u], litn, vb, nupd);
                 } else {
@@ -942,12 +942,11 @@ __device__ __forceinline__ void feedback_quads_global(const TrainK &k, const Sme
                 }
             }
             if (nw != word[u]) {
-                int8_t *grow = k.states + (int64_t)c * k.P;
                 if (k.vec4 && p0 + 4 <= k.P) {
-                    __stcg(reinterpret_cast<unsigned int *>(grow + p0), nw);
+                    __stcg(reinterpret_cast<unsigned int *>(gp[u]), nw);
                 } else {
                     for (int b = 0; b < 4; ++b)
-                        if (p0 + b < k.P) __stcg(grow + p0 + b, (int8_t)(nw >> (8 * b)));
+                        if (p0 + b < k.P) __stcg(gp[u] + b, (int8_t)(nw >> (8 * b)));
                 }
             }
             // mask word for positions 32w..32w+31 (lanes 8g..8g+7 hold its
@@ -1583,8 +1582,11 @@ __global__ void __launch_bounds__(NT, 1) k_train(TrainK k) {
                     }
                     const int64_t o = (int64_t)lo * k.cmax + (g - s.gpref[lo]);
                     s.rc_clause[t] = __ldcg(&k.gw_clause[o]);
-                    s.rc_info[t] = __ldcg(&k.gw_info[o]);
-                    s.rc_sk[2 * t] = __ldcg(&k.gw_sk[2 * o]);
+                    const int info_t = __ldcg(&k.gw_info[o]);
+                    s.rc_info[t] = info_t | (fb_class(info_t) << 8);  // event class decided once per item
+                    // (a single-event row's key in slot 0, whichever event it is)
+                    const bool neg_only = (info_t & (I_TEV | I_NEV)) == I_NEV;
+                    s.rc_sk[2 * t] = __ldcg(&k.gw_sk[2 * o + (neg_only ? 1 : 0)]);
                     s.rc_sk[2 * t + 1] = __ldcg(&k.gw_sk[2 * o + 1]);
                 }
                 __syncthreads();
