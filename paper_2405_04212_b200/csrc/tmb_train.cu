@@ -667,7 +667,8 @@ __device__ __forceinline__ int fb_class(int info) {
     return t1 ? 2 : 3;
 }
 
-template <bool SMEM_STATES>
+// PRECLS: s.info[j] carries the row's event class in bits 8.. (spec_events).
+template <bool SMEM_STATES, bool PRECLS = false>
 __device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, int c0,
                                               const uint32_t *lit, int n_work, Counters &cn) {
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
@@ -694,8 +695,11 @@ __device__ __forceinline__ void feedback_simd(const TrainK &k, const Smem &s, in
         const int lim = k.P - p0;
         const uint64_t zp = kGolden * (uint64_t)p0;
         uint32_t w;
-        const int cls = fb_class(info);
-        const uint32_t vb = lim >= 4 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
+        const int cls = PRECLS ? (info >> 8) : fb_class(info);
+        // valid-position byte mask: all ones except in a row's last warp
+        uint32_t vb = 0xFFFFFFFFu;
+        if (__any_sync(0xffffffffu, lim < 4))
+            vb = lim >= 4 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - lim))));
         if (cls == 1) {
             w = quad_silent_type1(word, vb, smin4, T_dec, ((info & I_TEV) ? s.sk_t[j] : s.sk_n[j]) + zp,
                                   nd, nupd);
@@ -2308,7 +2312,7 @@ __device__ __forceinline__ void spec_events(const TrainK &k, const Smem &s, Coun
         if (t_ev) w[label] += 1;
         if (n_ev) w[neg] -= 1;
     }
-    s.info[j] = info;
+    s.info[j] = info | (fb_class(info) << 8);  // event class for feedback_simd<., true>
     if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
         s.work[atomicAdd(&s.misc[0], 1)] = j;
 }
@@ -2586,7 +2590,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
         if (tid == 0) SPEC_TL(wn, 3, clock64());
         const int n_work = (k.dbg & 1) ? 0 : s.misc[0];
         if (n_work > 0) {
-            feedback_simd<SMEM_STATES>(k, s, c0, lit, n_work, cn);
+            feedback_simd<SMEM_STATES, true>(k, s, c0, lit, n_work, cn);
             __syncthreads();
         }
         SPH(3);
