@@ -2288,7 +2288,8 @@ __device__ __forceinline__ void spec_push(const TrainK &k, const Smem &s, int t,
 
 // Event bookkeeping of own clause j for the applied step (fast_events
 // without the next-example correction).
-__device__ __forceinline__ void spec_events(const TrainK &k, const Smem &s, Counters &cn, int j,
+// Returns whether the clause joins the work list (a state can move).
+__device__ __forceinline__ bool spec_events(const TrainK &k, const Smem &s, Counters &cn, int j,
                                             bool t_ev, bool n_ev, uint64_t ord, int label, int neg) {
     int info = s.info[j] & I_OUT;
     const bool out = info & I_OUT;
@@ -2313,8 +2314,7 @@ __device__ __forceinline__ void spec_events(const TrainK &k, const Smem &s, Coun
         if (n_ev) w[neg] -= 1;
     }
     s.info[j] = info | (fb_class(info) << 8);  // event class for feedback_simd<., true>
-    if ((t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out)))
-        s.work[atomicAdd(&s.misc[0], 1)] = j;
+    return (t_ev && ((info & I_T1) || out)) || (n_ev && ((info & I_N1) || out));
 }
 
 __device__ __forceinline__ int mine_lane(int lane, int kk) { return lane < 2 * kk ? lane : 0; }
@@ -2532,10 +2532,9 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
             }
         };
         auto own_events = [&](unsigned pv, unsigned tv) {
-            if (lane == 0) s.misc[0] = 0;
-            __syncwarp();
             const uint64_t obase = s.blk_ctr[0] + pv;
             unsigned carry = 0;
+            int n_wl = 0;  // work-list slots by ballot (no shared-memory atomics)
             for (int jb = 0; jb < cown; jb += 32) {
                 const int j = jb + lane;
                 const int f = j < cown ? s.oflag[j] : 0;
@@ -2543,16 +2542,21 @@ __global__ void __launch_bounds__(kFastMaxThreads, 1) k_train_spec(TrainK k) {
                 const unsigned bt = __ballot_sync(0xffffffffu, f & 1);
                 const unsigned bn = __ballot_sync(0xffffffffu, f & 2);
                 const unsigned below = (1u << lane) - 1u;
+                bool wk = false;
                 if (f) {
                     s.oflag[j] = 0;
-                    spec_events(k, s, cn, j, f & 1, f & 2,
-                                obase + carry + (unsigned)(__popc(bt & below) + __popc(bn & below)),
-                                label, neg);
+                    wk = spec_events(k, s, cn, j, f & 1, f & 2,
+                                     obase + carry + (unsigned)(__popc(bt & below) + __popc(bn & below)),
+                                     label, neg);
                 }
+                const unsigned wb = __ballot_sync(0xffffffffu, wk);
+                if (wk) s.work[n_wl + __popc(wb & below)] = j;
+                n_wl += __popc(wb);
                 carry += (unsigned)(__popc(bt) + __popc(bn));
             }
             __syncwarp();
             if (lane == 0) {
+                s.misc[0] = n_wl;
                 s.blk_ctr[0] += (uint64_t)tv;
                 if (k.trace && rank == 0) k.trace[i * 4 + 3] = tv;
             }
